@@ -1,0 +1,202 @@
+/*
+ * hapigpu.h -- C ABI of the B200 trace post-processing engine (libhapigpu.so).
+ *
+ * The reference (THAPI re-created as the Python package `hapitrace`) has no
+ * FFI on this path: its boundary is the Python plugin API
+ *   run_pipeline(source, sinks, registry)      pipeline.py:275-314
+ *   TallySink / TallyReport                     sinks.py:113-248
+ *   TimelineSink                                sinks.py:341-418
+ *   merge_tallies                               aggregator.py:35-76
+ * Each entry point below names the reference interface it replaces.  The
+ * Python package `paper_2504_03683_b200` binds this header with ctypes and
+ * re-exposes the reference API on top of it.
+ *
+ * Conventions: plain C types only; return 0 (HG_OK) on success, a negative
+ * HG_E* code on an engine failure (text via hg_last_error), or HG_TRACE_ERROR
+ * (> 0) when the trace itself is malformed -- the caller then reads the
+ * per-stream error candidates (hg_get_trace_errors) and raises the same
+ * exception the reference would (CorruptRecordError, UnknownSchemaError,
+ * MuxOrderingError, HapitraceError ...).  One context per pipeline; a context
+ * is not reentrant, distinct contexts may run concurrently.  The library owns
+ * all device memory; output arrays are caller-allocated.
+ */
+#ifndef HAPIGPU_H
+#define HAPIGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_ABI_VERSION 1
+
+/* return codes */
+#define HG_OK 0
+#define HG_TRACE_ERROR 1
+#define HG_EARG (-1)
+#define HG_ESTATE (-2)
+#define HG_ECUDA (-3)
+#define HG_ENOMEM (-4)
+#define HG_EUNSUPPORTED (-5)
+
+/* field kinds (registry.py:23 FIELD_KINDS order) */
+enum { HG_KIND_U64 = 0, HG_KIND_I64 = 1, HG_KIND_F64 = 2, HG_KIND_ADDRESS = 3, HG_KIND_STRING = 4, HG_KIND_BLOB = 5 };
+/* event classes (registry.py:24 EVENT_CLASSES order) */
+enum { HG_CLASS_ENTRY = 0, HG_CLASS_EXIT = 1, HG_CLASS_DEVICE = 2, HG_CLASS_TELEMETRY = 3, HG_CLASS_META = 4 };
+/* field roles resolved by name on the host (pipeline.py:183, 192-214; sinks.py:381-395) */
+enum {
+  HG_ROLE_RESULT = 0,   /* host_exit "result"                  */
+  HG_ROLE_START = 1,    /* device "device_start_ns"            */
+  HG_ROLE_END = 2,      /* device "device_end_ns"              */
+  HG_ROLE_NAME = 3,     /* device "name"                       */
+  HG_ROLE_TILE = 4,     /* device "tile"                       */
+  HG_ROLE_ENGINE = 5,   /* device "engine"                     */
+  HG_ROLE_CMDKIND = 6,  /* device "command_kind"               */
+  HG_ROLE_VALUE = 7,    /* telemetry "value"                   */
+  HG_ROLE_DEVICE = 8,   /* telemetry "device"                  */
+  HG_NUM_ROLES = 10
+};
+/* telemetry counter kinds (sampler.py:51-64) */
+enum { HG_COUNTER_POWER = 0, HG_COUNTER_FREQUENCY = 1, HG_COUNTER_COMPUTE = 2, HG_COUNTER_COPY = 3 };
+
+/* One schema of the registry, flattened (registry.py:61-71 EventSchema).
+ * feed_error != 0: every event of this schema raises when it reaches the
+ * interval stage (e.g. a telemetry schema whose name parse_counter_key
+ * rejects); the host keeps the exception text, the engine reports where. */
+typedef struct hg_schema {
+  uint32_t id;             /* schema id as stored in records                 */
+  uint8_t event_class;     /* HG_CLASS_*                                     */
+  uint8_t n_fields;
+  uint8_t counter_kind;    /* HG_COUNTER_* (telemetry only)                  */
+  uint8_t feed_error;      /* 0 = none                                       */
+  int32_t function;        /* function-name id (pairing/tally key), -1: None */
+  int32_t counter_domain;  /* telemetry domain index                         */
+  uint32_t kinds_offset;   /* first field kind in the kinds[] array          */
+  int16_t role[HG_NUM_ROLES]; /* field index per HG_ROLE_*, -1 if absent     */
+} hg_schema;
+
+typedef struct hg_config {
+  int32_t device;          /* CUDA device ordinal                            */
+  uint32_t tile_bytes;     /* stream bytes per warp tile (0 = default)       */
+  uint32_t flags;          /* reserved                                       */
+  int32_t timeline_device_index; /* TimelineSink(device_index=) (sinks.py:347-349) */
+} hg_config;
+
+typedef struct hg_stats {  /* IntervalStats (pipeline.py:117-129) */
+  uint64_t events_in, passed, host_spans, truncated_spans, device_spans, samples, orphan_exits;
+} hg_stats;
+
+/* one tally row (TallyRow, sinks.py:113-136).  Sums and extrema are exact
+ * signed 128-bit integers split into (lo, hi) words. */
+typedef struct hg_tally_row {
+  uint32_t section;        /* 0 host, 1 device                               */
+  uint32_t name_id;        /* host: function id; device: device-name id      */
+  uint64_t count, error_count;
+  uint64_t time_lo; int64_t time_hi;
+  uint64_t min_lo;  int64_t min_hi;
+  uint64_t max_lo;  int64_t max_hi;
+} hg_tally_row;
+
+/* orphan exit diagnostic (pipeline.py:163-168), unordered; the host sorts
+ * by (ts, stream, seq) = mux order. */
+typedef struct hg_orphan {
+  uint32_t stream;         /* stream index as added                          */
+  int32_t function;
+  uint64_t ts;
+  uint64_t seq;            /* record index within the stream                 */
+} hg_orphan;
+
+/* trace error candidates: the first failing record of each stream
+ * (pipeline.py:92-100, tracefile.py:198-215) and value-dependent
+ * interval-stage errors (sampler.py:44-48).  The host picks the one the
+ * reference's muxer would hit first and formats the exception. */
+enum {
+  HG_ERR_TRUNC_HEADER = 1,   /* CorruptRecordError "truncated record header"  */
+  HG_ERR_TRUNC_PAYLOAD = 2,  /* CorruptRecordError "truncated record payload" */
+  HG_ERR_UNKNOWN_SCHEMA = 3, /* UnknownSchemaError                            */
+  HG_ERR_LEN_MISMATCH = 4,   /* CorruptRecordError "payload length mismatch"  */
+  HG_ERR_TRUNC_VAR = 5,      /* CorruptRecordError "truncated variable field" */
+  HG_ERR_TRAILING = 6,       /* CorruptRecordError "trailing payload bytes"   */
+  HG_ERR_UTF8 = 7,           /* CorruptRecordError from UnicodeDecodeError    */
+  HG_ERR_STRUCT = 8,         /* struct.error escaping _decode_one             */
+  HG_ERR_ORDER = 9,          /* MuxOrderingError                              */
+  HG_ERR_FEED = 10,          /* schema feed_error at this event               */
+  HG_ERR_TELEMETRY = 11,     /* TelemetrySample range check                   */
+  HG_ERR_RESULT = 12         /* int(result) of a NaN/inf f64 result           */
+};
+typedef struct hg_trace_error {
+  uint32_t code;           /* HG_ERR_*                                       */
+  uint32_t stream;
+  uint64_t seq;            /* index of the failing record                    */
+  uint64_t offset;         /* its byte offset in the stream file             */
+  uint64_t ts;             /* its timestamp (if decodable)                   */
+  uint64_t prev_ts;        /* timestamp of record seq-1 (pull position)      */
+  uint64_t aux;            /* code-specific: schema id, utf-8 position ...   */
+} hg_trace_error;
+
+typedef struct hg_ctx hg_ctx;
+
+/* create/destroy a pipeline context bound to one GPU
+ * replaces: run_pipeline's per-call IntervalBuilder/sink set-up (pipeline.py:282-299) */
+int hg_create(const hg_config* cfg, hg_ctx** out);
+void hg_destroy(hg_ctx* ctx);
+const char* hg_last_error(hg_ctx* ctx);
+int hg_abi_version(void);
+
+/* install the decode contract: TraceReader registry + _CodecTable
+ * (tracefile.py:172-180, 530-531; registry.py:116-129) */
+int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas,
+                    const uint8_t* kinds, uint32_t n_kinds, uint32_t n_functions);
+
+/* add one stream file (bytes incl. the 16-byte header, already validated by
+ * the host) in (hostname, pid, tid) order; replaces StreamCursor
+ * (tracefile.py:477-508).  `data` is a host pointer that must stay valid
+ * until hg_run returns. */
+int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid,
+                  const void* data, uint64_t size);
+int hg_clear_streams(hg_ctx* ctx);
+
+/* copy all added streams to HBM now; later runs reuse the resident copy
+ * (used to time the device-resident path separately from ingest). */
+int hg_stage(hg_ctx* ctx);
+
+/* run decode -> pair -> tally (+ timeline) over all streams:
+ * replaces run_pipeline(reader, [TallySink(), TimelineSink()]) (pipeline.py:275-314) */
+#define HG_WANT_TALLY 1u
+#define HG_WANT_TIMELINE 2u
+int hg_run(hg_ctx* ctx, uint32_t want);
+
+/* split form for sharded (multi-GPU) runs: phase 1 over the local streams,
+ * then the caller all-reduces the max timestamp (pipeline.py:152, :235) and
+ * finishes with the global value. */
+int hg_run_local(hg_ctx* ctx, uint32_t want);
+int hg_local_last_ts(hg_ctx* ctx, uint64_t* last_ts, uint64_t* n_events);
+int hg_finish(hg_ctx* ctx, uint64_t global_last_ts);
+
+/* results */
+int hg_get_stats(hg_ctx* ctx, hg_stats* out);                       /* IntervalStats */
+int hg_get_tally(hg_ctx* ctx, hg_tally_row* rows, uint64_t cap, uint64_t* n_rows); /* TallySink.on_finish */
+int hg_get_device_names(hg_ctx* ctx, char* bytes, uint64_t cap, uint64_t* offsets,
+                        uint64_t n_offsets, uint64_t* n_names, uint64_t* n_bytes);
+int hg_get_stream_spans(hg_ctx* ctx, uint64_t* per_stream, uint64_t n); /* span identities (sinks.py:240-242) */
+int hg_get_orphans(hg_ctx* ctx, hg_orphan* out, uint64_t cap, uint64_t* n); /* IntervalBuilder.orphans */
+int hg_get_trace_errors(hg_ctx* ctx, hg_trace_error* out, uint64_t cap, uint64_t* n);
+
+/* timeline: Chrome-trace JSON bytes exactly as json.dump(objs, fh, indent=1)
+ * writes them (sinks.py:414-418) */
+int hg_timeline_size(hg_ctx* ctx, uint64_t* n_bytes);
+int hg_get_timeline(hg_ctx* ctx, char* out, uint64_t cap);
+
+/* device-resident dense tally for NCCL merging across ranks: host rows are
+ * function-indexed.  Returns device pointers owned by the context. */
+int hg_device_tally(hg_ctx* ctx, void** host_rows, uint64_t* n_host_rows);
+
+/* timing of the last run (CUDA events around the kernels, ms) */
+int hg_last_timing(hg_ctx* ctx, float* kernel_ms, float* total_ms, uint64_t* h2d_bytes, uint64_t* d2h_bytes,
+                   uint64_t* kernel_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HAPIGPU_H */

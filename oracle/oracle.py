@@ -1,0 +1,195 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes front of the CPU oracle (hapi_oracle.c).
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+--impl reference) import this module.  It runs the literal CPU restatement of
+the reference path and returns results in the same shapes the GPU engine's
+Python front returns, so tests compare like with like:
+
+    OracleResult.report      TallyReport        (sinks.py:139-248)
+    OracleResult.stats       IntervalStats dict (pipeline.py:117-129)
+    OracleResult.orphans     [(label, ts, fn)]  (pipeline.py:138, 163-168)
+    OracleResult.error       the exception the reference raises, or None
+    OracleResult.timeline    json.dump(objs, indent=1) text (sinks.py:414-418)
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import struct
+import subprocess
+from dataclasses import dataclass
+from pathlib import Path
+
+from paper_2504_03683_b200.abi import (
+    HgOrphan, HgStats, HgTallyRow, HgTraceError, flatten_registry, i128,
+)
+from paper_2504_03683_b200.results import build_report, make_exception, orphan_list, rows_from_native
+from paper_2504_03683_b200.timeline import TimelineBuilder
+from paper_2504_03683_b200.registry import COUNTER_KINDS
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "liboracle.so"
+SRC = HERE / "hapi_oracle.c"
+
+
+class TlItem(C.Structure):
+    _fields_ = [
+        ("kind", C.c_uint8), ("truncated", C.c_uint8), ("value_kind", C.c_uint8), ("pad", C.c_uint8),
+        ("stream", C.c_uint32), ("name", C.c_int32), ("cmdkind", C.c_int32),
+        ("start", C.c_uint64), ("end", C.c_uint64), ("result", C.c_uint64),
+        ("tile", C.c_uint64), ("engine", C.c_uint64),
+        ("counter_kind", C.c_int64), ("counter_domain", C.c_int64),
+    ]
+
+
+def build(force: bool = False) -> Path:
+    if force or not LIB.exists() or LIB.stat().st_mtime < SRC.stat().st_mtime:
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", str(LIB), str(SRC), "-lpthread"])
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(str(LIB))
+        vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
+        L.oracle_run.restype = vp
+        L.oracle_run.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32]
+        L.oracle_tally_threads.restype = vp
+        L.oracle_tally_threads.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32]
+        L.oracle_free.argtypes = [vp]
+        L.oracle_has_error.argtypes = [vp, vp]
+        L.oracle_has_error.restype = C.c_int
+        L.oracle_stats.argtypes = [vp, vp]
+        L.oracle_rows.argtypes = [vp, vp, u64]
+        L.oracle_rows.restype = u64
+        L.oracle_names.argtypes = [vp, C.c_int, vp, u64, vp, u64]
+        L.oracle_names.restype = u64
+        L.oracle_name_bytes.argtypes = [vp, C.c_int]
+        L.oracle_name_bytes.restype = u64
+        L.oracle_orphans.argtypes = [vp, vp, u64]
+        L.oracle_orphans.restype = u64
+        L.oracle_stream_spans.argtypes = [vp, vp, u64]
+        L.oracle_stream_spans.restype = u64
+        L.oracle_timeline.argtypes = [vp, vp, u64]
+        L.oracle_timeline.restype = u64
+        L.oracle_tl_item_size.restype = u64
+        L.oracle_last_ts.argtypes = [vp]
+        L.oracle_last_ts.restype = u64
+        assert L.oracle_tl_item_size() == C.sizeof(TlItem)
+        _lib = L
+    return _lib
+
+
+@dataclass
+class OracleResult:
+    report: object
+    stats: dict
+    orphans: list
+    error: BaseException | None
+    timeline: str | None
+    last_ts: int
+
+
+def _names(L, h, which):
+    nb = L.oracle_name_bytes(h, which)
+    n = L.oracle_names(h, which, None, 0, None, 0)
+    buf = (C.c_uint8 * max(nb, 1))()
+    offs = (C.c_uint64 * (n + 1))()
+    L.oracle_names(h, which, buf, nb, offs, n + 1)
+    raw = bytes(buf)[:nb]
+    return [raw[offs[i]:offs[i + 1]].decode("utf-8") for i in range(n)]
+
+
+def _py_value(kind, bits):
+    if kind == 2:  # f64
+        return struct.unpack("<d", struct.pack("<Q", bits))[0]
+    if kind == 1:  # i64
+        return struct.unpack("<q", struct.pack("<Q", bits))[0]
+    return bits
+
+
+def run(raw_streams, registry, stream_infos=None, want_timeline=False, threads=0, device_index=0,
+        labels=None) -> OracleResult:
+    """Run the oracle over RawStream objects in (hostname, pid, tid) order."""
+    L = lib()
+    flat = flatten_registry(registry)
+    n = len(raw_streams)
+    bufs = [C.create_string_buffer(s.data, len(s.data)) if s.data else None for s in raw_streams]
+    ptrs = (C.c_void_p * max(n, 1))(*[C.cast(b, C.c_void_p) if b is not None else None for b in bufs])
+    sizes = (C.c_uint64 * max(n, 1))(*[len(s.data) for s in raw_streams])
+    if threads:
+        h = L.oracle_tally_threads(flat.schemas, flat.n_schemas, flat.kinds, len(flat.function_names), n,
+                                   ptrs, sizes, threads)
+    else:
+        h = L.oracle_run(flat.schemas, flat.n_schemas, flat.kinds, len(flat.function_names), n, ptrs, sizes,
+                         1 if want_timeline else 0)
+    if not h:
+        raise RuntimeError("oracle: registry ids too large")
+    try:
+        return _collect(L, h, flat, raw_streams, stream_infos, want_timeline, device_index, labels)
+    finally:
+        L.oracle_free(h)
+
+
+def _collect(L, h, flat, raw_streams, stream_infos, want_timeline, device_index, labels):
+    n = len(raw_streams)
+    idents = [(s.hostname, s.pid, s.tid) for s in raw_streams]
+    if labels is None:
+        labels = [f"{s.hostname}/{s.pid}/{s.tid}" for s in raw_streams]
+    st = HgStats()
+    L.oracle_stats(h, C.byref(st))
+    stats = {k: getattr(st, k) for k, _ in HgStats._fields_}
+    n_orph = L.oracle_orphans(h, None, 0)
+    orph = (HgOrphan * max(n_orph, 1))()
+    L.oracle_orphans(h, orph, n_orph)
+    orphans_raw = list(orph)[:n_orph]
+    err = HgTraceError()
+    error = None
+    if L.oracle_has_error(h, C.byref(err)):
+        error = make_exception(err, raw_streams[err.stream], flat)
+    # the oracle stops at the first error, so every collected orphan precedes it
+    orphans = orphan_list(orphans_raw, labels, flat)
+    n_rows = L.oracle_rows(h, None, 0)
+    rows = (HgTallyRow * max(n_rows, 1))()
+    L.oracle_rows(h, rows, n_rows)
+    names = _names(L, h, 0)
+    spans = (C.c_uint64 * max(n, 1))()
+    L.oracle_stream_spans(h, spans, n)
+    report = build_report(flat, rows_from_native(list(rows)[:n_rows]), names, stream_infos, idents, list(spans)[:n])
+    timeline = None
+    if want_timeline and error is None:
+        cmdkinds = _names(L, h, 1)
+        n_items = L.oracle_timeline(h, None, 0)
+        items = (TlItem * max(n_items, 1))()
+        L.oracle_timeline(h, items, n_items)
+        tb = TimelineBuilder(device_index)
+        for it in list(items)[:n_items]:
+            s = raw_streams[it.stream]
+            if it.kind == 0:
+                tb.host_span(flat.function_names[it.name], s.hostname, s.pid, s.tid, it.start, it.end,
+                             _py_value(it.value_kind, it.result) if it.value_kind != 2 else
+                             int(_py_value(2, it.result)), bool(it.truncated))
+            elif it.kind == 1:
+                start = struct.unpack("<q", struct.pack("<Q", it.start))[0] if it.value_kind & 1 else it.start
+                end = struct.unpack("<q", struct.pack("<Q", it.end))[0] if it.value_kind & 2 else it.end
+                tb.device_span(names[it.name], start, end, it.tile, it.engine,
+                               cmdkinds[it.cmdkind] if it.cmdkind >= 0 else "")
+            else:
+                tb.sample(COUNTER_KINDS[it.counter_kind], it.counter_domain, it.start,
+                          _py_value(it.value_kind, it.result), it.tile)
+        timeline = tb.dumps()
+    return OracleResult(report, stats, orphans, error, timeline, L.oracle_last_ts(h))
+
+
+def run_dir(directory, want_timeline=False, threads=0, device_index=0) -> OracleResult:
+    from paper_2504_03683_b200.tracefile import open_trace_reader
+
+    reader = open_trace_reader(directory)
+    return run(reader.raw_streams(), reader.registry, reader.stream_infos(), want_timeline, threads,
+               device_index)
