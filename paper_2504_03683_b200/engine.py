@@ -1,0 +1,204 @@
+"""Engine: one GPU pipeline context (hg_ctx) behind a small Python class.
+
+`Engine.run(raw_streams, registry, ...)` replaces the body of the reference's
+`run_pipeline` for tally/timeline sinks (pipeline.py:275-314): it hands the
+undecoded stream bytes to libhapigpu, which decodes, pairs and reduces them
+on the GPU, and returns the reference objects (TallyReport, IntervalStats
+values, orphan list) or the exception the reference would raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import native
+from .abi import (
+    HG_OK, HG_TRACE_ERROR, HG_WANT_TALLY, HG_WANT_TIMELINE, HgConfig, HgOrphan, HgStats, HgTallyRow,
+    HgTraceError, flatten_registry,
+)
+from .errors import EngineError, UnsupportedTraceError
+from .results import build_report, error_key, first_error, make_exception, orphan_list, rows_from_native
+
+HG_EUNSUPPORTED = -5
+
+
+@dataclass
+class RunResult:
+    report: object | None
+    stats: dict
+    orphans: list
+    error: BaseException | None
+    timeline: bytes | None
+    kernel_ms: float
+    total_ms: float
+    h2d_bytes: int
+    d2h_bytes: int
+    launches: int
+
+
+class Engine:
+    """A GPU pipeline context bound to one CUDA device."""
+
+    def __init__(self, device: int = 0, timeline_device_index: int = 0):
+        self._L = native.lib()
+        self._ctx = C.c_void_p()
+        cfg = HgConfig(device=device, tile_bytes=0, flags=0, timeline_device_index=timeline_device_index)
+        rc = self._L.hg_create(C.byref(cfg), C.byref(self._ctx))
+        if rc != HG_OK:
+            msg = self._L.hg_last_error(self._ctx).decode() if self._ctx else "hg_create failed"
+            self.close()
+            raise EngineError(msg)
+        self._flat = None
+        self._registry_key = None
+        self._keep = []
+        self._streams = []
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_ctx", None):
+            self._L.hg_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _check(self, rc, what):
+        if rc == HG_OK:
+            return
+        msg = self._L.hg_last_error(self._ctx).decode(errors="replace")
+        if rc == HG_EUNSUPPORTED:
+            raise UnsupportedTraceError(f"{what}: {msg}")
+        raise EngineError(f"{what} failed ({rc}): {msg}")
+
+    # -- inputs
+    def set_registry(self, registry):
+        if self._registry_key is registry:
+            return self._flat
+        flat = flatten_registry(registry)
+        self._check(self._L.hg_set_registry(self._ctx, flat.schemas, flat.n_schemas, flat.kinds, len(flat.kinds),
+                                            len(flat.function_names)), "hg_set_registry")
+        self._flat = flat
+        self._registry_key = registry
+        return flat
+
+    def set_streams(self, raw_streams):
+        """raw_streams: RawStream list in mux order (hostname, pid, tid)."""
+        self._check(self._L.hg_clear_streams(self._ctx), "hg_clear_streams")
+        self._keep = []
+        self._streams = list(raw_streams)
+        for s in self._streams:
+            self.add_stream_ptr(s.hostname, s.pid, s.tid, s.data)
+
+    def add_stream_ptr(self, hostname, pid, tid, data, size=None):
+        """data: bytes (kept alive here) or an integer host address (+ size)."""
+        if isinstance(data, int):
+            ptr, n = data, size
+        else:
+            buf = C.c_char_p(data) if data else None
+            self._keep.append(data)
+            ptr, n = (C.cast(buf, C.c_void_p).value if buf else None), len(data)
+        h = (hostname if hostname is not None else "").encode()
+        self._check(self._L.hg_add_stream(self._ctx, h, int(pid or 0), int(tid or 0), ptr, n), "hg_add_stream")
+
+    def stage(self):
+        self._check(self._L.hg_stage(self._ctx), "hg_stage")
+
+    # -- execution
+    def run_raw(self, want=HG_WANT_TALLY):
+        rc = self._L.hg_run(self._ctx, want)
+        if rc not in (HG_OK, HG_TRACE_ERROR):
+            self._check(rc, "hg_run")
+        return rc
+
+    def timing(self):
+        k, t = C.c_float(), C.c_float()
+        h2d, d2h, nl = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._L.hg_last_timing(self._ctx, C.byref(k), C.byref(t), C.byref(h2d), C.byref(d2h), C.byref(nl))
+        return k.value, t.value, h2d.value, d2h.value, nl.value
+
+    def stats(self) -> dict:
+        st = HgStats()
+        self._check(self._L.hg_get_stats(self._ctx, C.byref(st)), "hg_get_stats")
+        return {k: getattr(st, k) for k, _ in HgStats._fields_}
+
+    def tally_rows(self):
+        n = C.c_uint64()
+        self._check(self._L.hg_get_tally(self._ctx, None, 0, C.byref(n)), "hg_get_tally")
+        rows = (HgTallyRow * max(n.value, 1))()
+        self._check(self._L.hg_get_tally(self._ctx, rows, n.value, C.byref(n)), "hg_get_tally")
+        return rows_from_native(list(rows)[: n.value])
+
+    def device_names(self):
+        nn, nb = C.c_uint64(), C.c_uint64()
+        self._check(self._L.hg_get_device_names(self._ctx, None, 0, None, 0, C.byref(nn), C.byref(nb)), "names")
+        buf = (C.c_char * max(nb.value, 1))()
+        offs = (C.c_uint64 * (nn.value + 1))()
+        self._check(self._L.hg_get_device_names(self._ctx, buf, nb.value, offs, nn.value + 1, C.byref(nn),
+                                                C.byref(nb)), "names")
+        raw = bytes(buf)[: nb.value]
+        return [raw[offs[i]: offs[i + 1]].decode("utf-8") for i in range(nn.value)]
+
+    def stream_spans(self):
+        n = len(self._streams)
+        arr = (C.c_uint64 * max(n, 1))()
+        self._check(self._L.hg_get_stream_spans(self._ctx, arr, n), "hg_get_stream_spans")
+        return list(arr)[:n]
+
+    def orphans_raw(self):
+        n = C.c_uint64()
+        self._check(self._L.hg_get_orphans(self._ctx, None, 0, C.byref(n)), "hg_get_orphans")
+        arr = (HgOrphan * max(n.value, 1))()
+        self._check(self._L.hg_get_orphans(self._ctx, arr, n.value, C.byref(n)), "hg_get_orphans")
+        return list(arr)[: n.value]
+
+    def errors_raw(self):
+        n = C.c_uint64()
+        self._check(self._L.hg_get_trace_errors(self._ctx, None, 0, C.byref(n)), "hg_get_trace_errors")
+        arr = (HgTraceError * max(n.value, 1))()
+        self._check(self._L.hg_get_trace_errors(self._ctx, arr, n.value, C.byref(n)), "hg_get_trace_errors")
+        return list(arr)[: n.value]
+
+    def timeline_bytes(self) -> bytes:
+        n = C.c_uint64()
+        self._check(self._L.hg_timeline_size(self._ctx, C.byref(n)), "hg_timeline_size")
+        buf = (C.c_char * max(n.value, 1))()
+        self._check(self._L.hg_get_timeline(self._ctx, buf, n.value), "hg_get_timeline")
+        return bytes(buf)[: n.value]
+
+    # -- the drop-in
+    def run(self, raw_streams, registry, stream_infos=None, want_timeline=False, labels=None,
+            orphan_labels=None) -> RunResult:
+        flat = self.set_registry(registry)
+        self.set_streams(raw_streams)
+        want = HG_WANT_TALLY | (HG_WANT_TIMELINE if want_timeline else 0)
+        rc = self.run_raw(want)
+        k, t, h2d, d2h, nl = self.timing()
+        stats = self.stats()
+        if orphan_labels is None:
+            orphan_labels = [f"{s.hostname}/{s.pid}/{s.tid}" for s in raw_streams]
+        orphans = self.orphans_raw()
+        error = None
+        if rc == HG_TRACE_ERROR:
+            cands = self.errors_raw()
+            e = first_error(cands)
+            cut = {}
+            for c in cands:
+                if c.code in (1, 2, 3, 4, 5, 6, 7, 8, 9) and (c.stream not in cut or c.seq < cut[c.stream]):
+                    cut[c.stream] = c.seq
+            named = raw_streams[e.stream]
+            if labels is not None:
+                from .tracefile import RawStream
+
+                named = RawStream(named.hostname, named.pid, named.tid, labels[e.stream], named.data, named.info)
+            error = make_exception(e, named, flat)
+            olist = orphan_list(orphans, orphan_labels, flat, cutoff=error_key(e), cut_streams=cut)
+            return RunResult(None, stats, olist, error, None, k, t, h2d, d2h, nl)
+        olist = orphan_list(orphans, orphan_labels, flat)
+        idents = [(s.hostname, s.pid, s.tid) for s in raw_streams]
+        report = build_report(flat, self.tally_rows(), self.device_names(), stream_infos, idents, self.stream_spans())
+        timeline = self.timeline_bytes() if want_timeline else None
+        return RunResult(report, stats, olist, None, timeline, k, t, h2d, d2h, nl)

@@ -1,0 +1,97 @@
+"""ctypes binding of libhapigpu.so (include/hapigpu.h).
+
+The library is built in-tree by `__graft_entry__.build()` (nvcc, sm_100a).
+There is no fallback: if the library or a CUDA device is missing, every entry
+point raises EngineError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+from .errors import EngineError
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "libhapigpu.so"
+CSRC = HERE / "csrc"
+INCLUDE = HERE.parent / "include"
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+    "--expt-relaxed-constexpr",
+]
+
+
+def sources():
+    return [CSRC / "engine.cu"]
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    deps = sources() + [CSRC / "hg_device.cuh", INCLUDE / "hapigpu.h"] + list(CSRC.glob("*.cuh"))
+    newest = max(p.stat().st_mtime for p in deps if p.exists())
+    if not force and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= newest:
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(LIB_PATH), *map(str, sources())]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    """Load libhapigpu.so once; raise EngineError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise EngineError(f"{LIB_PATH} is not built; run __graft_entry__.build()")
+    L = C.CDLL(str(LIB_PATH))
+    vp, u32, u64, i32, i64 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int32, C.c_int64
+    sig = {
+        "hg_abi_version": ([], C.c_int),
+        "hg_last_error": ([vp], C.c_char_p),
+        "hg_create": ([vp, vp], C.c_int),
+        "hg_destroy": ([vp], None),
+        "hg_set_registry": ([vp, vp, u32, C.c_char_p, u32, u32], C.c_int),
+        "hg_add_stream": ([vp, C.c_char_p, i64, i64, vp, u64], C.c_int),
+        "hg_clear_streams": ([vp], C.c_int),
+        "hg_stage": ([vp], C.c_int),
+        "hg_run": ([vp, u32], C.c_int),
+        "hg_run_local": ([vp, u32], C.c_int),
+        "hg_local_last_ts": ([vp, vp, vp], C.c_int),
+        "hg_finish": ([vp, u64], C.c_int),
+        "hg_get_stats": ([vp, vp], C.c_int),
+        "hg_get_tally": ([vp, vp, u64, vp], C.c_int),
+        "hg_get_device_names": ([vp, vp, u64, vp, u64, vp, vp], C.c_int),
+        "hg_get_stream_spans": ([vp, vp, u64], C.c_int),
+        "hg_get_orphans": ([vp, vp, u64, vp], C.c_int),
+        "hg_get_trace_errors": ([vp, vp, u64, vp], C.c_int),
+        "hg_timeline_size": ([vp, vp], C.c_int),
+        "hg_get_timeline": ([vp, vp, u64], C.c_int),
+        "hg_device_tally": ([vp, vp, vp], C.c_int),
+        "hg_last_timing": ([vp, vp, vp, vp, vp, vp], C.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    if L.hg_abi_version() != 1:
+        raise EngineError("libhapigpu ABI version mismatch")
+    _lib = L
+    return L
+
+
+EXPORTED = (
+    "hg_abi_version", "hg_last_error", "hg_create", "hg_destroy", "hg_set_registry", "hg_add_stream",
+    "hg_clear_streams", "hg_stage", "hg_run", "hg_run_local", "hg_local_last_ts", "hg_finish", "hg_get_stats",
+    "hg_get_tally", "hg_get_device_names", "hg_get_stream_spans", "hg_get_orphans", "hg_get_trace_errors",
+    "hg_timeline_size", "hg_get_timeline", "hg_device_tally", "hg_last_timing",
+)

@@ -1,0 +1,264 @@
+"""`run_pipeline` and the sink plugin API, served by the GPU engine.
+
+Mirrors `/root/reference/pkg/src/hapitrace/pipeline.py:250-314` and the tally
+and timeline sinks of `sinks.py:209-248, 341-418`: same sink contract
+(`name`, `consumes`, `on_start`, `on_streams`, `on_diagnostics`, `on_finish`),
+same duplicate-name and missing-registry errors, same `PipelineResult` /
+`IntervalStats` shapes.  The difference is where the work happens: the
+decode -> mux -> pair -> tally/timeline loop runs as CUDA kernels
+(csrc/engine.cu) instead of a per-event Python loop.
+
+Supported sinks: TallySink and TimelineSink from this package, plus any sink
+that does not override `on_message` (diagnostics-only sinks).  Sinks that
+need per-message callbacks are rejected with UnsupportedTraceError -- there
+is no CPU fallback path.
+"""
+
+from __future__ import annotations
+
+import json
+import threading
+from dataclasses import dataclass, field
+
+from .errors import PipelineError, UnsupportedTraceError
+from .registry import SchemaRegistry
+from .tally import TallyReport
+from .tracefile import RawStream, encode_record, stream_bytes
+
+END_OF_STREAM = "end_of_stream"
+
+
+@dataclass(frozen=True)
+class Message:
+    kind: str
+    event: object = None
+    span: object = None
+    sample: object = None
+
+
+@dataclass(frozen=True)
+class Span:
+    name: str
+    kind: str
+    hostname: str
+    pid: int
+    tid: int
+    start_ns: int
+    end_ns: int
+    entry_payload: dict = field(default_factory=dict)
+    exit_payload: dict = field(default_factory=dict)
+    result: int = 0
+    truncated: bool = False
+
+    @property
+    def duration_ns(self) -> int:
+        return self.end_ns - self.start_ns
+
+
+@dataclass
+class IntervalStats:
+    events_in: int = 0
+    passed: int = 0
+    host_spans: int = 0
+    truncated_spans: int = 0
+    device_spans: int = 0
+    samples: int = 0
+    orphan_exits: int = 0
+
+    def converted_events(self) -> int:
+        return 2 * self.host_spans + self.truncated_spans + self.device_spans + self.samples
+
+
+class Sink:
+    """Base class for analysis sinks (pipeline.py:250-263)."""
+
+    name = "sink"
+    consumes = "intervals"
+
+    def on_start(self, registry):
+        pass
+
+    def on_message(self, msg):
+        pass
+
+    def on_finish(self):
+        return None
+
+
+@dataclass
+class PipelineResult:
+    sink_results: dict
+    stats: IntervalStats
+    orphans: list = field(default_factory=list)
+    timing: dict = field(default_factory=dict)
+
+    def __getitem__(self, sink_name):
+        return self.sink_results[sink_name]
+
+
+class TallySink(Sink):
+    """Tally sink whose fold runs on the GPU (sinks.py:209-248 semantics)."""
+
+    name = "tally"
+    consumes = "intervals"
+
+    def on_start(self, registry):
+        self.report = TallyReport(fingerprint=registry.fingerprint,
+                                  backends=(f"BACKEND_{registry.api_name.upper()}",))
+
+    def on_message(self, msg):
+        raise UnsupportedTraceError("hapigpu's TallySink is fed by the GPU engine through run_pipeline")
+
+    def _gpu_result(self, report: TallyReport):
+        self.report = report
+
+    def on_finish(self) -> TallyReport:
+        return self.report
+
+
+class TimelineSink(Sink):
+    """Chrome-trace timeline whose JSON bytes are produced on the GPU (sinks.py:341-418)."""
+
+    name = "timeline"
+    consumes = "intervals"
+
+    def __init__(self, out_path=None, device_index: int = 0):
+        self.out_path = out_path
+        self.device_index = device_index
+        self._bytes = b"[]"
+
+    def on_message(self, msg):
+        raise UnsupportedTraceError("hapigpu's TimelineSink is fed by the GPU engine through run_pipeline")
+
+    def _gpu_result(self, blob: bytes):
+        self._bytes = blob
+
+    @property
+    def json_bytes(self) -> bytes:
+        return self._bytes
+
+    def on_finish(self):
+        if self.out_path is not None:
+            with open(self.out_path, "wb") as fh:
+                fh.write(self._bytes)
+        return json.loads(self._bytes)
+
+
+def _is_passive(sink) -> bool:
+    return type(sink).on_message is Sink.on_message or not hasattr(sink, "on_message")
+
+
+# ---------------------------------------------------------------------------
+# sources
+
+
+def _stream_label(cur, idx):
+    name = getattr(cur, "name", None)
+    if name:
+        return name
+    host = getattr(cur, "hostname", None)
+    if host is not None:
+        return f"{host}/{getattr(cur, 'pid', '?')}/{getattr(cur, 'tid', '?')}"
+    return f"input[{idx}]"
+
+
+def _raw_from_records(cursors, registry):
+    """Encode in-memory record iterables (pipeline.py:286 list sources) to stream bytes."""
+    raws, labels = [], []
+    for idx, cur in enumerate(cursors):
+        recs = list(cur)
+        label = _stream_label(cur, idx)
+        idents = {(r.hostname, r.pid, r.tid) for r in recs}
+        if len(idents) > 1:
+            raise UnsupportedTraceError(f"stream {label} mixes record identities {sorted(map(str, idents))}")
+        host, pid, tid = idents.pop() if idents else (None, None, None)
+        body = []
+        for r in recs:
+            if r.timestamp_ns is None:
+                raise UnsupportedTraceError("records without timestamps")
+            schema = registry.by_id.get(r.schema_id)
+            if schema is None:
+                raise UnsupportedTraceError(f"record with unknown schema id {r.schema_id}")
+            try:
+                body.append(encode_record(schema, r.timestamp_ns, r.payload))
+            except Exception as e:  # noqa: BLE001
+                raise UnsupportedTraceError(f"payload does not match its schema: {e}") from None
+        raws.append(RawStream(host, pid, tid, label, stream_bytes(body) if recs else b""))
+        labels.append(label)
+    # mux order: (hostname or "", pid or 0, tid or 0, input index)  (pipeline.py:88-91)
+    order = sorted(range(len(raws)), key=lambda i: (raws[i].hostname or "", raws[i].pid or 0, raws[i].tid or 0, i))
+    return [raws[i] for i in order]
+
+
+def _resolve_source(source, registry):
+    if hasattr(source, "raw_streams"):
+        return source.raw_streams(), (source.stream_infos() if hasattr(source, "stream_infos") else None)
+    if hasattr(source, "dir") and hasattr(source, "metadata"):  # a reference TraceReader
+        from .tracefile import open_trace_reader
+
+        ours = open_trace_reader(source.dir)
+        return ours.raw_streams(), ours.stream_infos()
+    cursors = source.streams() if hasattr(source, "streams") else list(source)
+    infos = source.stream_infos() if hasattr(source, "stream_infos") else None
+    return _raw_from_records(cursors, registry), infos
+
+
+# ---------------------------------------------------------------------------
+
+_engines = threading.local()
+
+
+def default_engine():
+    eng = getattr(_engines, "engine", None)
+    if eng is None:
+        from .engine import Engine
+
+        eng = Engine()
+        _engines.engine = eng
+    return eng
+
+
+def run_pipeline(source, sinks=(), registry=None, engine=None) -> PipelineResult:
+    """One GPU pass: decode, mux-order semantics, interval pairing, sinks' results."""
+    if registry is None:
+        registry = getattr(source, "registry", None)
+        if registry is None:
+            raise PipelineError("a registry is required when source is not a TraceReader")
+    if not isinstance(registry, SchemaRegistry):  # e.g. a reference registry object
+        registry = SchemaRegistry.from_dict(registry.to_dict())
+    raws, infos = _resolve_source(source, registry)
+    names = [s.name for s in sinks]
+    if len(set(names)) != len(names):
+        raise PipelineError(f"duplicate sink names: {names}")
+    tally = [s for s in sinks if isinstance(s, TallySink)]
+    timeline = [s for s in sinks if isinstance(s, TimelineSink)]
+    for s in sinks:
+        if not isinstance(s, (TallySink, TimelineSink)) and not _is_passive(s):
+            raise UnsupportedTraceError(
+                f"sink {s.name!r} needs per-message callbacks; hapigpu serves TallySink/TimelineSink")
+    device_index = {s.device_index for s in timeline}
+    if len(device_index) > 1:
+        raise UnsupportedTraceError("several TimelineSinks with different device_index")
+    for s in sinks:
+        s.on_start(registry)
+        if infos is not None and hasattr(s, "on_streams"):
+            s.on_streams(infos)
+    eng = engine or default_engine()
+    labels = [r.name for r in raws]
+    olabels = [f"{r.hostname}/{r.pid}/{r.tid}" for r in raws]
+    res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels, orphan_labels=olabels)
+    for s in sinks:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
+        hook = getattr(s, "on_diagnostics", None)
+        if hook is not None:
+            hook(list(res.orphans))
+    if res.error is not None:
+        raise res.error
+    for s in tally:
+        s._gpu_result(res.report)
+    for s in timeline:
+        s._gpu_result(res.timeline)
+    results = {s.name: s.on_finish() for s in sinks}
+    stats = IntervalStats(**res.stats)
+    timing = {"kernel_ms": res.kernel_ms, "total_ms": res.total_ms, "h2d_bytes": res.h2d_bytes,
+              "d2h_bytes": res.d2h_bytes, "launches": res.launches}
+    return PipelineResult(results, stats, res.orphans, timing)

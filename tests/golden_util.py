@@ -46,3 +46,23 @@ def check(exp, *, error, report=None, render=None, stats=None, orphans=None, tim
         blob = timeline if isinstance(timeline, bytes) else timeline.encode()
         assert len(blob) == exp["timeline_len"]
         assert hashlib.sha256(blob).hexdigest() == exp["timeline_sha256"]
+
+
+def Diag_factory():
+    """A diagnostics-only sink (no on_message override): collects on_diagnostics orphans."""
+    from paper_2504_03683_b200.pipeline import Sink
+
+    class Diag(Sink):
+        name = "diag"
+        consumes = "intervals"
+
+        def __init__(self):
+            self.orphans = None
+
+        def on_diagnostics(self, orphans):
+            self.orphans = list(orphans)
+
+        def on_finish(self):
+            return self.orphans
+
+    return Diag()
