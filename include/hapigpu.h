@@ -192,7 +192,9 @@ int hg_get_timeline(hg_ctx* ctx, char* out, uint64_t cap);
  * function-indexed.  Returns device pointers owned by the context. */
 int hg_device_tally(hg_ctx* ctx, void** host_rows, uint64_t* n_host_rows);
 
-/* timing of the last run (CUDA events around the kernels, ms) */
+/* timing of the last run, CUDA events on the engine's stream: kernel_ms = the
+ * dominant kernel (tile_kernel), total_ms = whole run from staging to results
+ * on the host; bytes moved host<->device and kernel launches of that run */
 int hg_last_timing(hg_ctx* ctx, float* kernel_ms, float* total_ms, uint64_t* h2d_bytes, uint64_t* d2h_bytes,
                    uint64_t* kernel_launches);
 

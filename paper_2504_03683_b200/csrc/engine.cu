@@ -9,19 +9,7 @@
 //   device spans, telemetry samples   pipeline.py:186-215, sampler.py:36-48
 //   truncation at the global last ts  pipeline.py:152, 220-240
 //   tally fold                        sinks.py:123-132, 230-242
-//
-// Kernel structure (one pass over the trace bytes):
-//   tile_kernel     persistent; one warp per 4 KiB stream tile.  The warp stages
-//                   the tile (+overhang) in shared memory, finds record
-//                   boundaries speculatively per lane, verifies them against the
-//                   preceding tile through a decoupled look-back on a tile-state
-//                   array, then decodes 32 records per round and runs the stack
-//                   automaton with ballot/shuffle elimination.  Completed spans
-//                   fold into a CTA-shared tally table; unresolved exits (empty
-//                   stack) and residual entries go to a small per-tile summary.
-//   compose_kernel  per stream, composes the tile summaries in order (the same
-//                   automaton over a tiny sequence), emits cross-tile spans,
-//                   orphans and the truncated spans at the global last ts.
+// Kernel design: see kernels.cuh.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,806 +18,571 @@
 #include <string>
 #include <vector>
 
-#include "hg_device.cuh"
+#include "kernels.cuh"
 
 using namespace hg;
 
 namespace {
 
-constexpr int kTile = 4096;                    // stream bytes per warp tile
-constexpr int kLaneBytes = kTile / kWarp;      // 128
-constexpr int kMaxRecLane = kLaneBytes / 16;   // 8
-constexpr int kMaxRecTile = kTile / 16;        // 256
-constexpr int kOverhang = 1024;
-constexpr int kWinBytes = kTile + kOverhang;   // staged window
-constexpr int kWarpsPerCta = 8;
-constexpr int kCtaThreads = kWarpsPerCta * kWarp;
-constexpr uint32_t kSmemFnMax = 2048;          // host rows tallied in shared memory up to this many functions
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-struct Elem {        // pending exit (bottom of the array) or stack frame (above)
-  uint64_t ts;
-  uint64_t result;
-  int32_t fn;
-  uint16_t seq;      // record index within the tile
-  uint16_t flags;    // bit0 exit, bit1 error, bit2 bad f64 result
+__device__ __forceinline__ void mbar_init(unsigned long long* m) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(m)));
+}
+__device__ __forceinline__ void bulk_load(uint32_t* dst, const void* src, uint32_t bytes, unsigned long long* m) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(m)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_addr(m)), "r"(parity) : "memory");
+  }
+}
+
+__host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~(size_t)127; }
+
+__host__ __device__ inline size_t lane_tab_bytes(uint32_t n_fn) { return ((size_t)3 * n_fn * kWarp + 3 * n_fn) * 4; }
+
+struct SmemLayout {
+  size_t tab, lanetab, dcache, ncache, warps, total;
+};
+__host__ __device__ inline SmemLayout smem_layout(uint32_t n_fn) {
+  SmemLayout L{};
+  size_t off = 0;
+  bool small = n_fn <= kSmallF;
+  L.tab = off;
+  if (!small && n_fn <= kSmemFnMax) off += align128(sizeof(SmemRow) * n_fn);
+  L.lanetab = off;
+  if (small) off += align128(lane_tab_bytes(n_fn) * kWarpsPerCta);
+  L.dcache = off;
+  off += align128(sizeof(DevRow) * kDevSlots);
+  L.ncache = off;
+  off += align128(sizeof(NameSlot) * kNameSlots);
+  L.warps = off;
+  off += sizeof(WarpSmem) * kWarpsPerCta;
+  L.total = off;
+  return L;
+}
+
+struct TileGeom {
+  uint32_t g, s, g0, j;
+  uint64_t size, t0, t1;
+  const uint8_t* gbase;
+  uint32_t nbytes;  // staged bytes
 };
 
-struct WarpSmem {
-  uint32_t win[kWinBytes / 4 + 4];
-  uint16_t roff[kMaxRecTile];
-  Elem elems[kMaxRecTile];
-};
-
-struct SmemRow {     // per-CTA host row accumulator
-  uint32_t count, err;
-  uint32_t s0, s1, s2, pad;   // 96-bit sum
-  unsigned long long mn, mx;
-};
-
-enum Stat { ST_EVENTS = 0, ST_PASSED, ST_HOST, ST_TRUNC, ST_DEVICE, ST_SAMPLES, ST_ORPHANS, ST_N };
-
-struct Params {
-  const uint8_t* data;
-  const uint64_t* stream_base;
-  const uint64_t* stream_size;
-  const uint32_t* tile_stream;    // stream-major tile id -> stream
-  const uint32_t* stream_tile0;   // stream -> first stream-major tile id
-  const uint32_t* order;          // processing order -> stream-major tile id
-  uint32_t n_tiles, n_streams;
-  const DSchema* schemas;
-  const int32_t* sid_map;
-  uint32_t max_sid;
-  const uint8_t* kinds;
-  const uint8_t* field_role;
-  uint32_t n_fn;
-  TileState* state;
-  uint32_t epoch;
-  SumEntry* pool;
-  unsigned long long* pool_used;
-  uint64_t pool_cap;
-  unsigned long long* host_acc;   // n_fn x 6: count, err, sum_lo, sum_hi, min, max
-  unsigned long long* dev_acc;    // row_cap x 6: count, err, sum_lo, sum_hi, min_b, max_b
-  uint32_t* wide_flag;
-  NameDict names;
-  hg_orphan* orphans;
-  unsigned long long* n_orphans;
-  uint64_t orphan_cap;
-  hg_trace_error* errors;
-  unsigned int* n_errors;
-  uint32_t error_cap;
-  unsigned long long* stats;
-  unsigned long long* last_ts;
-  unsigned long long* stream_spans;
-  unsigned int* work_counter;
-  uint32_t* watchdog;
-  uint32_t want;
-  // compose
-  SumEntry* stack_scratch;
-  unsigned long long* stack_used;
-  uint64_t stack_cap;
-  uint64_t global_last_ts;
-};
-
-// ---------------------------------------------------------------------------
-// small device helpers
-
-__device__ __forceinline__ const DSchema* schema_of(const Params& p, uint32_t sid) {
-  if (sid > p.max_sid) return nullptr;
-  int32_t si = __ldg(&p.sid_map[sid]);
-  return si < 0 ? nullptr : &p.schemas[si];
-}
-
-// header-level validity used to walk a chain (tracefile.py:199-210 order)
-__device__ __forceinline__ bool header_walkable(const Params& p, const Window& w, uint64_t off, uint64_t& next) {
-  if (off + 16 > w.size) return false;
-  uint32_t sid = rd32(w, off);
-  uint32_t plen = rd32(w, off + 12);
-  if (off + 16 + plen > w.size) return false;
-  if (!schema_of(p, sid)) return false;
-  next = off + 16 + plen;
-  return true;
-}
-
-// stricter plausibility used to pick speculative sync points
-__device__ __forceinline__ bool header_plausible(const Params& p, const Window& w, uint64_t off, uint64_t& next, uint64_t& ts) {
-  if (off + 16 > w.size) return false;
-  uint32_t sid = rd32(w, off);
-  const DSchema* s = schema_of(p, sid);
-  if (!s) return false;
-  uint32_t plen = rd32(w, off + 12);
-  if (off + 16 + plen > w.size) return false;
-  if (s->flags & SF_VAR) { if (plen < s->fixed_len) return false; }
-  else if (plen != s->fixed_len) return false;
-  next = off + 16 + plen;
-  ts = rd64(w, off + 4);
-  return true;
-}
-
-__device__ __forceinline__ bool sync_ok(const Params& p, const Window& w, uint64_t off) {
-  uint64_t next, ts, n2, ts2;
-  if (!header_plausible(p, w, off, next, ts)) return false;
-  if (next == w.size) return true;
-  if (!header_plausible(p, w, next, n2, ts2)) return false;
-  return ts2 >= ts;
-}
-
-// walk records from `entry` while they start before `sub1`; offsets go to roff
-__device__ __forceinline__ void lane_walk(const Params& p, const Window& w, uint64_t t0, uint64_t entry, uint64_t sub1,
-                                          uint16_t* roff_lane, uint32_t& cnt, uint64_t& exit, bool& fail,
-                                          uint64_t& fail_off) {
-  uint64_t off = entry;
-  cnt = 0;
-  fail = false;
-  while (off < sub1) {
-    uint64_t next;
-    if (!header_walkable(p, w, off, next)) { fail = true; fail_off = off; exit = kNone; return; }
-    roff_lane[cnt++] = (uint16_t)(off - t0);
-    off = next;
-  }
-  exit = off;
-}
-
-// intra-warp consistency of lane walks given the tile entry e0 (kNone = dead)
-__device__ void warp_verify(const Params& p, const Window& w, uint64_t t0, uint64_t sub1, uint16_t* roff_lane,
-                            uint64_t e0, uint64_t& hyp, uint32_t& cnt, uint64_t& exit, bool& fail, uint64_t& fail_off) {
-  const uint32_t lane = lane_id();
-  for (int it = 0; it < 2 * kWarp + 2; it++) {
-    uint64_t up = __shfl_up_sync(0xffffffffu, exit, 1);
-    uint64_t e_in = lane == 0 ? e0 : up;
-    bool good;
-    if (e_in == kNone) good = true;  // behind a failed lane: dead
-    else if (e_in >= sub1) good = (cnt == 0 && !fail && exit == e_in);
-    else good = (hyp == e_in);
-    if (__all_sync(0xffffffffu, good)) return;
-    if (!good) {
-      if (e_in >= sub1) { cnt = 0; fail = false; exit = e_in; hyp = e_in; }
-      else { hyp = e_in; lane_walk(p, w, t0, e_in, sub1, roff_lane, cnt, exit, fail, fail_off); }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// tile-state publication (decoupled look-back)
-
-__device__ __forceinline__ uint32_t st_status(const TileState* s) { return *(volatile const uint32_t*)&s->status; }
-__device__ __forceinline__ uint64_t vld(const uint64_t* a) { return *(volatile const uint64_t*)a; }
-__device__ __forceinline__ uint32_t vld32(const uint32_t* a) { return *(volatile const uint32_t*)a; }
-
-// state fields: spec_* and done_* never alias (see TileState in hg_device.cuh)
-struct Look {
-  uint64_t entry;  // true entry offset of this tile (kNone: predecessor chain failed)
-  uint64_t base;   // records of the stream before this tile
-  uint64_t prev_ts;
-  bool has_prev;
-};
-
-__device__ __forceinline__ uint32_t wait_status(const Params& p, const TileState* s, bool need_final) {
-  long long t_start = clock64();
-  for (uint32_t spins = 0;; spins++) {
-    uint32_t st = st_status(s);
-    if ((st >> 2) == p.epoch) {
-      uint32_t c = st & 3u;
-      if (c == TS_DONE || c == TS_ERROR || (!need_final && c == TS_SPEC)) { __threadfence(); return c; }
-    }
-    __nanosleep(64);
-    // watchdog: a predecessor that never publishes is an engine bug; fail loudly instead of hanging
-    if ((spins & 1023u) == 1023u && clock64() - t_start > (long long)8e9) {
-      atomicExch(p.watchdog, 1u);
-      return TS_ERROR;
-    }
-  }
-}
-
-// layout of the two publications inside TileState
-//   SPEC : spec_entry, exit (=spec exit), n_local (spec count), last_ts (spec last ts)
-//   DONE : pool_* unused here; done values in `incl`, `has_last`, and exit/last in
-//          the second half (we reuse pad fields through a side array, see below)
-struct DoneState { uint64_t exit, incl, last_ts; uint32_t has_last, pad; };
-
-__device__ Look lookback(const Params& p, const DoneState* done, uint32_t g0, uint32_t g, uint64_t size) {
-  Look L;
-  uint32_t k = g - 1;
-  for (;;) {  // walk back to the nearest final tile
-    uint32_t c = wait_status(p, &p.state[k], false);
-    if (c != TS_SPEC) break;
-    k--;  // the stream's first tile never publishes SPEC
-  }
-  for (;;) {
-    uint32_t c = wait_status(p, &p.state[k], true);
-    if (c == TS_ERROR) { L.entry = kNone; L.base = 0; L.prev_ts = 0; L.has_prev = false; return L; }
-    uint64_t e = vld(&done[k].exit);
-    uint64_t base = vld(&done[k].incl);
-    uint64_t last = vld(&done[k].last_ts);
-    bool has = vld32(&done[k].has_last) != 0;
-    bool broken = false;
-    uint32_t i = k + 1;
-    for (; i < g; i++) {
-      uint32_t ci = wait_status(p, &p.state[i], false);
-      if (ci == TS_ERROR) { L.entry = kNone; L.base = 0; L.prev_ts = 0; L.has_prev = false; return L; }
-      if (ci == TS_DONE) {
-        e = vld(&done[i].exit); base = vld(&done[i].incl); last = vld(&done[i].last_ts); has = vld32(&done[i].has_last) != 0;
-        continue;
-      }
-      const TileState* s = &p.state[i];
-      uint64_t se = vld(&s->spec_entry), sx = vld(&s->exit);
-      uint32_t sn = vld32(&s->n_local);
-      uint64_t t1 = min(16 + (uint64_t)(i - g0 + 1) * kTile, size);  // tile end (stream offset)
-      bool ok;
-      if (se == kNone) ok = (e >= t1);          // pass-through tile
-      else ok = (e == se) && sx != kNone;
-      if (!ok) { broken = true; break; }
-      if (se != kNone) {
-        e = sx;
-        base += sn;
-        if (sn) { last = vld(&s->last_ts); has = true; }
-      }
-    }
-    if (!broken) { L.entry = e; L.base = base; L.prev_ts = last; L.has_prev = has; return L; }
-    wait_status(p, &p.state[i], true);  // tile i repairs itself; continue from it
-    k = i;
-  }
-}
-
-__device__ __forceinline__ void publish(TileState* s, uint32_t epoch, uint32_t code) {
-  __threadfence();
-  *(volatile uint32_t*)&s->status = (epoch << 2) | code;
-}
-
-// ---------------------------------------------------------------------------
-// host-row folding (CTA shared table or global)
-
-__device__ __forceinline__ void smem_min_u64(unsigned long long* a, unsigned long long v) {
-  if (v < *(volatile unsigned long long*)a) atomicMin(a, v);
-}
-__device__ __forceinline__ void smem_max_u64(unsigned long long* a, unsigned long long v) {
-  if (v > *(volatile unsigned long long*)a) atomicMax(a, v);
-}
-
-__device__ void fold_host_lane(const Params& p, SmemRow* tab, int32_t fn, uint64_t dur, bool err) {
-  if (tab) {
-    SmemRow* r = &tab[fn];
-    atomicAdd(&r->count, 1u);
-    if (err) atomicAdd(&r->err, 1u);
-    uint32_t lo = (uint32_t)dur, hi = (uint32_t)(dur >> 32);
-    uint32_t o0 = atomicAdd(&r->s0, lo);
-    uint32_t c0 = (o0 + lo) < o0;
-    uint32_t add1 = hi + c0;
-    uint32_t c1 = (add1 < hi);  // hi + c0 overflowed
-    uint32_t o1 = atomicAdd(&r->s1, add1);
-    c1 += (o1 + add1) < o1;
-    if (c1) atomicAdd(&r->s2, c1);
-    smem_min_u64(&r->mn, dur);
-    smem_max_u64(&r->mx, dur);
-  } else {
-    unsigned long long* a = p.host_acc + 6ull * fn;
-    atomicAdd(&a[0], 1ull);
-    if (err) atomicAdd(&a[1], 1ull);
-    add_i128(&a[2], &a[3], dur, 0);
-    atomicMin(&a[4], dur);
-    atomicMax(&a[5], dur);
-  }
-}
-
-// fold this round's completed host spans, aggregating lanes with the same function
-__device__ void fold_host_round(const Params& p, SmemRow* tab, bool paired, int32_t fn, uint64_t dur, bool err) {
-  uint32_t todo = __ballot_sync(0xffffffffu, paired);
-  bool wide = __any_sync(0xffffffffu, paired && dur >= (1ull << 32));
-  if (wide || !tab) {
-    if (paired) fold_host_lane(p, tab, fn, dur, err);
-    return;
-  }
-  const uint32_t lane = lane_id();
-  while (todo) {
-    int leader = __ffs(todo) - 1;
-    int32_t f = __shfl_sync(0xffffffffu, fn, leader);
-    bool in = paired && fn == f;
-    uint32_t grp = __ballot_sync(0xffffffffu, in);
-    uint32_t errs = __ballot_sync(0xffffffffu, in && err);
-    if (in) {
-      uint32_t d = (uint32_t)dur;
-      uint32_t lo = __reduce_add_sync(grp, d & 0xffffu);
-      uint32_t hi = __reduce_add_sync(grp, d >> 16);
-      uint32_t mn = __reduce_min_sync(grp, d);
-      uint32_t mx = __reduce_max_sync(grp, d);
-      if ((int)lane == leader) {
-        SmemRow* r = &tab[f];
-        atomicAdd(&r->count, (uint32_t)__popc(grp));
-        if (errs) atomicAdd(&r->err, (uint32_t)__popc(errs));
-        uint64_t sum = (uint64_t)lo + ((uint64_t)hi << 16);  // < 2^37
-        uint32_t slo = (uint32_t)sum, shi = (uint32_t)(sum >> 32);
-        uint32_t o0 = atomicAdd(&r->s0, slo);
-        uint32_t add1 = shi + ((o0 + slo) < o0 ? 1u : 0u);
-        if (add1) {
-          uint32_t o1 = atomicAdd(&r->s1, add1);
-          if ((o1 + add1) < o1) atomicAdd(&r->s2, 1u);
-        }
-        smem_min_u64(&r->mn, mn);
-        smem_max_u64(&r->mx, mx);
-      }
-    }
-    todo &= ~grp;
-  }
-}
-
-__device__ __forceinline__ void fold_device(const Params& p, uint32_t row, uint64_t d_lo, int64_t d_hi) {
-  unsigned long long* a = p.dev_acc + 6ull * row;
-  atomicAdd(&a[0], 1ull);
-  add_i128(&a[2], &a[3], d_lo, d_hi);
-  // i128 (d_hi:d_lo) fits in i64 iff d_hi is the sign extension of d_lo
-  if (d_hi == ((int64_t)d_lo >> 63)) {
-    atomicMin(&a[4], bias64((int64_t)d_lo));
-    atomicMax(&a[5], bias64((int64_t)d_lo));
-  } else {
-    atomicExch(p.wide_flag, 1u);
-  }
-}
-
-__device__ void push_error(const Params& p, uint32_t code, uint32_t stream, uint64_t seq, uint64_t off, uint64_t ts,
-                           uint64_t prev_ts, uint64_t aux) {
-  unsigned int i = atomicAdd(p.n_errors, 1u);
-  if (i < p.error_cap) {
-    hg_trace_error e;
-    e.code = code; e.stream = stream; e.seq = seq; e.offset = off; e.ts = ts; e.prev_ts = prev_ts; e.aux = aux;
-    p.errors[i] = e;
-  }
-}
-
-__device__ void push_orphans(const Params& p, bool is_orphan, uint32_t stream, int32_t fn, uint64_t ts, uint64_t seq) {
-  uint32_t m = __ballot_sync(0xffffffffu, is_orphan);
-  if (!m) return;
-  unsigned long long base = 0;
-  if (lane_id() == 0) base = atomicAdd(p.n_orphans, (unsigned long long)__popc(m));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (is_orphan) {
-    uint64_t i = base + __popc(m & lanemask_lt());
-    if (i < p.orphan_cap) { hg_orphan o; o.stream = stream; o.function = fn; o.ts = ts; o.seq = seq; p.orphans[i] = o; }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// per-record decode (tracefile.py:147-169 + pipeline.py:150-218 classification)
-
-enum RecKind : uint32_t { RK_NONE = 0, RK_ENTRY = 1, RK_EXIT = 2 };
-
-struct RecOut {
-  uint32_t kind;     // RK_*
-  int32_t fn;
-  uint64_t ts;
-  uint64_t result;
-  uint32_t flags;    // bit1 error, bit2 bad f64 result
-  uint32_t dec_err;  // HG_ERR_* decode-level (pull) error
-  uint64_t dec_aux;
-  uint32_t feed_err; // HG_ERR_FEED / HG_ERR_TELEMETRY at this record
-  uint64_t feed_aux;
-};
-
-__device__ void decode_record(const Params& p, const Window& w, uint64_t off, uint32_t stream, RecOut& o,
-                              uint32_t& dev_spans, uint32_t& samples, uint32_t& passed) {
-  o.kind = RK_NONE; o.flags = 0; o.dec_err = 0; o.feed_err = 0; o.result = 0; o.fn = -1;
-  uint32_t sid = rd32(w, off);
-  o.ts = rd64(w, off + 4);
-  uint32_t plen = rd32(w, off + 12);
-  const uint64_t body = off + 16;
-  const DSchema* s = schema_of(p, sid);  // non-null: checked by the walk
-  uint64_t role_off[HG_NUM_ROLES];
-  #pragma unroll
-  for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
-  uint32_t name_len = 0;
-  if (!(s->flags & SF_VAR)) {
-    if (plen != s->fixed_len) { o.dec_err = HG_ERR_LEN_MISMATCH; return; }
-    #pragma unroll
-    for (int r = 0; r < HG_NUM_ROLES; r++) if (s->role[r] >= 0) role_off[r] = body + 8u * (uint32_t)s->role[r];
-  } else {
-    uint64_t q = 0;
-    const uint8_t* kd = p.kinds + s->kinds_off;
-    const uint8_t* fr = p.field_role + s->kinds_off;
-    for (uint32_t i = 0; i < s->nfields; i++) {
-      uint8_t k = __ldg(&kd[i]);
-      uint8_t role = __ldg(&fr[i]);
-      if (k < HG_KIND_STRING) {
-        if (q + 8 > plen) { o.dec_err = HG_ERR_STRUCT; o.dec_aux = (q << 8) | 8; return; }
-        if (role != 0xff) role_off[role] = body + q;
-        q += 8;
-      } else {
-        if (q + 4 > plen) { o.dec_err = HG_ERR_STRUCT; o.dec_aux = (q << 8) | 4; return; }
-        uint32_t ln = rd32(w, body + q);
-        q += 4;
-        if (q + ln > plen) { o.dec_err = HG_ERR_TRUNC_VAR; return; }
-        if (k == HG_KIND_STRING && !utf8_valid(w, body + q, ln)) { o.dec_err = HG_ERR_UTF8; o.dec_aux = q; return; }
-        if (role != 0xff) {
-          role_off[role] = body + q;
-          if (role == HG_ROLE_NAME) name_len = ln;
-        }
-        q += ln;
-      }
-    }
-    if (q != plen) { o.dec_err = HG_ERR_TRAILING; return; }
-  }
-  switch (s->cls) {
-    case HG_CLASS_ENTRY:
-      o.kind = RK_ENTRY; o.fn = s->fn;
-      return;
-    case HG_CLASS_EXIT: {
-      o.kind = RK_EXIT; o.fn = s->fn;
-      if (s->flags & SF_RESULT) {
-        uint64_t bits = rd64(w, role_off[HG_ROLE_RESULT]);
-        o.result = bits;
-        if (s->flags & SF_RESULT_F64) {
-          double x = __longlong_as_double((long long)bits);
-          if (isnan(x) || isinf(x)) o.flags |= 4;
-          else if (x >= 1.0 || x <= -1.0) o.flags |= 2;
-        } else if (bits != 0) {
-          o.flags |= 2;
-        }
-      }
-      return;
-    }
-    case HG_CLASS_DEVICE: {
-      if (s->flags & SF_FEED_ALWAYS) { o.feed_err = HG_ERR_FEED; o.feed_aux = sid; return; }
-      uint64_t a = rd64(w, role_off[HG_ROLE_START]);
-      uint64_t b = rd64(w, role_off[HG_ROLE_END]);
-      int64_t ah = (s->role_kind[HG_ROLE_START] == HG_KIND_I64 && (int64_t)a < 0) ? -1 : 0;
-      int64_t bh = (s->role_kind[HG_ROLE_END] == HG_KIND_I64 && (int64_t)b < 0) ? -1 : 0;
-      uint64_t d_lo = b - a;
-      int64_t d_hi = bh - ah - (b < a ? 1 : 0);
-      uint32_t row = name_lookup(p.names, w, role_off[HG_ROLE_NAME], name_len);
-      if (row != 0xffffffffu) fold_device(p, row, d_lo, d_hi);
-      dev_spans++;
-      return;
-    }
-    case HG_CLASS_TELEMETRY: {
-      if (s->flags & SF_FEED_ALWAYS) { o.feed_err = HG_ERR_FEED; o.feed_aux = sid; return; }
-      uint64_t bits = rd64(w, role_off[HG_ROLE_VALUE]);
-      uint8_t vk = s->role_kind[HG_ROLE_VALUE];
-      bool util = s->counter_kind >= HG_COUNTER_COMPUTE;
-      bool bad;
-      if (vk == HG_KIND_F64) {
-        double v = __longlong_as_double((long long)bits);
-        bad = util ? !(v >= 0.0 && v <= 1.0) : (v < 0.0);
-      } else if (vk == HG_KIND_I64) {
-        int64_t v = (int64_t)bits;
-        bad = util ? !(v >= 0 && v <= 1) : (v < 0);
-      } else {
-        bad = util ? (bits > 1) : false;
-      }
-      if (bad) { o.feed_err = HG_ERR_TELEMETRY; o.feed_aux = bits; return; }
-      samples++;
-      if ((s->flags & SF_FEED_TIMELINE) && (p.want & HG_WANT_TIMELINE)) { o.feed_err = HG_ERR_FEED; o.feed_aux = sid; }
-      return;
-    }
-    default:
-      passed++;
-      return;
-  }
+__device__ __forceinline__ TileGeom geom(const Params& p, uint32_t work) {
+  TileGeom G;
+  G.g = p.order[work];
+  G.s = p.tile_stream[G.g];
+  G.g0 = p.stream_tile0[G.s];
+  G.j = G.g - G.g0;
+  G.size = p.stream_size[G.s];
+  G.gbase = p.data + p.stream_base[G.s];
+  G.t0 = 16 + (uint64_t)G.j * kTile;
+  G.t1 = min(G.t0 + (uint64_t)kTile, G.size);
+  uint64_t padded = (G.size + 15) & ~(uint64_t)15;
+  G.nbytes = (uint32_t)min((uint64_t)kWinBytes, padded - G.t0);
+  return G;
 }
 
 // ---------------------------------------------------------------------------
 // the tile kernel
 
-__global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* done) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  SmemRow* tab = nullptr;
-  size_t tab_bytes = 0;
-  if (p.n_fn <= kSmemFnMax) {
-    tab = reinterpret_cast<SmemRow*>(smem_raw);
-    tab_bytes = ((sizeof(SmemRow) * p.n_fn + 127) / 128) * 128;
-    for (uint32_t i = threadIdx.x; i < p.n_fn; i += blockDim.x) {
-      SmemRow z; z.count = z.err = z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = ~0ull; z.mx = 0;
-      tab[i] = z;
+// one decoded record (lockstep round)
+struct Rec {
+  int32_t x;        // +1 entry, -1 exit, 0 other / inactive
+  uint32_t meta;    // packed meta (fn, flags, tile record index)
+  uint64_t ts;
+  uint64_t res;     // exit result bits
+};
+
+struct Seg { uint32_t s[5]; };
+
+// rare_record result: x = feed error, y = bit0 device span, bit1 sample; z/w = feed aux (lo/hi)
+using RareOut = uint4;
+
+// device-profiling and telemetry records (pipeline.py:186-215): out of line to keep the hot loop small
+__device__ __noinline__ RareOut rare_record(const Params& p, const uint32_t* win, Window w, uint64_t t0,
+                                            uint32_t win_len, uint32_t o, uint32_t sid, uint32_t plen, bool planned,
+                                            Seg seg, DevRow* dcache, NameSlot* ncache) {
+  RareOut out = make_uint4(0, 0, 0, 0);
+  const uint64_t a = t0 + o;
+  const uint2 d = desc_of(p, sid);
+  const uint32_t cls = d_cls(d), fl = d_flags(d);
+  const DSchema* sc = schema_of(p, sid);
+  if (fl & SF_FEED_ALWAYS) { out.x = HG_ERR_FEED; out.z = sid; return out; }
+  uint64_t role_off[HG_NUM_ROLES];
+  uint32_t name_len = 0;
+  if (!(fl & SF_VAR)) {
+    for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = sc->role[r] >= 0 ? a + 16 + 8u * (uint32_t)sc->role[r] : 0;
+  } else if (planned) {
+    for (int r = 0; r < HG_NUM_ROLES; r++) {
+      uint32_t sg = sc->role_seg[r];
+      role_off[r] = sg == 0xFF ? 0 : a + 16 + seg.s[sg] + sc->role_delta[r];
     }
+    if (sc->role_seg[HG_ROLE_NAME] != 0xFF) { name_len = rd32(w, role_off[HG_ROLE_NAME]); role_off[HG_ROLE_NAME] += 4; }
+    if (sc->role_seg[HG_ROLE_CMDKIND] != 0xFF) role_off[HG_ROLE_CMDKIND] += 4;
+  } else {
+    for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
+    uint64_t aux;
+    walk_fields(p, d, sid, a + 16, plen, [&](uint64_t x) { return rd32(w, x); }, w, role_off, name_len, aux);
   }
-  WarpSmem* ws = reinterpret_cast<WarpSmem*>(smem_raw + tab_bytes) + (threadIdx.x >> 5);
-  __syncthreads();
-
-  const uint32_t lane = lane_id();
-  uint32_t st_events = 0, st_passed = 0, st_host = 0, st_dev = 0, st_samples = 0, st_orph = 0;
-  uint64_t my_last_ts = 0;
-
-  for (;;) {
-    uint32_t work = 0;
-    if (lane == 0) work = atomicAdd(p.work_counter, 1u);
-    work = __shfl_sync(0xffffffffu, work, 0);
-    if (work >= p.n_tiles) break;
-    const uint32_t g = p.order[work];
-    const uint32_t s = p.tile_stream[g];
-    const uint32_t g0 = p.stream_tile0[s];
-    const uint32_t j = g - g0;
-    const uint64_t size = p.stream_size[s];
-    const uint8_t* gbase = p.data + p.stream_base[s];
-    const uint64_t t0 = 16 + (uint64_t)j * kTile;
-    const uint64_t t1 = min(t0 + kTile, size);
-
-    // ---- stage [t0, t0 + kWinBytes) (clipped to the padded stream end) in shared memory
-    Window w;
-    w.s = ws->win;
-    w.win_start = t0;
-    w.g = gbase;
-    w.size = size;
-    {
-      uint64_t want_end = min(t0 + (uint64_t)kWinBytes, (uint64_t)((size + 15) & ~(uint64_t)15));
-      uint32_t nvec = (uint32_t)((want_end - t0 + 15) / 16);
-      const uint4* src = reinterpret_cast<const uint4*>(gbase + t0);
-      uint4* dst = reinterpret_cast<uint4*>(ws->win);
-      for (uint32_t v = lane; v < nvec; v += kWarp) dst[v] = __ldg(&src[v]);
-      // staged bytes usable by rd32/rd64 (they read up to 8 bytes past off)
-      w.win_end = t0 + (uint64_t)nvec * 16;
-      if (lane < 4) ws->win[nvec * 4 + lane] = 0;
+  if (cls == HG_CLASS_DEVICE) {
+    uint64_t ua = rd64(w, role_off[HG_ROLE_START]);
+    uint64_t ub = rd64(w, role_off[HG_ROLE_END]);
+    int64_t ah = (sc->role_kind[HG_ROLE_START] == HG_KIND_I64 && (int64_t)ua < 0) ? -1 : 0;
+    int64_t bh = (sc->role_kind[HG_ROLE_END] == HG_KIND_I64 && (int64_t)ub < 0) ? -1 : 0;
+    uint64_t d_lo = ub - ua;
+    int64_t d_hi = bh - ah - (ub < ua ? 1 : 0);
+    uint64_t no = role_off[HG_ROLE_NAME];
+    uint32_t row = 0xffffffffu;
+    const bool inwin = no + name_len + 8 <= t0 + win_len;
+    const uint32_t nw = (uint32_t)(no - t0);
+    uint64_t h = inwin ? hash_window(win, nw, name_len) : hash_bytes(w, no, name_len);
+    NameSlot* slot = &ncache[h % kNameSlots];
+    unsigned long long ch = *(volatile unsigned long long*)&slot->hash;
+    uint32_t cr = *(volatile uint32_t*)&slot->row;
+    if (ch == h && cr < *(volatile uint32_t*)p.names.n_rows &&
+        (inwin ? name_equal_window(p.names, cr, win, nw, name_len) : name_equal(p.names, cr, w, no, name_len)))
+      row = cr;
+    if (row == 0xffffffffu) {
+      row = name_lookup(p.names, w, no, name_len);
+      if (row != 0xffffffffu) { slot->row = row; __threadfence_block(); slot->hash = h; }
     }
-    __syncwarp();
+    if (row != 0xffffffffu) fold_device(p, dcache, row, d_lo, d_hi);
+    out.y = 1;
+    return out;
+  }
+  // telemetry (sampler.py:36-48 range checks)
+  uint64_t bits = rd64(w, role_off[HG_ROLE_VALUE]);
+  uint8_t vk = sc->role_kind[HG_ROLE_VALUE];
+  bool util = sc->counter_kind >= HG_COUNTER_COMPUTE;
+  bool bad;
+  if (vk == HG_KIND_F64) {
+    double v = __longlong_as_double((long long)bits);
+    bad = util ? !(v >= 0.0 && v <= 1.0) : (v < 0.0);
+  } else if (vk == HG_KIND_I64) {
+    int64_t v = (int64_t)bits;
+    bad = util ? !(v >= 0 && v <= 1) : (v < 0);
+  } else {
+    bad = util ? (bits > 1) : false;
+  }
+  if (bad) { out.x = HG_ERR_TELEMETRY; out.z = (uint32_t)bits; out.w = (uint32_t)(bits >> 32); return out; }
+  out.y = 2;
+  if ((fl & SF_FEED_TIMELINE) && (p.want & HG_WANT_TIMELINE)) { out.x = HG_ERR_FEED; out.z = sid; }
+  return out;
+}
 
-    // ---- pass A: speculative boundaries per lane
-    const uint64_t sub0 = min(t0 + (uint64_t)lane * kLaneBytes, t1);
-    const uint64_t sub1 = min(sub0 + kLaneBytes, t1);
-    uint16_t* roff_lane = ws->roff + lane * kMaxRecLane;
-    uint64_t hyp = kNone, exit = kNone, fail_off = 0;
-    uint32_t cnt = 0;
-    bool fail = false;
-    for (uint64_t o = sub0; o < sub1; o++) {
-      if (sync_ok(p, w, o)) { hyp = o; break; }
-    }
-    if (hyp != kNone) lane_walk(p, w, t0, hyp, sub1, roff_lane, cnt, exit, fail, fail_off);
-    // tile hypothesis: first lane's sync point
-    uint32_t hmask = __ballot_sync(0xffffffffu, hyp != kNone);
-    uint64_t S = hmask ? __shfl_sync(0xffffffffu, hyp, __ffs(hmask) - 1) : kNone;
-    if (S != kNone) warp_verify(p, w, t0, sub1, roff_lane, S, hyp, cnt, exit, fail, fail_off);
+// generic payload validation for records the plan does not cover (or that leave the window)
+__device__ __noinline__ uint32_t generic_payload(const Params& p, const Window& w, uint64_t a, uint32_t sid,
+                                                 uint32_t plen, uint64_t& result_off, uint64_t& aux) {
+  const uint2 d = desc_of(p, sid);
+  uint64_t role_off[HG_NUM_ROLES];
+  for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
+  uint32_t name_len = 0;
+  uint32_t e = walk_fields(p, d, sid, a + 16, plen, [&](uint64_t x) { return rd32(w, x); }, w, role_off, name_len, aux);
+  result_off = role_off[HG_ROLE_RESULT];
+  return e;
+}
 
-    // ---- look-back: true entry, record base, previous ts
-    Look L;
-    if (j == 0) {
-      L.entry = 16; L.base = 0; L.prev_ts = 0; L.has_prev = false;
-    } else {
-      // publish the speculation
-      uint32_t n_spec = __reduce_add_sync(0xffffffffu, cnt);
-      uint64_t x31 = __shfl_sync(0xffffffffu, exit, 31);
-      // last record under the speculation
-      uint32_t lastmask = __ballot_sync(0xffffffffu, cnt > 0);
-      uint64_t spec_last = 0;
-      if (lastmask) {
-        int ll = 31 - __clz(lastmask);
-        uint64_t lo = 0;
-        if ((int)lane == ll) lo = rd64(w, t0 + roff_lane[cnt - 1] + 4);
-        spec_last = __shfl_sync(0xffffffffu, lo, ll);
-      }
-      bool spec_failed = __any_sync(0xffffffffu, fail && exit == kNone && hyp != kNone);
-      if (lane == 0) {
-        TileState* st = &p.state[g];
-        st->spec_entry = S;
-        st->exit = (S == kNone) ? kNone : (spec_failed ? kNone : x31);
-        st->n_local = S == kNone ? 0 : n_spec;
-        st->last_ts = spec_last;
-        publish(st, p.epoch, TS_SPEC);
-        L = lookback(p, done, g0, g, size);
-      }
-      L.entry = __shfl_sync(0xffffffffu, L.entry, 0);
-      L.base = __shfl_sync(0xffffffffu, L.base, 0);
-      L.prev_ts = __shfl_sync(0xffffffffu, L.prev_ts, 0);
-      L.has_prev = __shfl_sync(0xffffffffu, L.has_prev, 0);
-      if (L.entry == kNone) {  // the stream died in an earlier tile
-        if (lane == 0) publish(&p.state[g], p.epoch, TS_ERROR);
-        if (lane == 0) { p.state[g].pool_n_pending = 0; p.state[g].pool_n_resid = 0; }
-        continue;
-      }
-      bool consistent = (S == kNone) ? (L.entry >= t1) : (L.entry == S);
-      if (!consistent) {
-        if (S == kNone) { hyp = kNone; cnt = 0; exit = kNone; fail = false; }
-        warp_verify(p, w, t0, sub1, roff_lane, L.entry, hyp, cnt, exit, fail, fail_off);
-      }
-    }
-    if (j == 0) {
-      if (S != 16) warp_verify(p, w, t0, sub1, roff_lane, 16, hyp, cnt, exit, fail, fail_off);
-    }
-    // pass-through tile (entry beyond it) cannot fail and owns nothing
-    if (L.entry >= t1) { cnt = 0; fail = false; exit = L.entry; }
+// result field of a variable-payload exit whose result follows a string/blob (rare:
+// registries put `result` first); validates the payload on the way
+__device__ __noinline__ uint32_t var_exit_result(const Params& p, const uint32_t* win, Window w, uint64_t t0,
+                                                 uint32_t win_len, uint32_t o, uint32_t sid, uint32_t plen,
+                                                 uint64_t* result_off, uint64_t* aux) {
+  const DSchema* sc = schema_of(p, sid);
+  const uint64_t a = t0 + o;
+  uint32_t seg[5];
+  if (o + 16 + plen <= win_len && var_plan(sc, win, w, o + 16, plen, seg)) {
+    *result_off = a + 16 + seg_sel(seg, sc->role_seg[HG_ROLE_RESULT]) + sc->role_delta[HG_ROLE_RESULT];
+    return 0;
+  }
+  return generic_payload(p, w, a, sid, plen, *result_off, *aux);
+}
 
-    // ---- header-level failure: first failing lane whose walk started at its true entry
-    uint64_t e_up = __shfl_up_sync(0xffffffffu, exit, 1);
-    uint64_t e_in = lane == 0 ? L.entry : e_up;
-    bool real_fail = fail && e_in != kNone && hyp == e_in;
-    uint32_t fmask = __ballot_sync(0xffffffffu, real_fail);
-    int fl = fmask ? __ffs(fmask) - 1 : 32;
-    if ((int)lane > fl) cnt = 0;
-    // inclusive count before each lane
-    uint32_t incl = cnt;
-    #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) { uint32_t v = __shfl_up_sync(0xffffffffu, incl, d); if ((int)lane >= d) incl += v; }
-    const uint32_t n_rec = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t lane_base = incl - cnt;
-    // compact record offsets into tile order
-    uint16_t tmp[kMaxRecLane];
-    #pragma unroll
-    for (int k = 0; k < kMaxRecLane; k++) tmp[k] = (k < (int)cnt) ? roff_lane[k] : 0;
-    __syncwarp();
-    #pragma unroll
-    for (int k = 0; k < kMaxRecLane; k++) if (k < (int)cnt) ws->roff[lane_base + k] = tmp[k];
-    __syncwarp();
-    uint64_t tile_last_ts = 0;
-    if (n_rec) {
-      uint64_t v = 0;
-      if (lane == 0) v = rd64(w, t0 + ws->roff[n_rec - 1] + 4);
-      tile_last_ts = __shfl_sync(0xffffffffu, v, 0);
-    }
-    uint64_t true_exit = __shfl_sync(0xffffffffu, exit, 31);
-    if (lane == 0) {
-      DoneState* d = &done[g];
-      d->exit = true_exit;
-      d->incl = L.base + n_rec;
-      d->last_ts = n_rec ? tile_last_ts : L.prev_ts;
-      d->has_last = (n_rec || L.has_prev) ? 1u : 0u;
-    }
-    uint64_t ffo = __shfl_sync(0xffffffffu, fail_off, fl < 32 ? fl : 0);
-    if (lane == 0) {
-      if (fmask) {
-        uint32_t code;
-        uint64_t aux = 0;
-        uint64_t ts_f = 0;
-        if (ffo + 16 > size) code = HG_ERR_TRUNC_HEADER;
-        else {
-          uint32_t sid = rd32(w, ffo);
-          uint32_t plen = rd32(w, ffo + 12);
-          ts_f = rd64(w, ffo + 4);
-          if (ffo + 16 + plen > size) code = HG_ERR_TRUNC_PAYLOAD;
-          else { code = HG_ERR_UNKNOWN_SCHEMA; aux = sid; }
-        }
-        uint64_t prev = n_rec ? tile_last_ts : L.prev_ts;
-        push_error(p, code, s, L.base + n_rec, ffo, ts_f, prev, aux);
-        publish(&p.state[g], p.epoch, TS_ERROR);
-      } else {
-        publish(&p.state[g], p.epoch, TS_DONE);
-      }
-    }
-
-    // ---- passes B + C: decode 32 records per round, run the stack automaton
-    uint32_t n_pend = 0, top = 0;   // elems[0, n_pend) pending exits, [n_pend, top) stack
-    uint64_t prev_round_ts = L.prev_ts;
-    bool have_prev = L.has_prev;
-    bool cut = false;
-    uint32_t feed_done = 0, dec_done = 0;
-    uint32_t tile_spans = 0;
-    for (uint32_t rb = 0; rb < n_rec && !cut; rb += kWarp) {
-      const uint32_t r = rb + lane;
-      const bool act = r < n_rec;
-      RecOut ro;
-      ro.kind = RK_NONE; ro.dec_err = 0; ro.feed_err = 0; ro.flags = 0; ro.ts = 0; ro.fn = -1; ro.result = 0;
-      uint64_t off = 0;
-      uint32_t dsp = 0;
-      if (act) {
-        off = t0 + ws->roff[r];
-        decode_record(p, w, off, s, ro, dsp, st_samples, st_passed);
-      }
-      // monotonicity (pipeline.py:98-99): against the previous record of the stream
-      uint64_t up_ts = __shfl_up_sync(0xffffffffu, ro.ts, 1);
-      bool has_p = lane == 0 ? have_prev : true;
-      uint64_t pts = lane == 0 ? prev_round_ts : up_ts;
-      if (act && ro.dec_err == 0 && has_p && ro.ts < pts) ro.dec_err = HG_ERR_ORDER;
-      // first decode-level error in the round cuts the stream
-      uint32_t dm = __ballot_sync(0xffffffffu, act && ro.dec_err != 0);
-      int dl = dm ? __ffs(dm) - 1 : 32;
-      if (dm) {
-        cut = true;
-        if ((int)lane == dl && !dec_done) {
-          push_error(p, ro.dec_err, s, L.base + r, off, ro.ts, has_p ? pts : 0, ro.dec_aux);
-        }
-        dec_done = 1;
-      }
-      bool live = act && (int)lane < dl;
-      if (live) {
-        st_events++;
-        st_dev += dsp;
-        if (ro.ts > my_last_ts) my_last_ts = ro.ts;
-      }
-      tile_spans += __reduce_add_sync(0xffffffffu, live ? dsp : 0u);
-      prev_round_ts = __shfl_sync(0xffffffffu, ro.ts, 31);
-      if (n_rec - rb < 32) prev_round_ts = __shfl_sync(0xffffffffu, ro.ts, (n_rec - rb - 1) & 31);
-      have_prev = true;
-
-      // ---- stack automaton over this round (pipeline.py:156-185)
-      const bool isE = live && ro.kind == RK_ENTRY;
-      const bool isX = live && ro.kind == RK_EXIT;
-      uint32_t unres = __ballot_sync(0xffffffffu, isE || isX);
-      const uint32_t Emask = __ballot_sync(0xffffffffu, isE);
-      bool paired = false, orphan = false, me_unres = isE || isX;
-      uint64_t entry_ts = 0;
-      for (int it = 0; it < kWarp; it++) {
-        uint32_t pm = unres & lanemask_lt();
-        int pred = pm ? 31 - __clz(pm) : 0;
-        int32_t pfn = __shfl_sync(0xffffffffu, ro.fn, pred);
-        uint64_t pts2 = __shfl_sync(0xffffffffu, ro.ts, pred);
-        bool act2 = isX && me_unres && pm && ((Emask >> pred) & 1u);
-        bool m = act2 && pfn == ro.fn;
-        bool o = act2 && pfn != ro.fn;
-        uint32_t Mx = __ballot_sync(0xffffffffu, m);
-        uint32_t Ox = __ballot_sync(0xffffffffu, o);
-        if (!(Mx | Ox)) break;
-        // entries claimed by a matching exit: the next unresolved element after them
-        uint32_t nm = unres & lanemask_gt();
-        int succ = nm ? __ffs(nm) - 1 : 0;
-        bool claimed = isE && me_unres && nm && ((Mx >> succ) & 1u);
-        uint32_t Ce = __ballot_sync(0xffffffffu, claimed);
-        if (m) { paired = true; entry_ts = pts2; me_unres = false; }
-        if (o) { orphan = true; me_unres = false; }
-        if (claimed) me_unres = false;
-        unres &= ~(Mx | Ox | Ce);
-      }
-      // remaining: X* E*.  Resolve the leading exits against the tile stack.
-      uint32_t Xs = __ballot_sync(0xffffffffu, isX && me_unres);
-      while (Xs) {
-        int jx = __ffs(Xs) - 1;
-        int32_t fj = __shfl_sync(0xffffffffu, ro.fn, jx);
-        if (top > n_pend) {
-          Elem tp = ws->elems[top - 1];
-          if (tp.fn == fj) {
-            if ((int)lane == jx) { paired = true; entry_ts = tp.ts; }
-            top--;
-          } else if ((int)lane == jx) {
-            orphan = true;
+// hot per-record decode: header, descriptor, fixed-length check, class, exit result.
+// Payload validation of variable records and all device/telemetry work is deferred
+// (returns true) to the warp queue, drained with every lane active.
+__device__ __forceinline__ bool decode_one_rec(const Params& p, const uint32_t* win, const Window& w, uint64_t t0,
+                                               uint32_t win_len, uint32_t o, uint32_t rec, Rec& R,
+                                               uint32_t& dec_err, uint64_t& dec_aux, uint32_t& st_passed) {
+  const uint32_t sid = s32(win, o);
+  const uint32_t plen = s32(win, o + 12);
+  R.ts = s64(win, o + 4);
+  R.x = 0;
+  R.res = 0;
+  const uint2 d = desc_of(p, sid);
+  const uint32_t cls = d_cls(d), fl = d_flags(d);
+  R.meta = (d.x & M_FN) | (rec << 23);
+  const bool var = (fl & SF_VAR) != 0;
+  if (!var && plen != d_fixed(d)) { dec_err = HG_ERR_LEN_MISMATCH; return false; }
+  if (cls == HG_CLASS_ENTRY) {
+    R.x = 1;
+    return var;
+  }
+  if (cls == HG_CLASS_EXIT) {
+    R.x = -1;
+    R.meta |= M_EXIT;
+    if (fl & SF_RESULT) {
+      const uint64_t a = t0 + o;
+      uint64_t result_off = a + 16 + 8u * d_resfield(d);  // fixed: field index * 8
+      if (var) {
+        // y carries (role_seg<<8 | role_delta>>...) only for fixed schemas; read the plan for var ones
+        const DSchema* sc = schema_of(p, sid);
+        if (sc->role_seg[HG_ROLE_RESULT] == 0 && sc->nvar != kNoPlan) {
+          result_off = a + 16 + sc->role_delta[HG_ROLE_RESULT];
+          if (result_off + 8 > a + 16 + plen) {  // malformed: let the generic walk name the error
+            uint32_t e = var_exit_result(p, win, w, t0, win_len, o, sid, plen, &result_off, &dec_aux);
+            if (e) { dec_err = e; return false; }
           }
         } else {
-          // empty tile stack: pending until composed with the preceding tiles
-          if ((int)lane == jx) {
-            Elem e; e.ts = ro.ts; e.result = ro.result; e.fn = ro.fn; e.seq = (uint16_t)r;
-            e.flags = (uint16_t)(1u | (ro.flags & 6u));
-            ws->elems[n_pend] = e;
-          }
-          n_pend++; top++;
+          uint32_t e = var_exit_result(p, win, w, t0, win_len, o, sid, plen, &result_off, &dec_aux);
+          if (e) { dec_err = e; return false; }
         }
-        __syncwarp();
-        Xs &= Xs - 1;
       }
-      // push the round's unresolved entries
-      uint32_t Es = __ballot_sync(0xffffffffu, isE && me_unres);
-      if (isE && me_unres) {
-        Elem e; e.ts = ro.ts; e.result = 0; e.fn = ro.fn; e.seq = (uint16_t)r; e.flags = 0;
-        ws->elems[top + __popc(Es & lanemask_lt())] = e;
-      }
-      top += __popc(Es);
-      __syncwarp();
-      // interval-stage errors (first per tile): device/telemetry feed errors, and
-      // NaN/inf f64 results, which only raise when the exit pairs (pipeline.py:169-183)
-      bool bad_res = paired && (ro.flags & 4u);
-      uint32_t fm = __ballot_sync(0xffffffffu, (live && ro.feed_err != 0) || bad_res);
-      if (fm && !feed_done) {
-        if ((int)lane == __ffs(fm) - 1) {
-          if (bad_res) push_error(p, HG_ERR_RESULT, s, L.base + r, off, ro.ts, 0, ro.result);
-          else push_error(p, ro.feed_err, s, L.base + r, off, ro.ts, 0, ro.feed_aux);
-        }
-        feed_done = 1;
-      }
-      fold_host_round(p, tab, paired, ro.fn, ro.ts - entry_ts, (ro.flags & 2u) != 0);
-      if (paired) st_host++;
-      tile_spans += __popc(__ballot_sync(0xffffffffu, paired));
-      push_orphans(p, orphan, s, ro.fn, ro.ts, L.base + r);
-      if (orphan) st_orph++;
-    }
-
-    // ---- tile summary for the composition pass
-    if (lane == 0) {
-      unsigned long long off = top ? atomicAdd(p.pool_used, (unsigned long long)top) : 0ull;
-      p.state[g].pool_off = off;
-      p.state[g].pool_n_pending = n_pend;
-      p.state[g].pool_n_resid = top - n_pend;
-      if (tile_spans) atomicAdd(&p.stream_spans[s], (unsigned long long)tile_spans);
-    }
-    unsigned long long poff = 0;
-    if (lane == 0) poff = p.state[g].pool_off;
-    poff = __shfl_sync(0xffffffffu, poff, 0);
-    __syncwarp();
-    for (uint32_t i = lane; i < top; i += kWarp) {
-      if (poff + i < p.pool_cap) {
-        Elem e = ws->elems[i];
-        SumEntry o;
-        o.ts = e.ts; o.seq = L.base + e.seq; o.fn = e.fn; o.flags = e.flags; o.result = e.result;
-        p.pool[poff + i] = o;
+      const uint64_t bits = (result_off + 12 <= t0 + win_len) ? s64(win, (uint32_t)(result_off - t0)) : rd64(w, result_off);
+      R.res = bits;
+      if (fl & SF_RESULT_F64) {
+        const double xv = __longlong_as_double((long long)bits);
+        if (isnan(xv)) R.meta |= M_BAD | M_NAN;
+        else if (isinf(xv)) R.meta |= M_BAD;
+        else if (xv >= 1.0 || xv <= -1.0) R.meta |= M_ERR;
+      } else if (bits) {
+        R.meta |= M_ERR;
       }
     }
-    __syncwarp();
+    return var;
   }
+  if (cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY) return true;
+  st_passed++;
+  return var;
+}
 
-  // ---- flush per-lane statistics
+// drain up to 32 deferred records, one per lane: payload validation (tracefile.py:152-169)
+// and device/telemetry handling (pipeline.py:186-215)
+__device__ __noinline__ uint4 drain_queue(const Params& p, WarpSmem* ws, Window w, uint64_t t0, uint32_t win_len,
+                                          uint32_t s, uint64_t base, uint32_t n, DevRow* dcache, NameSlot* ncache) {
+  const uint32_t lane = lane_id();
+  const uint32_t* win = ws->win;
+  uint32_t dev = 0, samples = 0;
+  if (lane < n) {
+    const uint32_t e = ws->q[lane];
+    const uint32_t o = e & 0xFFFFu, rec = e >> 16;
+    const uint64_t a = t0 + o;
+    const uint32_t sid = s32(win, o);
+    const uint32_t plen = s32(win, o + 12);
+    const uint2 d = desc_of(p, sid);
+    const uint32_t cls = d_cls(d);
+    bool planned = false;
+    Seg seg;
+    uint32_t err = 0;
+    uint64_t aux = 0;
+    if (d_flags(d) & SF_VAR) {
+      const DSchema* sc = schema_of(p, sid);
+      if (o + 16 + plen <= win_len && var_plan(sc, win, w, o + 16, plen, seg.s)) {
+        planned = true;
+      } else {
+        uint64_t ro;
+        err = generic_payload(p, w, a, sid, plen, ro, aux);
+      }
+    }
+    if (err) {
+      push_error(p, err, s, base + rec, a, s64(win, o + 4), 0, aux);
+    } else if (cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY) {
+      RareOut ro = rare_record(p, win, w, t0, win_len, o, sid, plen, planned, seg, dcache, ncache);
+      if (ro.x) push_error(p, ro.x, s, base + rec, a, s64(win, o + 4), 0, (uint64_t)ro.z | ((uint64_t)ro.w << 32));
+      dev = ro.y & 1u;
+      samples = (ro.y >> 1) & 1u;
+    }
+  }
+  return make_uint4(dev, samples, 0, 0);
+}
+
+// materialise the fast-path tile state (pending exits + open levels) as an explicit stack
+__device__ __noinline__ void to_exact(WarpSmem* ws, SumEntry* scratch, uint64_t base, uint32_t n_pend, int32_t Dc) {
+  const uint32_t lane = lane_id();
+  for (uint32_t i = lane; i < n_pend; i += kWarp) {
+    SumEntry e;
+    uint32_t m = ws->pend_meta[i];
+    e.ts = ws->pend_ts[i]; e.seq = base + m_rec(m); e.fn = m_fn(m);
+    e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u);
+    e.result = ws->pend_res[i];
+    scratch[i] = e;
+  }
+  for (int32_t lv = 1 + (int32_t)lane; lv <= Dc; lv += kWarp) {
+    SumEntry e;
+    uint32_t m = ws->lvl_meta[lv];
+    e.ts = ws->lvl_ts[lv]; e.seq = base + m_rec(m); e.fn = m_fn(m);
+    e.flags = 0; e.result = 0;
+    scratch[n_pend + lv - 1] = e;
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// per-tile phases (out of line: executed once per tile, kept out of the hot loop)
+
+struct TileCtx {
+  SmemRow* tab;
+  DevRow* dcache;
+  NameSlot* ncache;
+  WarpSmem* ws;
+  SumEntry* scratch;
+  HostFold hf;
+};
+
+struct Found {      // result of pass A + look-back
+  Look L;
+  uint32_t n_rec;
+  bool dead;       // the stream failed in an earlier tile: nothing to do
+};
+
+// pass A + look-back + record list (tracefile.py:198-210 boundaries)
+__device__ __noinline__ Found find_records(const Params& p, DoneState* done, WarpSmem* ws, const TileGeom G,
+                                           const Window w) {
+  const uint32_t lane = lane_id();
+  const uint32_t* win = ws->win;
+  const uint64_t t0 = G.t0, size = G.size;
+  const uint32_t tlen = (uint32_t)(G.t1 - G.t0);
+  const uint32_t win_len = G.nbytes;
+  const uint32_t s = G.s;
+  Found F;
+  F.dead = false;
+  // speculative sync per lane, in lockstep: 4 candidate offsets per step, each
+  // screened (known schema id, payload length consistent with it) without
+  // branching; only survivors get the two-header check
+  const uint32_t sub0 = min(lane * (uint32_t)kLaneBytes, tlen);
+  const uint32_t sub1 = min(sub0 + (uint32_t)kLaneBytes, tlen);
+  uint32_t hyp = kNone32, exit = kNone32, cnt = 0, fail_off = 0;
+  bool fail = false;
+  {
+    uint32_t wo = sub0 & ~3u;
+    bool searching = sub0 < sub1;
+    while (__any_sync(0xffffffffu, searching)) {
+      if (searching) {
+        const uint32_t wi = wo >> 2;
+        const uint32_t a0 = win[wi], a1 = win[wi + 1], c0 = win[wi + 3], c1 = win[wi + 4];
+        uint32_t cm = 0;
+        #pragma unroll
+        for (uint32_t b = 0; b < 4; b++) {
+          const uint32_t o = wo + b;
+          const uint32_t sid = __funnelshift_r(a0, a1, 8 * b);
+          const uint32_t plen = __funnelshift_r(c0, c1, 8 * b);
+          uint2 d = make_uint2(0, 0);
+          if (sid <= p.max_sid) d = __ldg(&p.desc[sid]);
+          const bool fixed_ok = !(d_flags(d) & SF_VAR) && plen == d_fixed(d);
+          const bool var_ok = (d_flags(d) & SF_VAR) && plen >= d_fixed(d);
+          const bool ok = d_present(d) && (fixed_ok || var_ok) && o >= sub0 && o < sub1 &&
+                          t0 + o + 16 + plen <= size;
+          cm |= (ok ? 1u : 0u) << b;
+        }
+        while (cm) {
+          const uint32_t b = __ffs(cm) - 1;
+          cm &= cm - 1;
+          if (sync_ok(p, win, t0, size, win_len, wo + b)) { hyp = wo + b; cm = 0; searching = false; }
+        }
+        wo += 4;
+        if (wo >= sub1) searching = false;
+      }
+    }
+  }
+  if (hyp != kNone32) lane_walk(p, ws, win, t0, size, hyp, sub1, cnt, exit, fail, fail_off);
+  uint32_t hmask = __ballot_sync(0xffffffffu, hyp != kNone32);
+  uint32_t S = hmask ? __shfl_sync(0xffffffffu, hyp, __ffs(hmask) - 1) : kNone32;
+  if (S != kNone32) warp_verify(p, ws, win, t0, size, sub1, S, hyp, cnt, exit, fail, fail_off);
+  Look L;
+  if (G.j == 0) {
+    L.entry = 16; L.base = 0; L.prev_ts = 0; L.has_prev = false;
+    if (S != 0) warp_verify(p, ws, win, t0, size, sub1, 0, hyp, cnt, exit, fail, fail_off);
+  } else {
+    uint32_t n_spec = __reduce_add_sync(0xffffffffu, cnt);
+    uint32_t x31 = __shfl_sync(0xffffffffu, exit, 31);
+    uint32_t lastmask = __ballot_sync(0xffffffffu, cnt > 0);
+    uint64_t spec_last = 0;
+    if (lastmask) {
+      int ll = 31 - __clz(lastmask);
+      uint64_t v = 0;
+      if ((int)lane == ll) v = s64(win, ws->roff[cnt - 1][lane] + 4);
+      spec_last = __shfl_sync(0xffffffffu, v, ll);
+    }
+    bool spec_failed = __any_sync(0xffffffffu, fail && exit == kNone32 && hyp != kNone32);
+    if (lane == 0) {
+      TileState* st = &p.state[G.g];
+      st->spec_entry = S == kNone32 ? kNone : t0 + S;
+      st->exit = (S == kNone32 || spec_failed || x31 == kNone32) ? kNone : t0 + x31;
+      st->n_local = S == kNone32 ? 0 : n_spec;
+      st->last_ts = spec_last;
+      publish(st, p.epoch, TS_SPEC);
+      L = lookback(p, done, G.g0, G.g, size);
+    }
+    L.entry = __shfl_sync(0xffffffffu, L.entry, 0);
+    L.base = __shfl_sync(0xffffffffu, L.base, 0);
+    L.prev_ts = __shfl_sync(0xffffffffu, L.prev_ts, 0);
+    L.has_prev = __shfl_sync(0xffffffffu, L.has_prev, 0);
+    if (L.entry == kNone) {
+      if (lane == 0) {
+        p.state[G.g].pool_n_pending = 0;
+        p.state[G.g].pool_n_resid = 0;
+        publish(&p.state[G.g], p.epoch, TS_ERROR);
+      }
+      F.dead = true;
+      F.L = L;
+      F.n_rec = 0;
+      return F;
+    }
+    uint64_t erel64 = L.entry - t0;
+    uint32_t erel = erel64 > 0x7FFFFFFFull ? 0x7FFFFFFFu : (uint32_t)erel64;
+    bool consistent = (S == kNone32) ? (erel >= tlen) : (erel == S);
+    if (!consistent) {
+      if (S == kNone32) { hyp = kNone32; cnt = 0; exit = kNone32; fail = false; }
+      warp_verify(p, ws, win, t0, size, sub1, erel, hyp, cnt, exit, fail, fail_off);
+    }
+    if (erel >= tlen) { cnt = 0; fail = false; exit = erel; }
+  }
+  // real header-level failure: the first failing lane whose walk started at its true entry
+  uint32_t e_up = __shfl_up_sync(0xffffffffu, exit, 1);
+  uint32_t e_in = lane == 0 ? (uint32_t)min(L.entry - t0, (uint64_t)0x7FFFFFFFu) : e_up;
+  bool real_fail = fail && e_in != kNone32 && hyp == e_in;
+  uint32_t fmask = __ballot_sync(0xffffffffu, real_fail);
+  int fl = fmask ? __ffs(fmask) - 1 : 32;
+  if ((int)lane > fl) cnt = 0;
+  uint32_t incl = cnt;
+  for (int d = 1; d < 32; d <<= 1) { uint32_t v = __shfl_up_sync(0xffffffffu, incl, d); if ((int)lane >= d) incl += v; }
+  const uint32_t n_rec = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t lane_base = incl - cnt;
+  for (uint32_t k = 0; k < cnt; k++) ws->rlist[lane_base + k] = ws->roff[k][lane];
+  __syncwarp();
+  uint64_t tile_last = 0;
+  if (n_rec) {
+    uint64_t v = 0;
+    if (lane == 0) v = s64(win, ws->rlist[n_rec - 1] + 4);
+    tile_last = __shfl_sync(0xffffffffu, v, 0);
+  }
+  uint32_t true_exit = __shfl_sync(0xffffffffu, exit, 31);
+  uint32_t ffo = __shfl_sync(0xffffffffu, fail_off, fl < 32 ? fl : 0);
+  if (lane == 0) {
+    DoneState* d = &done[G.g];
+    d->exit = t0 + true_exit;
+    d->incl = L.base + n_rec;
+    d->last_ts = n_rec ? tile_last : L.prev_ts;
+    d->has_last = (n_rec || L.has_prev) ? 1u : 0u;
+    if (fmask) {
+      uint64_t a = t0 + ffo;
+      uint32_t code;
+      uint64_t aux = 0, ts_f = 0;
+      if (a + 16 > size) code = HG_ERR_TRUNC_HEADER;
+      else {
+        uint32_t sid = rd32(w, a);
+        uint32_t plen = rd32(w, a + 12);
+        ts_f = rd64(w, a + 4);
+        if (a + 16 + plen > size) code = HG_ERR_TRUNC_PAYLOAD;
+        else { code = HG_ERR_UNKNOWN_SCHEMA; aux = sid; }
+      }
+      push_error(p, code, s, L.base + n_rec, a, ts_f, n_rec ? tile_last : L.prev_ts, aux);
+      publish(&p.state[G.g], p.epoch, TS_ERROR);
+    } else {
+      publish(&p.state[G.g], p.epoch, TS_DONE);
+    }
+  }
+  F.L = L;
+  F.n_rec = n_rec;
+  return F;
+}
+
+// tile summary for compose_kernel: pending exits, then open entries (innermost last)
+__device__ __noinline__ void write_summary(const Params& p, WarpSmem* ws, SumEntry* scratch, uint32_t g, uint32_t s,
+                                           uint64_t base, bool slow, uint32_t n_pend, int32_t Dc, const GStack gs,
+                                           uint32_t spans) {
+  const uint32_t lane = lane_id();
+  uint32_t sum_np, sum_n;
+  if (!slow) { sum_np = n_pend; sum_n = n_pend + (uint32_t)Dc; }
+  else { sum_np = gs.n_pend; sum_n = gs.top; }
+  const uint32_t tspans = __reduce_add_sync(0xffffffffu, spans);
+  unsigned long long poff = 0;
+  if (lane == 0) {
+    poff = sum_n ? atomicAdd(p.pool_used, (unsigned long long)sum_n) : 0ull;
+    p.state[g].pool_off = poff;
+    p.state[g].pool_n_pending = sum_np;
+    p.state[g].pool_n_resid = sum_n - sum_np;
+    if (tspans) atomicAdd(&p.stream_spans[s], (unsigned long long)tspans);
+  }
+  poff = __shfl_sync(0xffffffffu, poff, 0);
+  for (uint32_t i = lane; i < sum_n; i += kWarp) {
+    if (poff + i >= p.pool_cap) continue;
+    SumEntry e;
+    if (slow) {
+      e = scratch[i];
+    } else if (i < n_pend) {
+      uint32_t m = ws->pend_meta[i];
+      e.ts = ws->pend_ts[i]; e.seq = base + m_rec(m); e.fn = m_fn(m); e.result = ws->pend_res[i];
+      e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u);
+    } else {
+      uint32_t lv = i - n_pend + 1;
+      uint32_t m = ws->lvl_meta[lv];
+      e.ts = ws->lvl_ts[lv]; e.seq = base + m_rec(m); e.fn = m_fn(m); e.result = 0; e.flags = 0;
+    }
+    p.pool[poff + i] = e;
+  }
+  __syncwarp();
+}
+
+__device__ __noinline__ void fold_slow(const Params& p, const HostFold hf, int32_t fn, uint64_t dur, bool err) {
+  hf.fold(p, fn, dur, err);
+}
+
+__device__ __noinline__ TileCtx tile_prologue(const Params& p, const SmemLayout SL, uint8_t* smem) {
+  TileCtx C;
+  const uint32_t lane = lane_id();
+  const uint32_t warp = threadIdx.x >> 5;
+  const bool small = p.n_fn <= kSmallF;
+  C.tab = (!small && p.n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(smem + SL.tab) : nullptr;
+  C.dcache = reinterpret_cast<DevRow*>(smem + SL.dcache);
+  C.ncache = reinterpret_cast<NameSlot*>(smem + SL.ncache);
+  C.ws = reinterpret_cast<WarpSmem*>(smem + SL.warps) + warp;
+  C.hf.small = small;
+  C.hf.tab = C.tab;
+  if (small) {
+    uint32_t* b = reinterpret_cast<uint32_t*>(smem + SL.lanetab + lane_tab_bytes(p.n_fn) * warp);
+    uint32_t n = p.n_fn * kWarp;
+    C.hf.lt.cnt = b; C.hf.lt.slo = b + n; C.hf.lt.shi = b + 2 * n;
+    C.hf.lt.err = b + 3 * n; C.hf.lt.mn = b + 3 * n + p.n_fn; C.hf.lt.mx = b + 3 * n + 2 * p.n_fn;
+    for (uint32_t i = lane; i < n; i += kWarp) { C.hf.lt.cnt[i] = 0; C.hf.lt.slo[i] = 0; C.hf.lt.shi[i] = 0; }
+    for (uint32_t i = lane; i < p.n_fn; i += kWarp) { C.hf.lt.err[i] = 0; C.hf.lt.mn[i] = 0xFFFFFFFFu; C.hf.lt.mx[i] = 0; }
+  }
+  if (C.tab)
+    for (uint32_t i = threadIdx.x; i < p.n_fn; i += blockDim.x) {
+      SmemRow z; z.count = z.err = z.s0 = z.s1 = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
+      C.tab[i] = z;
+    }
+  for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
+    DevRow z; z.tag = 0; z.count = 0; z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = ~0ull; z.mx = 0;
+    C.dcache[i] = z;
+  }
+  for (uint32_t i = threadIdx.x; i < kNameSlots; i += blockDim.x) { C.ncache[i].hash = 0; C.ncache[i].row = 0; }
+  if (lane == 0) {
+    mbar_init(&C.ws->mbar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  C.scratch = p.warp_scratch + (size_t)(blockIdx.x * kWarpsPerCta + warp) * kMaxRecTile;
+  return C;
+}
+
+struct Counters {
+  uint32_t events, passed, host, dev, samples, orph;
+  uint64_t last_ts;
+};
+
+__device__ __noinline__ void tile_epilogue(const Params& p, const TileCtx C, const Counters K) {
+  const uint32_t lane = lane_id();
   auto wsum = [](uint32_t v) { return __reduce_add_sync(0xffffffffu, v); };
-  uint32_t a0 = wsum(st_events), a1 = wsum(st_passed), a2 = wsum(st_host), a3 = wsum(st_dev), a4 = wsum(st_samples),
-           a5 = wsum(st_orph);
-  uint64_t mts = my_last_ts;
-  #pragma unroll
+  uint32_t a0 = wsum(K.events), a1 = wsum(K.passed), a2 = wsum(K.host), a3 = wsum(K.dev), a4 = wsum(K.samples),
+           a5 = wsum(K.orph);
+  uint64_t mts = K.last_ts;
   for (int d = 16; d; d >>= 1) { uint64_t v = __shfl_xor_sync(0xffffffffu, mts, d); mts = v > mts ? v : mts; }
   if (lane == 0) {
     if (a0) atomicAdd(&p.stats[ST_EVENTS], (unsigned long long)a0);
@@ -840,7 +593,365 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
     if (a5) atomicAdd(&p.stats[ST_ORPHANS], (unsigned long long)a5);
     atomicMax(p.last_ts, (unsigned long long)mts);
   }
-  // ---- flush the CTA host table
+  __syncwarp();
+  if (C.hf.small) {
+    for (uint32_t f = 0; f < p.n_fn; f++) {
+      uint32_t i = f * kWarp + lane;
+      uint64_t cc = C.hf.lt.cnt[i], sum = ((uint64_t)C.hf.lt.shi[i] << 32) | C.hf.lt.slo[i];
+      if (!__any_sync(0xffffffffu, cc != 0)) continue;
+      for (int d = 16; d; d >>= 1) {
+        cc += __shfl_xor_sync(0xffffffffu, cc, d);
+        sum += __shfl_xor_sync(0xffffffffu, sum, d);
+      }
+      if (lane == 0 && cc) {
+        unsigned long long* a = p.host_acc + 6ull * f;
+        atomicAdd(&a[0], (unsigned long long)cc);
+        if (C.hf.lt.err[f]) atomicAdd(&a[1], (unsigned long long)C.hf.lt.err[f]);
+        add_i128(&a[2], &a[3], sum, 0);
+        atomicMin(&a[4], (unsigned long long)C.hf.lt.mn[f]);
+        atomicMax(&a[5], (unsigned long long)C.hf.lt.mx[f]);
+      }
+    }
+  }
+  __syncthreads();
+  if (C.tab) {
+    for (uint32_t f = threadIdx.x; f < p.n_fn; f += blockDim.x) {
+      SmemRow r = C.tab[f];
+      if (!r.count) continue;
+      unsigned long long* a = p.host_acc + 6ull * f;
+      atomicAdd(&a[0], (unsigned long long)r.count);
+      if (r.err) atomicAdd(&a[1], (unsigned long long)r.err);
+      add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), 0);
+      atomicMin(&a[4], (unsigned long long)r.mn);
+      atomicMax(&a[5], (unsigned long long)r.mx);
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
+    DevRow r = C.dcache[i];
+    if (!r.tag || !r.count) continue;
+    unsigned long long* a = p.dev_acc + 6ull * (r.tag - 1);
+    atomicAdd(&a[0], (unsigned long long)r.count);
+    add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), (int64_t)(int32_t)r.s2);
+    atomicMin(&a[4], r.mn);
+    atomicMax(&a[5], r.mx);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the tile kernel
+
+__global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* done) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const SmemLayout SL = smem_layout(p.n_fn);
+  const uint32_t lane = lane_id();
+  const TileCtx C = tile_prologue(p, SL, smem);
+  __syncthreads();
+  WarpSmem* ws = C.ws;
+  const uint32_t* win = ws->win;
+  Counters K;
+  K.events = K.passed = K.host = K.dev = K.samples = K.orph = 0;
+  K.last_ts = 0;
+  uint32_t parity = 0;
+
+  for (;;) {
+    uint32_t work = 0;
+    if (lane == 0) work = atomicAdd(p.work_counter, 1u);
+    work = __shfl_sync(0xffffffffu, work, 0);
+    if (work >= p.n_tiles) break;
+    const TileGeom G = geom(p, work);
+    __syncwarp();
+    if (lane == 0) bulk_load(ws->win, G.gbase + G.t0, G.nbytes, &ws->mbar);
+    mbar_wait(&ws->mbar, parity);
+    parity ^= 1u;
+    Window w;  // generic accessor for fields that leave the window
+    w.s = win; w.win_start = G.t0; w.win_end = G.t0 + G.nbytes; w.g = G.gbase; w.size = G.size;
+    const Found F = find_records(p, done, ws, G, w);
+    if (F.dead) continue;
+    const Look& L = F.L;
+    const uint32_t n_rec = F.n_rec;
+    const uint32_t s = G.s;
+    const uint64_t t0 = G.t0;
+    const uint32_t win_len = G.nbytes;
+
+    // ---- rounds: lockstep decode + pairing
+    uint64_t prev_ts = L.prev_ts;
+    bool have_prev = L.has_prev;
+    int32_t Dc = 0;            // depth (open entries of this tile) before the round
+    uint32_t n_pend = 0;       // pending exits so far
+    bool slow = false;         // exact elimination mode (GStack in scratch)
+    GStack gs;
+    gs.base = C.scratch;
+    gs.n_pend = 0;
+    gs.top = 0;
+    bool feed_done = false;
+    uint32_t spans = 0;
+    uint32_t qn = 0;           // deferred records waiting in ws->q
+    for (uint32_t rb = 0; rb < n_rec; rb += kWarp) {
+      const uint32_t r = rb + lane;
+      const bool act = r < n_rec;
+      Rec R;
+      R.x = 0; R.meta = 0; R.ts = 0; R.res = 0;
+      uint32_t dec_err = 0;
+      uint64_t dec_aux = 0;
+      uint32_t o = 0;
+      bool defer = false;
+      if (act) {
+        o = ws->rlist[r];
+        defer = decode_one_rec(p, win, w, t0, win_len, o, r, R, dec_err, dec_aux, K.passed);
+      }
+      // monotonicity against the previous record of the stream (pipeline.py:98-99)
+      const uint64_t up_ts = __shfl_up_sync(0xffffffffu, R.ts, 1);
+      const bool hp = lane == 0 ? have_prev : true;
+      const uint64_t pts = lane == 0 ? prev_ts : up_ts;
+      if (act && !dec_err && hp && R.ts < pts) dec_err = HG_ERR_ORDER;
+      const uint32_t dm = __ballot_sync(0xffffffffu, act && dec_err);
+      const int dl = dm ? __ffs(dm) - 1 : 32;
+      if (dm && (int)lane == dl) push_error(p, dec_err, s, L.base + r, t0 + o, R.ts, hp ? pts : 0, dec_aux);
+      const bool live = act && (int)lane < dl;
+      if (!live) R.x = 0;
+      if (live) {
+        K.events++;
+        K.last_ts = R.ts > K.last_ts ? R.ts : K.last_ts;
+      }
+      {  // defer payload work to the queue; drain it 32 at a time
+        const uint32_t Qm = __ballot_sync(0xffffffffu, live && defer);
+        if (live && defer) ws->q[qn + __popc(Qm & lanemask_lt())] = o | (r << 16);
+        qn += __popc(Qm);
+        __syncwarp();
+        if (qn >= (uint32_t)kWarp) {
+          const uint4 dq = drain_queue(p, ws, w, t0, win_len, s, L.base, kWarp, C.dcache, C.ncache);
+          K.dev += dq.x;
+          K.samples += dq.y;
+          spans += dq.x;
+          qn -= kWarp;
+          if (lane < qn) ws->q[lane] = ws->q[kWarp + lane];
+          __syncwarp();
+        }
+      }
+      prev_ts = __shfl_sync(0xffffffffu, R.ts, min(31u, n_rec - 1 - rb));
+      have_prev = true;
+
+      // ---- pairing
+      const bool isE = R.x > 0, isX = R.x < 0;
+      bool paired = false, orphan = false;
+      uint64_t ets = 0;
+      if (!slow) {
+        const uint32_t Em = __ballot_sync(0xffffffffu, isE);
+        const uint32_t Xm = __ballot_sync(0xffffffffu, isX);
+        const uint32_t le = lanemask_lt() | (1u << lane);
+        // depth within the tile: ballot prefix counts, clamped at zero when exits meet an empty stack
+        const int32_t ps = (int32_t)__popc(Em & le) - (int32_t)__popc(Xm & le);
+        int32_t after = Dc + ps;
+        if (__any_sync(0xffffffffu, after < 0)) {
+          int32_t m = ps;
+          for (int d = 1; d < 32; d <<= 1) {
+            int32_t t = __shfl_up_sync(0xffffffffu, m, d);
+            if ((int)lane >= d) m = min(m, t);
+          }
+          after = Dc + ps - min(0, Dc + min(-Dc, m));
+        }
+        int32_t before = __shfl_up_sync(0xffffffffu, after, 1);
+        if (lane == 0) before = Dc;
+        const bool pops = isX && before > 0;
+        const bool pend = isX && before <= 0;
+        const int32_t level = isE ? after : before;
+        const bool too_deep = __any_sync(0xffffffffu, (isE || pops) && level >= kLevels);
+        const uint32_t Pm = __ballot_sync(0xffffffffu, pend);
+        const bool pend_full = n_pend + __popc(Pm) > (uint32_t)kPendCap;
+        const uint32_t key = (isE || pops) ? (uint32_t)level : (0x80000000u | lane);
+        const uint32_t same = __match_any_sync(0xffffffffu, key);
+        const uint32_t cand = same & Em & lanemask_lt();
+        const int el = cand ? 31 - __clz(cand) : 0;
+        const uint32_t cmeta = __shfl_sync(0xffffffffu, R.meta, el);
+        const uint64_t cts = __shfl_sync(0xffffffffu, R.ts, el);
+        uint32_t emeta = 0;
+        if (pops) {
+          if (cand) { emeta = cmeta; ets = cts; }
+          else if (level < kLevels) { emeta = ws->lvl_meta[level]; ets = ws->lvl_ts[level]; }
+        }
+        const bool mism = pops && ((emeta ^ R.meta) & M_FN) != 0;
+        if (!__any_sync(0xffffffffu, mism) && !too_deep && !pend_full) {
+          paired = pops;
+          if (isE && !(same & Em & lanemask_gt())) { ws->lvl_ts[level] = R.ts; ws->lvl_meta[level] = R.meta; }
+          if (pend) {
+            const uint32_t i = n_pend + __popc(Pm & lanemask_lt());
+            ws->pend_ts[i] = R.ts; ws->pend_res[i] = R.res; ws->pend_meta[i] = R.meta;
+          }
+          n_pend += __popc(Pm);
+          Dc = __shfl_sync(0xffffffffu, after, 31);
+          __syncwarp();
+        } else {
+          to_exact(ws, C.scratch, L.base, n_pend, Dc);
+          gs.n_pend = n_pend;
+          gs.top = n_pend + (uint32_t)Dc;
+          slow = true;
+        }
+      }
+      if (slow) {
+        SumEntry mine;
+        mine.ts = R.ts; mine.seq = L.base + r; mine.fn = m_fn(R.meta);
+        mine.flags = (isX ? 1u : 0u) | ((R.meta & M_ERR) ? 2u : 0u) | ((R.meta & M_BAD) ? 4u : 0u) |
+                     ((R.meta & M_NAN) ? 8u : 0u);
+        mine.result = R.res;
+        const RoundOut ro2 = round_resolve(gs, true, isE, isX, m_fn(R.meta), R.ts, mine);
+        paired = ro2.flags & 1u;
+        orphan = (ro2.flags >> 1) & 1u;
+        ets = ro2.ets;
+        gs.n_pend = ro2.n_pend;
+        gs.top = ro2.top;
+      }
+      if (paired) {
+        const uint64_t dur = R.ts - ets;
+        const int32_t fn = m_fn(R.meta);
+        if (C.hf.small && (dur >> 32) == 0) {
+          const uint32_t i = (uint32_t)fn * kWarp + lane, d = (uint32_t)dur;
+          C.hf.lt.cnt[i] += 1;
+          const uint32_t lo = C.hf.lt.slo[i] + d;
+          C.hf.lt.shi[i] += lo < d ? 1u : 0u;
+          C.hf.lt.slo[i] = lo;
+          if (d < C.hf.lt.mn[fn]) atomicMin(&C.hf.lt.mn[fn], d);
+          if (d > C.hf.lt.mx[fn]) atomicMax(&C.hf.lt.mx[fn], d);
+          if (R.meta & M_ERR) atomicAdd(&C.hf.lt.err[fn], 1u);
+        } else {
+          fold_slow(p, C.hf, fn, dur, (R.meta & M_ERR) != 0);
+        }
+        K.host++;
+        spans++;
+      }
+      const uint32_t bm = __ballot_sync(0xffffffffu, paired && (R.meta & M_BAD));
+      if (bm && !feed_done) {
+        if ((int)lane == __ffs(bm) - 1) push_error(p, HG_ERR_RESULT, s, L.base + r, t0 + o, R.ts, 0, R.res);
+        feed_done = true;
+      }
+      if (orphan) { push_orphan(p, s, m_fn(R.meta), R.ts, L.base + r); K.orph++; }
+      if (dm) break;  // the stream is cut at the failing record
+    }
+    if (qn) {
+      const uint4 dq = drain_queue(p, ws, w, t0, win_len, s, L.base, qn, C.dcache, C.ncache);
+      K.dev += dq.x;
+      K.samples += dq.y;
+      spans += dq.x;
+    }
+    write_summary(p, ws, C.scratch, G.g, s, L.base, slow, n_pend, Dc, gs, spans);
+  }
+  tile_epilogue(p, C, K);
+}
+
+// ---------------------------------------------------------------------------
+// composition of tile summaries per stream (exact automaton from an empty stack)
+
+constexpr int kComposeWarps = 4;
+
+__global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t lane = lane_id();
+  const uint32_t warp = threadIdx.x >> 5;
+  SmemRow* tab = p.n_fn <= kSmemFnMax ? reinterpret_cast<SmemRow*>(smem) : nullptr;
+  if (tab)
+    for (uint32_t i = threadIdx.x; i < p.n_fn; i += blockDim.x) {
+      SmemRow z; z.count = z.err = z.s0 = z.s1 = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
+      tab[i] = z;
+    }
+  __syncthreads();
+  HostFold hf;
+  hf.small = false;
+  hf.tab = tab;
+  const uint32_t s = blockIdx.x * kComposeWarps + warp;
+  uint32_t host = 0, orph = 0, trunc = 0, spans = 0;
+  if (s < p.n_streams) {
+    const uint32_t g0 = p.stream_tile0[s];
+    const uint32_t g1 = (s + 1 < p.n_streams) ? p.stream_tile0[s + 1] : p.n_tiles;
+    // first failed tile (its summary is still composed) and the stack capacity
+    uint32_t gerr = g1;
+    unsigned long long need = 0;
+    for (uint32_t g = g0 + lane; g < g1; g += kWarp) {
+      if ((p.state[g].status & 3u) == TS_ERROR && g < gerr) gerr = g;
+      need += p.state[g].pool_n_resid;
+    }
+    gerr = __reduce_min_sync(0xffffffffu, gerr);
+    #pragma unroll
+    for (int d = 16; d; d >>= 1) need += __shfl_xor_sync(0xffffffffu, need, d);
+    const uint32_t gend = gerr < g1 ? gerr + 1 : g1;
+    unsigned long long sbase = 0;
+    if (lane == 0 && need) sbase = atomicAdd(p.stack_used, need);
+    sbase = __shfl_sync(0xffffffffu, sbase, 0);
+    if (sbase + need <= p.stack_cap) {
+      GStack gs;
+      gs.base = p.stack_scratch + sbase;
+      gs.n_pend = 0;
+      gs.top = 0;
+      bool res_done = false;
+      for (uint32_t gb = g0; gb < gend; gb += kWarp) {
+        uint32_t g = gb + lane;
+        bool valid = g < gend;
+        uint32_t np = valid ? p.state[g].pool_n_pending : 0;
+        uint32_t nr = valid ? p.state[g].pool_n_resid : 0;
+        unsigned long long poff = valid ? p.state[g].pool_off : 0;
+        uint32_t c = np + nr, ein = c;
+        #pragma unroll
+        for (int d = 1; d < 32; d <<= 1) { uint32_t v = __shfl_up_sync(0xffffffffu, ein, d); if ((int)lane >= d) ein += v; }
+        const uint32_t T = __shfl_sync(0xffffffffu, ein, 31);
+        const uint32_t ebase = ein - c;
+        for (uint32_t r = 0; r < T; r += kWarp) {
+          uint32_t e = r + lane;
+          bool act = e < T;
+          uint32_t owner = 0;
+          #pragma unroll
+          for (int step = 16; step; step >>= 1) {
+            uint32_t cand = owner + step;
+            uint32_t b = __shfl_sync(0xffffffffu, ebase, cand & 31);
+            if (cand < 32 && b <= e) owner = cand;
+          }
+          uint32_t ob = __shfl_sync(0xffffffffu, ebase, owner);
+          uint32_t onp = __shfl_sync(0xffffffffu, np, owner);
+          unsigned long long opoff = __shfl_sync(0xffffffffu, poff, owner);
+          uint32_t k = e - ob;
+          SumEntry x;
+          x.ts = 0; x.seq = 0; x.fn = -1; x.flags = 0; x.result = 0;
+          if (act && opoff + k < p.pool_cap) x = p.pool[opoff + k];
+          bool isX = act && k < onp;
+          bool isE = act && k >= onp;
+          bool paired, orphan;
+          uint64_t ets;
+          const RoundOut ro2 = round_resolve(gs, false, isE, isX, x.fn, x.ts, x);
+          paired = ro2.flags & 1u;
+          orphan = (ro2.flags >> 1) & 1u;
+          ets = ro2.ets;
+          gs.n_pend = ro2.n_pend;
+          gs.top = ro2.top;
+          if (paired) {
+            hf.fold(p, x.fn, x.ts - ets, (x.flags & 2u) != 0);
+            host++;
+            spans++;
+          }
+          uint32_t bm = __ballot_sync(0xffffffffu, paired && (x.flags & 4u));
+          if (bm && !res_done) {
+            if ((int)lane == __ffs(bm) - 1)
+              push_error(p, HG_ERR_RESULT, s, x.seq, 0, x.ts, 0, x.result ? x.result : ((x.flags & 8u) ? 0x7FF8000000000000ull : 0x7FF0000000000000ull));
+            res_done = true;
+          }
+          if (orphan) { push_orphan(p, s, x.fn, x.ts, x.seq); orph++; }
+        }
+      }
+      // open calls become truncated spans ending at the global last timestamp
+      for (uint32_t i = lane; i < gs.top; i += kWarp) {
+        SumEntry en = gs.base[i];
+        hf.fold(p, en.fn, p.global_last_ts - en.ts, false);
+        trunc++;
+        spans++;
+      }
+    } else if (lane == 0) {
+      atomicExch(p.watchdog, 2u);  // stack scratch exhausted (host grows and reruns)
+    }
+  }
+  uint32_t a0 = __reduce_add_sync(0xffffffffu, host), a1 = __reduce_add_sync(0xffffffffu, orph),
+           a2 = __reduce_add_sync(0xffffffffu, trunc), a3 = __reduce_add_sync(0xffffffffu, spans);
+  if (lane == 0) {
+    if (a0) atomicAdd(&p.stats[ST_HOST], (unsigned long long)a0);
+    if (a1) atomicAdd(&p.stats[ST_ORPHANS], (unsigned long long)a1);
+    if (a2) atomicAdd(&p.stats[ST_TRUNC], (unsigned long long)a2);
+    if (a3 && s < p.n_streams) atomicAdd(&p.stream_spans[s], (unsigned long long)a3);
+  }
   __syncthreads();
   if (tab) {
     for (uint32_t f = threadIdx.x; f < p.n_fn; f += blockDim.x) {
@@ -849,74 +960,11 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
       unsigned long long* a = p.host_acc + 6ull * f;
       atomicAdd(&a[0], (unsigned long long)r.count);
       if (r.err) atomicAdd(&a[1], (unsigned long long)r.err);
-      uint64_t lo = (uint64_t)r.s0 | ((uint64_t)r.s1 << 32);
-      add_i128(&a[2], &a[3], lo, (int64_t)r.s2);
-      atomicMin(&a[4], r.mn);
-      atomicMax(&a[5], r.mx);
+      add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), 0);
+      atomicMin(&a[4], (unsigned long long)r.mn);
+      atomicMax(&a[5], (unsigned long long)r.mx);
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// composition of tile summaries per stream (exact automaton from an empty stack)
-
-__global__ void compose_kernel(Params p) {
-  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= p.n_streams) return;
-  const uint32_t g0 = p.stream_tile0[s];
-  const uint32_t g1 = (s + 1 < p.n_streams) ? p.stream_tile0[s + 1] : p.n_tiles;
-  uint64_t need = 0;
-  uint32_t gend = g1;
-  for (uint32_t g = g0; g < g1; g++) {
-    need += p.state[g].pool_n_resid;
-    if ((p.state[g].status & 3u) == TS_ERROR) { gend = g + 1; break; }
-  }
-  unsigned long long sbase = need ? atomicAdd(p.stack_used, (unsigned long long)need) : 0ull;
-  if (sbase + need > p.stack_cap) return;  // host detects via stack_used
-  SumEntry* st = p.stack_scratch + sbase;
-  uint64_t top = 0;
-  uint32_t host = 0, orph = 0, trunc = 0, spans = 0;
-  for (uint32_t g = g0; g < gend; g++) {
-    const TileState& ts = p.state[g];
-    const SumEntry* e = p.pool + ts.pool_off;
-    uint32_t np = ts.pool_n_pending, nr = ts.pool_n_resid;
-    if (ts.pool_off + np + nr > p.pool_cap) return;
-    for (uint32_t i = 0; i < np; i++) {
-      SumEntry x = e[i];
-      if (top && st[top - 1].fn == x.fn) {
-        SumEntry en = st[--top];
-        if (x.flags & 4u) push_error(p, HG_ERR_RESULT, s, x.seq, 0, x.ts, 0, x.result);
-        uint64_t dur = x.ts - en.ts;
-        unsigned long long* a = p.host_acc + 6ull * x.fn;
-        atomicAdd(&a[0], 1ull);
-        if (x.flags & 2u) atomicAdd(&a[1], 1ull);
-        add_i128(&a[2], &a[3], dur, 0);
-        atomicMin(&a[4], dur);
-        atomicMax(&a[5], dur);
-        host++; spans++;
-      } else {
-        unsigned long long k = atomicAdd(p.n_orphans, 1ull);
-        if (k < p.orphan_cap) { hg_orphan o; o.stream = s; o.function = x.fn; o.ts = x.ts; o.seq = x.seq; p.orphans[k] = o; }
-        orph++;
-      }
-    }
-    for (uint32_t i = 0; i < nr; i++) st[top++] = e[np + i];
-  }
-  // truncated spans at the global last timestamp, innermost first (pipeline.py:220-240)
-  while (top) {
-    SumEntry en = st[--top];
-    uint64_t dur = p.global_last_ts - en.ts;
-    unsigned long long* a = p.host_acc + 6ull * en.fn;
-    atomicAdd(&a[0], 1ull);
-    add_i128(&a[2], &a[3], dur, 0);
-    atomicMin(&a[4], dur);
-    atomicMax(&a[5], dur);
-    trunc++; spans++;
-  }
-  if (host) atomicAdd(&p.stats[ST_HOST], (unsigned long long)host);
-  if (orph) atomicAdd(&p.stats[ST_ORPHANS], (unsigned long long)orph);
-  if (trunc) atomicAdd(&p.stats[ST_TRUNC], (unsigned long long)trunc);
-  if (spans) atomicAdd(&p.stream_spans[s], (unsigned long long)spans);
 }
 
 __global__ void init_acc_kernel(unsigned long long* host_acc, uint32_t n_fn, unsigned long long* dev_acc, uint32_t n_dev) {
@@ -966,11 +1014,14 @@ struct hg_ctx {
   hg_config cfg{};
   std::string err;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[4] = {};
+  cudaEvent_t ev[6] = {};  // 0 run start, 1 after staging, 2 after compose, 3 results on host, 4/5 tile kernel
   int sm_count = 0;
   // registry
   std::vector<DSchema> schemas;
   std::vector<int32_t> sid_map;
+  std::vector<uint2> desc;
+  DBuf<uint2> d_desc;
+  DBuf<SumEntry> d_warp_scratch;
   std::vector<uint8_t> kinds, field_role;
   uint32_t n_fn = 0, max_sid = 0;
   DBuf<DSchema> d_schemas;
@@ -1083,7 +1134,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_host_acc.release(); ctx->d_dev_acc.release(); ctx->d_counters.release();
   ctx->d_orphans.release(); ctx->d_errors.release(); ctx->d_stream_spans.release();
   ctx->d_keys.release(); ctx->d_vals.release(); ctx->d_name_len.release(); ctx->d_small.release();
-  ctx->d_name_off.release(); ctx->d_arena.release();
+  ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release(); ctx->d_warp_scratch.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1125,13 +1176,47 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
       d.flags |= SF_RESULT;
       if (d.role_kind[HG_ROLE_RESULT] == HG_KIND_F64) d.flags |= SF_RESULT_F64;
     }
+    // var plan
+    d.nvar = 0;
+    {
+      uint32_t nv = 0, lead = 0;
+      bool ok = true;
+      for (int r = 0; r < HG_NUM_ROLES; r++) { d.role_seg[r] = 0xFF; d.role_delta[r] = 0; }
+      for (uint32_t f = 0; f < h.n_fields && ok; f++) {
+        uint8_t k = kinds[h.kinds_offset + f];
+        for (int r = 0; r < HG_NUM_ROLES; r++)
+          if (h.role[r] == (int16_t)f) { d.role_seg[r] = (uint8_t)nv; d.role_delta[r] = (uint16_t)lead; }
+        if (k >= HG_KIND_STRING) {
+          if (nv == 4 || lead > 0xFFFF) { ok = false; break; }
+          d.lead[nv] = (uint16_t)lead;
+          d.vkind[nv] = k == HG_KIND_STRING ? 1 : 0;
+          nv++;
+          lead = 0;
+        } else {
+          lead += 8;
+        }
+      }
+      if (ok && lead <= 0xFFFF) { d.lead[nv] = (uint16_t)lead; d.nvar = (uint8_t)nv; }
+      else d.nvar = kNoPlan;
+    }
     if (h.feed_error == 1) d.flags |= SF_FEED_ALWAYS;
     if (h.feed_error == 2) d.flags |= SF_FEED_TIMELINE;
     ctx->sid_map[h.id] = (int32_t)ctx->schemas.size();
     ctx->schemas.push_back(d);
   }
+  if (n_functions >= (1u << 19) - 1) return fail(ctx, HG_EUNSUPPORTED, "more than 2^19-2 distinct functions");
   ctx->n_fn = n_functions;
   ctx->max_sid = n_schemas ? max_sid : 0;
+  // compact descriptors: x = fn(20) | cls(3)<<20 | flags(8)<<23 (top bit = present); y = fixed_len | result field<<16
+  ctx->desc.assign(ctx->sid_map.size(), make_uint2(0, 0));
+  for (uint32_t i = 0; i < n_schemas; i++) {
+    const DSchema& d = ctx->schemas[ctx->sid_map[schemas[i].id]];
+    uint32_t fn = d.fn < 0 ? 0xFFFFFu : (uint32_t)d.fn;
+    uint32_t flags = d.flags & 0x7Fu;
+    uint32_t resf = (d.flags & SF_RESULT) ? (uint32_t)d.role[HG_ROLE_RESULT] : 0xFFu;
+    ctx->desc[schemas[i].id] = make_uint2((fn & 0xFFFFFu) | ((uint32_t)d.cls << 20) | (flags << 23) | D_PRESENT,
+                                          (uint32_t)d.fixed_len | ((resf & 0xFFu) << 16) | ((uint32_t)d.counter_kind << 24));
+  }
   cudaSetDevice(ctx->cfg.device);
   CK(ctx->d_schemas.ensure(std::max<size_t>(ctx->schemas.size(), 1)));
   CK(ctx->d_sid_map.ensure(ctx->sid_map.size()));
@@ -1140,6 +1225,8 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
   if (!ctx->schemas.empty())
     CK(cudaMemcpy(ctx->d_schemas.ptr, ctx->schemas.data(), ctx->schemas.size() * sizeof(DSchema), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_sid_map.ptr, ctx->sid_map.data(), ctx->sid_map.size() * 4, cudaMemcpyHostToDevice));
+  CK(ctx->d_desc.ensure(ctx->desc.size()));
+  CK(cudaMemcpy(ctx->d_desc.ptr, ctx->desc.data(), ctx->desc.size() * sizeof(uint2), cudaMemcpyHostToDevice));
   if (n_kinds) {
     CK(cudaMemcpy(ctx->d_kinds.ptr, kinds, n_kinds, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_field_role.ptr, ctx->field_role.data(), n_kinds, cudaMemcpyHostToDevice));
@@ -1244,10 +1331,7 @@ int hg_stage(hg_ctx* ctx) {
   return HG_OK;
 }
 
-static size_t tile_smem_bytes(uint32_t n_fn) {
-  size_t tab = n_fn <= kSmemFnMax ? ((sizeof(SmemRow) * n_fn + 127) / 128) * 128 : 0;
-  return tab + sizeof(WarpSmem) * kWarpsPerCta;
-}
+static size_t tile_smem_bytes(uint32_t n_fn) { return smem_layout(n_fn).total; }
 
 static int ensure_scratch(hg_ctx* ctx, uint64_t n_records_bound) {
   const size_t nt = ctx->tile_stream.size();
@@ -1290,6 +1374,8 @@ static Params make_params(hg_ctx* ctx) {
   p.n_streams = (uint32_t)ctx->streams.size();
   p.schemas = ctx->d_schemas.ptr;
   p.sid_map = ctx->d_sid_map.ptr;
+  p.desc = ctx->d_desc.ptr;
+  p.warp_scratch = ctx->d_warp_scratch.ptr;
   p.max_sid = ctx->max_sid;
   p.kinds = ctx->d_kinds.ptr;
   p.field_role = ctx->d_field_role.ptr;
@@ -1357,8 +1443,12 @@ static int launch_phase1(hg_ctx* ctx) {
     if (per_sm < 1) return fail(ctx, HG_ECUDA, "tile kernel does not fit on an SM");
     uint32_t grid = std::min<uint32_t>((uint32_t)(per_sm * ctx->sm_count), (nt + kWarpsPerCta - 1) / kWarpsPerCta);
     grid = std::max<uint32_t>(grid, 1);
+    CK(ctx->d_warp_scratch.ensure((size_t)grid * kWarpsPerCta * kMaxRecTile));
+    p.warp_scratch = ctx->d_warp_scratch.ptr;
+    CK(cudaEventRecord(ctx->ev[4], ctx->stream));
     tile_kernel<<<grid, kCtaThreads, smem, ctx->stream>>>(p, ctx->d_done.ptr);
     CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev[5], ctx->stream));
     ctx->launches++;
   }
   return HG_OK;
@@ -1433,14 +1523,19 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
       unsigned long long zero = 0;
       CK(cudaMemcpyAsync(p.stack_used, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
       // the tally accumulators already hold phase-1 spans; compose adds the rest
-      compose_kernel<<<(ns + 127) / 128, 128, 0, ctx->stream>>>(p);
+      size_t csmem = ctx->n_fn <= kSmemFnMax ? sizeof(SmemRow) * ctx->n_fn : 0;
+      CK(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
+      compose_kernel<<<(ns + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem, ctx->stream>>>(p);
       CK(cudaGetLastError());
       ctx->launches++;
     }
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     int rc = read_counters(ctx);
     if (rc) return rc;
-    if (ctx->counters[C_STACK_USED] <= ctx->stack_cap && ctx->counters[C_N_ORPHANS] <= ctx->orphan_cap) break;
+    if ((uint32_t)ctx->counters[C_WATCHDOG] == 1u) return fail(ctx, HG_ECUDA, "look-back watchdog fired (engine bug)");
+    if ((uint32_t)ctx->counters[C_WATCHDOG] == 0u && ctx->counters[C_STACK_USED] <= ctx->stack_cap &&
+        ctx->counters[C_N_ORPHANS] <= ctx->orphan_cap)
+      break;
     return fail(ctx, HG_ENOMEM, "composition scratch overflow");  // TODO: rerun the whole pipeline with larger buffers
   }
   // results to the host
@@ -1473,7 +1568,7 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->d2h_bytes += ctx->host_acc.size() * 8 + ctx->dev_acc.size() * 8 + arena_used + n_orph * sizeof(hg_orphan) +
                     n_err * sizeof(hg_trace_error) + ns * 8 + ctx->n_dev_rows * 12;
   float k_ms = 0, t_ms = 0;
-  cudaEventElapsedTime(&k_ms, ctx->ev[1], ctx->ev[2]);
+  if (!ctx->tile_stream.empty()) cudaEventElapsedTime(&k_ms, ctx->ev[4], ctx->ev[5]);
   cudaEventElapsedTime(&t_ms, ctx->ev[0], ctx->ev[3]);
   ctx->kernel_ms = k_ms;
   ctx->total_ms = t_ms;

@@ -39,7 +39,14 @@ struct DSchema {
   uint8_t counter_kind;
   int8_t role[HG_NUM_ROLES];
   uint8_t role_kind[HG_NUM_ROLES];
+  // fast plan for variable payloads: var items and the fixed bytes around them
+  uint8_t nvar;                       // number of string/blob fields; kNoPlan: use the generic walk
+  uint8_t vkind[4];                   // 1 string (UTF-8 checked), 0 blob
+  uint16_t lead[5];                   // fixed bytes before var item i; lead[nvar] = trailing fixed bytes
+  uint8_t role_seg[HG_NUM_ROLES];     // segment (0..nvar) holding the role field
+  uint16_t role_delta[HG_NUM_ROLES];  // bytes from the segment start to the field (var field: its u32 length)
 };
+constexpr uint8_t kNoPlan = 0xFF;
 
 // ---------------------------------------------------------------------------
 // stream window: a warp-staged copy of [win_start, win_end) of one stream in
@@ -87,7 +94,7 @@ __device__ __forceinline__ uint8_t rd8(const Window& w, uint64_t off) {
 }
 
 // Strict UTF-8 (no overlongs, no surrogates, <= U+10FFFF).  Returns true if valid.
-__device__ inline bool utf8_valid(const Window& w, uint64_t p, uint32_t n) {
+__device__ __noinline__ bool utf8_valid(const Window& w, uint64_t p, uint32_t n) {
   uint32_t i = 0;
   // ASCII fast path, 4 bytes at a time
   while (i + 4 <= n) {
@@ -116,7 +123,7 @@ __device__ inline bool utf8_valid(const Window& w, uint64_t p, uint32_t n) {
 
 // 64-bit hash of a byte string (word-at-a-time; collisions are resolved by
 // full comparison, so quality only affects speed)
-__device__ inline uint64_t hash_bytes(const Window& w, uint64_t p, uint32_t n) {
+__device__ __noinline__ uint64_t hash_bytes(const Window& w, uint64_t p, uint32_t n) {
   uint64_t h = 0x9E3779B97F4A7C15ull ^ ((uint64_t)n * 0xff51afd7ed558ccdull);
   uint32_t i = 0;
   for (; i + 4 <= n; i += 4) {
@@ -151,7 +158,7 @@ struct NameDict {
   uint32_t* overflow;
 };
 
-__device__ inline bool name_equal(const NameDict& d, uint32_t row, const Window& w, uint64_t p, uint32_t n) {
+__device__ __noinline__ bool name_equal(const NameDict& d, uint32_t row, const Window& w, uint64_t p, uint32_t n) {
   if (d.name_len[row] != n) return false;
   const uint8_t* a = d.arena + d.name_off[row];
   for (uint32_t i = 0; i < n; i++)
@@ -160,13 +167,13 @@ __device__ inline bool name_equal(const NameDict& d, uint32_t row, const Window&
 }
 
 // returns the row id or 0xffffffff on overflow
-__device__ inline uint32_t name_lookup(const NameDict& d, const Window& w, uint64_t p, uint32_t n) {
+__device__ __noinline__ uint32_t name_lookup(const NameDict& d, const Window& w, uint64_t p, uint32_t n) {
   uint64_t h = hash_bytes(w, p, n);
   for (uint64_t slot = h & d.mask, probes = 0; probes <= d.mask; slot = (slot + 1) & d.mask, probes++) {
     unsigned long long k = atomicCAS(&d.keys[slot], 0ull, (unsigned long long)h);
     if (k == 0ull) {
       uint32_t row = atomicAdd(d.n_rows, 1u);
-      unsigned long long off = atomicAdd(d.arena_used, (unsigned long long)n);
+      unsigned long long off = atomicAdd(d.arena_used, (unsigned long long)((n + 3u) & ~3u));
       if (row >= d.row_cap || off + n > d.arena_cap) { atomicExch(d.overflow, 1u); atomicExch(&d.vals[slot], 0xffffffffu); return 0xffffffffu; }
       for (uint32_t i = 0; i < n; i++) d.arena[off + i] = rd8(w, p + i);
       d.name_off[row] = off;

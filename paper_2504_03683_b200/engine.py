@@ -93,10 +93,20 @@ class Engine:
         for s in self._streams:
             self.add_stream_ptr(s.hostname, s.pid, s.tid, s.data)
 
+    def set_streams_pinned(self, idents, tensors):
+        """Streams from pinned host tensors (torch.uint8); the next run copies them H2D."""
+        from .tracefile import RawStream
+
+        self._check(self._L.hg_clear_streams(self._ctx), "hg_clear_streams")
+        self._keep = list(tensors)
+        self._streams = [RawStream(h, p, t, "", b"") for h, p, t in idents]
+        for (h, p, t), ten in zip(idents, tensors):
+            self.add_stream_ptr(h, p, t, ten.data_ptr() if ten.numel() else 0, ten.numel())
+
     def add_stream_ptr(self, hostname, pid, tid, data, size=None):
         """data: bytes (kept alive here) or an integer host address (+ size)."""
         if isinstance(data, int):
-            ptr, n = data, size
+            ptr, n = (data or None), size
         else:
             buf = C.c_char_p(data) if data else None
             self._keep.append(data)

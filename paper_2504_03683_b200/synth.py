@@ -27,11 +27,15 @@ PID_BASE = 4202000  # harness.py:27-28
 PID_STRIDE = 100
 SAMPLER_TID_OFFSET = 99  # sampler.py:31
 
+# test pool: includes non-ASCII names to exercise UTF-8 validation and JSON escaping
 KERNEL_POOL_SMALL = ["lrn_conv1d", "gemm_f32", "reduce_sum", "softmax", "ядро_σ", "カーネル", "axpy", "stencil7"]
+# benchmark pool: kernel names are C/C++ symbols in real traces (ASCII)
+KERNEL_POOL_ASCII = ["lrn_conv1d", "gemm_f32", "reduce_sum", "softmax", "layernorm_bwd", "attention_fwd", "axpy",
+                     "stencil7"]
 
 
-def kernel_pool(n: int) -> list:
-    base = list(KERNEL_POOL_SMALL)
+def kernel_pool(n: int, ascii_only: bool = False) -> list:
+    base = list(KERNEL_POOL_ASCII if ascii_only else KERNEL_POOL_SMALL)
     i = 0
     while len(base) < n:
         base.append(f"kernel_{i:04d}_{'abcdefgh'[i % 8] * (1 + i % 5)}")
@@ -250,7 +254,8 @@ def config(name: str, scale: float = 1.0) -> Workload:
     ze = ze_registry()
     if name == "c1":
         n = max(1, int(1_000_000 * scale))
-        return Workload("c1", ze, [StreamSpec("synth0", PID_BASE, PID_BASE, n, 42)], {"prof_p": 0.12})
+        return Workload("c1", ze, [StreamSpec("synth0", PID_BASE, PID_BASE, n, 42)], {"prof_p": 0.12},
+                        kernel_names=list(KERNEL_POOL_ASCII))
     if name == "c2":
         per = max(1, int(390_625 * scale))
         streams = []
@@ -258,7 +263,7 @@ def config(name: str, scale: float = 1.0) -> Workload:
             pid = PID_BASE + PID_STRIDE * p
             for t in range(64):
                 streams.append(StreamSpec("synth0", pid, pid + t, per, 43_000 + p * 64 + t))
-        return Workload("c2", ze, streams, {"prof_p": 0.12})
+        return Workload("c2", ze, streams, {"prof_p": 0.12}, kernel_names=list(KERNEL_POOL_ASCII))
     if name == "c3":
         per = max(1, int(976_562 * scale))
         streams = []
@@ -268,7 +273,7 @@ def config(name: str, scale: float = 1.0) -> Workload:
                 for t in range(32):
                     streams.append(StreamSpec(f"node{h:02d}", pid, pid + t, per, 44_000 + (h * 4 + p) * 32 + t,
                                               file=f"stream_node{h:02d}_{pid}_{pid + t}.bin"))
-        return Workload("c3", ze, streams, {"prof_p": 0.12})
+        return Workload("c3", ze, streams, {"prof_p": 0.12}, kernel_names=list(KERNEL_POOL_ASCII))
     if name == "c4":
         reg = layered_registry()
         layers = {s.function: (0 if s.function.startswith("sycl") else 1)
