@@ -48,7 +48,7 @@ __host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~(s
 __host__ __device__ inline size_t lane_tab_bytes(uint32_t n_fn) { return ((size_t)3 * n_fn * kWarp + 3 * n_fn) * 4; }
 
 struct SmemLayout {
-  size_t tab, lanetab, dcache, ncache, warps, total;
+  size_t tab, lanetab, dcache, ncache, sdesc, warps, total;
 };
 __host__ __device__ inline SmemLayout smem_layout(uint32_t n_fn) {
   SmemLayout L{};
@@ -62,10 +62,38 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t n_fn) {
   off += align128(sizeof(DevRow) * kDevSlots);
   L.ncache = off;
   off += align128(sizeof(NameSlot) * kNameSlots);
+  L.sdesc = off;
+  off += align128(sizeof(uint32_t) * kSdescMax);
   L.warps = off;
   off += sizeof(WarpSmem) * kWarpsPerCta;
   L.total = off;
   return L;
+}
+
+constexpr uint32_t SD_PRESENT = 0x80000000u, SD_VAR = 0x40000000u;
+
+// schema screening entry: present | var | fixed payload length (var: minimum)
+__device__ __forceinline__ uint32_t sdesc_lookup(const Params& p, const uint32_t* sdesc, uint32_t sid) {
+  if (sdesc) return sdesc[sid];
+  const uint2 d = __ldg(&p.desc[sid]);
+  return d_present(d) ? (SD_PRESENT | ((d_flags(d) & SF_VAR) ? SD_VAR : 0u) | d_fixed(d)) : 0u;
+}
+
+// the record after a screened candidate must be a plausible header too, not earlier in time
+__device__ __forceinline__ bool second_header_ok(const Params& p, const uint32_t* win, uint64_t t0, uint64_t size,
+                                                 uint32_t win_len, const uint32_t* sdesc, uint32_t o) {
+  const uint32_t plen = s32(win, o + 12);
+  if (t0 + o + 16 + plen > size) return false;
+  const uint32_t n = o + 16 + plen;
+  if (t0 + n == size) return true;
+  if (n + 16 > win_len) return false;
+  const uint32_t sid2 = s32(win, n);
+  const uint32_t plen2 = s32(win, n + 12);
+  const uint32_t e = sid2 <= p.max_sid ? sdesc_lookup(p, sdesc, sid2) : 0u;
+  if (!(e & SD_PRESENT)) return false;
+  if ((e & SD_VAR) ? plen2 < (e & 0xFFFFu) : plen2 != (e & 0xFFFFu)) return false;
+  if (t0 + n + 16 + plen2 > size) return false;
+  return s64(win, n + 4) >= s64(win, o + 4);
 }
 
 struct TileGeom {
@@ -106,68 +134,91 @@ struct Seg { uint32_t s[5]; };
 // rare_record result: x = feed error, y = bit0 device span, bit1 sample; z/w = feed aux (lo/hi)
 using RareOut = uint4;
 
-// device-profiling and telemetry records (pipeline.py:186-215): out of line to keep the hot loop small
-__device__ __noinline__ RareOut rare_record(const Params& p, const uint32_t* win, Window w, uint64_t t0,
-                                            uint32_t win_len, uint32_t o, uint32_t sid, uint32_t plen, bool planned,
-                                            Seg seg, DevRow* dcache, NameSlot* ncache) {
+// role field offset of a validated record (fixed: field index; planned var: segment + delta)
+__device__ __forceinline__ uint64_t role_at(const DSchema* sc, uint64_t a, uint32_t fl, bool planned, const Seg& seg,
+                                            int r) {
+  if (!(fl & SF_VAR)) return a + 16 + 8u * (uint32_t)sc->role[r];
+  return a + 16 + seg_sel(seg.s, sc->role_seg[r]) + sc->role_delta[r];
+}
+
+// device-profiling record (pipeline.py:186-202): duration into its name's row
+__device__ __noinline__ RareOut device_record(const Params& p, const uint32_t* win, Window w, uint64_t t0,
+                                              uint32_t win_len, uint32_t o, uint32_t sid, uint32_t plen, bool planned,
+                                              Seg seg, DevRow* dcache, NameSlot* ncache) {
   RareOut out = make_uint4(0, 0, 0, 0);
   const uint64_t a = t0 + o;
   const uint2 d = desc_of(p, sid);
-  const uint32_t cls = d_cls(d), fl = d_flags(d);
-  const DSchema* sc = schema_of(p, sid);
+  const uint32_t fl = d_flags(d);
   if (fl & SF_FEED_ALWAYS) { out.x = HG_ERR_FEED; out.z = sid; return out; }
-  uint64_t role_off[HG_NUM_ROLES];
+  const DSchema* sc = schema_of(p, sid);
+  uint64_t o_start, o_end, no;
   uint32_t name_len = 0;
-  if (!(fl & SF_VAR)) {
-    for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = sc->role[r] >= 0 ? a + 16 + 8u * (uint32_t)sc->role[r] : 0;
-  } else if (planned) {
-    for (int r = 0; r < HG_NUM_ROLES; r++) {
-      uint32_t sg = sc->role_seg[r];
-      role_off[r] = sg == 0xFF ? 0 : a + 16 + seg.s[sg] + sc->role_delta[r];
-    }
-    if (sc->role_seg[HG_ROLE_NAME] != 0xFF) { name_len = rd32(w, role_off[HG_ROLE_NAME]); role_off[HG_ROLE_NAME] += 4; }
-    if (sc->role_seg[HG_ROLE_CMDKIND] != 0xFF) role_off[HG_ROLE_CMDKIND] += 4;
-  } else {
+  if ((fl & SF_VAR) && !planned) {
+    uint64_t role_off[HG_NUM_ROLES];
     for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
     uint64_t aux;
     walk_fields(p, d, sid, a + 16, plen, [&](uint64_t x) { return rd32(w, x); }, w, role_off, name_len, aux);
+    o_start = role_off[HG_ROLE_START]; o_end = role_off[HG_ROLE_END]; no = role_off[HG_ROLE_NAME];
+  } else {
+    o_start = role_at(sc, a, fl, planned, seg, HG_ROLE_START);
+    o_end = role_at(sc, a, fl, planned, seg, HG_ROLE_END);
+    no = role_at(sc, a, fl, planned, seg, HG_ROLE_NAME);
+    name_len = rd32(w, no);
+    no += 4;
   }
-  if (cls == HG_CLASS_DEVICE) {
-    uint64_t ua = rd64(w, role_off[HG_ROLE_START]);
-    uint64_t ub = rd64(w, role_off[HG_ROLE_END]);
-    int64_t ah = (sc->role_kind[HG_ROLE_START] == HG_KIND_I64 && (int64_t)ua < 0) ? -1 : 0;
-    int64_t bh = (sc->role_kind[HG_ROLE_END] == HG_KIND_I64 && (int64_t)ub < 0) ? -1 : 0;
-    uint64_t d_lo = ub - ua;
-    int64_t d_hi = bh - ah - (ub < ua ? 1 : 0);
-    uint64_t no = role_off[HG_ROLE_NAME];
-    uint32_t row = 0xffffffffu;
-    const bool inwin = no + name_len + 8 <= t0 + win_len;
-    const uint32_t nw = (uint32_t)(no - t0);
-    uint64_t h = inwin ? hash_window(win, nw, name_len) : hash_bytes(w, no, name_len);
-    NameSlot* slot = &ncache[h % kNameSlots];
-    unsigned long long ch = *(volatile unsigned long long*)&slot->hash;
-    uint32_t cr = *(volatile uint32_t*)&slot->row;
-    if (ch == h && cr < *(volatile uint32_t*)p.names.n_rows &&
-        (inwin ? name_equal_window(p.names, cr, win, nw, name_len) : name_equal(p.names, cr, w, no, name_len)))
-      row = cr;
-    if (row == 0xffffffffu) {
-      row = name_lookup(p.names, w, no, name_len);
-      if (row != 0xffffffffu) { slot->row = row; __threadfence_block(); slot->hash = h; }
-    }
-    if (row != 0xffffffffu) fold_device(p, dcache, row, d_lo, d_hi);
-    out.y = 1;
-    return out;
+  const uint64_t ua = rd64(w, o_start), ub = rd64(w, o_end);
+  const int64_t ah = (sc->role_kind[HG_ROLE_START] == HG_KIND_I64 && (int64_t)ua < 0) ? -1 : 0;
+  const int64_t bh = (sc->role_kind[HG_ROLE_END] == HG_KIND_I64 && (int64_t)ub < 0) ? -1 : 0;
+  const uint64_t d_lo = ub - ua;
+  const int64_t d_hi = bh - ah - (ub < ua ? 1 : 0);
+  uint32_t row = 0xffffffffu;
+  const bool inwin = no + name_len + 8 <= t0 + win_len;
+  const uint32_t nw = (uint32_t)(no - t0);
+  const uint64_t h = inwin ? hash_window(win, nw, name_len) : hash_bytes(w, no, name_len);
+  NameSlot* slot = &ncache[h % kNameSlots];
+  const unsigned long long ch = *(volatile unsigned long long*)&slot->hash;
+  const uint32_t cr = *(volatile uint32_t*)&slot->row;
+  if (ch == h && cr < *(volatile uint32_t*)p.names.n_rows &&
+      (inwin ? name_equal_window(p.names, cr, win, nw, name_len) : name_equal(p.names, cr, w, no, name_len)))
+    row = cr;
+  if (row == 0xffffffffu) {
+    row = name_lookup(p.names, w, no, name_len);
+    if (row != 0xffffffffu) { slot->row = row; __threadfence_block(); slot->hash = h; }
   }
-  // telemetry (sampler.py:36-48 range checks)
-  uint64_t bits = rd64(w, role_off[HG_ROLE_VALUE]);
-  uint8_t vk = sc->role_kind[HG_ROLE_VALUE];
-  bool util = sc->counter_kind >= HG_COUNTER_COMPUTE;
+  if (row != 0xffffffffu) fold_device(p, dcache, row, d_lo, d_hi);
+  out.y = 1;
+  return out;
+}
+
+// telemetry sample (pipeline.py:203-215; sampler.py:44-48 range checks)
+__device__ __noinline__ RareOut telemetry_record(const Params& p, Window w, uint64_t t0, uint32_t o, uint32_t sid,
+                                                 uint32_t plen, bool planned, Seg seg) {
+  RareOut out = make_uint4(0, 0, 0, 0);
+  const uint64_t a = t0 + o;
+  const uint2 d = desc_of(p, sid);
+  const uint32_t fl = d_flags(d);
+  if (fl & SF_FEED_ALWAYS) { out.x = HG_ERR_FEED; out.z = sid; return out; }
+  const DSchema* sc = schema_of(p, sid);
+  uint64_t va;
+  if ((fl & SF_VAR) && !planned) {
+    uint64_t role_off[HG_NUM_ROLES];
+    for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
+    uint64_t aux;
+    uint32_t nl = 0;
+    walk_fields(p, d, sid, a + 16, plen, [&](uint64_t x) { return rd32(w, x); }, w, role_off, nl, aux);
+    va = role_off[HG_ROLE_VALUE];
+  } else {
+    va = role_at(sc, a, fl, planned, seg, HG_ROLE_VALUE);
+  }
+  const uint64_t bits = rd64(w, va);
+  const uint8_t vk = sc->role_kind[HG_ROLE_VALUE];
+  const bool util = sc->counter_kind >= HG_COUNTER_COMPUTE;
   bool bad;
   if (vk == HG_KIND_F64) {
-    double v = __longlong_as_double((long long)bits);
+    const double v = __longlong_as_double((long long)bits);
     bad = util ? !(v >= 0.0 && v <= 1.0) : (v < 0.0);
   } else if (vk == HG_KIND_I64) {
-    int64_t v = (int64_t)bits;
+    const int64_t v = (int64_t)bits;
     bad = util ? !(v >= 0 && v <= 1) : (v < 0);
   } else {
     bad = util ? (bits > 1) : false;
@@ -189,6 +240,8 @@ __device__ __noinline__ uint32_t generic_payload(const Params& p, const Window& 
   result_off = role_off[HG_ROLE_RESULT];
   return e;
 }
+
+__device__ __noinline__ uint64_t rd64_far(Window w, uint64_t off) { return rd64(w, off); }
 
 // result field of a variable-payload exit whose result follows a string/blob (rare:
 // registries put `result` first); validates the payload on the way
@@ -245,7 +298,7 @@ __device__ __forceinline__ bool decode_one_rec(const Params& p, const uint32_t* 
           if (e) { dec_err = e; return false; }
         }
       }
-      const uint64_t bits = (result_off + 12 <= t0 + win_len) ? s64(win, (uint32_t)(result_off - t0)) : rd64(w, result_off);
+      const uint64_t bits = (result_off + 12 <= t0 + win_len) ? s64(win, (uint32_t)(result_off - t0)) : rd64_far(w, result_off);
       R.res = bits;
       if (fl & SF_RESULT_F64) {
         const double xv = __longlong_as_double((long long)bits);
@@ -294,7 +347,8 @@ __device__ __noinline__ uint4 drain_queue(const Params& p, WarpSmem* ws, Window 
     if (err) {
       push_error(p, err, s, base + rec, a, s64(win, o + 4), 0, aux);
     } else if (cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY) {
-      RareOut ro = rare_record(p, win, w, t0, win_len, o, sid, plen, planned, seg, dcache, ncache);
+      RareOut ro = cls == HG_CLASS_DEVICE ? device_record(p, win, w, t0, win_len, o, sid, plen, planned, seg, dcache, ncache)
+                                          : telemetry_record(p, w, t0, o, sid, plen, planned, seg);
       if (ro.x) push_error(p, ro.x, s, base + rec, a, s64(win, o + 4), 0, (uint64_t)ro.z | ((uint64_t)ro.w << 32));
       dev = ro.y & 1u;
       samples = (ro.y >> 1) & 1u;
@@ -328,6 +382,7 @@ __device__ __noinline__ void to_exact(WarpSmem* ws, SumEntry* scratch, uint64_t 
 // per-tile phases (out of line: executed once per tile, kept out of the hot loop)
 
 struct TileCtx {
+  const uint32_t* sdesc;   // shared screening table (nullptr: too many schema ids)
   SmemRow* tab;
   DevRow* dcache;
   NameSlot* ncache;
@@ -344,7 +399,7 @@ struct Found {      // result of pass A + look-back
 
 // pass A + look-back + record list (tracefile.py:198-210 boundaries)
 __device__ __noinline__ Found find_records(const Params& p, DoneState* done, WarpSmem* ws, const TileGeom G,
-                                           const Window w) {
+                                           const Window w, const uint32_t* sdesc) {
   const uint32_t lane = lane_id();
   const uint32_t* win = ws->win;
   const uint64_t t0 = G.t0, size = G.size;
@@ -361,34 +416,37 @@ __device__ __noinline__ Found find_records(const Params& p, DoneState* done, War
   uint32_t hyp = kNone32, exit = kNone32, cnt = 0, fail_off = 0;
   bool fail = false;
   {
-    uint32_t wo = sub0 & ~3u;
+    // bounded lockstep search (kSyncSpan bytes).  Each iteration every searching lane
+    // either screens the next 4 offsets against the shared schema table (known id,
+    // payload length consistent with it) or checks ONE survivor's following header,
+    // so the warp never serialises per-lane loops.  Lanes that find nothing are
+    // chained from their predecessor by warp_verify.
+    uint32_t wo = sub0 & ~3u, wcur = 0, cm = 0;
+    const uint32_t stop = min(sub1, sub0 + (uint32_t)kSyncSpan);
     bool searching = sub0 < sub1;
     while (__any_sync(0xffffffffu, searching)) {
-      if (searching) {
+      if (searching && cm == 0) {
         const uint32_t wi = wo >> 2;
         const uint32_t a0 = win[wi], a1 = win[wi + 1], c0 = win[wi + 3], c1 = win[wi + 4];
-        uint32_t cm = 0;
-        #pragma unroll
+        #pragma unroll 1
         for (uint32_t b = 0; b < 4; b++) {
-          const uint32_t o = wo + b;
           const uint32_t sid = __funnelshift_r(a0, a1, 8 * b);
           const uint32_t plen = __funnelshift_r(c0, c1, 8 * b);
-          uint2 d = make_uint2(0, 0);
-          if (sid <= p.max_sid) d = __ldg(&p.desc[sid]);
-          const bool fixed_ok = !(d_flags(d) & SF_VAR) && plen == d_fixed(d);
-          const bool var_ok = (d_flags(d) & SF_VAR) && plen >= d_fixed(d);
-          const bool ok = d_present(d) && (fixed_ok || var_ok) && o >= sub0 && o < sub1 &&
-                          t0 + o + 16 + plen <= size;
+          const uint32_t e = sid <= p.max_sid ? sdesc_lookup(p, sdesc, sid) : 0u;
+          const bool ok = (e & SD_PRESENT) && ((e & SD_VAR) ? plen >= (e & 0xFFFFu) : plen == (e & 0xFFFFu));
           cm |= (ok ? 1u : 0u) << b;
         }
-        while (cm) {
-          const uint32_t b = __ffs(cm) - 1;
-          cm &= cm - 1;
-          if (sync_ok(p, win, t0, size, win_len, wo + b)) { hyp = wo + b; cm = 0; searching = false; }
-        }
+        if (wo < sub0) cm &= ~((1u << (sub0 - wo)) - 1u);
+        if (stop - wo < 4) cm &= (1u << (stop - wo)) - 1u;
+        wcur = wo;
         wo += 4;
-        if (wo >= sub1) searching = false;
       }
+      if (searching && cm) {
+        const uint32_t o = wcur + __ffs(cm) - 1;
+        cm &= cm - 1;
+        if (second_header_ok(p, win, t0, size, win_len, sdesc, o)) { hyp = o; searching = false; }
+      }
+      if (searching && !cm && wo >= stop) searching = false;
     }
   }
   if (hyp != kNone32) lane_walk(p, ws, win, t0, size, hyp, sub1, cnt, exit, fail, fail_off);
@@ -543,6 +601,18 @@ __device__ __noinline__ TileCtx tile_prologue(const Params& p, const SmemLayout 
   C.tab = (!small && p.n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(smem + SL.tab) : nullptr;
   C.dcache = reinterpret_cast<DevRow*>(smem + SL.dcache);
   C.ncache = reinterpret_cast<NameSlot*>(smem + SL.ncache);
+  if (p.max_sid < (uint32_t)kSdescMax) {
+    uint32_t* t = reinterpret_cast<uint32_t*>(smem + SL.sdesc);
+    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) {
+      const uint2 d = __ldg(&p.desc[i]);
+      uint32_t e = 0;
+      if (d_present(d)) e = SD_PRESENT | ((d_flags(d) & SF_VAR) ? SD_VAR : 0u) | d_fixed(d);
+      t[i] = e;
+    }
+    C.sdesc = t;
+  } else {
+    C.sdesc = nullptr;
+  }
   C.ws = reinterpret_cast<WarpSmem*>(smem + SL.warps) + warp;
   C.hf.small = small;
   C.hf.tab = C.tab;
@@ -560,7 +630,7 @@ __device__ __noinline__ TileCtx tile_prologue(const Params& p, const SmemLayout 
       C.tab[i] = z;
     }
   for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
-    DevRow z; z.tag = 0; z.count = 0; z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = ~0ull; z.mx = 0;
+    DevRow z; z.tag = 0; z.count = 0; z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
     C.dcache[i] = z;
   }
   for (uint32_t i = threadIdx.x; i < kNameSlots; i += blockDim.x) { C.ncache[i].hash = 0; C.ncache[i].row = 0; }
@@ -632,8 +702,9 @@ __device__ __noinline__ void tile_epilogue(const Params& p, const TileCtx C, con
     unsigned long long* a = p.dev_acc + 6ull * (r.tag - 1);
     atomicAdd(&a[0], (unsigned long long)r.count);
     add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), (int64_t)(int32_t)r.s2);
-    atomicMin(&a[4], r.mn);
-    atomicMax(&a[5], r.mx);
+    // biased 32-bit -> biased 64-bit
+    atomicMin(&a[4], bias64((int64_t)(int32_t)(r.mn ^ 0x80000000u)));
+    atomicMax(&a[5], bias64((int64_t)(int32_t)(r.mx ^ 0x80000000u)));
   }
 }
 
@@ -665,7 +736,7 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
     parity ^= 1u;
     Window w;  // generic accessor for fields that leave the window
     w.s = win; w.win_start = G.t0; w.win_end = G.t0 + G.nbytes; w.g = G.gbase; w.size = G.size;
-    const Found F = find_records(p, done, ws, G, w);
+    const Found F = find_records(p, done, ws, G, w, C.sdesc);
     if (F.dead) continue;
     const Look& L = F.L;
     const uint32_t n_rec = F.n_rec;

@@ -42,6 +42,8 @@ constexpr int kNameSlots = 64;                 // CTA cache of device-name hashe
 constexpr int kLevels = 64;                    // depth levels tracked in shared memory (fast path)
 constexpr int kPendCap = 64;                   // pending exits kept in shared memory (fast path)
 constexpr int kQCap = 64;                      // deferred-record queue per warp
+constexpr int kSyncSpan = 48;                  // bytes a lane scans for a speculative record start
+constexpr int kSdescMax = 512;                 // schema ids screened from shared memory
 
 // packed record meta used in residues and level slots
 //   fn (19 bits) | exit (bit 19) | error (bit 20) | bad f64 result (bit 21) | NaN (bit 22) | tile record index (bits 23..31)
@@ -73,8 +75,9 @@ struct SmemRow {   // CTA-shared host row (larger function sets); durations >= 2
 struct DevRow {    // CTA-shared device row cache entry
   uint32_t tag;    // row + 1, 0 = free
   uint32_t count;
-  uint32_t s0, s1, s2, pad;     // 96-bit two's complement sum
-  unsigned long long mn, mx;    // biased signed 64-bit
+  uint32_t s0, s1, s2;          // 96-bit two's complement sum
+  uint32_t mn, mx;              // biased signed 32-bit extrema (wider values go to global)
+  uint32_t pad;
 };
 
 struct NameSlot {
@@ -413,26 +416,28 @@ __device__ __noinline__ void fold_device_global(const Params& p, uint32_t row, u
   }
 }
 
-__device__ __forceinline__ void fold_device(const Params& p, DevRow* cache, uint32_t row, uint64_t d_lo, int64_t d_hi) {
+__device__ __noinline__ void fold_device(const Params& p, DevRow* cache, uint32_t row, uint64_t d_lo, int64_t d_hi) {
   DevRow* r = &cache[row % kDevSlots];
   uint32_t tag = *(volatile uint32_t*)&r->tag;
   if (tag == 0) { tag = atomicCAS(&r->tag, 0u, row + 1); if (tag == 0) tag = row + 1; }
-  if (tag != row + 1 || d_hi != ((int64_t)d_lo >> 63)) { fold_device_global(p, row, d_lo, d_hi); return; }
+  const bool fits32 = d_hi == ((int64_t)d_lo >> 63) && (int64_t)d_lo >= INT32_MIN && (int64_t)d_lo <= INT32_MAX;
+  if (tag != row + 1 || !fits32) { fold_device_global(p, row, d_lo, d_hi); return; }
   atomicAdd(&r->count, 1u);
-  // 96-bit two's complement accumulation of a sign-extended 64-bit value
-  uint32_t lo = (uint32_t)d_lo, mid = (uint32_t)(d_lo >> 32);
-  uint32_t ext = d_hi < 0 ? 0xFFFFFFFFu : 0u;
-  uint32_t o0 = atomicAdd(&r->s0, lo);
-  uint32_t c0 = (o0 + lo) < o0 ? 1u : 0u;
-  uint32_t add1 = mid + c0;
-  uint32_t c1 = add1 < mid ? 1u : 0u;
-  uint32_t o1 = atomicAdd(&r->s1, add1);
-  c1 += (o1 + add1) < o1 ? 1u : 0u;
-  uint32_t add2 = ext + c1;
-  if (add2) atomicAdd(&r->s2, add2);
-  unsigned long long b = bias64((int64_t)d_lo);
-  smem_min_u64(&r->mn, b);
-  smem_max_u64(&r->mx, b);
+  // 96-bit two's complement accumulation of a sign-extended 32-bit value
+  const uint32_t lo = (uint32_t)d_lo;
+  const uint32_t ext = (int32_t)lo < 0 ? 0xFFFFFFFFu : 0u;
+  const uint32_t o0 = atomicAdd(&r->s0, lo);
+  const uint32_t c0 = (o0 + lo) < o0 ? 1u : 0u;
+  const uint32_t add1 = ext + c0;  // 0, 1, 0xFFFFFFFF or 0 (wrapped)
+  if (add1) {
+    const uint32_t o1 = atomicAdd(&r->s1, add1);
+    const uint32_t c1 = (o1 + add1) < o1 ? 1u : 0u;
+    const uint32_t add2 = ext + c1;
+    if (add2) atomicAdd(&r->s2, add2);
+  }
+  const uint32_t b = lo ^ 0x80000000u;
+  if (b < *(volatile uint32_t*)&r->mn) atomicMin(&r->mn, b);
+  if (b > *(volatile uint32_t*)&r->mx) atomicMax(&r->mx, b);
 }
 
 // device-name row: CTA hash cache verified by full comparison with the row's stored bytes
@@ -605,14 +610,11 @@ __device__ __noinline__ uint32_t walk_fields(const Params& p, uint2 d, uint32_t 
 // ---------------------------------------------------------------------------
 // fast paths for records entirely inside the staged window
 
-// strict UTF-8 (tracefile.py:165 semantics) over window bytes: ASCII 4 bytes at a
-// time, multi-byte sequences checked in place
-__device__ __forceinline__ bool utf8_window(const uint32_t* win, const Window& w, uint32_t o, uint32_t n) {
-  (void)w;
+// strict UTF-8 (tracefile.py:165 semantics) over window bytes: multi-byte sequences
+__device__ __noinline__ bool utf8_window_slow(const uint32_t* win, uint32_t o, uint32_t n) {
   const uint8_t* b = reinterpret_cast<const uint8_t*>(win);
   uint32_t i = 0;
   while (i < n) {
-    if (i + 4 <= n && !(s32(win, o + i) & 0x80808080u)) { i += 4; continue; }
     uint32_t c = b[o + i];
     if (c < 0x80) { i++; continue; }
     uint32_t need, lo = 0x80, hi = 0xBF;
@@ -629,6 +631,17 @@ __device__ __forceinline__ bool utf8_window(const uint32_t* win, const Window& w
     }
     i += need + 1;
   }
+  return true;
+}
+
+// ASCII 4 bytes at a time; anything else through the strict validator
+__device__ __forceinline__ bool utf8_window(const uint32_t* win, const Window& w, uint32_t o, uint32_t n) {
+  (void)w;
+  uint32_t i = 0;
+  for (; i + 4 <= n; i += 4)
+    if (s32(win, o + i) & 0x80808080u) return utf8_window_slow(win, o, n);
+  if (i < n && (s32(win, o + i) & (0xffffffffu >> (8 * (4 - (n - i))))) & 0x80808080u)
+    return utf8_window_slow(win, o, n);
   return true;
 }
 
