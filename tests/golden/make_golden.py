@@ -471,6 +471,24 @@ def fx_errors():
         yield f"err_custom_{k}", custom_err(k)
 
 
+def tally_fixture():
+    """The reference's paper-style tally render (its test_sinks.py:382-408 fixture)."""
+    from hapitrace.sinks import TallyReport, TallyRow
+
+    rows = [("hipDeviceSynchronize", 4_730_000_000, 1), ("zeEventHostSynchronize", 4_680_000_000, 9),
+            ("hipMemcpy", 1_770_000_000, 3), ("__hipUnregisterFatBinary", 500_910_000, 1),
+            ("zeCommandListAppendMemoryCopy", 394_500_000, 5), ("hipLaunchKernel", 262_700_000, 2),
+            ("zeModuleCreate", 256_090_000, 1), ("other", 55_800_000, 4)]
+    rep = TallyReport(fingerprint=None, backends=("BACKEND_HIP", "BACKEND_ZE"),
+                      hostnames=frozenset({"aurora-node"}), processes=frozenset({("aurora-node", 1)}),
+                      threads=frozenset({("aurora-node", 1, 1)}))
+    for n, t, c in rows:
+        rep.rows[("host", n)] = TallyRow(n, "host", time_ns=t, count=c, min_ns=t // c, max_ns=t // c)
+    (EXPECTED / "tally_fixture.json").write_text(json.dumps(
+        {"rows": rows, "render": render_tally(rep),
+         "source": "reference sinks.render_tally on test_sinks.py:382-408 fixture"}, indent=1))
+
+
 def main(only=None):
     EXPECTED.mkdir(parents=True, exist_ok=True)
     TRACES.mkdir(parents=True, exist_ok=True)
@@ -489,6 +507,7 @@ def main(only=None):
             print(f"{name:24s} {status}")
     if not only:
         (EXPECTED / "index.json").write_text(json.dumps(sorted(index), indent=1))
+        tally_fixture()
 
 
 if __name__ == "__main__":
