@@ -96,6 +96,30 @@ __device__ __forceinline__ bool second_header_ok(const Params& p, const uint32_t
   return s64(win, n + 4) >= s64(win, o + 4);
 }
 
+__device__ __forceinline__ uint32_t warp_smem_off(uint32_t n_fn) {
+  return (uint32_t)(smem_layout(n_fn).warps + sizeof(WarpSmem) * (threadIdx.x >> 5));
+}
+__device__ __forceinline__ WarpSmem* warp_smem(uint32_t n_fn) {
+  return reinterpret_cast<WarpSmem*>(g_smem + warp_smem_off(n_fn));
+}
+__device__ __forceinline__ DevRow* sm_dcache(uint32_t n_fn) {
+  return reinterpret_cast<DevRow*>(g_smem + smem_layout(n_fn).dcache);
+}
+__device__ __forceinline__ NameSlot* sm_ncache(uint32_t n_fn) {
+  return reinterpret_cast<NameSlot*>(g_smem + smem_layout(n_fn).ncache);
+}
+__device__ __forceinline__ const uint32_t* sm_sdesc(const Params& p) {
+  return p.max_sid < (uint32_t)kSdescMax ? reinterpret_cast<const uint32_t*>(g_smem + smem_layout(p.n_fn).sdesc)
+                                         : nullptr;
+}
+__device__ __forceinline__ SmemRow* sm_tab(uint32_t n_fn) {
+  return (n_fn > kSmallF && n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(g_smem + smem_layout(n_fn).tab) : nullptr;
+}
+// per-lane host columns of this warp: [3][n_fn][32] then err/mn/mx [3][n_fn]
+__device__ __forceinline__ uint32_t* sm_lanetab(uint32_t n_fn) {
+  return reinterpret_cast<uint32_t*>(g_smem + smem_layout(n_fn).lanetab + lane_tab_bytes(n_fn) * (threadIdx.x >> 5));
+}
+
 struct TileGeom {
   uint32_t g, s, g0, j;
   uint64_t size, t0, t1;
@@ -142,10 +166,12 @@ __device__ __forceinline__ uint64_t role_at(const DSchema* sc, uint64_t a, uint3
 }
 
 // device-profiling record (pipeline.py:186-202): duration into its name's row
-__device__ __noinline__ RareOut device_record(const Params& p, const uint32_t* win, Window w, uint64_t t0,
-                                              uint32_t win_len, uint32_t o, uint32_t sid, uint32_t plen, bool planned,
-                                              Seg seg, DevRow* dcache, NameSlot* ncache) {
+__device__ __noinline__ RareOut device_record(const Params& p, Window w, uint64_t t0, uint32_t win_len, uint32_t o,
+                                              uint32_t sid, uint32_t plen, bool planned, Seg seg) {
   RareOut out = make_uint4(0, 0, 0, 0);
+  const uint32_t* win = warp_smem(p.n_fn)->win;
+  DevRow* dcache = sm_dcache(p.n_fn);
+  NameSlot* ncache = sm_ncache(p.n_fn);
   const uint64_t a = t0 + o;
   const uint2 d = desc_of(p, sid);
   const uint32_t fl = d_flags(d);
@@ -318,8 +344,9 @@ __device__ __forceinline__ bool decode_one_rec(const Params& p, const uint32_t* 
 
 // drain up to 32 deferred records, one per lane: payload validation (tracefile.py:152-169)
 // and device/telemetry handling (pipeline.py:186-215)
-__device__ __noinline__ uint4 drain_queue(const Params& p, WarpSmem* ws, Window w, uint64_t t0, uint32_t win_len,
-                                          uint32_t s, uint64_t base, uint32_t n, DevRow* dcache, NameSlot* ncache) {
+__device__ __noinline__ uint4 drain_queue(const Params& p, Window w, uint64_t t0, uint32_t win_len, uint32_t s,
+                                          uint64_t base, uint32_t n) {
+  WarpSmem* ws = warp_smem(p.n_fn);
   const uint32_t lane = lane_id();
   const uint32_t* win = ws->win;
   uint32_t dev = 0, samples = 0;
@@ -347,7 +374,7 @@ __device__ __noinline__ uint4 drain_queue(const Params& p, WarpSmem* ws, Window 
     if (err) {
       push_error(p, err, s, base + rec, a, s64(win, o + 4), 0, aux);
     } else if (cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY) {
-      RareOut ro = cls == HG_CLASS_DEVICE ? device_record(p, win, w, t0, win_len, o, sid, plen, planned, seg, dcache, ncache)
+      RareOut ro = cls == HG_CLASS_DEVICE ? device_record(p, w, t0, win_len, o, sid, plen, planned, seg)
                                           : telemetry_record(p, w, t0, o, sid, plen, planned, seg);
       if (ro.x) push_error(p, ro.x, s, base + rec, a, s64(win, o + 4), 0, (uint64_t)ro.z | ((uint64_t)ro.w << 32));
       dev = ro.y & 1u;
@@ -358,7 +385,8 @@ __device__ __noinline__ uint4 drain_queue(const Params& p, WarpSmem* ws, Window 
 }
 
 // materialise the fast-path tile state (pending exits + open levels) as an explicit stack
-__device__ __noinline__ void to_exact(WarpSmem* ws, SumEntry* scratch, uint64_t base, uint32_t n_pend, int32_t Dc) {
+__device__ __noinline__ void to_exact(uint32_t n_fn, SumEntry* scratch, uint64_t base, uint32_t n_pend, int32_t Dc) {
+  WarpSmem* ws = warp_smem(n_fn);
   const uint32_t lane = lane_id();
   for (uint32_t i = lane; i < n_pend; i += kWarp) {
     SumEntry e;
@@ -382,13 +410,7 @@ __device__ __noinline__ void to_exact(WarpSmem* ws, SumEntry* scratch, uint64_t 
 // per-tile phases (out of line: executed once per tile, kept out of the hot loop)
 
 struct TileCtx {
-  const uint32_t* sdesc;   // shared screening table (nullptr: too many schema ids)
-  SmemRow* tab;
-  DevRow* dcache;
-  NameSlot* ncache;
-  WarpSmem* ws;
   SumEntry* scratch;
-  HostFold hf;
 };
 
 struct Found {      // result of pass A + look-back
@@ -398,8 +420,9 @@ struct Found {      // result of pass A + look-back
 };
 
 // pass A + look-back + record list (tracefile.py:198-210 boundaries)
-__device__ __noinline__ Found find_records(const Params& p, DoneState* done, WarpSmem* ws, const TileGeom G,
-                                           const Window w, const uint32_t* sdesc) {
+__device__ __noinline__ Found find_records(const Params& p, DoneState* done, const TileGeom G, const Window w) {
+  WarpSmem* ws = warp_smem(p.n_fn);
+  const uint32_t* sdesc = sm_sdesc(p);
   const uint32_t lane = lane_id();
   const uint32_t* win = ws->win;
   const uint64_t t0 = G.t0, size = G.size;
@@ -452,11 +475,11 @@ __device__ __noinline__ Found find_records(const Params& p, DoneState* done, War
   if (hyp != kNone32) lane_walk(p, ws, win, t0, size, hyp, sub1, cnt, exit, fail, fail_off);
   uint32_t hmask = __ballot_sync(0xffffffffu, hyp != kNone32);
   uint32_t S = hmask ? __shfl_sync(0xffffffffu, hyp, __ffs(hmask) - 1) : kNone32;
-  if (S != kNone32) warp_verify(p, ws, win, t0, size, sub1, S, hyp, cnt, exit, fail, fail_off);
+  if (S != kNone32) warp_verify(p, warp_smem_off(p.n_fn), t0, size, sub1, S, hyp, cnt, exit, fail, fail_off);
   Look L;
   if (G.j == 0) {
     L.entry = 16; L.base = 0; L.prev_ts = 0; L.has_prev = false;
-    if (S != 0) warp_verify(p, ws, win, t0, size, sub1, 0, hyp, cnt, exit, fail, fail_off);
+    if (S != 0) warp_verify(p, warp_smem_off(p.n_fn), t0, size, sub1, 0, hyp, cnt, exit, fail, fail_off);
   } else {
     uint32_t n_spec = __reduce_add_sync(0xffffffffu, cnt);
     uint32_t x31 = __shfl_sync(0xffffffffu, exit, 31);
@@ -498,7 +521,7 @@ __device__ __noinline__ Found find_records(const Params& p, DoneState* done, War
     bool consistent = (S == kNone32) ? (erel >= tlen) : (erel == S);
     if (!consistent) {
       if (S == kNone32) { hyp = kNone32; cnt = 0; exit = kNone32; fail = false; }
-      warp_verify(p, ws, win, t0, size, sub1, erel, hyp, cnt, exit, fail, fail_off);
+      warp_verify(p, warp_smem_off(p.n_fn), t0, size, sub1, erel, hyp, cnt, exit, fail, fail_off);
     }
     if (erel >= tlen) { cnt = 0; fail = false; exit = erel; }
   }
@@ -553,9 +576,10 @@ __device__ __noinline__ Found find_records(const Params& p, DoneState* done, War
 }
 
 // tile summary for compose_kernel: pending exits, then open entries (innermost last)
-__device__ __noinline__ void write_summary(const Params& p, WarpSmem* ws, SumEntry* scratch, uint32_t g, uint32_t s,
+__device__ __noinline__ void write_summary(const Params& p, SumEntry* scratch, uint32_t g, uint32_t s,
                                            uint64_t base, bool slow, uint32_t n_pend, int32_t Dc, const GStack gs,
                                            uint32_t spans) {
+  WarpSmem* ws = warp_smem(p.n_fn);
   const uint32_t lane = lane_id();
   uint32_t sum_np, sum_n;
   if (!slow) { sum_np = n_pend; sum_n = n_pend + (uint32_t)Dc; }
@@ -589,57 +613,47 @@ __device__ __noinline__ void write_summary(const Params& p, WarpSmem* ws, SumEnt
   __syncwarp();
 }
 
-__device__ __noinline__ void fold_slow(const Params& p, const HostFold hf, int32_t fn, uint64_t dur, bool err) {
+// host span that does not fit the per-lane columns (duration >= 2^32 or a large function set)
+__device__ __noinline__ void fold_slow(const Params& p, int32_t fn, uint64_t dur, bool err) {
+  HostFold hf;
+  hf.small = false;
+  hf.tab = sm_tab(p.n_fn);
   hf.fold(p, fn, dur, err);
 }
 
-__device__ __noinline__ TileCtx tile_prologue(const Params& p, const SmemLayout SL, uint8_t* smem) {
-  TileCtx C;
+__device__ __noinline__ void tile_prologue(const Params& p) {
   const uint32_t lane = lane_id();
-  const uint32_t warp = threadIdx.x >> 5;
   const bool small = p.n_fn <= kSmallF;
-  C.tab = (!small && p.n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(smem + SL.tab) : nullptr;
-  C.dcache = reinterpret_cast<DevRow*>(smem + SL.dcache);
-  C.ncache = reinterpret_cast<NameSlot*>(smem + SL.ncache);
-  if (p.max_sid < (uint32_t)kSdescMax) {
-    uint32_t* t = reinterpret_cast<uint32_t*>(smem + SL.sdesc);
-    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) {
-      const uint2 d = __ldg(&p.desc[i]);
-      uint32_t e = 0;
-      if (d_present(d)) e = SD_PRESENT | ((d_flags(d) & SF_VAR) ? SD_VAR : 0u) | d_fixed(d);
-      t[i] = e;
-    }
-    C.sdesc = t;
-  } else {
-    C.sdesc = nullptr;
-  }
-  C.ws = reinterpret_cast<WarpSmem*>(smem + SL.warps) + warp;
-  C.hf.small = small;
-  C.hf.tab = C.tab;
   if (small) {
-    uint32_t* b = reinterpret_cast<uint32_t*>(smem + SL.lanetab + lane_tab_bytes(p.n_fn) * warp);
-    uint32_t n = p.n_fn * kWarp;
-    C.hf.lt.cnt = b; C.hf.lt.slo = b + n; C.hf.lt.shi = b + 2 * n;
-    C.hf.lt.err = b + 3 * n; C.hf.lt.mn = b + 3 * n + p.n_fn; C.hf.lt.mx = b + 3 * n + 2 * p.n_fn;
-    for (uint32_t i = lane; i < n; i += kWarp) { C.hf.lt.cnt[i] = 0; C.hf.lt.slo[i] = 0; C.hf.lt.shi[i] = 0; }
-    for (uint32_t i = lane; i < p.n_fn; i += kWarp) { C.hf.lt.err[i] = 0; C.hf.lt.mn[i] = 0xFFFFFFFFu; C.hf.lt.mx[i] = 0; }
+    uint32_t* b = sm_lanetab(p.n_fn);
+    const uint32_t n = p.n_fn * kWarp;
+    for (uint32_t i = lane; i < 3 * n; i += kWarp) b[i] = 0;
+    for (uint32_t i = lane; i < p.n_fn; i += kWarp) { b[3 * n + i] = 0; b[3 * n + p.n_fn + i] = 0xFFFFFFFFu; b[3 * n + 2 * p.n_fn + i] = 0; }
   }
-  if (C.tab)
+  SmemRow* tab = sm_tab(p.n_fn);
+  if (tab)
     for (uint32_t i = threadIdx.x; i < p.n_fn; i += blockDim.x) {
       SmemRow z; z.count = z.err = z.s0 = z.s1 = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
-      C.tab[i] = z;
+      tab[i] = z;
     }
+  DevRow* dcache = sm_dcache(p.n_fn);
   for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
     DevRow z; z.tag = 0; z.count = 0; z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
-    C.dcache[i] = z;
+    dcache[i] = z;
   }
-  for (uint32_t i = threadIdx.x; i < kNameSlots; i += blockDim.x) { C.ncache[i].hash = 0; C.ncache[i].row = 0; }
+  NameSlot* ncache = sm_ncache(p.n_fn);
+  for (uint32_t i = threadIdx.x; i < kNameSlots; i += blockDim.x) { ncache[i].hash = 0; ncache[i].row = 0; }
+  if (p.max_sid < (uint32_t)kSdescMax) {
+    uint32_t* t = reinterpret_cast<uint32_t*>(g_smem + smem_layout(p.n_fn).sdesc);
+    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) {
+      const uint2 d = __ldg(&p.desc[i]);
+      t[i] = d_present(d) ? (SD_PRESENT | ((d_flags(d) & SF_VAR) ? SD_VAR : 0u) | d_fixed(d)) : 0u;
+    }
+  }
   if (lane == 0) {
-    mbar_init(&C.ws->mbar);
+    mbar_init(&warp_smem(p.n_fn)->mbar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  C.scratch = p.warp_scratch + (size_t)(blockIdx.x * kWarpsPerCta + warp) * kMaxRecTile;
-  return C;
 }
 
 struct Counters {
@@ -647,8 +661,12 @@ struct Counters {
   uint64_t last_ts;
 };
 
-__device__ __noinline__ void tile_epilogue(const Params& p, const TileCtx C, const Counters K) {
+__device__ __noinline__ void tile_epilogue(const Params& p, const Counters K) {
   const uint32_t lane = lane_id();
+  uint32_t* lt = sm_lanetab(p.n_fn);
+  const uint32_t nn = p.n_fn * kWarp;
+  SmemRow* tab = sm_tab(p.n_fn);
+  DevRow* dcache = sm_dcache(p.n_fn);
   auto wsum = [](uint32_t v) { return __reduce_add_sync(0xffffffffu, v); };
   uint32_t a0 = wsum(K.events), a1 = wsum(K.passed), a2 = wsum(K.host), a3 = wsum(K.dev), a4 = wsum(K.samples),
            a5 = wsum(K.orph);
@@ -664,10 +682,10 @@ __device__ __noinline__ void tile_epilogue(const Params& p, const TileCtx C, con
     atomicMax(p.last_ts, (unsigned long long)mts);
   }
   __syncwarp();
-  if (C.hf.small) {
+  if (p.n_fn <= kSmallF) {
     for (uint32_t f = 0; f < p.n_fn; f++) {
       uint32_t i = f * kWarp + lane;
-      uint64_t cc = C.hf.lt.cnt[i], sum = ((uint64_t)C.hf.lt.shi[i] << 32) | C.hf.lt.slo[i];
+      uint64_t cc = lt[i], sum = ((uint64_t)lt[2 * nn + i] << 32) | lt[nn + i];
       if (!__any_sync(0xffffffffu, cc != 0)) continue;
       for (int d = 16; d; d >>= 1) {
         cc += __shfl_xor_sync(0xffffffffu, cc, d);
@@ -676,17 +694,17 @@ __device__ __noinline__ void tile_epilogue(const Params& p, const TileCtx C, con
       if (lane == 0 && cc) {
         unsigned long long* a = p.host_acc + 6ull * f;
         atomicAdd(&a[0], (unsigned long long)cc);
-        if (C.hf.lt.err[f]) atomicAdd(&a[1], (unsigned long long)C.hf.lt.err[f]);
+        if (lt[3 * nn + f]) atomicAdd(&a[1], (unsigned long long)lt[3 * nn + f]);
         add_i128(&a[2], &a[3], sum, 0);
-        atomicMin(&a[4], (unsigned long long)C.hf.lt.mn[f]);
-        atomicMax(&a[5], (unsigned long long)C.hf.lt.mx[f]);
+        atomicMin(&a[4], (unsigned long long)lt[3 * nn + p.n_fn + f]);
+        atomicMax(&a[5], (unsigned long long)lt[3 * nn + 2 * p.n_fn + f]);
       }
     }
   }
   __syncthreads();
-  if (C.tab) {
+  if (tab) {
     for (uint32_t f = threadIdx.x; f < p.n_fn; f += blockDim.x) {
-      SmemRow r = C.tab[f];
+      SmemRow r = tab[f];
       if (!r.count) continue;
       unsigned long long* a = p.host_acc + 6ull * f;
       atomicAdd(&a[0], (unsigned long long)r.count);
@@ -697,7 +715,7 @@ __device__ __noinline__ void tile_epilogue(const Params& p, const TileCtx C, con
     }
   }
   for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
-    DevRow r = C.dcache[i];
+    DevRow r = dcache[i];
     if (!r.tag || !r.count) continue;
     unsigned long long* a = p.dev_acc + 6ull * (r.tag - 1);
     atomicAdd(&a[0], (unsigned long long)r.count);
@@ -712,13 +730,15 @@ __device__ __noinline__ void tile_epilogue(const Params& p, const TileCtx C, con
 // the tile kernel
 
 __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* done) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  const SmemLayout SL = smem_layout(p.n_fn);
   const uint32_t lane = lane_id();
-  const TileCtx C = tile_prologue(p, SL, smem);
+  tile_prologue(p);
   __syncthreads();
-  WarpSmem* ws = C.ws;
+  WarpSmem* ws = warp_smem(p.n_fn);
   const uint32_t* win = ws->win;
+  const bool small = p.n_fn <= kSmallF;
+  uint32_t* const lt = sm_lanetab(p.n_fn);
+  const uint32_t nn = p.n_fn * kWarp;
+  SumEntry* const scratch = p.warp_scratch + (size_t)(blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5)) * kMaxRecTile;
   Counters K;
   K.events = K.passed = K.host = K.dev = K.samples = K.orph = 0;
   K.last_ts = 0;
@@ -736,7 +756,7 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
     parity ^= 1u;
     Window w;  // generic accessor for fields that leave the window
     w.s = win; w.win_start = G.t0; w.win_end = G.t0 + G.nbytes; w.g = G.gbase; w.size = G.size;
-    const Found F = find_records(p, done, ws, G, w, C.sdesc);
+    const Found F = find_records(p, done, G, w);
     if (F.dead) continue;
     const Look& L = F.L;
     const uint32_t n_rec = F.n_rec;
@@ -751,7 +771,7 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
     uint32_t n_pend = 0;       // pending exits so far
     bool slow = false;         // exact elimination mode (GStack in scratch)
     GStack gs;
-    gs.base = C.scratch;
+    gs.base = scratch;
     gs.n_pend = 0;
     gs.top = 0;
     bool feed_done = false;
@@ -790,7 +810,7 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
         qn += __popc(Qm);
         __syncwarp();
         if (qn >= (uint32_t)kWarp) {
-          const uint4 dq = drain_queue(p, ws, w, t0, win_len, s, L.base, kWarp, C.dcache, C.ncache);
+          const uint4 dq = drain_queue(p, w, t0, win_len, s, L.base, kWarp);
           K.dev += dq.x;
           K.samples += dq.y;
           spans += dq.x;
@@ -852,7 +872,7 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
           Dc = __shfl_sync(0xffffffffu, after, 31);
           __syncwarp();
         } else {
-          to_exact(ws, C.scratch, L.base, n_pend, Dc);
+          to_exact(p.n_fn, scratch, L.base, n_pend, Dc);
           gs.n_pend = n_pend;
           gs.top = n_pend + (uint32_t)Dc;
           slow = true;
@@ -874,17 +894,19 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
       if (paired) {
         const uint64_t dur = R.ts - ets;
         const int32_t fn = m_fn(R.meta);
-        if (C.hf.small && (dur >> 32) == 0) {
+        if (small && (dur >> 32) == 0) {
           const uint32_t i = (uint32_t)fn * kWarp + lane, d = (uint32_t)dur;
-          C.hf.lt.cnt[i] += 1;
-          const uint32_t lo = C.hf.lt.slo[i] + d;
-          C.hf.lt.shi[i] += lo < d ? 1u : 0u;
-          C.hf.lt.slo[i] = lo;
-          if (d < C.hf.lt.mn[fn]) atomicMin(&C.hf.lt.mn[fn], d);
-          if (d > C.hf.lt.mx[fn]) atomicMax(&C.hf.lt.mx[fn], d);
-          if (R.meta & M_ERR) atomicAdd(&C.hf.lt.err[fn], 1u);
+          lt[i] += 1;
+          const uint32_t lo = lt[nn + i] + d;
+          lt[2 * nn + i] += lo < d ? 1u : 0u;
+          lt[nn + i] = lo;
+          uint32_t* const mn = lt + 3 * nn + p.n_fn;
+          uint32_t* const mx = mn + p.n_fn;
+          if (d < mn[fn]) atomicMin(&mn[fn], d);
+          if (d > mx[fn]) atomicMax(&mx[fn], d);
+          if (R.meta & M_ERR) atomicAdd(&lt[3 * nn + fn], 1u);
         } else {
-          fold_slow(p, C.hf, fn, dur, (R.meta & M_ERR) != 0);
+          fold_slow(p, fn, dur, (R.meta & M_ERR) != 0);
         }
         K.host++;
         spans++;
@@ -898,14 +920,14 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
       if (dm) break;  // the stream is cut at the failing record
     }
     if (qn) {
-      const uint4 dq = drain_queue(p, ws, w, t0, win_len, s, L.base, qn, C.dcache, C.ncache);
+      const uint4 dq = drain_queue(p, w, t0, win_len, s, L.base, qn);
       K.dev += dq.x;
       K.samples += dq.y;
       spans += dq.x;
     }
-    write_summary(p, ws, C.scratch, G.g, s, L.base, slow, n_pend, Dc, gs, spans);
+    write_summary(p, scratch, G.g, s, L.base, slow, n_pend, Dc, gs, spans);
   }
-  tile_epilogue(p, C, K);
+  tile_epilogue(p, K);
 }
 
 // ---------------------------------------------------------------------------

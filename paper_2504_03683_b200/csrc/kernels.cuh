@@ -26,6 +26,10 @@
 
 namespace hg {
 
+// dynamic shared memory of the tile kernel; every shared pointer is derived from this
+// symbol in the function that uses it so accesses compile to LDS/STS
+extern __shared__ __align__(128) uint8_t g_smem[];
+
 constexpr int kLaneBytes = 256;                // stream bytes per lane in pass A
 constexpr int kTile = kWarp * kLaneBytes;      // 8 KiB per warp tile
 constexpr int kMaxRecLane = kLaneBytes / 16;   // records per lane (16-byte minimum)
@@ -228,9 +232,11 @@ __device__ __forceinline__ void lane_walk(const Params& p, WarpSmem* ws, const u
 }
 
 // offsets are window-relative u32; kNone32 marks "dead/unknown"
-__device__ __noinline__ void warp_verify(const Params& p, WarpSmem* ws, const uint32_t* win, uint64_t t0, uint64_t size,
-                            uint32_t sub1, uint32_t e0, uint32_t& hyp, uint32_t& cnt, uint32_t& exit, bool& fail,
-                            uint32_t& fail_off) {
+__device__ __noinline__ void warp_verify(const Params& p, uint32_t ws_off, uint64_t t0, uint64_t size,
+                                         uint32_t sub1, uint32_t e0, uint32_t& hyp, uint32_t& cnt, uint32_t& exit,
+                                         bool& fail, uint32_t& fail_off) {
+  WarpSmem* ws = reinterpret_cast<WarpSmem*>(g_smem + ws_off);
+  const uint32_t* win = ws->win;
   const uint32_t lane = lane_id();
   for (int it = 0; it < 2 * kWarp + 2; it++) {
     uint32_t up = __shfl_up_sync(0xffffffffu, exit, 1);
@@ -416,7 +422,7 @@ __device__ __noinline__ void fold_device_global(const Params& p, uint32_t row, u
   }
 }
 
-__device__ __noinline__ void fold_device(const Params& p, DevRow* cache, uint32_t row, uint64_t d_lo, int64_t d_hi) {
+__device__ __forceinline__ void fold_device(const Params& p, DevRow* cache, uint32_t row, uint64_t d_lo, int64_t d_hi) {
   DevRow* r = &cache[row % kDevSlots];
   uint32_t tag = *(volatile uint32_t*)&r->tag;
   if (tag == 0) { tag = atomicCAS(&r->tag, 0u, row + 1); if (tag == 0) tag = row + 1; }
