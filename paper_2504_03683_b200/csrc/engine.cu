@@ -384,6 +384,25 @@ __device__ __noinline__ uint4 drain_queue(const Params& p, Window w, uint64_t t0
   return make_uint4(dev, samples, 0, 0);
 }
 
+// clamped depth walk when exits meet an empty tile stack (Lindley recursion:
+// depth_i = S_i - min(0, min_j<=i S_j) with S the unclamped walk from Dc)
+__device__ __noinline__ int32_t clamped_depth(int32_t Dc, int32_t ps) {
+  const uint32_t lane = lane_id();
+  int32_t m = ps;
+  for (int d = 1; d < 32; d <<= 1) {
+    int32_t t = __shfl_up_sync(0xffffffffu, m, d);
+    if ((int)lane >= d) m = min(m, t);
+  }
+  return Dc + ps - min(0, Dc + min(-Dc, m));
+}
+
+// first NaN/inf result of the tile whose exit paired (per lane: the caller keeps one per tile)
+__device__ __noinline__ bool push_result_error(const Params& p, uint32_t s, uint64_t seq, uint64_t off, uint64_t ts,
+                                               uint64_t res) {
+  push_error(p, HG_ERR_RESULT, s, seq, off, ts, 0, res);
+  return true;
+}
+
 // materialise the fast-path tile state (pending exits + open levels) as an explicit stack
 __device__ __noinline__ void to_exact(uint32_t n_fn, SumEntry* scratch, uint64_t base, uint32_t n_pend, int32_t Dc) {
   WarpSmem* ws = warp_smem(n_fn);
@@ -764,17 +783,19 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
     const uint64_t t0 = G.t0;
     const uint32_t win_len = G.nbytes;
 
-    // ---- rounds: lockstep decode + pairing
+    // ---- rounds: lockstep decode + pairing, 32 records per round.  All rare events
+    // (decode errors, clamped depths, typed mismatches, deep stacks, NaN results) are
+    // behind single warp votes so the common round stays short.
     uint64_t prev_ts = L.prev_ts;
     bool have_prev = L.has_prev;
-    int32_t Dc = 0;            // depth (open entries of this tile) before the round
+    int32_t Dc = 0;            // open entries of this tile before the round
     uint32_t n_pend = 0;       // pending exits so far
     bool slow = false;         // exact elimination mode (GStack in scratch)
     GStack gs;
     gs.base = scratch;
     gs.n_pend = 0;
     gs.top = 0;
-    bool feed_done = false;
+    bool res_done = false;
     uint32_t spans = 0;
     uint32_t qn = 0;           // deferred records waiting in ws->q
     for (uint32_t rb = 0; rb < n_rec; rb += kWarp) {
@@ -792,21 +813,29 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
       }
       // monotonicity against the previous record of the stream (pipeline.py:98-99)
       const uint64_t up_ts = __shfl_up_sync(0xffffffffu, R.ts, 1);
-      const bool hp = lane == 0 ? have_prev : true;
       const uint64_t pts = lane == 0 ? prev_ts : up_ts;
-      if (act && !dec_err && hp && R.ts < pts) dec_err = HG_ERR_ORDER;
-      const uint32_t dm = __ballot_sync(0xffffffffu, act && dec_err);
-      const int dl = dm ? __ffs(dm) - 1 : 32;
-      if (dm && (int)lane == dl) push_error(p, dec_err, s, L.base + r, t0 + o, R.ts, hp ? pts : 0, dec_aux);
-      const bool live = act && (int)lane < dl;
-      if (!live) R.x = 0;
+      if (act && !dec_err && (lane != 0 || have_prev) && R.ts < pts) dec_err = HG_ERR_ORDER;
+      uint32_t live_mask = __ballot_sync(0xffffffffu, act);
+      const uint32_t dm = __ballot_sync(0xffffffffu, dec_err != 0);
+      if (dm) {  // the stream is cut at the first failing record
+        const int dl = __ffs(dm) - 1;
+        if ((int)lane == dl)
+          push_error(p, dec_err, s, L.base + r, t0 + o, R.ts, (lane != 0 || have_prev) ? pts : 0, dec_aux);
+        live_mask &= (1u << dl) - 1u;
+        if (!((live_mask >> lane) & 1u)) { R.x = 0; defer = false; }
+      }
+      const bool live = (live_mask >> lane) & 1u;
       if (live) {
         K.events++;
         K.last_ts = R.ts > K.last_ts ? R.ts : K.last_ts;
       }
-      {  // defer payload work to the queue; drain it 32 at a time
-        const uint32_t Qm = __ballot_sync(0xffffffffu, live && defer);
-        if (live && defer) ws->q[qn + __popc(Qm & lanemask_lt())] = o | (r << 16);
+      if (live_mask) {
+        prev_ts = __shfl_sync(0xffffffffu, R.ts, 31 - __clz(live_mask));
+        have_prev = true;
+      }
+      const uint32_t Qm = __ballot_sync(0xffffffffu, defer);
+      if (Qm) {  // defer payload work; drain 32 at a time with every lane active
+        if (defer) ws->q[qn + __popc(Qm & lanemask_lt())] = o | (r << 16);
         qn += __popc(Qm);
         __syncwarp();
         if (qn >= (uint32_t)kWarp) {
@@ -819,10 +848,8 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
           __syncwarp();
         }
       }
-      prev_ts = __shfl_sync(0xffffffffu, R.ts, min(31u, n_rec - 1 - rb));
-      have_prev = true;
 
-      // ---- pairing
+      // ---- pairing (pipeline.py:156-185)
       const bool isE = R.x > 0, isX = R.x < 0;
       bool paired = false, orphan = false;
       uint64_t ets = 0;
@@ -830,45 +857,35 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
         const uint32_t Em = __ballot_sync(0xffffffffu, isE);
         const uint32_t Xm = __ballot_sync(0xffffffffu, isX);
         const uint32_t le = lanemask_lt() | (1u << lane);
-        // depth within the tile: ballot prefix counts, clamped at zero when exits meet an empty stack
         const int32_t ps = (int32_t)__popc(Em & le) - (int32_t)__popc(Xm & le);
         int32_t after = Dc + ps;
-        if (__any_sync(0xffffffffu, after < 0)) {
-          int32_t m = ps;
-          for (int d = 1; d < 32; d <<= 1) {
-            int32_t t = __shfl_up_sync(0xffffffffu, m, d);
-            if ((int)lane >= d) m = min(m, t);
-          }
-          after = Dc + ps - min(0, Dc + min(-Dc, m));
-        }
+        if (__any_sync(0xffffffffu, after < 0)) after = clamped_depth(Dc, ps);  // exits met an empty tile stack
         int32_t before = __shfl_up_sync(0xffffffffu, after, 1);
         if (lane == 0) before = Dc;
         const bool pops = isX && before > 0;
-        const bool pend = isX && before <= 0;
         const int32_t level = isE ? after : before;
-        const bool too_deep = __any_sync(0xffffffffu, (isE || pops) && level >= kLevels);
-        const uint32_t Pm = __ballot_sync(0xffffffffu, pend);
-        const bool pend_full = n_pend + __popc(Pm) > (uint32_t)kPendCap;
         const uint32_t key = (isE || pops) ? (uint32_t)level : (0x80000000u | lane);
         const uint32_t same = __match_any_sync(0xffffffffu, key);
         const uint32_t cand = same & Em & lanemask_lt();
-        const int el = cand ? 31 - __clz(cand) : 0;
+        const int el = cand ? 31 - __clz(cand) : (int)lane;
         const uint32_t cmeta = __shfl_sync(0xffffffffu, R.meta, el);
         const uint64_t cts = __shfl_sync(0xffffffffu, R.ts, el);
-        uint32_t emeta = 0;
-        if (pops) {
-          if (cand) { emeta = cmeta; ets = cts; }
-          else if (level < kLevels) { emeta = ws->lvl_meta[level]; ets = ws->lvl_ts[level]; }
-        }
-        const bool mism = pops && ((emeta ^ R.meta) & M_FN) != 0;
-        if (!__any_sync(0xffffffffu, mism) && !too_deep && !pend_full) {
+        uint32_t emeta = cmeta;
+        ets = cts;
+        const bool deep = (isE || pops) && level >= kLevels;
+        if (pops && !cand && !deep) { emeta = ws->lvl_meta[level]; ets = ws->lvl_ts[level]; }
+        const uint32_t Pm = __ballot_sync(0xffffffffu, isX && before <= 0);
+        const bool bad = deep || (pops && ((emeta ^ R.meta) & M_FN) != 0);
+        if (!__any_sync(0xffffffffu, bad) && n_pend + __popc(Pm) <= (uint32_t)kPendCap) {
           paired = pops;
           if (isE && !(same & Em & lanemask_gt())) { ws->lvl_ts[level] = R.ts; ws->lvl_meta[level] = R.meta; }
-          if (pend) {
-            const uint32_t i = n_pend + __popc(Pm & lanemask_lt());
-            ws->pend_ts[i] = R.ts; ws->pend_res[i] = R.res; ws->pend_meta[i] = R.meta;
+          if (Pm) {
+            if ((Pm >> lane) & 1u) {
+              const uint32_t i = n_pend + __popc(Pm & lanemask_lt());
+              ws->pend_ts[i] = R.ts; ws->pend_res[i] = R.res; ws->pend_meta[i] = R.meta;
+            }
+            n_pend += __popc(Pm);
           }
-          n_pend += __popc(Pm);
           Dc = __shfl_sync(0xffffffffu, after, 31);
           __syncwarp();
         } else {
@@ -890,6 +907,7 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
         ets = ro2.ets;
         gs.n_pend = ro2.n_pend;
         gs.top = ro2.top;
+        if (orphan) { push_orphan(p, s, m_fn(R.meta), R.ts, L.base + r); K.orph++; }
       }
       if (paired) {
         const uint64_t dur = R.ts - ets;
@@ -910,13 +928,9 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
         }
         K.host++;
         spans++;
+        if ((R.meta & M_BAD) && !res_done)  // int(NaN/inf) raises only when the exit pairs
+          res_done = push_result_error(p, s, L.base + r, t0 + o, R.ts, R.res);
       }
-      const uint32_t bm = __ballot_sync(0xffffffffu, paired && (R.meta & M_BAD));
-      if (bm && !feed_done) {
-        if ((int)lane == __ffs(bm) - 1) push_error(p, HG_ERR_RESULT, s, L.base + r, t0 + o, R.ts, 0, R.res);
-        feed_done = true;
-      }
-      if (orphan) { push_orphan(p, s, m_fn(R.meta), R.ts, L.base + r); K.orph++; }
       if (dm) break;  // the stream is cut at the failing record
     }
     if (qn) {
