@@ -52,7 +52,7 @@ struct SmemLayout {
 };
 __host__ __device__ inline SmemLayout smem_layout(uint32_t n_fn) {
   SmemLayout L{};
-  size_t off = 0;
+  size_t off = align128(sizeof(uint2) * kSdescMax);  // compact descriptors at offset 0 (desc_of)
   bool small = n_fn <= kSmallF;
   L.tab = off;
   if (!small && n_fn <= kSmemFnMax) off += align128(sizeof(SmemRow) * n_fn);
@@ -62,8 +62,7 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t n_fn) {
   off += align128(sizeof(DevRow) * kDevSlots);
   L.ncache = off;
   off += align128(sizeof(NameSlot) * kNameSlots);
-  L.sdesc = off;
-  off += align128(sizeof(uint32_t) * kSdescMax);
+  L.sdesc = 0;
   L.warps = off;
   off += sizeof(WarpSmem) * kWarpsPerCta;
   L.total = off;
@@ -74,8 +73,8 @@ constexpr uint32_t SD_PRESENT = 0x80000000u, SD_VAR = 0x40000000u;
 
 // schema screening entry: present | var | fixed payload length (var: minimum)
 __device__ __forceinline__ uint32_t sdesc_lookup(const Params& p, const uint32_t* sdesc, uint32_t sid) {
-  if (sdesc) return sdesc[sid];
-  const uint2 d = __ldg(&p.desc[sid]);
+  (void)sdesc;
+  const uint2 d = desc_of(p, sid);
   return d_present(d) ? (SD_PRESENT | ((d_flags(d) & SF_VAR) ? SD_VAR : 0u) | d_fixed(d)) : 0u;
 }
 
@@ -663,11 +662,8 @@ __device__ __noinline__ void tile_prologue(const Params& p) {
   NameSlot* ncache = sm_ncache(p.n_fn);
   for (uint32_t i = threadIdx.x; i < kNameSlots; i += blockDim.x) { ncache[i].hash = 0; ncache[i].row = 0; }
   if (p.max_sid < (uint32_t)kSdescMax) {
-    uint32_t* t = reinterpret_cast<uint32_t*>(g_smem + smem_layout(p.n_fn).sdesc);
-    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) {
-      const uint2 d = __ldg(&p.desc[i]);
-      t[i] = d_present(d) ? (SD_PRESENT | ((d_flags(d) & SF_VAR) ? SD_VAR : 0u) | d_fixed(d)) : 0u;
-    }
+    uint2* t = reinterpret_cast<uint2*>(g_smem);
+    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) t[i] = __ldg(&p.desc[i]);
   }
   if (lane == 0) {
     mbar_init(&warp_smem(p.n_fn)->mbar);

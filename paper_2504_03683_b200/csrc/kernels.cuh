@@ -156,8 +156,11 @@ __device__ __forceinline__ uint64_t s64(const uint32_t* w, uint32_t o) {
   return ((uint64_t)__funnelshift_r(b, c, sh) << 32) | __funnelshift_r(a, b, sh);
 }
 
+// compact descriptors live at the start of the tile kernel's shared memory when the
+// registry's ids fit (kSdescMax); otherwise they are read through L1
 __device__ __forceinline__ uint2 desc_of(const Params& p, uint32_t sid) {
   if (sid > p.max_sid) return make_uint2(0, 0);
+  if (p.max_sid < (uint32_t)kSdescMax) return reinterpret_cast<const uint2*>(g_smem)[sid];
   return __ldg(&p.desc[sid]);
 }
 __device__ __forceinline__ bool d_present(uint2 d) { return (d.x & D_PRESENT) != 0; }
@@ -190,7 +193,7 @@ __device__ __forceinline__ bool plausible(const Params& p, const uint32_t* win, 
   if (o + 16 > win_len) return false;
   uint32_t sid = s32(win, o);
   if (sid > p.max_sid) return false;
-  uint2 d = __ldg(&p.desc[sid]);
+  uint2 d = desc_of(p, sid);
   if (!d_present(d)) return false;
   uint32_t plen = s32(win, o + 12);
   if (t0 + o + 16 + plen > size) return false;
