@@ -183,10 +183,21 @@ int hg_get_stream_spans(hg_ctx* ctx, uint64_t* per_stream, uint64_t n); /* span 
 int hg_get_orphans(hg_ctx* ctx, hg_orphan* out, uint64_t cap, uint64_t* n); /* IntervalBuilder.orphans */
 int hg_get_trace_errors(hg_ctx* ctx, hg_trace_error* out, uint64_t cap, uint64_t* n);
 
+/* function names (UTF-8, id = index, offsets[n] = end; is_null[i] != 0 for a
+ * None name, may be NULL): the "name" of host-span timeline objects
+ * (sinks.py:369, registry.py:61-71 EventSchema.function).  Required before a
+ * run with HG_WANT_TIMELINE. */
+int hg_set_function_names(hg_ctx* ctx, const char* bytes, const uint64_t* offsets, const uint8_t* is_null,
+                          uint32_t n);
+
 /* timeline: Chrome-trace JSON bytes exactly as json.dump(objs, fh, indent=1)
- * writes them (sinks.py:414-418) */
+ * writes them (TimelineSink, sinks.py:341-418), built on the GPU by the run
+ * that had HG_WANT_TIMELINE (and no trace error). */
 int hg_timeline_size(hg_ctx* ctx, uint64_t* n_bytes);
 int hg_get_timeline(hg_ctx* ctx, char* out, uint64_t cap);
+int hg_timeline_ms(hg_ctx* ctx, float* ms);  /* device time of the ordering + formatting */
+/* TimelineSink(device_index=) (sinks.py:347-349): device pid 9000000 + index */
+int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index);
 
 /* device-resident dense tally for NCCL merging across ranks: host rows are
  * function-indexed.  Returns device pointers owned by the context. */

@@ -15,10 +15,12 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
 #include "kernels.cuh"
+#include "timeline.cuh"
 
 using namespace hg;
 
@@ -349,11 +351,14 @@ __device__ __noinline__ uint4 drain_queue(const Params& p, Window w, uint64_t t0
   const uint32_t lane = lane_id();
   const uint32_t* win = ws->win;
   uint32_t dev = 0, samples = 0;
+  uint32_t sid = 0, rec = 0;
+  uint64_t a = 0;
   if (lane < n) {
     const uint32_t e = ws->q[lane];
-    const uint32_t o = e & 0xFFFFu, rec = e >> 16;
-    const uint64_t a = t0 + o;
-    const uint32_t sid = s32(win, o);
+    const uint32_t o = e & 0xFFFFu;
+    rec = e >> 16;
+    a = t0 + o;
+    sid = s32(win, o);
     const uint32_t plen = s32(win, o + 12);
     const uint2 d = desc_of(p, sid);
     const uint32_t cls = d_cls(d);
@@ -380,6 +385,9 @@ __device__ __noinline__ uint4 drain_queue(const Params& p, Window w, uint64_t t0
       samples = (ro.y >> 1) & 1u;
     }
   }
+  if (p.tl_items)  // device span / sample message at its record (pipeline.py:186-215)
+    tl_emit(p, (dev | samples) != 0, (dev | samples) ? rd64(w, a + 4) : 0, tl_klo(s, base + rec),
+            (uint64_t)(w.g + a + 16), 0, dev ? TL_DEVICE : TL_SAMPLE, sid);
   return make_uint4(dev, samples, 0, 0);
 }
 
@@ -402,15 +410,22 @@ __device__ __noinline__ bool push_result_error(const Params& p, uint32_t s, uint
   return true;
 }
 
+// result kind of a pending exit (its record is still in the window)
+__device__ __forceinline__ uint32_t pend_result_kind(const Params& p, const WarpSmem* ws, uint32_t m) {
+  const uint32_t sid = s32(ws->win, ws->rlist[m_rec(m)]);
+  return result_kind(d_flags(desc_of(p, sid)));
+}
+
 // materialise the fast-path tile state (pending exits + open levels) as an explicit stack
-__device__ __noinline__ void to_exact(uint32_t n_fn, SumEntry* scratch, uint64_t base, uint32_t n_pend, int32_t Dc) {
-  WarpSmem* ws = warp_smem(n_fn);
+__device__ __noinline__ void to_exact(const Params& p, SumEntry* scratch, uint64_t base, uint32_t n_pend, int32_t Dc) {
+  WarpSmem* ws = warp_smem(p.n_fn);
   const uint32_t lane = lane_id();
   for (uint32_t i = lane; i < n_pend; i += kWarp) {
     SumEntry e;
     uint32_t m = ws->pend_meta[i];
     e.ts = ws->pend_ts[i]; e.seq = base + m_rec(m); e.fn = m_fn(m);
-    e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u);
+    e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u) |
+              (pend_result_kind(p, ws, m) << 4);
     e.result = ws->pend_res[i];
     scratch[i] = e;
   }
@@ -620,7 +635,8 @@ __device__ __noinline__ void write_summary(const Params& p, SumEntry* scratch, u
     } else if (i < n_pend) {
       uint32_t m = ws->pend_meta[i];
       e.ts = ws->pend_ts[i]; e.seq = base + m_rec(m); e.fn = m_fn(m); e.result = ws->pend_res[i];
-      e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u);
+      e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u) |
+                (pend_result_kind(p, ws, m) << 4);
     } else {
       uint32_t lv = i - n_pend + 1;
       uint32_t m = ws->lvl_meta[lv];
@@ -885,7 +901,7 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
           Dc = __shfl_sync(0xffffffffu, after, 31);
           __syncwarp();
         } else {
-          to_exact(p.n_fn, scratch, L.base, n_pend, Dc);
+          to_exact(p, scratch, L.base, n_pend, Dc);
           gs.n_pend = n_pend;
           gs.top = n_pend + (uint32_t)Dc;
           slow = true;
@@ -895,7 +911,8 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
         SumEntry mine;
         mine.ts = R.ts; mine.seq = L.base + r; mine.fn = m_fn(R.meta);
         mine.flags = (isX ? 1u : 0u) | ((R.meta & M_ERR) ? 2u : 0u) | ((R.meta & M_BAD) ? 4u : 0u) |
-                     ((R.meta & M_NAN) ? 8u : 0u);
+                     ((R.meta & M_NAN) ? 8u : 0u) |
+                     (isX ? result_kind(d_flags(desc_of(p, s32(win, o)))) << 4 : 0u);
         mine.result = R.res;
         const RoundOut ro2 = round_resolve(gs, true, isE, isX, m_fn(R.meta), R.ts, mine);
         paired = ro2.flags & 1u;
@@ -926,6 +943,11 @@ __global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* 
         spans++;
         if ((R.meta & M_BAD) && !res_done)  // int(NaN/inf) raises only when the exit pairs
           res_done = push_result_error(p, s, L.base + r, t0 + o, R.ts, R.res);
+      }
+      if (p.tl_items) {  // host span message at the exit (pipeline.py:170-185)
+        const uint32_t fl = paired ? d_flags(desc_of(p, s32(win, o))) : 0u;
+        tl_emit(p, paired, R.ts, tl_klo(s, L.base + r), ets, R.res, TL_HOST | (result_kind(fl) << 4),
+                (uint32_t)m_fn(R.meta));
       }
       if (dm) break;  // the stream is cut at the failing record
     }
@@ -1027,6 +1049,9 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
             host++;
             spans++;
           }
+          if (p.tl_items)
+            tl_emit(p, paired, x.ts, tl_klo(s, x.seq), ets, x.result, TL_HOST | (((x.flags >> 4) & 3u) << 4),
+                    (uint32_t)x.fn);
           uint32_t bm = __ballot_sync(0xffffffffu, paired && (x.flags & 4u));
           if (bm && !res_done) {
             if ((int)lane == __ffs(bm) - 1)
@@ -1037,11 +1062,20 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
         }
       }
       // open calls become truncated spans ending at the global last timestamp
-      for (uint32_t i = lane; i < gs.top; i += kWarp) {
-        SumEntry en = gs.base[i];
-        hf.fold(p, en.fn, p.global_last_ts - en.ts, false);
-        trunc++;
-        spans++;
+      for (uint32_t ib = 0; ib < gs.top; ib += kWarp) {
+        const uint32_t i = ib + lane;
+        const bool on = i < gs.top;
+        SumEntry en;
+        en.ts = 0; en.fn = 0;
+        if (on) {
+          en = gs.base[i];
+          hf.fold(p, en.fn, p.global_last_ts - en.ts, false);
+          trunc++;
+          spans++;
+        }
+        if (p.tl_items)  // innermost first (pipeline.py:230-238)
+          tl_emit(p, on, ~0ull, (1ull << 63) | tl_klo(s, on ? gs.top - 1 - i : 0), en.ts, 0,
+                  TL_HOST | TL_TRUNC | (1u << 4), (uint32_t)en.fn);
       }
     } else if (lane == 0) {
       atomicExch(p.watchdog, 2u);  // stack scratch exhausted (host grows and reruns)
@@ -1175,6 +1209,22 @@ struct hg_ctx {
   bool phase1_done = false;
   float kernel_ms = 0, total_ms = 0;
   uint64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
+  // timeline
+  std::vector<std::string> fn_names;
+  std::vector<uint8_t> fn_null;
+  bool have_fn_names = false;
+  DBuf<TlItem> d_tl_items;
+  uint64_t tl_cap = 0;
+  DBuf<ulonglong2> d_tl_keys[2];
+  DBuf<uint32_t> d_tl_idx[2];
+  DBuf<uint32_t> d_tl_lens, d_tl_stream_proc;
+  DBuf<uint64_t> d_tl_offs, d_tl_bsum, d_tl_fnq_off, d_tl_sstr_off;
+  DBuf<char> d_tl_fnq, d_tl_sstr, d_tl_out, d_tl_devpid;
+  DBuf<unsigned int> d_tl_proc_first, d_tl_th_state, d_tl_th_first;
+  DBuf<unsigned long long> d_tl_th_hi, d_tl_th_lo;
+  uint64_t tl_size = 0;
+  bool tl_ready = false;
+  float tl_ms = 0;
 };
 
 // counter slots in d_counters
@@ -1191,7 +1241,10 @@ enum {
   C_OVERFLOW = 16,        // unsigned int
   C_WIDE = 17,            // unsigned int
   C_WATCHDOG = 18,        // unsigned int
-  C_NUM = 19
+  C_TL_N = 19,            // timeline messages appended
+  C_TL_TOTAL = 20,        // timeline body bytes (scan total)
+  C_TL_TH_OVF = 21,       // unsigned int: thread-name table overflow
+  C_NUM = 22
 };
 
 static int fail(hg_ctx* c, int code, const std::string& msg) {
@@ -1204,6 +1257,195 @@ static int fail(hg_ctx* c, int code, const std::string& msg) {
     cudaError_t e_ = (call);                                                                \
     if (e_ != cudaSuccess) return fail(ctx, HG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
+
+// json.dumps(str) with ensure_ascii (json/encoder.py) of a valid UTF-8 string
+static std::string json_quote(const std::string& s) {
+  static const char* hx = "0123456789abcdef";
+  std::string o = "\"";
+  auto u4 = [&](uint32_t v) {
+    o += "\\u";
+    o += hx[(v >> 12) & 15]; o += hx[(v >> 8) & 15]; o += hx[(v >> 4) & 15]; o += hx[v & 15];
+  };
+  for (size_t i = 0; i < s.size();) {
+    uint32_t c = (uint8_t)s[i], cp;
+    auto b = [&](size_t k) { return (uint32_t)(k < s.size() ? (uint8_t)s[k] : 0x80) & 0x3F; };
+    if (c < 0x80) { cp = c; i += 1; }
+    else if (c < 0xE0) { cp = ((c & 0x1F) << 6) | b(i + 1); i += 2; }
+    else if (c < 0xF0) { cp = ((c & 0x0F) << 12) | (b(i + 1) << 6) | b(i + 2); i += 3; }
+    else { cp = ((c & 0x07) << 18) | (b(i + 1) << 12) | (b(i + 2) << 6) | b(i + 3); i += 4; }
+    if (cp == '"') o += "\\\"";
+    else if (cp == '\\') o += "\\\\";
+    else if (cp >= 0x20 && cp < 0x7F) o += (char)cp;
+    else if (cp == '\n') o += "\\n";
+    else if (cp == '\r') o += "\\r";
+    else if (cp == '\t') o += "\\t";
+    else if (cp == '\b') o += "\\b";
+    else if (cp == '\f') o += "\\f";
+    else if (cp < 0x10000) u4(cp);
+    else { uint32_t v = cp - 0x10000; u4(0xD800 | (v >> 10)); u4(0xDC00 | (v & 0x3FF)); }
+  }
+  o += "\"";
+  return o;
+}
+
+template <class T>
+static cudaError_t upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
+  cudaError_t e = d.ensure(std::max<size_t>(h.size(), 1));
+  if (e != cudaSuccess || h.empty()) return e;
+  return cudaMemcpyAsync(d.ptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st);
+}
+
+// order, format and store the timeline JSON (TimelineSink.on_finish, sinks.py:414-418)
+static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
+  ctx->tl_ready = false;
+  if (!ctx->have_fn_names || ctx->fn_names.size() != ctx->n_fn)
+    return fail(ctx, HG_ESTATE, "hg_set_function_names is required for the timeline");
+  const unsigned long long* C = ctx->counters.data();
+  if (C[C_TL_N] > ctx->tl_cap) return fail(ctx, HG_ENOMEM, "timeline message buffer overflow (engine bug)");
+  const uint32_t n = (uint32_t)C[C_TL_N];
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  cudaStream_t st = ctx->stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  // host tables: quoted function names; per stream pid, tid, process name
+  std::vector<char> fnq;
+  std::vector<uint64_t> fnq_off(1, 0);
+  for (uint32_t f = 0; f < ctx->n_fn; f++) {
+    std::string q = ctx->fn_null[f] ? std::string("null") : json_quote(ctx->fn_names[f]);
+    fnq.insert(fnq.end(), q.begin(), q.end());
+    fnq_off.push_back(fnq.size());
+  }
+  const int64_t dev_pid = 9000000 + (int64_t)ctx->cfg.timeline_device_index;
+  std::vector<char> sstr;
+  std::vector<uint64_t> sstr_off(1, 0);
+  std::vector<uint32_t> sproc(std::max<uint32_t>(ns, 1), 0);
+  std::map<int64_t, uint32_t> proc_id;  // process_name metas are keyed by (pid, 0)
+  for (uint32_t s = 0; s < ns; s++) {
+    const HostStream& hs = ctx->streams[s];
+    std::string a = std::to_string(hs.pid), b = std::to_string(hs.tid);
+    std::string c = json_quote("Host " + hs.host + " pid " + a);
+    for (const std::string* x : {&a, &b, &c}) {
+      sstr.insert(sstr.end(), x->begin(), x->end());
+      sstr_off.push_back(sstr.size());
+    }
+    auto it = proc_id.find(hs.pid);
+    if (it == proc_id.end()) it = proc_id.emplace(hs.pid, (uint32_t)proc_id.size()).first;
+    sproc[s] = it->second;
+  }
+  auto dit = proc_id.find(dev_pid);
+  const uint32_t dev_proc = dit != proc_id.end() ? dit->second : (uint32_t)proc_id.size();
+  const uint32_t n_proc = (uint32_t)proc_id.size() + 1;
+  std::string dps = std::to_string(dev_pid);
+  std::vector<char> devpid(dps.begin(), dps.end());
+  CK(upload(ctx->d_tl_fnq, fnq, st));
+  CK(upload(ctx->d_tl_fnq_off, fnq_off, st));
+  CK(upload(ctx->d_tl_sstr, sstr, st));
+  CK(upload(ctx->d_tl_sstr_off, sstr_off, st));
+  CK(upload(ctx->d_tl_stream_proc, sproc, st));
+  CK(upload(ctx->d_tl_devpid, devpid, st));
+  // sort by mux key
+  const uint32_t nblk = (n + kSortTile - 1) / kSortTile;
+  for (int k = 0; k < 2; k++) {
+    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
+  }
+  int cur = 0;
+  if (n) {
+    tl_blocksort_kernel<<<nblk, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, n, ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr);
+    CK(cudaGetLastError());
+    ctx->launches++;
+    for (uint64_t width = kSortTile; width < n; width *= 2) {
+      tl_merge_kernel<<<nblk, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
+                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr, n, width);
+      CK(cudaGetLastError());
+      ctx->launches++;
+      cur ^= 1;
+    }
+  }
+  // metadata first occurrences
+  uint64_t n_dev = C[C_STATS + ST_DEVICE];
+  uint32_t th_size = 64;
+  while (th_size < 2 * n_dev && th_size < (1u << 30)) th_size <<= 1;
+  CK(ctx->d_tl_proc_first.ensure(n_proc));
+  CK(ctx->d_tl_th_state.ensure(th_size));
+  CK(ctx->d_tl_th_first.ensure(th_size));
+  CK(ctx->d_tl_th_hi.ensure(th_size));
+  CK(ctx->d_tl_th_lo.ensure(th_size));
+  CK(cudaMemsetAsync(ctx->d_tl_proc_first.ptr, 0xFF, n_proc * 4, st));
+  CK(cudaMemsetAsync(ctx->d_tl_th_state.ptr, 0, (size_t)th_size * 4, st));
+  CK(cudaMemsetAsync(ctx->d_tl_th_first.ptr, 0xFF, (size_t)th_size * 4, st));
+  CK(ctx->d_tl_lens.ensure(std::max<uint32_t>(n, 1)));
+  CK(ctx->d_tl_offs.ensure(std::max<uint32_t>(n, 1)));
+  const uint32_t nsb = (n + kScanBlock - 1) / kScanBlock;
+  CK(ctx->d_tl_bsum.ensure(std::max<uint32_t>(nsb, 1)));
+  TlTables T{};
+  T.items = ctx->d_tl_items.ptr;
+  T.n = n;
+  T.order = ctx->d_tl_idx[cur].ptr;
+  T.fnq = ctx->d_tl_fnq.ptr;
+  T.fnq_off = ctx->d_tl_fnq_off.ptr;
+  T.sstr = ctx->d_tl_sstr.ptr;
+  T.sstr_off = ctx->d_tl_sstr_off.ptr;
+  T.stream_proc = ctx->d_tl_stream_proc.ptr;
+  T.dev_proc = dev_proc;
+  T.dev_pid = ctx->d_tl_devpid.ptr;
+  T.dev_pid_len = (uint32_t)devpid.size();
+  T.proc_first = ctx->d_tl_proc_first.ptr;
+  T.th_state = ctx->d_tl_th_state.ptr;
+  T.th_hi = ctx->d_tl_th_hi.ptr;
+  T.th_lo = ctx->d_tl_th_lo.ptr;
+  T.th_first = ctx->d_tl_th_first.ptr;
+  T.th_mask = th_size - 1;
+  T.th_overflow = reinterpret_cast<unsigned int*>(ctx->d_counters.ptr + C_TL_TH_OVF);
+  T.schemas = ctx->d_schemas.ptr;
+  T.sid_map = ctx->d_sid_map.ptr;
+  T.kinds = ctx->d_kinds.ptr;
+  T.max_sid = ctx->max_sid;
+  T.last_ts = global_last_ts;
+  T.lens = ctx->d_tl_lens.ptr;
+  T.offs = ctx->d_tl_offs.ptr;
+  uint64_t total = 0;
+  if (n) {
+    const uint32_t g = std::min<uint32_t>((n + 255) / 256, (uint32_t)ctx->sm_count * 16);
+    tl_meta_kernel<<<g, 256, 0, st>>>(T);
+    tl_len_kernel<<<g, 256, 0, st>>>(T);
+    tl_scan1_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr);
+    tl_scan2_kernel<<<1, kScanBlock, 0, st>>>(ctx->d_tl_bsum.ptr, nsb, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
+    tl_scan3_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr, T.offs);
+    CK(cudaGetLastError());
+    ctx->launches += 5;
+    unsigned long long tail[2] = {0, 0};
+    CK(cudaMemcpyAsync(tail, ctx->d_counters.ptr + C_TL_TOTAL, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if ((uint32_t)tail[1]) return fail(ctx, HG_ENOMEM, "timeline thread-name table overflow");
+    total = tail[0];
+  }
+  // "[" + body + "\n]"  (json.dump of a non-empty list, indent=1); "[]" when empty
+  ctx->tl_size = n ? total + 3 : 2;
+  CK(ctx->d_tl_out.ensure(ctx->tl_size + 32));
+  T.out = ctx->d_tl_out.ptr;
+  static const char open_close[4] = {'[', '\n', ']', 0};
+  if (n) {
+    CK(cudaMemcpyAsync(T.out, open_close, 1, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(T.out + 1 + total, open_close + 1, 2, cudaMemcpyHostToDevice, st));
+    const uint32_t g = std::min<uint32_t>((n + kTlWarps * 32 - 1) / (kTlWarps * 32), (uint32_t)ctx->sm_count * 8);
+    tl_write_kernel<<<g, kTlWarps * 32, 0, st>>>(T);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  } else {
+    static const char empty[2] = {'[', ']'};
+    CK(cudaMemcpyAsync(T.out, empty, 2, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaEventRecord(e1, st));
+  CK(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&ctx->tl_ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->tl_ready = true;
+  return HG_OK;
+}
 
 extern "C" {
 
@@ -1238,6 +1480,12 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_orphans.release(); ctx->d_errors.release(); ctx->d_stream_spans.release();
   ctx->d_keys.release(); ctx->d_vals.release(); ctx->d_name_len.release(); ctx->d_small.release();
   ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release(); ctx->d_warp_scratch.release();
+  ctx->d_tl_items.release();
+  for (int k = 0; k < 2; k++) { ctx->d_tl_keys[k].release(); ctx->d_tl_idx[k].release(); }
+  ctx->d_tl_lens.release(); ctx->d_tl_stream_proc.release(); ctx->d_tl_offs.release(); ctx->d_tl_bsum.release();
+  ctx->d_tl_fnq_off.release(); ctx->d_tl_sstr_off.release(); ctx->d_tl_fnq.release(); ctx->d_tl_sstr.release();
+  ctx->d_tl_out.release(); ctx->d_tl_devpid.release(); ctx->d_tl_proc_first.release(); ctx->d_tl_th_state.release();
+  ctx->d_tl_th_first.release(); ctx->d_tl_th_hi.release(); ctx->d_tl_th_lo.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1278,6 +1526,13 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
     if (h.event_class == HG_CLASS_EXIT && h.role[HG_ROLE_RESULT] >= 0) {
       d.flags |= SF_RESULT;
       if (d.role_kind[HG_ROLE_RESULT] == HG_KIND_F64) d.flags |= SF_RESULT_F64;
+      if (d.role_kind[HG_ROLE_RESULT] == HG_KIND_I64) d.flags |= SF_RESULT_I64;
+    }
+    d.track = 0xFF;  // COUNTER_TRACKS (sinks.py:309-319)
+    if (h.event_class == HG_CLASS_TELEMETRY) {
+      static const int first[4] = {0, 3, 5, 7}, count[4] = {3, 2, 2, 2};
+      if (h.counter_kind < 4 && h.counter_domain >= 0 && h.counter_domain < count[h.counter_kind])
+        d.track = (uint8_t)(first[h.counter_kind] + h.counter_domain);
     }
     // var plan
     d.nvar = 0;
@@ -1449,6 +1704,12 @@ static int ensure_scratch(hg_ctx* ctx, uint64_t n_records_bound) {
     ctx->arena_cap = 1 << 22;
   }
   (void)n_records_bound;
+  if (ctx->want & HG_WANT_TIMELINE) {
+    // every message belongs to a distinct record (truncated spans to their entry);
+    // records are at least 16 bytes
+    ctx->tl_cap = ctx->total_bytes / 16 + 64;
+    CK(ctx->d_tl_items.ensure(ctx->tl_cap));
+  }
   CK(ctx->d_pool.ensure(ctx->pool_cap));
   CK(ctx->d_stack.ensure(ctx->stack_cap));
   CK(ctx->d_orphans.ensure(ctx->orphan_cap));
@@ -1518,6 +1779,9 @@ static Params make_params(hg_ctx* ctx) {
   p.stack_scratch = ctx->d_stack.ptr;
   p.stack_used = C + C_STACK_USED;
   p.stack_cap = ctx->stack_cap;
+  p.tl_items = (ctx->want & HG_WANT_TIMELINE) ? ctx->d_tl_items.ptr : nullptr;
+  p.tl_n = C + C_TL_N;
+  p.tl_cap = ctx->tl_cap;
   return p;
 }
 
@@ -1676,7 +1940,10 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->kernel_ms = k_ms;
   ctx->total_ms = t_ms;
   ctx->have_results = true;
-  return ctx->errors.empty() ? HG_OK : HG_TRACE_ERROR;
+  ctx->tl_ready = false;
+  if (!ctx->errors.empty()) return HG_TRACE_ERROR;
+  if (ctx->want & HG_WANT_TIMELINE) return run_timeline(ctx, global_last_ts);
+  return HG_OK;
 }
 
 int hg_run(hg_ctx* ctx, uint32_t want) {
@@ -1774,14 +2041,45 @@ int hg_get_trace_errors(hg_ctx* ctx, hg_trace_error* out, uint64_t cap, uint64_t
   return HG_OK;
 }
 
+int hg_set_function_names(hg_ctx* ctx, const char* bytes, const uint64_t* offsets, const uint8_t* is_null,
+                          uint32_t n) {
+  if (!ctx || (n && !offsets)) return HG_EARG;
+  ctx->fn_names.clear();
+  ctx->fn_null.assign(n, 0);
+  for (uint32_t i = 0; i < n; i++) {
+    ctx->fn_names.emplace_back(bytes + offsets[i], bytes + offsets[i + 1]);
+    if (is_null) ctx->fn_null[i] = is_null[i];
+  }
+  ctx->have_fn_names = true;
+  return HG_OK;
+}
+
 int hg_timeline_size(hg_ctx* ctx, uint64_t* n_bytes) {
   if (!ctx || !n_bytes) return HG_EARG;
-  return fail(ctx, HG_EUNSUPPORTED, "timeline export not built yet");
+  if (!ctx->tl_ready) return fail(ctx, HG_ESTATE, "no timeline: run with HG_WANT_TIMELINE first");
+  *n_bytes = ctx->tl_size;
+  return HG_OK;
 }
 
 int hg_get_timeline(hg_ctx* ctx, char* out, uint64_t cap) {
-  (void)out; (void)cap;
-  return fail(ctx, HG_EUNSUPPORTED, "timeline export not built yet");
+  if (!ctx || !out) return HG_EARG;
+  if (!ctx->tl_ready) return fail(ctx, HG_ESTATE, "no timeline: run with HG_WANT_TIMELINE first");
+  if (cap < ctx->tl_size) return fail(ctx, HG_EARG, "timeline buffer too small");
+  cudaSetDevice(ctx->cfg.device);
+  CK(cudaMemcpy(out, ctx->d_tl_out.ptr, ctx->tl_size, cudaMemcpyDeviceToHost));
+  return HG_OK;
+}
+
+int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index) {
+  if (!ctx) return HG_EARG;
+  ctx->cfg.timeline_device_index = device_index;
+  return HG_OK;
+}
+
+int hg_timeline_ms(hg_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return HG_EARG;
+  *ms = ctx->tl_ms;
+  return HG_OK;
 }
 
 int hg_device_tally(hg_ctx* ctx, void** host_rows, uint64_t* n_host_rows) {

@@ -27,7 +27,16 @@ enum : uint8_t {
   SF_RESULT_F64 = 4,   // ... of kind f64
   SF_FEED_ALWAYS = 8,  // raises when fed (host holds the exception)
   SF_FEED_TIMELINE = 16,
+  SF_RESULT_I64 = 32,  // ... of kind i64 (else u64/address)
 };
+
+// result kind of an exit schema for the timeline's int(result) (pipeline.py:183):
+// 0 unsigned, 1 signed (absent result -> 0), 2 f64
+__host__ __device__ inline uint32_t result_kind(uint32_t fl) {
+  if (!(fl & SF_RESULT)) return 1;
+  if (fl & SF_RESULT_F64) return 2;
+  return (fl & SF_RESULT_I64) ? 1u : 0u;
+}
 
 struct DSchema {
   uint32_t kinds_off;
@@ -45,6 +54,7 @@ struct DSchema {
   uint16_t lead[5];                   // fixed bytes before var item i; lead[nvar] = trailing fixed bytes
   uint8_t role_seg[HG_NUM_ROLES];     // segment (0..nvar) holding the role field
   uint16_t role_delta[HG_NUM_ROLES];  // bytes from the segment start to the field (var field: its u32 length)
+  uint8_t track;                      // telemetry: timeline counter track (0..8), 0xFF none
 };
 constexpr uint8_t kNoPlan = 0xFF;
 
@@ -231,8 +241,25 @@ struct SumEntry {      // tile summary: pending exit or residual entry
   uint64_t ts;
   uint64_t seq;
   int32_t fn;
-  uint32_t flags;      // bit0 exit, bit1 error, bit2 bad (NaN/inf) f64 result
+  uint32_t flags;      // bit0 exit, bit1 error, bit2 bad (NaN/inf) f64 result, bit3 NaN, bits4-5 result kind
   uint64_t result;     // exit result bits (timeline)
 };
+
+// ---------------------------------------------------------------------------
+// timeline item: one message of the interval stage that TimelineSink turns into
+// a JSON object (sinks.py:363-410).  Sorted by (khi, klo) = mux order of the
+// triggering record (pipeline.py:68-114): ts, stream rank, record index; the
+// truncated spans of finish() (pipeline.py:220-240) carry klo bit 63 and sort
+// after everything, stream by stream, innermost first.
+enum : uint32_t { TL_HOST = 0, TL_DEVICE = 1, TL_SAMPLE = 2, TL_TRUNC = 1u << 8 };
+struct TlItem {
+  uint64_t khi;        // ts of the triggering record (~0 for truncated spans)
+  uint64_t klo;        // trunc << 63 | stream << 40 | record index (truncated: pop order)
+  uint64_t a;          // host: entry ts; device/sample: payload address in HBM
+  uint64_t b;          // host: result bits
+  uint32_t kind;       // TL_* | result kind << 4 (host)
+  uint32_t x;          // host: function id; device/sample: schema id
+};
+__host__ __device__ inline uint64_t tl_klo(uint32_t s, uint64_t seq) { return ((uint64_t)s << 40) | seq; }
 
 }  // namespace hg

@@ -134,6 +134,10 @@ struct Params {
   unsigned long long* stack_used;
   uint64_t stack_cap;
   uint64_t global_last_ts;
+  // timeline messages (nullptr unless HG_WANT_TIMELINE)
+  TlItem* tl_items;
+  unsigned long long* tl_n;
+  uint64_t tl_cap;
 };
 
 // compact descriptor: x = fn(20) | cls(3)<<20 | flags(8)<<23 ; y = fixed_len(16) | result field index(8)<<16 | counter(8)<<24
@@ -557,6 +561,26 @@ __device__ __noinline__ RoundOut round_resolve(GStack st, bool allow_pending, bo
   out.n_pend = st.n_pend;
   out.top = st.top;
   return out;
+}
+
+// append one timeline message per lane with `on` (warp-aggregated slot claim);
+// called by all 32 lanes
+__device__ __noinline__ void tl_emit(const Params& p, bool on, uint64_t khi, uint64_t klo, uint64_t a, uint64_t b,
+                                     uint32_t kind, uint32_t x) {
+  const uint32_t m = __ballot_sync(0xffffffffu, on);
+  if (!m) return;
+  const int leader = __ffs(m) - 1;
+  unsigned long long base = 0;
+  if ((int)lane_id() == leader) base = atomicAdd(p.tl_n, (unsigned long long)__popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (on) {
+    const unsigned long long i = base + __popc(m & lanemask_lt());
+    if (i < p.tl_cap) {
+      TlItem it;
+      it.khi = khi; it.klo = klo; it.a = a; it.b = b; it.kind = kind; it.x = x;
+      p.tl_items[i] = it;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,575 @@
+// timeline.cuh -- the Chrome-trace JSON of TimelineSink, produced on the GPU.
+//
+// Phase 1 / compose append one TlItem per interval-stage message that the
+// reference's TimelineSink turns into an object (sinks.py:363-410): host spans
+// at their exit record, device spans and telemetry samples at their record,
+// truncated spans at finish().  This file orders and prints them:
+//
+//   tl_blocksort_kernel / tl_merge_kernel   merge sort of (khi, klo) keys = mux
+//        order (pipeline.py:68-114); keys are unique, 2048-element CTA tiles,
+//        merge-path partitioned passes
+//   tl_meta_kernel    first sorted position of every metadata key
+//        (pid, tid, kind) -- TimelineSink._meta emits at first sight (sinks.py:351-359)
+//   tl_len_kernel     exact byte length of every item's JSON text (+ metas)
+//   tl_scan*          exclusive scan -> byte offsets
+//   tl_write_kernel   formats each warp's 32 consecutive items into a shared
+//        staging buffer, then stores it with aligned 16-byte writes
+//
+// The bytes equal json.dump(objects, fh, indent=1) (sinks.py:414-418): floats
+// via numfmt.cuh (CPython repr), strings JSON-escaped with ensure_ascii.
+#pragma once
+#include "kernels.cuh"
+#include "numfmt.cuh"
+
+namespace hg {
+
+struct TlTables {
+  const TlItem* items;
+  uint32_t n;
+  const uint32_t* order;          // sorted position -> item index
+  const char* fnq;                // JSON-quoted function names
+  const uint64_t* fnq_off;        // n_fn + 1
+  const char* sstr;               // per stream: pid, tid, quoted "Host {h} pid {pid}"
+  const uint64_t* sstr_off;       // 3 * n_streams + 1
+  const uint32_t* stream_proc;    // process_name meta id per stream
+  uint32_t dev_proc;              // meta id of (device_pid, 0, process_name)
+  const char* dev_pid;            // decimal device pid (9000000 + device_index)
+  uint32_t dev_pid_len;
+  unsigned int* proc_first;       // first sorted position per process meta id
+  unsigned int* th_state;         // device thread_name metas: table keyed by tid
+  unsigned long long* th_hi;
+  unsigned long long* th_lo;
+  unsigned int* th_first;
+  uint32_t th_mask;
+  unsigned int* th_overflow;
+  const DSchema* schemas;
+  const int32_t* sid_map;
+  const uint8_t* kinds;
+  uint32_t max_sid;
+  uint64_t last_ts;               // global last timestamp: end of truncated spans
+  uint32_t* lens;
+  uint64_t* offs;
+  char* out;                      // output buffer; item text starts at 1 + offs[i]
+};
+
+// ---------------------------------------------------------------------------
+// byte writer (p == nullptr: count only)
+
+struct TW {
+  char* p;
+  uint64_t n;
+  __device__ __forceinline__ void c(char ch) {
+    if (p) p[n] = ch;
+    n++;
+  }
+  __device__ __forceinline__ void s(const char* q, uint32_t l) {
+    if (p)
+      for (uint32_t i = 0; i < l; i++) p[n + i] = q[i];
+    n += l;
+  }
+  template <int N>
+  __device__ __forceinline__ void lit(const char (&q)[N]) { s(q, N - 1); }
+};
+
+__device__ __forceinline__ uint64_t ldu64(const uint8_t* q) {
+  uint64_t v = 0;
+  for (int i = 7; i >= 0; i--) v = (v << 8) | q[i];
+  return v;
+}
+__device__ __forceinline__ uint32_t ldu32(const uint8_t* q) {
+  return (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24);
+}
+
+__device__ __forceinline__ void hex4(TW& w, uint32_t v) {
+  const char* hx = "0123456789abcdef";
+  w.c('\\'); w.c('u');
+  w.c(hx[(v >> 12) & 15]); w.c(hx[(v >> 8) & 15]); w.c(hx[(v >> 4) & 15]); w.c(hx[v & 15]);
+}
+
+// json.dumps(str) with ensure_ascii of validated UTF-8 bytes (json/encoder.py ESCAPE_ASCII)
+__device__ __noinline__ void json_str(TW& w, const uint8_t* s, uint32_t len) {
+  w.c('"');
+  for (uint32_t i = 0; i < len;) {
+    uint32_t c = s[i], cp;
+    if (c < 0x80) { cp = c; i += 1; }
+    else if (c < 0xE0) { cp = ((c & 0x1F) << 6) | (s[i + 1] & 0x3F); i += 2; }
+    else if (c < 0xF0) { cp = ((c & 0x0F) << 12) | ((s[i + 1] & 0x3F) << 6) | (s[i + 2] & 0x3F); i += 3; }
+    else { cp = ((c & 0x07) << 18) | ((s[i + 1] & 0x3F) << 12) | ((s[i + 2] & 0x3F) << 6) | (s[i + 3] & 0x3F); i += 4; }
+    if (cp == '"') { w.c('\\'); w.c('"'); }
+    else if (cp == '\\') { w.c('\\'); w.c('\\'); }
+    else if (cp >= 0x20 && cp < 0x7F) w.c((char)cp);
+    else if (cp == '\n') { w.c('\\'); w.c('n'); }
+    else if (cp == '\r') { w.c('\\'); w.c('r'); }
+    else if (cp == '\t') { w.c('\\'); w.c('t'); }
+    else if (cp == '\b') { w.c('\\'); w.c('b'); }
+    else if (cp == '\f') { w.c('\\'); w.c('f'); }
+    else if (cp < 0x10000) hex4(w, cp);
+    else { const uint32_t v = cp - 0x10000; hex4(w, 0xD800 | (v >> 10)); hex4(w, 0xDC00 | (v & 0x3FF)); }
+  }
+  w.c('"');
+}
+
+// ---------------------------------------------------------------------------
+// payload fields of a device/telemetry record (already validated by phase 1)
+
+struct TlFields {
+  const uint8_t* at[HG_NUM_ROLES];
+  uint32_t len[HG_NUM_ROLES];
+};
+
+__device__ __noinline__ void tl_locate(const TlTables& T, const DSchema* sc, const uint8_t* pay, TlFields& F) {
+  for (int r = 0; r < HG_NUM_ROLES; r++) { F.at[r] = nullptr; F.len[r] = 0; }
+  uint32_t off = 0;
+  for (uint32_t f = 0; f < sc->nfields; f++) {
+    const uint8_t k = T.kinds[sc->kinds_off + f];
+    int role = -1;
+    for (int r = 0; r < HG_NUM_ROLES; r++)
+      if (sc->role[r] == (int)f) role = r;
+    if (k >= HG_KIND_STRING) {
+      const uint32_t l = ldu32(pay + off);
+      if (role >= 0) { F.at[role] = pay + off + 4; F.len[role] = l; }
+      off += 4 + l;
+    } else {
+      if (role >= 0) F.at[role] = pay + off;
+      off += 8;
+    }
+  }
+}
+
+struct I128 { int64_t hi; uint64_t lo; };
+
+// Python int of an integer field (absent -> 0, payload.get(key, 0))
+__device__ __forceinline__ I128 int_field(const TlFields& F, const DSchema* sc, int role) {
+  I128 r{0, 0};
+  if (!F.at[role]) return r;
+  r.lo = ldu64(F.at[role]);
+  r.hi = (sc->role_kind[role] == HG_KIND_I64 && (int64_t)r.lo < 0) ? -1 : 0;
+  return r;
+}
+__device__ __forceinline__ I128 add128(I128 a, I128 b) {
+  I128 r;
+  r.lo = a.lo + b.lo;
+  r.hi = a.hi + b.hi + (r.lo < a.lo ? 1 : 0);
+  return r;
+}
+__device__ __forceinline__ I128 sub128(I128 a, I128 b) {
+  I128 r;
+  r.lo = a.lo - b.lo;
+  r.hi = a.hi - b.hi - (a.lo < b.lo ? 1 : 0);
+  return r;
+}
+__device__ __forceinline__ bool eq128(I128 a, I128 b) { return a.hi == b.hi && a.lo == b.lo; }
+
+__device__ __forceinline__ void w_i128(TW& w, I128 v) {
+  char b[48];
+  w.s(b, (uint32_t)nf::fmt_i128(v.hi, v.lo, b));
+}
+__device__ __forceinline__ void w_us(TW& w, I128 ns) {  // ns / 1000.0
+  char b[40];
+  w.s(b, (uint32_t)nf::fmt_ns_div1000(ns.hi, ns.lo, b));
+}
+
+// device track id tile * 2 + engine (sinks.py:379-381)
+__device__ __forceinline__ I128 dev_tid(I128 tile, I128 engine) {
+  I128 t2;
+  t2.lo = tile.lo << 1;
+  t2.hi = (int64_t)(((uint64_t)tile.hi << 1) | (tile.lo >> 63));
+  return add128(t2, engine);
+}
+
+// thread_name meta table (keyed by tid)
+__device__ __noinline__ int th_slot(const TlTables& T, I128 tid, bool insert) {
+  uint64_t h = (tid.lo * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)tid.hi * 0xC2B2AE3D27D4EB4Full);
+  h ^= h >> 29;
+  for (uint32_t probe = 0, slot = (uint32_t)h & T.th_mask; probe <= T.th_mask; probe++, slot = (slot + 1) & T.th_mask) {
+    uint32_t st = *(volatile unsigned int*)&T.th_state[slot];
+    if (st == 0) {
+      if (!insert) return -1;
+      st = atomicCAS(&T.th_state[slot], 0u, 1u);
+      if (st == 0) {
+        T.th_hi[slot] = (unsigned long long)tid.hi;
+        T.th_lo[slot] = tid.lo;
+        __threadfence();
+        atomicExch(&T.th_state[slot], 2u);
+        return (int)slot;
+      }
+    }
+    while ((st = *(volatile unsigned int*)&T.th_state[slot]) == 1u) __nanosleep(20);
+    __threadfence();
+    if (*(volatile unsigned long long*)&T.th_hi[slot] == (unsigned long long)tid.hi &&
+        *(volatile unsigned long long*)&T.th_lo[slot] == tid.lo)
+      return (int)slot;
+  }
+  if (insert) atomicExch(T.th_overflow, 1u);
+  return -1;
+}
+
+__device__ __forceinline__ uint32_t tl_stream(uint64_t klo) { return (uint32_t)((klo >> 40) & 0x7FFFFFu); }
+
+__device__ __forceinline__ const DSchema* tl_schema(const TlTables& T, uint32_t sid) {
+  if (sid > T.max_sid) return nullptr;
+  const int32_t si = T.sid_map[sid];
+  return si < 0 ? nullptr : &T.schemas[si];
+}
+
+__device__ __forceinline__ void first_min(unsigned int* a, uint32_t i) {
+  if (*(volatile unsigned int*)a > i) atomicMin(a, i);
+}
+
+// ---------------------------------------------------------------------------
+// sort
+
+constexpr int kSortTile = 2048;
+constexpr int kSortThreads = 256;
+
+__device__ __forceinline__ bool key_lt(ulonglong2 a, ulonglong2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
+
+__global__ void __launch_bounds__(kSortThreads) tl_blocksort_kernel(const TlItem* items, uint32_t n, ulonglong2* keys,
+                                                                    uint32_t* idx) {
+  __shared__ ulonglong2 sk[kSortTile];
+  __shared__ uint32_t si[kSortTile];
+  const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+  for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    const uint64_t g = base + t;
+    if (g < n) { sk[t] = make_ulonglong2(items[g].khi, items[g].klo); si[t] = (uint32_t)g; }
+    else { sk[t] = make_ulonglong2(~0ull, ~0ull); si[t] = 0xFFFFFFFFu; }
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= (uint32_t)kSortTile; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+        const uint32_t u = t ^ j;
+        if (u > t) {
+          const bool up = (t & k) == 0;
+          const ulonglong2 a = sk[t], b = sk[u];
+          if (key_lt(b, a) == up) {
+            sk[t] = b; sk[u] = a;
+            const uint32_t x = si[t]; si[t] = si[u]; si[u] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    const uint64_t g = base + t;
+    if (g < n) { keys[g] = sk[t]; idx[g] = si[t]; }
+  }
+}
+
+// merge-path co-rank: how many of the first k merged elements come from A
+template <class F, class G>
+__device__ __forceinline__ uint64_t corank(uint64_t k, uint64_t na, uint64_t nb, F A, G B) {
+  uint64_t lo = k > nb ? k - nb : 0, hi = k < na ? k : na;
+  while (lo < hi) {
+    const uint64_t i = (lo + hi) >> 1;
+    if (key_lt(A(i), B(k - i - 1))) lo = i + 1;
+    else hi = i;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2* ki, const uint32_t* ii, ulonglong2* ko,
+                                                                uint32_t* io, uint32_t n, uint64_t width) {
+  __shared__ ulonglong2 sk[kSortTile];
+  __shared__ uint32_t si[kSortTile];
+  __shared__ uint64_t bnd[4];
+  const uint64_t out0 = (uint64_t)blockIdx.x * kSortTile;
+  if (out0 >= n) return;
+  const uint64_t pair0 = out0 / (2 * width) * (2 * width);
+  const uint64_t a0 = pair0, a1 = min((uint64_t)n, pair0 + width);
+  const uint64_t b0 = a1, b1 = min((uint64_t)n, pair0 + 2 * width);
+  const uint64_t na = a1 - a0, nb = b1 - b0;
+  const uint64_t k0 = out0 - pair0, k1 = min(k0 + kSortTile, na + nb);
+  if (threadIdx.x < 2) {
+    const uint64_t k = threadIdx.x ? k1 : k0;
+    const uint64_t i = corank(k, na, nb, [&](uint64_t x) { return ki[a0 + x]; }, [&](uint64_t x) { return ki[b0 + x]; });
+    bnd[2 * threadIdx.x] = i;
+    bnd[2 * threadIdx.x + 1] = k - i;
+  }
+  __syncthreads();
+  const uint64_t i0 = bnd[0], j0 = bnd[1], i1 = bnd[2], j1 = bnd[3];
+  const uint32_t la = (uint32_t)(i1 - i0), lb = (uint32_t)(j1 - j0);
+  for (uint32_t t = threadIdx.x; t < la + lb; t += blockDim.x) {
+    const uint64_t g = t < la ? a0 + i0 + t : b0 + j0 + (t - la);
+    sk[t] = ki[g];
+    si[t] = ii[g];
+  }
+  __syncthreads();
+  const uint32_t per = kSortTile / kSortThreads;
+  const uint32_t kk = threadIdx.x * per;
+  if (kk < la + lb) {
+    uint32_t i = (uint32_t)corank(kk, la, lb, [&](uint64_t x) { return sk[x]; }, [&](uint64_t x) { return sk[la + x]; });
+    uint32_t j = kk - i;
+    const uint32_t end = min(kk + per, la + lb);
+    for (uint32_t k = kk; k < end; k++) {
+      bool takeA = j >= lb || (i < la && key_lt(sk[i], sk[la + j]));
+      const uint32_t src = takeA ? i++ : la + j++;
+      ko[out0 + k] = sk[src];
+      io[out0 + k] = si[src];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// metadata first occurrences
+
+__global__ void tl_meta_kernel(TlTables T) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const TlItem it = T.items[T.order[i]];
+    const uint32_t kind = it.kind & 3u;
+    if (kind == TL_HOST) {
+      first_min(&T.proc_first[T.stream_proc[tl_stream(it.klo)]], (uint32_t)i);
+    } else if (kind == TL_DEVICE) {
+      first_min(&T.proc_first[T.dev_proc], (uint32_t)i);
+      const DSchema* sc = tl_schema(T, it.x);
+      TlFields F;
+      tl_locate(T, sc, reinterpret_cast<const uint8_t*>(it.a), F);
+      const int slot = th_slot(T, dev_tid(int_field(F, sc, HG_ROLE_TILE), int_field(F, sc, HG_ROLE_ENGINE)), true);
+      if (slot >= 0) first_min(&T.th_first[slot], (uint32_t)i);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// one item's JSON text: [metas] + object, each element prefixed by ",\n " ("\n " first)
+
+__device__ __forceinline__ void elem_open(TW& w, bool first) {
+  if (!first) w.c(',');
+  w.lit("\n {\n  \"name\": ");
+}
+
+__device__ __noinline__ void meta_obj(TW& w, bool first, bool thread, const char* pid, uint32_t pid_len, I128 tid,
+                                      const char* nameq, uint32_t name_len, const uint8_t* raw_name, uint32_t raw_len) {
+  elem_open(w, first);
+  if (thread) w.lit("\"thread_name\""); else w.lit("\"process_name\"");
+  w.lit(",\n  \"ph\": \"M\",\n  \"ts\": 0,\n  \"pid\": ");
+  w.s(pid, pid_len);
+  w.lit(",\n  \"tid\": ");
+  w_i128(w, tid);
+  w.lit(",\n  \"args\": {\n   \"name\": ");
+  if (raw_name) json_str(w, raw_name, raw_len);
+  else w.s(nameq, name_len);
+  w.lit("\n  }\n }");
+}
+
+__device__ __noinline__ void tl_format(const TlTables& T, uint32_t i, TW& w) {
+  const TlItem it = T.items[T.order[i]];
+  const uint32_t kind = it.kind & 3u;
+  bool first = i == 0;
+  if (kind == TL_HOST) {
+    const uint32_t s = tl_stream(it.klo);
+    const uint64_t* so = T.sstr_off + 3ull * s;
+    if (T.proc_first[T.stream_proc[s]] == i) {
+      meta_obj(w, first, false, T.sstr + so[0], (uint32_t)(so[1] - so[0]), I128{0, 0}, T.sstr + so[2],
+               (uint32_t)(so[3] - so[2]), nullptr, 0);
+      first = false;
+    }
+    const bool trunc = (it.kind & TL_TRUNC) != 0;
+    const uint64_t end = trunc ? T.last_ts : it.khi;
+    elem_open(w, first);
+    w.s(T.fnq + T.fnq_off[it.x], (uint32_t)(T.fnq_off[it.x + 1] - T.fnq_off[it.x]));
+    w.lit(",\n  \"ph\": \"X\",\n  \"ts\": ");
+    w_us(w, I128{0, it.a});
+    w.lit(",\n  \"dur\": ");
+    w_us(w, I128{0, end - it.a});
+    w.lit(",\n  \"pid\": ");
+    w.s(T.sstr + so[0], (uint32_t)(so[1] - so[0]));
+    w.lit(",\n  \"tid\": ");
+    w.s(T.sstr + so[1], (uint32_t)(so[2] - so[1]));
+    w.lit(",\n  \"args\": {\n   \"result\": ");
+    {
+      char b[400];
+      const uint32_t rk = (it.kind >> 4) & 3u;
+      int l;
+      if (rk == 2) l = nf::fmt_int_of_double(__longlong_as_double((long long)it.b), b);
+      else if (rk == 1) l = nf::fmt_i64((int64_t)it.b, b);
+      else l = nf::fmt_u64(it.b, b);
+      w.s(b, (uint32_t)l);
+    }
+    if (trunc) w.lit(",\n   \"truncated\": true");
+    w.lit("\n  }\n }");
+    return;
+  }
+  const DSchema* sc = tl_schema(T, it.x);
+  TlFields F;
+  tl_locate(T, sc, reinterpret_cast<const uint8_t*>(it.a), F);
+  if (kind == TL_DEVICE) {
+    const I128 tile = int_field(F, sc, HG_ROLE_TILE), engine = int_field(F, sc, HG_ROLE_ENGINE);
+    const I128 tid = dev_tid(tile, engine);
+    if (T.proc_first[T.dev_proc] == i) {
+      meta_obj(w, first, false, T.dev_pid, T.dev_pid_len, I128{0, 0}, "\"Device 0\"", 10, nullptr, 0);
+      first = false;
+    }
+    const int slot = th_slot(T, tid, false);
+    if (slot >= 0 && T.th_first[slot] == i) {
+      // _DEVICE_TRACK_NAMES (sinks.py:323-328)
+      const bool known = tile.hi == 0 && engine.hi == 0 && tile.lo <= 1 && engine.lo <= 1;
+      char nm[20];
+      uint32_t nl = 0;
+      if (known) {
+        const char* base = engine.lo ? "\"Tile 0 Copy\"" : "\"Tile 0 Compute\"";
+        for (; base[nl]; nl++) nm[nl] = base[nl];
+        nm[6] = (char)('0' + tile.lo);
+      } else {
+        const char* base = "\"Device\"";
+        for (; base[nl]; nl++) nm[nl] = base[nl];
+      }
+      meta_obj(w, first, true, T.dev_pid, T.dev_pid_len, tid, nm, nl, nullptr, 0);
+      first = false;
+    }
+    const I128 st = int_field(F, sc, HG_ROLE_START), en = int_field(F, sc, HG_ROLE_END);
+    elem_open(w, first);
+    json_str(w, F.at[HG_ROLE_NAME], F.len[HG_ROLE_NAME]);
+    w.lit(",\n  \"ph\": \"X\",\n  \"ts\": ");
+    w_us(w, st);
+    w.lit(",\n  \"dur\": ");
+    w_us(w, sub128(en, st));
+    w.lit(",\n  \"pid\": ");
+    w.s(T.dev_pid, T.dev_pid_len);
+    w.lit(",\n  \"tid\": ");
+    w_i128(w, tid);
+    w.lit(",\n  \"args\": {\n   \"kind\": ");
+    if (F.at[HG_ROLE_CMDKIND]) json_str(w, F.at[HG_ROLE_CMDKIND], F.len[HG_ROLE_CMDKIND]);
+    else w.lit("\"\"");
+    w.lit("\n  }\n }");
+    return;
+  }
+  // telemetry sample (sinks.py:397-410)
+  elem_open(w, first);
+  {
+    const uint32_t t = sc->track;
+    if (t < 3) w.lit("\"Power|Domain ");
+    else if (t < 5) w.lit("\"GPU Frequency|Domain ");
+    else if (t < 7) w.lit("\"Compute Engine|Tile ");
+    else w.lit("\"Copy Engine|Tile ");
+    w.c((char)('0' + (t < 3 ? t : (t - 3) & 1)));
+    w.c('"');
+  }
+  w.lit(",\n  \"ph\": \"C\",\n  \"ts\": ");
+  w_us(w, I128{0, it.khi});
+  w.lit(",\n  \"pid\": ");
+  w_i128(w, add128(I128{0, 9000000ull}, int_field(F, sc, HG_ROLE_DEVICE)));
+  w.lit(",\n  \"tid\": 0,\n  \"args\": {\n   \"value\": ");
+  {
+    char b[40];
+    const uint64_t bits = ldu64(F.at[HG_ROLE_VALUE]);
+    const uint8_t vk = sc->role_kind[HG_ROLE_VALUE];
+    int l;
+    if (vk == HG_KIND_F64) l = nf::fmt_double(__longlong_as_double((long long)bits), b);
+    else if (vk == HG_KIND_I64) l = nf::fmt_i64((int64_t)bits, b);
+    else l = nf::fmt_u64(bits, b);
+    w.s(b, (uint32_t)l);
+  }
+  w.lit("\n  }\n }");
+}
+
+__global__ void tl_len_kernel(TlTables T) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
+    TW w{nullptr, 0};
+    tl_format(T, (uint32_t)i, w);
+    T.lens[i] = (uint32_t)w.n;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan of lens -> offs (three kernels, 1024 per block)
+
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* total) {
+  __shared__ uint64_t wsum[32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t x = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t t = __shfl_up_sync(0xffffffffu, x, d);
+    if ((int)lane >= d) x += t;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t y = lane < (blockDim.x >> 5) ? wsum[lane] : 0;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t t = __shfl_up_sync(0xffffffffu, y, d);
+      if ((int)lane >= d) y += t;
+    }
+    wsum[lane] = y;
+  }
+  __syncthreads();
+  const uint64_t before = (warp ? wsum[warp - 1] : 0) + x - v;
+  if (total) *total = wsum[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return before;
+}
+
+__global__ void __launch_bounds__(kScanBlock) tl_scan1_kernel(const uint32_t* lens, uint32_t n, uint64_t* bsum) {
+  const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+  uint64_t tot;
+  block_excl_scan(i < n ? lens[i] : 0, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanBlock) tl_scan2_kernel(uint64_t* bsum, uint32_t nb, uint64_t* grand) {
+  uint64_t carry = 0;
+  for (uint32_t b0 = 0; b0 < nb; b0 += kScanBlock) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint64_t v = b < nb ? bsum[b] : 0;
+    uint64_t tot;
+    const uint64_t ex = block_excl_scan(v, &tot);
+    if (b < nb) bsum[b] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *grand = carry;
+}
+
+__global__ void __launch_bounds__(kScanBlock) tl_scan3_kernel(const uint32_t* lens, uint32_t n, const uint64_t* bsum,
+                                                              uint64_t* offs) {
+  const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
+  const uint64_t ex = block_excl_scan(i < n ? lens[i] : 0, nullptr);
+  if (i < n) offs[i] = bsum[blockIdx.x] + ex;
+}
+
+// ---------------------------------------------------------------------------
+// writer: a warp formats 32 consecutive items into shared memory, then stores
+// the contiguous range with aligned 16-byte writes
+
+constexpr int kTlWarps = 8;
+constexpr int kTlStage = 5120;
+
+__global__ void __launch_bounds__(kTlWarps * 32) tl_write_kernel(TlTables T) {
+  __shared__ __align__(16) char stage[kTlWarps][kTlStage + 32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  char* buf = stage[warp];
+  for (uint64_t base = ((uint64_t)blockIdx.x * kTlWarps + warp) * 32; base < T.n;
+       base += (uint64_t)gridDim.x * kTlWarps * 32) {
+    const uint64_t i = base + lane;
+    const bool on = i < T.n;
+    const uint64_t off = on ? 1 + T.offs[i] : 0;
+    const uint64_t len = on ? T.lens[i] : 0;
+    const uint32_t last = (uint32_t)(min((uint64_t)T.n, base + 32) - 1 - base);
+    const uint64_t o0 = __shfl_sync(0xffffffffu, off, 0);
+    const uint64_t oend = __shfl_sync(0xffffffffu, off + len, last);
+    const uint64_t al = o0 & ~15ull;
+    const uint64_t total = oend - al;
+    if (total <= (uint64_t)kTlStage) {
+      if (on) {
+        TW w{buf + (off - al), 0};
+        tl_format(T, (uint32_t)i, w);
+      }
+      __syncwarp();
+      const uint32_t nch = (uint32_t)((total + 15) / 16);
+      for (uint32_t c = lane; c < nch; c += 32) {
+        const uint64_t g0 = al + 16ull * c;
+        const uint64_t lo = g0 > o0 ? g0 : o0, hi = g0 + 16 < oend ? g0 + 16 : oend;
+        if (lo == g0 && hi == g0 + 16) *reinterpret_cast<uint4*>(T.out + g0) = *reinterpret_cast<const uint4*>(buf + 16 * c);
+        else for (uint64_t b = lo; b < hi; b++) T.out[b] = buf[b - al];
+      }
+      __syncwarp();
+    } else if (on) {
+      TW w{T.out + off, 0};
+      tl_format(T, (uint32_t)i, w);
+    }
+  }
+}
+
+}  // namespace hg

@@ -81,6 +81,16 @@ class Engine:
         flat = flatten_registry(registry)
         self._check(self._L.hg_set_registry(self._ctx, flat.schemas, flat.n_schemas, flat.kinds, len(flat.kinds),
                                             len(flat.function_names)), "hg_set_registry")
+        names = [("" if n is None else str(n)).encode("utf-8") for n in flat.function_names]
+        offs = [0]
+        for b in names:
+            offs.append(offs[-1] + len(b))
+        blob = b"".join(names)
+        null = bytes(1 if n is None else 0 for n in flat.function_names)
+        n = len(names)
+        self._check(self._L.hg_set_function_names(
+            self._ctx, C.c_char_p(blob) if blob else None, (C.c_uint64 * (n + 1))(*offs),
+            C.c_char_p(null) if null else None, n), "hg_set_function_names")
         self._flat = flat
         self._registry_key = registry
         return flat
@@ -172,6 +182,11 @@ class Engine:
         self._check(self._L.hg_get_trace_errors(self._ctx, arr, n.value, C.byref(n)), "hg_get_trace_errors")
         return list(arr)[: n.value]
 
+    def timeline_ms(self) -> float:
+        ms = C.c_float()
+        self._check(self._L.hg_timeline_ms(self._ctx, C.byref(ms)), "hg_timeline_ms")
+        return ms.value
+
     def timeline_bytes(self) -> bytes:
         n = C.c_uint64()
         self._check(self._L.hg_timeline_size(self._ctx, C.byref(n)), "hg_timeline_size")
@@ -181,8 +196,9 @@ class Engine:
 
     # -- the drop-in
     def run(self, raw_streams, registry, stream_infos=None, want_timeline=False, labels=None,
-            orphan_labels=None) -> RunResult:
+            orphan_labels=None, timeline_device_index=0) -> RunResult:
         flat = self.set_registry(registry)
+        self._check(self._L.hg_set_timeline_device(self._ctx, int(timeline_device_index)), "hg_set_timeline_device")
         self.set_streams(raw_streams)
         want = HG_WANT_TALLY | (HG_WANT_TIMELINE if want_timeline else 0)
         rc = self.run_raw(want)

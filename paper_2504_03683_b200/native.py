@@ -74,7 +74,10 @@ def lib():
         "hg_get_stream_spans": ([vp, vp, u64], C.c_int),
         "hg_get_orphans": ([vp, vp, u64, vp], C.c_int),
         "hg_get_trace_errors": ([vp, vp, u64, vp], C.c_int),
+        "hg_set_function_names": ([vp, vp, vp, vp, u32], C.c_int),
         "hg_timeline_size": ([vp, vp], C.c_int),
+        "hg_timeline_ms": ([vp, vp], C.c_int),
+        "hg_set_timeline_device": ([vp, i32], C.c_int),
         "hg_get_timeline": ([vp, vp, u64], C.c_int),
         "hg_device_tally": ([vp, vp, vp], C.c_int),
         "hg_last_timing": ([vp, vp, vp, vp, vp, vp], C.c_int),
@@ -93,5 +96,6 @@ EXPORTED = (
     "hg_abi_version", "hg_last_error", "hg_create", "hg_destroy", "hg_set_registry", "hg_add_stream",
     "hg_clear_streams", "hg_stage", "hg_run", "hg_run_local", "hg_local_last_ts", "hg_finish", "hg_get_stats",
     "hg_get_tally", "hg_get_device_names", "hg_get_stream_spans", "hg_get_orphans", "hg_get_trace_errors",
-    "hg_timeline_size", "hg_get_timeline", "hg_device_tally", "hg_last_timing",
+    "hg_timeline_size", "hg_get_timeline", "hg_device_tally", "hg_last_timing", "hg_set_function_names",
+    "hg_timeline_ms", "hg_set_timeline_device",
 )

@@ -246,7 +246,8 @@ def run_pipeline(source, sinks=(), registry=None, engine=None) -> PipelineResult
     eng = engine or default_engine()
     labels = [r.name for r in raws]
     olabels = [f"{r.hostname}/{r.pid}/{r.tid}" for r in raws]
-    res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels, orphan_labels=olabels)
+    res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels, orphan_labels=olabels,
+                  timeline_device_index=next(iter(device_index), 0))
     for s in sinks:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
         hook = getattr(s, "on_diagnostics", None)
         if hook is not None:

@@ -1,7 +1,7 @@
 """GPU vs CPU oracle on seeded synthetic traces of every SURVEY.md §8(d) configuration shape.
 
-Bit-exact comparison of the TallyReport, IntervalStats and the ordered orphan
-list.  Sizes are chosen so the oracle finishes in seconds; the full-size
+Bit-exact comparison of the TallyReport, IntervalStats, the ordered orphan
+list and the timeline JSON bytes.  Sizes are chosen so the oracle finishes in seconds; the full-size
 workloads are exercised by bench.py with size-independent checks."""
 
 import pytest
@@ -18,14 +18,15 @@ def engine():
     eng.close()
 
 
-def _cmp(engine, wl):
+def _cmp(engine, wl, timeline=True):
+    """Report, stats, orphans and (tally + timeline run) the timeline JSON bytes."""
     from oracle import oracle
     from paper_2504_03683_b200 import synth
 
     raws = synth.generate(wl)
     infos = [r.info for r in raws]
-    got = engine.run(raws, wl.registry, infos)
-    want = oracle.run(raws, wl.registry, infos)
+    got = engine.run(raws, wl.registry, infos, want_timeline=timeline)
+    want = oracle.run(raws, wl.registry, infos, want_timeline=timeline)
     assert (got.error is None) == (want.error is None), (got.error, want.error)
     if want.error is not None:
         assert type(got.error) is type(want.error) and str(got.error) == str(want.error)
@@ -33,6 +34,8 @@ def _cmp(engine, wl):
     assert got.stats == want.stats
     assert got.report == want.report
     assert got.orphans == want.orphans
+    if timeline:
+        assert got.timeline == want.timeline.encode()
     return got
 
 
