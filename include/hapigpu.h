@@ -196,6 +196,8 @@ int hg_set_function_names(hg_ctx* ctx, const char* bytes, const uint64_t* offset
 int hg_timeline_size(hg_ctx* ctx, uint64_t* n_bytes);
 int hg_get_timeline(hg_ctx* ctx, char* out, uint64_t cap);
 int hg_timeline_ms(hg_ctx* ctx, float* ms);  /* device time of the ordering + formatting */
+/* phase-1 kernel times of the last run (segment walk, chain, decode), CUDA events */
+int hg_phase_timing(hg_ctx* ctx, float* walk_ms, float* chain_ms, float* decode_ms);
 /* TimelineSink(device_index=) (sinks.py:347-349): device pid 9000000 + index */
 int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index);
 

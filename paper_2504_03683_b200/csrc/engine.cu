@@ -21,6 +21,7 @@
 
 #include "kernels.cuh"
 #include "timeline.cuh"
+#include "seg.cuh"
 
 using namespace hg;
 
@@ -1151,7 +1152,7 @@ struct hg_ctx {
   hg_config cfg{};
   std::string err;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[6] = {};  // 0 run start, 1 after staging, 2 after compose, 3 results on host, 4/5 tile kernel
+  cudaEvent_t ev[8] = {};  // 0 run start, 1 after staging, 2 after compose, 3 results on host, 4/5 phase 1, 6 after walk, 7 after chain
   int sm_count = 0;
   // registry
   std::vector<DSchema> schemas;
@@ -1225,6 +1226,15 @@ struct hg_ctx {
   uint64_t tl_size = 0;
   bool tl_ready = false;
   float tl_ms = 0;
+  uint64_t tl_comp_base = 0;
+  float walk_ms = 0, chain_ms = 0, decode_ms = 0;
+  // segments
+  uint32_t seg_bytes = 8192;
+  DBuf<SegW> d_segw;
+  DBuf<SegInfo> d_seginfo;
+  DBuf<unsigned long long> d_stream_nrec, d_tl_rec_off;
+  DBuf<SumEntry> d_deep;
+  uint64_t deep_cap = 0;
 };
 
 // counter slots in d_counters
@@ -1244,7 +1254,10 @@ enum {
   C_TL_N = 19,            // timeline messages appended
   C_TL_TOTAL = 20,        // timeline body bytes (scan total)
   C_TL_TH_OVF = 21,       // unsigned int: thread-name table overflow
-  C_NUM = 22
+  C_DEEP_USED = 22,       // deep lane-stack chunks handed out
+  C_TL_N2 = 23,           // timeline messages appended by compose
+  C_REC_TOTAL = 24,       // records of all streams (timeline slots)
+  C_NUM = 25
 };
 
 static int fail(hg_ctx* c, int code, const std::string& msg) {
@@ -1301,8 +1314,11 @@ static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   if (!ctx->have_fn_names || ctx->fn_names.size() != ctx->n_fn)
     return fail(ctx, HG_ESTATE, "hg_set_function_names is required for the timeline");
   const unsigned long long* C = ctx->counters.data();
-  if (C[C_TL_N] > ctx->tl_cap) return fail(ctx, HG_ENOMEM, "timeline message buffer overflow (engine bug)");
-  const uint32_t n = (uint32_t)C[C_TL_N];
+  const uint64_t n_slots = ctx->tl_comp_base + C[C_TL_N2];
+  if (n_slots > ctx->tl_cap || n_slots >= (1ull << 32))
+    return fail(ctx, HG_ENOMEM, "timeline message buffer overflow");
+  const uint32_t n = (uint32_t)(C[C_TL_N] + C[C_TL_N2]);  // messages; the sort moves the empty slots last
+  const uint32_t N = (uint32_t)n_slots;
   const uint32_t ns = (uint32_t)ctx->streams.size();
   cudaStream_t st = ctx->stream;
   cudaEvent_t e0, e1;
@@ -1346,19 +1362,19 @@ static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   CK(upload(ctx->d_tl_stream_proc, sproc, st));
   CK(upload(ctx->d_tl_devpid, devpid, st));
   // sort by mux key
-  const uint32_t nblk = (n + kSortTile - 1) / kSortTile;
+  const uint32_t nblk = (N + kSortTile - 1) / kSortTile;
   for (int k = 0; k < 2; k++) {
-    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
-    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(N, 1)));
+    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(N, 1)));
   }
   int cur = 0;
-  if (n) {
-    tl_blocksort_kernel<<<nblk, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, n, ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr);
+  if (N) {
+    tl_blocksort_kernel<<<nblk, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, N, ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr);
     CK(cudaGetLastError());
     ctx->launches++;
-    for (uint64_t width = kSortTile; width < n; width *= 2) {
+    for (uint64_t width = kSortTile; width < N; width *= 2) {
       tl_merge_kernel<<<nblk, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
-                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr, n, width);
+                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr, N, width);
       CK(cudaGetLastError());
       ctx->launches++;
       cur ^= 1;
@@ -1457,6 +1473,7 @@ int hg_create(const hg_config* cfg, hg_ctx** out) {
   if (!out) return HG_EARG;
   hg_ctx* ctx = new hg_ctx();
   if (cfg) ctx->cfg = *cfg;
+  if (ctx->cfg.tile_bytes) ctx->seg_bytes = std::max<uint32_t>(256, ctx->cfg.tile_bytes);
   *out = ctx;
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -1486,6 +1503,8 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_tl_fnq_off.release(); ctx->d_tl_sstr_off.release(); ctx->d_tl_fnq.release(); ctx->d_tl_sstr.release();
   ctx->d_tl_out.release(); ctx->d_tl_devpid.release(); ctx->d_tl_proc_first.release(); ctx->d_tl_th_state.release();
   ctx->d_tl_th_first.release(); ctx->d_tl_th_hi.release(); ctx->d_tl_th_lo.release();
+  ctx->d_segw.release(); ctx->d_seginfo.release(); ctx->d_stream_nrec.release(); ctx->d_tl_rec_off.release();
+  ctx->d_deep.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1571,7 +1590,12 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
     const DSchema& d = ctx->schemas[ctx->sid_map[schemas[i].id]];
     uint32_t fn = d.fn < 0 ? 0xFFFFFu : (uint32_t)d.fn;
     uint32_t flags = d.flags & 0x7Fu;
+    // result field index (its byte offset / 8); for variable schemas only when every field
+    // before it is fixed-size (the segment decoder then reads it without a field walk)
     uint32_t resf = (d.flags & SF_RESULT) ? (uint32_t)d.role[HG_ROLE_RESULT] : 0xFFu;
+    if ((d.flags & SF_VAR) && (d.flags & SF_RESULT) && !(d.nvar != kNoPlan && d.role_seg[HG_ROLE_RESULT] == 0 &&
+                                                         d.role_delta[HG_ROLE_RESULT] == 8u * resf))
+      resf = 0xFFu;
     ctx->desc[schemas[i].id] = make_uint2((fn & 0xFFFFFu) | ((uint32_t)d.cls << 20) | (flags << 23) | D_PRESENT,
                                           (uint32_t)d.fixed_len | ((resf & 0xFFu) << 16) | ((uint32_t)d.counter_kind << 24));
   }
@@ -1628,7 +1652,7 @@ static int build_layout(hg_ctx* ctx) {
   for (uint32_t s = 0; s < ns; s++) {
     ctx->stream_tile0[s] = (uint32_t)ctx->tile_stream.size();
     uint64_t sz = ctx->sizes[s];
-    uint32_t nt = sz > 16 ? (uint32_t)((sz - 16 + kTile - 1) / kTile) : 0;
+    uint32_t nt = sz > 16 ? (uint32_t)((sz - 16 + ctx->seg_bytes - 1) / ctx->seg_bytes) : 0;
     ntiles[s] = nt;
     maxt = std::max(maxt, nt);
     for (uint32_t t = 0; t < nt; t++) ctx->tile_stream.push_back(s);
@@ -1704,12 +1728,12 @@ static int ensure_scratch(hg_ctx* ctx, uint64_t n_records_bound) {
     ctx->arena_cap = 1 << 22;
   }
   (void)n_records_bound;
-  if (ctx->want & HG_WANT_TIMELINE) {
-    // every message belongs to a distinct record (truncated spans to their entry);
-    // records are at least 16 bytes
-    ctx->tl_cap = ctx->total_bytes / 16 + 64;
-    CK(ctx->d_tl_items.ensure(ctx->tl_cap));
-  }
+  if (ctx->deep_cap == 0) ctx->deep_cap = 1 << 20;
+  CK(ctx->d_deep.ensure(ctx->deep_cap));
+  CK(ctx->d_segw.ensure(std::max<size_t>(nt, 1)));
+  CK(ctx->d_seginfo.ensure(std::max<size_t>(nt, 1)));
+  CK(ctx->d_stream_nrec.ensure(std::max<uint32_t>(ns, 1)));
+  CK(ctx->d_tl_rec_off.ensure(std::max<uint32_t>(ns, 1)));
   CK(ctx->d_pool.ensure(ctx->pool_cap));
   CK(ctx->d_stack.ensure(ctx->stack_cap));
   CK(ctx->d_orphans.ensure(ctx->orphan_cap));
@@ -1781,7 +1805,14 @@ static Params make_params(hg_ctx* ctx) {
   p.stack_cap = ctx->stack_cap;
   p.tl_items = (ctx->want & HG_WANT_TIMELINE) ? ctx->d_tl_items.ptr : nullptr;
   p.tl_n = C + C_TL_N;
+  p.tl_n2 = C + C_TL_N2;
+  p.tl_comp_base = ctx->tl_comp_base;
   p.tl_cap = ctx->tl_cap;
+  p.tl_rec_off = ctx->d_tl_rec_off.ptr;
+  p.seg_bytes = ctx->seg_bytes;
+  p.deep = ctx->d_deep.ptr;
+  p.deep_used = C + C_DEEP_USED;
+  p.deep_cap = ctx->deep_cap;
   return p;
 }
 
@@ -1803,17 +1834,36 @@ static int launch_phase1(hg_ctx* ctx) {
   ctx->launches = 1;
   if (nt) {
     Params p = make_params(ctx);
-    size_t smem = tile_smem_bytes(ctx->n_fn);
-    CK(cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile_kernel, kCtaThreads, smem));
-    if (per_sm < 1) return fail(ctx, HG_ECUDA, "tile kernel does not fit on an SM");
-    uint32_t grid = std::min<uint32_t>((uint32_t)(per_sm * ctx->sm_count), (nt + kWarpsPerCta - 1) / kWarpsPerCta);
-    grid = std::max<uint32_t>(grid, 1);
-    CK(ctx->d_warp_scratch.ensure((size_t)grid * kWarpsPerCta * kMaxRecTile));
-    p.warp_scratch = ctx->d_warp_scratch.ptr;
+    const size_t dsm = sizeof(uint2) * kSdescMax;
     CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-    tile_kernel<<<grid, kCtaThreads, smem, ctx->stream>>>(p, ctx->d_done.ptr);
+    const uint32_t gw = std::min<uint32_t>((nt + 255) / 256, (uint32_t)ctx->sm_count * 8);
+    seg_walk_kernel<<<gw, 256, dsm, ctx->stream>>>(p, ctx->d_segw.ptr);
+    CK(cudaEventRecord(ctx->ev[6], ctx->stream));
+    seg_chain_kernel<<<(ns + 3) / 4, 128, dsm, ctx->stream>>>(p, ctx->d_segw.ptr, ctx->d_seginfo.ptr, ctx->d_stream_nrec.ptr);
+    CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+    CK(cudaGetLastError());
+    ctx->launches += 2;
+    if (ctx->want & HG_WANT_TIMELINE) {
+      // timeline slots: one per record (segment decode), then compose's messages
+      seg_rec_off_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_stream_nrec.ptr, ns, ctx->d_tl_rec_off.ptr,
+                                                      ctx->d_counters.ptr + C_REC_TOTAL);
+      ctx->launches++;
+      unsigned long long total = 0;
+      CK(cudaMemcpyAsync(&total, ctx->d_counters.ptr + C_REC_TOTAL, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      ctx->tl_comp_base = total;
+      ctx->tl_cap = 2 * total + 64;  // compose adds at most one message per summary entry
+      CK(ctx->d_tl_items.ensure(ctx->tl_cap));
+      p = make_params(ctx);
+    }
+    const size_t smem = seg_smem_layout(ctx->n_fn).total;
+    CK(cudaFuncSetAttribute(seg_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_decode_kernel, kSegThreads, smem));
+    if (per_sm < 1) return fail(ctx, HG_ECUDA, "segment kernel does not fit on an SM");
+    uint32_t grid = std::min<uint32_t>((uint32_t)(per_sm * ctx->sm_count), (nt + kSegThreads - 1) / kSegThreads);
+    grid = std::max<uint32_t>(grid, 1);
+    seg_decode_kernel<<<grid, kSegThreads, smem, ctx->stream>>>(p, ctx->d_seginfo.ptr);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[5], ctx->stream));
     ctx->launches++;
@@ -1854,6 +1904,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     unsigned long long* C = ctx->counters.data();
     if (C[C_POOL_USED] > ctx->pool_cap) { ctx->pool_cap = C[C_POOL_USED] + (C[C_POOL_USED] >> 2); ctx->stack_cap = ctx->pool_cap; grow = true; }
     if (C[C_N_ORPHANS] > ctx->orphan_cap) { ctx->orphan_cap = C[C_N_ORPHANS] * 2; grow = true; }
+    if (C[C_DEEP_USED] > ctx->deep_cap) { ctx->deep_cap = C[C_DEEP_USED] * 2; grow = true; }
     if ((uint32_t)C[C_N_ERRORS] > ctx->error_cap) { ctx->error_cap = (uint32_t)C[C_N_ERRORS] * 2; grow = true; }
     if ((uint32_t)C[C_OVERFLOW]) {
       ctx->row_cap *= 4; ctx->dict_mask = ctx->dict_mask * 4 + 3; ctx->arena_cap = std::max<uint64_t>(ctx->arena_cap * 4, C[C_ARENA_USED] * 2);
@@ -1935,7 +1986,12 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->d2h_bytes += ctx->host_acc.size() * 8 + ctx->dev_acc.size() * 8 + arena_used + n_orph * sizeof(hg_orphan) +
                     n_err * sizeof(hg_trace_error) + ns * 8 + ctx->n_dev_rows * 12;
   float k_ms = 0, t_ms = 0;
-  if (!ctx->tile_stream.empty()) cudaEventElapsedTime(&k_ms, ctx->ev[4], ctx->ev[5]);
+  if (!ctx->tile_stream.empty()) {
+    cudaEventElapsedTime(&k_ms, ctx->ev[4], ctx->ev[5]);
+    cudaEventElapsedTime(&ctx->walk_ms, ctx->ev[4], ctx->ev[6]);
+    cudaEventElapsedTime(&ctx->chain_ms, ctx->ev[6], ctx->ev[7]);
+    cudaEventElapsedTime(&ctx->decode_ms, ctx->ev[7], ctx->ev[5]);
+  }
   cudaEventElapsedTime(&t_ms, ctx->ev[0], ctx->ev[3]);
   ctx->kernel_ms = k_ms;
   ctx->total_ms = t_ms;
@@ -2067,6 +2123,14 @@ int hg_get_timeline(hg_ctx* ctx, char* out, uint64_t cap) {
   if (cap < ctx->tl_size) return fail(ctx, HG_EARG, "timeline buffer too small");
   cudaSetDevice(ctx->cfg.device);
   CK(cudaMemcpy(out, ctx->d_tl_out.ptr, ctx->tl_size, cudaMemcpyDeviceToHost));
+  return HG_OK;
+}
+
+int hg_phase_timing(hg_ctx* ctx, float* walk_ms, float* chain_ms, float* decode_ms) {
+  if (!ctx) return HG_EARG;
+  if (walk_ms) *walk_ms = ctx->walk_ms;
+  if (chain_ms) *chain_ms = ctx->chain_ms;
+  if (decode_ms) *decode_ms = ctx->decode_ms;
   return HG_OK;
 }
 

@@ -134,10 +134,19 @@ struct Params {
   unsigned long long* stack_used;
   uint64_t stack_cap;
   uint64_t global_last_ts;
-  // timeline messages (nullptr unless HG_WANT_TIMELINE)
+  // timeline messages (nullptr unless HG_WANT_TIMELINE): slots [0, tl_comp_base) are
+  // indexed by global record number (segment decode), compose appends after them
   TlItem* tl_items;
-  unsigned long long* tl_n;
+  unsigned long long* tl_n;        // messages written by the segment decode
+  unsigned long long* tl_n2;       // messages appended by compose
+  uint64_t tl_comp_base;
   uint64_t tl_cap;
+  const unsigned long long* tl_rec_off;  // per stream: global record number of its first record
+  // segments
+  uint32_t seg_bytes;
+  SumEntry* deep;                  // per-lane automaton chunks of deep segments
+  unsigned long long* deep_used;
+  uint64_t deep_cap;
 };
 
 // compact descriptor: x = fn(20) | cls(3)<<20 | flags(8)<<23 ; y = fixed_len(16) | result field index(8)<<16 | counter(8)<<24
@@ -571,10 +580,10 @@ __device__ __noinline__ void tl_emit(const Params& p, bool on, uint64_t khi, uin
   if (!m) return;
   const int leader = __ffs(m) - 1;
   unsigned long long base = 0;
-  if ((int)lane_id() == leader) base = atomicAdd(p.tl_n, (unsigned long long)__popc(m));
+  if ((int)lane_id() == leader) base = atomicAdd(p.tl_n2, (unsigned long long)__popc(m));
   base = __shfl_sync(0xffffffffu, base, leader);
   if (on) {
-    const unsigned long long i = base + __popc(m & lanemask_lt());
+    const unsigned long long i = p.tl_comp_base + base + __popc(m & lanemask_lt());
     if (i < p.tl_cap) {
       TlItem it;
       it.khi = khi; it.klo = klo; it.a = a; it.b = b; it.kind = kind; it.x = x;

@@ -40,10 +40,10 @@ class RunResult:
 class Engine:
     """A GPU pipeline context bound to one CUDA device."""
 
-    def __init__(self, device: int = 0, timeline_device_index: int = 0):
+    def __init__(self, device: int = 0, timeline_device_index: int = 0, seg_bytes: int = 0):
         self._L = native.lib()
         self._ctx = C.c_void_p()
-        cfg = HgConfig(device=device, tile_bytes=0, flags=0, timeline_device_index=timeline_device_index)
+        cfg = HgConfig(device=device, tile_bytes=seg_bytes, flags=0, timeline_device_index=timeline_device_index)
         rc = self._L.hg_create(C.byref(cfg), C.byref(self._ctx))
         if rc != HG_OK:
             msg = self._L.hg_last_error(self._ctx).decode() if self._ctx else "hg_create failed"
@@ -181,6 +181,12 @@ class Engine:
         arr = (HgTraceError * max(n.value, 1))()
         self._check(self._L.hg_get_trace_errors(self._ctx, arr, n.value, C.byref(n)), "hg_get_trace_errors")
         return list(arr)[: n.value]
+
+    def phase_timing(self):
+        """(walk, chain, decode) device ms of the last run's phase 1."""
+        a, b, c = C.c_float(), C.c_float(), C.c_float()
+        self._check(self._L.hg_phase_timing(self._ctx, C.byref(a), C.byref(b), C.byref(c)), "hg_phase_timing")
+        return a.value, b.value, c.value
 
     def timeline_ms(self) -> float:
         ms = C.c_float()
