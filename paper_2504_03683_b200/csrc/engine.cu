@@ -1235,6 +1235,7 @@ struct hg_ctx {
   DBuf<unsigned long long> d_stream_nrec, d_tl_rec_off;
   DBuf<SumEntry> d_deep;
   uint64_t deep_cap = 0;
+  DBuf<Params> d_params;
 };
 
 // counter slots in d_counters
@@ -1504,7 +1505,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_tl_out.release(); ctx->d_tl_devpid.release(); ctx->d_tl_proc_first.release(); ctx->d_tl_th_state.release();
   ctx->d_tl_th_first.release(); ctx->d_tl_th_hi.release(); ctx->d_tl_th_lo.release();
   ctx->d_segw.release(); ctx->d_seginfo.release(); ctx->d_stream_nrec.release(); ctx->d_tl_rec_off.release();
-  ctx->d_deep.release();
+  ctx->d_deep.release(); ctx->d_params.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -1863,7 +1864,9 @@ static int launch_phase1(hg_ctx* ctx) {
     if (per_sm < 1) return fail(ctx, HG_ECUDA, "segment kernel does not fit on an SM");
     uint32_t grid = std::min<uint32_t>((uint32_t)(per_sm * ctx->sm_count), (nt + kSegThreads - 1) / kSegThreads);
     grid = std::max<uint32_t>(grid, 1);
-    seg_decode_kernel<<<grid, kSegThreads, smem, ctx->stream>>>(p, ctx->d_seginfo.ptr);
+    CK(ctx->d_params.ensure(1));
+    CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
+    seg_decode_kernel<<<grid, kSegThreads, smem, ctx->stream>>>(p, ctx->d_seginfo.ptr, ctx->d_params.ptr);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev[5], ctx->stream));
     ctx->launches++;

@@ -369,7 +369,7 @@ __device__ __forceinline__ uint32_t* seg_lanetab(const SegSmem& L) {
 }
 
 // move the lane's automaton state to a global chunk (capacity: the segment's record count)
-__device__ __noinline__ bool go_deep(const Params& p, LaneStack& S, uint64_t base, uint32_t cap) {
+__device__ __forceinline__ bool go_deep(const Params& p, LaneStack& S, uint64_t base, uint32_t cap) {
   const unsigned long long off = atomicAdd(p.deep_used, (unsigned long long)cap);
   if (off + cap > p.deep_cap) return false;  // the host grows the pool and reruns
   SumEntry* d = p.deep + off;
@@ -503,18 +503,21 @@ __device__ __forceinline__ bool g_var_plan(const DSchema* sc, const uint8_t* g, 
 // generic walk).  role_ptr: field data (var fields: first byte after the length);
 // role_len: var field lengths.
 __device__ __noinline__ uint32_t seg_fields(const Params& p, const uint8_t* g, uint64_t size, uint64_t a, uint32_t sid,
-                                           uint32_t plen, uint64_t* role_ptr, uint32_t* role_len, uint64_t& aux) {
+                                           uint32_t plen, uint64_t* role_ptr, uint32_t* role_len, uint64_t& aux,
+                                           bool roles) {
   const uint2 d = desc_of(p, sid);
   const DSchema* sc = schema_of(p, sid);
   const uint64_t body = a + 16;
   for (int r = 0; r < HG_NUM_ROLES; r++) { role_ptr[r] = 0; role_len[r] = 0; }
   if (!(d_flags(d) & SF_VAR)) {
+    if (!roles) return 0;
     for (int r = 0; r < HG_NUM_ROLES; r++)
       if (sc->role[r] >= 0) role_ptr[r] = body + 8u * (uint32_t)sc->role[r];
     return 0;
   }
   uint32_t seg[5];
   if (g_var_plan(sc, g, body, plen, seg)) {
+    if (!roles) return 0;
     for (int r = 0; r < HG_NUM_ROLES; r++) {
       if (sc->role[r] < 0) continue;
       const uint64_t at = body + seg_sel(seg, sc->role_seg[r]) + sc->role_delta[r];
@@ -534,7 +537,7 @@ __device__ __noinline__ uint32_t seg_fields(const Params& p, const uint8_t* g, u
 }
 
 // device-profiling record (pipeline.py:186-202): duration into its name's row
-__device__ __noinline__ uint32_t seg_device(const Params& p, const SegSmem& L, const uint8_t* g, uint64_t size,
+__device__ __noinline__ uint32_t seg_device(const Params& p, const SegSmem L, const uint8_t* g, uint64_t size,
                                            uint32_t sid, const uint64_t* rp, const uint32_t* rl, uint64_t& aux) {
   const uint2 d = desc_of(p, sid);
   if (d_flags(d) & SF_FEED_ALWAYS) { aux = sid; return HG_ERR_FEED; }
@@ -608,7 +611,8 @@ __device__ __forceinline__ void seg_status(const Params& p, uint32_t g, uint32_t
 }
 
 // drain n deferred records, one per lane
-__device__ __noinline__ void seg_drain(const Params& p, const SegSmem& L, uint32_t n, SegCounters& K) {
+__device__ __noinline__ uint4 seg_drain(const Params& p, const SegSmem L, uint32_t n) {
+  uint4 K = make_uint4(0, 0, 0, 0);  // device spans, samples, timeline messages
   const SegQ Q = seg_queue(L);
   const uint32_t lane = lane_id();
   if (lane < n) {
@@ -624,7 +628,8 @@ __device__ __noinline__ void seg_drain(const Params& p, const SegSmem& L, uint32
     uint64_t rp[HG_NUM_ROLES];
     uint32_t rl[HG_NUM_ROLES];
     uint64_t aux = 0;
-    uint32_t err = seg_fields(p, gb, size, a, h.sid, h.plen, rp, rl, aux);
+    uint32_t err = seg_fields(p, gb, size, a, h.sid, h.plen, rp, rl, aux,
+                              cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY);
     bool feed = false;
     if (!err && order_bad) err = HG_ERR_ORDER;
     if (!err && !order_bad) {
@@ -637,16 +642,17 @@ __device__ __noinline__ void seg_drain(const Params& p, const SegSmem& L, uint32
       seg_status(p, g, TS_ERROR);
     } else if (cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY) {
       const bool dev = cls == HG_CLASS_DEVICE;
-      if (dev) { K.dev++; atomicAdd(&p.stream_spans[s], 1ull); }
-      else K.samples++;
+      if (dev) { K.x++; atomicAdd(&p.stream_spans[s], 1ull); }
+      else K.y++;
       if (p.tl_items) {
         seg_item(p, p.tl_rec_off[s] + seq, h.ts, tl_klo(s, seq), (uint64_t)(gb + a + 16), 0, dev ? TL_DEVICE : TL_SAMPLE,
                  h.sid);
-        K.items++;
+        K.z++;
       }
     }
   }
   __syncwarp();
+  return K;
 }
 
 // open the lane's next live segment at or after g (dead ones are closed on the way)
@@ -675,7 +681,7 @@ __device__ __forceinline__ bool seg_begin(const Params& p, const SegInfo* info, 
 }
 
 // segment summary for compose_kernel: pending exits, then open entries bottom..top
-__device__ __noinline__ void seg_end(const Params& p, LaneSeg& C, LaneStack& S) {
+__device__ __forceinline__ void seg_end(const Params& p, LaneSeg& C, LaneStack& S) {
   const uint32_t sum_n = S.np + S.ne;
   const unsigned long long poff = sum_n ? atomicAdd(p.pool_used, (unsigned long long)sum_n) : 0ull;
   TileState* st = &p.state[C.g];
@@ -716,11 +722,11 @@ __device__ __noinline__ uint64_t var_result_off(const Params& p, const uint8_t* 
   uint64_t rp[HG_NUM_ROLES];
   uint32_t rl[HG_NUM_ROLES];
   uint64_t aux = 0;
-  if (seg_fields(p, g, size, a, sid, plen, rp, rl, aux)) return kNone;  // invalid payload: the drain reports it
+  if (seg_fields(p, g, size, a, sid, plen, rp, rl, aux, true)) return kNone;  // invalid payload: the drain reports it
   return rp[HG_ROLE_RESULT];
 }
 
-__device__ __noinline__ void seg_prologue(const Params& p, const SegSmem& L) {
+__device__ __noinline__ void seg_prologue(const Params& p, const SegSmem L) {
   const uint32_t lane = lane_id();
   if (p.max_sid < (uint32_t)kSdescMax) {
     uint2* t = reinterpret_cast<uint2*>(g_smem);
@@ -748,7 +754,7 @@ __device__ __noinline__ void seg_prologue(const Params& p, const SegSmem& L) {
   __syncthreads();
 }
 
-__device__ __noinline__ void seg_epilogue(const Params& p, const SegSmem& L, const SegCounters K) {
+__device__ __noinline__ void seg_epilogue(const Params& p, const SegSmem L, const SegCounters K) {
   const uint32_t lane = lane_id();
   auto wsum = [](uint32_t v) { return __reduce_add_sync(0xffffffffu, v); };
   const uint32_t a0 = wsum(K.events), a1 = wsum(K.passed), a2 = wsum(K.host), a3 = wsum(K.dev), a4 = wsum(K.samples),
@@ -932,9 +938,12 @@ __device__ __forceinline__ bool seg_record_full(const Params& p, LaneSeg& C, Lan
   return defer;
 }
 
-__global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, const SegInfo* info) {
+__global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, const SegInfo* info, const Params* gp) {
+  // noinline helpers read the parameters from a global copy: taking the address of the
+  // kernel parameter block would move every hot-loop parameter read to local memory
+  const Params& gpr = *gp;
   const SegSmem L = seg_smem_layout(p.n_fn);
-  seg_prologue(p, L);
+  seg_prologue(gpr, L);
   const uint32_t lane = lane_id();
   SegCounters K;
   K.events = K.passed = K.host = K.dev = K.samples = K.orph = K.items = 0;
@@ -987,6 +996,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
       const uint32_t k = C.k++;
       C.o = a + 16 + h.plen;
       C.nh = g_hdr(C.gbase, C.o);  // next header in flight while this record is handled
+      if (((C.o + 256) ^ (a + 256)) >> 7)  // entering a new 128-byte line: pull the one two lines ahead into L1
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(C.gbase + C.o + 256));
       K.events++;
       K.last_ts = h.ts > K.last_ts ? h.ts : K.last_ts;
       C.prev_ts = h.ts;
@@ -1015,7 +1026,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
           if (du < *(volatile uint32_t*)&hf.lt.mn[fnm]) atomicMin(&hf.lt.mn[fnm], du);
           if (du > *(volatile uint32_t*)&hf.lt.mx[fnm]) atomicMax(&hf.lt.mx[fnm], du);
         } else {
-          hf.fold(p, (int32_t)fnm, dur, err);
+          hf.fold(gpr, (int32_t)fnm, dur, err);
         }
         K.host++;
         C.spans++;
@@ -1032,7 +1043,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
     }
     const bool slow = act && !fast;
     if (__any_sync(0xffffffffu, slow)) {
-      if (slow) defer = seg_record_full(p, C, S, K, hf, tl, q_off, q_prev, order_bad);
+      if (slow) defer = seg_record_full(gpr, C, S, K, hf, tl, q_off, q_prev, order_bad);
     }
     const bool ending = have && !act;
     if (__any_sync(0xffffffffu, ending)) {
@@ -1051,7 +1062,8 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
       qn += __popc(qm);
       __syncwarp();
       if (qn >= (uint32_t)kWarp) {
-        seg_drain(p, L, kWarp, K);
+        const uint4 dk = seg_drain(gpr, L, kWarp);
+        K.dev += dk.x; K.samples += dk.y; K.items += dk.z;
         qn -= kWarp;
         if (lane < qn) {
           Q.off[lane] = Q.off[kWarp + lane]; Q.seq[lane] = Q.seq[kWarp + lane]; Q.prev[lane] = Q.prev[kWarp + lane];
@@ -1062,8 +1074,11 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
     }
   }
   (void)nn;
-  if (qn) seg_drain(p, L, qn, K);
-  seg_epilogue(p, L, K);
+  if (qn) {
+    const uint4 dk = seg_drain(gpr, L, qn);
+    K.dev += dk.x; K.samples += dk.y; K.items += dk.z;
+  }
+  seg_epilogue(gpr, L, K);
 }
 
 // exclusive scan of per-stream record totals -> timeline slot offset of each stream
