@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(128) seg_chain_kernel(Params p, SegW* segw, Se
 // telemetry records -- is queued per warp and drained 32 at a time with every
 // lane active, so one lane's long record does not stall the other 31.
 
-constexpr int kSQ = 64;  // deferred records per warp
+constexpr int kSQ = 64;            // deferred records per warp
+constexpr int kSegNameSlots = 256; // CTA cache of device-name hashes
 
 struct SegSmem {
   uint32_t tab, lanetab, lanetab_warp, dcache, ncache, warps, warp_bytes, total;
@@ -302,7 +303,7 @@ __host__ __device__ inline SegSmem seg_smem_layout(uint32_t n_fn) {
   L.dcache = off;
   off += (uint32_t)((sizeof(DevRow) * kDevSlots + 127) & ~(size_t)127);
   L.ncache = off;
-  off += (uint32_t)((sizeof(NameSlot) * kNameSlots + 127) & ~(size_t)127);
+  off += (uint32_t)((sizeof(NameSlot) * kSegNameSlots + 127) & ~(size_t)127);
   L.warps = off;
   // per warp: open-entry stack [kLS][32] (ts 8, meta 4, seq 4), pending exits [kLP][32]
   // (ts 8, result 8, meta 4, seq 4), deferred queue [kSQ] (off 8, seq 8, prev 8, s 4, g 4)
@@ -474,6 +475,42 @@ __device__ __forceinline__ bool g_name_equal(const NameDict& d, uint32_t row, co
   return true;
 }
 
+// device-name dictionary lookup/insert (same layout, hash and probing as name_lookup)
+__device__ __noinline__ uint32_t g_name_lookup(const NameDict& d, const uint8_t* g, uint64_t o, uint32_t n, uint64_t h) {
+  for (uint64_t slot = h & d.mask, probes = 0; probes <= d.mask; slot = (slot + 1) & d.mask, probes++) {
+    const unsigned long long k = atomicCAS(&d.keys[slot], 0ull, (unsigned long long)h);
+    if (k == 0ull) {
+      const uint32_t row = atomicAdd(d.n_rows, 1u);
+      const unsigned long long off = atomicAdd(d.arena_used, (unsigned long long)((n + 3u) & ~3u));
+      if (row >= d.row_cap || off + n > d.arena_cap) {
+        atomicExch(d.overflow, 1u);
+        atomicExch(&d.vals[slot], 0xffffffffu);
+        return 0xffffffffu;
+      }
+      uint32_t* dst = reinterpret_cast<uint32_t*>(d.arena + off);
+      for (uint32_t i = 0; i < n; i += 4) {
+        uint32_t wv = g32(g, o + i);
+        if (n - i < 4) wv &= 0xffffffffu >> (8 * (4 - (n - i)));
+        dst[i >> 2] = wv;
+      }
+      d.name_off[row] = off;
+      d.name_len[row] = n;
+      __threadfence();
+      atomicExch(&d.vals[slot], row + 1);
+      return row;
+    }
+    if (k == h) {
+      uint32_t v;
+      while ((v = *(volatile uint32_t*)&d.vals[slot]) == 0) __nanosleep(32);
+      if (v == 0xffffffffu) return 0xffffffffu;
+      __threadfence();
+      if (g_name_equal(d, v - 1, g, o, n)) return v - 1;
+    }
+  }
+  atomicExch(d.overflow, 1u);
+  return 0xffffffffu;
+}
+
 // variable payload through the schema's plan, reading HBM (tracefile.py:152-169);
 // false -> the generic walk decides (and names the exact error)
 __device__ __forceinline__ bool g_var_plan(const DSchema* sc, const uint8_t* g, uint64_t body, uint32_t plen,
@@ -504,28 +541,29 @@ __device__ __forceinline__ bool g_var_plan(const DSchema* sc, const uint8_t* g, 
 // role_len: var field lengths.
 __device__ __noinline__ uint32_t seg_fields(const Params& p, const uint8_t* g, uint64_t size, uint64_t a, uint32_t sid,
                                            uint32_t plen, uint64_t* role_ptr, uint32_t* role_len, uint64_t& aux,
-                                           bool roles) {
+                                           uint32_t roles) {
+  // roles: bit mask of the HG_ROLE_* fields wanted (their schemas have them)
   const uint2 d = desc_of(p, sid);
   const DSchema* sc = schema_of(p, sid);
   const uint64_t body = a + 16;
-  for (int r = 0; r < HG_NUM_ROLES; r++) { role_ptr[r] = 0; role_len[r] = 0; }
   if (!(d_flags(d) & SF_VAR)) {
-    if (!roles) return 0;
-    for (int r = 0; r < HG_NUM_ROLES; r++)
-      if (sc->role[r] >= 0) role_ptr[r] = body + 8u * (uint32_t)sc->role[r];
+    for (uint32_t m = roles; m; m &= m - 1) {
+      const int r = __ffs(m) - 1;
+      role_ptr[r] = body + 8u * (uint32_t)sc->role[r];
+    }
     return 0;
   }
   uint32_t seg[5];
   if (g_var_plan(sc, g, body, plen, seg)) {
-    if (!roles) return 0;
-    for (int r = 0; r < HG_NUM_ROLES; r++) {
-      if (sc->role[r] < 0) continue;
+    for (uint32_t m = roles; m; m &= m - 1) {
+      const int r = __ffs(m) - 1;
       const uint64_t at = body + seg_sel(seg, sc->role_seg[r]) + sc->role_delta[r];
       if (sc->role_kind[r] >= HG_KIND_STRING) { role_len[r] = g32(g, at); role_ptr[r] = at + 4; }
       else role_ptr[r] = at;
     }
     return 0;
   }
+  for (int r = 0; r < HG_NUM_ROLES; r++) { role_ptr[r] = 0; role_len[r] = 0; }
   Window w;
   w.s = nullptr; w.win_start = 0; w.win_end = 0; w.g = g; w.size = size;
   uint32_t name_len = 0;
@@ -552,15 +590,14 @@ __device__ __noinline__ uint32_t seg_device(const Params& p, const SegSmem L, co
   DevRow* dcache = reinterpret_cast<DevRow*>(g_smem + L.dcache);
   NameSlot* ncache = reinterpret_cast<NameSlot*>(g_smem + L.ncache);
   const uint64_t h = g_hash(g, no, nl);
-  NameSlot* slot = &ncache[h % kNameSlots];
+  NameSlot* slot = &ncache[h % kSegNameSlots];
   const unsigned long long ch = *(volatile unsigned long long*)&slot->hash;
   const uint32_t cr = *(volatile uint32_t*)&slot->row;
   uint32_t row = 0xffffffffu;
   if (ch == h && cr < *(volatile uint32_t*)p.names.n_rows && g_name_equal(p.names, cr, g, no, nl)) row = cr;
   if (row == 0xffffffffu) {
-    Window w;
-    w.s = nullptr; w.win_start = 0; w.win_end = 0; w.g = g; w.size = size;
-    row = name_lookup(p.names, w, no, nl);
+    (void)size;
+    row = g_name_lookup(p.names, g, no, nl, h);
     if (row != 0xffffffffu) { slot->row = row; __threadfence_block(); slot->hash = h; }
   }
   if (row != 0xffffffffu) fold_device(p, dcache, row, d_lo, d_hi);
@@ -628,8 +665,13 @@ __device__ __noinline__ uint4 seg_drain(const Params& p, const SegSmem L, uint32
     uint64_t rp[HG_NUM_ROLES];
     uint32_t rl[HG_NUM_ROLES];
     uint64_t aux = 0;
-    uint32_t err = seg_fields(p, gb, size, a, h.sid, h.plen, rp, rl, aux,
-                              cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY);
+    uint32_t err = 0;
+    const uint32_t roles = cls == HG_CLASS_DEVICE ? ((1u << HG_ROLE_START) | (1u << HG_ROLE_END) | (1u << HG_ROLE_NAME))
+                           : cls == HG_CLASS_TELEMETRY ? (1u << HG_ROLE_VALUE) : 0u;
+    const bool feed_always = (d_flags(d) & SF_FEED_ALWAYS) != 0;  // role fields may be missing
+    uint32_t segs[5];
+    if (roles || !g_var_plan(schema_of(p, h.sid), gb, a + 16, h.plen, segs))  // validation only: the plan suffices
+      err = seg_fields(p, gb, size, a, h.sid, h.plen, rp, rl, aux, feed_always ? 0u : roles);
     bool feed = false;
     if (!err && order_bad) err = HG_ERR_ORDER;
     if (!err && !order_bad) {
@@ -722,7 +764,7 @@ __device__ __noinline__ uint64_t var_result_off(const Params& p, const uint8_t* 
   uint64_t rp[HG_NUM_ROLES];
   uint32_t rl[HG_NUM_ROLES];
   uint64_t aux = 0;
-  if (seg_fields(p, g, size, a, sid, plen, rp, rl, aux, true)) return kNone;  // invalid payload: the drain reports it
+  if (seg_fields(p, g, size, a, sid, plen, rp, rl, aux, 1u << HG_ROLE_RESULT)) return kNone;  // invalid payload: the drain reports it
   return rp[HG_ROLE_RESULT];
 }
 
@@ -750,7 +792,7 @@ __device__ __noinline__ void seg_prologue(const Params& p, const SegSmem L) {
     dcache[i] = z;
   }
   NameSlot* ncache = reinterpret_cast<NameSlot*>(g_smem + L.ncache);
-  for (uint32_t i = threadIdx.x; i < kNameSlots; i += blockDim.x) { ncache[i].hash = 0; ncache[i].row = 0; }
+  for (uint32_t i = threadIdx.x; i < kSegNameSlots; i += blockDim.x) { ncache[i].hash = 0; ncache[i].row = 0; }
   __syncthreads();
 }
 
@@ -998,6 +1040,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
       C.nh = g_hdr(C.gbase, C.o);  // next header in flight while this record is handled
       if (((C.o + 256) ^ (a + 256)) >> 7)  // entering a new 128-byte line: pull the one two lines ahead into L1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(C.gbase + C.o + 256));
+
       K.events++;
       K.last_ts = h.ts > K.last_ts ? h.ts : K.last_ts;
       C.prev_ts = h.ts;
