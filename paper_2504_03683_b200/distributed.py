@@ -127,7 +127,9 @@ class ShardedRun:
         if rc not in (0, 1):
             eng._check(rc, "hg_finish")
         k, tot, h2d, d2h, nl = eng.timing()
-        return {"device_ms": tot, "tile_ms": k, "h2d_bytes": h2d, "d2h_bytes": d2h, "launches": nl, "rc": rc}
+        walk, chain, decode = eng.phase_timing()
+        return {"device_ms": tot, "phase1_ms": k, "walk_ms": walk, "chain_ms": chain, "decode_ms": decode,
+                "h2d_bytes": h2d, "d2h_bytes": d2h, "launches": nl, "rc": rc}
 
     def report(self, stream_infos) -> TallyReport:
         eng = self.engine
