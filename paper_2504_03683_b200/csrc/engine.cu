@@ -9,7 +9,8 @@
 //   device spans, telemetry samples   pipeline.py:186-215, sampler.py:36-48
 //   truncation at the global last ts  pipeline.py:152, 220-240
 //   tally fold                        sinks.py:123-132, 230-242
-// Kernel design: see kernels.cuh.
+// Kernel design: phase 1 in seg.cuh (segment walk / chain / decode), composition
+// here, timeline ordering and formatting in timeline.cuh.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -27,944 +28,8 @@ using namespace hg;
 
 namespace {
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* m) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(m)));
-}
-__device__ __forceinline__ void bulk_load(uint32_t* dst, const void* src, uint32_t bytes, unsigned long long* m) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(m)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(m)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* m, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(done) : "r"(smem_addr(m)), "r"(parity) : "memory");
-  }
-}
-
-__host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~(size_t)127; }
-
-__host__ __device__ inline size_t lane_tab_bytes(uint32_t n_fn) { return ((size_t)3 * n_fn * kWarp + 3 * n_fn) * 4; }
-
-struct SmemLayout {
-  size_t tab, lanetab, dcache, ncache, sdesc, warps, total;
-};
-__host__ __device__ inline SmemLayout smem_layout(uint32_t n_fn) {
-  SmemLayout L{};
-  size_t off = align128(sizeof(uint2) * kSdescMax);  // compact descriptors at offset 0 (desc_of)
-  bool small = n_fn <= kSmallF;
-  L.tab = off;
-  if (!small && n_fn <= kSmemFnMax) off += align128(sizeof(SmemRow) * n_fn);
-  L.lanetab = off;
-  if (small) off += align128(lane_tab_bytes(n_fn) * kWarpsPerCta);
-  L.dcache = off;
-  off += align128(sizeof(DevRow) * kDevSlots);
-  L.ncache = off;
-  off += align128(sizeof(NameSlot) * kNameSlots);
-  L.sdesc = 0;
-  L.warps = off;
-  off += sizeof(WarpSmem) * kWarpsPerCta;
-  L.total = off;
-  return L;
-}
-
-constexpr uint32_t SD_PRESENT = 0x80000000u, SD_VAR = 0x40000000u;
-
-// schema screening entry: present | var | fixed payload length (var: minimum)
-__device__ __forceinline__ uint32_t sdesc_lookup(const Params& p, const uint32_t* sdesc, uint32_t sid) {
-  (void)sdesc;
-  const uint2 d = desc_of(p, sid);
-  return d_present(d) ? (SD_PRESENT | ((d_flags(d) & SF_VAR) ? SD_VAR : 0u) | d_fixed(d)) : 0u;
-}
-
-// the record after a screened candidate must be a plausible header too, not earlier in time
-__device__ __forceinline__ bool second_header_ok(const Params& p, const uint32_t* win, uint64_t t0, uint64_t size,
-                                                 uint32_t win_len, const uint32_t* sdesc, uint32_t o) {
-  const uint32_t plen = s32(win, o + 12);
-  if (t0 + o + 16 + plen > size) return false;
-  const uint32_t n = o + 16 + plen;
-  if (t0 + n == size) return true;
-  if (n + 16 > win_len) return false;
-  const uint32_t sid2 = s32(win, n);
-  const uint32_t plen2 = s32(win, n + 12);
-  const uint32_t e = sid2 <= p.max_sid ? sdesc_lookup(p, sdesc, sid2) : 0u;
-  if (!(e & SD_PRESENT)) return false;
-  if ((e & SD_VAR) ? plen2 < (e & 0xFFFFu) : plen2 != (e & 0xFFFFu)) return false;
-  if (t0 + n + 16 + plen2 > size) return false;
-  return s64(win, n + 4) >= s64(win, o + 4);
-}
-
-__device__ __forceinline__ uint32_t warp_smem_off(uint32_t n_fn) {
-  return (uint32_t)(smem_layout(n_fn).warps + sizeof(WarpSmem) * (threadIdx.x >> 5));
-}
-__device__ __forceinline__ WarpSmem* warp_smem(uint32_t n_fn) {
-  return reinterpret_cast<WarpSmem*>(g_smem + warp_smem_off(n_fn));
-}
-__device__ __forceinline__ DevRow* sm_dcache(uint32_t n_fn) {
-  return reinterpret_cast<DevRow*>(g_smem + smem_layout(n_fn).dcache);
-}
-__device__ __forceinline__ NameSlot* sm_ncache(uint32_t n_fn) {
-  return reinterpret_cast<NameSlot*>(g_smem + smem_layout(n_fn).ncache);
-}
-__device__ __forceinline__ const uint32_t* sm_sdesc(const Params& p) {
-  return p.max_sid < (uint32_t)kSdescMax ? reinterpret_cast<const uint32_t*>(g_smem + smem_layout(p.n_fn).sdesc)
-                                         : nullptr;
-}
-__device__ __forceinline__ SmemRow* sm_tab(uint32_t n_fn) {
-  return (n_fn > kSmallF && n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(g_smem + smem_layout(n_fn).tab) : nullptr;
-}
-// per-lane host columns of this warp: [3][n_fn][32] then err/mn/mx [3][n_fn]
-__device__ __forceinline__ uint32_t* sm_lanetab(uint32_t n_fn) {
-  return reinterpret_cast<uint32_t*>(g_smem + smem_layout(n_fn).lanetab + lane_tab_bytes(n_fn) * (threadIdx.x >> 5));
-}
-
-struct TileGeom {
-  uint32_t g, s, g0, j;
-  uint64_t size, t0, t1;
-  const uint8_t* gbase;
-  uint32_t nbytes;  // staged bytes
-};
-
-__device__ __forceinline__ TileGeom geom(const Params& p, uint32_t work) {
-  TileGeom G;
-  G.g = p.order[work];
-  G.s = p.tile_stream[G.g];
-  G.g0 = p.stream_tile0[G.s];
-  G.j = G.g - G.g0;
-  G.size = p.stream_size[G.s];
-  G.gbase = p.data + p.stream_base[G.s];
-  G.t0 = 16 + (uint64_t)G.j * kTile;
-  G.t1 = min(G.t0 + (uint64_t)kTile, G.size);
-  uint64_t padded = (G.size + 15) & ~(uint64_t)15;
-  G.nbytes = (uint32_t)min((uint64_t)kWinBytes, padded - G.t0);
-  return G;
-}
-
 // ---------------------------------------------------------------------------
-// the tile kernel
-
-// one decoded record (lockstep round)
-struct Rec {
-  int32_t x;        // +1 entry, -1 exit, 0 other / inactive
-  uint32_t meta;    // packed meta (fn, flags, tile record index)
-  uint64_t ts;
-  uint64_t res;     // exit result bits
-};
-
-struct Seg { uint32_t s[5]; };
-
-// rare_record result: x = feed error, y = bit0 device span, bit1 sample; z/w = feed aux (lo/hi)
-using RareOut = uint4;
-
-// role field offset of a validated record (fixed: field index; planned var: segment + delta)
-__device__ __forceinline__ uint64_t role_at(const DSchema* sc, uint64_t a, uint32_t fl, bool planned, const Seg& seg,
-                                            int r) {
-  if (!(fl & SF_VAR)) return a + 16 + 8u * (uint32_t)sc->role[r];
-  return a + 16 + seg_sel(seg.s, sc->role_seg[r]) + sc->role_delta[r];
-}
-
-// device-profiling record (pipeline.py:186-202): duration into its name's row
-__device__ __noinline__ RareOut device_record(const Params& p, Window w, uint64_t t0, uint32_t win_len, uint32_t o,
-                                              uint32_t sid, uint32_t plen, bool planned, Seg seg) {
-  RareOut out = make_uint4(0, 0, 0, 0);
-  const uint32_t* win = warp_smem(p.n_fn)->win;
-  DevRow* dcache = sm_dcache(p.n_fn);
-  NameSlot* ncache = sm_ncache(p.n_fn);
-  const uint64_t a = t0 + o;
-  const uint2 d = desc_of(p, sid);
-  const uint32_t fl = d_flags(d);
-  if (fl & SF_FEED_ALWAYS) { out.x = HG_ERR_FEED; out.z = sid; return out; }
-  const DSchema* sc = schema_of(p, sid);
-  uint64_t o_start, o_end, no;
-  uint32_t name_len = 0;
-  if ((fl & SF_VAR) && !planned) {
-    uint64_t role_off[HG_NUM_ROLES];
-    for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
-    uint64_t aux;
-    walk_fields(p, d, sid, a + 16, plen, [&](uint64_t x) { return rd32(w, x); }, w, role_off, name_len, aux);
-    o_start = role_off[HG_ROLE_START]; o_end = role_off[HG_ROLE_END]; no = role_off[HG_ROLE_NAME];
-  } else {
-    o_start = role_at(sc, a, fl, planned, seg, HG_ROLE_START);
-    o_end = role_at(sc, a, fl, planned, seg, HG_ROLE_END);
-    no = role_at(sc, a, fl, planned, seg, HG_ROLE_NAME);
-    name_len = rd32(w, no);
-    no += 4;
-  }
-  const uint64_t ua = rd64(w, o_start), ub = rd64(w, o_end);
-  const int64_t ah = (sc->role_kind[HG_ROLE_START] == HG_KIND_I64 && (int64_t)ua < 0) ? -1 : 0;
-  const int64_t bh = (sc->role_kind[HG_ROLE_END] == HG_KIND_I64 && (int64_t)ub < 0) ? -1 : 0;
-  const uint64_t d_lo = ub - ua;
-  const int64_t d_hi = bh - ah - (ub < ua ? 1 : 0);
-  uint32_t row = 0xffffffffu;
-  const bool inwin = no + name_len + 8 <= t0 + win_len;
-  const uint32_t nw = (uint32_t)(no - t0);
-  const uint64_t h = inwin ? hash_window(win, nw, name_len) : hash_bytes(w, no, name_len);
-  NameSlot* slot = &ncache[h % kNameSlots];
-  const unsigned long long ch = *(volatile unsigned long long*)&slot->hash;
-  const uint32_t cr = *(volatile uint32_t*)&slot->row;
-  if (ch == h && cr < *(volatile uint32_t*)p.names.n_rows &&
-      (inwin ? name_equal_window(p.names, cr, win, nw, name_len) : name_equal(p.names, cr, w, no, name_len)))
-    row = cr;
-  if (row == 0xffffffffu) {
-    row = name_lookup(p.names, w, no, name_len);
-    if (row != 0xffffffffu) { slot->row = row; __threadfence_block(); slot->hash = h; }
-  }
-  if (row != 0xffffffffu) fold_device(p, dcache, row, d_lo, d_hi);
-  out.y = 1;
-  return out;
-}
-
-// telemetry sample (pipeline.py:203-215; sampler.py:44-48 range checks)
-__device__ __noinline__ RareOut telemetry_record(const Params& p, Window w, uint64_t t0, uint32_t o, uint32_t sid,
-                                                 uint32_t plen, bool planned, Seg seg) {
-  RareOut out = make_uint4(0, 0, 0, 0);
-  const uint64_t a = t0 + o;
-  const uint2 d = desc_of(p, sid);
-  const uint32_t fl = d_flags(d);
-  if (fl & SF_FEED_ALWAYS) { out.x = HG_ERR_FEED; out.z = sid; return out; }
-  const DSchema* sc = schema_of(p, sid);
-  uint64_t va;
-  if ((fl & SF_VAR) && !planned) {
-    uint64_t role_off[HG_NUM_ROLES];
-    for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
-    uint64_t aux;
-    uint32_t nl = 0;
-    walk_fields(p, d, sid, a + 16, plen, [&](uint64_t x) { return rd32(w, x); }, w, role_off, nl, aux);
-    va = role_off[HG_ROLE_VALUE];
-  } else {
-    va = role_at(sc, a, fl, planned, seg, HG_ROLE_VALUE);
-  }
-  const uint64_t bits = rd64(w, va);
-  const uint8_t vk = sc->role_kind[HG_ROLE_VALUE];
-  const bool util = sc->counter_kind >= HG_COUNTER_COMPUTE;
-  bool bad;
-  if (vk == HG_KIND_F64) {
-    const double v = __longlong_as_double((long long)bits);
-    bad = util ? !(v >= 0.0 && v <= 1.0) : (v < 0.0);
-  } else if (vk == HG_KIND_I64) {
-    const int64_t v = (int64_t)bits;
-    bad = util ? !(v >= 0 && v <= 1) : (v < 0);
-  } else {
-    bad = util ? (bits > 1) : false;
-  }
-  if (bad) { out.x = HG_ERR_TELEMETRY; out.z = (uint32_t)bits; out.w = (uint32_t)(bits >> 32); return out; }
-  out.y = 2;
-  if ((fl & SF_FEED_TIMELINE) && (p.want & HG_WANT_TIMELINE)) { out.x = HG_ERR_FEED; out.z = sid; }
-  return out;
-}
-
-// generic payload validation for records the plan does not cover (or that leave the window)
-__device__ __noinline__ uint32_t generic_payload(const Params& p, const Window& w, uint64_t a, uint32_t sid,
-                                                 uint32_t plen, uint64_t& result_off, uint64_t& aux) {
-  const uint2 d = desc_of(p, sid);
-  uint64_t role_off[HG_NUM_ROLES];
-  for (int r = 0; r < HG_NUM_ROLES; r++) role_off[r] = 0;
-  uint32_t name_len = 0;
-  uint32_t e = walk_fields(p, d, sid, a + 16, plen, [&](uint64_t x) { return rd32(w, x); }, w, role_off, name_len, aux);
-  result_off = role_off[HG_ROLE_RESULT];
-  return e;
-}
-
-__device__ __noinline__ uint64_t rd64_far(Window w, uint64_t off) { return rd64(w, off); }
-
-// result field of a variable-payload exit whose result follows a string/blob (rare:
-// registries put `result` first); validates the payload on the way
-__device__ __noinline__ uint32_t var_exit_result(const Params& p, const uint32_t* win, Window w, uint64_t t0,
-                                                 uint32_t win_len, uint32_t o, uint32_t sid, uint32_t plen,
-                                                 uint64_t* result_off, uint64_t* aux) {
-  const DSchema* sc = schema_of(p, sid);
-  const uint64_t a = t0 + o;
-  uint32_t seg[5];
-  if (o + 16 + plen <= win_len && var_plan(sc, win, w, o + 16, plen, seg)) {
-    *result_off = a + 16 + seg_sel(seg, sc->role_seg[HG_ROLE_RESULT]) + sc->role_delta[HG_ROLE_RESULT];
-    return 0;
-  }
-  return generic_payload(p, w, a, sid, plen, *result_off, *aux);
-}
-
-// hot per-record decode: header, descriptor, fixed-length check, class, exit result.
-// Payload validation of variable records and all device/telemetry work is deferred
-// (returns true) to the warp queue, drained with every lane active.
-__device__ __forceinline__ bool decode_one_rec(const Params& p, const uint32_t* win, const Window& w, uint64_t t0,
-                                               uint32_t win_len, uint32_t o, uint32_t rec, Rec& R,
-                                               uint32_t& dec_err, uint64_t& dec_aux, uint32_t& st_passed) {
-  const uint32_t sid = s32(win, o);
-  const uint32_t plen = s32(win, o + 12);
-  R.ts = s64(win, o + 4);
-  R.x = 0;
-  R.res = 0;
-  const uint2 d = desc_of(p, sid);
-  const uint32_t cls = d_cls(d), fl = d_flags(d);
-  R.meta = (d.x & M_FN) | (rec << 23);
-  const bool var = (fl & SF_VAR) != 0;
-  if (!var && plen != d_fixed(d)) { dec_err = HG_ERR_LEN_MISMATCH; return false; }
-  if (cls == HG_CLASS_ENTRY) {
-    R.x = 1;
-    return var;
-  }
-  if (cls == HG_CLASS_EXIT) {
-    R.x = -1;
-    R.meta |= M_EXIT;
-    if (fl & SF_RESULT) {
-      const uint64_t a = t0 + o;
-      uint64_t result_off = a + 16 + 8u * d_resfield(d);  // fixed: field index * 8
-      if (var) {
-        // y carries (role_seg<<8 | role_delta>>...) only for fixed schemas; read the plan for var ones
-        const DSchema* sc = schema_of(p, sid);
-        if (sc->role_seg[HG_ROLE_RESULT] == 0 && sc->nvar != kNoPlan) {
-          result_off = a + 16 + sc->role_delta[HG_ROLE_RESULT];
-          if (result_off + 8 > a + 16 + plen) {  // malformed: let the generic walk name the error
-            uint32_t e = var_exit_result(p, win, w, t0, win_len, o, sid, plen, &result_off, &dec_aux);
-            if (e) { dec_err = e; return false; }
-          }
-        } else {
-          uint32_t e = var_exit_result(p, win, w, t0, win_len, o, sid, plen, &result_off, &dec_aux);
-          if (e) { dec_err = e; return false; }
-        }
-      }
-      const uint64_t bits = (result_off + 12 <= t0 + win_len) ? s64(win, (uint32_t)(result_off - t0)) : rd64_far(w, result_off);
-      R.res = bits;
-      if (fl & SF_RESULT_F64) {
-        const double xv = __longlong_as_double((long long)bits);
-        if (isnan(xv)) R.meta |= M_BAD | M_NAN;
-        else if (isinf(xv)) R.meta |= M_BAD;
-        else if (xv >= 1.0 || xv <= -1.0) R.meta |= M_ERR;
-      } else if (bits) {
-        R.meta |= M_ERR;
-      }
-    }
-    return var;
-  }
-  if (cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY) return true;
-  st_passed++;
-  return var;
-}
-
-// drain up to 32 deferred records, one per lane: payload validation (tracefile.py:152-169)
-// and device/telemetry handling (pipeline.py:186-215)
-__device__ __noinline__ uint4 drain_queue(const Params& p, Window w, uint64_t t0, uint32_t win_len, uint32_t s,
-                                          uint64_t base, uint32_t n) {
-  WarpSmem* ws = warp_smem(p.n_fn);
-  const uint32_t lane = lane_id();
-  const uint32_t* win = ws->win;
-  uint32_t dev = 0, samples = 0;
-  uint32_t sid = 0, rec = 0;
-  uint64_t a = 0;
-  if (lane < n) {
-    const uint32_t e = ws->q[lane];
-    const uint32_t o = e & 0xFFFFu;
-    rec = e >> 16;
-    a = t0 + o;
-    sid = s32(win, o);
-    const uint32_t plen = s32(win, o + 12);
-    const uint2 d = desc_of(p, sid);
-    const uint32_t cls = d_cls(d);
-    bool planned = false;
-    Seg seg;
-    uint32_t err = 0;
-    uint64_t aux = 0;
-    if (d_flags(d) & SF_VAR) {
-      const DSchema* sc = schema_of(p, sid);
-      if (o + 16 + plen <= win_len && var_plan(sc, win, w, o + 16, plen, seg.s)) {
-        planned = true;
-      } else {
-        uint64_t ro;
-        err = generic_payload(p, w, a, sid, plen, ro, aux);
-      }
-    }
-    if (err) {
-      push_error(p, err, s, base + rec, a, s64(win, o + 4), 0, aux);
-    } else if (cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY) {
-      RareOut ro = cls == HG_CLASS_DEVICE ? device_record(p, w, t0, win_len, o, sid, plen, planned, seg)
-                                          : telemetry_record(p, w, t0, o, sid, plen, planned, seg);
-      if (ro.x) push_error(p, ro.x, s, base + rec, a, s64(win, o + 4), 0, (uint64_t)ro.z | ((uint64_t)ro.w << 32));
-      dev = ro.y & 1u;
-      samples = (ro.y >> 1) & 1u;
-    }
-  }
-  if (p.tl_items)  // device span / sample message at its record (pipeline.py:186-215)
-    tl_emit(p, (dev | samples) != 0, (dev | samples) ? rd64(w, a + 4) : 0, tl_klo(s, base + rec),
-            (uint64_t)(w.g + a + 16), 0, dev ? TL_DEVICE : TL_SAMPLE, sid);
-  return make_uint4(dev, samples, 0, 0);
-}
-
-// clamped depth walk when exits meet an empty tile stack (Lindley recursion:
-// depth_i = S_i - min(0, min_j<=i S_j) with S the unclamped walk from Dc)
-__device__ __noinline__ int32_t clamped_depth(int32_t Dc, int32_t ps) {
-  const uint32_t lane = lane_id();
-  int32_t m = ps;
-  for (int d = 1; d < 32; d <<= 1) {
-    int32_t t = __shfl_up_sync(0xffffffffu, m, d);
-    if ((int)lane >= d) m = min(m, t);
-  }
-  return Dc + ps - min(0, Dc + min(-Dc, m));
-}
-
-// first NaN/inf result of the tile whose exit paired (per lane: the caller keeps one per tile)
-__device__ __noinline__ bool push_result_error(const Params& p, uint32_t s, uint64_t seq, uint64_t off, uint64_t ts,
-                                               uint64_t res) {
-  push_error(p, HG_ERR_RESULT, s, seq, off, ts, 0, res);
-  return true;
-}
-
-// result kind of a pending exit (its record is still in the window)
-__device__ __forceinline__ uint32_t pend_result_kind(const Params& p, const WarpSmem* ws, uint32_t m) {
-  const uint32_t sid = s32(ws->win, ws->rlist[m_rec(m)]);
-  return result_kind(d_flags(desc_of(p, sid)));
-}
-
-// materialise the fast-path tile state (pending exits + open levels) as an explicit stack
-__device__ __noinline__ void to_exact(const Params& p, SumEntry* scratch, uint64_t base, uint32_t n_pend, int32_t Dc) {
-  WarpSmem* ws = warp_smem(p.n_fn);
-  const uint32_t lane = lane_id();
-  for (uint32_t i = lane; i < n_pend; i += kWarp) {
-    SumEntry e;
-    uint32_t m = ws->pend_meta[i];
-    e.ts = ws->pend_ts[i]; e.seq = base + m_rec(m); e.fn = m_fn(m);
-    e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u) |
-              (pend_result_kind(p, ws, m) << 4);
-    e.result = ws->pend_res[i];
-    scratch[i] = e;
-  }
-  for (int32_t lv = 1 + (int32_t)lane; lv <= Dc; lv += kWarp) {
-    SumEntry e;
-    uint32_t m = ws->lvl_meta[lv];
-    e.ts = ws->lvl_ts[lv]; e.seq = base + m_rec(m); e.fn = m_fn(m);
-    e.flags = 0; e.result = 0;
-    scratch[n_pend + lv - 1] = e;
-  }
-  __syncwarp();
-}
-
-// ---------------------------------------------------------------------------
-// per-tile phases (out of line: executed once per tile, kept out of the hot loop)
-
-struct TileCtx {
-  SumEntry* scratch;
-};
-
-struct Found {      // result of pass A + look-back
-  Look L;
-  uint32_t n_rec;
-  bool dead;       // the stream failed in an earlier tile: nothing to do
-};
-
-// pass A + look-back + record list (tracefile.py:198-210 boundaries)
-__device__ __noinline__ Found find_records(const Params& p, DoneState* done, const TileGeom G, const Window w) {
-  WarpSmem* ws = warp_smem(p.n_fn);
-  const uint32_t* sdesc = sm_sdesc(p);
-  const uint32_t lane = lane_id();
-  const uint32_t* win = ws->win;
-  const uint64_t t0 = G.t0, size = G.size;
-  const uint32_t tlen = (uint32_t)(G.t1 - G.t0);
-  const uint32_t win_len = G.nbytes;
-  const uint32_t s = G.s;
-  Found F;
-  F.dead = false;
-  // speculative sync per lane, in lockstep: 4 candidate offsets per step, each
-  // screened (known schema id, payload length consistent with it) without
-  // branching; only survivors get the two-header check
-  const uint32_t sub0 = min(lane * (uint32_t)kLaneBytes, tlen);
-  const uint32_t sub1 = min(sub0 + (uint32_t)kLaneBytes, tlen);
-  uint32_t hyp = kNone32, exit = kNone32, cnt = 0, fail_off = 0;
-  bool fail = false;
-  {
-    // bounded lockstep search (kSyncSpan bytes).  Each iteration every searching lane
-    // either screens the next 4 offsets against the shared schema table (known id,
-    // payload length consistent with it) or checks ONE survivor's following header,
-    // so the warp never serialises per-lane loops.  Lanes that find nothing are
-    // chained from their predecessor by warp_verify.
-    uint32_t wo = sub0 & ~3u, wcur = 0, cm = 0;
-    const uint32_t stop = min(sub1, sub0 + (uint32_t)kSyncSpan);
-    bool searching = sub0 < sub1;
-    while (__any_sync(0xffffffffu, searching)) {
-      if (searching && cm == 0) {
-        const uint32_t wi = wo >> 2;
-        const uint32_t a0 = win[wi], a1 = win[wi + 1], c0 = win[wi + 3], c1 = win[wi + 4];
-        #pragma unroll 1
-        for (uint32_t b = 0; b < 4; b++) {
-          const uint32_t sid = __funnelshift_r(a0, a1, 8 * b);
-          const uint32_t plen = __funnelshift_r(c0, c1, 8 * b);
-          const uint32_t e = sid <= p.max_sid ? sdesc_lookup(p, sdesc, sid) : 0u;
-          const bool ok = (e & SD_PRESENT) && ((e & SD_VAR) ? plen >= (e & 0xFFFFu) : plen == (e & 0xFFFFu));
-          cm |= (ok ? 1u : 0u) << b;
-        }
-        if (wo < sub0) cm &= ~((1u << (sub0 - wo)) - 1u);
-        if (stop - wo < 4) cm &= (1u << (stop - wo)) - 1u;
-        wcur = wo;
-        wo += 4;
-      }
-      if (searching && cm) {
-        const uint32_t o = wcur + __ffs(cm) - 1;
-        cm &= cm - 1;
-        if (second_header_ok(p, win, t0, size, win_len, sdesc, o)) { hyp = o; searching = false; }
-      }
-      if (searching && !cm && wo >= stop) searching = false;
-    }
-  }
-  if (hyp != kNone32) lane_walk(p, ws, win, t0, size, hyp, sub1, cnt, exit, fail, fail_off);
-  uint32_t hmask = __ballot_sync(0xffffffffu, hyp != kNone32);
-  uint32_t S = hmask ? __shfl_sync(0xffffffffu, hyp, __ffs(hmask) - 1) : kNone32;
-  if (S != kNone32) warp_verify(p, warp_smem_off(p.n_fn), t0, size, sub1, S, hyp, cnt, exit, fail, fail_off);
-  Look L;
-  if (G.j == 0) {
-    L.entry = 16; L.base = 0; L.prev_ts = 0; L.has_prev = false;
-    if (S != 0) warp_verify(p, warp_smem_off(p.n_fn), t0, size, sub1, 0, hyp, cnt, exit, fail, fail_off);
-  } else {
-    uint32_t n_spec = __reduce_add_sync(0xffffffffu, cnt);
-    uint32_t x31 = __shfl_sync(0xffffffffu, exit, 31);
-    uint32_t lastmask = __ballot_sync(0xffffffffu, cnt > 0);
-    uint64_t spec_last = 0;
-    if (lastmask) {
-      int ll = 31 - __clz(lastmask);
-      uint64_t v = 0;
-      if ((int)lane == ll) v = s64(win, ws->roff[cnt - 1][lane] + 4);
-      spec_last = __shfl_sync(0xffffffffu, v, ll);
-    }
-    bool spec_failed = __any_sync(0xffffffffu, fail && exit == kNone32 && hyp != kNone32);
-    if (lane == 0) {
-      TileState* st = &p.state[G.g];
-      st->spec_entry = S == kNone32 ? kNone : t0 + S;
-      st->exit = (S == kNone32 || spec_failed || x31 == kNone32) ? kNone : t0 + x31;
-      st->n_local = S == kNone32 ? 0 : n_spec;
-      st->last_ts = spec_last;
-      publish(st, p.epoch, TS_SPEC);
-      L = lookback(p, done, G.g0, G.g, size);
-    }
-    L.entry = __shfl_sync(0xffffffffu, L.entry, 0);
-    L.base = __shfl_sync(0xffffffffu, L.base, 0);
-    L.prev_ts = __shfl_sync(0xffffffffu, L.prev_ts, 0);
-    L.has_prev = __shfl_sync(0xffffffffu, L.has_prev, 0);
-    if (L.entry == kNone) {
-      if (lane == 0) {
-        p.state[G.g].pool_n_pending = 0;
-        p.state[G.g].pool_n_resid = 0;
-        publish(&p.state[G.g], p.epoch, TS_ERROR);
-      }
-      F.dead = true;
-      F.L = L;
-      F.n_rec = 0;
-      return F;
-    }
-    uint64_t erel64 = L.entry - t0;
-    uint32_t erel = erel64 > 0x7FFFFFFFull ? 0x7FFFFFFFu : (uint32_t)erel64;
-    bool consistent = (S == kNone32) ? (erel >= tlen) : (erel == S);
-    if (!consistent) {
-      if (S == kNone32) { hyp = kNone32; cnt = 0; exit = kNone32; fail = false; }
-      warp_verify(p, warp_smem_off(p.n_fn), t0, size, sub1, erel, hyp, cnt, exit, fail, fail_off);
-    }
-    if (erel >= tlen) { cnt = 0; fail = false; exit = erel; }
-  }
-  // real header-level failure: the first failing lane whose walk started at its true entry
-  uint32_t e_up = __shfl_up_sync(0xffffffffu, exit, 1);
-  uint32_t e_in = lane == 0 ? (uint32_t)min(L.entry - t0, (uint64_t)0x7FFFFFFFu) : e_up;
-  bool real_fail = fail && e_in != kNone32 && hyp == e_in;
-  uint32_t fmask = __ballot_sync(0xffffffffu, real_fail);
-  int fl = fmask ? __ffs(fmask) - 1 : 32;
-  if ((int)lane > fl) cnt = 0;
-  uint32_t incl = cnt;
-  for (int d = 1; d < 32; d <<= 1) { uint32_t v = __shfl_up_sync(0xffffffffu, incl, d); if ((int)lane >= d) incl += v; }
-  const uint32_t n_rec = __shfl_sync(0xffffffffu, incl, 31);
-  const uint32_t lane_base = incl - cnt;
-  for (uint32_t k = 0; k < cnt; k++) ws->rlist[lane_base + k] = ws->roff[k][lane];
-  __syncwarp();
-  uint64_t tile_last = 0;
-  if (n_rec) {
-    uint64_t v = 0;
-    if (lane == 0) v = s64(win, ws->rlist[n_rec - 1] + 4);
-    tile_last = __shfl_sync(0xffffffffu, v, 0);
-  }
-  uint32_t true_exit = __shfl_sync(0xffffffffu, exit, 31);
-  uint32_t ffo = __shfl_sync(0xffffffffu, fail_off, fl < 32 ? fl : 0);
-  if (lane == 0) {
-    DoneState* d = &done[G.g];
-    d->exit = t0 + true_exit;
-    d->incl = L.base + n_rec;
-    d->last_ts = n_rec ? tile_last : L.prev_ts;
-    d->has_last = (n_rec || L.has_prev) ? 1u : 0u;
-    if (fmask) {
-      uint64_t a = t0 + ffo;
-      uint32_t code;
-      uint64_t aux = 0, ts_f = 0;
-      if (a + 16 > size) code = HG_ERR_TRUNC_HEADER;
-      else {
-        uint32_t sid = rd32(w, a);
-        uint32_t plen = rd32(w, a + 12);
-        ts_f = rd64(w, a + 4);
-        if (a + 16 + plen > size) code = HG_ERR_TRUNC_PAYLOAD;
-        else { code = HG_ERR_UNKNOWN_SCHEMA; aux = sid; }
-      }
-      push_error(p, code, s, L.base + n_rec, a, ts_f, n_rec ? tile_last : L.prev_ts, aux);
-      publish(&p.state[G.g], p.epoch, TS_ERROR);
-    } else {
-      publish(&p.state[G.g], p.epoch, TS_DONE);
-    }
-  }
-  F.L = L;
-  F.n_rec = n_rec;
-  return F;
-}
-
-// tile summary for compose_kernel: pending exits, then open entries (innermost last)
-__device__ __noinline__ void write_summary(const Params& p, SumEntry* scratch, uint32_t g, uint32_t s,
-                                           uint64_t base, bool slow, uint32_t n_pend, int32_t Dc, const GStack gs,
-                                           uint32_t spans) {
-  WarpSmem* ws = warp_smem(p.n_fn);
-  const uint32_t lane = lane_id();
-  uint32_t sum_np, sum_n;
-  if (!slow) { sum_np = n_pend; sum_n = n_pend + (uint32_t)Dc; }
-  else { sum_np = gs.n_pend; sum_n = gs.top; }
-  const uint32_t tspans = __reduce_add_sync(0xffffffffu, spans);
-  unsigned long long poff = 0;
-  if (lane == 0) {
-    poff = sum_n ? atomicAdd(p.pool_used, (unsigned long long)sum_n) : 0ull;
-    p.state[g].pool_off = poff;
-    p.state[g].pool_n_pending = sum_np;
-    p.state[g].pool_n_resid = sum_n - sum_np;
-    if (tspans) atomicAdd(&p.stream_spans[s], (unsigned long long)tspans);
-  }
-  poff = __shfl_sync(0xffffffffu, poff, 0);
-  for (uint32_t i = lane; i < sum_n; i += kWarp) {
-    if (poff + i >= p.pool_cap) continue;
-    SumEntry e;
-    if (slow) {
-      e = scratch[i];
-    } else if (i < n_pend) {
-      uint32_t m = ws->pend_meta[i];
-      e.ts = ws->pend_ts[i]; e.seq = base + m_rec(m); e.fn = m_fn(m); e.result = ws->pend_res[i];
-      e.flags = 1u | ((m & M_ERR) ? 2u : 0u) | ((m & M_BAD) ? 4u : 0u) | ((m & M_NAN) ? 8u : 0u) |
-                (pend_result_kind(p, ws, m) << 4);
-    } else {
-      uint32_t lv = i - n_pend + 1;
-      uint32_t m = ws->lvl_meta[lv];
-      e.ts = ws->lvl_ts[lv]; e.seq = base + m_rec(m); e.fn = m_fn(m); e.result = 0; e.flags = 0;
-    }
-    p.pool[poff + i] = e;
-  }
-  __syncwarp();
-}
-
-// host span that does not fit the per-lane columns (duration >= 2^32 or a large function set)
-__device__ __noinline__ void fold_slow(const Params& p, int32_t fn, uint64_t dur, bool err) {
-  HostFold hf;
-  hf.small = false;
-  hf.tab = sm_tab(p.n_fn);
-  hf.fold(p, fn, dur, err);
-}
-
-__device__ __noinline__ void tile_prologue(const Params& p) {
-  const uint32_t lane = lane_id();
-  const bool small = p.n_fn <= kSmallF;
-  if (small) {
-    uint32_t* b = sm_lanetab(p.n_fn);
-    const uint32_t n = p.n_fn * kWarp;
-    for (uint32_t i = lane; i < 3 * n; i += kWarp) b[i] = 0;
-    for (uint32_t i = lane; i < p.n_fn; i += kWarp) { b[3 * n + i] = 0; b[3 * n + p.n_fn + i] = 0xFFFFFFFFu; b[3 * n + 2 * p.n_fn + i] = 0; }
-  }
-  SmemRow* tab = sm_tab(p.n_fn);
-  if (tab)
-    for (uint32_t i = threadIdx.x; i < p.n_fn; i += blockDim.x) {
-      SmemRow z; z.count = z.err = z.s0 = z.s1 = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
-      tab[i] = z;
-    }
-  DevRow* dcache = sm_dcache(p.n_fn);
-  for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
-    DevRow z; z.tag = 0; z.count = 0; z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
-    dcache[i] = z;
-  }
-  NameSlot* ncache = sm_ncache(p.n_fn);
-  for (uint32_t i = threadIdx.x; i < kNameSlots; i += blockDim.x) { ncache[i].hash = 0; ncache[i].row = 0; }
-  if (p.max_sid < (uint32_t)kSdescMax) {
-    uint2* t = reinterpret_cast<uint2*>(g_smem);
-    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) t[i] = __ldg(&p.desc[i]);
-  }
-  if (lane == 0) {
-    mbar_init(&warp_smem(p.n_fn)->mbar);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-}
-
-struct Counters {
-  uint32_t events, passed, host, dev, samples, orph;
-  uint64_t last_ts;
-};
-
-__device__ __noinline__ void tile_epilogue(const Params& p, const Counters K) {
-  const uint32_t lane = lane_id();
-  uint32_t* lt = sm_lanetab(p.n_fn);
-  const uint32_t nn = p.n_fn * kWarp;
-  SmemRow* tab = sm_tab(p.n_fn);
-  DevRow* dcache = sm_dcache(p.n_fn);
-  auto wsum = [](uint32_t v) { return __reduce_add_sync(0xffffffffu, v); };
-  uint32_t a0 = wsum(K.events), a1 = wsum(K.passed), a2 = wsum(K.host), a3 = wsum(K.dev), a4 = wsum(K.samples),
-           a5 = wsum(K.orph);
-  uint64_t mts = K.last_ts;
-  for (int d = 16; d; d >>= 1) { uint64_t v = __shfl_xor_sync(0xffffffffu, mts, d); mts = v > mts ? v : mts; }
-  if (lane == 0) {
-    if (a0) atomicAdd(&p.stats[ST_EVENTS], (unsigned long long)a0);
-    if (a1) atomicAdd(&p.stats[ST_PASSED], (unsigned long long)a1);
-    if (a2) atomicAdd(&p.stats[ST_HOST], (unsigned long long)a2);
-    if (a3) atomicAdd(&p.stats[ST_DEVICE], (unsigned long long)a3);
-    if (a4) atomicAdd(&p.stats[ST_SAMPLES], (unsigned long long)a4);
-    if (a5) atomicAdd(&p.stats[ST_ORPHANS], (unsigned long long)a5);
-    atomicMax(p.last_ts, (unsigned long long)mts);
-  }
-  __syncwarp();
-  if (p.n_fn <= kSmallF) {
-    for (uint32_t f = 0; f < p.n_fn; f++) {
-      uint32_t i = f * kWarp + lane;
-      uint64_t cc = lt[i], sum = ((uint64_t)lt[2 * nn + i] << 32) | lt[nn + i];
-      if (!__any_sync(0xffffffffu, cc != 0)) continue;
-      for (int d = 16; d; d >>= 1) {
-        cc += __shfl_xor_sync(0xffffffffu, cc, d);
-        sum += __shfl_xor_sync(0xffffffffu, sum, d);
-      }
-      if (lane == 0 && cc) {
-        unsigned long long* a = p.host_acc + 6ull * f;
-        atomicAdd(&a[0], (unsigned long long)cc);
-        if (lt[3 * nn + f]) atomicAdd(&a[1], (unsigned long long)lt[3 * nn + f]);
-        add_i128(&a[2], &a[3], sum, 0);
-        atomicMin(&a[4], (unsigned long long)lt[3 * nn + p.n_fn + f]);
-        atomicMax(&a[5], (unsigned long long)lt[3 * nn + 2 * p.n_fn + f]);
-      }
-    }
-  }
-  __syncthreads();
-  if (tab) {
-    for (uint32_t f = threadIdx.x; f < p.n_fn; f += blockDim.x) {
-      SmemRow r = tab[f];
-      if (!r.count) continue;
-      unsigned long long* a = p.host_acc + 6ull * f;
-      atomicAdd(&a[0], (unsigned long long)r.count);
-      if (r.err) atomicAdd(&a[1], (unsigned long long)r.err);
-      add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), 0);
-      atomicMin(&a[4], (unsigned long long)r.mn);
-      atomicMax(&a[5], (unsigned long long)r.mx);
-    }
-  }
-  for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
-    DevRow r = dcache[i];
-    if (!r.tag || !r.count) continue;
-    unsigned long long* a = p.dev_acc + 6ull * (r.tag - 1);
-    atomicAdd(&a[0], (unsigned long long)r.count);
-    add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), (int64_t)(int32_t)r.s2);
-    // biased 32-bit -> biased 64-bit
-    atomicMin(&a[4], bias64((int64_t)(int32_t)(r.mn ^ 0x80000000u)));
-    atomicMax(&a[5], bias64((int64_t)(int32_t)(r.mx ^ 0x80000000u)));
-  }
-}
-
-// ---------------------------------------------------------------------------
-// the tile kernel
-
-__global__ void __launch_bounds__(kCtaThreads) tile_kernel(Params p, DoneState* done) {
-  const uint32_t lane = lane_id();
-  tile_prologue(p);
-  __syncthreads();
-  WarpSmem* ws = warp_smem(p.n_fn);
-  const uint32_t* win = ws->win;
-  const bool small = p.n_fn <= kSmallF;
-  uint32_t* const lt = sm_lanetab(p.n_fn);
-  const uint32_t nn = p.n_fn * kWarp;
-  SumEntry* const scratch = p.warp_scratch + (size_t)(blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5)) * kMaxRecTile;
-  Counters K;
-  K.events = K.passed = K.host = K.dev = K.samples = K.orph = 0;
-  K.last_ts = 0;
-  uint32_t parity = 0;
-
-  for (;;) {
-    uint32_t work = 0;
-    if (lane == 0) work = atomicAdd(p.work_counter, 1u);
-    work = __shfl_sync(0xffffffffu, work, 0);
-    if (work >= p.n_tiles) break;
-    const TileGeom G = geom(p, work);
-    __syncwarp();
-    if (lane == 0) bulk_load(ws->win, G.gbase + G.t0, G.nbytes, &ws->mbar);
-    mbar_wait(&ws->mbar, parity);
-    parity ^= 1u;
-    Window w;  // generic accessor for fields that leave the window
-    w.s = win; w.win_start = G.t0; w.win_end = G.t0 + G.nbytes; w.g = G.gbase; w.size = G.size;
-    const Found F = find_records(p, done, G, w);
-    if (F.dead) continue;
-    const Look& L = F.L;
-    const uint32_t n_rec = F.n_rec;
-    const uint32_t s = G.s;
-    const uint64_t t0 = G.t0;
-    const uint32_t win_len = G.nbytes;
-
-    // ---- rounds: lockstep decode + pairing, 32 records per round.  All rare events
-    // (decode errors, clamped depths, typed mismatches, deep stacks, NaN results) are
-    // behind single warp votes so the common round stays short.
-    uint64_t prev_ts = L.prev_ts;
-    bool have_prev = L.has_prev;
-    int32_t Dc = 0;            // open entries of this tile before the round
-    uint32_t n_pend = 0;       // pending exits so far
-    bool slow = false;         // exact elimination mode (GStack in scratch)
-    GStack gs;
-    gs.base = scratch;
-    gs.n_pend = 0;
-    gs.top = 0;
-    bool res_done = false;
-    uint32_t spans = 0;
-    uint32_t qn = 0;           // deferred records waiting in ws->q
-    for (uint32_t rb = 0; rb < n_rec; rb += kWarp) {
-      const uint32_t r = rb + lane;
-      const bool act = r < n_rec;
-      Rec R;
-      R.x = 0; R.meta = 0; R.ts = 0; R.res = 0;
-      uint32_t dec_err = 0;
-      uint64_t dec_aux = 0;
-      uint32_t o = 0;
-      bool defer = false;
-      if (act) {
-        o = ws->rlist[r];
-        defer = decode_one_rec(p, win, w, t0, win_len, o, r, R, dec_err, dec_aux, K.passed);
-      }
-      // monotonicity against the previous record of the stream (pipeline.py:98-99)
-      const uint64_t up_ts = __shfl_up_sync(0xffffffffu, R.ts, 1);
-      const uint64_t pts = lane == 0 ? prev_ts : up_ts;
-      if (act && !dec_err && (lane != 0 || have_prev) && R.ts < pts) dec_err = HG_ERR_ORDER;
-      uint32_t live_mask = __ballot_sync(0xffffffffu, act);
-      const uint32_t dm = __ballot_sync(0xffffffffu, dec_err != 0);
-      if (dm) {  // the stream is cut at the first failing record
-        const int dl = __ffs(dm) - 1;
-        if ((int)lane == dl)
-          push_error(p, dec_err, s, L.base + r, t0 + o, R.ts, (lane != 0 || have_prev) ? pts : 0, dec_aux);
-        live_mask &= (1u << dl) - 1u;
-        if (!((live_mask >> lane) & 1u)) { R.x = 0; defer = false; }
-      }
-      const bool live = (live_mask >> lane) & 1u;
-      if (live) {
-        K.events++;
-        K.last_ts = R.ts > K.last_ts ? R.ts : K.last_ts;
-      }
-      if (live_mask) {
-        prev_ts = __shfl_sync(0xffffffffu, R.ts, 31 - __clz(live_mask));
-        have_prev = true;
-      }
-      const uint32_t Qm = __ballot_sync(0xffffffffu, defer);
-      if (Qm) {  // defer payload work; drain 32 at a time with every lane active
-        if (defer) ws->q[qn + __popc(Qm & lanemask_lt())] = o | (r << 16);
-        qn += __popc(Qm);
-        __syncwarp();
-        if (qn >= (uint32_t)kWarp) {
-          const uint4 dq = drain_queue(p, w, t0, win_len, s, L.base, kWarp);
-          K.dev += dq.x;
-          K.samples += dq.y;
-          spans += dq.x;
-          qn -= kWarp;
-          if (lane < qn) ws->q[lane] = ws->q[kWarp + lane];
-          __syncwarp();
-        }
-      }
-
-      // ---- pairing (pipeline.py:156-185)
-      const bool isE = R.x > 0, isX = R.x < 0;
-      bool paired = false, orphan = false;
-      uint64_t ets = 0;
-      if (!slow) {
-        const uint32_t Em = __ballot_sync(0xffffffffu, isE);
-        const uint32_t Xm = __ballot_sync(0xffffffffu, isX);
-        const uint32_t le = lanemask_lt() | (1u << lane);
-        const int32_t ps = (int32_t)__popc(Em & le) - (int32_t)__popc(Xm & le);
-        int32_t after = Dc + ps;
-        if (__any_sync(0xffffffffu, after < 0)) after = clamped_depth(Dc, ps);  // exits met an empty tile stack
-        int32_t before = __shfl_up_sync(0xffffffffu, after, 1);
-        if (lane == 0) before = Dc;
-        const bool pops = isX && before > 0;
-        const int32_t level = isE ? after : before;
-        const uint32_t key = (isE || pops) ? (uint32_t)level : (0x80000000u | lane);
-        const uint32_t same = __match_any_sync(0xffffffffu, key);
-        const uint32_t cand = same & Em & lanemask_lt();
-        const int el = cand ? 31 - __clz(cand) : (int)lane;
-        const uint32_t cmeta = __shfl_sync(0xffffffffu, R.meta, el);
-        const uint64_t cts = __shfl_sync(0xffffffffu, R.ts, el);
-        uint32_t emeta = cmeta;
-        ets = cts;
-        const bool deep = (isE || pops) && level >= kLevels;
-        if (pops && !cand && !deep) { emeta = ws->lvl_meta[level]; ets = ws->lvl_ts[level]; }
-        const uint32_t Pm = __ballot_sync(0xffffffffu, isX && before <= 0);
-        const bool bad = deep || (pops && ((emeta ^ R.meta) & M_FN) != 0);
-        if (!__any_sync(0xffffffffu, bad) && n_pend + __popc(Pm) <= (uint32_t)kPendCap) {
-          paired = pops;
-          if (isE && !(same & Em & lanemask_gt())) { ws->lvl_ts[level] = R.ts; ws->lvl_meta[level] = R.meta; }
-          if (Pm) {
-            if ((Pm >> lane) & 1u) {
-              const uint32_t i = n_pend + __popc(Pm & lanemask_lt());
-              ws->pend_ts[i] = R.ts; ws->pend_res[i] = R.res; ws->pend_meta[i] = R.meta;
-            }
-            n_pend += __popc(Pm);
-          }
-          Dc = __shfl_sync(0xffffffffu, after, 31);
-          __syncwarp();
-        } else {
-          to_exact(p, scratch, L.base, n_pend, Dc);
-          gs.n_pend = n_pend;
-          gs.top = n_pend + (uint32_t)Dc;
-          slow = true;
-        }
-      }
-      if (slow) {
-        SumEntry mine;
-        mine.ts = R.ts; mine.seq = L.base + r; mine.fn = m_fn(R.meta);
-        mine.flags = (isX ? 1u : 0u) | ((R.meta & M_ERR) ? 2u : 0u) | ((R.meta & M_BAD) ? 4u : 0u) |
-                     ((R.meta & M_NAN) ? 8u : 0u) |
-                     (isX ? result_kind(d_flags(desc_of(p, s32(win, o)))) << 4 : 0u);
-        mine.result = R.res;
-        const RoundOut ro2 = round_resolve(gs, true, isE, isX, m_fn(R.meta), R.ts, mine);
-        paired = ro2.flags & 1u;
-        orphan = (ro2.flags >> 1) & 1u;
-        ets = ro2.ets;
-        gs.n_pend = ro2.n_pend;
-        gs.top = ro2.top;
-        if (orphan) { push_orphan(p, s, m_fn(R.meta), R.ts, L.base + r); K.orph++; }
-      }
-      if (paired) {
-        const uint64_t dur = R.ts - ets;
-        const int32_t fn = m_fn(R.meta);
-        if (small && (dur >> 32) == 0) {
-          const uint32_t i = (uint32_t)fn * kWarp + lane, d = (uint32_t)dur;
-          lt[i] += 1;
-          const uint32_t lo = lt[nn + i] + d;
-          lt[2 * nn + i] += lo < d ? 1u : 0u;
-          lt[nn + i] = lo;
-          uint32_t* const mn = lt + 3 * nn + p.n_fn;
-          uint32_t* const mx = mn + p.n_fn;
-          if (d < mn[fn]) atomicMin(&mn[fn], d);
-          if (d > mx[fn]) atomicMax(&mx[fn], d);
-          if (R.meta & M_ERR) atomicAdd(&lt[3 * nn + fn], 1u);
-        } else {
-          fold_slow(p, fn, dur, (R.meta & M_ERR) != 0);
-        }
-        K.host++;
-        spans++;
-        if ((R.meta & M_BAD) && !res_done)  // int(NaN/inf) raises only when the exit pairs
-          res_done = push_result_error(p, s, L.base + r, t0 + o, R.ts, R.res);
-      }
-      if (p.tl_items) {  // host span message at the exit (pipeline.py:170-185)
-        const uint32_t fl = paired ? d_flags(desc_of(p, s32(win, o))) : 0u;
-        tl_emit(p, paired, R.ts, tl_klo(s, L.base + r), ets, R.res, TL_HOST | (result_kind(fl) << 4),
-                (uint32_t)m_fn(R.meta));
-      }
-      if (dm) break;  // the stream is cut at the failing record
-    }
-    if (qn) {
-      const uint4 dq = drain_queue(p, w, t0, win_len, s, L.base, qn);
-      K.dev += dq.x;
-      K.samples += dq.y;
-      spans += dq.x;
-    }
-    write_summary(p, scratch, G.g, s, L.base, slow, n_pend, Dc, gs, spans);
-  }
-  tile_epilogue(p, K);
-}
-
-// ---------------------------------------------------------------------------
-// composition of tile summaries per stream (exact automaton from an empty stack)
+// composition of segment summaries per stream (exact automaton from an empty stack)
 
 constexpr int kComposeWarps = 4;
 
@@ -1159,7 +224,6 @@ struct hg_ctx {
   std::vector<int32_t> sid_map;
   std::vector<uint2> desc;
   DBuf<uint2> d_desc;
-  DBuf<SumEntry> d_warp_scratch;
   std::vector<uint8_t> kinds, field_role;
   uint32_t n_fn = 0, max_sid = 0;
   DBuf<DSchema> d_schemas;
@@ -1172,11 +236,10 @@ struct hg_ctx {
   uint64_t total_bytes = 0;
   DBuf<uint8_t> d_data;
   DBuf<uint64_t> d_base, d_size;
-  std::vector<uint32_t> tile_stream, stream_tile0, order;
-  DBuf<uint32_t> d_tile_stream, d_stream_tile0, d_order;
+  std::vector<uint32_t> tile_stream, stream_tile0;  // segment -> stream, stream -> first segment
+  DBuf<uint32_t> d_tile_stream, d_stream_tile0;
   // scratch
-  DBuf<TileState> d_state;
-  DBuf<DoneState> d_done;
+  DBuf<SegState> d_state;
   uint32_t epoch = 0;
   DBuf<SumEntry> d_pool, d_stack;
   uint64_t pool_cap = 0, stack_cap = 0;
@@ -1492,12 +555,12 @@ void hg_destroy(hg_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   ctx->d_schemas.release(); ctx->d_sid_map.release(); ctx->d_kinds.release(); ctx->d_field_role.release();
   ctx->d_data.release(); ctx->d_base.release(); ctx->d_size.release();
-  ctx->d_tile_stream.release(); ctx->d_stream_tile0.release(); ctx->d_order.release();
-  ctx->d_state.release(); ctx->d_done.release(); ctx->d_pool.release(); ctx->d_stack.release();
+  ctx->d_tile_stream.release(); ctx->d_stream_tile0.release();
+  ctx->d_state.release(); ctx->d_pool.release(); ctx->d_stack.release();
   ctx->d_host_acc.release(); ctx->d_dev_acc.release(); ctx->d_counters.release();
   ctx->d_orphans.release(); ctx->d_errors.release(); ctx->d_stream_spans.release();
   ctx->d_keys.release(); ctx->d_vals.release(); ctx->d_name_len.release(); ctx->d_small.release();
-  ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release(); ctx->d_warp_scratch.release();
+  ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release();
   ctx->d_tl_items.release();
   for (int k = 0; k < 2; k++) { ctx->d_tl_keys[k].release(); ctx->d_tl_idx[k].release(); }
   ctx->d_tl_lens.release(); ctx->d_tl_stream_proc.release(); ctx->d_tl_offs.release(); ctx->d_tl_bsum.release();
@@ -1645,25 +708,15 @@ static int build_layout(hg_ctx* ctx) {
     off += (ctx->streams[s].size + 255) & ~255ull;
   }
   ctx->total_bytes = off;
-  // tiles
+  // segments: stream-major, each stream cut into seg_bytes pieces from byte 16
   ctx->tile_stream.clear();
   ctx->stream_tile0.assign(ns, 0);
-  std::vector<uint32_t> ntiles(ns, 0);
-  uint32_t maxt = 0;
   for (uint32_t s = 0; s < ns; s++) {
     ctx->stream_tile0[s] = (uint32_t)ctx->tile_stream.size();
-    uint64_t sz = ctx->sizes[s];
-    uint32_t nt = sz > 16 ? (uint32_t)((sz - 16 + ctx->seg_bytes - 1) / ctx->seg_bytes) : 0;
-    ntiles[s] = nt;
-    maxt = std::max(maxt, nt);
+    const uint64_t sz = ctx->sizes[s];
+    const uint32_t nt = sz > 16 ? (uint32_t)((sz - 16 + ctx->seg_bytes - 1) / ctx->seg_bytes) : 0;
     for (uint32_t t = 0; t < nt; t++) ctx->tile_stream.push_back(s);
   }
-  // processing order: tile index major, streams interleaved (predecessors finish early)
-  ctx->order.clear();
-  ctx->order.reserve(ctx->tile_stream.size());
-  for (uint32_t t = 0; t < maxt; t++)
-    for (uint32_t s = 0; s < ns; s++)
-      if (t < ntiles[s]) ctx->order.push_back(ctx->stream_tile0[s] + t);
   return HG_OK;
 }
 
@@ -1671,7 +724,7 @@ static int stage(hg_ctx* ctx) {
   cudaSetDevice(ctx->cfg.device);
   build_layout(ctx);
   const uint32_t ns = (uint32_t)ctx->streams.size();
-  const size_t pad = kWinBytes + 4096;
+  const size_t pad = kDataPad;
   CK(ctx->d_data.ensure(ctx->total_bytes + pad));
   CK(cudaMemsetAsync(ctx->d_data.ptr + ctx->total_bytes, 0, pad, ctx->stream));
   ctx->h2d_bytes = 0;
@@ -1689,19 +742,16 @@ static int stage(hg_ctx* ctx) {
   }
   size_t nt = ctx->tile_stream.size();
   CK(ctx->d_tile_stream.ensure(std::max<size_t>(nt, 1)));
-  CK(ctx->d_order.ensure(std::max<size_t>(nt, 1)));
   CK(ctx->d_stream_tile0.ensure(std::max<uint32_t>(ns, 1)));
   if (nt) {
     CK(cudaMemcpyAsync(ctx->d_tile_stream.ptr, ctx->tile_stream.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->d_order.ptr, ctx->order.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
   }
   if (ns) CK(cudaMemcpyAsync(ctx->d_stream_tile0.ptr, ctx->stream_tile0.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->d_state.n < nt) {
     CK(ctx->d_state.ensure(nt));
-    CK(cudaMemsetAsync(ctx->d_state.ptr, 0, nt * sizeof(TileState), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_state.ptr, 0, nt * sizeof(SegState), ctx->stream));
     ctx->epoch = 0;
   }
-  CK(ctx->d_done.ensure(std::max<size_t>(nt, 1)));
   ctx->staged = true;
   return HG_OK;
 }
@@ -1714,7 +764,6 @@ int hg_stage(hg_ctx* ctx) {
   return HG_OK;
 }
 
-static size_t tile_smem_bytes(uint32_t n_fn) { return smem_layout(n_fn).total; }
 
 static int ensure_scratch(hg_ctx* ctx, uint64_t n_records_bound) {
   const size_t nt = ctx->tile_stream.size();
@@ -1758,13 +807,11 @@ static Params make_params(hg_ctx* ctx) {
   p.stream_size = ctx->d_size.ptr;
   p.tile_stream = ctx->d_tile_stream.ptr;
   p.stream_tile0 = ctx->d_stream_tile0.ptr;
-  p.order = ctx->d_order.ptr;
   p.n_tiles = (uint32_t)ctx->tile_stream.size();
   p.n_streams = (uint32_t)ctx->streams.size();
   p.schemas = ctx->d_schemas.ptr;
   p.sid_map = ctx->d_sid_map.ptr;
   p.desc = ctx->d_desc.ptr;
-  p.warp_scratch = ctx->d_warp_scratch.ptr;
   p.max_sid = ctx->max_sid;
   p.kinds = ctx->d_kinds.ptr;
   p.field_role = ctx->d_field_role.ptr;
@@ -1822,7 +869,7 @@ static int launch_phase1(hg_ctx* ctx) {
   const uint32_t ns = (uint32_t)ctx->streams.size();
   ctx->epoch++;
   if (ctx->epoch >= (1u << 29)) {
-    CK(cudaMemsetAsync(ctx->d_state.ptr, 0, ctx->d_state.n * sizeof(TileState), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_state.ptr, 0, ctx->d_state.n * sizeof(SegState), ctx->stream));
     ctx->epoch = 1;
   }
   CK(cudaMemsetAsync(ctx->d_counters.ptr, 0, C_NUM * 8, ctx->stream));

@@ -1,9 +1,9 @@
 // hg_device.cuh -- device-side building blocks of the hapigpu engine (sm_100a).
 //
-// Byte access into warp-staged stream windows, strict UTF-8 validation with
-// CPython's acceptance rules (tracefile.py:165 `raw.decode("utf-8")`), the
-// device-name dictionary, exact 128-bit tally accumulators and the tile
-// lookback state.  Included by engine.cu only.
+// Byte access into stream bytes in HBM, strict UTF-8 validation with CPython's
+// acceptance rules (tracefile.py:165 `raw.decode("utf-8")`), the device-name
+// dictionary layout, exact 128-bit tally accumulators, the per-segment state and
+// the timeline message record.  Included by engine.cu only.
 #pragma once
 #include <cstdint>
 
@@ -131,25 +131,6 @@ __device__ __noinline__ bool utf8_valid(const Window& w, uint64_t p, uint32_t n)
   return true;
 }
 
-// 64-bit hash of a byte string (word-at-a-time; collisions are resolved by
-// full comparison, so quality only affects speed)
-__device__ __noinline__ uint64_t hash_bytes(const Window& w, uint64_t p, uint32_t n) {
-  uint64_t h = 0x9E3779B97F4A7C15ull ^ ((uint64_t)n * 0xff51afd7ed558ccdull);
-  uint32_t i = 0;
-  for (; i + 4 <= n; i += 4) {
-    h ^= rd32(w, p + i);
-    h *= 0x100000001b3ull;
-    h ^= h >> 29;
-  }
-  if (i < n) {
-    uint32_t x = rd32(w, p + i) & (0xffffffffu >> (8 * (4 - (n - i))));
-    h ^= x;
-    h *= 0x100000001b3ull;
-  }
-  h ^= h >> 33; h *= 0xc4ceb9fe1a85ec53ull; h ^= h >> 33;
-  return h | 1ull;  // 0 marks an empty slot
-}
-
 // ---------------------------------------------------------------------------
 // device-name dictionary (device rows are keyed by the profiling payload's
 // "name" string, pipeline.py:192; first-seen order assigns row ids)
@@ -168,42 +149,6 @@ struct NameDict {
   uint32_t* overflow;
 };
 
-__device__ __noinline__ bool name_equal(const NameDict& d, uint32_t row, const Window& w, uint64_t p, uint32_t n) {
-  if (d.name_len[row] != n) return false;
-  const uint8_t* a = d.arena + d.name_off[row];
-  for (uint32_t i = 0; i < n; i++)
-    if (a[i] != rd8(w, p + i)) return false;
-  return true;
-}
-
-// returns the row id or 0xffffffff on overflow
-__device__ __noinline__ uint32_t name_lookup(const NameDict& d, const Window& w, uint64_t p, uint32_t n) {
-  uint64_t h = hash_bytes(w, p, n);
-  for (uint64_t slot = h & d.mask, probes = 0; probes <= d.mask; slot = (slot + 1) & d.mask, probes++) {
-    unsigned long long k = atomicCAS(&d.keys[slot], 0ull, (unsigned long long)h);
-    if (k == 0ull) {
-      uint32_t row = atomicAdd(d.n_rows, 1u);
-      unsigned long long off = atomicAdd(d.arena_used, (unsigned long long)((n + 3u) & ~3u));
-      if (row >= d.row_cap || off + n > d.arena_cap) { atomicExch(d.overflow, 1u); atomicExch(&d.vals[slot], 0xffffffffu); return 0xffffffffu; }
-      for (uint32_t i = 0; i < n; i++) d.arena[off + i] = rd8(w, p + i);
-      d.name_off[row] = off;
-      d.name_len[row] = n;
-      __threadfence();
-      atomicExch(&d.vals[slot], row + 1);
-      return row;
-    }
-    if (k == h) {
-      uint32_t v;
-      while ((v = *(volatile uint32_t*)&d.vals[slot]) == 0) { __nanosleep(32); }
-      if (v == 0xffffffffu) return 0xffffffffu;
-      __threadfence();
-      if (name_equal(d, v - 1, w, p, n)) return v - 1;
-    }
-  }
-  atomicExch(d.overflow, 1u);
-  return 0xffffffffu;
-}
-
 // ---------------------------------------------------------------------------
 // exact accumulators
 
@@ -219,25 +164,19 @@ __device__ __forceinline__ void add_i128(unsigned long long* lo, unsigned long l
 __device__ __forceinline__ uint64_t bias64(int64_t x) { return (uint64_t)x ^ 0x8000000000000000ull; }
 
 // ---------------------------------------------------------------------------
-// tile chain state for the decoupled lookback over record boundaries
+// per-segment state read by compose_kernel
 
-enum : uint32_t { TS_INVALID = 0, TS_SPEC = 1, TS_DONE = 2, TS_ERROR = 3 };
+enum : uint32_t { TS_INVALID = 0, TS_DONE = 2, TS_ERROR = 3 };
 
-struct TileState {
-  uint32_t status;     // (epoch << 2) | TS_*
-  uint32_t n_local;    // records owned by this tile (spec or final)
-  uint64_t spec_entry; // speculative entry offset; kNone = pass-through
-  uint64_t exit;       // exit offset under spec_entry (spec) or the true exit (done)
-  uint64_t last_ts;    // ts of the tile's last record (spec) / of the stream so far (done)
-  uint64_t incl;       // done: records in the stream up to and including this tile
-  uint32_t has_last;   // done: any record so far; spec: n_local > 0
+struct SegState {
+  uint32_t status;     // (epoch << 2) | TS_*, raised with atomicMax (a deferred error wins)
   uint32_t pool_n_pending;
   uint64_t pool_off;   // summary entries in the pool
   uint32_t pool_n_resid;
   uint32_t pad;
 };
 
-struct SumEntry {      // tile summary: pending exit or residual entry
+struct SumEntry {      // segment summary: pending exit or residual entry
   uint64_t ts;
   uint64_t seq;
   int32_t fn;

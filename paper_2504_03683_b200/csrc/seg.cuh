@@ -29,6 +29,7 @@
 namespace hg {
 
 constexpr int kSegWarps = 4;
+constexpr size_t kDataPad = 8192;  // zero bytes after the last stream (look-ahead reads and prefetches)
 constexpr int kSegThreads = kSegWarps * kWarp;
 constexpr int kLS = 8;   // open entries per lane in shared memory
 constexpr int kLP = 4;   // pending exits per lane in shared memory
@@ -702,7 +703,7 @@ __device__ __forceinline__ bool seg_begin(const Params& p, const SegInfo* info, 
   for (; g < p.n_tiles; g += gridDim.x * blockDim.x) {
     const SegInfo I = info[g];
     if (I.flags & SI_DEAD) {
-      TileState* st = &p.state[g];
+      SegState* st = &p.state[g];
       st->pool_n_pending = 0; st->pool_n_resid = 0; st->pool_off = 0;
       seg_status(p, g, TS_ERROR);
       continue;
@@ -726,7 +727,7 @@ __device__ __forceinline__ bool seg_begin(const Params& p, const SegInfo* info, 
 __device__ __forceinline__ void seg_end(const Params& p, LaneSeg& C, LaneStack& S) {
   const uint32_t sum_n = S.np + S.ne;
   const unsigned long long poff = sum_n ? atomicAdd(p.pool_used, (unsigned long long)sum_n) : 0ull;
-  TileState* st = &p.state[C.g];
+  SegState* st = &p.state[C.g];
   st->pool_off = poff;
   st->pool_n_pending = S.np;
   st->pool_n_resid = S.ne;
