@@ -285,8 +285,9 @@ __global__ void __launch_bounds__(128) seg_chain_kernel(Params p, SegW* segw, Se
 // telemetry records -- is queued per warp and drained 32 at a time with every
 // lane active, so one lane's long record does not stall the other 31.
 
-constexpr int kSQ = 64;            // deferred records per warp
-constexpr int kSegNameSlots = 256; // CTA cache of device-name hashes
+constexpr int kSQ = 64;            // deferred payload validations per warp (drained at 32)
+constexpr int kSQD = 40;           // deferred device/telemetry records per warp (drained at 8)
+constexpr int kSegNameSlots = 128; // CTA cache of device-name hashes
 
 struct SegSmem {
   uint32_t tab, lanetab, lanetab_warp, dcache, ncache, warps, warp_bytes, total;
@@ -307,8 +308,8 @@ __host__ __device__ inline SegSmem seg_smem_layout(uint32_t n_fn) {
   off += (uint32_t)((sizeof(NameSlot) * kSegNameSlots + 127) & ~(size_t)127);
   L.warps = off;
   // per warp: open-entry stack [kLS][32] (ts 8, meta 4, seq 4), pending exits [kLP][32]
-  // (ts 8, result 8, meta 4, seq 4), deferred queue [kSQ] (off 8, seq 8, prev 8, s 4, g 4)
-  L.warp_bytes = (uint32_t)(kLS * kWarp * 16 + kLP * kWarp * 24 + kSQ * 32);
+  // (ts 8, result 8, meta 4, seq 4), two deferred queues (off 8, seq 8, prev 8, s 4, g 4, sid 4, plen 4)
+  L.warp_bytes = (uint32_t)(kLS * kWarp * 16 + kLP * kWarp * 24 + (kSQ + kSQD) * 40);
   off += L.warp_bytes * kSegWarps;
   L.total = off;
   return L;
@@ -326,12 +327,14 @@ struct LaneStack {
   uint32_t np, ne;
 };
 
-struct SegQ {        // per-warp deferred queue (shared)
+struct SegQ {        // per-warp deferred queue (shared, SoA)
   uint64_t* off;
   uint64_t* seq;
   uint64_t* prev;
   uint32_t* s;
   uint32_t* g;       // segment | order-violation flag << 31
+  uint32_t* sid;
+  uint32_t* plen;
 };
 
 __device__ __forceinline__ uint8_t* seg_warp_base(const SegSmem& L) {
@@ -355,14 +358,18 @@ __device__ __forceinline__ LaneStack lane_stack(const SegSmem& L) {
   return S;
 }
 
-__device__ __forceinline__ SegQ seg_queue(const SegSmem& L) {
-  uint8_t* b = seg_warp_base(L) + kLS * kWarp * 16 + kLP * kWarp * 24;
+// queue 0: payload validations (kSQ entries); queue 1: device/telemetry work (kSQD)
+__device__ __forceinline__ SegQ seg_queue(const SegSmem& L, int which) {
+  const uint32_t cap = which ? kSQD : kSQ;
+  uint8_t* b = seg_warp_base(L) + kLS * kWarp * 16 + kLP * kWarp * 24 + (which ? kSQ * 40 : 0);
   SegQ Q;
   Q.off = reinterpret_cast<uint64_t*>(b);
-  Q.seq = reinterpret_cast<uint64_t*>(b + kSQ * 8);
-  Q.prev = reinterpret_cast<uint64_t*>(b + kSQ * 16);
-  Q.s = reinterpret_cast<uint32_t*>(b + kSQ * 24);
-  Q.g = reinterpret_cast<uint32_t*>(b + kSQ * 28);
+  Q.seq = reinterpret_cast<uint64_t*>(b + cap * 8);
+  Q.prev = reinterpret_cast<uint64_t*>(b + cap * 16);
+  Q.s = reinterpret_cast<uint32_t*>(b + cap * 24);
+  Q.g = reinterpret_cast<uint32_t*>(b + cap * 28);
+  Q.sid = reinterpret_cast<uint32_t*>(b + cap * 32);
+  Q.plen = reinterpret_cast<uint32_t*>(b + cap * 36);
   return Q;
 }
 
@@ -649,9 +656,34 @@ __device__ __forceinline__ void seg_status(const Params& p, uint32_t g, uint32_t
 }
 
 // drain n deferred records, one per lane
+// payload validation of variable records (tracefile.py:152-169); the exact error
+// (and the ordering error it takes precedence over) comes from the full walk
+__device__ __noinline__ void seg_drain_v(const Params& p, const SegSmem L, uint32_t n) {
+  const SegQ Q = seg_queue(L, 0);
+  const uint32_t lane = lane_id();
+  if (lane < n) {
+    const uint64_t a = Q.off[lane];
+    const uint32_t s = Q.s[lane], sid = Q.sid[lane], plen = Q.plen[lane];
+    const uint8_t* gb = p.data + p.stream_base[s];
+    uint32_t segs[5];
+    if (!g_var_plan(schema_of(p, sid), gb, a + 16, plen, segs)) {
+      uint64_t rp[HG_NUM_ROLES];
+      uint32_t rl[HG_NUM_ROLES];
+      uint64_t aux = 0;
+      const uint32_t err = seg_fields(p, gb, p.stream_size[s], a, sid, plen, rp, rl, aux, 0u);
+      if (err) {
+        push_error(p, err, s, Q.seq[lane], a, g64(gb, a + 4), Q.prev[lane], aux);
+        seg_status(p, Q.g[lane] & 0x7FFFFFFFu, TS_ERROR);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// device-profiling / telemetry records and ordering-failed variable records
 __device__ __noinline__ uint4 seg_drain(const Params& p, const SegSmem L, uint32_t n) {
   uint4 K = make_uint4(0, 0, 0, 0);  // device spans, samples, timeline messages
-  const SegQ Q = seg_queue(L);
+  const SegQ Q = seg_queue(L, 1);
   const uint32_t lane = lane_id();
   if (lane < n) {
     const uint64_t a = Q.off[lane], seq = Q.seq[lane], prev = Q.prev[lane];
@@ -862,9 +894,11 @@ __device__ __noinline__ void seg_epilogue(const Params& p, const SegSmem L, cons
 
 // one record with every check and rare case (errors, variable payloads, pending or
 // orphan exits, deep stacks, f64 results); returns true when the record is deferred
-__device__ __forceinline__ bool seg_record_full(const Params& p, LaneSeg& C, LaneStack& S, SegCounters& K, HostFold& hf,
-                                                bool tl, uint64_t& q_off, uint64_t& q_prev, bool& order_bad) {
-  bool defer = false;
+// returns 0 (nothing deferred), 1 (payload validation queue) or 2 (device/telemetry queue)
+__device__ __forceinline__ uint32_t seg_record_full(const Params& p, LaneSeg& C, LaneStack& S, SegCounters& K,
+                                                    HostFold& hf, bool tl, uint64_t& q_off, uint64_t& q_prev,
+                                                    bool& order_bad, uint32_t& q_sid, uint32_t& q_plen) {
+  uint32_t defer = 0;
   const uint32_t k = C.k++;
   const uint64_t a = C.o;
   const Hdr h = C.nh;
@@ -882,9 +916,12 @@ __device__ __forceinline__ bool seg_record_full(const Params& p, LaneSeg& C, Lan
     C.failed = true;
   } else {
     // payload checks of variable records, device and telemetry work: deferred
-    defer = var || cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY;
+    const bool dt = cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY;
+    defer = (dt || ob) ? 2u : (var ? 1u : 0u);
     q_off = a;
     q_prev = C.have_prev ? C.prev_ts : 0;
+    q_sid = h.sid;
+    q_plen = h.plen;
     order_bad = ob;
     if (ob) C.failed = true;  // var record: the drain names payload error or ordering
   }
@@ -1001,14 +1038,14 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
     hf.lt.err = b + 3 * nn; hf.lt.mn = b + 3 * nn + p.n_fn; hf.lt.mx = b + 3 * nn + 2 * p.n_fn;
   }
   LaneStack S = lane_stack(L);
-  const SegQ Q = seg_queue(L);
+  const SegQ QV = seg_queue(L, 0), QD = seg_queue(L, 1);
   const bool tl = p.tl_items != nullptr;
   const bool small = hf.small;
   const uint32_t nn = p.n_fn * kWarp;
   const uint32_t stride = gridDim.x * blockDim.x;
   LaneSeg C;
   bool have = seg_begin(p, info, blockIdx.x * blockDim.x + threadIdx.x, C);
-  uint32_t qn = 0;
+  uint32_t qn = 0, qd = 0;
   while (__any_sync(0xffffffffu, have)) {
     const bool act = have && C.k < C.n && !C.failed;
     // ---- fast path: entry push, matching exit pop, device/telemetry/meta pass-through
@@ -1033,8 +1070,10 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
     const bool f_exit = ok && isX && S.ne != 0 && tm == fnm;
     const bool f_other = ok && !isE && !isX;
     const bool fast = f_entry || f_exit || f_other;
-    bool defer = false, order_bad = false;
+    uint32_t defer = 0;  // 1: validation queue, 2: device/telemetry queue
+    bool order_bad = false;
     uint64_t q_off = a, q_prev = C.prev_ts;
+    uint32_t q_sid = h.sid, q_plen = h.plen;
     if (fast) {
       const uint32_t k = C.k++;
       C.o = a + 16 + h.plen;
@@ -1052,7 +1091,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
         S.ne++;
       }
       const bool dev_or_tel = cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY;
-      defer = dev_or_tel || var;
+      defer = dev_or_tel ? 2u : (var ? 1u : 0u);
       if (f_other && !dev_or_tel) K.passed++;
       uint64_t res = 0;
       if (f_exit) {
@@ -1087,7 +1126,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
     }
     const bool slow = act && !fast;
     if (__any_sync(0xffffffffu, slow)) {
-      if (slow) defer = seg_record_full(gpr, C, S, K, hf, tl, q_off, q_prev, order_bad);
+      if (slow) defer = seg_record_full(gpr, C, S, K, hf, tl, q_off, q_prev, order_bad, q_sid, q_plen);
     }
     const bool ending = have && !act;
     if (__any_sync(0xffffffffu, ending)) {
@@ -1096,30 +1135,54 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
         have = seg_begin(p, info, C.g + stride, C);
       }
     }
-    const uint32_t qm = __ballot_sync(0xffffffffu, defer);
+    const uint32_t qm = __ballot_sync(0xffffffffu, defer == 1u);
     if (qm) {
-      if (defer) {
+      if (defer == 1u) {
         const uint32_t i = qn + __popc(qm & lanemask_lt());
-        Q.off[i] = q_off; Q.seq[i] = C.base + C.k - 1; Q.prev[i] = q_prev; Q.s[i] = C.s;
-        Q.g[i] = C.g | (order_bad ? 0x80000000u : 0u);
+        QV.off[i] = q_off; QV.seq[i] = C.base + C.k - 1; QV.prev[i] = q_prev; QV.s[i] = C.s; QV.g[i] = C.g;
+        QV.sid[i] = q_sid; QV.plen[i] = q_plen;
       }
       qn += __popc(qm);
       __syncwarp();
       if (qn >= (uint32_t)kWarp) {
-        const uint4 dk = seg_drain(gpr, L, kWarp);
-        K.dev += dk.x; K.samples += dk.y; K.items += dk.z;
+        seg_drain_v(gpr, L, kWarp);
         qn -= kWarp;
         if (lane < qn) {
-          Q.off[lane] = Q.off[kWarp + lane]; Q.seq[lane] = Q.seq[kWarp + lane]; Q.prev[lane] = Q.prev[kWarp + lane];
-          Q.s[lane] = Q.s[kWarp + lane]; Q.g[lane] = Q.g[kWarp + lane];
+          QV.off[lane] = QV.off[kWarp + lane]; QV.seq[lane] = QV.seq[kWarp + lane]; QV.prev[lane] = QV.prev[kWarp + lane];
+          QV.s[lane] = QV.s[kWarp + lane]; QV.g[lane] = QV.g[kWarp + lane];
+          QV.sid[lane] = QV.sid[kWarp + lane]; QV.plen[lane] = QV.plen[kWarp + lane];
+        }
+        __syncwarp();
+      }
+    }
+    const uint32_t dm = __ballot_sync(0xffffffffu, defer == 2u);
+    if (dm) {
+      if (defer == 2u) {
+        const uint32_t i = qd + __popc(dm & lanemask_lt());
+        QD.off[i] = q_off; QD.seq[i] = C.base + C.k - 1; QD.prev[i] = q_prev; QD.s[i] = C.s;
+        QD.g[i] = C.g | (order_bad ? 0x80000000u : 0u);
+        QD.sid[i] = q_sid; QD.plen[i] = q_plen;
+      }
+      qd += __popc(dm);
+      __syncwarp();
+      if (qd >= 8u) {  // device work is rarer: drain smaller batches to keep the queue short
+        const uint32_t nd = qd < (uint32_t)kWarp ? qd : (uint32_t)kWarp;
+        const uint4 dk = seg_drain(gpr, L, nd);
+        K.dev += dk.x; K.samples += dk.y; K.items += dk.z;
+        qd -= nd;
+        if (lane < qd) {
+          QD.off[lane] = QD.off[nd + lane]; QD.seq[lane] = QD.seq[nd + lane]; QD.prev[lane] = QD.prev[nd + lane];
+          QD.s[lane] = QD.s[nd + lane]; QD.g[lane] = QD.g[nd + lane];
+          QD.sid[lane] = QD.sid[nd + lane]; QD.plen[lane] = QD.plen[nd + lane];
         }
         __syncwarp();
       }
     }
   }
   (void)nn;
-  if (qn) {
-    const uint4 dk = seg_drain(gpr, L, qn);
+  if (qn) seg_drain_v(gpr, L, qn);
+  if (qd) {
+    const uint4 dk = seg_drain(gpr, L, qd);
     K.dev += dk.x; K.samples += dk.y; K.items += dk.z;
   }
   seg_epilogue(gpr, L, K);
