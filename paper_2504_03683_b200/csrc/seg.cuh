@@ -272,7 +272,13 @@ __global__ void __launch_bounds__(128) seg_chain_kernel(Params p, SegW* segw, Se
     c_exit = __shfl_sync(0xffffffffu, W.exit, 31);
     if (fl < 32) c_dead = true;
   }
-  if (lane == 0) stream_nrec[s] = c_base;
+  if (lane == 0) {
+    stream_nrec[s] = c_base;
+    // IntervalStats.events_in and the global last timestamp (pipeline.py:152): every
+    // record of an error-free run is decoded, and timestamps rise along each stream
+    if (c_base) atomicAdd(&p.stats[ST_EVENTS], (unsigned long long)c_base);
+    if (c_has) atomicMax(p.last_ts, (unsigned long long)c_last);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -405,8 +411,7 @@ __device__ __forceinline__ bool go_deep(const Params& p, LaneStack& S, uint64_t 
 }
 
 struct SegCounters {
-  uint32_t events, passed, host, dev, samples, orph, items;
-  uint64_t last_ts;
+  uint32_t passed, host, dev, samples, orph, items;
 };
 
 // the lane's current segment
@@ -832,19 +837,16 @@ __device__ __noinline__ void seg_prologue(const Params& p, const SegSmem L) {
 __device__ __noinline__ void seg_epilogue(const Params& p, const SegSmem L, const SegCounters K) {
   const uint32_t lane = lane_id();
   auto wsum = [](uint32_t v) { return __reduce_add_sync(0xffffffffu, v); };
-  const uint32_t a0 = wsum(K.events), a1 = wsum(K.passed), a2 = wsum(K.host), a3 = wsum(K.dev), a4 = wsum(K.samples),
+  // events and the last timestamp come from the chain (every record of an error-free run is decoded)
+  const uint32_t a1 = wsum(K.passed), a2 = wsum(K.host), a3 = wsum(K.dev), a4 = wsum(K.samples),
                  a5 = wsum(K.orph), a6 = wsum(K.items);
-  uint64_t mts = K.last_ts;
-  for (int d = 16; d; d >>= 1) { const uint64_t v = __shfl_xor_sync(0xffffffffu, mts, d); mts = v > mts ? v : mts; }
   if (lane == 0) {
-    if (a0) atomicAdd(&p.stats[ST_EVENTS], (unsigned long long)a0);
     if (a1) atomicAdd(&p.stats[ST_PASSED], (unsigned long long)a1);
     if (a2) atomicAdd(&p.stats[ST_HOST], (unsigned long long)a2);
     if (a3) atomicAdd(&p.stats[ST_DEVICE], (unsigned long long)a3);
     if (a4) atomicAdd(&p.stats[ST_SAMPLES], (unsigned long long)a4);
     if (a5) atomicAdd(&p.stats[ST_ORPHANS], (unsigned long long)a5);
     if (a6) atomicAdd(p.tl_n, (unsigned long long)a6);  // record-indexed timeline messages
-    atomicMax(p.last_ts, (unsigned long long)mts);
   }
   __syncthreads();
   const uint32_t nn = p.n_fn * kWarp;
@@ -926,8 +928,6 @@ __device__ __forceinline__ uint32_t seg_record_full(const Params& p, LaneSeg& C,
     if (ob) C.failed = true;  // var record: the drain names payload error or ordering
   }
   if (C.failed) return defer;
-  K.events++;
-  K.last_ts = h.ts > K.last_ts ? h.ts : K.last_ts;
   C.prev_ts = h.ts;
   C.have_prev = true;
   bool item = cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY;  // written by the drain
@@ -1026,8 +1026,7 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
   seg_prologue(gpr, L);
   const uint32_t lane = lane_id();
   SegCounters K;
-  K.events = K.passed = K.host = K.dev = K.samples = K.orph = K.items = 0;
-  K.last_ts = 0;
+  K.passed = K.host = K.dev = K.samples = K.orph = K.items = 0;
   HostFold hf;
   hf.small = p.n_fn <= kSmallF;
   hf.tab = (!hf.small && p.n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(g_smem + L.tab) : nullptr;
@@ -1081,8 +1080,6 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
       if (((C.o + 256) ^ (a + 256)) >> 7)  // entering a new 128-byte line: pull the one two lines ahead into L1
         asm volatile("prefetch.global.L1 [%0];" ::"l"(C.gbase + C.o + 256));
 
-      K.events++;
-      K.last_ts = h.ts > K.last_ts ? h.ts : K.last_ts;
       C.prev_ts = h.ts;
       C.have_prev = true;
       if (f_entry) {
