@@ -211,6 +211,20 @@ int hg_device_tally(hg_ctx* ctx, void** host_rows, uint64_t* n_host_rows);
 int hg_last_timing(hg_ctx* ctx, float* kernel_ms, float* total_ms, uint64_t* h2d_bytes, uint64_t* d2h_bytes,
                    uint64_t* kernel_launches);
 
+/* engine options.  HG_OPT_PATH: 0 = single pass over HBM (fast.cuh) with the
+ * exact three-kernel path as fallback whenever the single pass cannot vouch for
+ * its result (any trace error, a wrong range speculation), 1 = exact path only,
+ * 2 = single pass only (a trace it rejects fails with HG_ESTATE; tests).
+ * HG_OPT_RANGE_BYTES: bytes per single-pass range (0 = sized so that one range
+ * runs per resident lane).  The environment variable HAPIGPU_PATH sets the
+ * default path at hg_create. */
+#define HG_OPT_PATH 1u
+#define HG_OPT_RANGE_BYTES 2u
+int hg_set_option(hg_ctx* ctx, uint32_t key, uint64_t value);
+/* which phase-1 path produced the last result (1 single pass, 0 exact), how many
+ * single-pass results were discarded so far, and the range size used */
+int hg_last_path(hg_ctx* ctx, uint32_t* path, uint64_t* fallbacks, uint32_t* range_bytes);
+
 #ifdef __cplusplus
 }
 #endif

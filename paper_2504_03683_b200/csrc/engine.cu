@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -23,6 +24,7 @@
 #include "kernels.cuh"
 #include "timeline.cuh"
 #include "seg.cuh"
+#include "fast.cuh"
 
 using namespace hg;
 
@@ -299,6 +301,20 @@ struct hg_ctx {
   DBuf<SumEntry> d_deep;
   uint64_t deep_cap = 0;
   DBuf<Params> d_params;
+  // single-pass range path (fast.cuh)
+  int path_opt = 0;                 // 0 auto (fast, exact on anomaly), 1 exact only, 2 fast only
+  uint32_t range_opt = 0;           // forced range bytes (0 = sized to the resident lanes)
+  uint32_t range_bytes = 0, n_ranges = 0, fast_warps = 0;
+  std::vector<uint32_t> range_stream, stream_range0;
+  DBuf<uint32_t> d_range_stream, d_stream_range0;
+  DBuf<RangeState> d_rstate;
+  DBuf<SegState> d_rseg;
+  DBuf<unsigned long long> d_range_base;
+  std::vector<uint32_t> vplan;
+  DBuf<uint32_t> d_vplan;
+  int last_path = 0;                // 1 = the last run's phase 1 was the single pass
+  uint64_t fallbacks = 0;
+  int smem_optin = 0;
 };
 
 // counter slots in d_counters
@@ -321,7 +337,8 @@ enum {
   C_DEEP_USED = 22,       // deep lane-stack chunks handed out
   C_TL_N2 = 23,           // timeline messages appended by compose
   C_REC_TOTAL = 24,       // records of all streams (timeline slots)
-  C_NUM = 25
+  C_ANOM = 25,            // unsigned int: single-pass result void (fast.cuh)
+  C_NUM = 26
 };
 
 static int fail(hg_ctx* c, int code, const std::string& msg) {
@@ -546,6 +563,8 @@ int hg_create(const hg_config* cfg, hg_ctx** out) {
   CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   for (auto& ev : ctx->ev) CK(cudaEventCreate(&ev));
   CK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, ctx->cfg.device));
+  CK(cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->cfg.device));
+  if (const char* e = getenv("HAPIGPU_PATH")) ctx->path_opt = atoi(e);
   return HG_OK;
 }
 
@@ -569,6 +588,8 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_tl_th_first.release(); ctx->d_tl_th_hi.release(); ctx->d_tl_th_lo.release();
   ctx->d_segw.release(); ctx->d_seginfo.release(); ctx->d_stream_nrec.release(); ctx->d_tl_rec_off.release();
   ctx->d_deep.release(); ctx->d_params.release();
+  ctx->d_range_stream.release(); ctx->d_stream_range0.release(); ctx->d_rstate.release(); ctx->d_rseg.release();
+  ctx->d_range_base.release(); ctx->d_vplan.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -648,6 +669,13 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
   if (n_functions >= (1u << 19) - 1) return fail(ctx, HG_EUNSUPPORTED, "more than 2^19-2 distinct functions");
   ctx->n_fn = n_functions;
   ctx->max_sid = n_schemas ? max_sid : 0;
+  // single-variable-field payload plans for the range kernel's inline checks
+  ctx->vplan.assign(ctx->sid_map.size(), 0u);
+  for (uint32_t i = 0; i < n_schemas; i++) {
+    const DSchema& d = ctx->schemas[ctx->sid_map[schemas[i].id]];
+    if ((d.flags & SF_VAR) && d.nvar == 1 && d.lead[0] < 0x4000 && d.lead[1] < 0x4000)
+      ctx->vplan[schemas[i].id] = VP_VALID | (d.vkind[0] ? VP_STR : 0u) | ((uint32_t)d.lead[1] << 14) | d.lead[0];
+  }
   // compact descriptors: x = fn(20) | cls(3)<<20 | flags(8)<<23 (top bit = present); y = fixed_len | result field<<16
   ctx->desc.assign(ctx->sid_map.size(), make_uint2(0, 0));
   for (uint32_t i = 0; i < n_schemas; i++) {
@@ -660,9 +688,15 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
     if ((d.flags & SF_VAR) && (d.flags & SF_RESULT) && !(d.nvar != kNoPlan && d.role_seg[HG_ROLE_RESULT] == 0 &&
                                                          d.role_delta[HG_ROLE_RESULT] == 8u * resf))
       resf = 0xFFu;
+    const bool dt = d.cls == HG_CLASS_DEVICE || d.cls == HG_CLASS_TELEMETRY;
+    if ((d.flags & (SF_RESULT_F64 | SF_FEED_ALWAYS)) || ((d.flags & SF_RESULT) && resf > 5u) ||  // result within 64 B
+        ((d.flags & SF_VAR) && !dt && !(ctx->vplan[schemas[i].id] & VP_VALID)))
+      flags |= SF_NOINLINE;
     ctx->desc[schemas[i].id] = make_uint2((fn & 0xFFFFFu) | ((uint32_t)d.cls << 20) | (flags << 23) | D_PRESENT,
                                           (uint32_t)d.fixed_len | ((resf & 0xFFu) << 16) | ((uint32_t)d.counter_kind << 24));
   }
+  ctx->fast_warps = 0;
+  ctx->staged = false;
   cudaSetDevice(ctx->cfg.device);
   CK(ctx->d_schemas.ensure(std::max<size_t>(ctx->schemas.size(), 1)));
   CK(ctx->d_sid_map.ensure(ctx->sid_map.size()));
@@ -673,6 +707,8 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
   CK(cudaMemcpy(ctx->d_sid_map.ptr, ctx->sid_map.data(), ctx->sid_map.size() * 4, cudaMemcpyHostToDevice));
   CK(ctx->d_desc.ensure(ctx->desc.size()));
   CK(cudaMemcpy(ctx->d_desc.ptr, ctx->desc.data(), ctx->desc.size() * sizeof(uint2), cudaMemcpyHostToDevice));
+  CK(ctx->d_vplan.ensure(ctx->vplan.size()));
+  CK(cudaMemcpy(ctx->d_vplan.ptr, ctx->vplan.data(), ctx->vplan.size() * 4, cudaMemcpyHostToDevice));
   if (n_kinds) {
     CK(cudaMemcpy(ctx->d_kinds.ptr, kinds, n_kinds, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_field_role.ptr, ctx->field_role.data(), n_kinds, cudaMemcpyHostToDevice));
@@ -717,6 +753,36 @@ static int build_layout(hg_ctx* ctx) {
     const uint32_t nt = sz > 16 ? (uint32_t)((sz - 16 + ctx->seg_bytes - 1) / ctx->seg_bytes) : 0;
     for (uint32_t t = 0; t < nt; t++) ctx->tile_stream.push_back(s);
   }
+  // ranges for the single pass: one per resident lane, never crossing a stream
+  uint32_t nw = 8;
+  while (nw > 1 && fast_smem_layout(ctx->n_fn, nw).total > (uint32_t)ctx->smem_optin) nw--;
+  ctx->fast_warps = nw;
+  const uint64_t lanes = (uint64_t)std::max(ctx->sm_count, 1) * nw * kWarp;
+  uint64_t payload = 0, max_pay = 0;
+  for (uint32_t s = 0; s < ns; s++) {
+    const uint64_t pay = ctx->sizes[s] > 16 ? ctx->sizes[s] - 16 : 0;
+    payload += pay;
+    max_pay = std::max(max_pay, pay);
+  }
+  auto count = [&](uint64_t R) {
+    uint64_t c = 0;
+    for (uint32_t s = 0; s < ns; s++) c += ctx->sizes[s] > 16 ? (ctx->sizes[s] - 16 + R - 1) / R : 0;
+    return c;
+  };
+  uint64_t R = ctx->range_opt ? ctx->range_opt : std::max<uint64_t>(1024, (payload + lanes - 1) / lanes);
+  R = (R + 15) & ~15ull;
+  if (!ctx->range_opt)
+    while (count(R) > lanes && R < max_pay) R = ((R + R / 16) + 15) & ~15ull;
+  R = std::min<uint64_t>(R, 1ull << 28);
+  ctx->range_bytes = (uint32_t)R;
+  ctx->range_stream.clear();
+  ctx->stream_range0.assign(ns, 0);
+  for (uint32_t s = 0; s < ns; s++) {
+    ctx->stream_range0[s] = (uint32_t)ctx->range_stream.size();
+    const uint64_t nr = ctx->sizes[s] > 16 ? (ctx->sizes[s] - 16 + R - 1) / R : 0;
+    for (uint64_t j = 0; j < nr; j++) ctx->range_stream.push_back(s);
+  }
+  ctx->n_ranges = (uint32_t)ctx->range_stream.size();
   return HG_OK;
 }
 
@@ -747,6 +813,14 @@ static int stage(hg_ctx* ctx) {
     CK(cudaMemcpyAsync(ctx->d_tile_stream.ptr, ctx->tile_stream.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
   }
   if (ns) CK(cudaMemcpyAsync(ctx->d_stream_tile0.ptr, ctx->stream_tile0.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream));
+  const size_t nr = ctx->n_ranges;
+  CK(ctx->d_range_stream.ensure(std::max<size_t>(nr, 1)));
+  CK(ctx->d_stream_range0.ensure(std::max<uint32_t>(ns, 1)));
+  CK(ctx->d_rstate.ensure(std::max<size_t>(nr, 1)));
+  CK(ctx->d_rseg.ensure(std::max<size_t>(nr, 1)));
+  CK(ctx->d_range_base.ensure(std::max<size_t>(nr, 1)));
+  if (nr) CK(cudaMemcpyAsync(ctx->d_range_stream.ptr, ctx->range_stream.data(), nr * 4, cudaMemcpyHostToDevice, ctx->stream));
+  if (ns) CK(cudaMemcpyAsync(ctx->d_stream_range0.ptr, ctx->stream_range0.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->d_state.n < nt) {
     CK(ctx->d_state.ensure(nt));
     CK(cudaMemsetAsync(ctx->d_state.ptr, 0, nt * sizeof(SegState), ctx->stream));
@@ -861,11 +935,19 @@ static Params make_params(hg_ctx* ctx) {
   p.deep = ctx->d_deep.ptr;
   p.deep_used = C + C_DEEP_USED;
   p.deep_cap = ctx->deep_cap;
+  p.range_stream = ctx->d_range_stream.ptr;
+  p.stream_range0 = ctx->d_stream_range0.ptr;
+  p.n_ranges = ctx->n_ranges;
+  p.range_bytes = ctx->range_bytes;
+  p.rstate = ctx->d_rstate.ptr;
+  p.range_base = ctx->d_range_base.ptr;
+  p.anom = reinterpret_cast<uint32_t*>(C + C_ANOM);
+  p.vplan = ctx->d_vplan.ptr;
   return p;
 }
 
-static int launch_phase1(hg_ctx* ctx) {
-  const uint32_t nt = (uint32_t)ctx->tile_stream.size();
+// per-run resets shared by both phase-1 paths
+static int init_run(hg_ctx* ctx) {
   const uint32_t ns = (uint32_t)ctx->streams.size();
   ctx->epoch++;
   if (ctx->epoch >= (1u << 29)) {
@@ -880,6 +962,42 @@ static int launch_phase1(hg_ctx* ctx) {
   init_acc_kernel<<<(nmax + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_host_acc.ptr, ctx->n_fn, ctx->d_dev_acc.ptr,
                                                                 ctx->row_cap);
   ctx->launches = 1;
+  return HG_OK;
+}
+
+// the single pass (fast.cuh): range kernel, chain verification, orphan index fix-up
+static int launch_fast(hg_ctx* ctx) {
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  int rc = init_run(ctx);
+  if (rc) return rc;
+  if (!ctx->n_ranges) return HG_OK;
+  Params p = make_params(ctx);
+  p.state = ctx->d_rseg.ptr;
+  const uint32_t nw = ctx->fast_warps;
+  const size_t smem = fast_smem_layout(ctx->n_fn, nw).total;
+  CK(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const uint32_t per_cta = nw * kWarp;
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));
+  CK(ctx->d_params.ensure(1));
+  CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+  CK(cudaEventRecord(ctx->ev[6], ctx->stream));
+  fast_kernel<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+  fast_verify_kernel<<<(ns + 3) / 4, 128, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
+  fast_orphan_fix_kernel<<<32, 256, 0, ctx->stream>>>(p);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[5], ctx->stream));
+  ctx->launches += 3;
+  return HG_OK;
+}
+
+static int launch_phase1(hg_ctx* ctx) {
+  const uint32_t nt = (uint32_t)ctx->tile_stream.size();
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  int rc0 = init_run(ctx);
+  if (rc0) return rc0;
   if (nt) {
     Params p = make_params(ctx);
     const size_t dsm = sizeof(uint2) * kSdescMax;
@@ -934,7 +1052,8 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->want = want;
   ctx->have_results = false;
   ctx->phase1_done = false;
-  for (int attempt = 0; attempt < 6; attempt++) {
+  bool fast = ctx->path_opt != 1 && !(want & HG_WANT_TIMELINE);
+  for (int attempt = 0; attempt < 8; attempt++) {
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
     uint64_t h2d = 0;
     if (!ctx->staged) {
@@ -945,7 +1064,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     int rc = ensure_scratch(ctx, 0);
     if (rc) return rc;
-    rc = launch_phase1(ctx);
+    rc = fast ? launch_fast(ctx) : launch_phase1(ctx);
     if (rc) return rc;
     rc = read_counters(ctx);
     if (rc) return rc;
@@ -960,9 +1079,17 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
       ctx->row_cap *= 4; ctx->dict_mask = ctx->dict_mask * 4 + 3; ctx->arena_cap = std::max<uint64_t>(ctx->arena_cap * 4, C[C_ARENA_USED] * 2);
       grow = true;
     }
+    if (!grow && fast && (uint32_t)ctx->counters[C_ANOM]) {
+      // the single pass met something it does not reproduce exactly: rerun the exact path
+      if (ctx->path_opt == 2) return fail(ctx, HG_ESTATE, "single-pass path rejected the trace (HAPIGPU_PATH=2)");
+      fast = false;
+      ctx->fallbacks++;
+      continue;
+    }
     if (!grow) break;
-    if (attempt == 5) return fail(ctx, HG_ENOMEM, "scratch buffers kept overflowing");
+    if (attempt == 7) return fail(ctx, HG_ENOMEM, "scratch buffers kept overflowing");
   }
+  ctx->last_path = fast ? 1 : 0;
   if ((uint32_t)ctx->counters[C_WATCHDOG])
     return fail(ctx, HG_ECUDA, "tile look-back watchdog fired (engine bug)");
   if ((uint32_t)ctx->counters[C_WIDE])
@@ -988,6 +1115,11 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
     if (ns) {
       Params p = make_params(ctx);
       p.global_last_ts = global_last_ts;
+      if (ctx->last_path == 1) {  // summaries per range (fast.cuh)
+        p.state = ctx->d_rseg.ptr;
+        p.stream_tile0 = ctx->d_stream_range0.ptr;
+        p.n_tiles = ctx->n_ranges;
+      }
       unsigned long long zero = 0;
       CK(cudaMemcpyAsync(p.stack_used, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
       // the tally accumulators already hold phase-1 spans; compose adds the rest
@@ -1200,6 +1332,29 @@ int hg_device_tally(hg_ctx* ctx, void** host_rows, uint64_t* n_host_rows) {
   if (!ctx) return HG_EARG;
   if (host_rows) *host_rows = ctx->d_host_acc.ptr;
   if (n_host_rows) *n_host_rows = ctx->n_fn;
+  return HG_OK;
+}
+
+int hg_set_option(hg_ctx* ctx, uint32_t key, uint64_t value) {
+  if (!ctx) return HG_EARG;
+  if (key == HG_OPT_PATH) {
+    if (value > 2) return fail(ctx, HG_EARG, "path option: 0 auto, 1 exact, 2 single pass");
+    ctx->path_opt = (int)value;
+  } else if (key == HG_OPT_RANGE_BYTES) {
+    if (value && (value < 16 || value > (1ull << 28))) return fail(ctx, HG_EARG, "range bytes out of [16, 2^28]");
+    ctx->range_opt = (uint32_t)((value + 15) & ~15ull);
+    ctx->staged = false;
+  } else {
+    return fail(ctx, HG_EARG, "unknown option");
+  }
+  return HG_OK;
+}
+
+int hg_last_path(hg_ctx* ctx, uint32_t* path, uint64_t* fallbacks, uint32_t* range_bytes) {
+  if (!ctx) return HG_EARG;
+  if (path) *path = (uint32_t)ctx->last_path;
+  if (fallbacks) *fallbacks = ctx->fallbacks;
+  if (range_bytes) *range_bytes = ctx->range_bytes;
   return HG_OK;
 }
 

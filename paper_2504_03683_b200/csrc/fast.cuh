@@ -1,0 +1,764 @@
+// fast.cuh -- phase 1 in ONE pass over HBM: the range kernel (sm_100a).
+//
+// Every stream is cut into contiguous byte ranges, one range per resident lane
+// (total_bytes / resident lanes each, so the grid is a single wave).  A lane
+// runs the reference's sequential algorithm over its range:
+//   decode every record (tracefile.py:147-215), the per-stream ordering check
+//   (pipeline.py:98), the IntervalBuilder LIFO automaton (pipeline.py:156-185)
+//   and the tally fold (sinks.py:123-132, 230-242),
+// reading the bytes from a private 512-byte ring in shared memory.  The warp
+// refills the rings cooperatively: every iteration the lanes that freed a
+// 128-byte slot are served four at a time by one cp.async (LDGSTS.128) warp
+// instruction (8 lanes x 16 B per line, whole coalesced lines), one commit
+// group per iteration; `cp.async.wait_group kRLag` then proves every group
+// older than kRLag iterations complete, so a lane may read a slot once its fill
+// group is that old.  HBM is read once, in whole lines; every record access is
+// an LDS.
+//
+// Range starts are speculative (first offset with three consistent record
+// headers).  fast_verify_kernel then checks, per stream, that every range
+// starts where the previous one ended and that timestamps keep rising across
+// ranges; it turns the range summaries into compose_kernel's input (pending
+// exits, open entries) and the record bases.  Anything the single pass does
+// not reproduce exactly -- any decode / ordering / telemetry error, a wrong
+// speculation, a NaN/inf f64 result -- sets `anom`, and the host discards the
+// pass and runs the exact three-kernel path (seg.cuh), which reports errors
+// with the reference's precedence.  A clean trace therefore costs one read.
+#pragma once
+#include "seg.cuh"
+
+namespace hg {
+
+constexpr uint32_t kRChunk = 128;                   // bytes per ring slot (one line)
+constexpr uint32_t kRSlots = 4;                     // slots per lane
+constexpr uint32_t kRRing = kRChunk * kRSlots;      // 512-byte ring
+constexpr uint32_t kRWordMask = kRRing / 4 - 1;
+constexpr uint32_t kRMirror = 64;                   // slot 0's first bytes again after the ring
+constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: any 64-byte read needs no wrap
+constexpr uint32_t kRInline = kRChunk;              // records up to this long are decoded from the ring
+constexpr int kRLag = 4;                            // iterations before a fill group is waited for
+constexpr int kRLS = 8;                             // open entries per lane in shared memory
+constexpr int kRLP = 4;                             // pending exits per lane in shared memory
+constexpr int kRQ = 64;                             // deferred-record queue per warp (drained at 32)
+constexpr uint32_t kRDeep = 256;                    // per-lane overflow chunk (SumEntry)
+constexpr uint32_t kRDeepHalf = kRDeep / 2;         // [0,128) pending exits, [128,256) open entries
+
+struct RangeState {
+  uint64_t entry;      // speculative first record (kNone: no plausible header in the range)
+  uint64_t exit;       // offset after the last record
+  uint64_t first_ts, last_ts;
+  uint64_t pool_off;   // summary: np pending exits, then ne open entries (bottom..top)
+  uint32_t n, np, ne, pad;
+};
+
+// single-field variable payload plan per schema id (vplan): valid << 31 | string << 30 |
+// trailing fixed bytes << 14 | leading fixed bytes
+constexpr uint32_t VP_VALID = 1u << 31, VP_STR = 1u << 30;
+
+struct RSmem {
+  uint32_t tab, lanetab, lanetab_warp, dcache, ncache, warps, warp_bytes, total;
+  uint32_t ring, st_ts, st_fn, pd_ts, pd_meta, pd_k, q_off, q_s, ftab, ferr;  // within a warp block
+};
+
+__host__ __device__ inline uint32_t r_align(uint32_t x) { return (x + 127u) & ~127u; }
+
+__host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw) {
+  RSmem L;
+  uint32_t off = r_align(8u * kSdescMax);  // compact descriptors first (desc_of, kernels.cuh)
+  const bool small = n_fn <= kSmallF;
+  L.tab = off;
+  if (!small && n_fn <= kSmemFnMax) off += r_align((uint32_t)sizeof(SmemRow) * n_fn);
+  L.lanetab = off;  // unused (the per-lane fold table lives in the warp block)
+  L.lanetab_warp = 0;
+  L.dcache = off;
+  off += r_align((uint32_t)sizeof(DevRow) * kDevSlots);
+  L.ncache = off;
+  off += r_align((uint32_t)sizeof(NameSlot) * kSegNameSlots);
+  L.warps = off;
+  uint32_t w = 0;
+  L.ring = w;    w += kRStride * kWarp;
+  L.ftab = w;    w += small ? 16u * n_fn * kWarp : 0u;   // [fn][lane] {count << 44 | sum (u64), min, max}
+  L.ferr = w;    w += small ? 4u * n_fn : 0u;            // [fn] error count
+  w = (w + 15u) & ~15u;
+  L.st_ts = w;   w += 8u * kRLS * kWarp;
+  L.st_fn = w;   w += 4u * kRLS * kWarp;
+  L.pd_ts = w;   w += 8u * kRLP * kWarp;
+  L.pd_meta = w; w += 4u * kRLP * kWarp;
+  L.pd_k = w;    w += 4u * kRLP * kWarp;
+  L.q_off = w;   w += 8u * kRQ;
+  L.q_s = w;     w += 4u * kRQ;
+  L.warp_bytes = r_align(w);
+  off += L.warp_bytes * nw;
+  L.total = off;
+  return L;
+}
+
+// SegSmem view of the shared tables, for the helpers shared with seg.cuh
+__device__ __forceinline__ SegSmem r_segsmem(const RSmem& R) {
+  SegSmem L;
+  L.tab = R.tab; L.lanetab = R.lanetab; L.lanetab_warp = R.lanetab_warp; L.dcache = R.dcache; L.ncache = R.ncache;
+  L.warps = R.warps; L.warp_bytes = R.warp_bytes; L.total = R.total;
+  return L;
+}
+
+__device__ __forceinline__ uint32_t s_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// ---- ring reads (the ring word index wraps)
+
+__device__ __forceinline__ uint32_t r_u32(const uint32_t* ring, uint32_t bp) {
+  const uint32_t wi = bp >> 2;
+  return __funnelshift_r(ring[wi & kRWordMask], ring[(wi + 1) & kRWordMask], (bp & 3u) << 3);
+}
+__device__ __forceinline__ uint64_t r_u64(const uint32_t* ring, uint32_t bp) {
+  const uint32_t wi = bp >> 2, sh = (bp & 3u) << 3;
+  const uint32_t a = ring[wi & kRWordMask], b = ring[(wi + 1) & kRWordMask], c = ring[(wi + 2) & kRWordMask];
+  return ((uint64_t)__funnelshift_r(b, c, sh) << 32) | __funnelshift_r(a, b, sh);
+}
+
+// ---- the lane's range (offsets relative to C0, the 128-aligned start of ring chunk 0)
+
+struct RLane {
+  const uint8_t* g;     // stream bytes from C0
+  uint64_t C0;          // stream offset of chunk 0
+  uint64_t size;        // stream size - C0
+  uint64_t prev_ts, first_ts;
+  SumEntry* deep;       // overflow chunk (nullptr until needed)
+  uint32_t o, t1, entry;
+  uint32_t r, s, n, spans;
+  uint32_t ci, clast;   // chunks requested, last chunk this range reads
+  uint32_t recent;      // bit i: a chunk was requested i iterations ago (its fill group may be pending)
+  uint32_t np, ne;
+  bool bad;
+  bool fresh;           // no requests until every pending fill of this lane completed (slot reuse)
+};
+
+// first offset in [t0, t1) with three consistent headers (see seg_walk_kernel)
+__device__ __noinline__ uint64_t r_scan(const Params& p, const uint8_t* g, uint64_t size, uint64_t t0, uint64_t t1) {
+  for (uint64_t o = t0; o < t1; o++) {
+    uint64_t n1, n2, n3, ts0, ts1, ts2;
+    if (!seg_plausible(p, g, size, o, n1, ts0)) continue;
+    if (n1 != size) {
+      if (!seg_plausible(p, g, size, n1, n2, ts1) || ts1 < ts0) continue;
+      if (n2 != size && (!seg_plausible(p, g, size, n2, n3, ts2) || ts2 < ts1)) continue;
+    }
+    return o;
+  }
+  return kNone;
+}
+
+// open the lane's next range (ranges without a plausible header are recorded and skipped)
+__device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, uint32_t stride) {
+  for (; r < p.n_ranges; r += stride) {
+    const uint32_t s = p.range_stream[r];
+    const uint32_t j = r - p.stream_range0[s];
+    const uint64_t size = p.stream_size[s];
+    const uint8_t* g = p.data + p.stream_base[s];
+    const uint64_t t0 = 16 + (uint64_t)j * p.range_bytes;
+    const uint64_t t1 = min(t0 + (uint64_t)p.range_bytes, size);
+    const uint64_t entry = j == 0 ? 16ull : r_scan(p, g, size, t0, t1);
+    if (entry == kNone) {
+      RangeState st;
+      st.entry = kNone; st.exit = kNone; st.first_ts = 0; st.last_ts = 0; st.pool_off = 0;
+      st.n = 0; st.np = 0; st.ne = 0; st.pad = 0;
+      p.rstate[r] = st;
+      continue;
+    }
+    R.C0 = entry & ~(uint64_t)(kRChunk - 1);
+    R.g = g + R.C0;
+    R.size = size - R.C0;
+    R.o = (uint32_t)(entry - R.C0);
+    R.entry = R.o;
+    R.t1 = (uint32_t)(t1 - R.C0);
+    // chunks this range can read from the ring: records that start before t1 and fit kRInline
+    R.clast = (uint32_t)min((size - 1 - R.C0) / kRChunk, (uint64_t)(R.t1 + kRInline - 1) / kRChunk);
+    R.ci = 0; R.fresh = true;
+    R.prev_ts = 0; R.first_ts = 0;
+    R.deep = nullptr;
+    R.r = r; R.s = s; R.n = 0; R.spans = 0; R.np = 0; R.ne = 0; R.bad = false;
+    return true;
+  }
+  R.r = p.n_ranges;
+  R.o = R.t1 = R.entry = 0; R.C0 = 0; R.size = 0; R.g = p.data;
+  R.n = R.np = R.ne = R.ci = R.clast = 0;
+  R.bad = false; R.fresh = true;
+  return false;
+}
+
+struct RTabs {           // the lane's views of its warp block
+  uint64_t* st_ts; uint32_t* st_fn;                     // [kRLS][32], pre-offset by lane
+  uint64_t* pd_ts; uint32_t* pd_meta; uint32_t* pd_k;   // [kRLP][32]
+};
+
+__device__ __forceinline__ RTabs r_tabs(const RSmem& L) {
+  const uint32_t lane = lane_id();
+  uint8_t* b = g_smem + L.warps + (threadIdx.x >> 5) * L.warp_bytes;
+  RTabs T;
+  T.st_ts = reinterpret_cast<uint64_t*>(b + L.st_ts) + lane;
+  T.st_fn = reinterpret_cast<uint32_t*>(b + L.st_fn) + lane;
+  T.pd_ts = reinterpret_cast<uint64_t*>(b + L.pd_ts) + lane;
+  T.pd_meta = reinterpret_cast<uint32_t*>(b + L.pd_meta) + lane;
+  T.pd_k = reinterpret_cast<uint32_t*>(b + L.pd_k) + lane;
+  return T;
+}
+
+// summary + range state.  Fills still in flight for this lane's slots are harmless:
+// the next range requests its chunks in later groups and reads them only once those
+// groups are proven complete (groups complete in order).
+__device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T) {
+  const uint32_t sum_n = R.np + R.ne;
+  const unsigned long long poff = sum_n ? atomicAdd(p.pool_used, (unsigned long long)sum_n) : 0ull;
+  if (poff + sum_n <= p.pool_cap) {
+    for (uint32_t i = 0; i < R.np; i++) {
+      SumEntry e;
+      if (i < (uint32_t)kRLP) {
+        e.ts = T.pd_ts[i * kWarp]; e.result = 0;  // result bits only feed the timeline (exact path)
+        const uint32_t m = T.pd_meta[i * kWarp];
+        e.fn = m_fn(m); e.flags = m >> 19; e.seq = T.pd_k[i * kWarp];
+      } else {
+        e = R.deep[i - kRLP];
+      }
+      p.pool[poff + i] = e;
+    }
+    for (uint32_t i = 0; i < R.ne; i++) {
+      SumEntry e;
+      if (i < (uint32_t)kRLS) {
+        e.ts = T.st_ts[i * kWarp];
+        e.fn = m_fn(T.st_fn[i * kWarp]);
+        e.seq = 0; e.flags = 0; e.result = 0;
+      } else {
+        e = R.deep[kRDeepHalf + i - kRLS];
+      }
+      p.pool[poff + R.np + i] = e;
+    }
+  }
+  RangeState st;
+  st.entry = R.C0 + R.entry; st.exit = R.C0 + R.o; st.first_ts = R.first_ts; st.last_ts = R.prev_ts;
+  st.pool_off = poff;
+  st.n = R.n; st.np = R.np; st.ne = R.ne; st.pad = 0;
+  p.rstate[R.r] = st;
+  if (R.spans) atomicAdd(&p.stream_spans[R.s], (unsigned long long)R.spans);
+  if (R.bad) atomicExch(p.anom, 1u);
+}
+
+// a per-lane overflow chunk for deep stacks / many pending exits
+__device__ __forceinline__ bool r_deep(const Params& p, RLane& R) {
+  if (R.deep) return true;
+  const unsigned long long off = atomicAdd(p.deep_used, (unsigned long long)kRDeep);
+  if (off + kRDeep > p.deep_cap) return false;  // the host grows the pool and reruns
+  R.deep = p.deep + off;
+  return true;
+}
+
+// every record the inline path does not take, decoded from HBM: long records,
+// payload plans other than one variable field, deep stacks, orphans, f64 results.
+// Returns true when the record goes to the deferred queue.
+__device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const RTabs& T, SegCounters& K,
+                                              const HostFold& hf) {
+  const uint64_t a = R.o;  // relative to C0
+  if (a + 16 > R.size) { R.bad = true; return false; }           // truncated header
+  const Hdr h = g_hdr(R.g, a);
+  const uint2 d = desc_of(p, h.sid);
+  if (!d_present(d)) { R.bad = true; return false; }             // unknown schema
+  const uint64_t L = 16ull + h.plen;
+  if (a + L > R.size) { R.bad = true; return false; }            // truncated payload
+  const uint32_t cls = d_cls(d), fl = d_flags(d);
+  const bool var = (fl & SF_VAR) != 0;
+  if (var ? h.plen < d_fixed(d) : h.plen != d_fixed(d)) { R.bad = true; return false; }
+  if (R.n && h.ts < R.prev_ts) { R.bad = true; return false; }  // MuxOrderingError
+  if (fl & SF_FEED_ALWAYS) { R.bad = true; return false; }
+  const bool dt = cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY;
+  uint64_t rp[HG_NUM_ROLES];
+  uint32_t rl[HG_NUM_ROLES];
+  uint64_t aux = 0;
+  const bool want_res = cls == HG_CLASS_EXIT && (fl & SF_RESULT);
+  if (var && !dt) {  // stream offsets for seg_fields: C0 is 128-aligned, so alignment is unchanged
+    if (seg_fields(p, R.g, R.size, a, h.sid, h.plen, rp, rl, aux, want_res ? (1u << HG_ROLE_RESULT) : 0u)) {
+      R.bad = true;
+      return false;
+    }
+  }
+  const uint32_t k = R.n++;
+  if (!k) R.first_ts = h.ts;
+  R.prev_ts = h.ts;
+  R.o = (uint32_t)(a + L);
+  if (dt) return true;
+  const uint32_t fnm = d.x & M_FN;
+  if (cls == HG_CLASS_ENTRY) {
+    const uint32_t i = R.ne;
+    if (i < (uint32_t)kRLS) {
+      T.st_ts[i * kWarp] = h.ts; T.st_fn[i * kWarp] = fnm;
+    } else {
+      if (i >= (uint32_t)kRLS + kRDeepHalf || !r_deep(p, R)) { R.bad = true; return false; }
+      SumEntry e;
+      e.ts = h.ts; e.seq = 0; e.fn = m_fn(fnm); e.flags = 0; e.result = 0;
+      R.deep[kRDeepHalf + i - kRLS] = e;
+    }
+    R.ne = i + 1;
+  } else if (cls == HG_CLASS_EXIT) {
+    uint64_t res = 0;
+    uint32_t xf = 1u | (result_kind(fl) << 4);
+    if (want_res) {
+      const uint64_t ro = var ? rp[HG_ROLE_RESULT] : a + 16 + 8u * (uint32_t)schema_of(p, h.sid)->role[HG_ROLE_RESULT];
+      res = g64(R.g, ro);
+      if (fl & SF_RESULT_F64) {
+        const double xv = __longlong_as_double((long long)res);
+        if (isnan(xv) || isinf(xv)) { R.bad = true; return false; }  // int() raises if it pairs: exact path
+        if (xv >= 1.0 || xv <= -1.0) xf |= 2u;
+      } else if (res) {
+        xf |= 2u;
+      }
+    }
+    const uint32_t ne = R.ne;
+    if (ne) {  // pipeline.py:156-168
+      uint64_t ets;
+      uint32_t tfn;
+      if (ne <= (uint32_t)kRLS) {
+        ets = T.st_ts[(ne - 1) * kWarp]; tfn = T.st_fn[(ne - 1) * kWarp];
+      } else {
+        const SumEntry e = R.deep[kRDeepHalf + ne - 1 - kRLS];
+        ets = e.ts; tfn = e.fn < 0 ? M_FN : (uint32_t)e.fn;
+      }
+      if (tfn == fnm) {
+        R.ne = ne - 1;
+        hf.fold(p, (int32_t)fnm, h.ts - ets, (xf & 2u) != 0);
+        K.host++;
+        R.spans++;
+      } else {
+        push_orphan(p, R.s, m_fn(fnm), h.ts, (1ull << 63) | ((uint64_t)R.r << 24) | k);
+        K.orph++;
+      }
+    } else {  // no local entry: compose decides
+      const uint32_t i = R.np;
+      if (i < (uint32_t)kRLP) {
+        T.pd_ts[i * kWarp] = h.ts; T.pd_meta[i * kWarp] = fnm | (xf << 19);
+        T.pd_k[i * kWarp] = k;
+      } else {
+        if (i >= (uint32_t)kRLP + kRDeepHalf || !r_deep(p, R)) { R.bad = true; return false; }
+        SumEntry e;
+        e.ts = h.ts; e.seq = k; e.fn = m_fn(fnm); e.flags = xf; e.result = res;
+        R.deep[i - kRLP] = e;
+      }
+      R.np = i + 1;
+    }
+  } else {
+    K.passed++;
+  }
+  return false;
+}
+
+// deferred records, one per lane, read from HBM (L2): device-profiling and telemetry
+// records (fold / range checks) and string payloads of inline records (UTF-8)
+__device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const uint64_t* q_off, const uint32_t* q_s,
+                                      uint32_t n) {
+  uint2 K = make_uint2(0, 0);
+  const uint32_t lane = lane_id();
+  if (lane < n) {
+    const uint64_t a = q_off[lane];
+    const uint32_t s = q_s[lane];
+    const uint8_t* gb = p.data + p.stream_base[s];
+    const uint64_t size = p.stream_size[s];
+    const Hdr h = g_hdr(gb, a);
+    const uint2 d = desc_of(p, h.sid);
+    const uint32_t cls = d_cls(d);
+    const uint32_t roles = cls == HG_CLASS_DEVICE ? ((1u << HG_ROLE_START) | (1u << HG_ROLE_END) | (1u << HG_ROLE_NAME))
+                           : cls == HG_CLASS_TELEMETRY ? (1u << HG_ROLE_VALUE) : 0u;
+    uint64_t rp[HG_NUM_ROLES];
+    uint32_t rl[HG_NUM_ROLES];
+    uint64_t aux = 0;
+    uint32_t err = 0;
+    if (roles) {
+      err = seg_fields(p, gb, size, a, h.sid, h.plen, rp, rl, aux, roles);
+    } else {  // the inline record's one string field (length already checked): strict UTF-8
+      const uint32_t vp = __ldg(&p.vplan[h.sid]);
+      const uint64_t at = a + 16 + (vp & 0x3FFFu);
+      if (!g_utf8(gb, at + 4, g32(gb, at))) err = HG_ERR_UTF8;
+    }
+    if (!err) {
+      if (cls == HG_CLASS_DEVICE) err = seg_device(p, L, gb, size, h.sid, rp, rl, aux);
+      else if (cls == HG_CLASS_TELEMETRY) err = seg_telemetry(p, gb, h.sid, rp, aux);
+    }
+    if (err) {
+      atomicExch(p.anom, 1u);
+    } else if (cls == HG_CLASS_DEVICE) {
+      K.x++;
+      atomicAdd(&p.stream_spans[s], 1ull);
+    } else if (cls == HG_CLASS_TELEMETRY) {
+      K.y++;
+    }
+  }
+  __syncwarp();
+  return K;
+}
+
+constexpr int kRMaxThreads = 8 * kWarp;
+
+__device__ __forceinline__ void r_cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+// per-lane fold table entry: count << 44 | sum (u64), min, max; flushed to the global
+// row before the sum can reach 2^44 or the count 2^20 (sinks.py:123-132 TallyRow.fold)
+constexpr uint64_t kFCount = 1ull << 44;
+constexpr uint64_t kFLimit = (1ull << 43) | (1ull << 63);
+
+__device__ __noinline__ void r_fold_flush(const Params& p, uint32_t fn, uint64_t cs, uint32_t mn, uint32_t mx) {
+  unsigned long long* a = p.host_acc + 6ull * fn;
+  atomicAdd(&a[0], (unsigned long long)(cs >> 44));
+  add_i128(&a[2], &a[3], cs & (kFCount - 1), 0);
+  atomicMin(&a[4], (unsigned long long)mn);
+  atomicMax(&a[5], (unsigned long long)mx);
+}
+
+__device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uint32_t nw) {
+  if (p.max_sid < (uint32_t)kSdescMax) {
+    uint2* t = reinterpret_cast<uint2*>(g_smem);
+    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) t[i] = __ldg(&p.desc[i]);
+  }
+  if (p.n_fn > kSmallF && p.n_fn <= kSmemFnMax) {
+    SmemRow* tab = reinterpret_cast<SmemRow*>(g_smem + RL.tab);
+    for (uint32_t i = threadIdx.x; i < p.n_fn; i += blockDim.x) {
+      SmemRow z; z.count = z.err = z.s0 = z.s1 = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
+      tab[i] = z;
+    }
+  }
+  if (p.n_fn <= kSmallF) {
+    uint8_t* wb = g_smem + RL.warps + (threadIdx.x >> 5) * RL.warp_bytes;
+    uint4* ft = reinterpret_cast<uint4*>(wb + RL.ftab);
+    for (uint32_t i = lane_id(); i < p.n_fn * kWarp; i += kWarp) ft[i] = make_uint4(0, 0, 0xFFFFFFFFu, 0);
+    uint32_t* fe = reinterpret_cast<uint32_t*>(wb + RL.ferr);
+    for (uint32_t i = lane_id(); i < p.n_fn; i += kWarp) fe[i] = 0;
+  }
+  DevRow* dcache = reinterpret_cast<DevRow*>(g_smem + RL.dcache);
+  for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
+    DevRow z; z.tag = 0; z.count = 0; z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
+    dcache[i] = z;
+  }
+  NameSlot* ncache = reinterpret_cast<NameSlot*>(g_smem + RL.ncache);
+  for (uint32_t i = threadIdx.x; i < kSegNameSlots; i += blockDim.x) { ncache[i].hash = 0; ncache[i].row = 0; }
+  (void)nw;
+  __syncthreads();
+}
+
+__device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, const SegCounters K) {
+  const uint32_t lane = lane_id();
+  const uint32_t a1 = __reduce_add_sync(0xffffffffu, K.passed), a2 = __reduce_add_sync(0xffffffffu, K.host),
+                 a3 = __reduce_add_sync(0xffffffffu, K.dev), a4 = __reduce_add_sync(0xffffffffu, K.samples),
+                 a5 = __reduce_add_sync(0xffffffffu, K.orph);
+  if (lane == 0) {
+    if (a1) atomicAdd(&p.stats[ST_PASSED], (unsigned long long)a1);
+    if (a2) atomicAdd(&p.stats[ST_HOST], (unsigned long long)a2);
+    if (a3) atomicAdd(&p.stats[ST_DEVICE], (unsigned long long)a3);
+    if (a4) atomicAdd(&p.stats[ST_SAMPLES], (unsigned long long)a4);
+    if (a5) atomicAdd(&p.stats[ST_ORPHANS], (unsigned long long)a5);
+  }
+  if (p.n_fn <= kSmallF) {  // per-lane table of this warp
+    const uint8_t* wb = g_smem + RL.warps + (threadIdx.x >> 5) * RL.warp_bytes;
+    const uint4* ft = reinterpret_cast<const uint4*>(wb + RL.ftab);
+    const uint32_t* fe = reinterpret_cast<const uint32_t*>(wb + RL.ferr);
+    for (uint32_t f = 0; f < p.n_fn; f++) {
+      const uint4 v = ft[f * kWarp + lane];
+      uint64_t cs = ((uint64_t)v.y << 32) | v.x;
+      uint64_t cnt = cs >> 44, sum = cs & (kFCount - 1);
+      uint32_t mn = v.z, mx = v.w;
+      if (!__any_sync(0xffffffffu, cnt != 0)) continue;
+      for (int dd = 16; dd; dd >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, dd);
+        sum += __shfl_xor_sync(0xffffffffu, sum, dd);
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, dd));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, dd));
+      }
+      if (lane == 0 && cnt) {
+        unsigned long long* a = p.host_acc + 6ull * f;
+        atomicAdd(&a[0], (unsigned long long)cnt);
+        if (fe[f]) atomicAdd(&a[1], (unsigned long long)fe[f]);
+        add_i128(&a[2], &a[3], sum, 0);
+        atomicMin(&a[4], (unsigned long long)mn);
+        atomicMax(&a[5], (unsigned long long)mx);
+      }
+    }
+  }
+  __syncthreads();
+  if (p.n_fn > kSmallF && p.n_fn <= kSmemFnMax) {
+    const SmemRow* tab = reinterpret_cast<const SmemRow*>(g_smem + RL.tab);
+    for (uint32_t f = threadIdx.x; f < p.n_fn; f += blockDim.x) {
+      const SmemRow r = tab[f];
+      if (!r.count) continue;
+      unsigned long long* a = p.host_acc + 6ull * f;
+      atomicAdd(&a[0], (unsigned long long)r.count);
+      if (r.err) atomicAdd(&a[1], (unsigned long long)r.err);
+      add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), 0);
+      atomicMin(&a[4], (unsigned long long)r.mn);
+      atomicMax(&a[5], (unsigned long long)r.mx);
+    }
+  }
+  const DevRow* dcache = reinterpret_cast<const DevRow*>(g_smem + RL.dcache);
+  for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
+    const DevRow r = dcache[i];
+    if (!r.tag || !r.count) continue;
+    unsigned long long* a = p.dev_acc + 6ull * (r.tag - 1);
+    atomicAdd(&a[0], (unsigned long long)r.count);
+    add_i128(&a[2], &a[3], (uint64_t)r.s0 | ((uint64_t)r.s1 << 32), (int64_t)(int32_t)r.s2);
+    atomicMin(&a[4], bias64((int64_t)(int32_t)(r.mn ^ 0x80000000u)));
+    atomicMax(&a[5], bias64((int64_t)(int32_t)(r.mx ^ 0x80000000u)));
+  }
+}
+
+__global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const Params* gp) {
+  const Params& gpr = *gp;
+  const uint32_t nw = blockDim.x >> 5;
+  const RSmem RL = fast_smem_layout(p.n_fn, nw);
+  const SegSmem L = r_segsmem(RL);
+  const uint32_t lane = lane_id();
+  uint8_t* wb = g_smem + RL.warps + (threadIdx.x >> 5) * RL.warp_bytes;
+  const uint32_t* ring = reinterpret_cast<const uint32_t*>(wb + RL.ring + lane * kRStride);
+  const uint32_t ring_s = s_addr(ring);
+  r_prologue(p, RL, nw);
+  SegCounters K;
+  K.passed = K.host = K.dev = K.samples = K.orph = K.items = 0;
+  HostFold hf;  // the slow path's fold: CTA table (medium function sets) or global rows
+  hf.small = false;
+  hf.tab = (p.n_fn > kSmallF && p.n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(g_smem + RL.tab) : nullptr;
+  const bool small = p.n_fn <= kSmallF;
+  uint4* ftab = reinterpret_cast<uint4*>(wb + RL.ftab) + lane;
+  uint32_t* ferr = reinterpret_cast<uint32_t*>(wb + RL.ferr);
+  const RTabs T = r_tabs(RL);
+  uint64_t* q_off = reinterpret_cast<uint64_t*>(wb + RL.q_off);
+  uint32_t* q_s = reinterpret_cast<uint32_t*>(wb + RL.q_s);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  constexpr uint32_t kPend = (1u << kRLag) - 1u;
+  RLane R;
+  R.recent = 0;
+  bool live = r_begin(gpr, R, blockIdx.x * blockDim.x + threadIdx.x, stride);
+  uint32_t qd = 0;
+  while (__any_sync(0xffffffffu, live)) {
+    const bool ending = live && (R.o >= R.t1 || R.bad);
+    if (__any_sync(0xffffffffu, ending)) {
+      if (ending) {
+        r_end(gpr, R, T);
+        live = r_begin(gpr, R, R.r + stride, stride);
+      }
+    }
+    const bool act = live && R.o < R.t1 && !R.bad;
+    const uint32_t o_start = R.o;
+    // ---- ring refill: one 128-byte chunk per lane and iteration; four chunks per cp.async instruction
+    const uint32_t cons = R.o / kRChunk;
+    if (act && cons > R.ci) { R.ci = cons; R.fresh = true; }  // a long record jumped over chunks
+    if (!(R.recent & kPend)) R.fresh = false;
+    const bool want = act && !R.fresh && R.ci <= R.clast && R.ci < cons + kRSlots;
+    if (want) {  // the lane copies its own line: 8 x 16 B (plus the mirror for slot 0)
+      const uint32_t q = R.ci & (kRSlots - 1);
+      const uint8_t* src = R.g + (uint64_t)R.ci * kRChunk;
+      const uint32_t dst = ring_s + q * kRChunk;
+      #pragma unroll
+      for (uint32_t k = 0; k < kRChunk; k += 16) r_cp16(dst + k, src + k);
+      if (q == 0) {
+        #pragma unroll
+        for (uint32_t k = 0; k < kRMirror; k += 16) r_cp16(ring_s + kRRing + k, src + k);
+      }
+    }
+    R.ci += want ? 1u : 0u;
+    R.recent = (R.recent << 1) | (want ? 1u : 0u);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kRLag) : "memory");
+    __syncwarp();
+    // ---- [o, o + kRInline) in the ring: every chunk requested before the last kRLag iterations is there
+    const uint32_t cr = R.ci - __popc(R.recent & kPend);
+    const uint32_t hi = min((R.o + kRInline - 1) / kRChunk, R.clast);
+    const bool ready = act && hi < cr;
+    const uint32_t pos = R.o & (kRRing - 1);
+    const uint32_t* w = ring + (pos >> 2);  // up to 64 bytes from here without wrapping (mirror)
+    const uint32_t sh = (pos & 3u) << 3;
+    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+    const uint32_t sid = __funnelshift_r(w0, w1, sh);
+    const uint64_t ts = ((uint64_t)__funnelshift_r(w2, w3, sh) << 32) | __funnelshift_r(w1, w2, sh);
+    const uint32_t plen = __funnelshift_r(w3, w4, sh);
+    const bool sid_ok = sid <= p.max_sid;
+    const uint32_t sidc = sid_ok ? sid : 0u;
+    uint2 d = __ldg(&p.desc[sidc]);
+    const uint32_t vp = __ldg(&p.vplan[sidc]);
+    if (!sid_ok) d.x = 0;
+    const uint32_t cls = d_cls(d), fl = d_flags(d);
+    const uint32_t fnm = d.x & M_FN;
+    const uint32_t fixed = d_fixed(d);
+    const bool var = (fl & SF_VAR) != 0;
+    const bool isE = cls == HG_CLASS_ENTRY, isX = cls == HG_CLASS_EXIT;
+    const bool dt = cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY;
+    const uint32_t ne = R.ne, np = R.np;
+    const uint32_t topi = ((ne - 1u) < (uint32_t)kRLS ? ne - 1u : 0u) * kWarp;
+    const uint64_t ets = T.st_ts[topi];
+    const uint32_t tfn = T.st_fn[topi];
+    const uint32_t size32 = R.size < 0xFFFFFFFFull ? (uint32_t)R.size : 0xFFFFFFFFu;
+    // inline: the whole record is in the ring, in order, with a length its schema allows
+    const bool good = ready && (d.x & (D_PRESENT | (SF_NOINLINE << 23))) == D_PRESENT &&
+                      (plen == fixed || (var && plen > fixed)) && plen <= kRInline - 16u &&
+                      R.o + 16u + plen <= size32 && !(R.n && ts < R.prev_ts);
+    const bool fE = good && isE && ne < (uint32_t)kRLS;
+    const bool fXp = good && isX && ne && ne <= (uint32_t)kRLS && tfn == fnm;  // pops a same-function top
+    const bool fXq = good && isX && !ne && np < (uint32_t)kRLP;               // pending: compose decides
+    const bool fO = good && !isE && !isX;
+    // one variable field (blob / string): exact length here, UTF-8 of strings in the drain
+    const uint32_t lead0 = vp & 0x3FFFu, lead1 = (vp >> 14) & 0x3FFFu;
+    const uint32_t ln = r_u32(ring, pos + 16u + lead0);
+    const bool chk = (fE || fXp || fXq || fO) && var && !dt;
+    const bool lenbad = chk && (uint64_t)lead0 + 4u + ln + lead1 != plen;
+    if (lenbad) R.bad = true;  // CorruptRecordError: the exact path names it
+    const bool fast = (fE || fXp || fXq || fO) && !lenbad;
+    bool qflag = fast && (dt || (chk && (vp & VP_STR) && ln));
+    const uint32_t rw = (16u + 8u * d_resfield(d) + (pos & 3u)) >> 2;  // result field <= 5: mirror reach
+    uint64_t res = 0;
+    if (fl & SF_RESULT) {
+      const uint32_t r0 = w[rw], r1 = w[rw + 1], r2 = w[rw + 2];
+      res = ((uint64_t)__funnelshift_r(r1, r2, sh) << 32) | __funnelshift_r(r0, r1, sh);
+    }
+    const bool err = res != 0;
+    if (fast) {
+      const uint32_t k = R.n;
+      R.n = k + 1;
+      R.first_ts = k ? R.first_ts : ts;
+      R.prev_ts = ts;
+      R.o += 16u + plen;
+    }
+    if (fE) {
+      T.st_ts[ne * kWarp] = ts;
+      T.st_fn[ne * kWarp] = fnm;
+    }
+    if (fXq) {
+      const uint32_t i = np * kWarp;
+      T.pd_ts[i] = ts;
+      T.pd_meta[i] = fnm | ((1u | (err ? 2u : 0u) | (result_kind(fl) << 4)) << 19);
+      T.pd_k[i] = R.n - 1;
+    }
+    R.ne = ne + (fE ? 1u : 0u) - (fXp ? 1u : 0u);
+    R.np = np + (fXq ? 1u : 0u);
+    if (fXp) {
+      const uint64_t dur = ts - ets;
+      if (small && (dur >> 32) == 0) {
+        uint4 v = ftab[fnm * kWarp];
+        const uint32_t du = (uint32_t)dur;
+        uint64_t cs = (((uint64_t)v.y << 32) | v.x) + kFCount + du;
+        v.z = min(v.z, du);
+        v.w = max(v.w, du);
+        if (cs & kFLimit) {  // flush before the packed count or sum can overflow
+          r_fold_flush(gpr, fnm, cs, v.z, v.w);
+          cs = 0;
+        }
+        v.x = (uint32_t)cs; v.y = (uint32_t)(cs >> 32);
+        ftab[fnm * kWarp] = v;
+        if (err) atomicAdd(&ferr[fnm], 1u);
+      } else {
+        hf.fold(gpr, (int32_t)fnm, dur, err);
+      }
+      K.host++;
+      R.spans++;
+    }
+    K.passed += (fO && !dt) ? 1u : 0u;
+    // everything else from HBM (the ring is only a cache of the stream)
+    const bool slow = ready && !fast && !R.bad;
+    if (__any_sync(0xffffffffu, slow)) {
+      if (slow) qflag = r_record_slow(gpr, R, T, K, hf);
+    }
+    // deferred records: the record at q_off is consumed; UTF-8 / device fold / telemetry checks in the drain
+    const uint32_t dm = __ballot_sync(0xffffffffu, qflag);
+    if (dm) {
+      if (qflag) {
+        const uint32_t i = qd + __popc(dm & lanemask_lt());
+        q_off[i] = R.C0 + o_start;
+        q_s[i] = R.s;
+      }
+      qd += __popc(dm);
+      __syncwarp();
+      if (qd >= (uint32_t)kWarp) {
+        const uint2 dk = r_drain(gpr, L, q_off, q_s, kWarp);
+        K.dev += dk.x; K.samples += dk.y;
+        qd -= kWarp;
+        if (lane < qd) { q_off[lane] = q_off[kWarp + lane]; q_s[lane] = q_s[kWarp + lane]; }
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (qd) {
+    const uint2 dk = r_drain(gpr, L, q_off, q_s, qd);
+    K.dev += dk.x; K.samples += dk.y;
+  }
+  __syncwarp();
+  r_epilogue(gpr, RL, K);
+}
+
+// per stream: verify the range chain, record bases, compose_kernel's per-range state
+__global__ void __launch_bounds__(128) fast_verify_kernel(Params p, unsigned long long* stream_nrec) {
+  const uint32_t lane = lane_id();
+  const uint32_t s = blockIdx.x * (blockDim.x / kWarp) + (threadIdx.x >> 5);
+  if (s >= p.n_streams) return;
+  const uint32_t r0 = p.stream_range0[s];
+  const uint32_t r1 = (s + 1 < p.n_streams) ? p.stream_range0[s + 1] : p.n_ranges;
+  const uint64_t size = p.stream_size[s];
+  uint64_t c_exit = 16, c_base = 0, c_last = 0;
+  bool c_has = false, bad = false;
+  for (uint32_t rb = r0; rb < r1; rb += kWarp) {
+    const uint32_t r = rb + lane;
+    const bool valid = r < r1;
+    RangeState st;
+    if (valid) st = p.rstate[r];
+    else { st.entry = kNone; st.exit = kNone; st.n = 0; st.np = 0; st.ne = 0; st.first_ts = st.last_ts = 0; st.pool_off = 0; }
+    const uint64_t t1 = valid ? min(16 + (uint64_t)(r - r0 + 1) * p.range_bytes, size) : 0;
+    const bool hasE = valid && st.entry != kNone;
+    // exit carried into each lane: nearest lower lane with an entry, else the carry
+    int src = hasE ? (int)lane : -1;
+    int pre = __shfl_up_sync(0xffffffffu, src, 1);
+    if (lane == 0) pre = -1;
+    for (int dd = 1; dd < 32; dd <<= 1) { const int v = __shfl_up_sync(0xffffffffu, pre, dd); if ((int)lane >= dd) pre = max(pre, v); }
+    const uint64_t px = __shfl_sync(0xffffffffu, st.exit, pre < 0 ? 0 : pre);
+    const uint64_t prev_exit = pre >= 0 ? px : c_exit;
+    bool ok = !valid || (hasE ? st.entry == prev_exit : prev_exit >= t1);
+    // timestamps keep rising across ranges (pipeline.py:98)
+    int srcn = (valid && st.n) ? (int)lane : -1;
+    int pn = __shfl_up_sync(0xffffffffu, srcn, 1);
+    if (lane == 0) pn = -1;
+    for (int dd = 1; dd < 32; dd <<= 1) { const int v = __shfl_up_sync(0xffffffffu, pn, dd); if ((int)lane >= dd) pn = max(pn, v); }
+    const uint64_t pl = __shfl_sync(0xffffffffu, st.last_ts, pn < 0 ? 0 : pn);
+    const uint64_t prev_last = pn >= 0 ? pl : c_last;
+    const bool has_prev = pn >= 0 || c_has;
+    if (valid && st.n && has_prev && st.first_ts < prev_last) ok = false;
+    // record bases
+    const uint64_t n = valid ? st.n : 0;
+    uint64_t incl = n;
+    for (int dd = 1; dd < 32; dd <<= 1) { const uint64_t v = __shfl_up_sync(0xffffffffu, incl, dd); if ((int)lane >= dd) incl += v; }
+    const uint64_t base = c_base + incl - n;
+    if (valid) {
+      p.range_base[r] = base;
+      SegState ss;
+      ss.status = (p.epoch << 2) | TS_DONE;
+      ss.pool_n_pending = st.np;
+      ss.pool_off = st.pool_off;
+      ss.pool_n_resid = st.ne;
+      ss.pad = 0;
+      p.state[r] = ss;
+      if (st.pool_off + st.np + st.ne <= p.pool_cap)
+        for (uint32_t i = 0; i < st.np; i++) p.pool[st.pool_off + i].seq += base;
+    }
+    bad |= !ok;
+    c_base += __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t me = __ballot_sync(0xffffffffu, hasE);
+    if (me) c_exit = __shfl_sync(0xffffffffu, st.exit, 31 - __clz(me));
+    const uint32_t mn = __ballot_sync(0xffffffffu, valid && st.n);
+    if (mn) { c_last = __shfl_sync(0xffffffffu, st.last_ts, 31 - __clz(mn)); c_has = true; }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(p.anom, 1u);
+  if (lane == 0) {
+    stream_nrec[s] = c_base;
+    if (c_base) atomicAdd(&p.stats[ST_EVENTS], (unsigned long long)c_base);
+    if (c_has) atomicMax(p.last_ts, (unsigned long long)c_last);
+  }
+}
+
+// orphans found inside a range carry (range, index in range); make them stream indices
+__global__ void fast_orphan_fix_kernel(Params p) {
+  const unsigned long long n = min(*(volatile unsigned long long*)p.n_orphans, (unsigned long long)p.orphan_cap);
+  for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t q = p.orphans[i].seq;
+    if (q >> 63) p.orphans[i].seq = p.range_base[(q >> 24) & ((1ull << 39) - 1)] + (q & 0xFFFFFFull);
+  }
+}
+
+}  // namespace hg

@@ -28,6 +28,7 @@ enum : uint8_t {
   SF_FEED_ALWAYS = 8,  // raises when fed (host holds the exception)
   SF_FEED_TIMELINE = 16,
   SF_RESULT_I64 = 32,  // ... of kind i64 (else u64/address)
+  SF_NOINLINE = 64,    // range kernel: never decoded inline (f64 result, feed error, payload plan needs HBM)
 };
 
 // result kind of an exit schema for the timeline's int(result) (pipeline.py:183):

@@ -98,6 +98,15 @@ struct Params {
   SumEntry* deep;                  // per-lane automaton chunks of deep segments
   unsigned long long* deep_used;
   uint64_t deep_cap;
+  // single-pass range path (fast.cuh)
+  const uint32_t* range_stream;    // range -> stream
+  const uint32_t* stream_range0;   // stream -> first range
+  uint32_t n_ranges;
+  uint32_t range_bytes;
+  struct RangeState* rstate;
+  unsigned long long* range_base;  // record index of each range's first record (verify kernel)
+  uint32_t* anom;                  // nonzero: the single-pass result is void, run the exact path
+  const uint32_t* vplan;           // per schema id: single-var-field payload plan (fast.cuh)
 };
 
 // compact descriptor: x = fn(20) | cls(3)<<20 | flags(8)<<23 ; y = fixed_len(16) | result field index(8)<<16 | counter(8)<<24

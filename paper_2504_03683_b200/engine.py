@@ -21,6 +21,9 @@ from .errors import EngineError, UnsupportedTraceError
 from .results import build_report, error_key, first_error, make_exception, orphan_list, rows_from_native
 
 HG_EUNSUPPORTED = -5
+OPT_PATH = 1
+OPT_RANGE_BYTES = 2
+PATH_AUTO, PATH_EXACT, PATH_FAST = 0, 1, 2
 
 
 @dataclass
@@ -126,6 +129,16 @@ class Engine:
 
     def stage(self):
         self._check(self._L.hg_stage(self._ctx), "hg_stage")
+
+    def set_option(self, key: int, value: int):
+        """hg_set_option: OPT_PATH (0 auto, 1 exact, 2 single pass only), OPT_RANGE_BYTES."""
+        self._check(self._L.hg_set_option(self._ctx, key, value), "hg_set_option")
+
+    def last_path(self):
+        """(path of the last phase 1: 1 single pass / 0 exact, discarded single passes so far, range bytes)"""
+        p, f, r = C.c_uint32(), C.c_uint64(), C.c_uint32()
+        self._check(self._L.hg_last_path(self._ctx, C.byref(p), C.byref(f), C.byref(r)), "hg_last_path")
+        return p.value, f.value, r.value
 
     # -- execution
     def run_raw(self, want=HG_WANT_TALLY):

@@ -82,6 +82,8 @@ def lib():
         "hg_get_timeline": ([vp, vp, u64], C.c_int),
         "hg_device_tally": ([vp, vp, vp], C.c_int),
         "hg_last_timing": ([vp, vp, vp, vp, vp, vp], C.c_int),
+        "hg_set_option": ([vp, u32, u64], C.c_int),
+        "hg_last_path": ([vp, vp, vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -98,5 +100,5 @@ EXPORTED = (
     "hg_clear_streams", "hg_stage", "hg_run", "hg_run_local", "hg_local_last_ts", "hg_finish", "hg_get_stats",
     "hg_get_tally", "hg_get_device_names", "hg_get_stream_spans", "hg_get_orphans", "hg_get_trace_errors",
     "hg_timeline_size", "hg_get_timeline", "hg_device_tally", "hg_last_timing", "hg_set_function_names",
-    "hg_timeline_ms", "hg_set_timeline_device", "hg_phase_timing",
+    "hg_timeline_ms", "hg_set_timeline_device", "hg_phase_timing", "hg_set_option", "hg_last_path",
 )

@@ -1,0 +1,112 @@
+"""The single-pass range path (csrc/fast.cuh) against the CPU oracle.
+
+Tally-only runs take the single pass; it must be bit-exact with the oracle on
+every configuration shape, at the default range size and at small range sizes
+that put many speculative range starts inside records.  Traces the single pass
+cannot vouch for (errors) must fall back to the exact path and still match."""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def engine():
+    from paper_2504_03683_b200.engine import Engine
+
+    eng = Engine(device=0)
+    yield eng
+    eng.close()
+
+
+def _run(engine, wl, range_bytes=0, path=0):
+    from oracle import oracle
+    from paper_2504_03683_b200 import synth
+    from paper_2504_03683_b200.engine import OPT_PATH, OPT_RANGE_BYTES
+
+    raws = synth.generate(wl)
+    infos = [r.info for r in raws]
+    engine.set_option(OPT_PATH, path)
+    engine.set_option(OPT_RANGE_BYTES, range_bytes)
+    try:
+        got = engine.run(raws, wl.registry, infos)
+    finally:
+        engine.set_option(OPT_PATH, 0)
+        engine.set_option(OPT_RANGE_BYTES, 0)
+    want = oracle.run(raws, wl.registry, infos)
+    assert (got.error is None) == (want.error is None), (got.error, want.error)
+    if want.error is None:
+        assert got.stats == want.stats
+        assert got.report == want.report
+        assert got.orphans == want.orphans
+    else:
+        assert type(got.error) is type(want.error) and str(got.error) == str(want.error)
+    return got
+
+
+@pytest.mark.parametrize("range_bytes", [0, 512, 1008, 4096])
+@pytest.mark.parametrize("name,scale", [("c1", 0.02), ("c2", 0.004), ("c3", 0.0005), ("c4", 0.003), ("c5", 0.003)])
+def test_single_pass_matches_oracle(engine, name, scale, range_bytes):
+    from paper_2504_03683_b200 import synth
+
+    _run(engine, synth.config(name, scale), range_bytes, path=2)
+    assert engine.last_path()[0] == 1
+
+
+@pytest.mark.parametrize("name,scale", [("c1", 0.01), ("c2", 0.002), ("c5", 0.002)])
+@pytest.mark.parametrize("range_bytes", [16, 64, 128])
+def test_tiny_ranges_fall_back_or_match(engine, name, scale, range_bytes):
+    """Ranges shorter than a record: wrong speculation is caught by the chain check (auto path)."""
+    from paper_2504_03683_b200 import synth
+
+    _run(engine, synth.config(name, scale), range_bytes)
+
+
+@pytest.mark.parametrize("range_bytes", [0, 512, 2048])
+@pytest.mark.parametrize("seed", range(6))
+def test_single_pass_adversarial(engine, seed, range_bytes):
+    """Orphans, typed mismatches, unclosed calls, equal timestamps, deep stacks (overflow chunks)."""
+    from paper_2504_03683_b200 import synth
+
+    P = synth.PID_BASE
+    params = dict(orphan_p=0.01 * seed, mismatch_p=0.02 * (seed % 3), meta_p=0.03, close_at_end=seed % 2,
+                  max_depth=[4, 8, 64, 300, 2, 16][seed], push_p=[0.5, 0.6, 0.7, 0.9, 0.5, 0.55][seed],
+                  gap_lo=0, gap_hi=[3, 600, 1, 50, 0, 5][seed], prof_p=0.3)
+    streams = [synth.StreamSpec(f"h{i % 3}", P + 100 * (i % 4), P + 100 * (i % 4) + i, 3000 + 997 * i,
+                                9000 + 31 * seed + i) for i in range(12)]
+    wl = synth.Workload(f"adv{seed}", synth.ze_registry(), streams, params, kernel_names=synth.kernel_pool(30))
+    _run(engine, wl, range_bytes)
+
+
+def test_single_pass_is_taken_on_clean_traces(engine):
+    from paper_2504_03683_b200 import synth
+
+    before = engine.last_path()[1]
+    _run(engine, synth.config("c2", 0.002))
+    path, fallbacks, rb = engine.last_path()
+    assert path == 1 and fallbacks == before and rb >= 1024
+
+
+def test_error_traces_fall_back_to_exact_path(engine):
+    """A corrupt record: the single pass flags it, the exact path names the error."""
+    from paper_2504_03683_b200 import synth
+
+    wl = synth.config("c2", 0.001)
+    raws = synth.generate(wl)
+    bad = bytearray(raws[7].data)
+    bad[16 + 40 * 16] ^= 0xFF  # scramble a byte somewhere inside the stream
+    from paper_2504_03683_b200.tracefile import RawStream
+
+    r = raws[7]
+    raws[7] = RawStream(r.hostname, r.pid, r.tid, r.name, bytes(bad), r.info)
+    from oracle import oracle
+
+    infos = [x.info for x in raws]
+    got = engine.run(raws, wl.registry, infos)
+    want = oracle.run(raws, wl.registry, infos)
+    assert (got.error is None) == (want.error is None)
+    if want.error is not None:
+        assert type(got.error) is type(want.error) and str(got.error) == str(want.error)
+        assert engine.last_path()[0] == 0
+    else:
+        assert got.report == want.report and got.stats == want.stats
