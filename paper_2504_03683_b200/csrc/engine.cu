@@ -754,7 +754,7 @@ static int build_layout(hg_ctx* ctx) {
     for (uint32_t t = 0; t < nt; t++) ctx->tile_stream.push_back(s);
   }
   // ranges for the single pass: one per resident lane, never crossing a stream
-  uint32_t nw = 8;
+  uint32_t nw = kRMaxThreads / kWarp;
   while (nw > 1 && fast_smem_layout(ctx->n_fn, nw).total > (uint32_t)ctx->smem_optin) nw--;
   ctx->fast_warps = nw;
   const uint64_t lanes = (uint64_t)std::max(ctx->sm_count, 1) * nw * kWarp;

@@ -30,13 +30,13 @@
 namespace hg {
 
 constexpr uint32_t kRChunk = 128;                   // bytes per ring slot (one line)
-constexpr uint32_t kRSlots = 4;                     // slots per lane
-constexpr uint32_t kRRing = kRChunk * kRSlots;      // 512-byte ring
+constexpr uint32_t kRSlots = 2;                     // slots per lane
+constexpr uint32_t kRRing = kRChunk * kRSlots;      // 256-byte ring
 constexpr uint32_t kRWordMask = kRRing / 4 - 1;
 constexpr uint32_t kRMirror = 64;                   // slot 0's first bytes again after the ring
 constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: any 64-byte read needs no wrap
 constexpr uint32_t kRInline = kRChunk;              // records up to this long are decoded from the ring
-constexpr int kRLag = 4;                            // iterations before a fill group is waited for
+constexpr int kRLag = 2;                            // iterations before a fill group is waited for
 constexpr int kRLS = 8;                             // open entries per lane in shared memory
 constexpr int kRLP = 4;                             // pending exits per lane in shared memory
 constexpr int kRQ = 64;                             // deferred-record queue per warp (drained at 32)
@@ -77,8 +77,8 @@ __host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw) {
   L.warps = off;
   uint32_t w = 0;
   L.ring = w;    w += kRStride * kWarp;
-  L.ftab = w;    w += small ? 16u * n_fn * kWarp : 0u;   // [fn][lane] {count << 44 | sum (u64), min, max}
-  L.ferr = w;    w += small ? 4u * n_fn : 0u;            // [fn] error count
+  L.ftab = w;    w += small ? 8u * n_fn * kWarp : 0u;   // [fn][lane] count << 44 | sum
+  L.ferr = w;    w += small ? 12u * n_fn : 0u;          // [fn] error count, min, max
   w = (w + 15u) & ~15u;
   L.st_ts = w;   w += 8u * kRLS * kWarp;
   L.st_fn = w;   w += 4u * kRLS * kWarp;
@@ -390,7 +390,7 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
   return K;
 }
 
-constexpr int kRMaxThreads = 8 * kWarp;
+constexpr int kRMaxThreads = 12 * kWarp;
 
 __device__ __forceinline__ void r_cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -401,12 +401,10 @@ __device__ __forceinline__ void r_cp16(uint32_t dst, const void* src) {
 constexpr uint64_t kFCount = 1ull << 44;
 constexpr uint64_t kFLimit = (1ull << 43) | (1ull << 63);
 
-__device__ __noinline__ void r_fold_flush(const Params& p, uint32_t fn, uint64_t cs, uint32_t mn, uint32_t mx) {
+__device__ __noinline__ void r_fold_flush(const Params& p, uint32_t fn, uint64_t cs) {
   unsigned long long* a = p.host_acc + 6ull * fn;
   atomicAdd(&a[0], (unsigned long long)(cs >> 44));
   add_i128(&a[2], &a[3], cs & (kFCount - 1), 0);
-  atomicMin(&a[4], (unsigned long long)mn);
-  atomicMax(&a[5], (unsigned long long)mx);
 }
 
 __device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uint32_t nw) {
@@ -423,10 +421,10 @@ __device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uin
   }
   if (p.n_fn <= kSmallF) {
     uint8_t* wb = g_smem + RL.warps + (threadIdx.x >> 5) * RL.warp_bytes;
-    uint4* ft = reinterpret_cast<uint4*>(wb + RL.ftab);
-    for (uint32_t i = lane_id(); i < p.n_fn * kWarp; i += kWarp) ft[i] = make_uint4(0, 0, 0xFFFFFFFFu, 0);
+    uint64_t* ft = reinterpret_cast<uint64_t*>(wb + RL.ftab);
+    for (uint32_t i = lane_id(); i < p.n_fn * kWarp; i += kWarp) ft[i] = 0;
     uint32_t* fe = reinterpret_cast<uint32_t*>(wb + RL.ferr);
-    for (uint32_t i = lane_id(); i < p.n_fn; i += kWarp) fe[i] = 0;
+    for (uint32_t i = lane_id(); i < p.n_fn; i += kWarp) { fe[i] = 0; fe[p.n_fn + i] = 0xFFFFFFFFu; fe[2 * p.n_fn + i] = 0; }
   }
   DevRow* dcache = reinterpret_cast<DevRow*>(g_smem + RL.dcache);
   for (uint32_t i = threadIdx.x; i < kDevSlots; i += blockDim.x) {
@@ -453,27 +451,24 @@ __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, const S
   }
   if (p.n_fn <= kSmallF) {  // per-lane table of this warp
     const uint8_t* wb = g_smem + RL.warps + (threadIdx.x >> 5) * RL.warp_bytes;
-    const uint4* ft = reinterpret_cast<const uint4*>(wb + RL.ftab);
+    const uint64_t* ft = reinterpret_cast<const uint64_t*>(wb + RL.ftab);
     const uint32_t* fe = reinterpret_cast<const uint32_t*>(wb + RL.ferr);
     for (uint32_t f = 0; f < p.n_fn; f++) {
-      const uint4 v = ft[f * kWarp + lane];
-      uint64_t cs = ((uint64_t)v.y << 32) | v.x;
+      const uint64_t cs = ft[f * kWarp + lane];
       uint64_t cnt = cs >> 44, sum = cs & (kFCount - 1);
-      uint32_t mn = v.z, mx = v.w;
-      if (!__any_sync(0xffffffffu, cnt != 0)) continue;
+      const bool seen = fe[2 * p.n_fn + f] != 0 || fe[p.n_fn + f] != 0xFFFFFFFFu;  // flushed spans count too
+      if (!__any_sync(0xffffffffu, cnt != 0) && !seen) continue;
       for (int dd = 16; dd; dd >>= 1) {
         cnt += __shfl_xor_sync(0xffffffffu, cnt, dd);
         sum += __shfl_xor_sync(0xffffffffu, sum, dd);
-        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, dd));
-        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, dd));
       }
-      if (lane == 0 && cnt) {
+      if (lane == 0) {
         unsigned long long* a = p.host_acc + 6ull * f;
-        atomicAdd(&a[0], (unsigned long long)cnt);
+        if (cnt) atomicAdd(&a[0], (unsigned long long)cnt);
         if (fe[f]) atomicAdd(&a[1], (unsigned long long)fe[f]);
-        add_i128(&a[2], &a[3], sum, 0);
-        atomicMin(&a[4], (unsigned long long)mn);
-        atomicMax(&a[5], (unsigned long long)mx);
+        if (sum) add_i128(&a[2], &a[3], sum, 0);
+        atomicMin(&a[4], (unsigned long long)fe[p.n_fn + f]);
+        atomicMax(&a[5], (unsigned long long)fe[2 * p.n_fn + f]);
       }
     }
   }
@@ -519,7 +514,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
   hf.small = false;
   hf.tab = (p.n_fn > kSmallF && p.n_fn <= kSmemFnMax) ? reinterpret_cast<SmemRow*>(g_smem + RL.tab) : nullptr;
   const bool small = p.n_fn <= kSmallF;
-  uint4* ftab = reinterpret_cast<uint4*>(wb + RL.ftab) + lane;
+  uint64_t* ftab = reinterpret_cast<uint64_t*>(wb + RL.ftab) + lane;
   uint32_t* ferr = reinterpret_cast<uint32_t*>(wb + RL.ferr);
   const RTabs T = r_tabs(RL);
   uint64_t* q_off = reinterpret_cast<uint64_t*>(wb + RL.q_off);
@@ -561,10 +556,9 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group %0;" ::"n"(kRLag) : "memory");
     __syncwarp();
-    // ---- [o, o + kRInline) in the ring: every chunk requested before the last kRLag iterations is there
+    // ---- every chunk requested before the last kRLag iterations is in the ring; first the header
     const uint32_t cr = R.ci - __popc(R.recent & kPend);
-    const uint32_t hi = min((R.o + kRInline - 1) / kRChunk, R.clast);
-    const bool ready = act && hi < cr;
+    const bool ready = act && min((R.o + 15u) / kRChunk, R.clast) < cr;
     const uint32_t pos = R.o & (kRRing - 1);
     const uint32_t* w = ring + (pos >> 2);  // up to 64 bytes from here without wrapping (mirror)
     const uint32_t sh = (pos & 3u) << 3;
@@ -589,8 +583,12 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const uint32_t tfn = T.st_fn[topi];
     const uint32_t size32 = R.size < 0xFFFFFFFFull ? (uint32_t)R.size : 0xFFFFFFFFu;
     // inline: the whole record is in the ring, in order, with a length its schema allows
-    const bool good = ready && (d.x & (D_PRESENT | (SF_NOINLINE << 23))) == D_PRESENT &&
-                      (plen == fixed || (var && plen > fixed)) && plen <= kRInline - 16u &&
+    // ... then the whole record (inline records are at most kRInline bytes: two slots)
+    const bool inl = plen <= kRInline - 16u;
+    const bool rec_in = (R.o + 15u + plen) / kRChunk < cr;
+    const bool stall = ready && inl && !rec_in && (uint64_t)R.o + 16u + plen <= R.size;
+    const bool good = ready && rec_in && (d.x & (D_PRESENT | (SF_NOINLINE << 23))) == D_PRESENT &&
+                      (plen == fixed || (var && plen > fixed)) && inl &&
                       R.o + 16u + plen <= size32 && !(R.n && ts < R.prev_ts);
     const bool fE = good && isE && ne < (uint32_t)kRLS;
     const bool fXp = good && isX && ne && ne <= (uint32_t)kRLS && tfn == fnm;  // pops a same-function top
@@ -633,18 +631,16 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     if (fXp) {
       const uint64_t dur = ts - ets;
       if (small && (dur >> 32) == 0) {
-        uint4 v = ftab[fnm * kWarp];
         const uint32_t du = (uint32_t)dur;
-        uint64_t cs = (((uint64_t)v.y << 32) | v.x) + kFCount + du;
-        v.z = min(v.z, du);
-        v.w = max(v.w, du);
+        uint64_t cs = ftab[fnm * kWarp] + kFCount + du;
         if (cs & kFLimit) {  // flush before the packed count or sum can overflow
-          r_fold_flush(gpr, fnm, cs, v.z, v.w);
+          r_fold_flush(gpr, fnm, cs);
           cs = 0;
         }
-        v.x = (uint32_t)cs; v.y = (uint32_t)(cs >> 32);
-        ftab[fnm * kWarp] = v;
+        ftab[fnm * kWarp] = cs;
         if (err) atomicAdd(&ferr[fnm], 1u);
+        if (du < *(volatile uint32_t*)&ferr[p.n_fn + fnm]) atomicMin(&ferr[p.n_fn + fnm], du);
+        if (du > *(volatile uint32_t*)&ferr[2 * p.n_fn + fnm]) atomicMax(&ferr[2 * p.n_fn + fnm], du);
       } else {
         hf.fold(gpr, (int32_t)fnm, dur, err);
       }
@@ -653,7 +649,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     }
     K.passed += (fO && !dt) ? 1u : 0u;
     // everything else from HBM (the ring is only a cache of the stream)
-    const bool slow = ready && !fast && !R.bad;
+    const bool slow = ready && !fast && !R.bad && !stall;
     if (__any_sync(0xffffffffu, slow)) {
       if (slow) qflag = r_record_slow(gpr, R, T, K, hf);
     }
