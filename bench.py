@@ -259,6 +259,8 @@ def run_ours(args):
             torch.distributed.destroy_process_group()
         return
     peak, peak_src = _peaks()
+    path, fallbacks, range_bytes = eng.last_path()
+    single = path == 1
     achieved = (n_bytes / (tms / 1e3)) / 1e9  # per GPU: rank-local trace bytes over the decode kernel time
     line = {
         "metric": METRIC,
@@ -293,11 +295,14 @@ def run_ours(args):
             "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": None,
-            "kernel": "seg_decode_kernel",
+            "kernel": "fast_kernel" if single else "seg_decode_kernel",
             "kernel_ms": tms,
             "algorithmic_bytes_per_launch": n_bytes,
             "peak_source": peak_src,
-            "phase1": {"kernels": "seg_walk_kernel + seg_chain_kernel + seg_decode_kernel", "ms": p1,
+            "phase1": {"kernels": ("fast_kernel + fast_verify_kernel + fast_orphan_fix_kernel" if single
+                                   else "seg_walk_kernel + seg_chain_kernel + seg_decode_kernel"),
+                       "path": "single pass over HBM (csrc/fast.cuh)" if single else "exact three-kernel path",
+                       "range_bytes": range_bytes, "fallbacks": fallbacks, "ms": p1,
                        "walk_ms": wms, "achieved": (n_bytes / (p1 / 1e3)) / 1e9,
                        "frac": (n_bytes / (p1 / 1e3)) / 1e9 / peak},
         },
@@ -307,7 +312,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    traffic = REPO / "profiles" / "seg_decode_traffic.json"
+    traffic = REPO / "profiles" / ("fast_kernel_traffic.json" if single else "seg_decode_traffic.json")
     if traffic.exists():
         tr = json.loads(traffic.read_text())
         line["roofline"]["traffic"] = tr.get("dram_bytes_per_launch")

@@ -981,7 +981,6 @@ static int launch_fast(hg_ctx* ctx) {
   CK(ctx->d_params.ensure(1));
   CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-  CK(cudaEventRecord(ctx->ev[6], ctx->stream));
   fast_kernel<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
@@ -1168,7 +1167,12 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->d2h_bytes += ctx->host_acc.size() * 8 + ctx->dev_acc.size() * 8 + arena_used + n_orph * sizeof(hg_orphan) +
                     n_err * sizeof(hg_trace_error) + ns * 8 + ctx->n_dev_rows * 12;
   float k_ms = 0, t_ms = 0;
-  if (!ctx->tile_stream.empty()) {
+  if (ctx->last_path == 1 && ctx->n_ranges) {  // single pass: decode = range kernel, chain = verification
+    cudaEventElapsedTime(&k_ms, ctx->ev[4], ctx->ev[5]);
+    ctx->walk_ms = 0;
+    cudaEventElapsedTime(&ctx->decode_ms, ctx->ev[4], ctx->ev[7]);
+    cudaEventElapsedTime(&ctx->chain_ms, ctx->ev[7], ctx->ev[5]);
+  } else if (!ctx->tile_stream.empty()) {
     cudaEventElapsedTime(&k_ms, ctx->ev[4], ctx->ev[5]);
     cudaEventElapsedTime(&ctx->walk_ms, ctx->ev[4], ctx->ev[6]);
     cudaEventElapsedTime(&ctx->chain_ms, ctx->ev[6], ctx->ev[7]);
