@@ -314,6 +314,7 @@ struct hg_ctx {
   DBuf<uint32_t> d_vplan;
   int last_path = 0;                // 1 = the last run's phase 1 was the single pass
   uint64_t fallbacks = 0;
+  uint32_t last_anom = 0;
   int smem_optin = 0;
 };
 
@@ -1083,6 +1084,8 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
       if (ctx->path_opt == 2) return fail(ctx, HG_ESTATE, "single-pass path rejected the trace (HAPIGPU_PATH=2)");
       fast = false;
       ctx->fallbacks++;
+      ctx->last_anom = (uint32_t)ctx->counters[C_ANOM];
+      if (getenv("HAPIGPU_DEBUG")) fprintf(stderr, "hapigpu: single pass rejected (reasons 0x%x)\n", ctx->last_anom);
       continue;
     }
     if (!grow) break;

@@ -33,13 +33,13 @@ constexpr uint32_t kRChunk = 128;                   // bytes per ring slot (one 
 constexpr uint32_t kRSlots = 2;                     // slots per lane
 constexpr uint32_t kRRing = kRChunk * kRSlots;      // 256-byte ring
 constexpr uint32_t kRWordMask = kRRing / 4 - 1;
-constexpr uint32_t kRMirror = 64;                   // slot 0's first bytes again after the ring
-constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: any 64-byte read needs no wrap
+constexpr uint32_t kRMirror = 32;                   // slot 0's first bytes again after the ring
+constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: header + first field need no wrap
 constexpr uint32_t kRInline = kRChunk;              // records up to this long are decoded from the ring
 constexpr int kRLag = 2;                            // iterations before a fill group is waited for
-constexpr int kRLS = 8;                             // open entries per lane in shared memory
-constexpr int kRLP = 4;                             // pending exits per lane in shared memory
-constexpr int kRQ = 64;                             // deferred-record queue per warp (drained at 32)
+constexpr int kRLS = 4;                             // open entries per lane in shared memory
+constexpr int kRLP = 2;                             // pending exits per lane in shared memory
+constexpr int kRQ = 64;                             // deferred-record queues per warp (drained at 32)
 constexpr uint32_t kRDeep = 256;                    // per-lane overflow chunk (SumEntry)
 constexpr uint32_t kRDeepHalf = kRDeep / 2;         // [0,128) pending exits, [128,256) open entries
 
@@ -57,7 +57,7 @@ constexpr uint32_t VP_VALID = 1u << 31, VP_STR = 1u << 30;
 
 struct RSmem {
   uint32_t tab, lanetab, lanetab_warp, dcache, ncache, warps, warp_bytes, total;
-  uint32_t ring, st_ts, st_fn, pd_ts, pd_meta, pd_k, q_off, q_s, ftab, ferr;  // within a warp block
+  uint32_t ring, st_ts, st_fn, pd_ts, pd_meta, pd_k, q_off, q_s, qs_off, qs_s, ftab, ferr;  // within a warp block
 };
 
 __host__ __device__ inline uint32_t r_align(uint32_t x) { return (x + 127u) & ~127u; }
@@ -85,8 +85,10 @@ __host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw) {
   L.pd_ts = w;   w += 8u * kRLP * kWarp;
   L.pd_meta = w; w += 4u * kRLP * kWarp;
   L.pd_k = w;    w += 4u * kRLP * kWarp;
-  L.q_off = w;   w += 8u * kRQ;
+  L.q_off = w;   w += 8u * kRQ;   // device / telemetry records
+  L.qs_off = w;  w += 8u * kRQ;   // string payloads to validate
   L.q_s = w;     w += 4u * kRQ;
+  L.qs_s = w;    w += 4u * kRQ;
   L.warp_bytes = r_align(w);
   off += L.warp_bytes * nw;
   L.total = off;
@@ -132,16 +134,23 @@ struct RLane {
   bool fresh;           // no requests until every pending fill of this lane completed (slot reuse)
 };
 
-// first offset in [t0, t1) with three consistent headers (see seg_walk_kernel)
+// first offset in [t0, t1) that starts a chain of kScanDepth plausible headers with
+// non-decreasing timestamps (or a shorter one that ends exactly at the stream end).
+// A wrong guess is caught by fast_verify_kernel and costs a whole exact pass, so the
+// single pass demands a longer chain than the segment walk (seg_walk_kernel: three).
+constexpr int kScanDepth = 8;
+
 __device__ __noinline__ uint64_t r_scan(const Params& p, const uint8_t* g, uint64_t size, uint64_t t0, uint64_t t1) {
   for (uint64_t o = t0; o < t1; o++) {
-    uint64_t n1, n2, n3, ts0, ts1, ts2;
-    if (!seg_plausible(p, g, size, o, n1, ts0)) continue;
-    if (n1 != size) {
-      if (!seg_plausible(p, g, size, n1, n2, ts1) || ts1 < ts0) continue;
-      if (n2 != size && (!seg_plausible(p, g, size, n2, n3, ts2) || ts2 < ts1)) continue;
+    uint64_t cur = o, nxt, ts, prev = 0;
+    int k = 0;
+    for (; k < kScanDepth; k++) {
+      if (!seg_plausible(p, g, size, cur, nxt, ts) || (k && ts < prev)) break;
+      prev = ts;
+      cur = nxt;
+      if (cur == size) { k = kScanDepth; break; }
     }
-    return o;
+    if (k == kScanDepth) return o;
   }
   return kNone;
 }
@@ -237,7 +246,7 @@ __device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T)
   st.n = R.n; st.np = R.np; st.ne = R.ne; st.pad = 0;
   p.rstate[R.r] = st;
   if (R.spans) atomicAdd(&p.stream_spans[R.s], (unsigned long long)R.spans);
-  if (R.bad) atomicExch(p.anom, 1u);
+  if (R.bad) atomicOr(p.anom, 1u);   // anomaly reasons (bits): 1 record, 2 drain, 4 string, 8 chain, 16 order
 }
 
 // a per-lane overflow chunk for deep stacks / many pending exits
@@ -378,7 +387,7 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
       else if (cls == HG_CLASS_TELEMETRY) err = seg_telemetry(p, gb, h.sid, rp, aux);
     }
     if (err) {
-      atomicExch(p.anom, 1u);
+      atomicOr(p.anom, 2u);
     } else if (cls == HG_CLASS_DEVICE) {
       K.x++;
       atomicAdd(&p.stream_spans[s], 1ull);
@@ -390,7 +399,20 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
   return K;
 }
 
-constexpr int kRMaxThreads = 12 * kWarp;
+constexpr int kRMaxThreads = 14 * kWarp;
+
+// strict UTF-8 of the one string field of inline records (tracefile.py:165), one per lane, from HBM
+__device__ __noinline__ void r_drain_str(const Params& p, const uint64_t* q_off, const uint32_t* q_s, uint32_t n) {
+  const uint32_t lane = lane_id();
+  if (lane < n) {
+    const uint64_t a = q_off[lane];
+    const uint8_t* gb = p.data + p.stream_base[q_s[lane]];
+    const uint32_t vp = __ldg(&p.vplan[g32(gb, a)]);
+    const uint64_t at = a + 16 + (vp & 0x3FFFu);
+    if (!g_utf8(gb, at + 4, g32(gb, at))) atomicOr(p.anom, 4u);
+  }
+  __syncwarp();
+}
 
 __device__ __forceinline__ void r_cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -519,6 +541,9 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
   const RTabs T = r_tabs(RL);
   uint64_t* q_off = reinterpret_cast<uint64_t*>(wb + RL.q_off);
   uint32_t* q_s = reinterpret_cast<uint32_t*>(wb + RL.q_s);
+  uint64_t* qs_off = reinterpret_cast<uint64_t*>(wb + RL.qs_off);
+  uint32_t* qs_s = reinterpret_cast<uint32_t*>(wb + RL.qs_s);
+  uint32_t qsn = 0;
   const uint32_t stride = gridDim.x * blockDim.x;
   constexpr uint32_t kPend = (1u << kRLag) - 1u;
   RLane R;
@@ -601,12 +626,17 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const bool lenbad = chk && (uint64_t)lead0 + 4u + ln + lead1 != plen;
     if (lenbad) R.bad = true;  // CorruptRecordError: the exact path names it
     const bool fast = (fE || fXp || fXq || fO) && !lenbad;
-    bool qflag = fast && (dt || (chk && (vp & VP_STR) && ln));
-    const uint32_t rw = (16u + 8u * d_resfield(d) + (pos & 3u)) >> 2;  // result field <= 5: mirror reach
+    bool qflag = fast && dt;
+    const bool sflag = fast && chk && (vp & VP_STR) && ln;
     uint64_t res = 0;
     if (fl & SF_RESULT) {
-      const uint32_t r0 = w[rw], r1 = w[rw + 1], r2 = w[rw + 2];
-      res = ((uint64_t)__funnelshift_r(r1, r2, sh) << 32) | __funnelshift_r(r0, r1, sh);
+      const uint32_t rf = d_resfield(d);
+      if (rf == 0) {  // the usual first field: inside the mirror reach
+        const uint32_t w5 = w[5], w6 = w[6];
+        res = ((uint64_t)__funnelshift_r(w5, w6, sh) << 32) | __funnelshift_r(w4, w5, sh);
+      } else {
+        res = r_u64(ring, pos + 16u + 8u * rf);
+      }
     }
     const bool err = res != 0;
     if (fast) {
@@ -653,7 +683,23 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     if (__any_sync(0xffffffffu, slow)) {
       if (slow) qflag = r_record_slow(gpr, R, T, K, hf);
     }
-    // deferred records: the record at q_off is consumed; UTF-8 / device fold / telemetry checks in the drain
+    // deferred records (already consumed): string UTF-8 checks, device folds and telemetry checks
+    const uint32_t sm = __ballot_sync(0xffffffffu, sflag);
+    if (sm) {
+      if (sflag) {
+        const uint32_t i = qsn + __popc(sm & lanemask_lt());
+        qs_off[i] = R.C0 + o_start;
+        qs_s[i] = R.s;
+      }
+      qsn += __popc(sm);
+      __syncwarp();
+      if (qsn >= (uint32_t)kWarp) {
+        r_drain_str(gpr, qs_off, qs_s, kWarp);
+        qsn -= kWarp;
+        if (lane < qsn) { qs_off[lane] = qs_off[kWarp + lane]; qs_s[lane] = qs_s[kWarp + lane]; }
+        __syncwarp();
+      }
+    }
     const uint32_t dm = __ballot_sync(0xffffffffu, qflag);
     if (dm) {
       if (qflag) {
@@ -673,6 +719,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if (qsn) r_drain_str(gpr, qs_off, qs_s, qsn);
   if (qd) {
     const uint2 dk = r_drain(gpr, L, q_off, q_s, qd);
     K.dev += dk.x; K.samples += dk.y;
@@ -706,7 +753,8 @@ __global__ void __launch_bounds__(128) fast_verify_kernel(Params p, unsigned lon
     for (int dd = 1; dd < 32; dd <<= 1) { const int v = __shfl_up_sync(0xffffffffu, pre, dd); if ((int)lane >= dd) pre = max(pre, v); }
     const uint64_t px = __shfl_sync(0xffffffffu, st.exit, pre < 0 ? 0 : pre);
     const uint64_t prev_exit = pre >= 0 ? px : c_exit;
-    bool ok = !valid || (hasE ? st.entry == prev_exit : prev_exit >= t1);
+    const bool chain_ok = !valid || (hasE ? st.entry == prev_exit : prev_exit >= t1);
+    bool ok = true;
     // timestamps keep rising across ranges (pipeline.py:98)
     int srcn = (valid && st.n) ? (int)lane : -1;
     int pn = __shfl_up_sync(0xffffffffu, srcn, 1);
@@ -716,6 +764,7 @@ __global__ void __launch_bounds__(128) fast_verify_kernel(Params p, unsigned lon
     const uint64_t prev_last = pn >= 0 ? pl : c_last;
     const bool has_prev = pn >= 0 || c_has;
     if (valid && st.n && has_prev && st.first_ts < prev_last) ok = false;
+    if (!chain_ok) atomicOr(p.anom, 8u);
     // record bases
     const uint64_t n = valid ? st.n : 0;
     uint64_t incl = n;
@@ -740,7 +789,7 @@ __global__ void __launch_bounds__(128) fast_verify_kernel(Params p, unsigned lon
     const uint32_t mn = __ballot_sync(0xffffffffu, valid && st.n);
     if (mn) { c_last = __shfl_sync(0xffffffffu, st.last_ts, 31 - __clz(mn)); c_has = true; }
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(p.anom, 1u);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.anom, 16u);
   if (lane == 0) {
     stream_nrec[s] = c_base;
     if (c_base) atomicAdd(&p.stats[ST_EVENTS], (unsigned long long)c_base);
