@@ -312,6 +312,8 @@ struct hg_ctx {
   DBuf<unsigned long long> d_range_base;
   std::vector<uint32_t> vplan;
   DBuf<uint32_t> d_vplan;
+  std::vector<uint4> fdesc;
+  DBuf<uint4> d_fdesc;
   int last_path = 0;                // 1 = the last run's phase 1 was the single pass
   uint64_t fallbacks = 0;
   uint32_t last_anom = 0;
@@ -590,7 +592,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_segw.release(); ctx->d_seginfo.release(); ctx->d_stream_nrec.release(); ctx->d_tl_rec_off.release();
   ctx->d_deep.release(); ctx->d_params.release();
   ctx->d_range_stream.release(); ctx->d_stream_range0.release(); ctx->d_rstate.release(); ctx->d_rseg.release();
-  ctx->d_range_base.release(); ctx->d_vplan.release();
+  ctx->d_range_base.release(); ctx->d_vplan.release(); ctx->d_fdesc.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -696,6 +698,33 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
     ctx->desc[schemas[i].id] = make_uint2((fn & 0xFFFFFu) | ((uint32_t)d.cls << 20) | (flags << 23) | D_PRESENT,
                                           (uint32_t)d.fixed_len | ((resf & 0xFFu) << 16) | ((uint32_t)d.counter_kind << 24));
   }
+  // inline-record descriptors of the range kernel (fast.cuh fdesc), one per id plus a sentinel
+  ctx->fdesc.assign(ctx->sid_map.size() + 1, make_uint4(M_FN | (FK_NEVER << 20), 1u, 0u, 0u));
+  for (uint32_t i = 0; i < n_schemas; i++) {
+    const uint32_t id = schemas[i].id;
+    const DSchema& d = ctx->schemas[ctx->sid_map[id]];
+    const uint2 dd = ctx->desc[id];
+    const uint32_t resf = (dd.y >> 16) & 0xFFu;
+    const bool var = (d.flags & SF_VAR) != 0;
+    const bool dt = d.cls == HG_CLASS_DEVICE || d.cls == HG_CLASS_TELEMETRY;
+    const uint32_t vp = ctx->vplan[id];
+    bool never = (d.flags & SF_FEED_ALWAYS) != 0;
+    if (d.cls == HG_CLASS_EXIT && (d.flags & SF_RESULT) && ((d.flags & SF_RESULT_F64) || resf != 0)) never = true;
+    if (var && !dt && !(vp & VP_VALID)) never = true;
+    const uint32_t lo = d.fixed_len, hi = var ? kRInline - 16u : d.fixed_len;
+    if (lo > kRInline - 16u) never = true;
+    if (never) continue;
+    const uint32_t kind = d.cls == HG_CLASS_ENTRY ? FK_ENTRY : d.cls == HG_CLASS_EXIT ? FK_EXIT : dt ? FK_DEFER : FK_PASS;
+    uint32_t x = (dd.x & M_FN) | (kind << 20) | (result_kind(d.flags) << 26);
+    if (d.cls == HG_CLASS_EXIT && (d.flags & SF_RESULT)) x |= FD_RES;
+    uint32_t z = 0;
+    if (var && !dt) {
+      x |= FD_VAR;
+      if (vp & VP_STR) x |= FD_STR;
+      z = (vp & 0x3FFFu) | (((vp >> 14) & 0x3FFFu) << 16);
+    }
+    ctx->fdesc[id] = make_uint4(x, lo | (hi << 16), z, 0u);
+  }
   ctx->fast_warps = 0;
   ctx->staged = false;
   cudaSetDevice(ctx->cfg.device);
@@ -710,6 +739,8 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
   CK(cudaMemcpy(ctx->d_desc.ptr, ctx->desc.data(), ctx->desc.size() * sizeof(uint2), cudaMemcpyHostToDevice));
   CK(ctx->d_vplan.ensure(ctx->vplan.size()));
   CK(cudaMemcpy(ctx->d_vplan.ptr, ctx->vplan.data(), ctx->vplan.size() * 4, cudaMemcpyHostToDevice));
+  CK(ctx->d_fdesc.ensure(ctx->fdesc.size()));
+  CK(cudaMemcpy(ctx->d_fdesc.ptr, ctx->fdesc.data(), ctx->fdesc.size() * sizeof(uint4), cudaMemcpyHostToDevice));
   if (n_kinds) {
     CK(cudaMemcpy(ctx->d_kinds.ptr, kinds, n_kinds, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_field_role.ptr, ctx->field_role.data(), n_kinds, cudaMemcpyHostToDevice));
@@ -755,8 +786,9 @@ static int build_layout(hg_ctx* ctx) {
     for (uint32_t t = 0; t < nt; t++) ctx->tile_stream.push_back(s);
   }
   // ranges for the single pass: one per resident lane, never crossing a stream
+  const uint32_t n_fd = ctx->max_sid < (uint32_t)kSdescMax ? ctx->max_sid + 2 : 0u;
   uint32_t nw = kRMaxThreads / kWarp;
-  while (nw > 1 && fast_smem_layout(ctx->n_fn, nw).total > (uint32_t)ctx->smem_optin) nw--;
+  while (nw > 1 && fast_smem_layout(ctx->n_fn, nw, n_fd).total > (uint32_t)ctx->smem_optin) nw--;
   ctx->fast_warps = nw;
   const uint64_t lanes = (uint64_t)std::max(ctx->sm_count, 1) * nw * kWarp;
   uint64_t payload = 0, max_pay = 0;
@@ -944,6 +976,7 @@ static Params make_params(hg_ctx* ctx) {
   p.range_base = ctx->d_range_base.ptr;
   p.anom = reinterpret_cast<uint32_t*>(C + C_ANOM);
   p.vplan = ctx->d_vplan.ptr;
+  p.fdesc = ctx->d_fdesc.ptr;
   return p;
 }
 
@@ -975,14 +1008,17 @@ static int launch_fast(hg_ctx* ctx) {
   Params p = make_params(ctx);
   p.state = ctx->d_rseg.ptr;
   const uint32_t nw = ctx->fast_warps;
-  const size_t smem = fast_smem_layout(ctx->n_fn, nw).total;
-  CK(cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
+  const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
+  CK(cudaFuncSetAttribute(fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CK(cudaFuncSetAttribute(fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint32_t per_cta = nw * kWarp;
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));
   CK(ctx->d_params.ensure(1));
   CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-  fast_kernel<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
+  if (sd) fast_kernel<true><<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
+  else fast_kernel<false><<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
   fast_verify_kernel<<<(ns + 3) / 4, 128, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);

@@ -56,13 +56,14 @@ struct RangeState {
 constexpr uint32_t VP_VALID = 1u << 31, VP_STR = 1u << 30;
 
 struct RSmem {
-  uint32_t tab, lanetab, lanetab_warp, dcache, ncache, warps, warp_bytes, total;
+  uint32_t tab, lanetab, lanetab_warp, dcache, ncache, fdesc, warps, warp_bytes, total;
   uint32_t ring, st_ts, st_fn, pd_ts, pd_meta, pd_k, q_off, q_s, qs_off, qs_s, ftab, ferr;  // within a warp block
 };
 
 __host__ __device__ inline uint32_t r_align(uint32_t x) { return (x + 127u) & ~127u; }
 
-__host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw) {
+// n_fd: inline-record descriptors staged in shared memory (0: read through L1)
+__host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw, uint32_t n_fd) {
   RSmem L;
   uint32_t off = r_align(8u * kSdescMax);  // compact descriptors first (desc_of, kernels.cuh)
   const bool small = n_fn <= kSmallF;
@@ -74,6 +75,8 @@ __host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw) {
   off += r_align((uint32_t)sizeof(DevRow) * kDevSlots);
   L.ncache = off;
   off += r_align((uint32_t)sizeof(NameSlot) * kSegNameSlots);
+  L.fdesc = off;
+  off += r_align(16u * n_fd);
   L.warps = off;
   uint32_t w = 0;
   L.ring = w;    w += kRStride * kWarp;
@@ -123,6 +126,7 @@ struct RLane {
   const uint8_t* g;     // stream bytes from C0
   uint64_t C0;          // stream offset of chunk 0
   uint64_t size;        // stream size - C0
+  uint32_t size32;      // min(size, 2^32 - 1)
   uint64_t prev_ts, first_ts;
   SumEntry* deep;       // overflow chunk (nullptr until needed)
   uint32_t o, t1, entry;
@@ -175,6 +179,7 @@ __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, u
     R.C0 = entry & ~(uint64_t)(kRChunk - 1);
     R.g = g + R.C0;
     R.size = size - R.C0;
+    R.size32 = R.size < 0xFFFFFFFFull ? (uint32_t)R.size : 0xFFFFFFFFu;
     R.o = (uint32_t)(entry - R.C0);
     R.entry = R.o;
     R.t1 = (uint32_t)(t1 - R.C0);
@@ -187,7 +192,7 @@ __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, u
     return true;
   }
   R.r = p.n_ranges;
-  R.o = R.t1 = R.entry = 0; R.C0 = 0; R.size = 0; R.g = p.data;
+  R.o = R.t1 = R.entry = 0; R.C0 = 0; R.size = 0; R.size32 = 0; R.g = p.data;
   R.n = R.np = R.ne = R.ci = R.clast = 0;
   R.bad = false; R.fresh = true;
   return false;
@@ -414,6 +419,17 @@ __device__ __noinline__ void r_drain_str(const Params& p, const uint64_t* q_off,
   __syncwarp();
 }
 
+// inline-record descriptor (fdesc, one uint4 per schema id, built by hg_set_registry):
+// x = function (19 bits) | kind << 20 | flags; y = min payload | max inline payload << 16;
+// z = fixed bytes before | after the one variable field (blob / string)
+enum : uint32_t { FK_ENTRY = 0, FK_EXIT = 1, FK_PASS = 2, FK_DEFER = 3, FK_NEVER = 7 };
+constexpr uint32_t FD_STR = 1u << 23, FD_VAR = 1u << 24, FD_RES = 1u << 25;  // result kind at bits 26-27
+
+__device__ __forceinline__ void r_cp16p(uint32_t dst, const void* src, uint32_t pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; }"
+               ::"r"(dst), "l"(src), "r"(pred) : "memory");
+}
+
 __device__ __forceinline__ void r_cp16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -429,7 +445,9 @@ __device__ __noinline__ void r_fold_flush(const Params& p, uint32_t fn, uint64_t
   add_i128(&a[2], &a[3], cs & (kFCount - 1), 0);
 }
 
-__device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uint32_t nw) {
+__device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uint32_t nw, uint32_t n_fd) {
+  uint4* fd = reinterpret_cast<uint4*>(g_smem + RL.fdesc);
+  for (uint32_t i = threadIdx.x; i < n_fd; i += blockDim.x) fd[i] = __ldg(&p.fdesc[i]);
   if (p.max_sid < (uint32_t)kSdescMax) {
     uint2* t = reinterpret_cast<uint2*>(g_smem);
     for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) t[i] = __ldg(&p.desc[i]);
@@ -520,16 +538,20 @@ __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, const S
   }
 }
 
+// kSD: the registry's inline descriptors fit in shared memory (max_sid < kSdescMax)
+template <bool kSD>
 __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const Params* gp) {
   const Params& gpr = *gp;
   const uint32_t nw = blockDim.x >> 5;
-  const RSmem RL = fast_smem_layout(p.n_fn, nw);
+  const uint32_t n_fd = kSD ? p.max_sid + 2 : 0u;
+  const RSmem RL = fast_smem_layout(p.n_fn, nw, n_fd);
+  const uint4* fdesc_s = reinterpret_cast<const uint4*>(g_smem + RL.fdesc);
   const SegSmem L = r_segsmem(RL);
   const uint32_t lane = lane_id();
   uint8_t* wb = g_smem + RL.warps + (threadIdx.x >> 5) * RL.warp_bytes;
   const uint32_t* ring = reinterpret_cast<const uint32_t*>(wb + RL.ring + lane * kRStride);
   const uint32_t ring_s = s_addr(ring);
-  r_prologue(p, RL, nw);
+  r_prologue(p, RL, nw, n_fd);
   SegCounters K;
   K.passed = K.host = K.dev = K.samples = K.orph = K.items = 0;
   HostFold hf;  // the slow path's fold: CTA table (medium function sets) or global rows
@@ -550,6 +572,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
   R.recent = 0;
   bool live = r_begin(gpr, R, blockIdx.x * blockDim.x + threadIdx.x, stride);
   uint32_t qd = 0;
+  const uint32_t sid_cap = p.max_sid + 1;  // fdesc[max_sid + 1]: never inline (unknown ids, slow path names them)
   while (__any_sync(0xffffffffu, live)) {
     const bool ending = live && (R.o >= R.t1 || R.bad);
     if (__any_sync(0xffffffffu, ending)) {
@@ -560,21 +583,20 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     }
     const bool act = live && R.o < R.t1 && !R.bad;
     const uint32_t o_start = R.o;
-    // ---- ring refill: one 128-byte chunk per lane and iteration; four chunks per cp.async instruction
+    // ---- ring refill: the lane copies its next line itself (8 x 16 B cp.async, + the mirror for slot 0)
     const uint32_t cons = R.o / kRChunk;
     if (act && cons > R.ci) { R.ci = cons; R.fresh = true; }  // a long record jumped over chunks
     if (!(R.recent & kPend)) R.fresh = false;
     const bool want = act && !R.fresh && R.ci <= R.clast && R.ci < cons + kRSlots;
-    if (want) {  // the lane copies its own line: 8 x 16 B (plus the mirror for slot 0)
+    {
       const uint32_t q = R.ci & (kRSlots - 1);
       const uint8_t* src = R.g + (uint64_t)R.ci * kRChunk;
       const uint32_t dst = ring_s + q * kRChunk;
+      const uint32_t pw = want ? 1u : 0u, pm = (want && q == 0) ? 1u : 0u;
       #pragma unroll
-      for (uint32_t k = 0; k < kRChunk; k += 16) r_cp16(dst + k, src + k);
-      if (q == 0) {
-        #pragma unroll
-        for (uint32_t k = 0; k < kRMirror; k += 16) r_cp16(ring_s + kRRing + k, src + k);
-      }
+      for (uint32_t k = 0; k < kRChunk; k += 16) r_cp16p(dst + k, src + k, pw);
+      #pragma unroll
+      for (uint32_t k = 0; k < kRMirror; k += 16) r_cp16p(ring_s + kRRing + k, src + k, pm);
     }
     R.ci += want ? 1u : 0u;
     R.recent = (R.recent << 1) | (want ? 1u : 0u);
@@ -585,64 +607,43 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const uint32_t cr = R.ci - __popc(R.recent & kPend);
     const bool ready = act && min((R.o + 15u) / kRChunk, R.clast) < cr;
     const uint32_t pos = R.o & (kRRing - 1);
-    const uint32_t* w = ring + (pos >> 2);  // up to 64 bytes from here without wrapping (mirror)
+    const uint32_t* w = ring + (pos >> 2);  // header and first field: no wrap (mirror)
     const uint32_t sh = (pos & 3u) << 3;
-    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4], w5 = w[5], w6 = w[6];
     const uint32_t sid = __funnelshift_r(w0, w1, sh);
     const uint64_t ts = ((uint64_t)__funnelshift_r(w2, w3, sh) << 32) | __funnelshift_r(w1, w2, sh);
     const uint32_t plen = __funnelshift_r(w3, w4, sh);
-    const bool sid_ok = sid <= p.max_sid;
-    const uint32_t sidc = sid_ok ? sid : 0u;
-    uint2 d = __ldg(&p.desc[sidc]);
-    const uint32_t vp = __ldg(&p.vplan[sidc]);
-    if (!sid_ok) d.x = 0;
-    const uint32_t cls = d_cls(d), fl = d_flags(d);
-    const uint32_t fnm = d.x & M_FN;
-    const uint32_t fixed = d_fixed(d);
-    const bool var = (fl & SF_VAR) != 0;
-    const bool isE = cls == HG_CLASS_ENTRY, isX = cls == HG_CLASS_EXIT;
-    const bool dt = cls == HG_CLASS_DEVICE || cls == HG_CLASS_TELEMETRY;
+    const uint4 D = kSD ? fdesc_s[min(sid, sid_cap)] : __ldg(&p.fdesc[min(sid, sid_cap)]);
+    const uint32_t fnm = D.x & M_FN;
+    const uint32_t kind = (D.x >> 20) & 7u;
     const uint32_t ne = R.ne, np = R.np;
     const uint32_t topi = ((ne - 1u) < (uint32_t)kRLS ? ne - 1u : 0u) * kWarp;
     const uint64_t ets = T.st_ts[topi];
     const uint32_t tfn = T.st_fn[topi];
-    const uint32_t size32 = R.size < 0xFFFFFFFFull ? (uint32_t)R.size : 0xFFFFFFFFu;
-    // inline: the whole record is in the ring, in order, with a length its schema allows
-    // ... then the whole record (inline records are at most kRInline bytes: two slots)
-    const bool inl = plen <= kRInline - 16u;
-    const bool rec_in = (R.o + 15u + plen) / kRChunk < cr;
-    const bool stall = ready && inl && !rec_in && (uint64_t)R.o + 16u + plen <= R.size;
-    const bool good = ready && rec_in && (d.x & (D_PRESENT | (SF_NOINLINE << 23))) == D_PRESENT &&
-                      (plen == fixed || (var && plen > fixed)) && inl &&
-                      R.o + 16u + plen <= size32 && !(R.n && ts < R.prev_ts);
-    const bool fE = good && isE && ne < (uint32_t)kRLS;
-    const bool fXp = good && isX && ne && ne <= (uint32_t)kRLS && tfn == fnm;  // pops a same-function top
-    const bool fXq = good && isX && !ne && np < (uint32_t)kRLP;               // pending: compose decides
-    const bool fO = good && !isE && !isX;
+    // inline: the whole record in the ring, in order, with a length its schema allows (lo <= plen <= hi <= 112)
+    const uint32_t lo = D.y & 0xFFFFu, hi = D.y >> 16;
+    const bool good = ready && plen - lo <= hi - lo && (R.o + 15u + plen) / kRChunk < cr &&
+                      R.o + 16u + plen <= R.size32 && (R.n == 0 || ts >= R.prev_ts);
+    const bool stall = ready && !good && plen <= kRInline - 16u && (R.o + 15u + plen) / kRChunk >= cr &&
+                       (uint64_t)R.o + 16u + plen <= R.size;
+    const bool fE = good && kind == FK_ENTRY && ne < (uint32_t)kRLS;
+    const bool fXp = good && kind == FK_EXIT && ne - 1u < (uint32_t)kRLS && tfn == fnm;  // pops a same-function top
+    const bool fXq = good && kind == FK_EXIT && ne == 0 && np < (uint32_t)kRLP;          // pending: compose decides
+    const bool fO = good && (kind == FK_PASS || kind == FK_DEFER);
     // one variable field (blob / string): exact length here, UTF-8 of strings in the drain
-    const uint32_t lead0 = vp & 0x3FFFu, lead1 = (vp >> 14) & 0x3FFFu;
+    const uint32_t lead0 = D.z & 0xFFFFu, lead1 = D.z >> 16;
+    const bool chk = (D.x & FD_VAR) != 0;
     const uint32_t ln = r_u32(ring, pos + 16u + lead0);
-    const bool chk = (fE || fXp || fXq || fO) && var && !dt;
-    const bool lenbad = chk && (uint64_t)lead0 + 4u + ln + lead1 != plen;
+    const bool lenbad = (fE || fXp || fXq || fO) && chk && lead0 + 4u + (uint64_t)ln + lead1 != plen;
     if (lenbad) R.bad = true;  // CorruptRecordError: the exact path names it
     const bool fast = (fE || fXp || fXq || fO) && !lenbad;
-    bool qflag = fast && dt;
-    const bool sflag = fast && chk && (vp & VP_STR) && ln;
-    uint64_t res = 0;
-    if (fl & SF_RESULT) {
-      const uint32_t rf = d_resfield(d);
-      if (rf == 0) {  // the usual first field: inside the mirror reach
-        const uint32_t w5 = w[5], w6 = w[6];
-        res = ((uint64_t)__funnelshift_r(w5, w6, sh) << 32) | __funnelshift_r(w4, w5, sh);
-      } else {
-        res = r_u64(ring, pos + 16u + 8u * rf);
-      }
-    }
+    bool qflag = fast && kind == FK_DEFER;
+    const bool sflag = fast && (D.x & FD_STR) && ln;
+    const uint64_t res = (D.x & FD_RES) ? ((uint64_t)__funnelshift_r(w5, w6, sh) << 32) | __funnelshift_r(w4, w5, sh) : 0ull;
     const bool err = res != 0;
     if (fast) {
-      const uint32_t k = R.n;
-      R.n = k + 1;
-      R.first_ts = k ? R.first_ts : ts;
+      R.first_ts = R.n ? R.first_ts : ts;
+      R.n++;
       R.prev_ts = ts;
       R.o += 16u + plen;
     }
@@ -653,7 +654,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     if (fXq) {
       const uint32_t i = np * kWarp;
       T.pd_ts[i] = ts;
-      T.pd_meta[i] = fnm | ((1u | (err ? 2u : 0u) | (result_kind(fl) << 4)) << 19);
+      T.pd_meta[i] = fnm | ((1u | (err ? 2u : 0u) | (((D.x >> 26) & 3u) << 4)) << 19);
       T.pd_k[i] = R.n - 1;
     }
     R.ne = ne + (fE ? 1u : 0u) - (fXp ? 1u : 0u);
@@ -669,17 +670,17 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
         }
         ftab[fnm * kWarp] = cs;
         if (err) atomicAdd(&ferr[fnm], 1u);
-        if (du < *(volatile uint32_t*)&ferr[p.n_fn + fnm]) atomicMin(&ferr[p.n_fn + fnm], du);
-        if (du > *(volatile uint32_t*)&ferr[2 * p.n_fn + fnm]) atomicMax(&ferr[2 * p.n_fn + fnm], du);
+        atomicMin(&ferr[p.n_fn + fnm], du);
+        atomicMax(&ferr[2 * p.n_fn + fnm], du);
       } else {
         hf.fold(gpr, (int32_t)fnm, dur, err);
       }
       K.host++;
       R.spans++;
     }
-    K.passed += (fO && !dt) ? 1u : 0u;
+    K.passed += (fO && kind == FK_PASS) ? 1u : 0u;
     // everything else from HBM (the ring is only a cache of the stream)
-    const bool slow = ready && !fast && !R.bad && !stall;
+    const bool slow = ready && !fast && !R.bad && !stall;  // unknown ids, long records, deep stacks, orphans ...
     if (__any_sync(0xffffffffu, slow)) {
       if (slow) qflag = r_record_slow(gpr, R, T, K, hf);
     }
