@@ -404,7 +404,7 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
   return K;
 }
 
-constexpr int kRMaxThreads = 14 * kWarp;
+constexpr int kRMaxThreads = 12 * kWarp;
 
 // strict UTF-8 of the one string field of inline records (tracefile.py:165), one per lane, from HBM
 __device__ __noinline__ void r_drain_str(const Params& p, const uint64_t* q_off, const uint32_t* q_s, uint32_t n) {
