@@ -29,13 +29,13 @@
 
 namespace hg {
 
-constexpr uint32_t kRChunk = 128;                   // bytes per ring slot (one line)
-constexpr uint32_t kRSlots = 2;                     // slots per lane
+constexpr uint32_t kRChunk = 64;                    // bytes per ring slot (half a line)
+constexpr uint32_t kRSlots = 4;                     // slots per lane
 constexpr uint32_t kRRing = kRChunk * kRSlots;      // 256-byte ring
 constexpr uint32_t kRWordMask = kRRing / 4 - 1;
 constexpr uint32_t kRMirror = 32;                   // slot 0's first bytes again after the ring
 constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: header + first field need no wrap
-constexpr uint32_t kRInline = kRChunk;              // records up to this long are decoded from the ring
+constexpr uint32_t kRInline = 128;                  // records up to this long are decoded from the ring
 constexpr int kRLag = 2;                            // iterations before a fill group is waited for
 constexpr int kRLS = 4;                             // open entries per lane in shared memory
 constexpr int kRLP = 2;                             // pending exits per lane in shared memory
