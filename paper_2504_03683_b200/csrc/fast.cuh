@@ -29,8 +29,8 @@
 
 namespace hg {
 
-constexpr uint32_t kRChunk = 64;                    // bytes per ring slot (half a line)
-constexpr uint32_t kRSlots = 4;                     // slots per lane
+constexpr uint32_t kRChunk = 32;                    // bytes per ring slot (one sector)
+constexpr uint32_t kRSlots = 8;                     // slots per lane
 constexpr uint32_t kRRing = kRChunk * kRSlots;      // 256-byte ring
 constexpr uint32_t kRWordMask = kRRing / 4 - 1;
 constexpr uint32_t kRMirror = 32;                   // slot 0's first bytes again after the ring
