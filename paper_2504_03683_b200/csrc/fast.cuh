@@ -38,10 +38,10 @@ constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: head
 constexpr uint32_t kRInline = 128;                  // records up to this long are decoded from the ring
 constexpr int kRLag = 2;                            // iterations before a fill group is waited for
 constexpr int kRLS = 4;                             // open entries per lane in shared memory
-constexpr int kRLP = 2;                             // pending exits per lane in shared memory
+constexpr int kRLP = 4;                             // pending exits per lane in shared memory
 constexpr int kRQ = 64;                             // deferred-record queues per warp (drained at 32)
-constexpr uint32_t kRDeep = 256;                    // per-lane overflow chunk (SumEntry)
-constexpr uint32_t kRDeepHalf = kRDeep / 2;         // [0,128) pending exits, [128,256) open entries
+constexpr uint32_t kRDeep = 128;                    // per-lane overflow chunk (SumEntry)
+constexpr uint32_t kRDeepHalf = kRDeep / 2;         // first half pending exits, second half open entries
 
 struct RangeState {
   uint64_t entry;      // speculative first record (kNone: no plausible header in the range)
