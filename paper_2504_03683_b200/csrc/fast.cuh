@@ -638,7 +638,21 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     if (lenbad) R.bad = true;  // CorruptRecordError: the exact path names it
     const bool fast = (fE || fXp || fXq || fO) && !lenbad;
     bool qflag = fast && kind == FK_DEFER;
-    const bool sflag = fast && (D.x & FD_STR) && ln;
+    bool sflag = fast && (D.x & FD_STR) && ln;
+    if (sflag && ln <= 16u) {  // short strings (kernel names): all-ASCII from the ring, else the drain decides
+      const uint32_t sp = pos + 20u + lead0, sw = sp >> 2, s0 = (sp & 3u) << 3;
+      const uint32_t e = sp + ln, ew = (e - 1u) >> 2;  // last word holding a string byte
+      uint32_t acc = 0;
+      #pragma unroll
+      for (uint32_t k = 0; k < 5; k++) {
+        const uint32_t wk = sw + k;
+        uint32_t x = ring[wk & kRWordMask];
+        if (k == 0) x &= 0xffffffffu << s0;
+        if (wk == ew) x &= 0xffffffffu >> (8u * ((4u - (e & 3u)) & 3u));
+        acc |= wk <= ew ? x : 0u;
+      }
+      sflag = (acc & 0x80808080u) != 0;
+    }
     const uint64_t res = (D.x & FD_RES) ? ((uint64_t)__funnelshift_r(w5, w6, sh) << 32) | __funnelshift_r(w4, w5, sh) : 0ull;
     const bool err = res != 0;
     if (fast) {

@@ -15,7 +15,7 @@ from pathlib import Path
 from .errors import EngineError
 
 HERE = Path(__file__).resolve().parent
-LIB_PATH = HERE / "libhapigpu.so"
+LIB_PATH = Path(os.environ["HAPIGPU_LIB"]) if os.environ.get("HAPIGPU_LIB") else HERE / "libhapigpu.so"
 CSRC = HERE / "csrc"
 INCLUDE = HERE.parent / "include"
 
