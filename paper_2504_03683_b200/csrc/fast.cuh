@@ -41,7 +41,9 @@ constexpr int kRLS = 4;                             // open entries per lane in 
 constexpr int kRLP = 4;                             // pending exits per lane in shared memory
 constexpr int kRQ = 64;                             // deferred-record queues per warp (drained at 32)
 constexpr uint32_t kRDeep = 128;                    // per-lane overflow chunk (SumEntry)
-constexpr uint32_t kRDeepHalf = kRDeep / 2;         // first half pending exits, second half open entries
+constexpr uint32_t kRDeepHalf = kRDeep / 2;
+constexpr uint32_t kRNames = 64;                    // CTA name cache slots (64 B: seq, row, len, hash, 40 name bytes)
+constexpr uint32_t kRNameMax = 40;         // first half pending exits, second half open entries
 
 struct RangeState {
   uint64_t entry;      // speculative first record (kNone: no plausible header in the range)
@@ -73,8 +75,8 @@ __host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw, ui
   L.lanetab_warp = 0;
   L.dcache = off;
   off += r_align((uint32_t)sizeof(DevRow) * kDevSlots);
-  L.ncache = off;
-  off += r_align((uint32_t)sizeof(NameSlot) * kSegNameSlots);
+  L.ncache = off;  // kRNames x 64 B seqlocked name cache (fast.cuh), not seg.cuh's NameSlot table
+  off += 64u * kRNames;
   L.fdesc = off;
   off += r_align(16u * n_fd);
   L.warps = off;
@@ -360,10 +362,61 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
   return false;
 }
 
+// ---- device-name cache: (hash, row, name bytes) slots under a sequence lock in shared memory,
+// filled by the drain after a global dictionary lookup; a hit avoids the dictionary's atomics
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+// fill the CTA name cache slot of a name found in (or added to) the global dictionary
+__device__ __forceinline__ void r_name_fill(uint32_t nc_s, uint64_t h, uint32_t row, const uint8_t* g, uint64_t no,
+                                            uint32_t nl) {
+  if (nl > kRNameMax) return;
+  const uint32_t slot = nc_s + (uint32_t)(h & (kRNames - 1)) * 64u;
+  uint32_t s;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s) : "r"(slot) : "memory");
+  if (s & 1u) return;
+  uint32_t old;
+  asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(slot), "r"(s), "r"(s + 1u) : "memory");
+  if (old != s) return;
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 4), "r"(row) : "memory");
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 8), "r"(nl) : "memory");
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 16), "r"((uint32_t)h) : "memory");
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 20), "r"((uint32_t)(h >> 32)) : "memory");
+  for (uint32_t i = 0; i < nl; i += 4) {
+    uint32_t w = g32(g, no + i);
+    if (nl - i < 4) w &= 0xffffffffu >> (8u * (4u - (nl - i)));
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 24 + i), "r"(w) : "memory");
+  }
+  asm volatile("membar.cta; st.volatile.shared.u32 [%0], %1;" ::"r"(slot), "r"(s + 2u) : "memory");
+}
+
+// CTA cache lookup of a name in HBM: the row, or ~0 (miss, long name or a slot being written)
+__device__ __forceinline__ uint32_t r_name_probe(uint32_t nc_s, uint64_t h, const uint8_t* g, uint64_t no, uint32_t nl) {
+  if (nl > kRNameMax) return 0xffffffffu;
+  const uint32_t slot = nc_s + (uint32_t)(h & (kRNames - 1)) * 64u;
+  uint32_t s1;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s1) : "r"(slot) : "memory");
+  if (!s1 || (s1 & 1u)) return 0xffffffffu;
+  const uint32_t row = lds32(slot + 4), len = lds32(slot + 8);
+  const uint64_t sh = ((uint64_t)lds32(slot + 20) << 32) | lds32(slot + 16);
+  if (sh != h || len != nl) return 0xffffffffu;
+  for (uint32_t i = 0; i < nl; i += 4) {
+    const uint32_t m = nl - i < 4 ? 0xffffffffu >> (8u * (4u - (nl - i))) : 0xffffffffu;
+    if ((g32(g, no + i) & m) != (lds32(slot + 24 + i) & m)) return 0xffffffffu;
+  }
+  uint32_t s2;
+  asm volatile("membar.cta; ld.volatile.shared.u32 %0, [%1];" : "=r"(s2) : "r"(slot) : "memory");
+  return s2 == s1 ? row : 0xffffffffu;
+}
+
 // deferred records, one per lane, read from HBM (L2): device-profiling and telemetry
 // records (fold / range checks) and string payloads of inline records (UTF-8)
 __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const uint64_t* q_off, const uint32_t* q_s,
-                                      uint32_t n) {
+                                      uint32_t n, uint32_t nc_s) {
   uint2 K = make_uint2(0, 0);
   const uint32_t lane = lane_id();
   if (lane < n) {
@@ -387,9 +440,28 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
       const uint64_t at = a + 16 + (vp & 0x3FFFu);
       if (!g_utf8(gb, at + 4, g32(gb, at))) err = HG_ERR_UTF8;
     }
-    if (!err) {
-      if (cls == HG_CLASS_DEVICE) err = seg_device(p, L, gb, size, h.sid, rp, rl, aux);
-      else if (cls == HG_CLASS_TELEMETRY) err = seg_telemetry(p, gb, h.sid, rp, aux);
+    if (!err && cls == HG_CLASS_DEVICE) {  // seg_device with the global dictionary, then fill the CTA cache
+      if (d_flags(d) & SF_FEED_ALWAYS) {
+        err = HG_ERR_FEED;
+      } else {
+        const DSchema* sc = schema_of(p, h.sid);
+        const uint64_t ua = g64(gb, rp[HG_ROLE_START]), ub = g64(gb, rp[HG_ROLE_END]);
+        const int64_t ah = (sc->role_kind[HG_ROLE_START] == HG_KIND_I64 && (int64_t)ua < 0) ? -1 : 0;
+        const int64_t bh = (sc->role_kind[HG_ROLE_END] == HG_KIND_I64 && (int64_t)ub < 0) ? -1 : 0;
+        const uint64_t no = rp[HG_ROLE_NAME];
+        const uint32_t nl = rl[HG_ROLE_NAME];
+        const uint64_t hh = g_hash(gb, no, nl);
+        uint32_t row = r_name_probe(nc_s, hh, gb, no, nl);  // CTA cache: no global atomics on a hit
+        if (row == 0xffffffffu) {
+          row = g_name_lookup(p.names, gb, no, nl, hh);
+          if (row != 0xffffffffu) r_name_fill(nc_s, hh, row, gb, no, nl);
+        }
+        if (row != 0xffffffffu) {
+          fold_device(p, reinterpret_cast<DevRow*>(g_smem + L.dcache), row, ub - ua, bh - ah - (ub < ua ? 1 : 0));
+        }
+      }
+    } else if (!err && cls == HG_CLASS_TELEMETRY) {
+      err = seg_telemetry(p, gb, h.sid, rp, aux);
     }
     if (err) {
       atomicOr(p.anom, 2u);
@@ -471,8 +543,8 @@ __device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uin
     DevRow z; z.tag = 0; z.count = 0; z.s0 = z.s1 = z.s2 = z.pad = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
     dcache[i] = z;
   }
-  NameSlot* ncache = reinterpret_cast<NameSlot*>(g_smem + RL.ncache);
-  for (uint32_t i = threadIdx.x; i < kSegNameSlots; i += blockDim.x) { ncache[i].hash = 0; ncache[i].row = 0; }
+  uint32_t* ncache = reinterpret_cast<uint32_t*>(g_smem + RL.ncache);
+  for (uint32_t i = threadIdx.x; i < kRNames; i += blockDim.x) ncache[16 * i] = 0;  // seq 0: empty
   (void)nw;
   __syncthreads();
 }
@@ -551,6 +623,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
   uint8_t* wb = g_smem + RL.warps + (threadIdx.x >> 5) * RL.warp_bytes;
   const uint32_t* ring = reinterpret_cast<const uint32_t*>(wb + RL.ring + lane * kRStride);
   const uint32_t ring_s = s_addr(ring);
+  const uint32_t nc_s = s_addr(g_smem + RL.ncache);
   r_prologue(p, RL, nw, n_fd);
   SegCounters K;
   K.passed = K.host = K.dev = K.samples = K.orph = K.items = 0;
@@ -725,7 +798,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       qd += __popc(dm);
       __syncwarp();
       if (qd >= (uint32_t)kWarp) {
-        const uint2 dk = r_drain(gpr, L, q_off, q_s, kWarp);
+        const uint2 dk = r_drain(gpr, L, q_off, q_s, kWarp, nc_s);
         K.dev += dk.x; K.samples += dk.y;
         qd -= kWarp;
         if (lane < qd) { q_off[lane] = q_off[kWarp + lane]; q_s[lane] = q_s[kWarp + lane]; }
@@ -736,7 +809,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
   asm volatile("cp.async.wait_all;" ::: "memory");
   if (qsn) r_drain_str(gpr, qs_off, qs_s, qsn);
   if (qd) {
-    const uint2 dk = r_drain(gpr, L, q_off, q_s, qd);
+    const uint2 dk = r_drain(gpr, L, q_off, q_s, qd, nc_s);
     K.dev += dk.x; K.samples += dk.y;
   }
   __syncwarp();
