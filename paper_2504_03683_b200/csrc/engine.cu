@@ -1021,7 +1021,7 @@ static int launch_fast(hg_ctx* ctx) {
   else fast_kernel<false><<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
-  fast_verify_kernel<<<(ns + 3) / 4, 128, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
+  fast_verify_kernel<<<ns, kVThreads, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
   fast_orphan_fix_kernel<<<32, 256, 0, ctx->stream>>>(p);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[5], ctx->stream));

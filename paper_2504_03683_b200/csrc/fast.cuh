@@ -816,72 +816,85 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
   r_epilogue(gpr, RL, K);
 }
 
-// per stream: verify the range chain, record bases, compose_kernel's per-range state
-__global__ void __launch_bounds__(128) fast_verify_kernel(Params p, unsigned long long* stream_nrec) {
-  const uint32_t lane = lane_id();
-  const uint32_t s = blockIdx.x * (blockDim.x / kWarp) + (threadIdx.x >> 5);
-  if (s >= p.n_streams) return;
+// per stream (one CTA): verify the range chain, record bases, compose_kernel's per-range state.
+// Thread t owns a contiguous block of the stream's ranges: a local pass composes the block
+// (exit carry, last timestamp, record count and what the block needs from its predecessor), a
+// CTA scan hands every block its incoming carry, a second pass writes the per-range outputs.
+constexpr int kVThreads = 128;
+
+__global__ void __launch_bounds__(kVThreads) fast_verify_kernel(Params p, unsigned long long* stream_nrec) {
+  __shared__ unsigned long long sx[kVThreads], st_[kVThreads], sb[kVThreads];
+  __shared__ uint32_t sflags[kVThreads];
+  const uint32_t s = blockIdx.x, t = threadIdx.x;
   const uint32_t r0 = p.stream_range0[s];
   const uint32_t r1 = (s + 1 < p.n_streams) ? p.stream_range0[s + 1] : p.n_ranges;
   const uint64_t size = p.stream_size[s];
-  uint64_t c_exit = 16, c_base = 0, c_last = 0;
-  bool c_has = false, bad = false;
-  for (uint32_t rb = r0; rb < r1; rb += kWarp) {
-    const uint32_t r = rb + lane;
-    const bool valid = r < r1;
-    RangeState st;
-    if (valid) st = p.rstate[r];
-    else { st.entry = kNone; st.exit = kNone; st.n = 0; st.np = 0; st.ne = 0; st.first_ts = st.last_ts = 0; st.pool_off = 0; }
-    const uint64_t t1 = valid ? min(16 + (uint64_t)(r - r0 + 1) * p.range_bytes, size) : 0;
-    const bool hasE = valid && st.entry != kNone;
-    // exit carried into each lane: nearest lower lane with an entry, else the carry
-    int src = hasE ? (int)lane : -1;
-    int pre = __shfl_up_sync(0xffffffffu, src, 1);
-    if (lane == 0) pre = -1;
-    for (int dd = 1; dd < 32; dd <<= 1) { const int v = __shfl_up_sync(0xffffffffu, pre, dd); if ((int)lane >= dd) pre = max(pre, v); }
-    const uint64_t px = __shfl_sync(0xffffffffu, st.exit, pre < 0 ? 0 : pre);
-    const uint64_t prev_exit = pre >= 0 ? px : c_exit;
-    const bool chain_ok = !valid || (hasE ? st.entry == prev_exit : prev_exit >= t1);
-    bool ok = true;
-    // timestamps keep rising across ranges (pipeline.py:98)
-    int srcn = (valid && st.n) ? (int)lane : -1;
-    int pn = __shfl_up_sync(0xffffffffu, srcn, 1);
-    if (lane == 0) pn = -1;
-    for (int dd = 1; dd < 32; dd <<= 1) { const int v = __shfl_up_sync(0xffffffffu, pn, dd); if ((int)lane >= dd) pn = max(pn, v); }
-    const uint64_t pl = __shfl_sync(0xffffffffu, st.last_ts, pn < 0 ? 0 : pn);
-    const uint64_t prev_last = pn >= 0 ? pl : c_last;
-    const bool has_prev = pn >= 0 || c_has;
-    if (valid && st.n && has_prev && st.first_ts < prev_last) ok = false;
-    if (!chain_ok) atomicOr(p.anom, 8u);
-    // record bases
-    const uint64_t n = valid ? st.n : 0;
-    uint64_t incl = n;
-    for (int dd = 1; dd < 32; dd <<= 1) { const uint64_t v = __shfl_up_sync(0xffffffffu, incl, dd); if ((int)lane >= dd) incl += v; }
-    const uint64_t base = c_base + incl - n;
-    if (valid) {
-      p.range_base[r] = base;
-      SegState ss;
-      ss.status = (p.epoch << 2) | TS_DONE;
-      ss.pool_n_pending = st.np;
-      ss.pool_off = st.pool_off;
-      ss.pool_n_resid = st.ne;
-      ss.pad = 0;
-      p.state[r] = ss;
-      if (st.pool_off + st.np + st.ne <= p.pool_cap)
-        for (uint32_t i = 0; i < st.np; i++) p.pool[st.pool_off + i].seq += base;
+  const uint32_t nr = r1 - r0, per = (nr + kVThreads - 1) / kVThreads;
+  const uint32_t a = min(r0 + t * per, r1), b = min(a + per, r1);
+  bool chain_ok = true, order_ok = true;
+  bool hx = false, ht = false, need_e = false, need_t = false;
+  uint64_t lx = 0, lt = 0, sum = 0, first_e = 0, first_t = 0, lead_t1 = 0;
+  for (uint32_t r = a; r < b; r++) {
+    const RangeState st = p.rstate[r];
+    const uint64_t t1 = min(16 + (uint64_t)(r - r0 + 1) * p.range_bytes, size);
+    if (st.entry != kNone) {  // starts where the previous range ended
+      if (!hx) { need_e = true; first_e = st.entry; }
+      else if (st.entry != lx) chain_ok = false;
+      hx = true;
+      lx = st.exit;
+    } else {                  // no plausible header: a record of an earlier range spans it
+      if (!hx) lead_t1 = max(lead_t1, t1);
+      else if (lx < t1) chain_ok = false;
     }
-    bad |= !ok;
-    c_base += __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t me = __ballot_sync(0xffffffffu, hasE);
-    if (me) c_exit = __shfl_sync(0xffffffffu, st.exit, 31 - __clz(me));
-    const uint32_t mn = __ballot_sync(0xffffffffu, valid && st.n);
-    if (mn) { c_last = __shfl_sync(0xffffffffu, st.last_ts, 31 - __clz(mn)); c_has = true; }
+    if (st.n) {               // timestamps keep rising across ranges (pipeline.py:98)
+      if (!ht) { need_t = true; first_t = st.first_ts; }
+      else if (st.first_ts < lt) order_ok = false;
+      ht = true;
+      lt = st.last_ts;
+    }
+    sum += st.n;
   }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.anom, 16u);
-  if (lane == 0) {
-    stream_nrec[s] = c_base;
-    if (c_base) atomicAdd(&p.stats[ST_EVENTS], (unsigned long long)c_base);
-    if (c_has) atomicMax(p.last_ts, (unsigned long long)c_last);
+  sx[t] = lx; st_[t] = lt; sb[t] = sum;
+  sflags[t] = (hx ? 1u : 0u) | (ht ? 2u : 0u);
+  __syncthreads();
+  if (t == 0) {  // exclusive scan of the block carries (the exit before range 0 is the header end, 16)
+    unsigned long long cx = 16, ct = 0, cb = 0;
+    bool cht = false;
+    for (uint32_t i = 0; i < kVThreads; i++) {
+      const unsigned long long x = sx[i], ts = st_[i], n = sb[i];
+      const uint32_t f = sflags[i];
+      sx[i] = cx; st_[i] = ct; sb[i] = cb;
+      sflags[i] = (f & 3u) | (cht ? 4u : 0u);
+      if (f & 1u) cx = x;
+      if (f & 2u) { ct = ts; cht = true; }
+      cb += n;
+    }
+    stream_nrec[s] = cb;
+    if (cb) atomicAdd(&p.stats[ST_EVENTS], cb);
+    if (cht) atomicMax(p.last_ts, ct);  // IntervalStats.events_in, the global last ts (pipeline.py:152)
+  }
+  __syncthreads();
+  const uint64_t in_x = sx[t], in_t = st_[t];
+  const bool in_ht = (sflags[t] & 4u) != 0;
+  if (need_e && first_e != in_x) chain_ok = false;
+  if (lead_t1 > in_x) chain_ok = false;
+  if (need_t && in_ht && first_t < in_t) order_ok = false;
+  if (!chain_ok) atomicOr(p.anom, 8u);
+  if (!order_ok) atomicOr(p.anom, 16u);
+  uint64_t base = sb[t];
+  for (uint32_t r = a; r < b; r++) {
+    const RangeState st = p.rstate[r];
+    p.range_base[r] = base;
+    SegState ss;
+    ss.status = (p.epoch << 2) | TS_DONE;
+    ss.pool_n_pending = st.np;
+    ss.pool_off = st.pool_off;
+    ss.pool_n_resid = st.ne;
+    ss.pad = 0;
+    p.state[r] = ss;
+    if (st.pool_off + st.np + st.ne <= p.pool_cap)
+      for (uint32_t i = 0; i < st.np; i++) p.pool[st.pool_off + i].seq += base;
+    base += st.n;
   }
 }
 

@@ -491,7 +491,10 @@ __device__ __forceinline__ bool g_name_equal(const NameDict& d, uint32_t row, co
 // device-name dictionary lookup/insert (same layout, hash and probing as name_lookup)
 __device__ __noinline__ uint32_t g_name_lookup(const NameDict& d, const uint8_t* g, uint64_t o, uint32_t n, uint64_t h) {
   for (uint64_t slot = h & d.mask, probes = 0; probes <= d.mask; slot = (slot + 1) & d.mask, probes++) {
-    const unsigned long long k = atomicCAS(&d.keys[slot], 0ull, (unsigned long long)h);
+    // a plain read first: names already in the dictionary cost no atomic (hot names are shared by
+    // every SM, so an atomicCAS per lookup would serialise on a few L2 lines)
+    unsigned long long k = *(volatile unsigned long long*)&d.keys[slot];
+    if (k == 0ull) k = atomicCAS(&d.keys[slot], 0ull, (unsigned long long)h);
     if (k == 0ull) {
       const uint32_t row = atomicAdd(d.n_rows, 1u);
       const unsigned long long off = atomicAdd(d.arena_used, (unsigned long long)((n + 3u) & ~3u));
