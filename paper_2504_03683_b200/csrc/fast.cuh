@@ -33,7 +33,7 @@ constexpr uint32_t kRChunk = 32;                    // bytes per ring slot (one 
 constexpr uint32_t kRSlots = 8;                     // slots per lane
 constexpr uint32_t kRRing = kRChunk * kRSlots;      // 256-byte ring
 constexpr uint32_t kRWordMask = kRRing / 4 - 1;
-constexpr uint32_t kRMirror = 32;                   // slot 0's first bytes again after the ring
+constexpr uint32_t kRMirror = 0;                    // (no mirror: header words are read with wrapped indices)
 constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: header + first field need no wrap
 constexpr uint32_t kRInline = 128;                  // records up to this long are decoded from the ring
 constexpr int kRLag = 2;                            // iterations before a fill group is waited for
@@ -670,6 +670,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       for (uint32_t k = 0; k < kRChunk; k += 16) r_cp16p(dst + k, src + k, pw);
       #pragma unroll
       for (uint32_t k = 0; k < kRMirror; k += 16) r_cp16p(ring_s + kRRing + k, src + k, pm);
+      (void)pm;
     }
     R.ci += want ? 1u : 0u;
     R.recent = (R.recent << 1) | (want ? 1u : 0u);
@@ -680,9 +681,11 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const uint32_t cr = R.ci - __popc(R.recent & kPend);
     const bool ready = act && min((R.o + 15u) / kRChunk, R.clast) < cr;
     const uint32_t pos = R.o & (kRRing - 1);
-    const uint32_t* w = ring + (pos >> 2);  // header and first field: no wrap (mirror)
+    const uint32_t wb0 = pos >> 2;
     const uint32_t sh = (pos & 3u) << 3;
-    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4], w5 = w[5], w6 = w[6];
+    const uint32_t w0 = ring[wb0], w1 = ring[(wb0 + 1) & kRWordMask], w2 = ring[(wb0 + 2) & kRWordMask],
+                   w3 = ring[(wb0 + 3) & kRWordMask], w4 = ring[(wb0 + 4) & kRWordMask],
+                   w5 = ring[(wb0 + 5) & kRWordMask], w6 = ring[(wb0 + 6) & kRWordMask];
     const uint32_t sid = __funnelshift_r(w0, w1, sh);
     const uint64_t ts = ((uint64_t)__funnelshift_r(w2, w3, sh) << 32) | __funnelshift_r(w1, w2, sh);
     const uint32_t plen = __funnelshift_r(w3, w4, sh);
