@@ -804,8 +804,14 @@ static int build_layout(hg_ctx* ctx) {
   };
   uint64_t R = ctx->range_opt ? ctx->range_opt : std::max<uint64_t>(1024, (payload + lanes - 1) / lanes);
   R = (R + 15) & ~15ull;
-  if (!ctx->range_opt)
-    while (count(R) > lanes && R < max_pay) R = ((R + R / 16) + 15) & ~15ull;
+  if (!ctx->range_opt && count(R) > lanes) {  // smallest R (16-byte steps) with at most one range per lane
+    uint64_t lo = R / 16, hi = std::max<uint64_t>(R / 16, (max_pay + 15) / 16);
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if (count(mid * 16) <= lanes) hi = mid; else lo = mid + 1;
+    }
+    R = lo * 16;
+  }
   R = std::min<uint64_t>(R, 1ull << 28);
   ctx->range_bytes = (uint32_t)R;
   ctx->range_stream.clear();
