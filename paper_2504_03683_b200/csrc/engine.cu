@@ -312,8 +312,8 @@ struct hg_ctx {
   DBuf<unsigned long long> d_range_base;
   std::vector<uint32_t> vplan;
   DBuf<uint32_t> d_vplan;
-  std::vector<uint4> fdesc;
-  DBuf<uint4> d_fdesc;
+  std::vector<uint4> fdesc, dplan;
+  DBuf<uint4> d_fdesc, d_dplan;
   int last_path = 0;                // 1 = the last run's phase 1 was the single pass
   uint64_t fallbacks = 0;
   uint32_t last_anom = 0;
@@ -592,7 +592,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_segw.release(); ctx->d_seginfo.release(); ctx->d_stream_nrec.release(); ctx->d_tl_rec_off.release();
   ctx->d_deep.release(); ctx->d_params.release();
   ctx->d_range_stream.release(); ctx->d_stream_range0.release(); ctx->d_rstate.release(); ctx->d_rseg.release();
-  ctx->d_range_base.release(); ctx->d_vplan.release(); ctx->d_fdesc.release();
+  ctx->d_range_base.release(); ctx->d_vplan.release(); ctx->d_fdesc.release(); ctx->d_dplan.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -700,6 +700,7 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
   }
   // inline-record descriptors of the range kernel (fast.cuh fdesc), one per id plus a sentinel
   ctx->fdesc.assign(ctx->sid_map.size() + 1, make_uint4(M_FN | (FK_NEVER << 20), 1u, 0u, 0u));
+  ctx->dplan.assign(ctx->sid_map.size() + 1, make_uint4(0u, 0u, 0u, 0u));
   for (uint32_t i = 0; i < n_schemas; i++) {
     const uint32_t id = schemas[i].id;
     const DSchema& d = ctx->schemas[ctx->sid_map[id]];
@@ -717,6 +718,7 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
     const uint32_t kind = d.cls == HG_CLASS_ENTRY ? FK_ENTRY : d.cls == HG_CLASS_EXIT ? FK_EXIT : dt ? FK_DEFER : FK_PASS;
     uint32_t x = (dd.x & M_FN) | (kind << 20) | (result_kind(d.flags) << 26);
     if (d.cls == HG_CLASS_EXIT && (d.flags & SF_RESULT)) x |= FD_RES;
+    if (d.cls == HG_CLASS_DEVICE) x |= FD_ISDEV;
     uint32_t z = 0;
     if (var && !dt) {
       x |= FD_VAR;
@@ -724,6 +726,19 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
       z = (vp & 0x3FFFu) | (((vp >> 14) & 0x3FFFu) << 16);
     }
     ctx->fdesc[id] = make_uint4(x, lo | (hi << 16), z, 0u);
+    // device-profiling records: two variable fields, start/end in the fixed prefix (fast.cuh dplan)
+    if (d.cls == HG_CLASS_DEVICE && d.nvar == 2 && d.role[HG_ROLE_START] >= 0 && d.role[HG_ROLE_END] >= 0 &&
+        d.role[HG_ROLE_NAME] >= 0 && d.role_seg[HG_ROLE_START] == 0 && d.role_seg[HG_ROLE_END] == 0 &&
+        d.role_seg[HG_ROLE_NAME] < 2 && d.role_kind[HG_ROLE_NAME] >= HG_KIND_STRING &&
+        d.role_delta[HG_ROLE_NAME] == d.lead[d.role_seg[HG_ROLE_NAME]] &&
+        d.role_kind[HG_ROLE_START] != HG_KIND_F64 && d.role_kind[HG_ROLE_END] != HG_KIND_F64 &&
+        d.role_kind[HG_ROLE_START] < HG_KIND_STRING && d.role_kind[HG_ROLE_END] < HG_KIND_STRING)
+      ctx->dplan[id] = make_uint4(
+          (uint32_t)d.lead[0] | ((uint32_t)d.lead[1] << 16),
+          (uint32_t)d.lead[2] | ((uint32_t)d.role_seg[HG_ROLE_NAME] << 16) | ((uint32_t)d.vkind[0] << 17) |
+              ((uint32_t)d.vkind[1] << 18) | ((d.role_kind[HG_ROLE_START] == HG_KIND_I64 ? 1u : 0u) << 19) |
+              ((d.role_kind[HG_ROLE_END] == HG_KIND_I64 ? 1u : 0u) << 20) | (1u << 31),
+          (uint32_t)d.role_delta[HG_ROLE_START] | ((uint32_t)d.role_delta[HG_ROLE_END] << 16), 0u);
   }
   ctx->fast_warps = 0;
   ctx->staged = false;
@@ -741,6 +756,8 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
   CK(cudaMemcpy(ctx->d_vplan.ptr, ctx->vplan.data(), ctx->vplan.size() * 4, cudaMemcpyHostToDevice));
   CK(ctx->d_fdesc.ensure(ctx->fdesc.size()));
   CK(cudaMemcpy(ctx->d_fdesc.ptr, ctx->fdesc.data(), ctx->fdesc.size() * sizeof(uint4), cudaMemcpyHostToDevice));
+  CK(ctx->d_dplan.ensure(ctx->dplan.size()));
+  CK(cudaMemcpy(ctx->d_dplan.ptr, ctx->dplan.data(), ctx->dplan.size() * sizeof(uint4), cudaMemcpyHostToDevice));
   if (n_kinds) {
     CK(cudaMemcpy(ctx->d_kinds.ptr, kinds, n_kinds, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_field_role.ptr, ctx->field_role.data(), n_kinds, cudaMemcpyHostToDevice));
@@ -983,6 +1000,7 @@ static Params make_params(hg_ctx* ctx) {
   p.anom = reinterpret_cast<uint32_t*>(C + C_ANOM);
   p.vplan = ctx->d_vplan.ptr;
   p.fdesc = ctx->d_fdesc.ptr;
+  p.dplan = ctx->d_dplan.ptr;
   return p;
 }
 

@@ -297,7 +297,10 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
   if (!k) R.first_ts = h.ts;
   R.prev_ts = h.ts;
   R.o = (uint32_t)(a + L);
-  if (dt) return true;
+  if (dt) {
+    if (cls == HG_CLASS_DEVICE) R.spans++;  // a device span's identity (sinks.py:240-242)
+    return true;
+  }
   const uint32_t fnm = d.x & M_FN;
   if (cls == HG_CLASS_ENTRY) {
     const uint32_t i = R.ne;
@@ -433,7 +436,27 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
     uint32_t rl[HG_NUM_ROLES];
     uint64_t aux = 0;
     uint32_t err = 0;
-    if (roles) {
+    const uint4 dp = cls == HG_CLASS_DEVICE ? __ldg(&p.dplan[h.sid]) : make_uint4(0, 0, 0, 0);
+    if (dp.y >> 31) {  // usual device layout (dplan): three dependent HBM round trips instead of a field walk
+      const uint32_t lead0 = dp.x & 0xFFFFu, lead1 = dp.x >> 16, lead2 = dp.y & 0xFFFFu;
+      const uint64_t body = a + 16;
+      const uint32_t l0 = g32(gb, body + lead0);
+      rp[HG_ROLE_START] = body + (dp.z & 0xFFFFu);
+      rp[HG_ROLE_END] = body + (dp.z >> 16);
+      if ((uint64_t)lead0 + 4u + l0 + lead1 + 4u > h.plen) {
+        err = HG_ERR_TRUNC_VAR;
+      } else {
+        const uint64_t b1 = body + lead0 + 4u + l0 + lead1;
+        const uint32_t l1 = g32(gb, b1);
+        if ((uint64_t)lead0 + 4u + l0 + lead1 + 4u + l1 + lead2 != h.plen) err = HG_ERR_TRAILING;
+        else if ((((dp.y >> 17) & 1u) && !g_utf8(gb, body + lead0 + 4u, l0)) ||
+                 (((dp.y >> 18) & 1u) && !g_utf8(gb, b1 + 4u, l1)))
+          err = HG_ERR_UTF8;
+        const bool second = (dp.y >> 16) & 1u;
+        rp[HG_ROLE_NAME] = second ? b1 + 4u : body + lead0 + 4u;
+        rl[HG_ROLE_NAME] = second ? l1 : l0;
+      }
+    } else if (roles) {
       err = seg_fields(p, gb, size, a, h.sid, h.plen, rp, rl, aux, roles);
     } else {  // the inline record's one string field (length already checked): strict UTF-8
       const uint32_t vp = __ldg(&p.vplan[h.sid]);
@@ -446,8 +469,10 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
       } else {
         const DSchema* sc = schema_of(p, h.sid);
         const uint64_t ua = g64(gb, rp[HG_ROLE_START]), ub = g64(gb, rp[HG_ROLE_END]);
-        const int64_t ah = (sc->role_kind[HG_ROLE_START] == HG_KIND_I64 && (int64_t)ua < 0) ? -1 : 0;
-        const int64_t bh = (sc->role_kind[HG_ROLE_END] == HG_KIND_I64 && (int64_t)ub < 0) ? -1 : 0;
+        const bool si = (dp.y >> 31) ? ((dp.y >> 19) & 1u) != 0 : sc->role_kind[HG_ROLE_START] == HG_KIND_I64;
+        const bool ei = (dp.y >> 31) ? ((dp.y >> 20) & 1u) != 0 : sc->role_kind[HG_ROLE_END] == HG_KIND_I64;
+        const int64_t ah = (si && (int64_t)ua < 0) ? -1 : 0;
+        const int64_t bh = (ei && (int64_t)ub < 0) ? -1 : 0;
         const uint64_t no = rp[HG_ROLE_NAME];
         const uint32_t nl = rl[HG_ROLE_NAME];
         const uint64_t hh = g_hash(gb, no, nl);
@@ -466,8 +491,7 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
     if (err) {
       atomicOr(p.anom, 2u);
     } else if (cls == HG_CLASS_DEVICE) {
-      K.x++;
-      atomicAdd(&p.stream_spans[s], 1ull);
+      K.x++;  // its span identity was counted by the record's lane (RLane::spans)
     } else if (cls == HG_CLASS_TELEMETRY) {
       K.y++;
     }
@@ -496,6 +520,7 @@ __device__ __noinline__ void r_drain_str(const Params& p, const uint64_t* q_off,
 // z = fixed bytes before | after the one variable field (blob / string)
 enum : uint32_t { FK_ENTRY = 0, FK_EXIT = 1, FK_PASS = 2, FK_DEFER = 3, FK_NEVER = 7 };
 constexpr uint32_t FD_STR = 1u << 23, FD_VAR = 1u << 24, FD_RES = 1u << 25;  // result kind at bits 26-27
+constexpr uint32_t FD_ISDEV = 1u << 28;  // device-profiling class
 
 __device__ __forceinline__ void r_cp16p(uint32_t dst, const void* src, uint32_t pred) {
   asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.cg.shared.global [%0], [%1], 16; }"
@@ -714,6 +739,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     if (lenbad) R.bad = true;  // CorruptRecordError: the exact path names it
     const bool fast = (fE || fXp || fXq || fO) && !lenbad;
     bool qflag = fast && kind == FK_DEFER;
+    R.spans += (qflag && (D.x & FD_ISDEV)) ? 1u : 0u;  // a device span's identity (sinks.py:240-242)
     bool sflag = fast && (D.x & FD_STR) && ln;
     if (sflag && ln <= 16u) {  // short strings (kernel names): all-ASCII from the ring, else the drain decides
       const uint32_t sp = pos + 20u + lead0, sw = sp >> 2, s0 = (sp & 3u) << 3;

@@ -108,6 +108,7 @@ struct Params {
   uint32_t* anom;                  // nonzero: the single-pass result is void, run the exact path
   const uint32_t* vplan;           // per schema id: single-var-field payload plan (fast.cuh)
   const uint4* fdesc;              // per schema id (+ one sentinel): inline-record descriptor (fast.cuh)
+  const uint4* dplan;              // per schema id: device-record layout for the drain (fast.cuh)
 };
 
 // compact descriptor: x = fn(20) | cls(3)<<20 | flags(8)<<23 ; y = fixed_len(16) | result field index(8)<<16 | counter(8)<<24
