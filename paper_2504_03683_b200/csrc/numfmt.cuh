@@ -25,11 +25,28 @@
 
 namespace nf {
 
+// decimal digits of v (1 for 0)
+NF_HD inline int dec_digits(uint64_t v) {
+  int n = 1;
+  if (v >= 10000000000000000ull) { n += 16; v /= 10000000000000000ull; }
+  if (v >= 100000000ull) { n += 8; v /= 100000000ull; }
+  if (v >= 10000ull) { n += 4; v /= 10000ull; }
+  if (v >= 100ull) { n += 2; v /= 100ull; }
+  if (v >= 10ull) n += 1;
+  return n;
+}
+
+// digits written backwards from out + n: 64-bit work only per 8-digit chunk
 NF_HD inline int fmt_u64(uint64_t v, char* out) {
-  char tmp[24];
-  int n = 0;
-  do { tmp[n++] = (char)('0' + v % 10); v /= 10; } while (v);
-  for (int i = 0; i < n; i++) out[i] = tmp[n - 1 - i];
+  const int n = dec_digits(v);
+  int k = n;
+  while (v >= 100000000ull) {
+    uint32_t c = (uint32_t)(v % 100000000ull);
+    v /= 100000000ull;
+    for (int j = 0; j < 8; j++) { out[--k] = (char)('0' + c % 10u); c /= 10u; }
+  }
+  uint32_t c = (uint32_t)v;
+  do { out[--k] = (char)('0' + c % 10u); c /= 10u; } while (c);
   return n;
 }
 

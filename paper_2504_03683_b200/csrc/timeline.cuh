@@ -55,39 +55,64 @@ struct TlTables {
 // ---------------------------------------------------------------------------
 // byte writer (p == nullptr: count only)
 
-struct TW {
+struct TW {        // writes the bytes
+  static constexpr bool kWrite = true;
   char* p;
   uint64_t n;
-  __device__ __forceinline__ void c(char ch) {
-    if (p) p[n] = ch;
-    n++;
-  }
+  __device__ __forceinline__ void c(char ch) { p[n++] = ch; }
   __device__ __forceinline__ void s(const char* q, uint32_t l) {
-    if (p)
-      for (uint32_t i = 0; i < l; i++) p[n + i] = q[i];
+    for (uint32_t i = 0; i < l; i++) p[n + i] = q[i];
     n += l;
   }
   template <int N>
   __device__ __forceinline__ void lit(const char (&q)[N]) { s(q, N - 1); }
 };
+struct TC {        // counts them (tl_len_kernel)
+  static constexpr bool kWrite = false;
+  uint64_t n;
+  __device__ __forceinline__ void c(char) { n++; }
+  __device__ __forceinline__ void s(const char*, uint32_t l) { n += l; }
+  template <int N>
+  __device__ __forceinline__ void lit(const char (&)[N]) { n += N - 1; }
+};
 
-__device__ __forceinline__ uint64_t ldu64(const uint8_t* q) {
-  uint64_t v = 0;
-  for (int i = 7; i >= 0; i--) v = (v << 8) | q[i];
-  return v;
-}
+// unaligned little-endian loads from the stream bytes in HBM (aligned words + funnel shifts;
+// the data array is zero-padded, so the word after the last byte is readable)
 __device__ __forceinline__ uint32_t ldu32(const uint8_t* q) {
-  return (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(q) & ~(uintptr_t)3);
+  return __funnelshift_r(w[0], w[1], (uint32_t)(reinterpret_cast<uintptr_t>(q) & 3) * 8);
+}
+__device__ __forceinline__ uint64_t ldu64(const uint8_t* q) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(q) & ~(uintptr_t)3);
+  const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(q) & 3) * 8;
+  const uint32_t a = w[0], b = w[1], c = w[2];
+  return ((uint64_t)__funnelshift_r(b, c, sh) << 32) | __funnelshift_r(a, b, sh);
 }
 
-__device__ __forceinline__ void hex4(TW& w, uint32_t v) {
+template <class W>
+__device__ __forceinline__ void hex4(W& w, uint32_t v) {
   const char* hx = "0123456789abcdef";
   w.c('\\'); w.c('u');
   w.c(hx[(v >> 12) & 15]); w.c(hx[(v >> 8) & 15]); w.c(hx[(v >> 4) & 15]); w.c(hx[v & 15]);
 }
 
 // json.dumps(str) with ensure_ascii of validated UTF-8 bytes (json/encoder.py ESCAPE_ASCII)
-__device__ __noinline__ void json_str(TW& w, const uint8_t* s, uint32_t len) {
+template <class W>
+__device__ __noinline__ void json_str(W& w, const uint8_t* s, uint32_t len) {
+  {  // plain printable ASCII without quote or backslash (kernel names): the bytes themselves
+    bool plain = true;
+    for (uint32_t i = 0; i < len && plain; i++) {
+      const uint32_t c = s[i];
+      plain = c >= 0x20 && c < 0x7F && c != '"' && c != '\\';
+    }
+    if (plain) {
+      w.c('"');
+      if (W::kWrite) w.s(reinterpret_cast<const char*>(s), len);
+      else w.s(nullptr, len);
+      w.c('"');
+      return;
+    }
+  }
   w.c('"');
   for (uint32_t i = 0; i < len;) {
     uint32_t c = s[i], cp;
@@ -119,6 +144,23 @@ struct TlFields {
 
 __device__ __noinline__ void tl_locate(const TlTables& T, const DSchema* sc, const uint8_t* pay, TlFields& F) {
   for (int r = 0; r < HG_NUM_ROLES; r++) { F.at[r] = nullptr; F.len[r] = 0; }
+  if (sc->nvar != kNoPlan) {  // payload plan: variable-field starts, then every role at its segment + delta
+    uint32_t seg[5];
+    uint32_t q = 0;
+    seg[0] = 0;
+    for (uint32_t i = 0; i < sc->nvar; i++) {
+      q += sc->lead[i];
+      q += 4 + ldu32(pay + q);
+      seg[i + 1] = q;
+    }
+    for (int r = 0; r < HG_NUM_ROLES; r++) {
+      if (sc->role[r] < 0) continue;
+      const uint32_t at = seg_sel(seg, sc->role_seg[r]) + sc->role_delta[r];
+      if (sc->role_kind[r] >= HG_KIND_STRING) { F.len[r] = ldu32(pay + at); F.at[r] = pay + at + 4; }
+      else F.at[r] = pay + at;
+    }
+    return;
+  }
   uint32_t off = 0;
   for (uint32_t f = 0; f < sc->nfields; f++) {
     const uint8_t k = T.kinds[sc->kinds_off + f];
@@ -160,11 +202,13 @@ __device__ __forceinline__ I128 sub128(I128 a, I128 b) {
 }
 __device__ __forceinline__ bool eq128(I128 a, I128 b) { return a.hi == b.hi && a.lo == b.lo; }
 
-__device__ __forceinline__ void w_i128(TW& w, I128 v) {
+template <class W>
+__device__ __forceinline__ void w_i128(W& w, I128 v) {
   char b[48];
   w.s(b, (uint32_t)nf::fmt_i128(v.hi, v.lo, b));
 }
-__device__ __forceinline__ void w_us(TW& w, I128 ns) {  // ns / 1000.0
+template <class W>
+__device__ __forceinline__ void w_us(W& w, I128 ns) {  // ns / 1000.0
   char b[40];
   w.s(b, (uint32_t)nf::fmt_ns_div1000(ns.hi, ns.lo, b));
 }
@@ -334,12 +378,14 @@ __global__ void tl_meta_kernel(TlTables T) {
 // ---------------------------------------------------------------------------
 // one item's JSON text: [metas] + object, each element prefixed by ",\n " ("\n " first)
 
-__device__ __forceinline__ void elem_open(TW& w, bool first) {
+template <class W>
+__device__ __forceinline__ void elem_open(W& w, bool first) {
   if (!first) w.c(',');
   w.lit("\n {\n  \"name\": ");
 }
 
-__device__ __noinline__ void meta_obj(TW& w, bool first, bool thread, const char* pid, uint32_t pid_len, I128 tid,
+template <class W>
+__device__ __noinline__ void meta_obj(W& w, bool first, bool thread, const char* pid, uint32_t pid_len, I128 tid,
                                       const char* nameq, uint32_t name_len, const uint8_t* raw_name, uint32_t raw_len) {
   elem_open(w, first);
   if (thread) w.lit("\"thread_name\""); else w.lit("\"process_name\"");
@@ -353,7 +399,8 @@ __device__ __noinline__ void meta_obj(TW& w, bool first, bool thread, const char
   w.lit("\n  }\n }");
 }
 
-__device__ __noinline__ void tl_format(const TlTables& T, uint32_t i, TW& w) {
+template <class W>
+__device__ __noinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   const TlItem it = T.items[T.order[i]];
   const uint32_t kind = it.kind & 3u;
   bool first = i == 0;
@@ -466,7 +513,7 @@ __device__ __noinline__ void tl_format(const TlTables& T, uint32_t i, TW& w) {
 
 __global__ void tl_len_kernel(TlTables T) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
-    TW w{nullptr, 0};
+    TC w{0};
     tl_format(T, (uint32_t)i, w);
     T.lens[i] = (uint32_t)w.n;
   }
