@@ -98,7 +98,7 @@ __device__ __forceinline__ void hex4(W& w, uint32_t v) {
 
 // json.dumps(str) with ensure_ascii of validated UTF-8 bytes (json/encoder.py ESCAPE_ASCII)
 template <class W>
-__device__ __noinline__ void json_str(W& w, const uint8_t* s, uint32_t len) {
+__device__ __forceinline__ void json_str(W& w, const uint8_t* s, uint32_t len) {
   {  // plain printable ASCII without quote or backslash (kernel names): the bytes themselves
     bool plain = true;
     for (uint32_t i = 0; i < len && plain; i++) {
@@ -385,7 +385,7 @@ __device__ __forceinline__ void elem_open(W& w, bool first) {
 }
 
 template <class W>
-__device__ __noinline__ void meta_obj(W& w, bool first, bool thread, const char* pid, uint32_t pid_len, I128 tid,
+__device__ __forceinline__ void meta_obj(W& w, bool first, bool thread, const char* pid, uint32_t pid_len, I128 tid,
                                       const char* nameq, uint32_t name_len, const uint8_t* raw_name, uint32_t raw_len) {
   elem_open(w, first);
   if (thread) w.lit("\"thread_name\""); else w.lit("\"process_name\"");
@@ -400,7 +400,7 @@ __device__ __noinline__ void meta_obj(W& w, bool first, bool thread, const char*
 }
 
 template <class W>
-__device__ __noinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
+__device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   const TlItem it = T.items[T.order[i]];
   const uint32_t kind = it.kind & 3u;
   bool first = i == 0;
