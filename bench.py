@@ -312,6 +312,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
+    if not args.no_timeline:
+        line["timeline"] = timeline_side(eng)
     traffic = REPO / "profiles" / ("fast_kernel_traffic.json" if single else "seg_decode_traffic.json")
     if traffic.exists():
         tr = json.loads(traffic.read_text())
@@ -320,6 +322,33 @@ def run_ours(args):
     print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def timeline_side(eng, config="c5", scale=0.1):
+    """Row a8 (TimelineSink): tally + timeline on the device-heavy config, device time of the ordering and
+    JSON formatting, with size-independent checks (object count = interval messages + metadata objects,
+    json.dump framing, tally equal to the tally-only run)."""
+    from paper_2504_03683_b200 import synth
+
+    wl = synth.config(config, scale)
+    raws = synth.generate(wl)
+    infos = [r.info for r in raws]
+    r0 = eng.run(raws, wl.registry, infos)
+    r1 = None
+    for _ in range(2):
+        r1 = eng.run(raws, wl.registry, infos, want_timeline=True)
+    ms = eng.timeline_ms()
+    tl, st = r1.timeline, r1.stats
+    msgs = st["host_spans"] + st["truncated_spans"] + st["device_spans"] + st["samples"]
+    n_obj = tl.count(b"\n {\n  \"name\": ")
+    n_meta = tl.count(b"\"ph\": \"M\"")
+    assert tl[:3] == b"[\n " and tl[-2:] == b"\n]" and n_obj - n_meta == msgs and r1.report == r0.report
+    return {"workload": f"{config} x{scale}: SURVEY.md §8(d) C5 (device-profiling heavy) + full timeline export",
+            "events": st["events_in"], "messages": msgs, "json_bytes": len(tl),
+            "phase1_ms": r1.kernel_ms, "timeline_ms": ms, "json_gb_per_s": len(tl) / ms / 1e6,
+            "events_per_s": st["events_in"] / ((r1.kernel_ms + ms) / 1e3),
+            "path": "exact three-kernel phase 1 (record-indexed messages) + mux-key merge sort + JSON formatting",
+            "checks": "object count = messages + metadata, json.dump framing, tally == tally-only run"}
 
 
 def main():
@@ -331,6 +360,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--no-timeline", action="store_true", help="skip the row-a8 timeline side measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
