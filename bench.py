@@ -314,6 +314,8 @@ def run_ours(args):
     }
     if not args.no_timeline:
         line["timeline"] = timeline_side(eng)
+    if not args.no_configs:
+        line["other_configs"] = configs_side(eng)
     traffic = REPO / "profiles" / ("fast_kernel_traffic.json" if single else "seg_decode_traffic.json")
     if traffic.exists():
         tr = json.loads(traffic.read_text())
@@ -351,6 +353,34 @@ def timeline_side(eng, config="c5", scale=0.1):
             "checks": "object count = messages + metadata, json.dump framing, tally == tally-only run"}
 
 
+def configs_side(eng, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 0.25), ("c5", 0.25))):
+    """The other SURVEY.md §8(d) shapes (tally, device-resident, single pass unless it falls back):
+    phase-1 device time and events/s at a bounded scale each (parity for them is in tests/)."""
+    from paper_2504_03683_b200 import synth
+    from paper_2504_03683_b200.abi import HG_WANT_TALLY
+
+    out = []
+    for name, scale in plan:
+        wl = synth.config(name, scale)
+        raws = synth.generate(wl)
+        eng.set_registry(wl.registry)
+        eng.set_streams(raws)
+        eng.stage()
+        ms = []
+        for i in range(4):
+            eng.run_raw(HG_WANT_TALLY)
+            k, t, *_ = eng.timing()
+            if i:
+                ms.append(t)
+        ev = eng.stats()["events_in"]
+        path, fallbacks, rb = eng.last_path()
+        d = statistics.mean(ms)
+        out.append({"config": name, "scale": scale, "events": ev, "streams": len(raws),
+                    "bytes": sum(len(r.data) for r in raws), "device_ms": d, "events_per_s": ev / (d / 1e3),
+                    "path": "single pass" if path == 1 else "exact", "range_bytes": rb})
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -361,6 +391,7 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-timeline", action="store_true", help="skip the row-a8 timeline side measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other-configuration side measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
