@@ -317,6 +317,7 @@ struct hg_ctx {
   int last_path = 0;                // 1 = the last run's phase 1 was the single pass
   uint64_t fallbacks = 0;
   uint32_t last_anom = 0;
+  bool deep_inline = false;  // fast_kernel<_, true>: overflow chunks handled inline
   int smem_optin = 0;
 };
 
@@ -601,6 +602,7 @@ void hg_destroy(hg_ctx* ctx) {
 int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, const uint8_t* kinds, uint32_t n_kinds,
                     uint32_t n_functions) {
   if (!ctx || (n_schemas && !schemas)) return HG_EARG;
+  ctx->deep_inline = false;
   uint32_t max_sid = 0;
   for (uint32_t i = 0; i < n_schemas; i++) max_sid = std::max(max_sid, schemas[i].id);
   if (n_schemas && max_sid > (1u << 24)) return fail(ctx, HG_EUNSUPPORTED, "schema ids above 2^24 are not supported");
@@ -776,6 +778,7 @@ int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid, c
 
 int hg_clear_streams(hg_ctx* ctx) {
   if (!ctx) return HG_EARG;
+  ctx->deep_inline = false;
   ctx->streams.clear();
   ctx->staged = false;
   ctx->have_results = false;
@@ -1041,15 +1044,15 @@ static int launch_fast(hg_ctx* ctx) {
   const uint32_t nw = ctx->fast_warps;
   const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
   const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
-  CK(cudaFuncSetAttribute(fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CK(cudaFuncSetAttribute(fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = sd ? (ctx->deep_inline ? fast_kernel<true, true> : fast_kernel<true, false>)
+                 : (ctx->deep_inline ? fast_kernel<false, true> : fast_kernel<false, false>);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint32_t per_cta = nw * kWarp;
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));
   CK(ctx->d_params.ensure(1));
   CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-  if (sd) fast_kernel<true><<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
-  else fast_kernel<false><<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
+  kern<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
   fast_verify_kernel<<<ns, kVThreads, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
@@ -1159,6 +1162,8 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     if (attempt == 7) return fail(ctx, HG_ENOMEM, "scratch buffers kept overflowing");
   }
   ctx->last_path = fast ? 1 : 0;
+  // stacks overflowed the inline slots: later runs keep them on the inline path
+  if (fast && ctx->counters[C_DEEP_USED] > 0) ctx->deep_inline = true;
   if ((uint32_t)ctx->counters[C_WATCHDOG])
     return fail(ctx, HG_ECUDA, "tile look-back watchdog fired (engine bug)");
   if ((uint32_t)ctx->counters[C_WIDE])

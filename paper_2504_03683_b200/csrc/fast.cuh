@@ -635,8 +635,10 @@ __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, const S
   }
 }
 
-// kSD: the registry's inline descriptors fit in shared memory (max_sid < kSdescMax)
-template <bool kSD>
+// kSD: the registry's inline descriptors fit in shared memory (max_sid < kSdescMax);
+// kDeep: stacks deeper than kRLS stay on the inline path (overflow chunk) -- chosen by the host
+// once a run of the trace needed overflow chunks
+template <bool kSD, bool kDeep>
 __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const Params* gp) {
   const Params& gpr = *gp;
   const uint32_t nw = blockDim.x >> 5;
@@ -719,16 +721,22 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const uint32_t kind = (D.x >> 20) & 7u;
     const uint32_t ne = R.ne, np = R.np;
     const uint32_t topi = ((ne - 1u) < (uint32_t)kRLS ? ne - 1u : 0u) * kWarp;
-    const uint64_t ets = T.st_ts[topi];
-    const uint32_t tfn = T.st_fn[topi];
+    uint64_t ets = T.st_ts[topi];
+    uint32_t tfn = T.st_fn[topi];
+    if (kDeep && ne > (uint32_t)kRLS && R.deep) {  // deeper entries live in the lane's overflow chunk (HBM, L1)
+      const SumEntry* de = R.deep + kRDeepHalf + (ne - 1u - kRLS);
+      ets = de->ts;
+      tfn = de->fn < 0 ? M_FN : (uint32_t)de->fn;
+    }
     // inline: the whole record in the ring, in order, with a length its schema allows (lo <= plen <= hi <= 112)
     const uint32_t lo = D.y & 0xFFFFu, hi = D.y >> 16;
     const bool good = ready && plen - lo <= hi - lo && (R.o + 15u + plen) / kRChunk < cr &&
                       R.o + 16u + plen <= R.size32 && (R.n == 0 || ts >= R.prev_ts);
     const bool stall = ready && !good && plen <= kRInline - 16u && (R.o + 15u + plen) / kRChunk >= cr &&
                        (uint64_t)R.o + 16u + plen <= R.size;
-    const bool fE = good && kind == FK_ENTRY && ne < (uint32_t)kRLS;
-    const bool fXp = good && kind == FK_EXIT && ne - 1u < (uint32_t)kRLS && tfn == fnm;  // pops a same-function top
+    const uint32_t cap = (kDeep && R.deep) ? (uint32_t)kRLS + kRDeepHalf : (uint32_t)kRLS;  // entries held inline
+    const bool fE = good && kind == FK_ENTRY && ne < cap;
+    const bool fXp = good && kind == FK_EXIT && ne - 1u < cap && tfn == fnm;  // pops a same-function top
     const bool fXq = good && kind == FK_EXIT && ne == 0 && np < (uint32_t)kRLP;          // pending: compose decides
     const bool fO = good && (kind == FK_PASS || kind == FK_DEFER);
     // one variable field (blob / string): exact length here, UTF-8 of strings in the drain
@@ -763,7 +771,11 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       R.prev_ts = ts;
       R.o += 16u + plen;
     }
-    if (fE) {
+    if (kDeep && fE && ne >= (uint32_t)kRLS) {
+      SumEntry e;
+      e.ts = ts; e.seq = 0; e.fn = m_fn(fnm); e.flags = 0; e.result = 0;
+      R.deep[kRDeepHalf + ne - kRLS] = e;
+    } else if (fE) {
       T.st_ts[ne * kWarp] = ts;
       T.st_fn[ne * kWarp] = fnm;
     }

@@ -215,10 +215,12 @@ class Engine:
 
     # -- the drop-in
     def run(self, raw_streams, registry, stream_infos=None, want_timeline=False, labels=None,
-            orphan_labels=None, timeline_device_index=0) -> RunResult:
+            orphan_labels=None, timeline_device_index=0, reuse_streams=False) -> RunResult:
+        """reuse_streams: run again over the streams of the previous call (still resident in HBM)."""
         flat = self.set_registry(registry)
         self._check(self._L.hg_set_timeline_device(self._ctx, int(timeline_device_index)), "hg_set_timeline_device")
-        self.set_streams(raw_streams)
+        if not reuse_streams:
+            self.set_streams(raw_streams)
         want = HG_WANT_TALLY | (HG_WANT_TIMELINE if want_timeline else 0)
         rc = self.run_raw(want)
         k, t, h2d, d2h, nl = self.timing()

@@ -110,3 +110,24 @@ def test_error_traces_fall_back_to_exact_path(engine):
         assert engine.last_path()[0] == 0
     else:
         assert got.report == want.report and got.stats == want.stats
+
+
+@pytest.mark.parametrize("max_depth,push_p", [(64, 0.55), (300, 0.9)])
+def test_deep_stacks_second_run_inline(engine, max_depth, push_p):
+    """The first run of a deep trace spills stacks to overflow chunks through the slow path; the
+    context then switches to the kernel variant that keeps them inline: both runs match the oracle."""
+    from oracle import oracle
+    from paper_2504_03683_b200 import synth
+
+    P = synth.PID_BASE
+    streams = [synth.StreamSpec("h", P, P + i, 20000 + 3001 * i, 7100 + i) for i in range(6)]
+    wl = synth.Workload("deep", synth.ze_registry(), streams,
+                        dict(max_depth=max_depth, push_p=push_p, mismatch_p=0.01, close_at_end=0, prof_p=0.2),
+                        kernel_names=synth.kernel_pool(12))
+    raws = synth.generate(wl)
+    infos = [r.info for r in raws]
+    want = oracle.run(raws, wl.registry, infos)
+    for i in range(2):
+        got = engine.run(raws, wl.registry, infos, reuse_streams=i > 0)
+        assert engine.last_path()[0] == 1
+        assert got.stats == want.stats and got.report == want.report and got.orphans == want.orphans
