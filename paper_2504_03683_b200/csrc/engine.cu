@@ -34,12 +34,25 @@ namespace {
 // composition of segment summaries per stream (exact automaton from an empty stack)
 
 constexpr int kComposeWarps = 4;
+constexpr uint32_t kComposeFast = 128;  // stack positions per warp held in shared memory
 
-__global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p) {
+// kBlock (single pass only): one warp per block of up to 32 consecutive ranges of a stream; exits
+// that meet the block's empty stack stay pending and the block's stack becomes its summary, which
+// the per-stream pass (kBlock = false) then composes -- 32x shorter sequential chains per stream.
+struct ComposeBlocks {
+  const uint32_t* stream;  // block -> stream
+  const uint32_t* u0;      // block -> first unit (n_blocks + 1 entries)
+  SegState* out;           // block summaries
+  uint32_t n;
+};
+
+template <bool kBlock>
+__global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p, ComposeBlocks B) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t lane = lane_id();
   const uint32_t warp = threadIdx.x >> 5;
   SmemRow* tab = p.n_fn <= kSmemFnMax ? reinterpret_cast<SmemRow*>(smem) : nullptr;
+  const uint32_t cfast_off = p.n_fn <= kSmemFnMax ? ((uint32_t)sizeof(SmemRow) * p.n_fn + 15u) & ~15u : 0u;
   if (tab)
     for (uint32_t i = threadIdx.x; i < p.n_fn; i += blockDim.x) {
       SmemRow z; z.count = z.err = z.s0 = z.s1 = 0; z.mn = 0xFFFFFFFFu; z.mx = 0;
@@ -49,17 +62,18 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
   HostFold hf;
   hf.small = false;
   hf.tab = tab;
-  const uint32_t s = blockIdx.x * kComposeWarps + warp;
+  const uint32_t wid = blockIdx.x * kComposeWarps + warp;
+  const uint32_t s = kBlock ? (wid < B.n ? B.stream[wid] : p.n_streams) : wid;
   uint32_t host = 0, orph = 0, trunc = 0, spans = 0;
   if (s < p.n_streams) {
-    const uint32_t g0 = p.stream_tile0[s];
-    const uint32_t g1 = (s + 1 < p.n_streams) ? p.stream_tile0[s + 1] : p.n_tiles;
+    const uint32_t g0 = kBlock ? B.u0[wid] : p.stream_tile0[s];
+    const uint32_t g1 = kBlock ? B.u0[wid + 1] : (s + 1 < p.n_streams) ? p.stream_tile0[s + 1] : p.n_tiles;
     // first failed tile (its summary is still composed) and the stack capacity
     uint32_t gerr = g1;
     unsigned long long need = 0;
     for (uint32_t g = g0 + lane; g < g1; g += kWarp) {
       if ((p.state[g].status & 3u) == TS_ERROR && g < gerr) gerr = g;
-      need += p.state[g].pool_n_resid;
+      need += p.state[g].pool_n_resid + (kBlock ? p.state[g].pool_n_pending : 0u);
     }
     gerr = __reduce_min_sync(0xffffffffu, gerr);
     #pragma unroll
@@ -71,6 +85,9 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
     if (sbase + need <= p.stack_cap) {
       GStack gs;
       gs.base = p.stack_scratch + sbase;
+      // the bottom kComposeFast positions in shared memory (call stacks are shallow; deeper ones spill)
+      gs.fast = reinterpret_cast<SumEntry*>(smem + cfast_off) + warp * kComposeFast;
+      gs.n_fast = kComposeFast;
       gs.n_pend = 0;
       gs.top = 0;
       bool res_done = false;
@@ -106,7 +123,7 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
           bool isE = act && k >= onp;
           bool paired, orphan;
           uint64_t ets;
-          const RoundOut ro2 = round_resolve(gs, false, isE, isX, x.fn, x.ts, x);
+          const RoundOut ro2 = round_resolve(gs, kBlock, isE, isX, x.fn, x.ts, x);
           paired = ro2.flags & 1u;
           orphan = (ro2.flags >> 1) & 1u;
           ets = ro2.ets;
@@ -129,14 +146,30 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
           if (orphan) { push_orphan(p, s, x.fn, x.ts, x.seq); orph++; }
         }
       }
+      if (kBlock) {  // the block's stack (pending exits, then open entries) is its summary
+        unsigned long long off = 0;
+        if (lane == 0 && gs.top) off = atomicAdd(p.pool_used, (unsigned long long)gs.top);
+        off = __shfl_sync(0xffffffffu, off, 0);
+        if (off + gs.top <= p.pool_cap)
+          for (uint32_t i = lane; i < gs.top; i += kWarp) p.pool[off + i] = gs.at(i);
+        if (lane == 0) {
+          SegState st;
+          st.status = (p.epoch << 2) | TS_DONE;
+          st.pool_n_pending = gs.n_pend;
+          st.pool_off = off;
+          st.pool_n_resid = gs.top - gs.n_pend;
+          st.pad = 0;
+          B.out[wid] = st;
+        }
+      }
       // open calls become truncated spans ending at the global last timestamp
-      for (uint32_t ib = 0; ib < gs.top; ib += kWarp) {
+      for (uint32_t ib = 0; !kBlock && ib < gs.top; ib += kWarp) {
         const uint32_t i = ib + lane;
         const bool on = i < gs.top;
         SumEntry en;
         en.ts = 0; en.fn = 0;
         if (on) {
-          en = gs.base[i];
+          en = gs.at(i);
           hf.fold(p, en.fn, p.global_last_ts - en.ts, false);
           trunc++;
           spans++;
@@ -319,6 +352,11 @@ struct hg_ctx {
   uint32_t last_anom = 0;
   bool deep_inline = false;  // fast_kernel<_, true>: overflow chunks handled inline
   int smem_optin = 0;
+  // compose blocks (single pass)
+  uint32_t n_blk = 0;
+  std::vector<uint32_t> blk_stream, blk_u0, stream_blk0;
+  DBuf<uint32_t> d_blk_stream, d_blk_u0, d_stream_blk0;
+  DBuf<SegState> d_blk_state;
 };
 
 // counter slots in d_counters
@@ -594,6 +632,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_deep.release(); ctx->d_params.release();
   ctx->d_range_stream.release(); ctx->d_stream_range0.release(); ctx->d_rstate.release(); ctx->d_rseg.release();
   ctx->d_range_base.release(); ctx->d_vplan.release(); ctx->d_fdesc.release(); ctx->d_dplan.release();
+  ctx->d_blk_stream.release(); ctx->d_blk_u0.release(); ctx->d_stream_blk0.release(); ctx->d_blk_state.release();
   for (auto& ev : ctx->ev) if (ev) cudaEventDestroy(ev);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -849,6 +888,21 @@ static int build_layout(hg_ctx* ctx) {
     for (uint64_t j = 0; j < nr; j++) ctx->range_stream.push_back(s);
   }
   ctx->n_ranges = (uint32_t)ctx->range_stream.size();
+  // compose blocks: up to 32 consecutive ranges of one stream
+  ctx->blk_stream.clear();
+  ctx->blk_u0.clear();
+  ctx->stream_blk0.assign(ns, 0);
+  for (uint32_t s = 0; s < ns; s++) {
+    ctx->stream_blk0[s] = (uint32_t)ctx->blk_stream.size();
+    const uint32_t r0 = ctx->stream_range0[s];
+    const uint32_t r1 = s + 1 < ns ? ctx->stream_range0[s + 1] : ctx->n_ranges;
+    for (uint32_t r = r0; r < r1; r += kWarp) {
+      ctx->blk_stream.push_back(s);
+      ctx->blk_u0.push_back(r);
+    }
+  }
+  ctx->n_blk = (uint32_t)ctx->blk_stream.size();
+  ctx->blk_u0.push_back(ctx->n_ranges);
   return HG_OK;
 }
 
@@ -886,6 +940,10 @@ static int stage(hg_ctx* ctx) {
   CK(ctx->d_rseg.ensure(std::max<size_t>(nr, 1)));
   CK(ctx->d_range_base.ensure(std::max<size_t>(nr, 1)));
   if (nr) CK(cudaMemcpyAsync(ctx->d_range_stream.ptr, ctx->range_stream.data(), nr * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(upload(ctx->d_blk_stream, ctx->blk_stream, ctx->stream));
+  CK(upload(ctx->d_blk_u0, ctx->blk_u0, ctx->stream));
+  CK(upload(ctx->d_stream_blk0, ctx->stream_blk0, ctx->stream));
+  CK(ctx->d_blk_state.ensure(std::max<uint32_t>(ctx->n_blk, 1)));
   if (ns) CK(cudaMemcpyAsync(ctx->d_stream_range0.ptr, ctx->stream_range0.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->d_state.n < nt) {
     CK(ctx->d_state.ensure(nt));
@@ -1141,7 +1199,11 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     ctx->h2d_bytes = h2d;
     bool grow = false;
     unsigned long long* C = ctx->counters.data();
-    if (C[C_POOL_USED] > ctx->pool_cap) { ctx->pool_cap = C[C_POOL_USED] + (C[C_POOL_USED] >> 2); ctx->stack_cap = ctx->pool_cap; grow = true; }
+    if (C[C_POOL_USED] > ctx->pool_cap || (fast && 2 * C[C_POOL_USED] > ctx->pool_cap)) {  // single pass: room for
+      ctx->pool_cap = 2 * C[C_POOL_USED] + (C[C_POOL_USED] >> 2);                         // the block summaries
+      ctx->stack_cap = ctx->pool_cap;
+      grow = true;
+    }
     if (C[C_N_ORPHANS] > ctx->orphan_cap) { ctx->orphan_cap = C[C_N_ORPHANS] * 2; grow = true; }
     if (C[C_DEEP_USED] > ctx->deep_cap) { ctx->deep_cap = C[C_DEEP_USED] * 2; grow = true; }
     if ((uint32_t)C[C_N_ERRORS] > ctx->error_cap) { ctx->error_cap = (uint32_t)C[C_N_ERRORS] * 2; grow = true; }
@@ -1197,9 +1259,23 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
       unsigned long long zero = 0;
       CK(cudaMemcpyAsync(p.stack_used, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
       // the tally accumulators already hold phase-1 spans; compose adds the rest
-      size_t csmem = ctx->n_fn <= kSmemFnMax ? sizeof(SmemRow) * ctx->n_fn : 0;
-      CK(cudaFuncSetAttribute(compose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
-      compose_kernel<<<(ns + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem, ctx->stream>>>(p);
+      size_t csmem = (ctx->n_fn <= kSmemFnMax ? ((sizeof(SmemRow) * ctx->n_fn + 15) & ~(size_t)15) : 0) +
+                     sizeof(SumEntry) * kComposeFast * kComposeWarps;
+      CK(cudaFuncSetAttribute(compose_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
+      CK(cudaFuncSetAttribute(compose_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
+      if (ctx->last_path == 1 && ctx->n_blk < ctx->n_ranges) {
+        // blocks of 32 ranges first, then each stream over its block summaries
+        ComposeBlocks B{ctx->d_blk_stream.ptr, ctx->d_blk_u0.ptr, ctx->d_blk_state.ptr, ctx->n_blk};
+        compose_kernel<true><<<(ctx->n_blk + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem,
+                               ctx->stream>>>(p, B);
+        CK(cudaMemcpyAsync(p.stack_used, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
+        p.state = ctx->d_blk_state.ptr;
+        p.stream_tile0 = ctx->d_stream_blk0.ptr;
+        p.n_tiles = ctx->n_blk;
+        ctx->launches++;
+      }
+      compose_kernel<false><<<(ns + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem, ctx->stream>>>(
+          p, ComposeBlocks{nullptr, nullptr, nullptr, 0});
       CK(cudaGetLastError());
       ctx->launches++;
     }

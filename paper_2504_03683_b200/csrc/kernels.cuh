@@ -256,9 +256,12 @@ __device__ __forceinline__ void fold_device(const Params& p, DevRow* cache, uint
 // composition instead of being orphans.
 
 struct GStack {
-  SumEntry* base;
+  SumEntry* base;      // positions >= n_fast (global scratch)
+  SumEntry* fast;      // positions < n_fast (the warp's shared-memory slice; nullptr: none)
+  uint32_t n_fast;
   uint32_t n_pend;
   uint32_t top;
+  __device__ __forceinline__ SumEntry& at(uint32_t i) const { return i < n_fast ? fast[i] : base[i]; }
 };
 
 struct RoundOut {
@@ -302,7 +305,7 @@ __device__ __noinline__ RoundOut round_resolve(GStack st, bool allow_pending, bo
     int jx = __ffs(Xs) - 1;
     int32_t fj = __shfl_sync(0xffffffffu, fn, jx);
     if (st.top > st.n_pend) {
-      SumEntry tp = st.base[st.top - 1];
+      SumEntry tp = st.at(st.top - 1);
       if (tp.fn == fj) {
         if ((int)lane == jx) { paired = true; entry_ts = tp.ts; }
         st.top--;
@@ -310,7 +313,7 @@ __device__ __noinline__ RoundOut round_resolve(GStack st, bool allow_pending, bo
         orphan = true;
       }
     } else if (allow_pending) {
-      if ((int)lane == jx) st.base[st.n_pend] = mine;
+      if ((int)lane == jx) st.at(st.n_pend) = mine;
       st.n_pend++;
       st.top++;
     } else if ((int)lane == jx) {
@@ -320,7 +323,7 @@ __device__ __noinline__ RoundOut round_resolve(GStack st, bool allow_pending, bo
     Xs &= Xs - 1;
   }
   uint32_t Es = __ballot_sync(0xffffffffu, isE && me_unres);
-  if (isE && me_unres) st.base[st.top + __popc(Es & lanemask_lt())] = mine;
+  if (isE && me_unres) st.at(st.top + __popc(Es & lanemask_lt())) = mine;
   st.top += __popc(Es);
   __syncwarp();
   RoundOut out;
