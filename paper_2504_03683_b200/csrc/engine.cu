@@ -874,7 +874,7 @@ static int build_layout(hg_ctx* ctx) {
   // compose_kernel resolves a stream's range summaries in order (one warp per stream): bound the
   // ranges per stream so a single huge stream does not serialise there
   if (!ctx->range_opt) {
-    uint64_t max_per = 2048;
+    uint64_t max_per = 8192;
     if (const char* e = getenv("HAPIGPU_MAX_RANGES")) max_per = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
     R = std::max<uint64_t>(R, ((max_pay + max_per - 1) / max_per + 15) & ~15ull);
   }
