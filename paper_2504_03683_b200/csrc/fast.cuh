@@ -256,6 +256,14 @@ __device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T)
   if (R.bad) atomicOr(p.anom, 1u);   // anomaly reasons (bits): 1 record, 2 drain, 4 string, 8 chain, 16 order
 }
 
+// close the lane's range and open its next one, out of line (rare; the lane state travels by value
+// so the hot loop keeps it in registers)
+__device__ __noinline__ RLane r_switch(const Params& p, RLane R, const RTabs T, uint32_t stride) {
+  r_end(p, R, T);
+  r_begin(p, R, R.r + stride, stride);
+  return R;
+}
+
 // a per-lane overflow chunk for deep stacks / many pending exits
 __device__ __forceinline__ bool r_deep(const Params& p, RLane& R) {
   if (R.deep) return true;
@@ -677,8 +685,8 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const bool ending = live && (R.o >= R.t1 || R.bad);
     if (__any_sync(0xffffffffu, ending)) {
       if (ending) {
-        r_end(gpr, R, T);
-        live = r_begin(gpr, R, R.r + stride, stride);
+        R = r_switch(gpr, R, T, stride);
+        live = R.r < p.n_ranges;
       }
     }
     const bool act = live && R.o < R.t1 && !R.bad;
