@@ -350,6 +350,8 @@ struct hg_ctx {
   int last_path = 0;                // 1 = the last run's phase 1 was the single pass
   uint64_t fallbacks = 0;
   uint32_t last_anom = 0;
+  uint32_t range_shift = 0;  // extra bytes per range (retry after a failed speculation)
+  uint64_t retries = 0;
   bool deep_inline = false;  // fast_kernel<_, true>: overflow chunks handled inline
   int smem_optin = 0;
   // compose blocks (single pass)
@@ -824,6 +826,8 @@ int hg_clear_streams(hg_ctx* ctx) {
   return HG_OK;
 }
 
+static int build_ranges(hg_ctx* ctx);
+
 static int build_layout(hg_ctx* ctx) {
   const uint32_t ns = (uint32_t)ctx->streams.size();
   ctx->base.resize(ns);
@@ -844,7 +848,13 @@ static int build_layout(hg_ctx* ctx) {
     const uint32_t nt = sz > 16 ? (uint32_t)((sz - 16 + ctx->seg_bytes - 1) / ctx->seg_bytes) : 0;
     for (uint32_t t = 0; t < nt; t++) ctx->tile_stream.push_back(s);
   }
-  // ranges for the single pass: one per resident lane, never crossing a stream
+  return build_ranges(ctx);
+}
+
+// ranges for the single pass: one per resident lane, never crossing a stream; range_shift moves
+// every cut point (the retry after a failed range speculation)
+static int build_ranges(hg_ctx* ctx) {
+  const uint32_t ns = (uint32_t)ctx->streams.size();
   const uint32_t n_fd = ctx->max_sid < (uint32_t)kSdescMax ? ctx->max_sid + 2 : 0u;
   uint32_t nw = kRMaxThreads / kWarp;
   while (nw > 1 && fast_smem_layout(ctx->n_fn, nw, n_fd).total > (uint32_t)ctx->smem_optin) nw--;
@@ -878,6 +888,7 @@ static int build_layout(hg_ctx* ctx) {
     if (const char* e = getenv("HAPIGPU_MAX_RANGES")) max_per = std::max<uint64_t>(1, strtoull(e, nullptr, 10));
     R = std::max<uint64_t>(R, ((max_pay + max_per - 1) / max_per + 15) & ~15ull);
   }
+  R += ctx->range_shift;
   R = std::min<uint64_t>(R, 1ull << 28);
   ctx->range_bytes = (uint32_t)R;
   ctx->range_stream.clear();
@@ -903,6 +914,23 @@ static int build_layout(hg_ctx* ctx) {
   }
   ctx->n_blk = (uint32_t)ctx->blk_stream.size();
   ctx->blk_u0.push_back(ctx->n_ranges);
+  return HG_OK;
+}
+
+static int upload_ranges(hg_ctx* ctx) {
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  const size_t nr = ctx->n_ranges;
+  CK(ctx->d_range_stream.ensure(std::max<size_t>(nr, 1)));
+  CK(ctx->d_stream_range0.ensure(std::max<uint32_t>(ns, 1)));
+  CK(ctx->d_rstate.ensure(std::max<size_t>(nr, 1)));
+  CK(ctx->d_rseg.ensure(std::max<size_t>(nr, 1)));
+  CK(ctx->d_range_base.ensure(std::max<size_t>(nr, 1)));
+  if (nr) CK(cudaMemcpyAsync(ctx->d_range_stream.ptr, ctx->range_stream.data(), nr * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(upload(ctx->d_blk_stream, ctx->blk_stream, ctx->stream));
+  CK(upload(ctx->d_blk_u0, ctx->blk_u0, ctx->stream));
+  CK(upload(ctx->d_stream_blk0, ctx->stream_blk0, ctx->stream));
+  CK(ctx->d_blk_state.ensure(std::max<uint32_t>(ctx->n_blk, 1)));
+  if (ns) CK(cudaMemcpyAsync(ctx->d_stream_range0.ptr, ctx->stream_range0.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream));
   return HG_OK;
 }
 
@@ -933,18 +961,8 @@ static int stage(hg_ctx* ctx) {
     CK(cudaMemcpyAsync(ctx->d_tile_stream.ptr, ctx->tile_stream.data(), nt * 4, cudaMemcpyHostToDevice, ctx->stream));
   }
   if (ns) CK(cudaMemcpyAsync(ctx->d_stream_tile0.ptr, ctx->stream_tile0.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream));
-  const size_t nr = ctx->n_ranges;
-  CK(ctx->d_range_stream.ensure(std::max<size_t>(nr, 1)));
-  CK(ctx->d_stream_range0.ensure(std::max<uint32_t>(ns, 1)));
-  CK(ctx->d_rstate.ensure(std::max<size_t>(nr, 1)));
-  CK(ctx->d_rseg.ensure(std::max<size_t>(nr, 1)));
-  CK(ctx->d_range_base.ensure(std::max<size_t>(nr, 1)));
-  if (nr) CK(cudaMemcpyAsync(ctx->d_range_stream.ptr, ctx->range_stream.data(), nr * 4, cudaMemcpyHostToDevice, ctx->stream));
-  CK(upload(ctx->d_blk_stream, ctx->blk_stream, ctx->stream));
-  CK(upload(ctx->d_blk_u0, ctx->blk_u0, ctx->stream));
-  CK(upload(ctx->d_stream_blk0, ctx->stream_blk0, ctx->stream));
-  CK(ctx->d_blk_state.ensure(std::max<uint32_t>(ctx->n_blk, 1)));
-  if (ns) CK(cudaMemcpyAsync(ctx->d_stream_range0.ptr, ctx->stream_range0.data(), ns * 4, cudaMemcpyHostToDevice, ctx->stream));
+  int rc = upload_ranges(ctx);
+  if (rc) return rc;
   if (ctx->d_state.n < nt) {
     CK(ctx->d_state.ensure(nt));
     CK(cudaMemsetAsync(ctx->d_state.ptr, 0, nt * sizeof(SegState), ctx->stream));
@@ -1181,7 +1199,8 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->have_results = false;
   ctx->phase1_done = false;
   bool fast = ctx->path_opt != 1 && !(want & HG_WANT_TIMELINE);
-  for (int attempt = 0; attempt < 8; attempt++) {
+  bool retried = false;
+  for (int attempt = 0; attempt < 9; attempt++) {
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
     uint64_t h2d = 0;
     if (!ctx->staged) {
@@ -1211,6 +1230,18 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
       ctx->row_cap *= 4; ctx->dict_mask = ctx->dict_mask * 4 + 3; ctx->arena_cap = std::max<uint64_t>(ctx->arena_cap * 4, C[C_ARENA_USED] * 2);
       grow = true;
     }
+    if (!grow && fast && (uint32_t)ctx->counters[C_ANOM] && !retried && !ctx->range_opt &&
+        !((uint32_t)ctx->counters[C_ANOM] & 6u)) {
+      // a record-level or chain failure may be a wrong range speculation: move every cut point once
+      retried = true;
+      ctx->range_shift = 16u * 61u;
+      int rr = build_ranges(ctx);
+      if (!rr) rr = upload_ranges(ctx);
+      ctx->range_shift = 0;
+      if (rr) return rr;
+      ctx->retries++;
+      continue;
+    }
     if (!grow && fast && (uint32_t)ctx->counters[C_ANOM]) {
       // the single pass met something it does not reproduce exactly: rerun the exact path
       if (ctx->path_opt == 2) return fail(ctx, HG_ESTATE, "single-pass path rejected the trace (HAPIGPU_PATH=2)");
@@ -1221,7 +1252,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
       continue;
     }
     if (!grow) break;
-    if (attempt == 7) return fail(ctx, HG_ENOMEM, "scratch buffers kept overflowing");
+    if (attempt == 8) return fail(ctx, HG_ENOMEM, "scratch buffers kept overflowing");
   }
   ctx->last_path = fast ? 1 : 0;
   // stacks overflowed the inline slots: later runs keep them on the inline path
