@@ -202,13 +202,34 @@ __device__ __forceinline__ I128 sub128(I128 a, I128 b) {
 }
 __device__ __forceinline__ bool eq128(I128 a, I128 b) { return a.hi == b.hi && a.lo == b.lo; }
 
+// decimal digit count of v by comparisons only (the counting writer's fast path)
+__device__ __forceinline__ uint32_t ndig(uint64_t v) {
+  if (v < 10000000000ull) {
+    if (v < 100000ull) return v < 100ull ? (v < 10ull ? 1 : 2) : (v < 1000ull ? 3 : (v < 10000ull ? 4 : 5));
+    return v < 10000000ull ? (v < 1000000ull ? 6 : 7) : (v < 100000000ull ? 8 : (v < 1000000000ull ? 9 : 10));
+  }
+  if (v < 1000000000000000ull)
+    return v < 1000000000000ull ? (v < 100000000000ull ? 11 : 12) : (v < 10000000000000ull ? 13 : (v < 100000000000000ull ? 14 : 15));
+  return v < 100000000000000000ull ? (v < 10000000000000000ull ? 16 : 17) : (v < 1000000000000000000ull ? 18 : (v < 10000000000000000000ull ? 19 : 20));
+}
+
 template <class W>
 __device__ __forceinline__ void w_i128(W& w, I128 v) {
+  if (!W::kWrite && (v.hi == 0 || (v.hi == -1 && (int64_t)v.lo < 0))) {  // fits in 64 bits: count
+    w.s(nullptr, v.hi == 0 ? ndig(v.lo) : 1u + ndig(0 - v.lo));
+    return;
+  }
   char b[48];
   w.s(b, (uint32_t)nf::fmt_i128(v.hi, v.lo, b));
 }
 template <class W>
 __device__ __forceinline__ void w_us(W& w, I128 ns) {  // ns / 1000.0
+  if (!W::kWrite && ns.hi == 0 && ns.lo < 8796093022208000ull) {  // fmt_ns_div1000's exact-decimal case
+    const uint64_t ip = ns.lo / 1000;
+    const uint32_t fp = (uint32_t)(ns.lo - ip * 1000);
+    w.s(nullptr, ndig(ip) + 1u + (fp == 0 ? 1u : (fp % 10u ? 3u : (fp % 100u ? 2u : 1u))));
+    return;
+  }
   char b[40];
   w.s(b, (uint32_t)nf::fmt_ns_div1000(ns.hi, ns.lo, b));
 }
@@ -426,13 +447,18 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
     w.s(T.sstr + so[1], (uint32_t)(so[2] - so[1]));
     w.lit(",\n  \"args\": {\n   \"result\": ");
     {
-      char b[400];
       const uint32_t rk = (it.kind >> 4) & 3u;
-      int l;
-      if (rk == 2) l = nf::fmt_int_of_double(__longlong_as_double((long long)it.b), b);
-      else if (rk == 1) l = nf::fmt_i64((int64_t)it.b, b);
-      else l = nf::fmt_u64(it.b, b);
-      w.s(b, (uint32_t)l);
+      if (!W::kWrite && rk != 2) {  // integer result: count its digits
+        const bool neg = rk == 1 && (int64_t)it.b < 0;
+        w.s(nullptr, neg ? 1u + ndig(0 - it.b) : ndig(it.b));
+      } else {
+        char b[400];
+        int l;
+        if (rk == 2) l = nf::fmt_int_of_double(__longlong_as_double((long long)it.b), b);
+        else if (rk == 1) l = nf::fmt_i64((int64_t)it.b, b);
+        else l = nf::fmt_u64(it.b, b);
+        w.s(b, (uint32_t)l);
+      }
     }
     if (trunc) w.lit(",\n   \"truncated\": true");
     w.lit("\n  }\n }");
