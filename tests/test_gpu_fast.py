@@ -131,3 +131,24 @@ def test_deep_stacks_second_run_inline(engine, max_depth, push_p):
         got = engine.run(raws, wl.registry, infos, reuse_streams=i > 0)
         assert engine.last_path()[0] == 1
         assert got.stats == want.stats and got.report == want.report and got.orphans == want.orphans
+
+
+@pytest.mark.parametrize("name,scale,prof_p", [("c5", 0.004, None), ("c2", 0.003, 0.6), ("c4", 0.003, 0.9)])
+def test_device_heavy_repeated_runs(engine, name, scale, prof_p):
+    """Device-heavy traces run repeatedly on the same staged streams (the CTA name caches and
+    the global name dictionary start over each run): every run matches the oracle."""
+    import dataclasses
+
+    from oracle import oracle
+    from paper_2504_03683_b200 import synth
+
+    wl = synth.config(name, scale)
+    if prof_p is not None:
+        wl = dataclasses.replace(wl, params=dict(wl.params, prof_p=prof_p))
+    raws = synth.generate(wl)
+    infos = [r.info for r in raws]
+    want = oracle.run(raws, wl.registry, infos)
+    for i in range(3):
+        got = engine.run(raws, wl.registry, infos, reuse_streams=i > 0)
+        assert engine.last_path()[0] == 1
+        assert got.stats == want.stats and got.report == want.report and got.orphans == want.orphans
