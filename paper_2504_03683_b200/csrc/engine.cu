@@ -316,6 +316,7 @@ struct hg_ctx {
   uint64_t tl_cap = 0;
   DBuf<ulonglong2> d_tl_keys[2];
   DBuf<uint32_t> d_tl_idx[2];
+  DBuf<uint32_t> d_tl_ro[2], d_tl_tcnt, d_tl_tile0, d_tl_split;  // sort: run offsets, tile counts, merge splits
   DBuf<uint32_t> d_tl_lens, d_tl_stream_proc;
   DBuf<uint64_t> d_tl_offs, d_tl_bsum, d_tl_fnq_off, d_tl_sstr_off;
   DBuf<char> d_tl_fnq, d_tl_sstr, d_tl_out, d_tl_devpid;
@@ -486,23 +487,51 @@ static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   CK(upload(ctx->d_tl_sstr_off, sstr_off, st));
   CK(upload(ctx->d_tl_stream_proc, sproc, st));
   CK(upload(ctx->d_tl_devpid, devpid, st));
-  // sort by mux key
-  const uint32_t nblk = (N + kSortTile - 1) / kSortTile;
+  // sort by mux key: the streams' record slots are sorted runs; drop the empty slots, sort
+  // compose's messages per tile, merge the runs pairwise
+  const uint32_t nrec_slots = (uint32_t)ctx->tl_comp_base;
+  const uint32_t ncomp = (uint32_t)C[C_TL_N2];
+  const uint32_t nrec = n - ncomp;
+  const uint32_t n_rtiles = (nrec_slots + kSortTile - 1) / kSortTile;
+  const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
+  uint32_t R = ns + ntc;
   for (int k = 0; k < 2; k++) {
-    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(N, 1)));
-    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(N, 1)));
+    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_ro[k].ensure(R + 2));
   }
+  CK(ctx->d_tl_tcnt.ensure(n_rtiles + 2));
+  CK(ctx->d_tl_tile0.ensure(R / 2 + 3));
+  CK(ctx->d_tl_split.ensure(n / kSortTile + R / 2 + 3));
   int cur = 0;
-  if (N) {
-    tl_blocksort_kernel<<<nblk, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, N, ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr);
-    CK(cudaGetLastError());
+  if (n) {
+    if (n_rtiles) {
+      tl_count_kernel<<<n_rtiles, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, nrec_slots, ctx->d_tl_tcnt.ptr);
+      tl_small_scan_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_tcnt.ptr, n_rtiles);
+      ctx->launches += 2;
+    }
+    tl_compact_kernel<<<n_rtiles + std::max<uint32_t>(ntc, 1), kSortThreads, 0, st>>>(
+        ctx->d_tl_items.ptr, nrec_slots, (uint32_t)N, ctx->d_tl_tcnt.ptr, n_rtiles, ctx->d_tl_rec_off.ptr, ns, nrec, n,
+        ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, ctx->d_tl_ro[0].ptr);
     ctx->launches++;
-    for (uint64_t width = kSortTile; width < N; width *= 2) {
-      tl_merge_kernel<<<nblk, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
-                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr, N, width);
-      CK(cudaGetLastError());
+    if (ntc) {
+      tl_tilesort_kernel<<<ntc, kSortThreads, 0, st>>>(ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, nrec, ncomp);
       ctx->launches++;
+    }
+    CK(cudaGetLastError());
+    while (R > 1) {
+      const uint32_t P = (R + 1) / 2;
+      const uint32_t tiles = n / kSortTile + P + 1;  // bound on the output tiles of the pass
+      tl_pairs_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_ro[cur ^ 1].ptr);
+      tl_split_kernel<<<(tiles + 127) / 128, 128, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_ro[cur].ptr, R,
+                                                           ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
+      tl_merge_kernel<<<tiles, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
+                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr,
+                                                      ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
+      CK(cudaGetLastError());
+      ctx->launches += 3;
       cur ^= 1;
+      R = P;
     }
   }
   // metadata first occurrences
@@ -625,7 +654,8 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_keys.release(); ctx->d_vals.release(); ctx->d_name_len.release(); ctx->d_small.release();
   ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release();
   ctx->d_tl_items.release();
-  for (int k = 0; k < 2; k++) { ctx->d_tl_keys[k].release(); ctx->d_tl_idx[k].release(); }
+  for (int k = 0; k < 2; k++) { ctx->d_tl_keys[k].release(); ctx->d_tl_idx[k].release(); ctx->d_tl_ro[k].release(); }
+  ctx->d_tl_tcnt.release(); ctx->d_tl_tile0.release(); ctx->d_tl_split.release();
   ctx->d_tl_lens.release(); ctx->d_tl_stream_proc.release(); ctx->d_tl_offs.release(); ctx->d_tl_bsum.release();
   ctx->d_tl_fnq_off.release(); ctx->d_tl_sstr_off.release(); ctx->d_tl_fnq.release(); ctx->d_tl_sstr.release();
   ctx->d_tl_out.release(); ctx->d_tl_devpid.release(); ctx->d_tl_proc_first.release(); ctx->d_tl_th_state.release();

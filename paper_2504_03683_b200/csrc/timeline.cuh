@@ -5,9 +5,10 @@
 // at their exit record, device spans and telemetry samples at their record,
 // truncated spans at finish().  This file orders and prints them:
 //
-//   tl_blocksort_kernel / tl_merge_kernel   merge sort of (khi, klo) keys = mux
-//        order (pipeline.py:68-114); keys are unique, 2048-element CTA tiles,
-//        merge-path partitioned passes
+//   tl_count / tl_compact / tl_tilesort / tl_pairs / tl_split / tl_merge
+//        order by (khi, klo) = mux order (pipeline.py:68-114): the streams are
+//        sorted runs already; empty slots dropped, runs merged pairwise with
+//        merge-path partitioned passes (keys are unique)
 //   tl_meta_kernel    first sorted position of every metadata key
 //        (pid, tid, kind) -- TimelineSink._meta emits at first sight (sinks.py:351-359)
 //   tl_len_kernel     exact byte length of every item's JSON text (+ metas)
@@ -289,14 +290,163 @@ constexpr int kSortThreads = 256;
 
 __device__ __forceinline__ bool key_lt(ulonglong2 a, ulonglong2 b) { return a.x < b.x || (a.x == b.x && a.y < b.y); }
 
-__global__ void __launch_bounds__(kSortThreads) tl_blocksort_kernel(const TlItem* items, uint32_t n, ulonglong2* keys,
-                                                                    uint32_t* idx) {
-  __shared__ ulonglong2 sk[kSortTile];
-  __shared__ uint32_t si[kSortTile];
+// The slots of the record region hold each stream's messages at their record index, so every
+// stream is already a sorted run (per-stream timestamps never decrease, the record index breaks
+// ties); the empty slots (records that emit nothing) are dropped first.  Compose's messages (in
+// claim order) are sorted per tile.  The runs are then merged pairwise -- the k-way merge of the
+// reference's muxer (heapq.merge over the streams) as log2(streams) merge-path passes.
+
+// messages per tile of the record region (empty slots: key ~0)
+__global__ void __launch_bounds__(kSortThreads) tl_count_kernel(const TlItem* items, uint32_t nrec, uint32_t* tcnt) {
+  __shared__ uint32_t wsum[kSortThreads / 32];
   const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
+  uint32_t c = 0;
   for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
     const uint64_t g = base + t;
-    if (g < n) { sk[t] = make_ulonglong2(items[g].khi, items[g].klo); si[t] = (uint32_t)g; }
+    if (g < nrec) c += (items[g].khi != ~0ull || items[g].klo != ~0ull) ? 1u : 0u;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s = 0;
+    for (int w = 0; w < kSortThreads / 32; w++) s += wsum[w];
+    tcnt[blockIdx.x] = s;
+  }
+}
+
+// exclusive scan of n counts in place by one 1024-thread CTA (all threads call it); a[n] = total
+__device__ __forceinline__ void cta_excl_scan(uint32_t* a, uint32_t n) {
+  __shared__ uint32_t ws[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t b = 0; b < n; b += 1024) {
+    const uint32_t i = b + threadIdx.x;
+    const uint32_t v = i < n ? a[i] : 0u;
+    uint32_t x = v;
+    #pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if ((threadIdx.x & 31) >= (uint32_t)d) x += y;
+    }
+    if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t w = ws[threadIdx.x];
+      #pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+        if (threadIdx.x >= (uint32_t)d) w += y;
+      }
+      ws[threadIdx.x] = w;
+    }
+    __syncthreads();
+    const uint32_t incl = carry + x + ((threadIdx.x >> 5) ? ws[(threadIdx.x >> 5) - 1] : 0u);
+    if (i < n) a[i] = incl - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a[n] = carry;
+}
+
+__global__ void __launch_bounds__(1024) tl_small_scan_kernel(uint32_t* a, uint32_t n) { cta_excl_scan(a, n); }
+
+// drop the empty slots: keys + item index of every message, record region then compose's
+// messages; run_off[s] = first message of stream s, then one run per compose tile, run_off[R] = n
+__global__ void __launch_bounds__(kSortThreads) tl_compact_kernel(const TlItem* items, uint32_t nrec_slots, uint32_t n_slots,
+                                                                  const uint32_t* tpre, uint32_t n_rtiles,
+                                                                  const unsigned long long* rec_off, uint32_t ns,
+                                                                  uint32_t nrec, uint32_t n, ulonglong2* keys,
+                                                                  uint32_t* idx, uint32_t* run_off) {
+  constexpr uint32_t kPer = kSortTile / kSortThreads;
+  __shared__ uint32_t wsum[kSortThreads / 32];
+  __shared__ uint32_t s_pre[kSortThreads];
+  if (blockIdx.x >= n_rtiles) {  // compose's messages: no empty slots
+    const uint64_t c0 = (uint64_t)(blockIdx.x - n_rtiles) * kSortTile;
+    for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+      const uint64_t g = nrec_slots + c0 + t;
+      if (g < n_slots) {
+        keys[nrec + c0 + t] = make_ulonglong2(items[g].khi, items[g].klo);
+        idx[nrec + c0 + t] = (uint32_t)g;
+      }
+    }
+    if (blockIdx.x == n_rtiles) {
+      const uint32_t R0 = ns;
+      for (uint32_t c = threadIdx.x; nrec + (uint64_t)c * kSortTile < n; c += blockDim.x) run_off[R0 + c] = nrec + c * kSortTile;
+      const uint32_t ntc = (n - nrec + kSortTile - 1) / kSortTile;
+      if (threadIdx.x == 0) run_off[R0 + ntc] = n;
+      for (uint32_t s = threadIdx.x; s < ns; s += blockDim.x)  // streams whose records start at the end
+        if (rec_off[s] >= nrec_slots) run_off[s] = nrec;
+    }
+    return;
+  }
+  const uint64_t base = (uint64_t)blockIdx.x * kSortTile + (uint64_t)threadIdx.x * kPer;  // kPer slots per thread
+  ulonglong2 k[kPer];
+  uint32_t m = 0;
+  #pragma unroll
+  for (uint32_t j = 0; j < kPer; j++) {
+    const uint64_t g = base + j;
+    k[j] = g < nrec_slots ? make_ulonglong2(items[g].khi, items[g].klo) : make_ulonglong2(~0ull, ~0ull);
+    m |= (k[j].x != ~0ull || k[j].y != ~0ull) ? 1u << j : 0u;
+  }
+  const uint32_t c = __popc(m);
+  uint32_t x = c;  // inclusive warp scan, then across warps
+  #pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if ((threadIdx.x & 31) >= (uint32_t)d) x += y;
+  }
+  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = x;
+  __syncthreads();
+  uint32_t wo = 0;
+  for (uint32_t w = 0; w < (threadIdx.x >> 5); w++) wo += wsum[w];
+  const uint32_t ex = tpre[blockIdx.x] + wo + x - c;  // first output of this thread
+  s_pre[threadIdx.x] = ex;
+  uint32_t o = ex;
+  #pragma unroll
+  for (uint32_t j = 0; j < kPer; j++) {
+    if (m >> j & 1u) {
+      keys[o] = k[j];
+      idx[o] = (uint32_t)(base + j);
+      o++;
+    }
+  }
+  __syncthreads();
+  // streams starting in this tile: their first message is the first at or after the start slot
+  if (threadIdx.x < 32) {
+    const uint64_t t0 = (uint64_t)blockIdx.x * kSortTile, t1 = t0 + kSortTile;
+    uint32_t lo = 0, hi = ns;  // first stream with rec_off >= t0
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (rec_off[mid] < t0) lo = mid + 1;
+      else hi = mid;
+    }
+    for (uint32_t s = lo + threadIdx.x; s < ns; s += 32) {
+      const uint64_t r = rec_off[s];
+      if (r >= t1 || r >= nrec_slots) break;
+      const uint32_t th = (uint32_t)(r - t0) / kPer, j = (uint32_t)(r - t0) % kPer;
+      uint32_t before = s_pre[th];
+      for (uint32_t q = 0; q < j; q++) {
+        const uint64_t g = t0 + (uint64_t)th * kPer + q;
+        before += (items[g].khi != ~0ull || items[g].klo != ~0ull) ? 1u : 0u;
+      }
+      run_off[s] = before;
+    }
+  }
+}
+
+// one compose tile sorted in place (bitonic, 2048 keys); the last tile is padded with ~0 keys
+__global__ void __launch_bounds__(kSortThreads) tl_tilesort_kernel(ulonglong2* keys, uint32_t* idx, uint32_t base,
+                                                                   uint32_t count) {
+  __shared__ ulonglong2 sk[kSortTile];
+  __shared__ uint32_t si[kSortTile];
+  const uint64_t b0 = base + (uint64_t)blockIdx.x * kSortTile;
+  const uint64_t end = (uint64_t)base + count;
+  for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    const uint64_t g = b0 + t;
+    if (g < end) { sk[t] = keys[g]; si[t] = idx[g]; }
     else { sk[t] = make_ulonglong2(~0ull, ~0ull); si[t] = 0xFFFFFFFFu; }
   }
   __syncthreads();
@@ -317,8 +467,8 @@ __global__ void __launch_bounds__(kSortThreads) tl_blocksort_kernel(const TlItem
     }
   }
   for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
-    const uint64_t g = base + t;
-    if (g < n) { keys[g] = sk[t]; idx[g] = si[t]; }
+    const uint64_t g = b0 + t;
+    if (g < end) { keys[g] = sk[t]; idx[g] = si[t]; }
   }
 }
 
@@ -334,45 +484,84 @@ __device__ __forceinline__ uint64_t corank(uint64_t k, uint64_t na, uint64_t nb,
   return lo;
 }
 
+// one merge pass over R runs: pair p = runs 2p, 2p+1 (the last may be alone); output tiles of
+// kSortTile per pair, tile0[p] = first tile of pair p (exclusive scan), nro = the merged runs
+__global__ void __launch_bounds__(1024) tl_pairs_kernel(const uint32_t* ro, uint32_t R, uint32_t* tile0, uint32_t* nro) {
+  const uint32_t P = (R + 1) / 2;
+  for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) {
+    const uint32_t len = ro[min(2 * p + 2, R)] - ro[2 * p];
+    tile0[p] = (len + kSortTile - 1) / kSortTile;
+    nro[p] = ro[2 * p];
+  }
+  if (threadIdx.x == 0) nro[P] = ro[R];
+  __syncthreads();
+  cta_excl_scan(tile0, P);
+}
+
+// co-rank of every output tile's first element within its pair
+__global__ void tl_split_kernel(const ulonglong2* ki, const uint32_t* ro, uint32_t R, const uint32_t* tile0,
+                                uint32_t* split) {
+  const uint32_t P = (R + 1) / 2;
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= tile0[P]) return;
+  uint32_t lo = 0, hi = P;  // last pair with tile0 <= b
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (tile0[mid] <= b) lo = mid;
+    else hi = mid;
+  }
+  const uint32_t p = lo;
+  const uint32_t a0 = ro[2 * p], a1 = ro[min(2 * p + 1, R)], b1 = ro[min(2 * p + 2, R)];
+  const uint32_t na = a1 - a0, nb = b1 - a1;
+  const uint64_t k = (uint64_t)(b - tile0[p]) * kSortTile;
+  split[b] = (uint32_t)corank(k, na, nb, [&](uint64_t x) { return ki[a0 + x]; }, [&](uint64_t x) { return ki[a1 + x]; });
+}
+
 __global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2* ki, const uint32_t* ii, ulonglong2* ko,
-                                                                uint32_t* io, uint32_t n, uint64_t width) {
+                                                                uint32_t* io, const uint32_t* ro, uint32_t R,
+                                                                const uint32_t* tile0, const uint32_t* split) {
   __shared__ ulonglong2 sk[kSortTile];
   __shared__ uint32_t si[kSortTile];
-  __shared__ uint64_t bnd[4];
-  const uint64_t out0 = (uint64_t)blockIdx.x * kSortTile;
-  if (out0 >= n) return;
-  const uint64_t pair0 = out0 / (2 * width) * (2 * width);
-  const uint64_t a0 = pair0, a1 = min((uint64_t)n, pair0 + width);
-  const uint64_t b0 = a1, b1 = min((uint64_t)n, pair0 + 2 * width);
-  const uint64_t na = a1 - a0, nb = b1 - b0;
-  const uint64_t k0 = out0 - pair0, k1 = min(k0 + kSortTile, na + nb);
-  if (threadIdx.x < 2) {
-    const uint64_t k = threadIdx.x ? k1 : k0;
-    const uint64_t i = corank(k, na, nb, [&](uint64_t x) { return ki[a0 + x]; }, [&](uint64_t x) { return ki[b0 + x]; });
-    bnd[2 * threadIdx.x] = i;
-    bnd[2 * threadIdx.x + 1] = k - i;
+  __shared__ uint16_t src[kSortTile];
+  const uint32_t P = (R + 1) / 2;
+  const uint32_t b = blockIdx.x;
+  if (b >= tile0[P]) return;
+  uint32_t lo = 0, hi = P;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (tile0[mid] <= b) lo = mid;
+    else hi = mid;
   }
-  __syncthreads();
-  const uint64_t i0 = bnd[0], j0 = bnd[1], i1 = bnd[2], j1 = bnd[3];
-  const uint32_t la = (uint32_t)(i1 - i0), lb = (uint32_t)(j1 - j0);
+  const uint32_t p = lo;
+  const uint32_t a0 = ro[2 * p], a1 = ro[min(2 * p + 1, R)], b1 = ro[min(2 * p + 2, R)];
+  const uint32_t na = a1 - a0, nb = b1 - a1;
+  const uint32_t k0 = (b - tile0[p]) * kSortTile, k1 = min(k0 + (uint32_t)kSortTile, na + nb);
+  const uint32_t i0 = split[b], i1 = b + 1 < tile0[p + 1] ? split[b + 1] : na;
+  const uint32_t j0 = k0 - i0, j1 = k1 - i1;
+  const uint32_t la = i1 - i0, lb = j1 - j0;
   for (uint32_t t = threadIdx.x; t < la + lb; t += blockDim.x) {
-    const uint64_t g = t < la ? a0 + i0 + t : b0 + j0 + (t - la);
+    const uint32_t g = t < la ? a0 + i0 + t : a1 + j0 + (t - la);
     sk[t] = ki[g];
     si[t] = ii[g];
   }
   __syncthreads();
-  const uint32_t per = kSortTile / kSortThreads;
+  constexpr uint32_t per = kSortTile / kSortThreads;
   const uint32_t kk = threadIdx.x * per;
   if (kk < la + lb) {
     uint32_t i = (uint32_t)corank(kk, la, lb, [&](uint64_t x) { return sk[x]; }, [&](uint64_t x) { return sk[la + x]; });
     uint32_t j = kk - i;
     const uint32_t end = min(kk + per, la + lb);
     for (uint32_t k = kk; k < end; k++) {
-      bool takeA = j >= lb || (i < la && key_lt(sk[i], sk[la + j]));
-      const uint32_t src = takeA ? i++ : la + j++;
-      ko[out0 + k] = sk[src];
-      io[out0 + k] = si[src];
+      const bool takeA = j >= lb || (i < la && key_lt(sk[i], sk[la + j]));
+      src[k] = (uint16_t)(takeA ? i++ : la + j++);
     }
+  }
+  __syncthreads();
+  const uint32_t out0 = a0 + k0;  // the merged run starts where run 2p did
+  for (uint32_t t = threadIdx.x; t < la + lb; t += blockDim.x) {
+    const uint32_t q = src[t];
+    ko[out0 + t] = sk[q];
+    io[out0 + t] = si[q];
   }
 }
 
