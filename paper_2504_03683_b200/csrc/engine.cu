@@ -481,6 +481,7 @@ static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   const uint32_t n_proc = (uint32_t)proc_id.size() + 1;
   std::string dps = std::to_string(dev_pid);
   std::vector<char> devpid(dps.begin(), dps.end());
+  for (std::vector<char>* v : {&fnq, &sstr, &devpid}) v->insert(v->end(), 8, '\0');  // word-wise readers
   CK(upload(ctx->d_tl_fnq, fnq, st));
   CK(upload(ctx->d_tl_fnq_off, fnq_off, st));
   CK(upload(ctx->d_tl_sstr, sstr, st));
@@ -561,7 +562,7 @@ static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   T.stream_proc = ctx->d_tl_stream_proc.ptr;
   T.dev_proc = dev_proc;
   T.dev_pid = ctx->d_tl_devpid.ptr;
-  T.dev_pid_len = (uint32_t)devpid.size();
+  T.dev_pid_len = (uint32_t)dps.size();
   T.proc_first = ctx->d_tl_proc_first.ptr;
   T.th_state = ctx->d_tl_th_state.ptr;
   T.th_hi = ctx->d_tl_th_hi.ptr;

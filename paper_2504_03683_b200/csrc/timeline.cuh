@@ -61,12 +61,34 @@ struct TW {        // writes the bytes
   char* p;
   uint64_t n;
   __device__ __forceinline__ void c(char ch) { p[n++] = ch; }
+  // a copy from a word-padded source (device tables and the stream bytes are padded): the
+  // destination's head bytes, then 4-byte stores of funnel-shifted source words, then the tail
   __device__ __forceinline__ void s(const char* q, uint32_t l) {
-    for (uint32_t i = 0; i < l; i++) p[n + i] = q[i];
+    char* d = p + n;
     n += l;
+    uint32_t i = 0;
+    while (i < l && (reinterpret_cast<uintptr_t>(d + i) & 3)) { d[i] = q[i]; i++; }
+    if (i + 4 <= l) {
+      const char* qs = q + i;
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(qs) & ~(uintptr_t)3);
+      const uint32_t sh = (uint32_t)(reinterpret_cast<uintptr_t>(qs) & 3) * 8;
+      uint32_t* dw = reinterpret_cast<uint32_t*>(d + i);
+      uint32_t a = w[0];
+      for (uint32_t k = 1; i + 4 <= l; i += 4, k++) {
+        const uint32_t b = w[k];
+        *dw++ = __funnelshift_r(a, b, sh);
+        a = b;
+      }
+    }
+    for (; i < l; i++) d[i] = q[i];
   }
   template <int N>
-  __device__ __forceinline__ void lit(const char (&q)[N]) { s(q, N - 1); }
+  __device__ __forceinline__ void lit(const char (&q)[N]) {
+    #pragma unroll
+    for (int i = 0; i < N - 1; i++) p[n + i] = q[i];
+    n += N - 1;
+  }
+  __device__ __forceinline__ char* at() { return p + n; }
 };
 struct TC {        // counts them (tl_len_kernel)
   static constexpr bool kWrite = false;
@@ -220,8 +242,12 @@ __device__ __forceinline__ void w_i128(W& w, I128 v) {
     w.s(nullptr, v.hi == 0 ? ndig(v.lo) : 1u + ndig(0 - v.lo));
     return;
   }
-  char b[48];
-  w.s(b, (uint32_t)nf::fmt_i128(v.hi, v.lo, b));
+  if constexpr (W::kWrite) {
+    w.n += nf::fmt_i128(v.hi, v.lo, w.at());
+  } else {
+    char b[48];
+    w.s(b, (uint32_t)nf::fmt_i128(v.hi, v.lo, b));
+  }
 }
 template <class W>
 __device__ __forceinline__ void w_us(W& w, I128 ns) {  // ns / 1000.0
@@ -231,8 +257,12 @@ __device__ __forceinline__ void w_us(W& w, I128 ns) {  // ns / 1000.0
     w.s(nullptr, ndig(ip) + 1u + (fp == 0 ? 1u : (fp % 10u ? 3u : (fp % 100u ? 2u : 1u))));
     return;
   }
-  char b[40];
-  w.s(b, (uint32_t)nf::fmt_ns_div1000(ns.hi, ns.lo, b));
+  if constexpr (W::kWrite) {
+    w.n += nf::fmt_ns_div1000(ns.hi, ns.lo, w.at());
+  } else {
+    char b[40];
+    w.s(b, (uint32_t)nf::fmt_ns_div1000(ns.hi, ns.lo, b));
+  }
 }
 
 // device track id tile * 2 + engine (sinks.py:379-381)
@@ -640,12 +670,11 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
       if (!W::kWrite && rk != 2) {  // integer result: count its digits
         const bool neg = rk == 1 && (int64_t)it.b < 0;
         w.s(nullptr, neg ? 1u + ndig(0 - it.b) : ndig(it.b));
+      } else if (rk != 2 && W::kWrite) {
+        if constexpr (W::kWrite) w.n += rk == 1 ? nf::fmt_i64((int64_t)it.b, w.at()) : nf::fmt_u64(it.b, w.at());
       } else {
         char b[400];
-        int l;
-        if (rk == 2) l = nf::fmt_int_of_double(__longlong_as_double((long long)it.b), b);
-        else if (rk == 1) l = nf::fmt_i64((int64_t)it.b, b);
-        else l = nf::fmt_u64(it.b, b);
+        const int l = nf::fmt_int_of_double(__longlong_as_double((long long)it.b), b);
         w.s(b, (uint32_t)l);
       }
     }
