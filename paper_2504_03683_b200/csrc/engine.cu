@@ -580,8 +580,9 @@ static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   uint64_t total = 0;
   if (n) {
     const uint32_t g = std::min<uint32_t>((n + 255) / 256, (uint32_t)ctx->sm_count * 16);
-    tl_meta_kernel<<<g, 256, 0, st>>>(T);
     tl_len_kernel<<<g, 256, 0, st>>>(T);
+    tl_meta_len_kernel<<<std::min<uint32_t>((n_proc + th_size + 255) / 256, (uint32_t)ctx->sm_count * 8), 256, 0, st>>>(
+        T, n_proc, th_size);
     tl_scan1_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr);
     tl_scan2_kernel<<<1, kScanBlock, 0, st>>>(ctx->d_tl_bsum.ptr, nsb, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
     tl_scan3_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr, T.offs);

@@ -9,9 +9,10 @@
 //        order by (khi, klo) = mux order (pipeline.py:68-114): the streams are
 //        sorted runs already; empty slots dropped, runs merged pairwise with
 //        merge-path partitioned passes (keys are unique)
-//   tl_meta_kernel    first sorted position of every metadata key
-//        (pid, tid, kind) -- TimelineSink._meta emits at first sight (sinks.py:351-359)
-//   tl_len_kernel     exact byte length of every item's JSON text (+ metas)
+//   tl_len_kernel     exact byte length of every item's JSON text, and the first
+//        sorted position of every metadata key (pid, tid, kind) -- TimelineSink._meta
+//        emits at first sight (sinks.py:351-359)
+//   tl_meta_len_kernel   the lengths of the items that carry metadata objects
 //   tl_scan*          exclusive scan -> byte offsets
 //   tl_write_kernel   formats each warp's 32 consecutive items into a shared
 //        staging buffer, then stores it with aligned 16-byte writes
@@ -598,23 +599,6 @@ __global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2
 // ---------------------------------------------------------------------------
 // metadata first occurrences
 
-__global__ void tl_meta_kernel(TlTables T) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const TlItem it = T.items[T.order[i]];
-    const uint32_t kind = it.kind & 3u;
-    if (kind == TL_HOST) {
-      first_min(&T.proc_first[T.stream_proc[tl_stream(it.klo)]], (uint32_t)i);
-    } else if (kind == TL_DEVICE) {
-      first_min(&T.proc_first[T.dev_proc], (uint32_t)i);
-      const DSchema* sc = tl_schema(T, it.x);
-      TlFields F;
-      tl_locate(T, sc, reinterpret_cast<const uint8_t*>(it.a), F);
-      const int slot = th_slot(T, dev_tid(int_field(F, sc, HG_ROLE_TILE), int_field(F, sc, HG_ROLE_ENGINE)), true);
-      if (slot >= 0) first_min(&T.th_first[slot], (uint32_t)i);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // one item's JSON text: [metas] + object, each element prefixed by ",\n " ("\n " first)
 
@@ -639,7 +623,10 @@ __device__ __forceinline__ void meta_obj(W& w, bool first, bool thread, const ch
   w.lit("\n  }\n }");
 }
 
-template <class W>
+// kLen: the length pass -- the item's own text only, while recording the first occurrences of
+// its metadata keys (TimelineSink._meta, sinks.py:351-359); tl_meta_len_kernel then measures
+// the items that carry metadata again, with it
+template <class W, bool kLen = false>
 __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   const TlItem it = T.items[T.order[i]];
   const uint32_t kind = it.kind & 3u;
@@ -647,7 +634,9 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   if (kind == TL_HOST) {
     const uint32_t s = tl_stream(it.klo);
     const uint64_t* so = T.sstr_off + 3ull * s;
-    if (T.proc_first[T.stream_proc[s]] == i) {
+    if (kLen) {
+      first_min(&T.proc_first[T.stream_proc[s]], i);
+    } else if (T.proc_first[T.stream_proc[s]] == i) {
       meta_obj(w, first, false, T.sstr + so[0], (uint32_t)(so[1] - so[0]), I128{0, 0}, T.sstr + so[2],
                (uint32_t)(so[3] - so[2]), nullptr, 0);
       first = false;
@@ -688,11 +677,15 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   if (kind == TL_DEVICE) {
     const I128 tile = int_field(F, sc, HG_ROLE_TILE), engine = int_field(F, sc, HG_ROLE_ENGINE);
     const I128 tid = dev_tid(tile, engine);
-    if (T.proc_first[T.dev_proc] == i) {
+    if (kLen) {
+      first_min(&T.proc_first[T.dev_proc], i);
+      const int slot = th_slot(T, tid, true);
+      if (slot >= 0) first_min(&T.th_first[slot], i);
+    } else if (T.proc_first[T.dev_proc] == i) {
       meta_obj(w, first, false, T.dev_pid, T.dev_pid_len, I128{0, 0}, "\"Device 0\"", 10, nullptr, 0);
       first = false;
     }
-    const int slot = th_slot(T, tid, false);
+    const int slot = kLen ? -1 : th_slot(T, tid, false);
     if (slot >= 0 && T.th_first[slot] == i) {
       // _DEVICE_TRACK_NAMES (sinks.py:323-328)
       const bool known = tile.hi == 0 && engine.hi == 0 && tile.lo <= 1 && engine.lo <= 1;
@@ -758,8 +751,21 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
 __global__ void tl_len_kernel(TlTables T) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
     TC w{0};
-    tl_format(T, (uint32_t)i, w);
+    tl_format<TC, true>(T, (uint32_t)i, w);
     T.lens[i] = (uint32_t)w.n;
+  }
+}
+
+// the items that open a metadata key: their length with the metadata objects (two keys may
+// share an item: both threads store the same length)
+__global__ void tl_meta_len_kernel(TlTables T, uint32_t n_proc, uint32_t th_size) {
+  for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (uint64_t)n_proc + th_size;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = e < n_proc ? T.proc_first[e] : T.th_first[e - n_proc];
+    if (f >= T.n) continue;
+    TC w{0};
+    tl_format<TC, false>(T, f, w);
+    T.lens[f] = (uint32_t)w.n;
   }
 }
 
