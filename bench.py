@@ -349,7 +349,7 @@ def timeline_side(eng, config="c5", scale=0.1):
             "events": st["events_in"], "messages": msgs, "json_bytes": len(tl),
             "phase1_ms": r1.kernel_ms, "timeline_ms": ms, "json_gb_per_s": len(tl) / ms / 1e6,
             "events_per_s": st["events_in"] / ((r1.kernel_ms + ms) / 1e3),
-            "path": "exact three-kernel phase 1 (record-indexed messages) + mux-key merge sort + JSON formatting",
+            "path": "exact three-kernel phase 1 (record-indexed messages) + k-way merge of the per-stream runs by mux key + JSON formatting",
             "checks": "object count = messages + metadata, json.dump framing, tally == tally-only run"}
 
 
