@@ -62,8 +62,8 @@ struct TW {        // writes the bytes
   char* p;
   uint64_t n;
   __device__ __forceinline__ void c(char ch) { p[n++] = ch; }
-  // a copy from a word-padded source (device tables and the stream bytes are padded): the
-  // destination's head bytes, then 4-byte stores of funnel-shifted source words, then the tail
+  // the destination's head bytes, then 4-byte stores of funnel-shifted source words, then the
+  // tail; every source word read holds a byte of the string (no read past its last word)
   __device__ __forceinline__ void s(const char* q, uint32_t l) {
     char* d = p + n;
     n += l;
@@ -76,7 +76,7 @@ struct TW {        // writes the bytes
       uint32_t* dw = reinterpret_cast<uint32_t*>(d + i);
       uint32_t a = w[0];
       for (uint32_t k = 1; i + 4 <= l; i += 4, k++) {
-        const uint32_t b = w[k];
+        const uint32_t b = (sh || i + 8 <= l) ? w[k] : 0u;
         *dw++ = __funnelshift_r(a, b, sh);
         a = b;
       }
@@ -123,13 +123,19 @@ __device__ __forceinline__ void hex4(W& w, uint32_t v) {
 // json.dumps(str) with ensure_ascii of validated UTF-8 bytes (json/encoder.py ESCAPE_ASCII)
 template <class W>
 __device__ __forceinline__ void json_str(W& w, const uint8_t* s, uint32_t len) {
-  {  // plain printable ASCII without quote or backslash (kernel names): the bytes themselves
-    bool plain = true;
-    for (uint32_t i = 0; i < len && plain; i++) {
-      const uint32_t c = s[i];
-      plain = c >= 0x20 && c < 0x7F && c != '"' && c != '\\';
+  {  // plain printable ASCII without quote or backslash (kernel names): the bytes themselves.
+     // Four bytes per step (exact SWAR byte tests: < 0x20, >= 0x7F, == '"', == '\\')
+    uint32_t bad = 0;
+    for (uint32_t i = 0; i < len; i += 4) {
+      uint32_t x = ldu32(s + i);
+      if (len - i < 4) {
+        const uint32_t m = 0xffffffffu >> (8u * (4u - (len - i)));
+        x = (x & m) | (0x61616161u & ~m);  // past the end: 'a'
+      }
+      const uint32_t y = x ^ 0x22222222u, z = x ^ 0x5C5C5C5Cu;
+      bad |= ((x - 0x20202020u) & ~x) | (x + 0x01010101u) | x | ((y - 0x01010101u) & ~y) | ((z - 0x01010101u) & ~z);
     }
-    if (plain) {
+    if (!(bad & 0x80808080u)) {
       w.c('"');
       if (W::kWrite) w.s(reinterpret_cast<const char*>(s), len);
       else w.s(nullptr, len);
