@@ -754,7 +754,10 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   w.lit("\n  }\n }");
 }
 
-__global__ void tl_len_kernel(TlTables T) {
+#ifndef HG_TL_LEN_MINB
+#define HG_TL_LEN_MINB 3  // 3 CTAs per SM (80 registers): 3.85 vs 5.2 ms for the timeline of C5 x0.1
+#endif
+__global__ void __launch_bounds__(256, HG_TL_LEN_MINB) tl_len_kernel(TlTables T) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
     TC w{0};
     tl_format<TC, true>(T, (uint32_t)i, w);
@@ -839,7 +842,10 @@ __global__ void __launch_bounds__(kScanBlock) tl_scan3_kernel(const uint32_t* le
 constexpr int kTlWarps = 8;
 constexpr int kTlStage = 5120;
 
-__global__ void __launch_bounds__(kTlWarps * 32) tl_write_kernel(TlTables T) {
+#ifndef HG_TL_WRITE_MINB
+#define HG_TL_WRITE_MINB 3  // (with the length pass at 3: both at 80 registers, the spills are cheaper than the latency)
+#endif
+__global__ void __launch_bounds__(kTlWarps * 32, HG_TL_WRITE_MINB) tl_write_kernel(TlTables T) {
   __shared__ __align__(16) char stage[kTlWarps][kTlStage + 32];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   char* buf = stage[warp];
