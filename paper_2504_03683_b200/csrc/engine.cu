@@ -353,6 +353,7 @@ struct hg_ctx {
   uint32_t last_anom = 0;
   uint32_t range_shift = 0;  // extra bytes per range (retry after a failed speculation)
   uint64_t retries = 0;
+  uint32_t max_rps = 0;      // most ranges in one stream (fast_verify_kernel's width)
   bool deep_inline = false;  // fast_kernel<_, true>: overflow chunks handled inline
   int smem_optin = 0;
   // compose blocks (single pass)
@@ -931,6 +932,9 @@ static int build_ranges(hg_ctx* ctx) {
     for (uint64_t j = 0; j < nr; j++) ctx->range_stream.push_back(s);
   }
   ctx->n_ranges = (uint32_t)ctx->range_stream.size();
+  ctx->max_rps = 0;
+  for (uint32_t s = 0; s < ns; s++)
+    ctx->max_rps = std::max<uint32_t>(ctx->max_rps, (s + 1 < ns ? ctx->stream_range0[s + 1] : ctx->n_ranges) - ctx->stream_range0[s]);
   // compose blocks: up to 32 consecutive ranges of one stream
   ctx->blk_stream.clear();
   ctx->blk_u0.clear();
@@ -1163,7 +1167,8 @@ static int launch_fast(hg_ctx* ctx) {
   kern<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
-  fast_verify_kernel<<<ns, kVThreads, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
+  if (ctx->max_rps > 1024) fast_verify_kernel<512><<<ns, 512, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
+  else fast_verify_kernel<128><<<ns, 128, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
   fast_orphan_fix_kernel<<<32, 256, 0, ctx->stream>>>(p);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[5], ctx->stream));

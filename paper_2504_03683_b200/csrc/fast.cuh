@@ -869,8 +869,9 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
 // Thread t owns a contiguous block of the stream's ranges: a local pass composes the block
 // (exit carry, last timestamp, record count and what the block needs from its predecessor), a
 // CTA scan hands every block its incoming carry, a second pass writes the per-range outputs.
-constexpr int kVThreads = 128;
-
+// kVThreads: 128 threads per stream; 512 when a stream has many ranges (one huge stream: the
+// two sequential passes shrink 4x, the carry scan over the blocks grows)
+template <int kVThreads>
 __global__ void __launch_bounds__(kVThreads) fast_verify_kernel(Params p, unsigned long long* stream_nrec) {
   __shared__ unsigned long long sx[kVThreads], st_[kVThreads], sb[kVThreads];
   __shared__ uint32_t sflags[kVThreads];
