@@ -69,3 +69,23 @@ def test_single_huge_stream_matches_oracle(engine):
     wl = synth.Workload("big1", synth.ze_registry(), [synth.StreamSpec("s", 1, 1, 400_000, 77)],
                         {"max_depth": 12, "push_p": 0.55, "mismatch_p": 0.001, "close_at_end": 0})
     _cmp(engine, wl)
+
+
+def test_timeline_many_runs_and_empty_streams(engine):
+    """2,100 streams (over 1,024 merge pairs in the first pass), every seventh empty, unclosed
+    calls (truncated spans sorted among compose's messages)."""
+    from paper_2504_03683_b200 import synth
+
+    P = synth.PID_BASE
+    streams = [synth.StreamSpec(f"h{i % 5}", P + 100 * (i % 9), P + 100 * (i % 9) + i, 0 if i % 7 == 3 else 20 + i % 61,
+                                5000 + i) for i in range(2100)]
+    wl = synth.Workload("many", synth.ze_registry(), streams, {"close_at_end": 0, "prof_p": 0.3},
+                        kernel_names=synth.kernel_pool(40))
+    _cmp(engine, wl)
+
+
+def test_timeline_record_region_over_1024_tiles(engine):
+    """Over 2M record slots: the tile-count scan of the run compaction spans several CTA rounds."""
+    from paper_2504_03683_b200 import synth
+
+    _cmp(engine, synth.config("c2", 0.022))  # 2.2M records: 1,074 tiles
