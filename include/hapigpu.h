@@ -198,6 +198,12 @@ int hg_get_timeline(hg_ctx* ctx, char* out, uint64_t cap);
 int hg_timeline_ms(hg_ctx* ctx, float* ms);  /* device time of the ordering + formatting */
 /* phase-1 kernel times of the last run (segment walk, chain, decode), CUDA events */
 int hg_phase_timing(hg_ctx* ctx, float* walk_ms, float* chain_ms, float* decode_ms);
+/* order in which open calls are flushed as truncated spans at the end of the run:
+ * the reference sorts its stacks by (str(hostname), pid, tid) (pipeline.py:230), which
+ * differs from the (hostname or "", pid or 0, tid or 0) stream order when hostnames are
+ * None.  rank[s] = position of stream s in the flush order (a permutation of the added
+ * streams); NULL restores stream order.  Reset by hg_clear_streams. */
+int hg_set_flush_order(hg_ctx* ctx, const uint32_t* rank, uint32_t n);
 /* TimelineSink(device_index=) (sinks.py:347-349): device pid 9000000 + index */
 int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index);
 

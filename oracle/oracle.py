@@ -59,9 +59,9 @@ def lib():
         L = C.CDLL(str(LIB))
         vp, u32, u64 = C.c_void_p, C.c_uint32, C.c_uint64
         L.oracle_run.restype = vp
-        L.oracle_run.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32]
+        L.oracle_run.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32, vp, vp]
         L.oracle_tally_threads.restype = vp
-        L.oracle_tally_threads.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32]
+        L.oracle_tally_threads.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32, vp]
         L.oracle_free.argtypes = [vp]
         L.oracle_has_error.argtypes = [vp, vp]
         L.oracle_has_error.restype = C.c_int
@@ -123,12 +123,21 @@ def run(raw_streams, registry, stream_infos=None, want_timeline=False, threads=0
     bufs = [C.create_string_buffer(s.data, len(s.data)) if s.data else None for s in raw_streams]
     ptrs = (C.c_void_p * max(n, 1))(*[C.cast(b, C.c_void_p) if b is not None else None for b in bufs])
     sizes = (C.c_uint64 * max(n, 1))(*[len(s.data) for s in raw_streams])
+    # streams sharing one (hostname, pid, tid) share a stack (pipeline.py:156-161)
+    first, grp = {}, []
+    for i, s in enumerate(raw_streams):
+        grp.append(first.setdefault((s.hostname, s.pid, s.tid), i))
+    group = (C.c_uint32 * max(n, 1))(*grp) if len(first) < n else None
+    # the reference flushes open calls per stack sorted by (str(hostname), pid, tid) (pipeline.py:230)
+    fo = sorted(range(n), key=lambda i: (str(raw_streams[i].hostname), raw_streams[i].pid or 0,
+                                         raw_streams[i].tid or 0, i))
+    flush = (C.c_uint32 * max(n, 1))(*fo) if fo != list(range(n)) else None
     if threads:
         h = L.oracle_tally_threads(flat.schemas, flat.n_schemas, flat.kinds, len(flat.function_names), n,
-                                   ptrs, sizes, threads)
+                                   ptrs, sizes, threads, group)
     else:
         h = L.oracle_run(flat.schemas, flat.n_schemas, flat.kinds, len(flat.function_names), n, ptrs, sizes,
-                         1 if want_timeline else 0)
+                         1 if want_timeline else 0, group, flush)
     if not h:
         raise RuntimeError("oracle: registry ids too large")
     try:

@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
           trunc++;
           spans++;
         }
-        if (p.tl_items)  // innermost first (pipeline.py:230-238)
-          tl_emit(p, on, ~0ull, (1ull << 63) | tl_klo(s, on ? gs.top - 1 - i : 0), en.ts, 0,
+        if (p.tl_items)  // stacks in (str(hostname), pid, tid) order, innermost first (pipeline.py:230-238)
+          tl_emit(p, on, ~0ull, (1ull << 63) | tl_klo(p.flush_rank ? p.flush_rank[s] : s, on ? gs.top - 1 - i : 0), en.ts, 0,
                   TL_HOST | TL_TRUNC | (1u << 4), (uint32_t)en.fn);
       }
     } else if (lane == 0) {
@@ -219,406 +219,7 @@ __global__ void init_acc_kernel(unsigned long long* host_acc, uint32_t n_fn, uns
 
 }  // namespace
 
-// ===========================================================================
-// host side: the C ABI (include/hapigpu.h)
-
-namespace {
-
-template <class T>
-struct DBuf {
-  T* ptr = nullptr;
-  size_t n = 0;
-  cudaError_t ensure(size_t want) {
-    if (want <= n) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr; n = 0;
-    cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(want, 1) * sizeof(T));
-    if (e == cudaSuccess) n = want;
-    return e;
-  }
-  void release() { if (ptr) cudaFree(ptr); ptr = nullptr; n = 0; }
-};
-
-struct HostStream {
-  std::string host;
-  int64_t pid, tid;
-  const uint8_t* data;
-  uint64_t size;
-};
-
-}  // namespace
-
-struct hg_ctx {
-  hg_config cfg{};
-  std::string err;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev[8] = {};  // 0 run start, 1 after staging, 2 after compose, 3 results on host, 4/5 phase 1, 6 after walk, 7 after chain
-  int sm_count = 0;
-  // registry
-  std::vector<DSchema> schemas;
-  std::vector<int32_t> sid_map;
-  std::vector<uint2> desc;
-  DBuf<uint2> d_desc;
-  std::vector<uint8_t> kinds, field_role;
-  uint32_t n_fn = 0, max_sid = 0;
-  DBuf<DSchema> d_schemas;
-  DBuf<int32_t> d_sid_map;
-  DBuf<uint8_t> d_kinds, d_field_role;
-  // streams
-  std::vector<HostStream> streams;
-  bool staged = false;
-  std::vector<uint64_t> base, sizes;
-  uint64_t total_bytes = 0;
-  DBuf<uint8_t> d_data;
-  DBuf<uint64_t> d_base, d_size;
-  std::vector<uint32_t> tile_stream, stream_tile0;  // segment -> stream, stream -> first segment
-  DBuf<uint32_t> d_tile_stream, d_stream_tile0;
-  // scratch
-  DBuf<SegState> d_state;
-  uint32_t epoch = 0;
-  DBuf<SumEntry> d_pool, d_stack;
-  uint64_t pool_cap = 0, stack_cap = 0;
-  DBuf<unsigned long long> d_host_acc, d_dev_acc;
-  DBuf<unsigned long long> d_counters;  // misc counters, see below
-  DBuf<hg_orphan> d_orphans;
-  uint64_t orphan_cap = 0;
-  DBuf<hg_trace_error> d_errors;
-  uint32_t error_cap = 0;
-  DBuf<unsigned long long> d_stream_spans;
-  // name dict
-  DBuf<unsigned long long> d_keys;
-  DBuf<uint32_t> d_vals, d_name_len, d_small;
-  DBuf<uint64_t> d_name_off;
-  DBuf<uint8_t> d_arena;
-  uint64_t dict_mask = 0, arena_cap = 0;
-  uint32_t row_cap = 0;
-  // results (host copies)
-  bool have_results = false;
-  uint32_t want = 0;
-  std::vector<unsigned long long> counters;
-  std::vector<unsigned long long> host_acc, dev_acc;
-  std::vector<uint8_t> arena;
-  std::vector<uint64_t> name_off;
-  std::vector<uint32_t> name_len;
-  uint32_t n_dev_rows = 0;
-  std::vector<hg_orphan> orphans;
-  std::vector<hg_trace_error> errors;
-  std::vector<unsigned long long> stream_spans;
-  uint64_t local_last_ts = 0, local_events = 0;
-  bool phase1_done = false;
-  float kernel_ms = 0, total_ms = 0;
-  uint64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
-  // timeline
-  std::vector<std::string> fn_names;
-  std::vector<uint8_t> fn_null;
-  bool have_fn_names = false;
-  DBuf<TlItem> d_tl_items;
-  uint64_t tl_cap = 0;
-  DBuf<ulonglong2> d_tl_keys[2];
-  DBuf<uint32_t> d_tl_idx[2];
-  DBuf<uint32_t> d_tl_ro[2], d_tl_tcnt, d_tl_tile0, d_tl_split;  // sort: run offsets, tile counts, merge splits
-  DBuf<uint32_t> d_tl_lens, d_tl_stream_proc;
-  DBuf<uint64_t> d_tl_offs, d_tl_bsum, d_tl_fnq_off, d_tl_sstr_off;
-  DBuf<char> d_tl_fnq, d_tl_sstr, d_tl_out, d_tl_devpid;
-  DBuf<unsigned int> d_tl_proc_first, d_tl_th_state, d_tl_th_first;
-  DBuf<unsigned long long> d_tl_th_hi, d_tl_th_lo;
-  uint64_t tl_size = 0;
-  bool tl_ready = false;
-  float tl_ms = 0;
-  uint64_t tl_comp_base = 0;
-  float walk_ms = 0, chain_ms = 0, decode_ms = 0;
-  // segments
-  uint32_t seg_bytes = 8192;
-  DBuf<SegW> d_segw;
-  DBuf<SegInfo> d_seginfo;
-  DBuf<unsigned long long> d_stream_nrec, d_tl_rec_off;
-  DBuf<SumEntry> d_deep;
-  uint64_t deep_cap = 0;
-  DBuf<Params> d_params;
-  // single-pass range path (fast.cuh)
-  int path_opt = 0;                 // 0 auto (fast, exact on anomaly), 1 exact only, 2 fast only
-  uint32_t range_opt = 0;           // forced range bytes (0 = sized to the resident lanes)
-  uint32_t range_bytes = 0, n_ranges = 0, fast_warps = 0;
-  std::vector<uint32_t> range_stream, stream_range0;
-  DBuf<uint32_t> d_range_stream, d_stream_range0;
-  DBuf<RangeState> d_rstate;
-  DBuf<SegState> d_rseg;
-  DBuf<unsigned long long> d_range_base;
-  std::vector<uint32_t> vplan;
-  DBuf<uint32_t> d_vplan;
-  std::vector<uint4> fdesc, dplan;
-  DBuf<uint4> d_fdesc, d_dplan;
-  int last_path = 0;                // 1 = the last run's phase 1 was the single pass
-  uint64_t fallbacks = 0;
-  uint32_t last_anom = 0;
-  uint32_t range_shift = 0;  // extra bytes per range (retry after a failed speculation)
-  uint64_t retries = 0;
-  uint32_t max_rps = 0;      // most ranges in one stream (fast_verify_kernel's width)
-  bool deep_inline = false;  // fast_kernel<_, true>: overflow chunks handled inline
-  int smem_optin = 0;
-  // compose blocks (single pass)
-  uint32_t n_blk = 0;
-  std::vector<uint32_t> blk_stream, blk_u0, stream_blk0;
-  DBuf<uint32_t> d_blk_stream, d_blk_u0, d_stream_blk0;
-  DBuf<SegState> d_blk_state;
-};
-
-// counter slots in d_counters
-enum {
-  C_STATS = 0,            // 7 slots
-  C_LAST_TS = 8,
-  C_POOL_USED = 9,
-  C_STACK_USED = 10,
-  C_N_ORPHANS = 11,
-  C_N_ERRORS = 12,        // unsigned int in a u64 slot
-  C_WORK = 13,            // unsigned int
-  C_ARENA_USED = 14,
-  C_N_ROWS = 15,          // unsigned int
-  C_OVERFLOW = 16,        // unsigned int
-  C_WIDE = 17,            // unsigned int
-  C_WATCHDOG = 18,        // unsigned int
-  C_TL_N = 19,            // timeline messages appended
-  C_TL_TOTAL = 20,        // timeline body bytes (scan total)
-  C_TL_TH_OVF = 21,       // unsigned int: thread-name table overflow
-  C_DEEP_USED = 22,       // deep lane-stack chunks handed out
-  C_TL_N2 = 23,           // timeline messages appended by compose
-  C_REC_TOTAL = 24,       // records of all streams (timeline slots)
-  C_ANOM = 25,            // unsigned int: single-pass result void (fast.cuh)
-  C_NUM = 26
-};
-
-static int fail(hg_ctx* c, int code, const std::string& msg) {
-  if (c) c->err = msg;
-  return code;
-}
-
-#define CK(call)                                                                            \
-  do {                                                                                      \
-    cudaError_t e_ = (call);                                                                \
-    if (e_ != cudaSuccess) return fail(ctx, HG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-
-// json.dumps(str) with ensure_ascii (json/encoder.py) of a valid UTF-8 string
-static std::string json_quote(const std::string& s) {
-  static const char* hx = "0123456789abcdef";
-  std::string o = "\"";
-  auto u4 = [&](uint32_t v) {
-    o += "\\u";
-    o += hx[(v >> 12) & 15]; o += hx[(v >> 8) & 15]; o += hx[(v >> 4) & 15]; o += hx[v & 15];
-  };
-  for (size_t i = 0; i < s.size();) {
-    uint32_t c = (uint8_t)s[i], cp;
-    auto b = [&](size_t k) { return (uint32_t)(k < s.size() ? (uint8_t)s[k] : 0x80) & 0x3F; };
-    if (c < 0x80) { cp = c; i += 1; }
-    else if (c < 0xE0) { cp = ((c & 0x1F) << 6) | b(i + 1); i += 2; }
-    else if (c < 0xF0) { cp = ((c & 0x0F) << 12) | (b(i + 1) << 6) | b(i + 2); i += 3; }
-    else { cp = ((c & 0x07) << 18) | (b(i + 1) << 12) | (b(i + 2) << 6) | b(i + 3); i += 4; }
-    if (cp == '"') o += "\\\"";
-    else if (cp == '\\') o += "\\\\";
-    else if (cp >= 0x20 && cp < 0x7F) o += (char)cp;
-    else if (cp == '\n') o += "\\n";
-    else if (cp == '\r') o += "\\r";
-    else if (cp == '\t') o += "\\t";
-    else if (cp == '\b') o += "\\b";
-    else if (cp == '\f') o += "\\f";
-    else if (cp < 0x10000) u4(cp);
-    else { uint32_t v = cp - 0x10000; u4(0xD800 | (v >> 10)); u4(0xDC00 | (v & 0x3FF)); }
-  }
-  o += "\"";
-  return o;
-}
-
-template <class T>
-static cudaError_t upload(DBuf<T>& d, const std::vector<T>& h, cudaStream_t st) {
-  cudaError_t e = d.ensure(std::max<size_t>(h.size(), 1));
-  if (e != cudaSuccess || h.empty()) return e;
-  return cudaMemcpyAsync(d.ptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, st);
-}
-
-// order, format and store the timeline JSON (TimelineSink.on_finish, sinks.py:414-418)
-static int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
-  ctx->tl_ready = false;
-  if (!ctx->have_fn_names || ctx->fn_names.size() != ctx->n_fn)
-    return fail(ctx, HG_ESTATE, "hg_set_function_names is required for the timeline");
-  const unsigned long long* C = ctx->counters.data();
-  const uint64_t n_slots = ctx->tl_comp_base + C[C_TL_N2];
-  if (n_slots > ctx->tl_cap || n_slots >= (1ull << 32))
-    return fail(ctx, HG_ENOMEM, "timeline message buffer overflow");
-  const uint32_t n = (uint32_t)(C[C_TL_N] + C[C_TL_N2]);  // messages; the sort moves the empty slots last
-  const uint32_t N = (uint32_t)n_slots;
-  const uint32_t ns = (uint32_t)ctx->streams.size();
-  cudaStream_t st = ctx->stream;
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventRecord(e0, st));
-  // host tables: quoted function names; per stream pid, tid, process name
-  std::vector<char> fnq;
-  std::vector<uint64_t> fnq_off(1, 0);
-  for (uint32_t f = 0; f < ctx->n_fn; f++) {
-    std::string q = ctx->fn_null[f] ? std::string("null") : json_quote(ctx->fn_names[f]);
-    fnq.insert(fnq.end(), q.begin(), q.end());
-    fnq_off.push_back(fnq.size());
-  }
-  const int64_t dev_pid = 9000000 + (int64_t)ctx->cfg.timeline_device_index;
-  std::vector<char> sstr;
-  std::vector<uint64_t> sstr_off(1, 0);
-  std::vector<uint32_t> sproc(std::max<uint32_t>(ns, 1), 0);
-  std::map<int64_t, uint32_t> proc_id;  // process_name metas are keyed by (pid, 0)
-  for (uint32_t s = 0; s < ns; s++) {
-    const HostStream& hs = ctx->streams[s];
-    std::string a = std::to_string(hs.pid), b = std::to_string(hs.tid);
-    std::string c = json_quote("Host " + hs.host + " pid " + a);
-    for (const std::string* x : {&a, &b, &c}) {
-      sstr.insert(sstr.end(), x->begin(), x->end());
-      sstr_off.push_back(sstr.size());
-    }
-    auto it = proc_id.find(hs.pid);
-    if (it == proc_id.end()) it = proc_id.emplace(hs.pid, (uint32_t)proc_id.size()).first;
-    sproc[s] = it->second;
-  }
-  auto dit = proc_id.find(dev_pid);
-  const uint32_t dev_proc = dit != proc_id.end() ? dit->second : (uint32_t)proc_id.size();
-  const uint32_t n_proc = (uint32_t)proc_id.size() + 1;
-  std::string dps = std::to_string(dev_pid);
-  std::vector<char> devpid(dps.begin(), dps.end());
-  for (std::vector<char>* v : {&fnq, &sstr, &devpid}) v->insert(v->end(), 8, '\0');  // word-wise readers
-  CK(upload(ctx->d_tl_fnq, fnq, st));
-  CK(upload(ctx->d_tl_fnq_off, fnq_off, st));
-  CK(upload(ctx->d_tl_sstr, sstr, st));
-  CK(upload(ctx->d_tl_sstr_off, sstr_off, st));
-  CK(upload(ctx->d_tl_stream_proc, sproc, st));
-  CK(upload(ctx->d_tl_devpid, devpid, st));
-  // sort by mux key: the streams' record slots are sorted runs; drop the empty slots, sort
-  // compose's messages per tile, merge the runs pairwise
-  const uint32_t nrec_slots = (uint32_t)ctx->tl_comp_base;
-  const uint32_t ncomp = (uint32_t)C[C_TL_N2];
-  const uint32_t nrec = n - ncomp;
-  const uint32_t n_rtiles = (nrec_slots + kSortTile - 1) / kSortTile;
-  const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
-  uint32_t R = ns + ntc;
-  for (int k = 0; k < 2; k++) {
-    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
-    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
-    CK(ctx->d_tl_ro[k].ensure(R + 2));
-  }
-  CK(ctx->d_tl_tcnt.ensure(n_rtiles + 2));
-  CK(ctx->d_tl_tile0.ensure(R / 2 + 3));
-  CK(ctx->d_tl_split.ensure(n / kSortTile + R / 2 + 3));
-  int cur = 0;
-  if (n) {
-    if (n_rtiles) {
-      tl_count_kernel<<<n_rtiles, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, nrec_slots, ctx->d_tl_tcnt.ptr);
-      tl_small_scan_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_tcnt.ptr, n_rtiles);
-      ctx->launches += 2;
-    }
-    tl_compact_kernel<<<n_rtiles + std::max<uint32_t>(ntc, 1), kSortThreads, 0, st>>>(
-        ctx->d_tl_items.ptr, nrec_slots, (uint32_t)N, ctx->d_tl_tcnt.ptr, n_rtiles, ctx->d_tl_rec_off.ptr, ns, nrec, n,
-        ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, ctx->d_tl_ro[0].ptr);
-    ctx->launches++;
-    if (ntc) {
-      tl_tilesort_kernel<<<ntc, kSortThreads, 0, st>>>(ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, nrec, ncomp);
-      ctx->launches++;
-    }
-    CK(cudaGetLastError());
-    while (R > 1) {
-      const uint32_t P = (R + 1) / 2;
-      const uint32_t tiles = n / kSortTile + P + 1;  // bound on the output tiles of the pass
-      tl_pairs_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_ro[cur ^ 1].ptr);
-      tl_split_kernel<<<(tiles + 127) / 128, 128, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_ro[cur].ptr, R,
-                                                           ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
-      tl_merge_kernel<<<tiles, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
-                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr,
-                                                      ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
-      CK(cudaGetLastError());
-      ctx->launches += 3;
-      cur ^= 1;
-      R = P;
-    }
-  }
-  // metadata first occurrences
-  uint64_t n_dev = C[C_STATS + ST_DEVICE];
-  uint32_t th_size = 64;
-  while (th_size < 2 * n_dev && th_size < (1u << 30)) th_size <<= 1;
-  CK(ctx->d_tl_proc_first.ensure(n_proc));
-  CK(ctx->d_tl_th_state.ensure(th_size));
-  CK(ctx->d_tl_th_first.ensure(th_size));
-  CK(ctx->d_tl_th_hi.ensure(th_size));
-  CK(ctx->d_tl_th_lo.ensure(th_size));
-  CK(cudaMemsetAsync(ctx->d_tl_proc_first.ptr, 0xFF, n_proc * 4, st));
-  CK(cudaMemsetAsync(ctx->d_tl_th_state.ptr, 0, (size_t)th_size * 4, st));
-  CK(cudaMemsetAsync(ctx->d_tl_th_first.ptr, 0xFF, (size_t)th_size * 4, st));
-  CK(ctx->d_tl_lens.ensure(std::max<uint32_t>(n, 1)));
-  CK(ctx->d_tl_offs.ensure(std::max<uint32_t>(n, 1)));
-  const uint32_t nsb = (n + kScanBlock - 1) / kScanBlock;
-  CK(ctx->d_tl_bsum.ensure(std::max<uint32_t>(nsb, 1)));
-  TlTables T{};
-  T.items = ctx->d_tl_items.ptr;
-  T.n = n;
-  T.order = ctx->d_tl_idx[cur].ptr;
-  T.fnq = ctx->d_tl_fnq.ptr;
-  T.fnq_off = ctx->d_tl_fnq_off.ptr;
-  T.sstr = ctx->d_tl_sstr.ptr;
-  T.sstr_off = ctx->d_tl_sstr_off.ptr;
-  T.stream_proc = ctx->d_tl_stream_proc.ptr;
-  T.dev_proc = dev_proc;
-  T.dev_pid = ctx->d_tl_devpid.ptr;
-  T.dev_pid_len = (uint32_t)dps.size();
-  T.proc_first = ctx->d_tl_proc_first.ptr;
-  T.th_state = ctx->d_tl_th_state.ptr;
-  T.th_hi = ctx->d_tl_th_hi.ptr;
-  T.th_lo = ctx->d_tl_th_lo.ptr;
-  T.th_first = ctx->d_tl_th_first.ptr;
-  T.th_mask = th_size - 1;
-  T.th_overflow = reinterpret_cast<unsigned int*>(ctx->d_counters.ptr + C_TL_TH_OVF);
-  T.schemas = ctx->d_schemas.ptr;
-  T.sid_map = ctx->d_sid_map.ptr;
-  T.kinds = ctx->d_kinds.ptr;
-  T.max_sid = ctx->max_sid;
-  T.last_ts = global_last_ts;
-  T.lens = ctx->d_tl_lens.ptr;
-  T.offs = ctx->d_tl_offs.ptr;
-  uint64_t total = 0;
-  if (n) {
-    const uint32_t g = std::min<uint32_t>((n + 255) / 256, (uint32_t)ctx->sm_count * 16);
-    tl_len_kernel<<<g, 256, 0, st>>>(T);
-    tl_meta_len_kernel<<<std::min<uint32_t>((n_proc + th_size + 255) / 256, (uint32_t)ctx->sm_count * 8), 256, 0, st>>>(
-        T, n_proc, th_size);
-    tl_scan1_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr);
-    tl_scan2_kernel<<<1, kScanBlock, 0, st>>>(ctx->d_tl_bsum.ptr, nsb, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
-    tl_scan3_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr, T.offs);
-    CK(cudaGetLastError());
-    ctx->launches += 5;
-    unsigned long long tail[2] = {0, 0};
-    CK(cudaMemcpyAsync(tail, ctx->d_counters.ptr + C_TL_TOTAL, 16, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if ((uint32_t)tail[1]) return fail(ctx, HG_ENOMEM, "timeline thread-name table overflow");
-    total = tail[0];
-  }
-  // "[" + body + "\n]"  (json.dump of a non-empty list, indent=1); "[]" when empty
-  ctx->tl_size = n ? total + 3 : 2;
-  CK(ctx->d_tl_out.ensure(ctx->tl_size + 32));
-  T.out = ctx->d_tl_out.ptr;
-  static const char open_close[4] = {'[', '\n', ']', 0};
-  if (n) {
-    CK(cudaMemcpyAsync(T.out, open_close, 1, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(T.out + 1 + total, open_close + 1, 2, cudaMemcpyHostToDevice, st));
-    const uint32_t g = std::min<uint32_t>((n + kTlWarps * 32 - 1) / (kTlWarps * 32), (uint32_t)ctx->sm_count * 8);
-    tl_write_kernel<<<g, kTlWarps * 32, 0, st>>>(T);
-    CK(cudaGetLastError());
-    ctx->launches++;
-  } else {
-    static const char empty[2] = {'[', ']'};
-    CK(cudaMemcpyAsync(T.out, empty, 2, cudaMemcpyHostToDevice, st));
-  }
-  CK(cudaEventRecord(e1, st));
-  CK(cudaStreamSynchronize(st));
-  cudaEventElapsedTime(&ctx->tl_ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  ctx->tl_ready = true;
-  return HG_OK;
-}
+#include "ctx.h"
 
 extern "C" {
 
@@ -852,6 +453,7 @@ int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid, c
 
 int hg_clear_streams(hg_ctx* ctx) {
   if (!ctx) return HG_EARG;
+  ctx->flush_order = false;
   ctx->deep_inline = false;
   ctx->streams.clear();
   ctx->staged = false;
@@ -1061,7 +663,7 @@ static int ensure_scratch(hg_ctx* ctx, uint64_t n_records_bound) {
   return HG_OK;
 }
 
-static Params make_params(hg_ctx* ctx) {
+Params make_params(hg_ctx* ctx) {
   Params p{};
   p.data = ctx->d_data.ptr;
   p.stream_base = ctx->d_base.ptr;
@@ -1132,11 +734,12 @@ static Params make_params(hg_ctx* ctx) {
   p.vplan = ctx->d_vplan.ptr;
   p.fdesc = ctx->d_fdesc.ptr;
   p.dplan = ctx->d_dplan.ptr;
+  p.flush_rank = ctx->flush_order ? ctx->d_flush_rank.ptr : nullptr;
   return p;
 }
 
 // per-run resets shared by both phase-1 paths
-static int init_run(hg_ctx* ctx) {
+int init_run(hg_ctx* ctx) {
   const uint32_t ns = (uint32_t)ctx->streams.size();
   ctx->epoch++;
   if (ctx->epoch >= (1u << 29)) {
@@ -1151,83 +754,6 @@ static int init_run(hg_ctx* ctx) {
   init_acc_kernel<<<(nmax + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_host_acc.ptr, ctx->n_fn, ctx->d_dev_acc.ptr,
                                                                 ctx->row_cap);
   ctx->launches = 1;
-  return HG_OK;
-}
-
-// the single pass (fast.cuh): range kernel, chain verification, orphan index fix-up
-static int launch_fast(hg_ctx* ctx) {
-  const uint32_t ns = (uint32_t)ctx->streams.size();
-  int rc = init_run(ctx);
-  if (rc) return rc;
-  if (!ctx->n_ranges) return HG_OK;
-  Params p = make_params(ctx);
-  p.state = ctx->d_rseg.ptr;
-  const uint32_t nw = ctx->fast_warps;
-  const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
-  const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
-  auto kern = sd ? (ctx->deep_inline ? fast_kernel<true, true> : fast_kernel<true, false>)
-                 : (ctx->deep_inline ? fast_kernel<false, true> : fast_kernel<false, false>);
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const uint32_t per_cta = nw * kWarp;
-  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));
-  CK(ctx->d_params.ensure(1));
-  CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-  kern<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
-  CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
-  if (ctx->max_rps > 1024) fast_verify_kernel<512><<<ns, 512, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
-  else fast_verify_kernel<128><<<ns, 128, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
-  fast_orphan_fix_kernel<<<32, 256, 0, ctx->stream>>>(p);
-  CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev[5], ctx->stream));
-  ctx->launches += 3;
-  return HG_OK;
-}
-
-static int launch_phase1(hg_ctx* ctx) {
-  const uint32_t nt = (uint32_t)ctx->tile_stream.size();
-  const uint32_t ns = (uint32_t)ctx->streams.size();
-  int rc0 = init_run(ctx);
-  if (rc0) return rc0;
-  if (nt) {
-    Params p = make_params(ctx);
-    const size_t dsm = sizeof(uint2) * kSdescMax;
-    CK(cudaEventRecord(ctx->ev[4], ctx->stream));
-    const uint32_t gw = std::min<uint32_t>((nt + 255) / 256, (uint32_t)ctx->sm_count * 8);
-    seg_walk_kernel<<<gw, 256, dsm, ctx->stream>>>(p, ctx->d_segw.ptr);
-    CK(cudaEventRecord(ctx->ev[6], ctx->stream));
-    seg_chain_kernel<<<(ns + 3) / 4, 128, dsm, ctx->stream>>>(p, ctx->d_segw.ptr, ctx->d_seginfo.ptr, ctx->d_stream_nrec.ptr);
-    CK(cudaEventRecord(ctx->ev[7], ctx->stream));
-    CK(cudaGetLastError());
-    ctx->launches += 2;
-    if (ctx->want & HG_WANT_TIMELINE) {
-      // timeline slots: one per record (segment decode), then compose's messages
-      seg_rec_off_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_stream_nrec.ptr, ns, ctx->d_tl_rec_off.ptr,
-                                                      ctx->d_counters.ptr + C_REC_TOTAL);
-      ctx->launches++;
-      unsigned long long total = 0;
-      CK(cudaMemcpyAsync(&total, ctx->d_counters.ptr + C_REC_TOTAL, 8, cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      ctx->tl_comp_base = total;
-      ctx->tl_cap = 2 * total + 64;  // compose adds at most one message per summary entry
-      CK(ctx->d_tl_items.ensure(ctx->tl_cap));
-      p = make_params(ctx);
-    }
-    const size_t smem = seg_smem_layout(ctx->n_fn).total;
-    CK(cudaFuncSetAttribute(seg_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_decode_kernel, kSegThreads, smem));
-    if (per_sm < 1) return fail(ctx, HG_ECUDA, "segment kernel does not fit on an SM");
-    uint32_t grid = std::min<uint32_t>((uint32_t)(per_sm * ctx->sm_count), (nt + kSegThreads - 1) / kSegThreads);
-    grid = std::max<uint32_t>(grid, 1);
-    CK(ctx->d_params.ensure(1));
-    CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
-    seg_decode_kernel<<<grid, kSegThreads, smem, ctx->stream>>>(p, ctx->d_seginfo.ptr, ctx->d_params.ptr);
-    CK(cudaGetLastError());
-    CK(cudaEventRecord(ctx->ev[5], ctx->stream));
-    ctx->launches++;
-  }
   return HG_OK;
 }
 
@@ -1545,6 +1071,23 @@ int hg_phase_timing(hg_ctx* ctx, float* walk_ms, float* chain_ms, float* decode_
   if (walk_ms) *walk_ms = ctx->walk_ms;
   if (chain_ms) *chain_ms = ctx->chain_ms;
   if (decode_ms) *decode_ms = ctx->decode_ms;
+  return HG_OK;
+}
+
+int hg_set_flush_order(hg_ctx* ctx, const uint32_t* rank, uint32_t n) {
+  if (!ctx) return HG_EARG;
+  if (!rank || !n) { ctx->flush_order = false; return HG_OK; }
+  if (n != ctx->streams.size()) return fail(ctx, HG_EARG, "flush order: one rank per added stream");
+  std::vector<uint32_t> r(rank, rank + n), inv(n, ~0u);
+  for (uint32_t s = 0; s < n; s++) {
+    if (r[s] >= n || inv[r[s]] != ~0u) return fail(ctx, HG_EARG, "flush order is not a permutation");
+    inv[r[s]] = s;
+  }
+  cudaSetDevice(ctx->cfg.device);
+  CK(upload(ctx->d_flush_rank, r, ctx->stream));
+  CK(upload(ctx->d_flush_stream, inv, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  ctx->flush_order = true;
   return HG_OK;
 }
 

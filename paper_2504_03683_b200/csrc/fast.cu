@@ -1,0 +1,35 @@
+// fast.cu -- the single pass over HBM (fast.cuh): launch of the range kernel, chain verification, orphan fix-up
+#define HG_FAST_KERNELS
+#include "ctx.h"
+
+// the single pass (fast.cuh): range kernel, chain verification, orphan index fix-up
+int launch_fast(hg_ctx* ctx) {
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  int rc = init_run(ctx);
+  if (rc) return rc;
+  if (!ctx->n_ranges) return HG_OK;
+  Params p = make_params(ctx);
+  p.state = ctx->d_rseg.ptr;
+  const uint32_t nw = ctx->fast_warps;
+  const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
+  const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
+  auto kern = sd ? (ctx->deep_inline ? fast_kernel<true, true> : fast_kernel<true, false>)
+                 : (ctx->deep_inline ? fast_kernel<false, true> : fast_kernel<false, false>);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const uint32_t per_cta = nw * kWarp;
+  const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));
+  CK(ctx->d_params.ensure(1));
+  CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+  kern<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[7], ctx->stream));
+  if (ctx->max_rps > 1024) fast_verify_kernel<512><<<ns, 512, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
+  else fast_verify_kernel<128><<<ns, 128, 0, ctx->stream>>>(p, ctx->d_stream_nrec.ptr);
+  fast_orphan_fix_kernel<<<32, 256, 0, ctx->stream>>>(p);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[5], ctx->stream));
+  ctx->launches += 3;
+  return HG_OK;
+}
+

@@ -149,7 +149,7 @@ struct RLane {
 // single pass demands a longer chain than the segment walk (seg_walk_kernel: three).
 constexpr int kScanDepth = 8;
 
-__device__ __noinline__ uint64_t r_scan(const Params& p, const uint8_t* g, uint64_t size, uint64_t t0, uint64_t t1) {
+static __device__ __noinline__ uint64_t r_scan(const Params& p, const uint8_t* g, uint64_t size, uint64_t t0, uint64_t t1) {
   for (uint64_t o = t0; o < t1; o++) {
     uint64_t cur = o, nxt, ts, prev = 0;
     int k = 0;
@@ -261,7 +261,7 @@ __device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T)
 
 // close the lane's range and open its next one, out of line (rare; the lane state travels by value
 // so the hot loop keeps it in registers)
-__device__ __noinline__ RLane r_switch(const Params& p, RLane R, const RTabs T, uint32_t stride) {
+static __device__ __noinline__ RLane r_switch(const Params& p, RLane R, const RTabs T, uint32_t stride) {
   r_end(p, R, T);
   r_begin(p, R, R.r + stride, stride);
   return R;
@@ -429,7 +429,7 @@ __device__ __forceinline__ uint32_t r_name_probe(uint32_t nc_s, uint64_t h, cons
 
 // deferred records, one per lane, read from HBM (L2): device-profiling and telemetry
 // records (fold / range checks) and string payloads of inline records (UTF-8)
-__device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const uint64_t* q_off, const uint32_t* q_s,
+static __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const uint64_t* q_off, const uint32_t* q_s,
                                       uint32_t n, uint32_t nc_s) {
   uint2 K = make_uint2(0, 0);
   const uint32_t lane = lane_id();
@@ -514,7 +514,7 @@ __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, const ui
 constexpr int kRMaxThreads = 12 * kWarp;
 
 // strict UTF-8 of the one string field of inline records (tracefile.py:165), one per lane, from HBM
-__device__ __noinline__ void r_drain_str(const Params& p, const uint64_t* q_off, const uint32_t* q_s, uint32_t n) {
+static __device__ __noinline__ void r_drain_str(const Params& p, const uint64_t* q_off, const uint32_t* q_s, uint32_t n) {
   const uint32_t lane = lane_id();
   if (lane < n) {
     const uint64_t a = q_off[lane];
@@ -547,7 +547,7 @@ __device__ __forceinline__ void r_cp16(uint32_t dst, const void* src) {
 constexpr uint64_t kFCount = 1ull << 44;
 constexpr uint64_t kFLimit = (1ull << 43) | (1ull << 63);
 
-__device__ __noinline__ void r_fold_flush(const Params& p, uint32_t fn, uint64_t cs) {
+static __device__ __noinline__ void r_fold_flush(const Params& p, uint32_t fn, uint64_t cs) {
   unsigned long long* a = p.host_acc + 6ull * fn;
   atomicAdd(&a[0], (unsigned long long)(cs >> 44));
   add_i128(&a[2], &a[3], cs & (kFCount - 1), 0);
@@ -585,7 +585,7 @@ __device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uin
   __syncthreads();
 }
 
-__device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, const SegCounters K) {
+static __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, const SegCounters K) {
   const uint32_t lane = lane_id();
   const uint32_t a1 = __reduce_add_sync(0xffffffffu, K.passed), a2 = __reduce_add_sync(0xffffffffu, K.host),
                  a3 = __reduce_add_sync(0xffffffffu, K.dev), a4 = __reduce_add_sync(0xffffffffu, K.samples),
@@ -706,8 +706,6 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       const uint32_t pw = want ? 1u : 0u, pm = (want && q == 0) ? 1u : 0u;
       #pragma unroll
       for (uint32_t k = 0; k < kRChunk; k += 16) r_cp16p(dst + k, src + k, pw);
-      #pragma unroll
-      for (uint32_t k = 0; k < kRMirror; k += 16) r_cp16p(ring_s + kRRing + k, src + k, pm);
       (void)pm;
     }
     R.ci += want ? 1u : 0u;
@@ -952,6 +950,7 @@ __global__ void __launch_bounds__(kVThreads) fast_verify_kernel(Params p, unsign
 }
 
 // orphans found inside a range carry (range, index in range); make them stream indices
+#ifdef HG_FAST_KERNELS
 __global__ void fast_orphan_fix_kernel(Params p) {
   const unsigned long long n = min(*(volatile unsigned long long*)p.n_orphans, (unsigned long long)p.orphan_cap);
   for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -959,5 +958,6 @@ __global__ void fast_orphan_fix_kernel(Params p) {
     if (q >> 63) p.orphans[i].seq = p.range_base[(q >> 24) & ((1ull << 39) - 1)] + (q & 0xFFFFFFull);
   }
 }
+#endif  // HG_FAST_KERNELS
 
 }  // namespace hg

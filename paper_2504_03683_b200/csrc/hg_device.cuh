@@ -105,7 +105,7 @@ __device__ __forceinline__ uint8_t rd8(const Window& w, uint64_t off) {
 }
 
 // Strict UTF-8 (no overlongs, no surrogates, <= U+10FFFF).  Returns true if valid.
-__device__ __noinline__ bool utf8_valid(const Window& w, uint64_t p, uint32_t n) {
+static __device__ __noinline__ bool utf8_valid(const Window& w, uint64_t p, uint32_t n) {
   uint32_t i = 0;
   // ASCII fast path, 4 bytes at a time
   while (i + 4 <= n) {

@@ -109,6 +109,7 @@ struct Params {
   const uint32_t* vplan;           // per schema id: single-var-field payload plan (fast.cuh)
   const uint4* fdesc;              // per schema id (+ one sentinel): inline-record descriptor (fast.cuh)
   const uint4* dplan;              // per schema id: device-record layout for the drain (fast.cuh)
+  const uint32_t* flush_rank;      // stream -> rank in the truncation flush order (nullptr: stream order)
 };
 
 // compact descriptor: x = fn(20) | cls(3)<<20 | flags(8)<<23 ; y = fixed_len(16) | result field index(8)<<16 | counter(8)<<24
@@ -137,7 +138,7 @@ __device__ __forceinline__ const DSchema* schema_of(const Params& p, uint32_t si
 // ---------------------------------------------------------------------------
 // error / orphan sinks
 
-__device__ __noinline__ void push_error(const Params& p, uint32_t code, uint32_t stream, uint64_t seq, uint64_t off, uint64_t ts,
+static __device__ __noinline__ void push_error(const Params& p, uint32_t code, uint32_t stream, uint64_t seq, uint64_t off, uint64_t ts,
                            uint64_t prev_ts, uint64_t aux) {
   unsigned int i = atomicAdd(p.n_errors, 1u);
   if (i < p.error_cap) {
@@ -147,7 +148,7 @@ __device__ __noinline__ void push_error(const Params& p, uint32_t code, uint32_t
   }
 }
 
-__device__ __noinline__ void push_orphan(const Params& p, uint32_t stream, int32_t fn, uint64_t ts, uint64_t seq) {
+static __device__ __noinline__ void push_orphan(const Params& p, uint32_t stream, int32_t fn, uint64_t ts, uint64_t seq) {
   unsigned long long i = atomicAdd(p.n_orphans, 1ull);
   if (i < p.orphan_cap) { hg_orphan o; o.stream = stream; o.function = fn; o.ts = ts; o.seq = seq; p.orphans[i] = o; }
 }
@@ -163,7 +164,7 @@ struct LaneTab {
   uint32_t* err; uint32_t* mn; uint32_t* mx;     // [fn]
 };
 
-__device__ __noinline__ void fold_host_global(const Params& p, int32_t fn, uint64_t dur, bool err) {
+static __device__ __noinline__ void fold_host_global(const Params& p, int32_t fn, uint64_t dur, bool err) {
   unsigned long long* a = p.host_acc + 6ull * fn;
   atomicAdd(&a[0], 1ull);
   if (err) atomicAdd(&a[1], 1ull);
@@ -211,7 +212,7 @@ struct HostFold {
 };
 
 // device rows: CTA cache keyed by the global row id, global atomics on a miss
-__device__ __noinline__ void fold_device_global(const Params& p, uint32_t row, uint64_t d_lo, int64_t d_hi) {
+static __device__ __noinline__ void fold_device_global(const Params& p, uint32_t row, uint64_t d_lo, int64_t d_hi) {
   unsigned long long* a = p.dev_acc + 6ull * row;
   atomicAdd(&a[0], 1ull);
   add_i128(&a[2], &a[3], d_lo, d_hi);
@@ -271,7 +272,7 @@ struct RoundOut {
   uint32_t top;
 };
 
-__device__ __noinline__ RoundOut round_resolve(GStack st, bool allow_pending, bool isE, bool isX, int32_t fn,
+static __device__ __noinline__ RoundOut round_resolve(GStack st, bool allow_pending, bool isE, bool isX, int32_t fn,
                                                uint64_t ts, SumEntry mine) {
   const uint32_t lane = lane_id();
   bool paired = false, orphan = false;
@@ -336,7 +337,7 @@ __device__ __noinline__ RoundOut round_resolve(GStack st, bool allow_pending, bo
 
 // append one timeline message per lane with `on` (warp-aggregated slot claim);
 // called by all 32 lanes
-__device__ __noinline__ void tl_emit(const Params& p, bool on, uint64_t khi, uint64_t klo, uint64_t a, uint64_t b,
+static __device__ __noinline__ void tl_emit(const Params& p, bool on, uint64_t khi, uint64_t klo, uint64_t a, uint64_t b,
                                      uint32_t kind, uint32_t x) {
   const uint32_t m = __ballot_sync(0xffffffffu, on);
   if (!m) return;
@@ -357,7 +358,7 @@ __device__ __noinline__ void tl_emit(const Params& p, bool on, uint64_t khi, uin
 // variable-payload field walk (tracefile.py:152-169); returns 0 or an HG_ERR_* code.
 // role_off receives stream offsets of role fields, name_len the name string length.
 template <class RD32>
-__device__ __noinline__ uint32_t walk_fields(const Params& p, uint2 d, uint32_t sid, uint64_t body, uint32_t plen,
+static __device__ __noinline__ uint32_t walk_fields(const Params& p, uint2 d, uint32_t sid, uint64_t body, uint32_t plen,
                                                 RD32 rd, const Window& w, uint64_t* role_off, uint32_t& name_len,
                                                 uint64_t& aux) {
   const DSchema* s = schema_of(p, sid);

@@ -119,7 +119,7 @@ __device__ __forceinline__ bool seg_plausible(const Params& p, const uint8_t* g,
 }
 
 // walk the chain from `entry` while records start before t1 (tracefile.py:198-210 header checks)
-__device__ __noinline__ SegW seg_walk_from(const Params& p, const uint8_t* g, uint64_t size, uint64_t entry, uint64_t t1) {
+static __device__ __noinline__ SegW seg_walk_from(const Params& p, const uint8_t* g, uint64_t size, uint64_t entry, uint64_t t1) {
   SegW W;
   W.spec_entry = entry;
   W.n = 0;
@@ -148,6 +148,7 @@ __device__ __forceinline__ void seg_load_desc(const Params& p) {
   __syncthreads();
 }
 
+#ifdef HG_SEG_KERNELS
 __global__ void __launch_bounds__(256) seg_walk_kernel(Params p, SegW* segw) {
   seg_load_desc(p);
   for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < p.n_tiles; g += gridDim.x * blockDim.x) {
@@ -177,10 +178,12 @@ __global__ void __launch_bounds__(256) seg_walk_kernel(Params p, SegW* segw) {
     segw[g] = W;
   }
 }
+#endif  // HG_SEG_KERNELS
 
 // ---------------------------------------------------------------------------
 // chain: warp per stream
 
+#ifdef HG_SEG_KERNELS
 __global__ void __launch_bounds__(128) seg_chain_kernel(Params p, SegW* segw, SegInfo* info, unsigned long long* stream_nrec) {
   seg_load_desc(p);
   const uint32_t lane = lane_id();
@@ -280,6 +283,7 @@ __global__ void __launch_bounds__(128) seg_chain_kernel(Params p, SegW* segw, Se
     if (c_has) atomicMax(p.last_ts, (unsigned long long)c_last);
   }
 }
+#endif  // HG_SEG_KERNELS
 
 // ---------------------------------------------------------------------------
 // decode + pair + tally: thread per segment, warp-convergent loop
@@ -429,7 +433,7 @@ struct LaneSeg {
 
 // ---- strict UTF-8 / hashing / comparison on HBM bytes
 
-__device__ __noinline__ bool g_utf8_slow(const uint8_t* g, uint64_t o, uint32_t n) {
+static __device__ __noinline__ bool g_utf8_slow(const uint8_t* g, uint64_t o, uint32_t n) {
   uint32_t i = 0;
   while (i < n) {
     const uint32_t c = g32(g, o + i) & 0xffu;
@@ -489,7 +493,7 @@ __device__ __forceinline__ bool g_name_equal(const NameDict& d, uint32_t row, co
 }
 
 // device-name dictionary lookup/insert (same layout, hash and probing as name_lookup)
-__device__ __noinline__ uint32_t g_name_lookup(const NameDict& d, const uint8_t* g, uint64_t o, uint32_t n, uint64_t h) {
+static __device__ __noinline__ uint32_t g_name_lookup(const NameDict& d, const uint8_t* g, uint64_t o, uint32_t n, uint64_t h) {
   for (uint64_t slot = h & d.mask, probes = 0; probes <= d.mask; slot = (slot + 1) & d.mask, probes++) {
     // a plain read first: names already in the dictionary cost no atomic (hot names are shared by
     // every SM, so an atomicCAS per lookup would serialise on a few L2 lines)
@@ -555,7 +559,7 @@ __device__ __forceinline__ bool g_var_plan(const DSchema* sc, const uint8_t* g, 
 // payload validation + role field locations of one record (var records: plan or
 // generic walk).  role_ptr: field data (var fields: first byte after the length);
 // role_len: var field lengths.
-__device__ __noinline__ uint32_t seg_fields(const Params& p, const uint8_t* g, uint64_t size, uint64_t a, uint32_t sid,
+static __device__ __noinline__ uint32_t seg_fields(const Params& p, const uint8_t* g, uint64_t size, uint64_t a, uint32_t sid,
                                            uint32_t plen, uint64_t* role_ptr, uint32_t* role_len, uint64_t& aux,
                                            uint32_t roles) {
   // roles: bit mask of the HG_ROLE_* fields wanted (their schemas have them)
@@ -591,7 +595,7 @@ __device__ __noinline__ uint32_t seg_fields(const Params& p, const uint8_t* g, u
 }
 
 // device-profiling record (pipeline.py:186-202): duration into its name's row
-__device__ __noinline__ uint32_t seg_device(const Params& p, const SegSmem L, const uint8_t* g, uint64_t size,
+static __device__ __noinline__ uint32_t seg_device(const Params& p, const SegSmem L, const uint8_t* g, uint64_t size,
                                            uint32_t sid, const uint64_t* rp, const uint32_t* rl, uint64_t& aux) {
   const uint2 d = desc_of(p, sid);
   if (d_flags(d) & SF_FEED_ALWAYS) { aux = sid; return HG_ERR_FEED; }
@@ -621,7 +625,7 @@ __device__ __noinline__ uint32_t seg_device(const Params& p, const SegSmem L, co
 }
 
 // telemetry sample checks (pipeline.py:203-215; sampler.py:44-48)
-__device__ __noinline__ uint32_t seg_telemetry(const Params& p, const uint8_t* g, uint32_t sid, const uint64_t* rp,
+static __device__ __noinline__ uint32_t seg_telemetry(const Params& p, const uint8_t* g, uint32_t sid, const uint64_t* rp,
                                               uint64_t& aux) {
   const uint2 d = desc_of(p, sid);
   const uint32_t fl = d_flags(d);
@@ -666,7 +670,7 @@ __device__ __forceinline__ void seg_status(const Params& p, uint32_t g, uint32_t
 // drain n deferred records, one per lane
 // payload validation of variable records (tracefile.py:152-169); the exact error
 // (and the ordering error it takes precedence over) comes from the full walk
-__device__ __noinline__ void seg_drain_v(const Params& p, const SegSmem L, uint32_t n) {
+static __device__ __noinline__ void seg_drain_v(const Params& p, const SegSmem L, uint32_t n) {
   const SegQ Q = seg_queue(L, 0);
   const uint32_t lane = lane_id();
   if (lane < n) {
@@ -689,7 +693,7 @@ __device__ __noinline__ void seg_drain_v(const Params& p, const SegSmem L, uint3
 }
 
 // device-profiling / telemetry records and ordering-failed variable records
-__device__ __noinline__ uint4 seg_drain(const Params& p, const SegSmem L, uint32_t n) {
+static __device__ __noinline__ uint4 seg_drain(const Params& p, const SegSmem L, uint32_t n) {
   uint4 K = make_uint4(0, 0, 0, 0);  // device spans, samples, timeline messages
   const SegQ Q = seg_queue(L, 1);
   const uint32_t lane = lane_id();
@@ -800,7 +804,7 @@ __device__ __forceinline__ void seg_end(const Params& p, LaneSeg& C, LaneStack& 
 }
 
 // result offset of a variable-payload exit whose result follows a string/blob (rare)
-__device__ __noinline__ uint64_t var_result_off(const Params& p, const uint8_t* g, uint64_t size, uint64_t a, uint32_t sid,
+static __device__ __noinline__ uint64_t var_result_off(const Params& p, const uint8_t* g, uint64_t size, uint64_t a, uint32_t sid,
                                                uint32_t plen) {
   uint64_t rp[HG_NUM_ROLES];
   uint32_t rl[HG_NUM_ROLES];
@@ -809,7 +813,7 @@ __device__ __noinline__ uint64_t var_result_off(const Params& p, const uint8_t* 
   return rp[HG_ROLE_RESULT];
 }
 
-__device__ __noinline__ void seg_prologue(const Params& p, const SegSmem L) {
+static __device__ __noinline__ void seg_prologue(const Params& p, const SegSmem L) {
   const uint32_t lane = lane_id();
   if (p.max_sid < (uint32_t)kSdescMax) {
     uint2* t = reinterpret_cast<uint2*>(g_smem);
@@ -837,7 +841,7 @@ __device__ __noinline__ void seg_prologue(const Params& p, const SegSmem L) {
   __syncthreads();
 }
 
-__device__ __noinline__ void seg_epilogue(const Params& p, const SegSmem L, const SegCounters K) {
+static __device__ __noinline__ void seg_epilogue(const Params& p, const SegSmem L, const SegCounters K) {
   const uint32_t lane = lane_id();
   auto wsum = [](uint32_t v) { return __reduce_add_sync(0xffffffffu, v); };
   // events and the last timestamp come from the chain (every record of an error-free run is decoded)
@@ -1021,6 +1025,7 @@ __device__ __forceinline__ uint32_t seg_record_full(const Params& p, LaneSeg& C,
   return defer;
 }
 
+#ifdef HG_SEG_KERNELS
 __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, const SegInfo* info, const Params* gp) {
   // noinline helpers read the parameters from a global copy: taking the address of the
   // kernel parameter block would move every hot-loop parameter read to local memory
@@ -1187,8 +1192,10 @@ __global__ void __launch_bounds__(kSegThreads, 3) seg_decode_kernel(Params p, co
   }
   seg_epilogue(gpr, L, K);
 }
+#endif  // HG_SEG_KERNELS
 
 // exclusive scan of per-stream record totals -> timeline slot offset of each stream
+#ifdef HG_SEG_KERNELS
 __global__ void __launch_bounds__(1024) seg_rec_off_kernel(const unsigned long long* stream_nrec, uint32_t n,
                                                            unsigned long long* off, unsigned long long* total) {
   unsigned long long carry = 0;
@@ -1202,5 +1209,6 @@ __global__ void __launch_bounds__(1024) seg_rec_off_kernel(const unsigned long l
   }
   if (threadIdx.x == 0) *total = carry;
 }
+#endif  // HG_SEG_KERNELS
 
 }  // namespace hg

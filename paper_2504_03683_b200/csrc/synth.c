@@ -22,13 +22,16 @@ typedef struct synth_params {
   uint64_t seed;
   uint64_t n_events;
   uint32_t max_depth;
-  uint32_t gap_lo, gap_hi;
+  uint32_t pad0;
+  uint64_t gap_lo, gap_hi;
   uint64_t ts0_hi;
   double push_p, err_p, prof_p, meta_p, orphan_p, mismatch_p;
   double zipf_s;
   uint32_t n_layers;
   int32_t close_at_end;
   int32_t meta_sid;
+  uint64_t dev_off_hi;       /* device span start = record ts + U[0, dev_off_hi]          */
+  int64_t dev_lo, dev_hi;    /* device span duration U[dev_lo, dev_hi] (negative: end < start) */
 } synth_params;
 
 typedef struct synth_fn {
@@ -201,7 +204,9 @@ int synth_stream(const synth_params* P, const hg_schema* by_id, uint32_t n_ids, 
       emit(&k, &r, &G, fns[fi].exit_sid, ts, res, 0, 0, "", 0);
       if (fns[fi].prof_sid >= 0 && unif(&r) < P->prof_p && k.events < P->n_events) {
         ts += range(&r, P->gap_lo, P->gap_hi);
-        uint64_t st = ts + range(&r, 0, 10000), en = st + range(&r, 1000, 100000);
+        uint64_t st = ts + range(&r, 0, P->dev_off_hi);
+        int64_t dur = P->dev_lo + (int64_t)range(&r, 0, (uint64_t)(P->dev_hi - P->dev_lo));
+        uint64_t en = st + (uint64_t)dur;
         const char* nm;
         int mc = fns[fi].memcpy;
         if (mc) nm = MEMCPY_TAGS[next64(&r) & 3];

@@ -1,0 +1,190 @@
+// timeline.cu -- timeline ordering and JSON formatting on the GPU (timeline.cuh)
+#define HG_TL_KERNELS
+#include "ctx.h"
+
+// order, format and store the timeline JSON (TimelineSink.on_finish, sinks.py:414-418)
+int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
+  ctx->tl_ready = false;
+  if (!ctx->have_fn_names || ctx->fn_names.size() != ctx->n_fn)
+    return fail(ctx, HG_ESTATE, "hg_set_function_names is required for the timeline");
+  const unsigned long long* C = ctx->counters.data();
+  const uint64_t n_slots = ctx->tl_comp_base + C[C_TL_N2];
+  if (n_slots > ctx->tl_cap || n_slots >= (1ull << 32))
+    return fail(ctx, HG_ENOMEM, "timeline message buffer overflow");
+  const uint32_t n = (uint32_t)(C[C_TL_N] + C[C_TL_N2]);  // messages; the sort moves the empty slots last
+  const uint32_t N = (uint32_t)n_slots;
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  cudaStream_t st = ctx->stream;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, st));
+  // host tables: quoted function names; per stream pid, tid, process name
+  std::vector<char> fnq;
+  std::vector<uint64_t> fnq_off(1, 0);
+  for (uint32_t f = 0; f < ctx->n_fn; f++) {
+    std::string q = ctx->fn_null[f] ? std::string("null") : json_quote(ctx->fn_names[f]);
+    fnq.insert(fnq.end(), q.begin(), q.end());
+    fnq_off.push_back(fnq.size());
+  }
+  const int64_t dev_pid = 9000000 + (int64_t)ctx->cfg.timeline_device_index;
+  std::vector<char> sstr;
+  std::vector<uint64_t> sstr_off(1, 0);
+  std::vector<uint32_t> sproc(std::max<uint32_t>(ns, 1), 0);
+  std::map<int64_t, uint32_t> proc_id;  // process_name metas are keyed by (pid, 0)
+  for (uint32_t s = 0; s < ns; s++) {
+    const HostStream& hs = ctx->streams[s];
+    std::string a = std::to_string(hs.pid), b = std::to_string(hs.tid);
+    std::string c = json_quote("Host " + hs.host + " pid " + a);
+    for (const std::string* x : {&a, &b, &c}) {
+      sstr.insert(sstr.end(), x->begin(), x->end());
+      sstr_off.push_back(sstr.size());
+    }
+    auto it = proc_id.find(hs.pid);
+    if (it == proc_id.end()) it = proc_id.emplace(hs.pid, (uint32_t)proc_id.size()).first;
+    sproc[s] = it->second;
+  }
+  auto dit = proc_id.find(dev_pid);
+  const uint32_t dev_proc = dit != proc_id.end() ? dit->second : (uint32_t)proc_id.size();
+  const uint32_t n_proc = (uint32_t)proc_id.size() + 1;
+  std::string dps = std::to_string(dev_pid);
+  std::vector<char> devpid(dps.begin(), dps.end());
+  for (std::vector<char>* v : {&fnq, &sstr, &devpid}) v->insert(v->end(), 8, '\0');  // word-wise readers
+  CK(upload(ctx->d_tl_fnq, fnq, st));
+  CK(upload(ctx->d_tl_fnq_off, fnq_off, st));
+  CK(upload(ctx->d_tl_sstr, sstr, st));
+  CK(upload(ctx->d_tl_sstr_off, sstr_off, st));
+  CK(upload(ctx->d_tl_stream_proc, sproc, st));
+  CK(upload(ctx->d_tl_devpid, devpid, st));
+  // sort by mux key: the streams' record slots are sorted runs; drop the empty slots, sort
+  // compose's messages per tile, merge the runs pairwise
+  const uint32_t nrec_slots = (uint32_t)ctx->tl_comp_base;
+  const uint32_t ncomp = (uint32_t)C[C_TL_N2];
+  const uint32_t nrec = n - ncomp;
+  const uint32_t n_rtiles = (nrec_slots + kSortTile - 1) / kSortTile;
+  const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
+  uint32_t R = ns + ntc;
+  for (int k = 0; k < 2; k++) {
+    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_ro[k].ensure(R + 2));
+  }
+  CK(ctx->d_tl_tcnt.ensure(n_rtiles + 2));
+  CK(ctx->d_tl_tile0.ensure(R / 2 + 3));
+  CK(ctx->d_tl_split.ensure(n / kSortTile + R / 2 + 3));
+  int cur = 0;
+  if (n) {
+    if (n_rtiles) {
+      tl_count_kernel<<<n_rtiles, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, nrec_slots, ctx->d_tl_tcnt.ptr);
+      tl_small_scan_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_tcnt.ptr, n_rtiles);
+      ctx->launches += 2;
+    }
+    tl_compact_kernel<<<n_rtiles + std::max<uint32_t>(ntc, 1), kSortThreads, 0, st>>>(
+        ctx->d_tl_items.ptr, nrec_slots, (uint32_t)N, ctx->d_tl_tcnt.ptr, n_rtiles, ctx->d_tl_rec_off.ptr, ns, nrec, n,
+        ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, ctx->d_tl_ro[0].ptr);
+    ctx->launches++;
+    if (ntc) {
+      tl_tilesort_kernel<<<ntc, kSortThreads, 0, st>>>(ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, nrec, ncomp);
+      ctx->launches++;
+    }
+    CK(cudaGetLastError());
+    while (R > 1) {
+      const uint32_t P = (R + 1) / 2;
+      const uint32_t tiles = n / kSortTile + P + 1;  // bound on the output tiles of the pass
+      tl_pairs_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_ro[cur ^ 1].ptr);
+      tl_split_kernel<<<(tiles + 127) / 128, 128, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_ro[cur].ptr, R,
+                                                           ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
+      tl_merge_kernel<<<tiles, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
+                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr,
+                                                      ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
+      CK(cudaGetLastError());
+      ctx->launches += 3;
+      cur ^= 1;
+      R = P;
+    }
+  }
+  // metadata first occurrences
+  uint64_t n_dev = C[C_STATS + ST_DEVICE];
+  uint32_t th_size = 64;
+  while (th_size < 2 * n_dev && th_size < (1u << 30)) th_size <<= 1;
+  CK(ctx->d_tl_proc_first.ensure(n_proc));
+  CK(ctx->d_tl_th_state.ensure(th_size));
+  CK(ctx->d_tl_th_first.ensure(th_size));
+  CK(ctx->d_tl_th_hi.ensure(th_size));
+  CK(ctx->d_tl_th_lo.ensure(th_size));
+  CK(cudaMemsetAsync(ctx->d_tl_proc_first.ptr, 0xFF, n_proc * 4, st));
+  CK(cudaMemsetAsync(ctx->d_tl_th_state.ptr, 0, (size_t)th_size * 4, st));
+  CK(cudaMemsetAsync(ctx->d_tl_th_first.ptr, 0xFF, (size_t)th_size * 4, st));
+  CK(ctx->d_tl_lens.ensure(std::max<uint32_t>(n, 1)));
+  CK(ctx->d_tl_offs.ensure(std::max<uint32_t>(n, 1)));
+  const uint32_t nsb = (n + kScanBlock - 1) / kScanBlock;
+  CK(ctx->d_tl_bsum.ensure(std::max<uint32_t>(nsb, 1)));
+  TlTables T{};
+  T.items = ctx->d_tl_items.ptr;
+  T.n = n;
+  T.order = ctx->d_tl_idx[cur].ptr;
+  T.fnq = ctx->d_tl_fnq.ptr;
+  T.fnq_off = ctx->d_tl_fnq_off.ptr;
+  T.sstr = ctx->d_tl_sstr.ptr;
+  T.sstr_off = ctx->d_tl_sstr_off.ptr;
+  T.stream_proc = ctx->d_tl_stream_proc.ptr;
+  T.dev_proc = dev_proc;
+  T.dev_pid = ctx->d_tl_devpid.ptr;
+  T.dev_pid_len = (uint32_t)dps.size();
+  T.proc_first = ctx->d_tl_proc_first.ptr;
+  T.th_state = ctx->d_tl_th_state.ptr;
+  T.th_hi = ctx->d_tl_th_hi.ptr;
+  T.th_lo = ctx->d_tl_th_lo.ptr;
+  T.th_first = ctx->d_tl_th_first.ptr;
+  T.th_mask = th_size - 1;
+  T.th_overflow = reinterpret_cast<unsigned int*>(ctx->d_counters.ptr + C_TL_TH_OVF);
+  T.schemas = ctx->d_schemas.ptr;
+  T.sid_map = ctx->d_sid_map.ptr;
+  T.kinds = ctx->d_kinds.ptr;
+  T.max_sid = ctx->max_sid;
+  T.last_ts = global_last_ts;
+  T.flush_stream = ctx->flush_order ? ctx->d_flush_stream.ptr : nullptr;
+  T.lens = ctx->d_tl_lens.ptr;
+  T.offs = ctx->d_tl_offs.ptr;
+  uint64_t total = 0;
+  if (n) {
+    const uint32_t g = std::min<uint32_t>((n + 255) / 256, (uint32_t)ctx->sm_count * 16);
+    tl_len_kernel<<<g, 256, 0, st>>>(T);
+    tl_meta_len_kernel<<<std::min<uint32_t>((n_proc + th_size + 255) / 256, (uint32_t)ctx->sm_count * 8), 256, 0, st>>>(
+        T, n_proc, th_size);
+    tl_scan1_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr);
+    tl_scan2_kernel<<<1, kScanBlock, 0, st>>>(ctx->d_tl_bsum.ptr, nsb, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
+    tl_scan3_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr, T.offs);
+    CK(cudaGetLastError());
+    ctx->launches += 5;
+    unsigned long long tail[2] = {0, 0};
+    CK(cudaMemcpyAsync(tail, ctx->d_counters.ptr + C_TL_TOTAL, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if ((uint32_t)tail[1]) return fail(ctx, HG_ENOMEM, "timeline thread-name table overflow");
+    total = tail[0];
+  }
+  // "[" + body + "\n]"  (json.dump of a non-empty list, indent=1); "[]" when empty
+  ctx->tl_size = n ? total + 3 : 2;
+  CK(ctx->d_tl_out.ensure(ctx->tl_size + 32));
+  T.out = ctx->d_tl_out.ptr;
+  static const char open_close[4] = {'[', '\n', ']', 0};
+  if (n) {
+    CK(cudaMemcpyAsync(T.out, open_close, 1, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(T.out + 1 + total, open_close + 1, 2, cudaMemcpyHostToDevice, st));
+    const uint32_t g = std::min<uint32_t>((n + kTlWarps * 32 - 1) / (kTlWarps * 32), (uint32_t)ctx->sm_count * 8);
+    tl_write_kernel<<<g, kTlWarps * 32, 0, st>>>(T);
+    CK(cudaGetLastError());
+    ctx->launches++;
+  } else {
+    static const char empty[2] = {'[', ']'};
+    CK(cudaMemcpyAsync(T.out, empty, 2, cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaEventRecord(e1, st));
+  CK(cudaStreamSynchronize(st));
+  cudaEventElapsedTime(&ctx->tl_ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->tl_ready = true;
+  return HG_OK;
+}
+

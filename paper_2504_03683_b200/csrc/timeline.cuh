@@ -49,6 +49,7 @@ struct TlTables {
   const uint8_t* kinds;
   uint32_t max_sid;
   uint64_t last_ts;               // global last timestamp: end of truncated spans
+  const uint32_t* flush_stream;   // truncated items carry their flush rank: rank -> stream (nullptr: identity)
   uint32_t* lens;
   uint64_t* offs;
   char* out;                      // output buffer; item text starts at 1 + offs[i]
@@ -172,7 +173,7 @@ struct TlFields {
   uint32_t len[HG_NUM_ROLES];
 };
 
-__device__ __noinline__ void tl_locate(const TlTables& T, const DSchema* sc, const uint8_t* pay, TlFields& F) {
+static __device__ __noinline__ void tl_locate(const TlTables& T, const DSchema* sc, const uint8_t* pay, TlFields& F) {
   for (int r = 0; r < HG_NUM_ROLES; r++) { F.at[r] = nullptr; F.len[r] = 0; }
   if (sc->nvar != kNoPlan) {  // payload plan: variable-field starts, then every role at its segment + delta
     uint32_t seg[5];
@@ -281,7 +282,7 @@ __device__ __forceinline__ I128 dev_tid(I128 tile, I128 engine) {
 }
 
 // thread_name meta table (keyed by tid)
-__device__ __noinline__ int th_slot(const TlTables& T, I128 tid, bool insert) {
+static __device__ __noinline__ int th_slot(const TlTables& T, I128 tid, bool insert) {
   uint64_t h = (tid.lo * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)tid.hi * 0xC2B2AE3D27D4EB4Full);
   h ^= h >> 29;
   for (uint32_t probe = 0, slot = (uint32_t)h & T.th_mask; probe <= T.th_mask; probe++, slot = (slot + 1) & T.th_mask) {
@@ -334,6 +335,7 @@ __device__ __forceinline__ bool key_lt(ulonglong2 a, ulonglong2 b) { return a.x 
 // reference's muxer (heapq.merge over the streams) as log2(streams) merge-path passes.
 
 // messages per tile of the record region (empty slots: key ~0)
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kSortThreads) tl_count_kernel(const TlItem* items, uint32_t nrec, uint32_t* tcnt) {
   __shared__ uint32_t wsum[kSortThreads / 32];
   const uint64_t base = (uint64_t)blockIdx.x * kSortTile;
@@ -351,6 +353,7 @@ __global__ void __launch_bounds__(kSortThreads) tl_count_kernel(const TlItem* it
     tcnt[blockIdx.x] = s;
   }
 }
+#endif  // HG_TL_KERNELS
 
 // exclusive scan of n counts in place by one 1024-thread CTA (all threads call it); a[n] = total
 __device__ __forceinline__ void cta_excl_scan(uint32_t* a, uint32_t n) {
@@ -388,10 +391,13 @@ __device__ __forceinline__ void cta_excl_scan(uint32_t* a, uint32_t n) {
   if (threadIdx.x == 0) a[n] = carry;
 }
 
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(1024) tl_small_scan_kernel(uint32_t* a, uint32_t n) { cta_excl_scan(a, n); }
+#endif  // HG_TL_KERNELS
 
 // drop the empty slots: keys + item index of every message, record region then compose's
 // messages; run_off[s] = first message of stream s, then one run per compose tile, run_off[R] = n
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kSortThreads) tl_compact_kernel(const TlItem* items, uint32_t nrec_slots, uint32_t n_slots,
                                                                   const uint32_t* tpre, uint32_t n_rtiles,
                                                                   const unsigned long long* rec_off, uint32_t ns,
@@ -473,8 +479,10 @@ __global__ void __launch_bounds__(kSortThreads) tl_compact_kernel(const TlItem* 
     }
   }
 }
+#endif  // HG_TL_KERNELS
 
 // one compose tile sorted in place (bitonic, 2048 keys); the last tile is padded with ~0 keys
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kSortThreads) tl_tilesort_kernel(ulonglong2* keys, uint32_t* idx, uint32_t base,
                                                                    uint32_t count) {
   __shared__ ulonglong2 sk[kSortTile];
@@ -508,6 +516,7 @@ __global__ void __launch_bounds__(kSortThreads) tl_tilesort_kernel(ulonglong2* k
     if (g < end) { keys[g] = sk[t]; idx[g] = si[t]; }
   }
 }
+#endif  // HG_TL_KERNELS
 
 // merge-path co-rank: how many of the first k merged elements come from A
 template <class F, class G>
@@ -523,6 +532,7 @@ __device__ __forceinline__ uint64_t corank(uint64_t k, uint64_t na, uint64_t nb,
 
 // one merge pass over R runs: pair p = runs 2p, 2p+1 (the last may be alone); output tiles of
 // kSortTile per pair, tile0[p] = first tile of pair p (exclusive scan), nro = the merged runs
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(1024) tl_pairs_kernel(const uint32_t* ro, uint32_t R, uint32_t* tile0, uint32_t* nro) {
   const uint32_t P = (R + 1) / 2;
   for (uint32_t p = threadIdx.x; p < P; p += blockDim.x) {
@@ -534,8 +544,10 @@ __global__ void __launch_bounds__(1024) tl_pairs_kernel(const uint32_t* ro, uint
   __syncthreads();
   cta_excl_scan(tile0, P);
 }
+#endif  // HG_TL_KERNELS
 
 // co-rank of every output tile's first element within its pair
+#ifdef HG_TL_KERNELS
 __global__ void tl_split_kernel(const ulonglong2* ki, const uint32_t* ro, uint32_t R, const uint32_t* tile0,
                                 uint32_t* split) {
   const uint32_t P = (R + 1) / 2;
@@ -553,7 +565,9 @@ __global__ void tl_split_kernel(const ulonglong2* ki, const uint32_t* ro, uint32
   const uint64_t k = (uint64_t)(b - tile0[p]) * kSortTile;
   split[b] = (uint32_t)corank(k, na, nb, [&](uint64_t x) { return ki[a0 + x]; }, [&](uint64_t x) { return ki[a1 + x]; });
 }
+#endif  // HG_TL_KERNELS
 
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2* ki, const uint32_t* ii, ulonglong2* ko,
                                                                 uint32_t* io, const uint32_t* ro, uint32_t R,
                                                                 const uint32_t* tile0, const uint32_t* split) {
@@ -601,6 +615,7 @@ __global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2
     io[out0 + t] = si[q];
   }
 }
+#endif  // HG_TL_KERNELS
 
 // ---------------------------------------------------------------------------
 // metadata first occurrences
@@ -638,7 +653,7 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   const uint32_t kind = it.kind & 3u;
   bool first = i == 0;
   if (kind == TL_HOST) {
-    const uint32_t s = tl_stream(it.klo);
+    const uint32_t s = ((it.kind & TL_TRUNC) && T.flush_stream) ? T.flush_stream[tl_stream(it.klo)] : tl_stream(it.klo);
     const uint64_t* so = T.sstr_off + 3ull * s;
     if (kLen) {
       first_min(&T.proc_first[T.stream_proc[s]], i);
@@ -757,6 +772,7 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
 #ifndef HG_TL_LEN_MINB
 #define HG_TL_LEN_MINB 3  // 3 CTAs per SM (80 registers): 3.85 vs 5.2 ms for the timeline of C5 x0.1
 #endif
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(256, HG_TL_LEN_MINB) tl_len_kernel(TlTables T) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
     TC w{0};
@@ -764,9 +780,11 @@ __global__ void __launch_bounds__(256, HG_TL_LEN_MINB) tl_len_kernel(TlTables T)
     T.lens[i] = (uint32_t)w.n;
   }
 }
+#endif  // HG_TL_KERNELS
 
 // the items that open a metadata key: their length with the metadata objects (two keys may
 // share an item: both threads store the same length)
+#ifdef HG_TL_KERNELS
 __global__ void tl_meta_len_kernel(TlTables T, uint32_t n_proc, uint32_t th_size) {
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (uint64_t)n_proc + th_size;
        e += (uint64_t)gridDim.x * blockDim.x) {
@@ -777,6 +795,7 @@ __global__ void tl_meta_len_kernel(TlTables T, uint32_t n_proc, uint32_t th_size
     T.lens[f] = (uint32_t)w.n;
   }
 }
+#endif  // HG_TL_KERNELS
 
 // ---------------------------------------------------------------------------
 // exclusive scan of lens -> offs (three kernels, 1024 per block)
@@ -808,13 +827,16 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* total)
   return before;
 }
 
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kScanBlock) tl_scan1_kernel(const uint32_t* lens, uint32_t n, uint64_t* bsum) {
   const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
   uint64_t tot;
   block_excl_scan(i < n ? lens[i] : 0, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
+#endif  // HG_TL_KERNELS
 
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kScanBlock) tl_scan2_kernel(uint64_t* bsum, uint32_t nb, uint64_t* grand) {
   uint64_t carry = 0;
   for (uint32_t b0 = 0; b0 < nb; b0 += kScanBlock) {
@@ -827,13 +849,16 @@ __global__ void __launch_bounds__(kScanBlock) tl_scan2_kernel(uint64_t* bsum, ui
   }
   if (threadIdx.x == 0) *grand = carry;
 }
+#endif  // HG_TL_KERNELS
 
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kScanBlock) tl_scan3_kernel(const uint32_t* lens, uint32_t n, const uint64_t* bsum,
                                                               uint64_t* offs) {
   const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
   const uint64_t ex = block_excl_scan(i < n ? lens[i] : 0, nullptr);
   if (i < n) offs[i] = bsum[blockIdx.x] + ex;
 }
+#endif  // HG_TL_KERNELS
 
 // ---------------------------------------------------------------------------
 // writer: a warp formats 32 consecutive items into shared memory, then stores
@@ -845,6 +870,7 @@ constexpr int kTlStage = 5120;
 #ifndef HG_TL_WRITE_MINB
 #define HG_TL_WRITE_MINB 3  // (with the length pass at 3: both at 80 registers, the spills are cheaper than the latency)
 #endif
+#ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kTlWarps * 32, HG_TL_WRITE_MINB) tl_write_kernel(TlTables T) {
   __shared__ __align__(16) char stage[kTlWarps][kTlStage + 32];
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -880,5 +906,6 @@ __global__ void __launch_bounds__(kTlWarps * 32, HG_TL_WRITE_MINB) tl_write_kern
     }
   }
 }
+#endif  // HG_TL_KERNELS
 
 }  // namespace hg

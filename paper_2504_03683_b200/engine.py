@@ -105,6 +105,22 @@ class Engine:
         self._streams = list(raw_streams)
         for s in self._streams:
             self.add_stream_ptr(s.hostname, s.pid, s.tid, s.data)
+        self._set_flush_order()
+
+    def _set_flush_order(self):
+        """Truncated spans flush per stack in (str(hostname), pid, tid) order (pipeline.py:230); the
+        streams are in (hostname or "", pid or 0, tid or 0) order -- they differ only around None."""
+        idents = [(s.hostname, s.pid, s.tid) for s in self._streams]
+        if not any(h is None for h, _, _ in idents):
+            return
+        order = sorted(range(len(idents)), key=lambda i: (str(idents[i][0]), idents[i][1] or 0, idents[i][2] or 0, i))
+        if order == list(range(len(idents))):
+            return
+        rank = [0] * len(order)
+        for r, i in enumerate(order):
+            rank[i] = r
+        self._check(self._L.hg_set_flush_order(self._ctx, (C.c_uint32 * len(rank))(*rank), len(rank)),
+                    "hg_set_flush_order")
 
     def set_streams_pinned(self, idents, tensors):
         """Streams from pinned host tensors (torch.uint8); the next run copies them H2D."""

@@ -21,25 +21,42 @@ INCLUDE = HERE.parent / "include"
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+    "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
     "--expt-relaxed-constexpr",
 ]
 
 
 def sources():
-    return [CSRC / "engine.cu"]
+    """One translation unit per kernel family (ctx.h): they compile in parallel."""
+    return [CSRC / "engine.cu", CSRC / "fast.cu", CSRC / "seg.cu", CSRC / "timeline.cu"]
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    deps = sources() + [CSRC / "hg_device.cuh", INCLUDE / "hapigpu.h"] + list(CSRC.glob("*.cuh"))
-    newest = max(p.stat().st_mtime for p in deps if p.exists())
-    if not force and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= newest:
-        return LIB_PATH
+    from concurrent.futures import ThreadPoolExecutor
+
+    headers = [INCLUDE / "hapigpu.h"] + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h"))
+    newest_h = max(p.stat().st_mtime for p in headers if p.exists())
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", str(INCLUDE), "-o", str(LIB_PATH), *map(str, sources())]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+    objdir = HERE / "build"
+    objdir.mkdir(exist_ok=True)
+    objs, jobs = [], []
+    for src in sources():
+        obj = objdir / (src.stem + ".o")
+        objs.append(obj)
+        if force or not obj.exists() or obj.stat().st_mtime < max(newest_h, src.stat().st_mtime):
+            jobs.append([nvcc, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", "-o", str(obj), str(src)])
+    if not jobs and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= max(o.stat().st_mtime for o in objs):
+        return LIB_PATH
+
+    def run(cmd):
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.check_call(cmd)
+
+    with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
+        list(ex.map(run, jobs))
+    link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(LIB_PATH), *map(str, objs)]
+    run(link)
     return LIB_PATH
 
 
@@ -84,6 +101,7 @@ def lib():
         "hg_last_timing": ([vp, vp, vp, vp, vp, vp], C.c_int),
         "hg_set_option": ([vp, u32, u64], C.c_int),
         "hg_last_path": ([vp, vp, vp, vp], C.c_int),
+        "hg_set_flush_order": ([vp, vp, u32], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -101,4 +119,5 @@ EXPORTED = (
     "hg_get_tally", "hg_get_device_names", "hg_get_stream_spans", "hg_get_orphans", "hg_get_trace_errors",
     "hg_timeline_size", "hg_get_timeline", "hg_device_tally", "hg_last_timing", "hg_set_function_names",
     "hg_timeline_ms", "hg_set_timeline_device", "hg_phase_timing", "hg_set_option", "hg_last_path",
+    "hg_set_flush_order",
 )

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 from .errors import PipelineError, UnsupportedTraceError
 from .registry import SchemaRegistry
 from .tally import TallyReport
-from .tracefile import RawStream, encode_record, stream_bytes
+from .tracefile import RECORD_HEADER, RawStream, encode_record, stream_bytes
 
 END_OF_STREAM = "end_of_stream"
 
@@ -145,7 +145,25 @@ class TimelineSink(Sink):
 
 
 def _is_passive(sink) -> bool:
-    return type(sink).on_message is Sink.on_message or not hasattr(sink, "on_message")
+    """A sink that never looks at messages: no on_message, or one inherited unchanged from a base
+    class named ``Sink`` (this package's or the reference's, pipeline.py:250-263)."""
+    if not hasattr(sink, "on_message"):
+        return True
+    for klass in type(sink).__mro__:
+        if "on_message" in klass.__dict__:
+            return klass is Sink or (klass.__name__ == "Sink" and _is_noop(klass.__dict__["on_message"]))
+    return True
+
+
+def _is_noop(fn) -> bool:
+    code = getattr(fn, "__code__", None)
+    if code is None:
+        return False
+    # a body that is just `pass` (or a docstring) compiles to RETURN_CONST None
+    import dis
+
+    ops = [i.opname for i in dis.get_instructions(code) if i.opname not in ("RESUME", "NOP")]
+    return ops in (["RETURN_CONST"], ["LOAD_CONST", "RETURN_VALUE"])
 
 
 # ---------------------------------------------------------------------------
@@ -187,17 +205,80 @@ def _raw_from_records(cursors, registry):
         labels.append(label)
     # mux order: (hostname or "", pid or 0, tid or 0, input index)  (pipeline.py:88-91)
     order = sorted(range(len(raws)), key=lambda i: (raws[i].hostname or "", raws[i].pid or 0, raws[i].tid or 0, i))
-    return [raws[i] for i in order]
+    return merge_same_identity([raws[i] for i in order])
+
+
+def _walk(raw):
+    """(offsets, timestamps) of every record of a stream; None if a header or payload is cut."""
+    data, off, offs, tss = raw.data, 16, [], []
+    n = len(data)
+    while off < n:
+        if off + 16 > n:
+            return None
+        _, ts, plen = RECORD_HEADER.unpack_from(data, off)
+        if off + 16 + plen > n:
+            return None
+        offs.append(off)
+        tss.append(ts)
+        off += 16 + plen
+    return offs, tss
+
+
+def merge_same_identity(raws):
+    """Streams that share one (hostname, pid, tid) identity share one LIFO stack in the reference
+    (pipeline.py:156-161) and meet in the muxer by (ts, seq, input index) (pipeline.py:88-91).  The
+    engine pairs per stream, so such streams are merged here into one stream in exactly that order.
+    ``raws`` is in mux order (identity, then input index); a group whose records cannot be walked
+    or are not timestamp-monotone (the reference would raise mid-run) is refused."""
+    out, i = [], 0
+    while i < len(raws):
+        j = i + 1
+        key = (raws[i].hostname, raws[i].pid, raws[i].tid)
+        while j < len(raws) and (raws[j].hostname, raws[j].pid, raws[j].tid) == key:
+            j += 1
+        if j - i == 1:
+            out.append(raws[i])
+            i = j
+            continue
+        group = [r for r in raws[i:j] if r.data]
+        if len(group) <= 1:
+            out.append(group[0] if group else raws[i])
+            i = j
+            continue
+        walks = []
+        for r in group:
+            w = _walk(r)
+            if w is None or any(b < a for a, b in zip(w[1], w[1][1:])):
+                raise UnsupportedTraceError(
+                    f"streams sharing identity {key} need a clean, timestamp-ordered record walk to be merged")
+            walks.append(w)
+        import heapq
+
+        heap = [(w[1][0], 0, g) for g, w in enumerate(walks) if w[0]]
+        heapq.heapify(heap)
+        parts = [group[0].data[:16]]
+        while heap:
+            ts, seq, g = heapq.heappop(heap)
+            offs, tss = walks[g]
+            a = offs[seq]
+            b = offs[seq + 1] if seq + 1 < len(offs) else len(group[g].data)
+            parts.append(group[g].data[a:b])
+            if seq + 1 < len(offs):
+                heapq.heappush(heap, (tss[seq + 1], seq + 1, g))
+        out.append(RawStream(key[0], key[1], key[2], group[0].name, b"".join(parts), group[0].info))
+        i = j
+    return out
 
 
 def _resolve_source(source, registry):
     if hasattr(source, "raw_streams"):
-        return source.raw_streams(), (source.stream_infos() if hasattr(source, "stream_infos") else None)
+        return (merge_same_identity(source.raw_streams()),
+                source.stream_infos() if hasattr(source, "stream_infos") else None)
     if hasattr(source, "dir") and hasattr(source, "metadata"):  # a reference TraceReader
         from .tracefile import open_trace_reader
 
         ours = open_trace_reader(source.dir)
-        return ours.raw_streams(), ours.stream_infos()
+        return merge_same_identity(ours.raw_streams()), ours.stream_infos()
     cursors = source.streams() if hasattr(source, "streams") else list(source)
     infos = source.stream_infos() if hasattr(source, "stream_infos") else None
     return _raw_from_records(cursors, registry), infos
@@ -246,12 +327,15 @@ def run_pipeline(source, sinks=(), registry=None, engine=None) -> PipelineResult
     eng = engine or default_engine()
     labels = [r.name for r in raws]
     olabels = [f"{r.hostname}/{r.pid}/{r.tid}" for r in raws]
-    res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels, orphan_labels=olabels,
-                  timeline_device_index=next(iter(device_index), 0))
-    for s in sinks:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
-        hook = getattr(s, "on_diagnostics", None)
-        if hook is not None:
-            hook(list(res.orphans))
+    res = None
+    try:
+        res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels, orphan_labels=olabels,
+                      timeline_device_index=next(iter(device_index), 0))
+    finally:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
+        for s in sinks:
+            hook = getattr(s, "on_diagnostics", None)
+            if hook is not None:
+                hook(list(res.orphans) if res is not None else [])
     if res.error is not None:
         raise res.error
     for s in tally:

@@ -45,11 +45,12 @@ def kernel_pool(n: int, ascii_only: bool = False) -> list:
 
 class SynthParams(C.Structure):
     _fields_ = [
-        ("seed", C.c_uint64), ("n_events", C.c_uint64), ("max_depth", C.c_uint32),
-        ("gap_lo", C.c_uint32), ("gap_hi", C.c_uint32), ("ts0_hi", C.c_uint64),
+        ("seed", C.c_uint64), ("n_events", C.c_uint64), ("max_depth", C.c_uint32), ("pad0", C.c_uint32),
+        ("gap_lo", C.c_uint64), ("gap_hi", C.c_uint64), ("ts0_hi", C.c_uint64),
         ("push_p", C.c_double), ("err_p", C.c_double), ("prof_p", C.c_double), ("meta_p", C.c_double),
         ("orphan_p", C.c_double), ("mismatch_p", C.c_double), ("zipf_s", C.c_double),
         ("n_layers", C.c_uint32), ("close_at_end", C.c_int32), ("meta_sid", C.c_int32),
+        ("dev_off_hi", C.c_uint64), ("dev_lo", C.c_int64), ("dev_hi", C.c_int64),
     ]
 
 
@@ -151,7 +152,8 @@ class Workload:
 
 
 DEFAULTS = dict(max_depth=4, gap_lo=1, gap_hi=600, ts0_hi=1000, push_p=0.5, err_p=0.02, prof_p=0.25,
-                meta_p=0.0, orphan_p=0.0, mismatch_p=0.0, zipf_s=0.0, n_layers=1, close_at_end=1)
+                meta_p=0.0, orphan_p=0.0, mismatch_p=0.0, zipf_s=0.0, n_layers=1, close_at_end=1,
+                dev_off_hi=10_000, dev_lo=1_000, dev_hi=100_000)
 
 
 def generate_stream(wl: Workload, spec: StreamSpec, flat=None, until_ns=None) -> bytes:

@@ -158,6 +158,40 @@ def fx_synthetic():
                                            for t in range(6)], gap_lo=0, gap_hi=2, close_at_end=0))
     yield "syn_deep", gen(_wl("deep", ze, [synth.StreamSpec("synth0", P, P, 6000, 800)],
                               max_depth=300, push_p=0.8, close_at_end=0, mismatch_p=0.01))
+    # wide values: host gaps in [2^32, 2^33] ns, timestamps from ~2^60 (CPython float repr
+    # beyond 2^53), device spans of +-2^40 ns (negative: end < start)
+    yield "syn_wide", gen(_wl("wide", ze, [synth.StreamSpec("synth0", P, P + t, 1200, 900 + t) for t in range(4)],
+                              gap_lo=1 << 32, gap_hi=1 << 33, ts0_hi=1 << 60, prof_p=0.5, close_at_end=0,
+                              dev_off_hi=1 << 41, dev_lo=-(1 << 40), dev_hi=1 << 40))
+
+
+def fx_dup_identity():
+    """Two stream files with one (hostname, pid, tid): they share a LIFO stack
+    (pipeline.py:156-161) and tie-break by seq then input index (pipeline.py:88-91)."""
+    ze = synth.ze_registry()
+    by = {s.name: s.id for s in ze.schemas}
+
+    def rec(name, ts, **payload):
+        sc = ze.by_id[by[f"ze:{name}"]]
+        full = {}
+        for f in sc.fields:
+            full[f.name] = payload.get(f.name, "" if f.kind == "string" else b"" if f.kind == "blob" else 0)
+        return encode_record(sc, ts, full)
+
+    def make(d):
+        a = [rec("zeMockInit_entry", 10), rec("zeMockMemAlloc_entry", 30), rec("zeMockMemAlloc_exit", 40),
+             rec("zeMockMemFree_entry", 50), rec("zeMockInit_exit", 70, result=3), rec("zeMockMemFree_entry", 90)]
+        b = [rec("zeMockMemFree_exit", 50), rec("zeMockMemFree_exit", 60), rec("zeMockEventCreate_entry", 70),
+             rec("zeMockEventCreate_exit", 75), rec("zeMockInit_entry", 95)]
+        c = [rec("zeMockInit_entry", 5), rec("zeMockInit_exit", 50)]
+        entries = [{"hostname": "dup", "pid": 7, "tid": 7, "data": stream_bytes(a), "event_count": len(a),
+                    "dropped_count": 0, "file": "stream_7_7_a.bin"},
+                   {"hostname": "dup", "pid": 7, "tid": 7, "data": stream_bytes(b), "event_count": len(b),
+                    "dropped_count": 0, "file": "stream_7_7_b.bin"},
+                   {"hostname": "dup", "pid": 7, "tid": 8, "data": stream_bytes(c), "event_count": len(c),
+                    "dropped_count": 0, "file": "stream_7_8.bin"}]
+        write_trace(d, ze, entries)
+    yield "dup_identity", make
 
 
 # --- hand-built registries and byte-level fixtures --------------------------
@@ -493,7 +527,7 @@ def main(only=None):
     EXPECTED.mkdir(parents=True, exist_ok=True)
     TRACES.mkdir(parents=True, exist_ok=True)
     index = []
-    for group in (fx_workloads, fx_synthetic, fx_custom, fx_errors):
+    for group in (fx_workloads, fx_synthetic, fx_dup_identity, fx_custom, fx_errors):
         for name, make in group():
             if only and name not in only:
                 continue

@@ -161,3 +161,62 @@ def test_synth_streams_are_well_formed():
     # deterministic
     again = generate(config("c2", 0.0002))
     assert [r.data for r in raws[:4]] == [r.data for r in again[:4]]
+
+
+def test_synth_reproduces_committed_goldens():
+    """The C generator still writes the committed syn_c1 / syn_c2 fixture bytes (make_golden.py)."""
+    from golden_util import trace_dir
+    from paper_2504_03683_b200.tracefile import open_trace_reader
+
+    for name, cfg, scale in (("syn_c1", "c1", 0.008), ("syn_c2", "c2", 0.0003)):
+        ours = {(r.hostname, r.pid, r.tid): r.data for r in generate(config(cfg, scale))}
+        committed = {(r.hostname, r.pid, r.tid): r.data for r in open_trace_reader(trace_dir(name)).raw_streams()}
+        assert ours == committed, name
+
+
+def test_merge_same_identity_matches_identity_keyed_oracle():
+    """Splitting streams into same-identity halves and merging them back (pipeline.merge_same_identity)
+    gives what the oracle -- which keys its stacks by identity like pipeline.py:156-161 -- computes
+    on the split streams; the dup_identity golden pins that oracle to the reference."""
+    from oracle import oracle
+    from paper_2504_03683_b200.pipeline import merge_same_identity
+
+    wl = config("c2", 0.0005)
+    raws = generate(wl)[:8]
+    rng = random.Random(5)
+    split = []
+    for r in raws:
+        parts, off = ([], []), 16
+        while off < len(r.data):
+            plen = struct.unpack_from("<I", r.data, off + 12)[0]
+            parts[rng.random() < 0.5].append(r.data[off: off + 16 + plen])
+            off += 16 + plen
+        for i, p in enumerate(parts):
+            split.append(RawStream(r.hostname, r.pid, r.tid, f"{r.name}.{i}", stream_bytes(p)))
+    merged = merge_same_identity(split)
+    assert len(merged) == len(raws)
+    a = oracle.run(split, wl.registry, want_timeline=True)
+    b = oracle.run(merged, wl.registry, want_timeline=True)
+    assert a.report == b.report and a.stats == b.stats and a.orphans == b.orphans and a.timeline == b.timeline
+    assert oracle.run(raws, wl.registry).report == b.report  # the split lost nothing
+
+
+def test_passive_sink_detection():
+    from paper_2504_03683_b200.pipeline import Sink, _is_passive
+
+    class Diag(Sink):
+        def on_diagnostics(self, orphans):
+            pass
+
+    class Ref:  # a sink deriving from a foreign base class named Sink with a no-op on_message
+        pass
+
+    RefSink = type("Sink", (), {"on_message": lambda self, msg: None, "name": "s"})
+    RefDiag = type("RefDiag", (RefSink,), {"on_diagnostics": lambda self, o: None})
+
+    class Busy(Sink):
+        def on_message(self, msg):
+            print(msg)
+
+    assert _is_passive(Diag()) and _is_passive(RefDiag()) and not _is_passive(Busy())
+    assert _is_passive(Ref())
