@@ -3,18 +3,22 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2] [--scale 1.0]
 
 A "step" is one pass of the hot path (decode -> pair -> tally, SURVEY.md §8a
-rows a2-a5) over one synthetic trace of the named configuration; at N=1 the
-workload is config C2 (100M events, 4 procs x 64 threads = 256 streams,
-bundled ze registry).  Under torchrun every rank processes its own C2-sized
-trace (weak scaling: distinct pids per rank) and the ranks exchange the global
-last timestamp and merge tallies over NCCL.
+rows a2-a5) over one synthetic trace of the named configuration.  N=1: config
+C2 (100M events, 4 procs x 64 threads = 256 streams, bundled ze registry).
+N>1 (one process per GPU; `--gpus N` relaunches itself under torchrun): config
+C3 (1B events, 1,024 streams) sharded over the ranks by the product's LPT
+partitioner -- each rank generates only its streams -- with the last-ts
+exchange and the device-resident tally merge (NCCL) inside every timed step
+(strong scaling).
 
 Rank 0 prints ONE JSON line.  `value` = whole-job events / max-over-ranks
-device time per step with the trace resident in HBM (CUDA events on the
-engine's stream); `e2e` = the same metric through the public API with the
-trace in pinned host memory, H2D and result D2H inside the timed region.
-`--impl reference` times the CPU oracle (C restatement of the reference path,
-oracle/hapi_oracle.c) with all host cores on a bounded sample.
+device time per step with the trace resident in HBM; `e2e` = the same metric
+through the public API with the trace in pinned host memory, H2D and result
+D2H inside the timed region; `parity` = the timed run's TallyReport and
+IntervalStats against the CPU oracle over the same streams at full size (the
+run exits non-zero on a mismatch).  `--impl reference` times the CPU oracle (C
+restatement of the reference path, oracle/hapi_oracle.c) with all host cores
+on a bounded sample of the same workload.
 """
 
 from __future__ import annotations
@@ -94,19 +98,60 @@ def _dist():
     return ws, rank, local
 
 
-def make_workload(name, scale, rank):
+def workload_name(args, ws):
+    """C2 (100M events, one B200) at N=1; C3 (1B events, 8 hosts x 4 procs x 32 threads) sharded over
+    the ranks at N>1 -- BASELINE.json configs[1] and configs[2]."""
+    if args.config:
+        return args.config
+    return "c2" if ws == 1 else "c3"
+
+
+DESCR = {
+    "c2": "SURVEY.md §8(d) C2: 100M-event synthetic L0-style trace, 4 procs x 64 threads (256 streams), bundled ze "
+          "registry, one B200",
+    "c3": "SURVEY.md §8(d) C3: 1B-event multi-host trace, 8 hosts x 4 procs x 32 threads (1,024 streams), streams "
+          "sharded over the ranks by LPT on bytes, NCCL merge",
+}
+
+
+def shared_config(name, scale, ws):
+    """The `config` both arms print (same dict -> the driver sees the same workload)."""
     from paper_2504_03683_b200 import synth
 
     wl = synth.config(name, scale)
-    if rank:  # weak scaling: every rank owns a distinct set of processes
-        for s in wl.streams:
-            s.pid += 1_000_000 * rank
-            s.tid += 1_000_000 * rank
-            s.seed += 7_919 * rank
-    return wl
+    events = sum(s.n_events for s in wl.streams if s.kind == "calls")
+    return {"workload": f"{name} x{scale}: {DESCR.get(name, name)}", "events": events,
+            "streams": len(wl.streams), "n_gpus": ws}
 
 
-def cpu_baseline(raws, registry, target_s=10.0):
+def my_streams(name, scale, ws, rank):
+    """This rank's part of the workload: the product's partitioner over the streams' expected sizes
+    (event counts); only those streams are generated.  Returns (workload, global index list)."""
+    from paper_2504_03683_b200 import synth
+    from paper_2504_03683_b200.distributed import partition_streams
+
+    wl = synth.config(name, scale)
+    order = sorted(range(len(wl.streams)), key=lambda i: (wl.streams[i].hostname, wl.streams[i].pid,
+                                                          wl.streams[i].tid))
+    specs = [wl.streams[i] for i in order]
+    mine = partition_streams([s.n_events for s in specs], ws)[rank] if ws > 1 else list(range(len(specs)))
+    sub = synth.Workload(wl.name, wl.registry, [specs[i] for i in mine], wl.params, wl.layers, wl.kernel_names,
+                         wl.sampler_period_ns)
+    return sub, mine, specs
+
+
+def oracle_check(raws, registry, threads, floor_last_ts=0, with_infos=True):
+    """The CPU oracle (C restatement of the reference path, test infrastructure) over these streams,
+    sharded over host threads: the parity reference for the timed run."""
+    from oracle import oracle
+
+    t = time.perf_counter()
+    r = oracle.run(raws, registry, [x.info for x in raws] if with_infos else None, threads=threads,
+                   floor_last_ts=floor_last_ts)
+    return r, time.perf_counter() - t
+
+
+def cpu_baseline(raws, registry, target_s=10.0, max_events=None):
     """Oracle (C restatement) tally with all host threads on a bounded sample of the workload."""
     from oracle import oracle
 
@@ -119,7 +164,7 @@ def cpu_baseline(raws, registry, target_s=10.0):
     oracle.run(probe, registry, [r.info for r in probe], threads=cores)
     dt = time.perf_counter() - t
     rate = sum(r.info.event_count for r in probe) / max(dt, 1e-9)
-    want_events = min(total, int(rate * target_s))
+    want_events = min(total, int(rate * target_s), max_events or total)
     n = k
     acc = sum(r.info.event_count for r in raws[:n])
     while n < len(raws) and acc < want_events:
@@ -139,11 +184,22 @@ def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
-    wl = make_workload(args.config, args.scale, 0)
     from paper_2504_03683_b200 import synth
 
+    name = workload_name(args, ws)
+    cfg = shared_config(name, args.scale, ws)
+    wl = synth.config(name, args.scale)
+    # a bounded sample of the workload: the first streams in mux order, about 100M events at most
+    specs = sorted([s for s in wl.streams if s.kind == "calls"], key=lambda s: (s.hostname, s.pid, s.tid))
+    keep, acc = [], 0
+    for s in specs:
+        if acc >= 100_000_000:
+            break
+        keep.append(s)
+        acc += s.n_events
+    if len(keep) < len(specs):
+        wl = synth.Workload(wl.name, wl.registry, keep, wl.params, wl.layers, wl.kernel_names, wl.sampler_period_ns)
     raws = synth.generate(wl)
-    total = sum(r.info.event_count for r in raws)
     times = []
     base = None
     for i in range(args.warmup + args.steps):
@@ -153,80 +209,117 @@ def run_reference(args):
             base = b
     value = statistics.mean(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "events/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": f"{args.config} x{args.scale}", "events": total},
+        "scaling": "weak" if ws == 1 else "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": cfg,
         "cpu_baseline": {**base, "value": value},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
+def _parity_line(got_rep, got_stats, want_rep, want_stats):
+    if got_rep == want_rep and got_stats == want_stats:
+        return "exact"
+    diff = [k for k in set(got_rep.rows) | set(want_rep.rows) if got_rep.rows.get(k) != want_rep.rows.get(k)]
+    return f"MISMATCH: stats {got_stats != want_stats}, rows {sorted(diff)[:5]}"
+
+
 def run_ours(args):
     import torch
 
     ws, rank, local = _dist()
+    comm = None
+    dev = local % max(torch.cuda.device_count(), 1)  # == local on a real node; >1 rank per GPU only with gloo
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:  # gloo: the N>1 code path on one GPU (tests), collectives through host memory
+            dist.init_process_group("gloo")
+        from paper_2504_03683_b200.distributed import Comm
+
+        comm = Comm()
     from paper_2504_03683_b200 import synth
     from paper_2504_03683_b200.distributed import ShardedRun
     from paper_2504_03683_b200.engine import Engine
+    from paper_2504_03683_b200.tally import merge_tallies
+    from paper_2504_03683_b200.tracefile import RawStream
 
+    name = workload_name(args, ws)
+    cfg = shared_config(name, args.scale, ws)
     t0 = time.perf_counter()
-    wl = make_workload(args.config, args.scale, rank)
-    raws = synth.generate(wl)
+    sub, mine, specs = my_streams(name, args.scale, ws, rank)
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+    threads = max(1, (os.cpu_count() or 1) // local_world)
+    raws = synth.generate(sub, threads=threads)
     gen_s = time.perf_counter() - t0
     n_events = sum(r.info.event_count for r in raws)
     n_bytes = sum(len(r.data) for r in raws)
     infos = [r.info for r in raws]
+    gstreams = [RawStream(s.hostname, s.pid, s.tid, s.file or f"stream_{s.pid}_{s.tid}.bin", b"") for s in specs]
 
-    eng = Engine(device=local if ws > 1 else 0)
-    runner = ShardedRun(eng, wl.registry, world_size=ws, rank=rank)
+    eng = Engine(device=dev)
+    runner = ShardedRun(eng, sub.registry, comm, stream_global=mine, global_streams=gstreams)
 
-    # ---- device-resident timing (value)
-    eng.set_registry(wl.registry)
+    # ---- device-resident timing (value): the trace is in HBM before the timed region
+    eng.set_registry(sub.registry)
     eng.set_streams(raws)
     eng.stage()
     for _ in range(args.warmup):
         runner.step()
-    step_ms, dec_ms, ph1_ms, walk_ms, launches = [], [], [], [], 0
+    step_ms, dec_ms, ph1_ms, launches = [], [], [], 0
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clk = Clocks(local)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clk = Clocks(dev)
     with clk:
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            ev0[i].record()
             info = runner.step()
-            step_ms.append(info["device_ms"])
+            ev1[i].record()
             dec_ms.append(info["decode_ms"])
             ph1_ms.append(info["phase1_ms"])
-            walk_ms.append(info["walk_ms"])
+            step_ms.append(info["device_ms"])
             launches += info["launches"]
     torch.cuda.synchronize()
+    if ws > 1:  # the whole step incl. the merge collectives, on the device clock of the current stream
+        step_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     ms = statistics.mean(step_ms)
     tms = statistics.mean(dec_ms)
     p1 = statistics.mean(ph1_ms)
-    wms = statistics.mean(walk_ms)
-    tot_events = n_events
+    tot_events, tot_bytes = n_events, n_bytes
     if ws > 1:
-        t = torch.tensor([ms, tms, p1, wms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms, tms, p1], dtype=torch.float64, device=comm.device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, tms, p1, wms = t.tolist()
-        e = torch.tensor([n_events, n_bytes], dtype=torch.int64, device="cuda")
+        ms, tms_max, p1 = t.tolist()
+        e = torch.tensor([n_events, n_bytes], dtype=torch.int64, device=comm.device)
         torch.distributed.all_reduce(e)
         tot_events, tot_bytes = e.tolist()
-    else:
-        tot_bytes = n_bytes
     value = tot_events / (ms / 1e3)
+    rep, stats, _, err = runner.result(infos if ws == 1 else None)
+    if err is not None:
+        raise err
 
-    # correctness of the timed path against the oracle on rank 0's first streams (cheap check)
-    rep = runner.report(infos)
+    # ---- parity of the timed run against the CPU oracle, at full size
+    t_or = time.perf_counter()
+    want, or_s = oracle_check(raws, sub.registry, threads, floor_last_ts=runner.global_last_ts,
+                              with_infos=ws == 1)
+    if ws > 1:  # per-shard oracle reports merged the reference's way (aggregator.py:35-76)
+        reps = comm.all_gather_object((want.report, want.stats))
+        want_rep = merge_tallies([r for r, _ in reps])
+        want_stats = {k: sum(s[k] for _, s in reps) for k in want.stats}
+    else:
+        want_rep, want_stats = want.report, want.stats
+    parity = _parity_line(rep, stats, want_rep, want_stats)
+    parity_s = time.perf_counter() - t_or
 
-    # ---- end-to-end through the public API from pinned host memory (e2e)
+    # ---- end to end through the public API from pinned host memory (e2e)
     pinned = []
     for r in raws:
         t = torch.empty(len(r.data), dtype=torch.uint8, pin_memory=True)
@@ -242,26 +335,29 @@ def run_ours(args):
         t = time.perf_counter()
         eng.set_streams_pinned([(r.hostname, r.pid, r.tid) for r in raws], pinned)
         info = runner.step()
-        rep2 = runner.report(infos)
+        rep2, _, _, _ = runner.result(infos if ws == 1 else None)
         dt = time.perf_counter() - t
         if i >= args.warmup:
             e2e_s.append(dt)
             h2d, d2h = info["h2d_bytes"], info["d2h_bytes"]
     e2e = statistics.mean(e2e_s)
     if ws > 1:
-        t = torch.tensor([e2e], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e], dtype=torch.float64, device=comm.device)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e = t.item()
-    assert rep2 == rep, "e2e run produced a different tally"
+    if rep2 != rep:
+        parity = "MISMATCH: e2e run differs from the resident run"
 
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
+        if parity != "exact":
+            sys.exit(1)
         return
     peak, peak_src = _peaks()
     path, fallbacks, range_bytes = eng.last_path()
     single = path == 1
-    achieved = (n_bytes / (tms / 1e3)) / 1e9  # per GPU: rank-local trace bytes over the decode kernel time
+    achieved = (n_bytes / (tms / 1e3)) / 1e9  # rank 0: its trace bytes over its decode kernel time
     line = {
         "metric": METRIC,
         "value": value,
@@ -271,22 +367,29 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if ws == 1 else "strong",
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic",
-        "config": {
-            "workload": f"{args.config}: SURVEY.md §8(d) C2 = 100M-event synthetic L0-style trace, 4 procs x 64 "
-                        f"threads (256 streams), bundled ze registry" if args.config == "c2" else args.config,
-            "scale": args.scale,
-            "events_per_gpu": n_events,
-            "bytes_per_gpu": n_bytes,
+        "config": cfg,
+        "parity": parity,
+        "workload_detail": {
+            "events_per_gpu_rank0": n_events,
+            "bytes_per_gpu_rank0": n_bytes,
             "bytes_per_event": n_bytes / max(n_events, 1),
             "total_events": tot_events,
-            "parallelism": f"streams per rank, {ws} rank(s); NCCL all-reduce of last ts + tally merge" if ws > 1
-            else "1 GPU",
+            "total_bytes": tot_bytes,
+            "parallelism": (f"{ws} ranks, streams by LPT on bytes (distributed.partition_streams); per step: "
+                            "MAX all-reduce of [last ts, status], device-name all-gather, SUM + MAX all-reduce of "
+                            "the device-resident tally buffer (csrc/merge.cu), all inside the timed step")
+            if ws > 1 else "1 GPU",
+            "timing": "engine CUDA events (staging -> results on host)" if ws == 1 else
+                      "CUDA events on the current stream around the whole step incl. merge, max over ranks",
             "l2": "input (GBs) >> 126 MB L2: no flush needed between steps",
             "generation_s": round(gen_s, 2),
+            "parity_check": f"timed run's TallyReport + IntervalStats vs oracle/hapi_oracle.c over the same "
+                            f"{'streams' if ws == 1 else 'shards (merged with merge_tallies)'} at full size, "
+                            f"{threads} host threads, {or_s:.2f} s",
         },
         "roofline": {
             "bound": "hbm",
@@ -303,27 +406,36 @@ def run_ours(args):
                                    else "seg_walk_kernel + seg_chain_kernel + seg_decode_kernel"),
                        "path": "single pass over HBM (csrc/fast.cuh)" if single else "exact three-kernel path",
                        "range_bytes": range_bytes, "fallbacks": fallbacks, "ms": p1,
-                       "walk_ms": wms, "achieved": (n_bytes / (p1 / 1e3)) / 1e9,
+                       "achieved": (n_bytes / (p1 / 1e3)) / 1e9,
                        "frac": (n_bytes / (p1 / 1e3)) / 1e9 / peak},
         },
-        "cpu_baseline": cpu_baseline(raws, wl.registry, target_s=args.ref_seconds),
+        "cpu_baseline": cpu_baseline(raws, sub.registry, target_s=args.ref_seconds, max_events=100_000_000),
         "e2e": {"value": tot_events / e2e, "unit": "events/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "path": "Engine.run via pinned host streams (public API)"},
+                "d2h_bytes_per_step": d2h,
+                "path": "Engine.set_streams_pinned + ShardedRun.step + ShardedRun.result (hg_add_stream host "
+                        "pointers into pinned memory, hg_run_local/hg_finish, merge), wall clock per step, max "
+                        "over ranks"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if not args.no_timeline:
+    if ws == 1 and not args.no_timeline:
         line["timeline"] = timeline_side(eng)
-    if not args.no_configs:
-        line["other_configs"] = configs_side(eng)
+    if ws == 1 and not args.no_configs:
+        line["other_configs"] = configs_side(eng, threads)
     traffic = REPO / "profiles" / ("fast_kernel_traffic.json" if single else "seg_decode_traffic.json")
     if traffic.exists():
         tr = json.loads(traffic.read_text())
         line["roofline"]["traffic"] = tr.get("dram_bytes_per_launch")
         line["roofline"]["traffic_source"] = tr.get("source")
+    bad = [c for c in line.get("other_configs", []) if c.get("parity") != "exact"]
+    if bad and parity == "exact":
+        parity = "MISMATCH in other_configs: " + ", ".join(c["config"] for c in bad)
+        line["parity"] = parity
     print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
+    if parity != "exact":
+        sys.exit(1)
 
 
 def timeline_side(eng, config="c5", scale=0.1):
@@ -353,11 +465,13 @@ def timeline_side(eng, config="c5", scale=0.1):
             "checks": "object count = messages + metadata, json.dump framing, tally == tally-only run"}
 
 
-def configs_side(eng, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 0.25), ("c5", 0.25))):
+def configs_side(eng, threads, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 0.25), ("c5", 0.25))):
     """The other SURVEY.md §8(d) shapes (tally, device-resident, single pass unless it falls back):
-    phase-1 device time and events/s at a bounded scale each (parity for them is in tests/)."""
+    phase-1 device time and events/s at a bounded scale each, and the tally + IntervalStats of the
+    last run against the CPU oracle over the same streams."""
     from paper_2504_03683_b200 import synth
     from paper_2504_03683_b200.abi import HG_WANT_TALLY
+    from paper_2504_03683_b200.results import build_report
 
     out = []
     for name, scale in plan:
@@ -372,12 +486,16 @@ def configs_side(eng, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 0.25), ("c5", 0.25)
             k, t, *_ = eng.timing()
             if i:
                 ms.append(t)
-        ev = eng.stats()["events_in"]
+        st = eng.stats()
         path, fallbacks, rb = eng.last_path()
+        rep = build_report(eng._flat, eng.tally_rows(), eng.device_names(), [r.info for r in raws],
+                           [(r.hostname, r.pid, r.tid) for r in raws], eng.stream_spans())
+        want, _ = oracle_check(raws, wl.registry, threads)
         d = statistics.mean(ms)
-        out.append({"config": name, "scale": scale, "events": ev, "streams": len(raws),
-                    "bytes": sum(len(r.data) for r in raws), "device_ms": d, "events_per_s": ev / (d / 1e3),
-                    "path": "single pass" if path == 1 else "exact", "range_bytes": rb})
+        out.append({"config": name, "scale": scale, "events": st["events_in"], "streams": len(raws),
+                    "bytes": sum(len(r.data) for r in raws), "device_ms": d, "events_per_s": st["events_in"] / (d / 1e3),
+                    "path": "single pass" if path == 1 else "exact", "range_bytes": rb,
+                    "parity": _parity_line(rep, st, want.report, want.stats)})
     return out
 
 
@@ -387,12 +505,19 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default=None, help="workload (default: c2 at N=1, c3 sharded at N>1)")
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 collectives (gloo: several ranks on one GPU, for tests)")
     ap.add_argument("--no-timeline", action="store_true", help="skip the row-a8 timeline side measurement")
     ap.add_argument("--no-configs", action="store_true", help="skip the other-configuration side measurements")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torchrun (the driver does the same)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000), *sys.argv]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

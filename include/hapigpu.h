@@ -78,7 +78,7 @@ typedef struct hg_schema {
 
 typedef struct hg_config {
   int32_t device;          /* CUDA device ordinal                            */
-  uint32_t tile_bytes;     /* stream bytes per warp tile (0 = default)       */
+  uint32_t tile_bytes;     /* exact-path segment bytes (0 = sized to the trace) */
   uint32_t flags;          /* reserved                                       */
   int32_t timeline_device_index; /* TimelineSink(device_index=) (sinks.py:347-349) */
 } hg_config;
@@ -152,7 +152,8 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas,
 /* add one stream file (bytes incl. the 16-byte header, already validated by
  * the host) in (hostname, pid, tid) order; replaces StreamCursor
  * (tracefile.py:477-508).  `data` is a host pointer that must stay valid
- * until hg_run returns. */
+ * until hg_run returns.  hostname NULL stands for None (record-list sources):
+ * it orders as "" and prints as "None" in timeline metadata (sinks.py:367). */
 int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid,
                   const void* data, uint64_t size);
 int hg_clear_streams(hg_ctx* ctx);
@@ -207,12 +208,29 @@ int hg_set_flush_order(hg_ctx* ctx, const uint32_t* rank, uint32_t n);
 /* TimelineSink(device_index=) (sinks.py:347-349): device pid 9000000 + index */
 int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index);
 
-/* device-resident dense tally for NCCL merging across ranks: host rows are
- * function-indexed.  Returns device pointers owned by the context. */
+/* device-resident dense tally: host rows are function-indexed, 6 x u64 each (count,
+ * errors, sum lo, sum hi, min, max).  Returns a device pointer owned by the context. */
 int hg_device_tally(hg_ctx* ctx, void** host_rows, uint64_t* n_host_rows);
 
+/* multi-GPU merge (aggregator.py:35-76 merge_tallies as two collectives).  After
+ * hg_finish, hg_merge_export writes this rank's tally, IntervalStats and per-stream
+ * span counts into `dst` (DEVICE memory on this context's GPU, hg_merge_size int64
+ * elements) in a rank-independent layout: rows of the n_fn functions, then the
+ * n_dev_global device names of the global name order (dev_map[d] = global row of
+ * local device row d, host array), span counts at stream_global[s] (host array, one
+ * entry per local stream).  The caller all-reduces elements [0, sum_elems) with SUM
+ * and the rest with MAX (NCCL), copies the buffer to host memory and hands it to
+ * hg_merge_import together with the global device-name list (UTF-8, offsets[n] =
+ * end); hg_get_tally / hg_get_device_names / hg_get_stats then return the merged
+ * results.  Layout: see merge.cu. */
+uint64_t hg_merge_size(uint32_t n_fn, uint32_t n_dev_global, uint32_t n_streams_global, uint64_t* sum_elems);
+int hg_merge_export(hg_ctx* ctx, void* dst, const uint32_t* dev_map, uint32_t n_dev_local, uint32_t n_dev_global,
+                    const uint32_t* stream_global, uint32_t n_streams_global);
+int hg_merge_import(hg_ctx* ctx, const void* src, uint32_t n_dev_global, uint32_t n_streams_global,
+                    const char* names, const uint64_t* name_offsets);
+
 /* timing of the last run, CUDA events on the engine's stream: kernel_ms = the
- * dominant kernel (tile_kernel), total_ms = whole run from staging to results
+ * dominant kernel (fast_kernel on the single pass, the decode kernel on the exact path), total_ms = whole run from staging to results
  * on the host; bytes moved host<->device and kernel launches of that run */
 int hg_last_timing(hg_ctx* ctx, float* kernel_ms, float* total_ms, uint64_t* h2d_bytes, uint64_t* d2h_bytes,
                    uint64_t* kernel_launches);

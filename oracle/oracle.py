@@ -62,6 +62,8 @@ def lib():
         L.oracle_run.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32, vp, vp]
         L.oracle_tally_threads.restype = vp
         L.oracle_tally_threads.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32, vp]
+        L.oracle_tally_threads_at.restype = vp
+        L.oracle_tally_threads_at.argtypes = [vp, u32, C.c_char_p, u32, u32, vp, vp, u32, vp, u64]
         L.oracle_free.argtypes = [vp]
         L.oracle_has_error.argtypes = [vp, vp]
         L.oracle_has_error.restype = C.c_int
@@ -115,8 +117,11 @@ def _py_value(kind, bits):
 
 
 def run(raw_streams, registry, stream_infos=None, want_timeline=False, threads=0, device_index=0,
-        labels=None) -> OracleResult:
-    """Run the oracle over RawStream objects in (hostname, pid, tid) order."""
+        labels=None, floor_last_ts=0) -> OracleResult:
+    """Run the oracle over RawStream objects in (hostname, pid, tid) order.
+
+    threads > 0: the sharded tally (no timeline, no orphan list); floor_last_ts then lower-bounds the
+    truncation end -- the global last timestamp when the streams are one rank's shard."""
     L = lib()
     flat = flatten_registry(registry)
     n = len(raw_streams)
@@ -133,8 +138,8 @@ def run(raw_streams, registry, stream_infos=None, want_timeline=False, threads=0
                                          raw_streams[i].tid or 0, i))
     flush = (C.c_uint32 * max(n, 1))(*fo) if fo != list(range(n)) else None
     if threads:
-        h = L.oracle_tally_threads(flat.schemas, flat.n_schemas, flat.kinds, len(flat.function_names), n,
-                                   ptrs, sizes, threads, group)
+        h = L.oracle_tally_threads_at(flat.schemas, flat.n_schemas, flat.kinds, len(flat.function_names), n,
+                                      ptrs, sizes, threads, group, int(floor_last_ts))
     else:
         h = L.oracle_run(flat.schemas, flat.n_schemas, flat.kinds, len(flat.function_names), n, ptrs, sizes,
                          1 if want_timeline else 0, group, flush)

@@ -43,6 +43,7 @@ struct HostStream {
   int64_t pid, tid;
   const uint8_t* data;
   uint64_t size;
+  bool host_none;  // hostname None (record sources): "Host None pid .." in the timeline (sinks.py:367)
 };
 
 struct hg_ctx {
@@ -161,6 +162,9 @@ struct hg_ctx {
   // truncation flush order (hg_set_flush_order)
   bool flush_order = false;
   DBuf<uint32_t> d_flush_rank, d_flush_stream;
+  // multi-GPU merge (merge.cu): results replaced by the all-reduced ones
+  bool merged = false;
+  DBuf<uint32_t> d_merge_map;
 };
 
 // counter slots in d_counters

@@ -445,7 +445,7 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
 
 int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid, const void* data, uint64_t size) {
   if (!ctx || (size && !data)) return HG_EARG;
-  ctx->streams.push_back(HostStream{hostname ? hostname : "", pid, tid, (const uint8_t*)data, size});
+  ctx->streams.push_back(HostStream{hostname ? hostname : "", pid, tid, (const uint8_t*)data, size, hostname == nullptr});
   ctx->staged = false;
   ctx->have_results = false;
   return HG_OK;
@@ -769,6 +769,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   cudaSetDevice(ctx->cfg.device);
   ctx->want = want;
   ctx->have_results = false;
+  ctx->merged = false;
   ctx->phase1_done = false;
   bool fast = ctx->path_opt != 1 && !(want & HG_WANT_TIMELINE);
   bool retried = false;

@@ -35,7 +35,7 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   for (uint32_t s = 0; s < ns; s++) {
     const HostStream& hs = ctx->streams[s];
     std::string a = std::to_string(hs.pid), b = std::to_string(hs.tid);
-    std::string c = json_quote("Host " + hs.host + " pid " + a);
+    std::string c = json_quote("Host " + (hs.host_none ? std::string("None") : hs.host) + " pid " + a);
     for (const std::string* x : {&a, &b, &c}) {
       sstr.insert(sstr.end(), x->begin(), x->end());
       sstr_off.push_back(sstr.size());

@@ -1,174 +1,306 @@
-"""Multi-GPU runs: one process per GPU, streams sharded per rank, NCCL for the two real exchanges.
+"""Multi-GPU runs: one process per GPU, streams sharded per rank, collectives for the real exchanges.
 
 The interval state is per (hostname, pid, tid) stream (pipeline.py:158-161) and
 the tally is a commutative monoid (aggregator.py:1-9), so ranks own disjoint
-stream sets and need exactly two collectives:
-  1. all-reduce MAX of the local last timestamp before truncated spans are
-     finalised -- truncation ends at the GLOBAL last ts (pipeline.py:152, :235);
-  2. the tally merge: dense per-function host rows and (name-aligned) device
-     rows reduced with SUM / MIN / MAX (aggregator.py:35-76 semantics).
-128-bit sums travel as three int64 limbs (lo32, hi32, signed hi64) so the
-SUM all-reduce is exact for any rank count below 2^31.  Extrema travel
-sign-biased so int64 MIN/MAX order equals the unsigned/128-bit order for the
-values the engine produces.  Identity sets, drops and orphans are gathered as
-Python objects (small).
+stream sets (`partition_streams`: LPT by bytes) and exchange:
 
-`merge_dense` / `limbs` are pure tensor functions so the merge runs on CPU
-gloo in tests (tests/test_distributed.py) exactly as on NCCL.
+  1. MAX of [local last timestamp, failure status] -- truncated spans end at the
+     GLOBAL last ts (pipeline.py:152, :235), and a rank whose engine failed
+     stops every rank instead of leaving them in the next collective;
+  2. the device-name lists (all-gather of bytes) -> one global name order;
+  3. the tally merge (aggregator.py:35-76): every rank's engine writes its
+     device-resident rows, IntervalStats and span counts into one int64 buffer
+     in a rank-independent layout (hg_merge_export, csrc/merge.cu); a SUM and a
+     MAX all-reduce over that buffer ARE merge_tallies; hg_merge_import installs
+     the result.  No row crosses Python on the way;
+  4. only when some rank hit one: the trace errors (the first in the
+     reference's pull order wins, results.error_key over GLOBAL stream
+     indices) and the orphan exits (gathered, then put in mux order).
+
+`Comm` wraps torch.distributed: tensors live on the GPU for NCCL and on the
+CPU for gloo, so the same code runs in the world-size-2 CPU tests.
 """
 
 from __future__ import annotations
 
-from .results import build_report, orphan_list
-from .tally import TallyReport
+from types import SimpleNamespace
 
-MASK32 = (1 << 32) - 1
+from .abi import HG_TRACE_ERROR, HG_WANT_TALLY
+from .errors import EngineError
+from .results import build_report, error_key, first_error, make_exception, orphan_list
 
-
-def limbs(value: int):
-    """signed 128-bit -> (lo32, hi32, hi64) with value = hi64*2^64 + hi32*2^32 + lo32."""
-    lo = value & ((1 << 64) - 1)
-    hi = value >> 64
-    return [lo & MASK32, lo >> 32, hi]
+STATUS_OK, STATUS_TRACE, STATUS_ENGINE, STATUS_INPUT = 0, 1, 2, 3
+_BIAS = 1 << 63
 
 
-def unlimbs(l0: int, l1: int, h: int) -> int:
-    return l0 + (l1 << 32) + (h << 64)
+def partition_streams(sizes, world_size: int, keys=None) -> list:
+    """Assign whole streams to ranks by LPT on byte size: largest first onto the
+    least-loaded rank (ties: lower rank).  Streams with equal ``keys`` entries (one (hostname, pid,
+    tid) identity, which shares one LIFO stack, pipeline.py:156-161) go to one rank together.
+    Returns, per rank, its global stream indices in ascending (= mux) order."""
+    n = len(sizes)
+    if world_size < 1:
+        raise ValueError("world_size must be >= 1")
+    groups = {}
+    for i in range(n):
+        groups.setdefault(keys[i] if keys is not None else i, []).append(i)
+    units = sorted(groups.values(), key=lambda g: (-sum(sizes[i] for i in g), g[0]))
+    load = [0] * world_size
+    out = [[] for _ in range(world_size)]
+    for g in units:
+        r = min(range(world_size), key=lambda k: (load[k], k))
+        out[r].extend(g)
+        load[r] += sum(sizes[i] for i in g)
+    return [sorted(x) for x in out]
 
 
-def encode_rows(rows, keys):
-    """rows: {key: (count, errors, sum, min, max)} -> flat int lists aligned to `keys`.
-
-    Returns (sum_part, min_part, max_part) where sum_part holds count, errors and
-    the sum limbs; extrema are clamped to int64 (engine values fit) and biased
-    only implicitly: int64 MIN/MAX equals the integer order.
-    """
-    big = (1 << 63) - 1
-    s, mn, mx = [], [], []
-    for k in keys:
-        r = rows.get(k)
-        if r is None:
-            s += [0, 0, 0, 0, 0]
-            mn.append(big)
-            mx.append(-big - 1)
-            continue
-        count, errs, total, lo, hi = r
-        s += [count, errs, *limbs(total)]
-        mn.append(lo)
-        mx.append(hi)
-    return s, mn, mx
+def pack_exception(e: BaseException):
+    """(class, str, attributes): exceptions whose __init__ formats its arguments do not unpickle."""
+    return (type(e), str(e), dict(getattr(e, "__dict__", {})))
 
 
-def decode_rows(keys, s, mn, mx):
-    out = {}
-    for i, k in enumerate(keys):
-        count, errs, l0, l1, h = s[5 * i: 5 * i + 5]
-        if count:
-            out[k] = (count, errs, unlimbs(l0, l1, h), mn[i], mx[i])
+def unpack_exception(packed) -> BaseException:
+    cls, text, attrs = packed
+    e = cls.__new__(cls)
+    BaseException.__init__(e, text)
+    e.__dict__.update(attrs)
+    return e
+
+
+class Comm:
+    """torch.distributed collectives on int64 / uint8 tensors (GPU for NCCL, CPU for gloo)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.torch = torch
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        nccl = dist.get_backend(group) == "nccl"
+        self.device = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+
+    def max_i64(self, values):
+        t = self.torch.tensor(values, dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return t.tolist()
+
+    def all_reduce_(self, t, op: str):
+        ops = {"sum": self.dist.ReduceOp.SUM, "max": self.dist.ReduceOp.MAX, "min": self.dist.ReduceOp.MIN}
+        self.dist.all_reduce(t, op=ops[op], group=self.group)
+
+    def all_gather_bytes(self, blob: bytes) -> list:
+        torch = self.torch
+        n = torch.tensor([len(blob)], dtype=torch.int64, device=self.device)
+        sizes = [torch.zeros_like(n) for _ in range(self.world)]
+        self.dist.all_gather(sizes, n, group=self.group)
+        sizes = [int(s.item()) for s in sizes]
+        cap = max(max(sizes), 1)
+        mine = torch.zeros(cap, dtype=torch.uint8)
+        if blob:
+            mine[: len(blob)] = torch.frombuffer(bytearray(blob), dtype=torch.uint8)
+        mine = mine.to(self.device)
+        bufs = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(bufs, mine, group=self.group)
+        return [bytes(b[:k].cpu().numpy().tobytes()) for b, k in zip(bufs, sizes)]
+
+    def all_gather_object(self, obj) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+
+def _names_blob(names):
+    enc = [n.encode("utf-8") for n in names]
+    offs = [0]
+    for b in enc:
+        offs.append(offs[-1] + len(b))
+    return b"".join(enc), offs
+
+
+def _split_names(blob: bytes) -> list:
+    """Inverse of the per-rank blob: u32 count, u32 lengths, then the bytes."""
+    import struct
+
+    if not blob:
+        return []
+    (n,) = struct.unpack_from("<I", blob, 0)
+    lens = struct.unpack_from(f"<{n}I", blob, 4)
+    out, at = [], 4 + 4 * n
+    for k in lens:
+        out.append(blob[at: at + k].decode("utf-8"))
+        at += k
     return out
 
 
-def merge_dense(local_rows, keys, all_reduce):
-    """Reduce aligned row tables across ranks with a caller-supplied all_reduce(list, op)."""
-    s, mn, mx = encode_rows(local_rows, keys)
-    s = all_reduce(s, "sum")
-    mn = all_reduce(mn, "min")
-    mx = all_reduce(mx, "max")
-    return decode_rows(keys, s, mn, mx)
+def _join_names(names) -> bytes:
+    import struct
 
-
-def torch_all_reduce(group=None, device=None):
-    import torch
-    import torch.distributed as dist
-
-    ops = {"sum": dist.ReduceOp.SUM, "min": dist.ReduceOp.MIN, "max": dist.ReduceOp.MAX}
-
-    def fn(values, op):
-        if not values:
-            return values
-        t = torch.tensor(values, dtype=torch.int64, device=device)
-        dist.all_reduce(t, op=ops[op], group=group)
-        return t.tolist()
-
-    return fn
+    enc = [n.encode("utf-8") for n in names]
+    return struct.pack(f"<I{len(enc)}I", len(enc), *map(len, enc)) + b"".join(enc)
 
 
 class ShardedRun:
-    """Drive one engine over this rank's streams; merge across ranks when world_size > 1."""
+    """Drive one engine over this rank's streams and merge across ranks.
 
-    def __init__(self, engine, registry, world_size=1, rank=0, device=None):
+    ``stream_global[i]``: global index of local stream i in the whole trace's (hostname, pid, tid)
+    order; ``global_streams``: the whole trace's RawStream-like objects (hostname, pid, tid, name)
+    in that order (labels, identities); ``comm``: a Comm, or None for one rank."""
+
+    def __init__(self, engine, registry, comm=None, stream_global=None, global_streams=None):
         self.engine = engine
         self.registry = registry
-        self.world_size = world_size
-        self.rank = rank
-        self.device = device
+        self.comm = comm
+        self.world = comm.world if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
+        self.stream_global = stream_global
+        self.global_streams = global_streams
         self.global_last_ts = None
+        self.rc = 0
+        self._merged = None
+        self._names = None
 
-    def step(self) -> dict:
+    # ------------------------------------------------------------------ step
+    def step(self, want=HG_WANT_TALLY, input_error=None) -> dict:
+        """Phase 1, the last-ts exchange, composition and the tally merge.  ``input_error``: an exception
+        this rank met before the engine (e.g. a stream file header, tracefile.py:491-499), keyed by the
+        global index of the stream it belongs to; every rank raises the first such error."""
         eng = self.engine
-        L, ctx = eng._L, eng._ctx
-        import ctypes as C
-
-        rc = L.hg_run_local(ctx, 1)
-        eng._check(rc, "hg_run_local")
-        last, nev = C.c_uint64(), C.c_uint64()
-        eng._check(L.hg_local_last_ts(ctx, C.byref(last), C.byref(nev)), "hg_local_last_ts")
-        g = last.value
-        if self.world_size > 1:
-            import torch
-            import torch.distributed as dist
-
-            # u64 timestamps < 2^63 in practice; bias keeps the order exact anyway
-            t = torch.tensor([g - (1 << 63)], dtype=torch.int64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            g = t.item() + (1 << 63)
+        sg = self.stream_global if self.stream_global is not None else list(range(len(eng._streams)))
+        status, failure, last = STATUS_OK, None, 0
+        if input_error is not None:
+            status, failure = STATUS_INPUT, ((0, input_error[0]), pack_exception(input_error[1]))
+        else:
+            try:
+                eng.run_local(want)
+                last = eng.local_last_ts()
+            except Exception as e:  # noqa: BLE001  (an engine failure: reported to every rank)
+                status, failure = STATUS_ENGINE, ((2, self.rank), pack_exception(e))
+        g, gstatus = last, status
+        if self.world > 1:
+            g, gstatus = self.comm.max_i64([last - _BIAS, status])
+            g += _BIAS
+        if gstatus:
+            self._raise_first(failure)
         self.global_last_ts = g
-        rc = L.hg_finish(ctx, g)
-        if rc not in (0, 1):
-            eng._check(rc, "hg_finish")
+        self.rc = eng.finish(g)
+        if self.world > 1:
+            self._merge(sg)
         k, tot, h2d, d2h, nl = eng.timing()
         walk, chain, decode = eng.phase_timing()
         return {"device_ms": tot, "phase1_ms": k, "walk_ms": walk, "chain_ms": chain, "decode_ms": decode,
-                "h2d_bytes": h2d, "d2h_bytes": d2h, "launches": nl, "rc": rc}
+                "h2d_bytes": h2d, "d2h_bytes": d2h, "launches": nl, "rc": self.rc}
 
-    def report(self, stream_infos) -> TallyReport:
+    def _raise_first(self, failure):
+        packed = [failure] if self.world == 1 else self.comm.all_gather_object(failure)
+        key, exc = min((f for f in packed if f is not None), key=lambda f: f[0])
+        if key[0] == 2 and failure is None:
+            raise EngineError(f"rank {key[1]} failed: {unpack_exception(exc)}")
+        raise unpack_exception(exc)
+
+    def _merge(self, sg):
+        """Names agreement, then the device-resident tally merge (two all-reduces, csrc/merge.cu)."""
+        import numpy as np
+        import torch
+
+        eng, comm = self.engine, self.comm
+        names = eng.device_names()
+        gathered = [_split_names(b) for b in comm.all_gather_bytes(_join_names(names))]
+        gnames = sorted({n for g in gathered for n in g})
+        pos = {n: i for i, n in enumerate(gnames)}
+        n_gs = len(self.global_streams) if self.global_streams is not None else max(sg, default=-1) + 1
+        total, sum_n = eng.merge_size(len(gnames), n_gs)
+        buf = torch.empty(total, dtype=torch.int64, device=eng.tensor_device())
+        eng.merge_export(buf.data_ptr(), [pos[n] for n in names], len(gnames), sg, n_gs)
+        coll = buf if buf.device == comm.device else buf.to(comm.device)
+        comm.all_reduce_(coll[:sum_n], "sum")
+        comm.all_reduce_(coll[sum_n:], "max")
+        host = np.ascontiguousarray(coll.cpu().numpy())
+        eng.merge_import(host.ctypes.data, gnames, n_gs)
+        self._names = gnames
+        self._merged = host
+        self._n_gs = n_gs
+
+    # ------------------------------------------------------------------ results
+    def stats(self) -> dict:
+        return self.engine.stats()
+
+    def _global_spans(self):
+        from .engine import MERGE_STATS
+
+        return [int(x) for x in self._merged[MERGE_STATS: MERGE_STATS + self._n_gs]]
+
+    def result(self, stream_infos=None, labels=None, orphan_labels=None):
+        """(report, stats, orphans) of the whole trace, or raise the trace error the reference's single
+        pipeline would raise (the same one on every rank)."""
+        from .engine import MERGE_STATS
+
         eng = self.engine
         flat = eng._flat
-        names = eng.device_names()
-        rows = eng.tally_rows()
-        idents = [(s.hostname, s.pid, s.tid) for s in eng._streams]
-        spans = eng.stream_spans()
-        if self.world_size == 1:
-            return build_report(flat, rows, names, stream_infos, idents, spans)
-        import torch.distributed as dist
+        stats = self.stats()
+        if self.world == 1:
+            gs = eng._streams
+            idents = [(s.hostname, s.pid, s.tid) for s in gs]
+            spans = eng.stream_spans()
+            sg = list(range(len(gs)))
+            any_error = self.rc == HG_TRACE_ERROR
+        else:
+            gs = self.global_streams
+            idents = [(s.hostname, s.pid, s.tid) for s in gs]
+            spans = self._global_spans()
+            sg = self.stream_global
+            any_error = int(self._merged[MERGE_STATS - 1]) > 0
+        if orphan_labels is None:
+            orphan_labels = [f"{s.hostname}/{s.pid}/{s.tid}" for s in gs]
+        if labels is None:
+            labels = [getattr(s, "name", "") for s in gs]
+        orph_local = [SimpleNamespace(stream=sg[o.stream], function=o.function, ts=o.ts, seq=o.seq)
+                      for o in eng.orphans_raw()]
+        if any_error:
+            err = self._first_error(sg, labels)
+            orphans = orph_local if self.world == 1 else [o for g in self.comm.all_gather_object(orph_local) for o in g]
+            key, exc, cut = err
+            olist = orphan_list(orphans, orphan_labels, flat, cutoff=key, cut_streams=cut)
+            return None, stats, olist, unpack_exception(exc)
+        if self.world > 1 and stats["orphan_exits"]:
+            orphans = [o for g in self.comm.all_gather_object(orph_local) for o in g]
+        else:
+            orphans = orph_local
+        olist = orphan_list(orphans, orphan_labels, flat)
+        report = build_report(flat, eng.tally_rows(), eng.device_names(), stream_infos, idents, spans)
+        return report, stats, olist, None
 
-        host = {("host", flat.function_names[r[1]]): r[2:] for r in rows if r[0] == 0}
-        dev = {("device", names[r[1]]): r[2:] for r in rows if r[0] == 1}
-        # device-name dictionaries differ per rank: agree on one key order first
-        gathered = [None] * self.world_size
-        dist.all_gather_object(gathered, sorted(dev))
-        dev_keys = sorted({k for g in gathered for k in g})
-        host_keys = [("host", n) for n in flat.function_names]
-        merged = merge_dense({**host, **dev}, host_keys + dev_keys, torch_all_reduce(device="cuda"))
-        infos = [None] * self.world_size
-        dist.all_gather_object(infos, (list(stream_infos or []), [i for i, n in zip(idents, spans) if n]))
-        rep = TallyReport(fingerprint=self.registry.fingerprint,
-                          backends=(f"BACKEND_{self.registry.api_name.upper()}",))
-        from .tally import TallyRow
+    def _first_error(self, sg, labels):
+        """The error the reference's muxer raises first: per rank the local first candidate (global
+        stream indices), then the minimum of error_key over all ranks."""
+        from .tracefile import RawStream
 
-        for (sec, name), (count, errs, total, mn, mx) in merged.items():
-            rep.rows[(sec, name)] = TallyRow(name, sec, total, count, mn, mx, errs)
-        hosts, procs, threads = set(), set(), set()
-        for inf, span_ids in infos:
-            for i in inf:
-                hosts.add(i.hostname)
-                procs.add((i.hostname, i.pid))
-                threads.add((i.hostname, i.pid, i.tid))
-                if i.dropped_count:
-                    rep.dropped[(i.hostname, i.pid, i.tid)] = i.dropped_count
-            for h, p, t in span_ids:
-                hosts.add(h)
-                procs.add((h, p))
-                threads.add((h, p, t))
-        rep.hostnames, rep.processes, rep.threads = frozenset(hosts), frozenset(procs), frozenset(threads)
+        eng = self.engine
+        cands = [SimpleNamespace(code=c.code, stream=sg[c.stream], seq=c.seq, offset=c.offset, ts=c.ts,
+                                 prev_ts=c.prev_ts, aux=c.aux, local=c.stream) for c in eng.errors_raw()]
+        cut = {}
+        for c in cands:
+            if c.code in (1, 2, 3, 4, 5, 6, 7, 8, 9) and (c.stream not in cut or c.seq < cut[c.stream]):
+                cut[c.stream] = c.seq
+        mine = None
+        e = first_error(cands)
+        if e is not None:
+            s = eng._streams[e.local]
+            named = RawStream(s.hostname, s.pid, s.tid, labels[e.stream], s.data, getattr(s, "info", None))
+            mine = (error_key(e), pack_exception(make_exception(e, named, eng._flat)), cut)
+        allc = [mine] if self.world == 1 else self.comm.all_gather_object(mine)
+        key, exc, _ = min((c for c in allc if c is not None), key=lambda c: c[0])
+        cuts = {}
+        for c in allc:
+            if c is not None:
+                cuts.update(c[2])
+        return key, exc, cuts
+
+    # the round-1 name, kept for callers that only want the tally
+    def report(self, stream_infos=None):
+        rep, _, _, err = self.result(stream_infos)
+        if err is not None:
+            raise err
         return rep

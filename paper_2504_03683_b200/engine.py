@@ -21,6 +21,7 @@ from .errors import EngineError, UnsupportedTraceError
 from .results import build_report, error_key, first_error, make_exception, orphan_list, rows_from_native
 
 HG_EUNSUPPORTED = -5
+MERGE_STATS = 8  # IntervalStats counters + trace-error ranks at the head of the merge buffer (csrc/merge.cu)
 OPT_PATH = 1
 OPT_RANGE_BYTES = 2
 PATH_AUTO, PATH_EXACT, PATH_FAST = 0, 1, 2
@@ -52,6 +53,7 @@ class Engine:
             msg = self._L.hg_last_error(self._ctx).decode() if self._ctx else "hg_create failed"
             self.close()
             raise EngineError(msg)
+        self.device = device
         self._flat = None
         self._registry_key = None
         self._keep = []
@@ -140,7 +142,7 @@ class Engine:
             buf = C.c_char_p(data) if data else None
             self._keep.append(data)
             ptr, n = (C.cast(buf, C.c_void_p).value if buf else None), len(data)
-        h = (hostname if hostname is not None else "").encode()
+        h = hostname.encode() if hostname is not None else None  # NULL: hostname None
         self._check(self._L.hg_add_stream(self._ctx, h, int(pid or 0), int(tid or 0), ptr, n), "hg_add_stream")
 
     def stage(self):
@@ -162,6 +164,51 @@ class Engine:
         if rc not in (HG_OK, HG_TRACE_ERROR):
             self._check(rc, "hg_run")
         return rc
+
+    def tensor_device(self):
+        import torch
+
+        return torch.device("cuda", self.device)
+
+    # -- split run for sharded (multi-GPU) use: distributed.ShardedRun
+    def run_local(self, want=HG_WANT_TALLY):
+        """hg_run_local: phase 1 over this context's streams; raises on an engine failure."""
+        self._check(self._L.hg_run_local(self._ctx, want), "hg_run_local")
+
+    def local_last_ts(self) -> int:
+        last = C.c_uint64()
+        self._check(self._L.hg_local_last_ts(self._ctx, C.byref(last), None), "hg_local_last_ts")
+        return last.value
+
+    def finish(self, global_last_ts: int) -> int:
+        """hg_finish: composition and truncation at the global last timestamp; HG_OK or HG_TRACE_ERROR."""
+        rc = self._L.hg_finish(self._ctx, global_last_ts)
+        if rc not in (HG_OK, HG_TRACE_ERROR):
+            self._check(rc, "hg_finish")
+        return rc
+
+    def merge_size(self, n_dev_global: int, n_streams_global: int):
+        """(total int64 elements, elements of the SUM region) of the merge buffer (csrc/merge.cu)."""
+        sum_n = C.c_uint64()
+        total = self._L.hg_merge_size(len(self._flat.function_names), n_dev_global, n_streams_global,
+                                      C.byref(sum_n))
+        return total, sum_n.value
+
+    def merge_export(self, dst_ptr: int, dev_map, n_dev_global: int, stream_global, n_streams_global: int):
+        """hg_merge_export into device memory at dst_ptr (a torch tensor on this engine's GPU)."""
+        dm = (C.c_uint32 * max(len(dev_map), 1))(*dev_map)
+        sg = (C.c_uint32 * max(len(stream_global), 1))(*stream_global)
+        self._check(self._L.hg_merge_export(self._ctx, C.c_void_p(dst_ptr), dm, len(dev_map), n_dev_global, sg,
+                                            n_streams_global), "hg_merge_export")
+
+    def merge_import(self, host_ptr: int, names, n_streams_global: int):
+        """hg_merge_import from host memory: the reduced buffer plus the global device-name list."""
+        enc = [n.encode("utf-8") for n in names]
+        offs = [0]
+        for b in enc:
+            offs.append(offs[-1] + len(b))
+        self._check(self._L.hg_merge_import(self._ctx, C.c_void_p(host_ptr), len(names), n_streams_global,
+                                            b"".join(enc), (C.c_uint64 * len(offs))(*offs)), "hg_merge_import")
 
     def timing(self):
         k, t = C.c_float(), C.c_float()

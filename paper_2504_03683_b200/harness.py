@@ -9,10 +9,11 @@ from .tally import TallyReport
 from .tracefile import open_trace_reader
 
 
-def tally_trace(trace_dir, engine=None) -> TallyReport:
-    """One GPU pipeline pass producing the tally report for a finalized trace."""
+def tally_trace(trace_dir, engine=None, distributed=False) -> TallyReport:
+    """One GPU pipeline pass producing the tally report for a finalized trace (harness.py:117-121).
+    ``distributed``: shard the streams over the ranks of a torch.distributed group (run_pipeline)."""
     reader = open_trace_reader(trace_dir)
-    return run_pipeline(reader, sinks=[TallySink()], engine=engine)["tally"]
+    return run_pipeline(reader, sinks=[TallySink()], engine=engine, distributed=distributed)["tally"]
 
 
 def write_tally_json(report: TallyReport, path):

@@ -20,7 +20,7 @@ import json
 import threading
 from dataclasses import dataclass, field
 
-from .errors import PipelineError, UnsupportedTraceError
+from .errors import HapitraceError, PipelineError, UnsupportedTraceError
 from .registry import SchemaRegistry
 from .tally import TallyReport
 from .tracefile import RECORD_HEADER, RawStream, encode_record, stream_bytes
@@ -299,15 +299,31 @@ def default_engine():
     return eng
 
 
-def run_pipeline(source, sinks=(), registry=None, engine=None) -> PipelineResult:
-    """One GPU pass: decode, mux-order semantics, interval pairing, sinks' results."""
+def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False) -> PipelineResult:
+    """One GPU pass: decode, mux-order semantics, interval pairing, sinks' results.
+
+    ``distributed``: False (this process's GPU does the whole trace), True (the default
+    torch.distributed group) or a ProcessGroup: every rank calls run_pipeline on the same source,
+    owns the streams `distributed.partition_streams` gives it, and every rank returns the result of
+    the whole trace (streams per rank, last-ts and tally merges as collectives)."""
     if registry is None:
         registry = getattr(source, "registry", None)
         if registry is None:
             raise PipelineError("a registry is required when source is not a TraceReader")
     if not isinstance(registry, SchemaRegistry):  # e.g. a reference registry object
         registry = SchemaRegistry.from_dict(registry.to_dict())
-    raws, infos = _resolve_source(source, registry)
+    comm = None
+    if distributed is not False:
+        from .distributed import Comm
+
+        comm = Comm(None if distributed is True else distributed)
+        if comm.world == 1:
+            comm = None
+    if comm is None:
+        raws, infos = _resolve_source(source, registry)
+    else:
+        shard = _resolve_sharded(source, registry, comm)
+        infos = shard.infos
     names = [s.name for s in sinks]
     if len(set(names)) != len(names):
         raise PipelineError(f"duplicate sink names: {names}")
@@ -317,6 +333,8 @@ def run_pipeline(source, sinks=(), registry=None, engine=None) -> PipelineResult
         if not isinstance(s, (TallySink, TimelineSink)) and not _is_passive(s):
             raise UnsupportedTraceError(
                 f"sink {s.name!r} needs per-message callbacks; hapigpu serves TallySink/TimelineSink")
+    if timeline and comm is not None:
+        raise UnsupportedTraceError("TimelineSink in a multi-rank run: run the timeline on one rank")
     device_index = {s.device_index for s in timeline}
     if len(device_index) > 1:
         raise UnsupportedTraceError("several TimelineSinks with different device_index")
@@ -325,12 +343,15 @@ def run_pipeline(source, sinks=(), registry=None, engine=None) -> PipelineResult
         if infos is not None and hasattr(s, "on_streams"):
             s.on_streams(infos)
     eng = engine or default_engine()
-    labels = [r.name for r in raws]
-    olabels = [f"{r.hostname}/{r.pid}/{r.tid}" for r in raws]
     res = None
     try:
-        res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels, orphan_labels=olabels,
-                      timeline_device_index=next(iter(device_index), 0))
+        if comm is None:
+            labels = [r.name for r in raws]
+            olabels = [f"{r.hostname}/{r.pid}/{r.tid}" for r in raws]
+            res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels,
+                          orphan_labels=olabels, timeline_device_index=next(iter(device_index), 0))
+        else:
+            res = _run_sharded(eng, registry, shard, comm)
     finally:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
         for s in sinks:
             hook = getattr(s, "on_diagnostics", None)
@@ -347,3 +368,70 @@ def run_pipeline(source, sinks=(), registry=None, engine=None) -> PipelineResult
     timing = {"kernel_ms": res.kernel_ms, "total_ms": res.total_ms, "h2d_bytes": res.h2d_bytes,
               "d2h_bytes": res.d2h_bytes, "launches": res.launches}
     return PipelineResult(results, stats, res.orphans, timing)
+
+
+# ---------------------------------------------------------------------------
+# multi-rank runs
+
+
+@dataclass
+class _Shard:
+    raws: list            # this rank's streams (identity-merged), in mux order
+    stream_global: list   # their global indices
+    global_streams: list  # identities + labels of the whole trace, in mux order
+    infos: list | None
+    input_error: tuple | None  # (global index, exception) met while reading this rank's files
+
+
+def _resolve_sharded(source, registry, comm) -> _Shard:
+    """This rank's part of the source.  Trace directories: sizes from the file system, each rank reads
+    only its own files (grouped by identity, pipeline.py:156-161).  In-memory sources: every rank holds
+    the whole trace already and keeps its part."""
+    from .distributed import partition_streams
+    from .tracefile import open_trace_reader
+
+    reader = None
+    if hasattr(source, "dir") and (hasattr(source, "metadata") or hasattr(source, "stream_sizes")):
+        reader = open_trace_reader(source.dir) if not hasattr(source, "stream_sizes") else source
+    if reader is None:
+        raws, infos = _resolve_source(source, registry)
+        parts = partition_streams([len(r.data) for r in raws], comm.world)
+        mine = parts[comm.rank]
+        ids = [RawStream(r.hostname, r.pid, r.tid, r.name, b"") for r in raws]
+        return _Shard([raws[i] for i in mine], mine, ids, infos, None)
+    infos = reader.stream_infos()
+    entries = reader._entries
+    keys = [(e["hostname"], e["pid"], e["tid"]) for e in entries]
+    parts = partition_streams(reader.stream_sizes(), comm.world, keys)
+    mine = parts[comm.rank]
+    ids = [RawStream(e["hostname"], e["pid"], e["tid"], e["file"], b"") for e in entries]
+    raws, err = [], None
+    for i in mine:
+        try:
+            raws.extend(reader.raw_streams(select=[i]))
+        except HapitraceError as e:
+            err = (i, e)
+            break
+    if err is not None:
+        return _Shard([], [], ids, infos, err)
+    merged = merge_same_identity(raws)
+    # a merged identity keeps the global index of its first file
+    first = {}
+    for i in mine:
+        first.setdefault(keys[i], i)
+    return _Shard(merged, [first[(r.hostname, r.pid, r.tid)] for r in merged], ids, infos, None)
+
+
+def _run_sharded(eng, registry, shard, comm):
+    from .distributed import ShardedRun
+    from .engine import RunResult
+
+    eng.set_registry(registry)
+    eng.set_streams(shard.raws)
+    run = ShardedRun(eng, registry, comm, shard.stream_global, shard.global_streams)
+    info = run.step(input_error=shard.input_error)
+    labels = [s.name for s in shard.global_streams]
+    olabels = [f"{s.hostname}/{s.pid}/{s.tid}" for s in shard.global_streams]
+    report, stats, orphans, error = run.result(shard.infos, labels, olabels)
+    return RunResult(report, stats, orphans, error, None, info["phase1_ms"], info["device_ms"], info["h2d_bytes"],
+                     info["d2h_bytes"], info["launches"])

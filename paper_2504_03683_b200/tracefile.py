@@ -84,10 +84,19 @@ class TraceReader:
             for e in self._entries
         ]
 
-    def raw_streams(self) -> list:
-        """Read every stream file in index order, validating its 16-byte header."""
+    def stream_sizes(self) -> list:
+        """Byte size of every stream file in index order, without reading it (0 for unread files);
+        the multi-GPU partitioner balances ranks by these."""
+        return [(self.dir / e["file"]).stat().st_size if e["event_count"] else 0 for e in self._entries]
+
+    def raw_streams(self, select=None) -> list:
+        """Read every stream file (or the index positions in ``select``) in index order, validating
+        its 16-byte header."""
         out = []
-        for e in self._entries:
+        select = None if select is None else set(select)
+        for i, e in enumerate(self._entries):
+            if select is not None and i not in select:
+                continue
             name = e["file"]
             data = (self.dir / name).read_bytes() if e["event_count"] else b""
             check_file_header(data, name)

@@ -1,13 +1,15 @@
 """Two ranks on one B200 (gloo carries the collectives; the engine path is the real one).
 
-Each rank owns half of the streams, runs phase 1 on the GPU, all-reduces the
-last timestamp (truncated spans end at the GLOBAL last ts, pipeline.py:152),
-finishes, and merges its dense tally rows with the other rank's through
-ShardedRun.report -- the code bench.py --gpus N runs over NCCL.  The merged
-report must equal the single-process oracle of the whole trace."""
+Every rank calls run_pipeline(reader, ..., distributed=True): it reads only the stream files the LPT
+partitioner gives it, runs phase 1 on the GPU, all-reduces [last ts, status] (truncated spans end at
+the GLOBAL last ts, pipeline.py:152), composes, and merges its device-resident tally rows through
+hg_merge_export / two all-reduces / hg_merge_import (csrc/merge.cu) -- the code bench.py --gpus N
+runs over NCCL.  Every rank's report, IntervalStats and orphan list must equal the single-process
+oracle of the whole trace; a corrupt record must raise the same exception on both ranks."""
 
 import os
 import socket
+import tempfile
 
 import pytest
 import torch.multiprocessing as mp
@@ -23,60 +25,92 @@ def _free_port():
     return port
 
 
-def _workload():
-    from paper_2504_03683_b200 import synth
-
-    P = synth.PID_BASE
-    streams = [synth.StreamSpec(f"n{i % 2}", P + 100 * (i % 3), P + 100 * (i % 3) + i, 4000 + 1301 * i, 8800 + i)
-               for i in range(10)]
-    # unclosed calls (truncation at the global last ts), orphans and device records with per-rank names
-    return synth.Workload("dist", synth.ze_registry(), streams,
-                          dict(close_at_end=0, orphan_p=0.01, prof_p=0.3, max_depth=6),
-                          kernel_names=synth.kernel_pool(40))
-
-
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, case, tmp):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2504_03683_b200 import synth
-        from paper_2504_03683_b200.distributed import ShardedRun
+        from test_distributed import _corrupt, _generate
+        from paper_2504_03683_b200 import run_pipeline, synth
+        from paper_2504_03683_b200.distributed import pack_exception
         from paper_2504_03683_b200.engine import Engine
+        from paper_2504_03683_b200.pipeline import Sink, TallySink
+        from paper_2504_03683_b200.tracefile import open_trace_reader
 
-        wl = _workload()
-        raws = synth.generate(wl)
-        mine = raws[rank::world]
-        eng = Engine(device=0)
-        eng.set_registry(wl.registry)
-        eng.set_streams(mine)
-        eng.stage()
-        run = ShardedRun(eng, wl.registry, world_size=world, rank=rank)
-        info = run.step()
-        rep = run.report([r.info for r in mine])
+        class Diag(Sink):
+            name = "diag"
+
+            def on_diagnostics(self, orphans):
+                self.orphans = orphans
+
+        wl, raws = _generate()
+        if case == "corrupt":
+            raws = _corrupt(raws, 5, 40)
+        d = os.path.join(tmp, "trace")
         if rank == 0:
-            from oracle import oracle
-
-            want = oracle.run(raws, wl.registry, [r.info for r in raws])
-            q.put((rep == want.report, info["rc"], run.global_last_ts == want.last_ts, len(want.report.rows),
-                   eng.last_path()[0]))
+            synth.write(wl, raws, d)
+        dist.barrier()
+        eng = Engine(device=0)
+        diag = Diag()
+        try:
+            res = run_pipeline(open_trace_reader(d), [TallySink(), diag], engine=eng, distributed=True)
+            out = ("ok", res["tally"], vars(res.stats), res.orphans, diag.orphans, eng.last_path()[0])
+        except Exception as e:  # noqa: BLE001
+            out = ("raised", pack_exception(e), getattr(diag, "orphans", None))
         eng.close()
+        q.put((rank, out))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_ranks_one_gpu_merge_equals_oracle():
+def _run(case):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    for p in procs:
-        p.join(timeout=600)
-    assert all(p.exitcode == 0 for p in procs)
-    same, rc, last_ok, n_rows, path = q.get(timeout=10)
-    assert rc == 0 and last_ok and n_rows > 10 and path == 1
-    assert same
+    with tempfile.TemporaryDirectory() as tmp:
+        procs = [ctx.Process(target=_worker, args=(r, 2, port, q, case, tmp)) for r in range(2)]
+        for p in procs:
+            p.start()
+        outs = dict(q.get(timeout=600) for _ in procs)
+        for p in procs:
+            p.join(timeout=120)
+        assert all(p.exitcode == 0 for p in procs)
+    return outs
+
+
+def _oracle(case):
+    from oracle import oracle
+    from test_distributed import _corrupt, _generate
+
+    wl, raws = _generate()
+    if case == "corrupt":
+        raws = _corrupt(raws, 5, 40)
+    return oracle.run(raws, wl.registry, [r.info for r in raws])
+
+
+def test_two_ranks_one_gpu_equal_single_process_oracle():
+    outs = _run("clean")
+    want = _oracle("clean")
+    assert want.stats["truncated_spans"] > 0 and want.stats["orphan_exits"] > 0
+    for rank in (0, 1):
+        kind, rep, stats, orphans, diag, path = outs[rank]
+        assert kind == "ok" and path == 1
+        assert rep == want.report
+        assert stats == want.stats
+        assert orphans == want.orphans == diag
+
+
+def test_two_ranks_one_gpu_raise_the_reference_first_error():
+    from paper_2504_03683_b200.distributed import unpack_exception
+
+    outs = _run("corrupt")
+    want = _oracle("corrupt")
+    assert want.error is not None
+    for rank in (0, 1):
+        kind, packed, diag = outs[rank]
+        assert kind == "raised"
+        e = unpack_exception(packed)
+        assert type(e).__name__ == type(want.error).__name__ and str(e) == str(want.error)
+        assert diag == want.orphans
