@@ -158,6 +158,23 @@ int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid,
                   const void* data, uint64_t size);
 int hg_clear_streams(hg_ctx* ctx);
 
+/* the same stream, its bytes already in DEVICE memory of this context's GPU (a torch
+ * tensor's data_ptr, a GPUDirect-Storage buffer): staged with one HBM->HBM copy, no
+ * PCIe.  Caller-owned until hg_run returns. */
+int hg_add_stream_device(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid,
+                         const void* device_ptr, uint64_t size);
+/* the same stream, read by the engine from a FILE (bytes [offset, offset+size)); the
+ * 16-byte file header must already be validated (tracefile.py:491-499 messages).
+ * Replaces StreamCursor's whole-file read (tracefile.py:489): staging reads files and
+ * pageable host buffers through per-thread double-buffered pinned chunks, so file
+ * reads and PCIe transfers overlap; pinned host buffers go straight to DMA. */
+int hg_add_stream_file(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid,
+                       const char* path, uint64_t offset, uint64_t size);
+/* how the last staging moved the bytes: per source kind, host wall ms of the whole
+ * staging (file reads + copies), host threads used */
+int hg_ingest_stats(hg_ctx* ctx, uint64_t* pinned_bytes, uint64_t* pageable_bytes, uint64_t* file_bytes,
+                    uint64_t* device_bytes, float* ms, uint32_t* threads);
+
 /* copy all added streams to HBM now; later runs reuse the resident copy
  * (used to time the device-resident path separately from ingest). */
 int hg_stage(hg_ctx* ctx);

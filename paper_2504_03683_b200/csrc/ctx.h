@@ -38,13 +38,25 @@ struct DBuf {
   void release() { if (ptr) cudaFree(ptr); ptr = nullptr; n = 0; }
 };
 
+enum StreamSource { SRC_HOST = 0, SRC_DEVICE = 1, SRC_FILE = 2 };
+
 struct HostStream {
   std::string host;
   int64_t pid, tid;
-  const uint8_t* data;
+  const uint8_t* data;  // host (SRC_HOST) or device (SRC_DEVICE) bytes; null for files
   uint64_t size;
   bool host_none;  // hostname None (record sources): "Host None pid .." in the timeline (sinks.py:367)
+  int src = SRC_HOST;
+  std::string path;       // SRC_FILE
+  uint64_t file_off = 0;  // SRC_FILE: offset of the stream's first byte in the file
 };
+
+struct IngestStats {
+  uint64_t pinned_bytes = 0, pageable_bytes = 0, file_bytes = 0, device_bytes = 0;
+  float ms = 0;
+  int threads = 0;
+};
+struct IngestPool;  // ingest.cu
 
 struct hg_ctx {
   hg_config cfg{};
@@ -162,6 +174,9 @@ struct hg_ctx {
   // truncation flush order (hg_set_flush_order)
   bool flush_order = false;
   DBuf<uint32_t> d_flush_rank, d_flush_stream;
+  // ingest (ingest.cu): pinned staging pool and the last staging's numbers
+  IngestPool* ingest = nullptr;
+  IngestStats ingest_stats;
   // multi-GPU merge (merge.cu): results replaced by the all-reduced ones
   bool merged = false;
   DBuf<uint32_t> d_merge_map;
@@ -247,4 +262,6 @@ int init_run(hg_ctx* ctx);
 int launch_fast(hg_ctx* ctx);      // fast.cu
 int launch_phase1(hg_ctx* ctx);    // seg.cu
 int run_timeline(hg_ctx* ctx, uint64_t global_last_ts);  // timeline.cu
+int ingest_streams(hg_ctx* ctx);   // ingest.cu
+void ingest_free(hg_ctx* ctx);     // ingest.cu
 }

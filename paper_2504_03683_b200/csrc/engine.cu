@@ -249,6 +249,7 @@ void hg_destroy(hg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cfg.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ingest_free(ctx);
   ctx->d_schemas.release(); ctx->d_sid_map.release(); ctx->d_kinds.release(); ctx->d_field_role.release();
   ctx->d_data.release(); ctx->d_base.release(); ctx->d_size.release();
   ctx->d_tile_stream.release(); ctx->d_stream_tile0.release();
@@ -589,12 +590,8 @@ static int stage(hg_ctx* ctx) {
   CK(ctx->d_data.ensure(ctx->total_bytes + pad));
   CK(cudaMemsetAsync(ctx->d_data.ptr + ctx->total_bytes, 0, pad, ctx->stream));
   ctx->h2d_bytes = 0;
-  for (uint32_t s = 0; s < ns; s++) {
-    if (!ctx->streams[s].size) continue;
-    CK(cudaMemcpyAsync(ctx->d_data.ptr + ctx->base[s], ctx->streams[s].data, ctx->streams[s].size, cudaMemcpyHostToDevice,
-                       ctx->stream));
-    ctx->h2d_bytes += ctx->streams[s].size;
-  }
+  int irc = ingest_streams(ctx);  // pinned / pageable / file / device sources (ingest.cu)
+  if (irc) return irc;
   CK(ctx->d_base.ensure(std::max<uint32_t>(ns, 1)));
   CK(ctx->d_size.ensure(std::max<uint32_t>(ns, 1)));
   if (ns) {

@@ -18,6 +18,7 @@ from .abi import (
     HgTraceError, flatten_registry,
 )
 from .errors import EngineError, UnsupportedTraceError
+from .tracefile import FileStream
 from .results import build_report, error_key, first_error, make_exception, orphan_list, rows_from_native
 
 HG_EUNSUPPORTED = -5
@@ -106,7 +107,10 @@ class Engine:
         self._keep = []
         self._streams = list(raw_streams)
         for s in self._streams:
-            self.add_stream_ptr(s.hostname, s.pid, s.tid, s.data)
+            if isinstance(s, FileStream):
+                self.add_stream_file(s.hostname, s.pid, s.tid, s.path, 0, s.size)
+            else:
+                self.add_stream_ptr(s.hostname, s.pid, s.tid, s.data)
         self._set_flush_order()
 
     def _set_flush_order(self):
@@ -133,6 +137,40 @@ class Engine:
         self._streams = [RawStream(h, p, t, "", b"") for h, p, t in idents]
         for (h, p, t), ten in zip(idents, tensors):
             self.add_stream_ptr(h, p, t, ten.data_ptr() if ten.numel() else 0, ten.numel())
+
+    def add_stream_file(self, hostname, pid, tid, path, offset, size):
+        """hg_add_stream_file: the engine reads the stream file itself (csrc/ingest.cu)."""
+        h = hostname.encode() if hostname is not None else None
+        self._check(self._L.hg_add_stream_file(self._ctx, h, int(pid or 0), int(tid or 0), str(path).encode(),
+                                               offset, size), "hg_add_stream_file")
+
+    def add_stream_device(self, hostname, pid, tid, tensor):
+        """hg_add_stream_device: stream bytes already in this GPU's memory (a CUDA uint8 tensor)."""
+        h = hostname.encode() if hostname is not None else None
+        n = tensor.numel() * tensor.element_size()
+        self._keep.append(tensor)
+        self._check(self._L.hg_add_stream_device(self._ctx, h, int(pid or 0), int(tid or 0),
+                                                 C.c_void_p(tensor.data_ptr() if n else 0), n),
+                    "hg_add_stream_device")
+
+    def set_streams_device(self, idents, tensors):
+        """Streams whose bytes are CUDA tensors on this engine's GPU (GDS, another kernel, a peer copy)."""
+        from .tracefile import RawStream
+
+        self._check(self._L.hg_clear_streams(self._ctx), "hg_clear_streams")
+        self._keep = []
+        self._streams = [RawStream(h, p, t, "", b"") for h, p, t in idents]
+        for (h, p, t), ten in zip(idents, tensors):
+            self.add_stream_device(h, p, t, ten)
+
+    def ingest_stats(self) -> dict:
+        """hg_ingest_stats of the last staging: bytes per source kind, host ms, threads."""
+        a, b, c, d = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        ms, th = C.c_float(), C.c_uint32()
+        self._check(self._L.hg_ingest_stats(self._ctx, C.byref(a), C.byref(b), C.byref(c), C.byref(d), C.byref(ms),
+                                            C.byref(th)), "hg_ingest_stats")
+        return {"pinned_bytes": a.value, "pageable_bytes": b.value, "file_bytes": c.value, "device_bytes": d.value,
+                "ms": ms.value, "threads": th.value}
 
     def add_stream_ptr(self, hostname, pid, tid, data, size=None):
         """data: bytes (kept alive here) or an integer host address (+ size)."""

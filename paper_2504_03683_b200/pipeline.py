@@ -271,14 +271,15 @@ def merge_same_identity(raws):
 
 
 def _resolve_source(source, registry):
+    if hasattr(source, "dir") and (hasattr(source, "metadata") or hasattr(source, "file_streams")):
+        # a trace directory (ours or the reference's TraceReader): the engine reads the files itself
+        from .tracefile import open_trace_reader
+
+        ours = source if hasattr(source, "file_streams") else open_trace_reader(source.dir)
+        return merge_same_identity(ours.file_streams()), ours.stream_infos()
     if hasattr(source, "raw_streams"):
         return (merge_same_identity(source.raw_streams()),
                 source.stream_infos() if hasattr(source, "stream_infos") else None)
-    if hasattr(source, "dir") and hasattr(source, "metadata"):  # a reference TraceReader
-        from .tracefile import open_trace_reader
-
-        ours = open_trace_reader(source.dir)
-        return merge_same_identity(ours.raw_streams()), ours.stream_infos()
     cursors = source.streams() if hasattr(source, "streams") else list(source)
     infos = source.stream_infos() if hasattr(source, "stream_infos") else None
     return _raw_from_records(cursors, registry), infos
@@ -408,7 +409,7 @@ def _resolve_sharded(source, registry, comm) -> _Shard:
     raws, err = [], None
     for i in mine:
         try:
-            raws.extend(reader.raw_streams(select=[i]))
+            raws.extend(reader.file_streams(select=[i]))
         except HapitraceError as e:
             err = (i, e)
             break

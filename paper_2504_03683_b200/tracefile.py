@@ -60,6 +60,23 @@ class RawStream:
     info: StreamInfo | None = None
 
 
+class FileStream:
+    """A stream file the engine stages itself (hg_add_stream_file: pinned double-buffered reads
+    overlapped with the PCIe copies, csrc/ingest.cu); its 16-byte header is already checked.  The
+    bytes are read on the host only if host-side code asks for ``data`` (error formatting)."""
+
+    def __init__(self, hostname, pid, tid, name, path, size, info=None):
+        self.hostname, self.pid, self.tid, self.name = hostname, pid, tid, name
+        self.path, self.size, self.info = str(path), size, info
+        self._data = None
+
+    @property
+    def data(self) -> bytes:
+        if self._data is None:
+            self._data = Path(self.path).read_bytes()
+        return self._data
+
+
 class TraceReader:
     """Finalized trace directory (tracefile.py:518-549 semantics up to decode)."""
 
@@ -88,6 +105,29 @@ class TraceReader:
         """Byte size of every stream file in index order, without reading it (0 for unread files);
         the multi-GPU partitioner balances ranks by these."""
         return [(self.dir / e["file"]).stat().st_size if e["event_count"] else 0 for e in self._entries]
+
+    def file_streams(self, select=None) -> list:
+        """Like raw_streams, but the files are left for the engine to read (FileStream); only the
+        16-byte headers are read here, in index order, for the reference's errors."""
+        out = []
+        select = None if select is None else set(select)
+        for i, e in enumerate(self._entries):
+            if select is not None and i not in select:
+                continue
+            name = e["file"]
+            info = StreamInfo(e["hostname"], e["pid"], e["tid"], e["event_count"], e["dropped_count"])
+            if not e["event_count"]:
+                out.append(RawStream(e["hostname"], e["pid"], e["tid"], name, b"", info))
+                continue
+            path = self.dir / name
+            with open(path, "rb") as fh:
+                head = fh.read(FILE_HEADER.size)
+            if not head:  # an empty file yields no records and is not checked (tracefile.py:489-490)
+                out.append(RawStream(e["hostname"], e["pid"], e["tid"], name, b"", info))
+                continue
+            check_file_header(head, name)
+            out.append(FileStream(e["hostname"], e["pid"], e["tid"], name, path, path.stat().st_size, info))
+        return out
 
     def raw_streams(self, select=None) -> list:
         """Read every stream file (or the index positions in ``select``) in index order, validating
