@@ -153,7 +153,8 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas,
  * the host) in (hostname, pid, tid) order; replaces StreamCursor
  * (tracefile.py:477-508).  `data` is a host pointer that must stay valid
  * until hg_run returns.  hostname NULL stands for None (record-list sources):
- * it orders as "" and prints as "None" in timeline metadata (sinks.py:367). */
+ * it orders as "" and prints as "None" in timeline metadata (sinks.py:367);
+ * pid / tid INT64_MIN stand for None in pretty-printed lines. */
 int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid,
                   const void* data, uint64_t size);
 int hg_clear_streams(hg_ctx* ctx);
@@ -183,6 +184,7 @@ int hg_stage(hg_ctx* ctx);
  * replaces run_pipeline(reader, [TallySink(), TimelineSink()]) (pipeline.py:275-314) */
 #define HG_WANT_TALLY 1u
 #define HG_WANT_TIMELINE 2u
+#define HG_WANT_EVENTS 4u   /* every record in mux order + PrettyPrintSink's text (events.cu) */
 int hg_run(hg_ctx* ctx, uint32_t want);
 
 /* split form for sharded (multi-GPU) runs: phase 1 over the local streams,
@@ -222,6 +224,17 @@ int hg_phase_timing(hg_ctx* ctx, float* walk_ms, float* chain_ms, float* decode_
  * None.  rank[s] = position of stream s in the flush order (a permutation of the added
  * streams); NULL restores stream order.  Reset by hg_clear_streams. */
 int hg_set_flush_order(hg_ctx* ctx, const uint32_t* rank, uint32_t n);
+/* event sinks (`consumes = "events"`, pipeline.py:250-263): a run with HG_WANT_EVENTS orders
+ * every record as mux_streams does (pipeline.py:68-114) and renders PrettyPrintSink's lines
+ * (sinks.py:66-106; "\n"-terminated, UTF-8).  Schema and field names (EventSchema.name,
+ * FieldSpec.name; fields in kinds[] order) are required first.  hg_get_event_order returns the
+ * mux order itself: (stream index, record index within the stream) per event. */
+int hg_set_schema_names(hg_ctx* ctx, const char* names, const uint64_t* offsets, uint32_t n_schemas,
+                        const char* field_names, const uint64_t* field_offsets, uint32_t n_fields);
+int hg_events_size(hg_ctx* ctx, uint64_t* n_bytes);
+int hg_get_events(hg_ctx* ctx, char* out, uint64_t cap);
+int hg_get_event_order(hg_ctx* ctx, uint32_t* stream, uint64_t* seq, uint64_t cap, uint64_t* n);
+int hg_events_ms(hg_ctx* ctx, float* ms);  /* device time of ordering + rendering */
 /* TimelineSink(device_index=) (sinks.py:347-349): device pid 9000000 + index */
 int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index);
 

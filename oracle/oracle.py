@@ -207,3 +207,74 @@ def run_dir(directory, want_timeline=False, threads=0, device_index=0) -> Oracle
     reader = open_trace_reader(directory)
     return run(reader.raw_streams(), reader.registry, reader.stream_infos(), want_timeline, threads,
                device_index)
+
+
+# ---------------------------------------------------------------------------
+# PrettyPrintSink (event sink) restatement -- TEST INFRASTRUCTURE, pinned by
+# tests/golden/expected/pretty_index.json (the reference's own output on every golden trace)
+
+def _fmt_timestamp(ns: int) -> str:  # sinks.py:43-46
+    s, frac = divmod(ns, 1_000_000_000)
+    s %= 86400
+    return f"{s // 3600:02d}:{s % 3600 // 60:02d}:{s % 60:02d}.{frac:09d}"
+
+
+def _fmt_value(kind: str, value) -> str:  # sinks.py:49-59
+    import json
+
+    if kind == "address":
+        return f"0x{value:016x}"
+    if kind == "string":
+        return json.dumps(value)
+    if kind == "blob":
+        return "[ " + ", ".join(str(b) for b in value) + " ]"
+    if kind == "f64":
+        return repr(float(value))
+    return str(value)
+
+
+def _decode_stream(data: bytes, registry):
+    """(ts, schema, payload dict) of every record (tracefile.py:147-215 on a clean stream)."""
+    out = []
+    off = 16
+    while off + 16 <= len(data):
+        sid, ts, plen = struct.unpack_from("<IQI", data, off)
+        schema = registry.by_id[sid]
+        p = off + 16
+        payload = {}
+        for f in schema.fields:
+            if f.kind in ("string", "blob"):
+                (n,) = struct.unpack_from("<I", data, p)
+                raw = data[p + 4: p + 4 + n]
+                payload[f.name] = raw.decode("utf-8") if f.kind == "string" else raw
+                p += 4 + n
+            else:
+                fmt = {"u64": "<Q", "i64": "<q", "f64": "<d", "address": "<Q"}[f.kind]
+                (payload[f.name],) = struct.unpack_from(fmt, data, p)
+                p += 8
+        out.append((ts, schema, payload))
+        off += 16 + plen
+    return out
+
+
+def pretty(raw_streams, registry) -> str:
+    """PrettyPrintSink.on_finish text over mux_streams order (pipeline.py:68-114, sinks.py:66-106)."""
+    import heapq
+
+    heap = []
+    decoded = [_decode_stream(r.data, registry) if r.data else [] for r in raw_streams]
+    for idx, (r, recs) in enumerate(zip(raw_streams, decoded)):
+        if recs:
+            heap.append((recs[0][0], r.hostname or "", r.pid or 0, r.tid or 0, 0, idx))
+    heapq.heapify(heap)
+    lines = []
+    while heap:
+        ts, _h, _p, _t, seq, idx = heapq.heappop(heap)
+        r = raw_streams[idx]
+        _, schema, payload = decoded[idx][seq]
+        fields = ", ".join(f"{f.name}: {_fmt_value(f.kind, payload[f.name])}" for f in schema.fields)
+        lines.append(f"{_fmt_timestamp(ts)} - {r.hostname} - vpid: {r.pid}, vtid: {r.tid} - {schema.name}: "
+                     + ("{ " + fields + " }" if fields else "{ }"))
+        if seq + 1 < len(decoded[idx]):
+            heapq.heappush(heap, (decoded[idx][seq + 1][0], _h, _p, _t, seq + 1, idx))
+    return "\n".join(lines) + ("\n" if lines else "")

@@ -11,7 +11,8 @@ from .errors import (  # noqa: F401
     TraceDirectoryError, TraceError, UnknownSchemaError, UnsupportedTraceError,
 )
 from .pipeline import (  # noqa: F401
-    END_OF_STREAM, IntervalStats, Message, PipelineResult, Sink, Span, TallySink, TimelineSink, run_pipeline,
+    END_OF_STREAM, IntervalStats, Message, PipelineResult, PrettyPrintSink, Sink, Span, TallySink, TimelineSink,
+    run_pipeline,
 )
 from .registry import EventSchema, FieldSpec, SchemaRegistry  # noqa: F401
 from .tally import TallyReport, TallyRow, empty_report, fmt_duration, merge_tallies, render_tally  # noqa: F401

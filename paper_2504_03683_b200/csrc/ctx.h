@@ -46,6 +46,7 @@ struct HostStream {
   const uint8_t* data;  // host (SRC_HOST) or device (SRC_DEVICE) bytes; null for files
   uint64_t size;
   bool host_none;  // hostname None (record sources): "Host None pid .." in the timeline (sinks.py:367)
+  bool pid_none = false, tid_none = false;  // pid / tid None (record sources): printed "None"
   int src = SRC_HOST;
   std::string path;       // SRC_FILE
   uint64_t file_off = 0;  // SRC_FILE: offset of the stream's first byte in the file
@@ -174,6 +175,17 @@ struct hg_ctx {
   // truncation flush order (hg_set_flush_order)
   bool flush_order = false;
   DBuf<uint32_t> d_flush_rank, d_flush_stream;
+  // event sinks (events.cu): schema / field names, the mux-ordered records and their text
+  bool have_schema_names = false;
+  std::vector<std::string> schema_names, field_names;
+  DBuf<TlItem> d_ev_items;
+  DBuf<char> d_ev_spre, d_ev_sname, d_ev_fname, d_ev_out;
+  DBuf<uint64_t> d_ev_spre_off, d_ev_sname_off, d_ev_fname_off, d_ev_offs;
+  DBuf<uint32_t> d_ev_lens;
+  const uint32_t* ev_order = nullptr;
+  uint64_t ev_size = 0;
+  bool ev_ready = false;
+  float ev_ms = 0;
   // ingest (ingest.cu): pinned staging pool and the last staging's numbers
   IngestPool* ingest = nullptr;
   IngestStats ingest_stats;
@@ -263,5 +275,9 @@ int launch_fast(hg_ctx* ctx);      // fast.cu
 int launch_phase1(hg_ctx* ctx);    // seg.cu
 int run_timeline(hg_ctx* ctx, uint64_t global_last_ts);  // timeline.cu
 int ingest_streams(hg_ctx* ctx);   // ingest.cu
+int run_events(hg_ctx* ctx);       // events.cu
+int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
+            const uint32_t** order);                                                   // timeline.cu
+int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint64_t* total);  // timeline.cu
 void ingest_free(hg_ctx* ctx);     // ingest.cu
 }

@@ -446,7 +446,10 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
 
 int hg_add_stream(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t tid, const void* data, uint64_t size) {
   if (!ctx || (size && !data)) return HG_EARG;
-  ctx->streams.push_back(HostStream{hostname ? hostname : "", pid, tid, (const uint8_t*)data, size, hostname == nullptr});
+  HostStream hs{hostname ? hostname : "", pid, tid, (const uint8_t*)data, size, hostname == nullptr};
+  hs.pid_none = pid == INT64_MIN;
+  hs.tid_none = tid == INT64_MIN;
+  ctx->streams.push_back(hs);
   ctx->staged = false;
   ctx->have_results = false;
   return HG_OK;
@@ -768,7 +771,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;
-  bool fast = ctx->path_opt != 1 && !(want & HG_WANT_TIMELINE);
+  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_TIMELINE | HG_WANT_EVENTS));
   bool retried = false;
   for (int attempt = 0; attempt < 9; attempt++) {
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
@@ -935,8 +938,13 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->total_ms = t_ms;
   ctx->have_results = true;
   ctx->tl_ready = false;
+  ctx->ev_ready = false;
   if (!ctx->errors.empty()) return HG_TRACE_ERROR;
-  if (ctx->want & HG_WANT_TIMELINE) return run_timeline(ctx, global_last_ts);
+  if (ctx->want & HG_WANT_TIMELINE) {
+    int rc = run_timeline(ctx, global_last_ts);
+    if (rc) return rc;
+  }
+  if (ctx->want & HG_WANT_EVENTS) return run_events(ctx);
   return HG_OK;
 }
 

@@ -187,6 +187,8 @@ int hg_add_stream_device(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t
     }
   }
   HostStream hs{hostname ? hostname : "", pid, tid, (const uint8_t*)dptr, size, hostname == nullptr};
+  hs.pid_none = pid == INT64_MIN;
+  hs.tid_none = tid == INT64_MIN;
   hs.src = SRC_DEVICE;
   ctx->streams.push_back(hs);
   ctx->staged = false;
@@ -198,6 +200,8 @@ int hg_add_stream_file(hg_ctx* ctx, const char* hostname, int64_t pid, int64_t t
                        uint64_t size) {
   if (!ctx || (size && !path)) return HG_EARG;
   HostStream hs{hostname ? hostname : "", pid, tid, nullptr, size, hostname == nullptr};
+  hs.pid_none = pid == INT64_MIN;
+  hs.tid_none = tid == INT64_MIN;
   hs.src = SRC_FILE;
   hs.path = path ? path : "";
   hs.file_off = offset;

@@ -2,6 +2,74 @@
 #define HG_TL_KERNELS
 #include "ctx.h"
 
+// stable order of message slots by mux key (khi, klo): items[0, nrec_slots) hold every stream's
+// record-region run (stream s from rec_off[s]; empty slots have key ~0), items[nrec_slots, N) the
+// ncomp messages compose appended (unsorted); n = messages in all.  The record-region runs are
+// compacted, compose's messages sorted per tile, then all runs merged pairwise with merge-path
+// passes -- the k-way merge of the reference's muxer (pipeline.py:68-114).  *order = item index
+// of every message in mux order (a scratch buffer of the context, valid until the next sort).
+int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
+            const uint32_t** order) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  const uint32_t nrec = n - ncomp;
+  const uint32_t n_rtiles = (nrec_slots + kSortTile - 1) / kSortTile;
+  const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
+  uint32_t R = ns + ntc;
+  for (int k = 0; k < 2; k++) {
+    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_ro[k].ensure(R + 2));
+  }
+  CK(ctx->d_tl_tcnt.ensure(n_rtiles + 2));
+  CK(ctx->d_tl_tile0.ensure(R / 2 + 3));
+  CK(ctx->d_tl_split.ensure(n / kSortTile + R / 2 + 3));
+  int cur = 0;
+  if (n) {
+    if (n_rtiles) {
+      tl_count_kernel<<<n_rtiles, kSortThreads, 0, st>>>(items, nrec_slots, ctx->d_tl_tcnt.ptr);
+      tl_small_scan_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_tcnt.ptr, n_rtiles);
+      ctx->launches += 2;
+    }
+    tl_compact_kernel<<<n_rtiles + std::max<uint32_t>(ntc, 1), kSortThreads, 0, st>>>(
+        items, nrec_slots, N, ctx->d_tl_tcnt.ptr, n_rtiles, ctx->d_tl_rec_off.ptr, ns, nrec, n,
+        ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, ctx->d_tl_ro[0].ptr);
+    ctx->launches++;
+    if (ntc) {
+      tl_tilesort_kernel<<<ntc, kSortThreads, 0, st>>>(ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, nrec, ncomp);
+      ctx->launches++;
+    }
+    CK(cudaGetLastError());
+    while (R > 1) {
+      const uint32_t P = (R + 1) / 2;
+      const uint32_t tiles = n / kSortTile + P + 1;  // bound on the output tiles of the pass
+      tl_pairs_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_ro[cur ^ 1].ptr);
+      tl_split_kernel<<<(tiles + 127) / 128, 128, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_ro[cur].ptr, R,
+                                                           ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
+      tl_merge_kernel<<<tiles, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
+                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr,
+                                                      ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
+      CK(cudaGetLastError());
+      ctx->launches += 3;
+      cur ^= 1;
+      R = P;
+    }
+  }
+  *order = ctx->d_tl_idx[cur].ptr;
+  return HG_OK;
+}
+
+// exclusive scan of n u32 lengths into u64 offsets, *total (device) = the sum
+int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint64_t* total) {
+  const uint32_t nsb = (n + kScanBlock - 1) / kScanBlock;
+  CK(ctx->d_tl_bsum.ensure(std::max<uint32_t>(nsb, 1)));
+  tl_scan1_kernel<<<nsb, kScanBlock, 0, ctx->stream>>>(lens, n, ctx->d_tl_bsum.ptr);
+  tl_scan2_kernel<<<1, kScanBlock, 0, ctx->stream>>>(ctx->d_tl_bsum.ptr, nsb, total);
+  tl_scan3_kernel<<<nsb, kScanBlock, 0, ctx->stream>>>(lens, n, ctx->d_tl_bsum.ptr, offs);
+  ctx->launches += 3;
+  return HG_OK;
+}
+
 // order, format and store the timeline JSON (TimelineSink.on_finish, sinks.py:414-418)
 int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->tl_ready = false;
@@ -34,8 +102,11 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   std::map<int64_t, uint32_t> proc_id;  // process_name metas are keyed by (pid, 0)
   for (uint32_t s = 0; s < ns; s++) {
     const HostStream& hs = ctx->streams[s];
-    std::string a = std::to_string(hs.pid), b = std::to_string(hs.tid);
-    std::string c = json_quote("Host " + (hs.host_none ? std::string("None") : hs.host) + " pid " + a);
+    // None pid / tid (record sources): JSON null, "None" in the process name (sinks.py:367-369)
+    std::string a = hs.pid_none ? std::string("null") : std::to_string(hs.pid);
+    std::string b = hs.tid_none ? std::string("null") : std::to_string(hs.tid);
+    std::string c = json_quote("Host " + (hs.host_none ? std::string("None") : hs.host) + " pid " +
+                               (hs.pid_none ? std::string("None") : a));
     for (const std::string* x : {&a, &b, &c}) {
       sstr.insert(sstr.end(), x->begin(), x->end());
       sstr_off.push_back(sstr.size());
@@ -58,50 +129,11 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   CK(upload(ctx->d_tl_devpid, devpid, st));
   // sort by mux key: the streams' record slots are sorted runs; drop the empty slots, sort
   // compose's messages per tile, merge the runs pairwise
-  const uint32_t nrec_slots = (uint32_t)ctx->tl_comp_base;
   const uint32_t ncomp = (uint32_t)C[C_TL_N2];
-  const uint32_t nrec = n - ncomp;
-  const uint32_t n_rtiles = (nrec_slots + kSortTile - 1) / kSortTile;
-  const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
-  uint32_t R = ns + ntc;
-  for (int k = 0; k < 2; k++) {
-    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
-    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
-    CK(ctx->d_tl_ro[k].ensure(R + 2));
-  }
-  CK(ctx->d_tl_tcnt.ensure(n_rtiles + 2));
-  CK(ctx->d_tl_tile0.ensure(R / 2 + 3));
-  CK(ctx->d_tl_split.ensure(n / kSortTile + R / 2 + 3));
-  int cur = 0;
-  if (n) {
-    if (n_rtiles) {
-      tl_count_kernel<<<n_rtiles, kSortThreads, 0, st>>>(ctx->d_tl_items.ptr, nrec_slots, ctx->d_tl_tcnt.ptr);
-      tl_small_scan_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_tcnt.ptr, n_rtiles);
-      ctx->launches += 2;
-    }
-    tl_compact_kernel<<<n_rtiles + std::max<uint32_t>(ntc, 1), kSortThreads, 0, st>>>(
-        ctx->d_tl_items.ptr, nrec_slots, (uint32_t)N, ctx->d_tl_tcnt.ptr, n_rtiles, ctx->d_tl_rec_off.ptr, ns, nrec, n,
-        ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, ctx->d_tl_ro[0].ptr);
-    ctx->launches++;
-    if (ntc) {
-      tl_tilesort_kernel<<<ntc, kSortThreads, 0, st>>>(ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, nrec, ncomp);
-      ctx->launches++;
-    }
-    CK(cudaGetLastError());
-    while (R > 1) {
-      const uint32_t P = (R + 1) / 2;
-      const uint32_t tiles = n / kSortTile + P + 1;  // bound on the output tiles of the pass
-      tl_pairs_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_ro[cur ^ 1].ptr);
-      tl_split_kernel<<<(tiles + 127) / 128, 128, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_ro[cur].ptr, R,
-                                                           ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
-      tl_merge_kernel<<<tiles, kSortThreads, 0, st>>>(ctx->d_tl_keys[cur].ptr, ctx->d_tl_idx[cur].ptr,
-                                                      ctx->d_tl_keys[cur ^ 1].ptr, ctx->d_tl_idx[cur ^ 1].ptr,
-                                                      ctx->d_tl_ro[cur].ptr, R, ctx->d_tl_tile0.ptr, ctx->d_tl_split.ptr);
-      CK(cudaGetLastError());
-      ctx->launches += 3;
-      cur ^= 1;
-      R = P;
-    }
+  const uint32_t* order = nullptr;
+  {
+    int rc = tl_sort(ctx, ctx->d_tl_items.ptr, (uint32_t)ctx->tl_comp_base, N, ncomp, n, &order);
+    if (rc) return rc;
   }
   // metadata first occurrences
   uint64_t n_dev = C[C_STATS + ST_DEVICE];
@@ -117,12 +149,10 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   CK(cudaMemsetAsync(ctx->d_tl_th_first.ptr, 0xFF, (size_t)th_size * 4, st));
   CK(ctx->d_tl_lens.ensure(std::max<uint32_t>(n, 1)));
   CK(ctx->d_tl_offs.ensure(std::max<uint32_t>(n, 1)));
-  const uint32_t nsb = (n + kScanBlock - 1) / kScanBlock;
-  CK(ctx->d_tl_bsum.ensure(std::max<uint32_t>(nsb, 1)));
   TlTables T{};
   T.items = ctx->d_tl_items.ptr;
   T.n = n;
-  T.order = ctx->d_tl_idx[cur].ptr;
+  T.order = order;
   T.fnq = ctx->d_tl_fnq.ptr;
   T.fnq_off = ctx->d_tl_fnq_off.ptr;
   T.sstr = ctx->d_tl_sstr.ptr;
@@ -152,11 +182,9 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
     tl_len_kernel<<<g, 256, 0, st>>>(T);
     tl_meta_len_kernel<<<std::min<uint32_t>((n_proc + th_size + 255) / 256, (uint32_t)ctx->sm_count * 8), 256, 0, st>>>(
         T, n_proc, th_size);
-    tl_scan1_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr);
-    tl_scan2_kernel<<<1, kScanBlock, 0, st>>>(ctx->d_tl_bsum.ptr, nsb, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
-    tl_scan3_kernel<<<nsb, kScanBlock, 0, st>>>(T.lens, n, ctx->d_tl_bsum.ptr, T.offs);
+    tl_scan(ctx, T.lens, n, T.offs, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
     CK(cudaGetLastError());
-    ctx->launches += 5;
+    ctx->launches += 2;
     unsigned long long tail[2] = {0, 0};
     CK(cudaMemcpyAsync(tail, ctx->d_counters.ptr + C_TL_TOTAL, 16, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 
 from . import native
 from .abi import (
-    HG_OK, HG_TRACE_ERROR, HG_WANT_TALLY, HG_WANT_TIMELINE, HgConfig, HgOrphan, HgStats, HgTallyRow,
+    HG_OK, HG_TRACE_ERROR, HG_WANT_EVENTS, HG_WANT_TALLY, HG_WANT_TIMELINE, HgConfig, HgOrphan, HgStats, HgTallyRow,
     HgTraceError, flatten_registry,
 )
 from .errors import EngineError, UnsupportedTraceError
@@ -26,6 +26,11 @@ MERGE_STATS = 8  # IntervalStats counters + trace-error ranks at the head of the
 OPT_PATH = 1
 OPT_RANGE_BYTES = 2
 PATH_AUTO, PATH_EXACT, PATH_FAST = 0, 1, 2
+
+
+def _ident(v):
+    """pid / tid for hg_add_stream: None travels as INT64_MIN (printed "None" by event sinks)."""
+    return -(1 << 63) if v is None else int(v)
 
 
 @dataclass
@@ -40,6 +45,7 @@ class RunResult:
     h2d_bytes: int
     d2h_bytes: int
     launches: int
+    events: bytes | None = None
 
 
 class Engine:
@@ -97,9 +103,31 @@ class Engine:
         self._check(self._L.hg_set_function_names(
             self._ctx, C.c_char_p(blob) if blob else None, (C.c_uint64 * (n + 1))(*offs),
             C.c_char_p(null) if null else None, n), "hg_set_function_names")
+        self._set_schema_names(flat)
         self._flat = flat
         self._registry_key = registry
         return flat
+
+    def _set_schema_names(self, flat):
+        """EventSchema / FieldSpec names for event sinks (hg_set_schema_names), in flat order."""
+        by_id = flat.registry.by_id
+        schemas = [by_id[h.id] for h in flat.schemas]
+        names = [s.name.encode("utf-8") for s in schemas]
+        fields = [f.name.encode("utf-8") for s in schemas for f in s.fields]
+
+        def blob(parts):
+            offs = [0]
+            for b in parts:
+                offs.append(offs[-1] + len(b))
+            return b"".join(parts), (C.c_uint64 * len(offs))(*offs)
+
+        nb, no = blob(names)
+        fb, fo = blob(fields)
+        self._check(self._L.hg_set_schema_names(self._ctx, nb, no, len(names), fb, fo, len(fields)),
+                    "hg_set_schema_names")
+        self._event_ok = all(len({f.name for f in s.fields}) == len(s.fields) and
+                             all(f.kind in ("u64", "i64", "f64", "address", "string", "blob") for f in s.fields)
+                             for s in schemas)
 
     def set_streams(self, raw_streams):
         """raw_streams: RawStream list in mux order (hostname, pid, tid)."""
@@ -141,7 +169,7 @@ class Engine:
     def add_stream_file(self, hostname, pid, tid, path, offset, size):
         """hg_add_stream_file: the engine reads the stream file itself (csrc/ingest.cu)."""
         h = hostname.encode() if hostname is not None else None
-        self._check(self._L.hg_add_stream_file(self._ctx, h, int(pid or 0), int(tid or 0), str(path).encode(),
+        self._check(self._L.hg_add_stream_file(self._ctx, h, _ident(pid), _ident(tid), str(path).encode(),
                                                offset, size), "hg_add_stream_file")
 
     def add_stream_device(self, hostname, pid, tid, tensor):
@@ -149,7 +177,7 @@ class Engine:
         h = hostname.encode() if hostname is not None else None
         n = tensor.numel() * tensor.element_size()
         self._keep.append(tensor)
-        self._check(self._L.hg_add_stream_device(self._ctx, h, int(pid or 0), int(tid or 0),
+        self._check(self._L.hg_add_stream_device(self._ctx, h, _ident(pid), _ident(tid),
                                                  C.c_void_p(tensor.data_ptr() if n else 0), n),
                     "hg_add_stream_device")
 
@@ -172,6 +200,28 @@ class Engine:
         return {"pinned_bytes": a.value, "pageable_bytes": b.value, "file_bytes": c.value, "device_bytes": d.value,
                 "ms": ms.value, "threads": th.value}
 
+    def events_text(self) -> bytes:
+        """PrettyPrintSink's text of the last HG_WANT_EVENTS run (every record in mux order)."""
+        n = C.c_uint64()
+        self._check(self._L.hg_events_size(self._ctx, C.byref(n)), "hg_events_size")
+        buf = (C.c_char * max(n.value, 1))()
+        self._check(self._L.hg_get_events(self._ctx, buf, n.value), "hg_get_events")
+        return bytes(buf)[: n.value]
+
+    def event_order(self):
+        """The mux order of the last HG_WANT_EVENTS run: (stream index, record index) per event."""
+        n = C.c_uint64()
+        self._check(self._L.hg_get_event_order(self._ctx, None, None, 0, C.byref(n)), "hg_get_event_order")
+        st = (C.c_uint32 * max(n.value, 1))()
+        sq = (C.c_uint64 * max(n.value, 1))()
+        self._check(self._L.hg_get_event_order(self._ctx, st, sq, n.value, C.byref(n)), "hg_get_event_order")
+        return list(zip(list(st)[: n.value], list(sq)[: n.value]))
+
+    def events_ms(self) -> float:
+        ms = C.c_float()
+        self._check(self._L.hg_events_ms(self._ctx, C.byref(ms)), "hg_events_ms")
+        return ms.value
+
     def add_stream_ptr(self, hostname, pid, tid, data, size=None):
         """data: bytes (kept alive here) or an integer host address (+ size)."""
         if isinstance(data, int):
@@ -181,7 +231,7 @@ class Engine:
             self._keep.append(data)
             ptr, n = (C.cast(buf, C.c_void_p).value if buf else None), len(data)
         h = hostname.encode() if hostname is not None else None  # NULL: hostname None
-        self._check(self._L.hg_add_stream(self._ctx, h, int(pid or 0), int(tid or 0), ptr, n), "hg_add_stream")
+        self._check(self._L.hg_add_stream(self._ctx, h, _ident(pid), _ident(tid), ptr, n), "hg_add_stream")
 
     def stage(self):
         self._check(self._L.hg_stage(self._ctx), "hg_stage")
@@ -316,13 +366,15 @@ class Engine:
 
     # -- the drop-in
     def run(self, raw_streams, registry, stream_infos=None, want_timeline=False, labels=None,
-            orphan_labels=None, timeline_device_index=0, reuse_streams=False) -> RunResult:
+            orphan_labels=None, timeline_device_index=0, reuse_streams=False, want_events=False) -> RunResult:
         """reuse_streams: run again over the streams of the previous call (still resident in HBM)."""
         flat = self.set_registry(registry)
         self._check(self._L.hg_set_timeline_device(self._ctx, int(timeline_device_index)), "hg_set_timeline_device")
         if not reuse_streams:
             self.set_streams(raw_streams)
-        want = HG_WANT_TALLY | (HG_WANT_TIMELINE if want_timeline else 0)
+        if want_events and not self._event_ok:
+            raise UnsupportedTraceError("event sinks: a schema with duplicate field names or an unknown field kind")
+        want = HG_WANT_TALLY | (HG_WANT_TIMELINE if want_timeline else 0) | (HG_WANT_EVENTS if want_events else 0)
         rc = self.run_raw(want)
         k, t, h2d, d2h, nl = self.timing()
         stats = self.stats()
@@ -349,4 +401,7 @@ class Engine:
         idents = [(s.hostname, s.pid, s.tid) for s in raw_streams]
         report = build_report(flat, self.tally_rows(), self.device_names(), stream_infos, idents, self.stream_spans())
         timeline = self.timeline_bytes() if want_timeline else None
-        return RunResult(report, stats, olist, None, timeline, k, t, h2d, d2h, nl)
+        r = RunResult(report, stats, olist, None, timeline, k, t, h2d, d2h, nl)
+        if want_events:
+            r.events = self.events_text()
+        return r

@@ -144,6 +144,42 @@ class TimelineSink(Sink):
         return json.loads(self._bytes)
 
 
+class PrettyPrintSink(Sink):
+    """One text line per event in mux order, rendered on the GPU (sinks.py:66-106 semantics):
+    ``HH:MM:SS.nnnnnnnnn - <hostname> - vpid: P, vtid: T - <schema>: { f: v, ... }``."""
+
+    name = "pretty"
+    consumes = "events"
+
+    def __init__(self, write=None):
+        self._write = write
+        self._lines: list = []
+
+    def on_start(self, registry):
+        self._registry = registry
+
+    def on_message(self, msg):
+        raise UnsupportedTraceError("hapigpu's PrettyPrintSink is fed by the GPU engine through run_pipeline")
+
+    def on_finish(self) -> str:
+        return "\n".join(self._lines) + ("\n" if self._lines else "")
+
+
+def _is_pretty(sink) -> bool:
+    """This package's PrettyPrintSink, or the reference's (same name and state: _write, _lines)."""
+    return isinstance(sink, PrettyPrintSink) or (
+        type(sink).__name__ == "PrettyPrintSink" and hasattr(sink, "_lines") and hasattr(sink, "_write"))
+
+
+def _feed_pretty(sink, text: bytes):
+    lines = text.decode("utf-8").split("\n")[:-1] if text else []
+    if sink._write is not None:
+        for line in lines:
+            sink._write(line)
+    else:
+        sink._lines = lines
+
+
 def _is_passive(sink) -> bool:
     """A sink that never looks at messages: no on_message, or one inherited unchanged from a base
     class named ``Sink`` (this package's or the reference's, pipeline.py:250-263)."""
@@ -330,12 +366,13 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
         raise PipelineError(f"duplicate sink names: {names}")
     tally = [s for s in sinks if isinstance(s, TallySink)]
     timeline = [s for s in sinks if isinstance(s, TimelineSink)]
+    pretty = [s for s in sinks if _is_pretty(s)]
     for s in sinks:
-        if not isinstance(s, (TallySink, TimelineSink)) and not _is_passive(s):
+        if not isinstance(s, (TallySink, TimelineSink)) and not _is_pretty(s) and not _is_passive(s):
             raise UnsupportedTraceError(
-                f"sink {s.name!r} needs per-message callbacks; hapigpu serves TallySink/TimelineSink")
-    if timeline and comm is not None:
-        raise UnsupportedTraceError("TimelineSink in a multi-rank run: run the timeline on one rank")
+                f"sink {s.name!r} needs per-message callbacks; hapigpu serves TallySink/TimelineSink/PrettyPrintSink")
+    if (timeline or pretty) and comm is not None:
+        raise UnsupportedTraceError("TimelineSink / PrettyPrintSink in a multi-rank run: run them on one rank")
     device_index = {s.device_index for s in timeline}
     if len(device_index) > 1:
         raise UnsupportedTraceError("several TimelineSinks with different device_index")
@@ -350,7 +387,8 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
             labels = [r.name for r in raws]
             olabels = [f"{r.hostname}/{r.pid}/{r.tid}" for r in raws]
             res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels,
-                          orphan_labels=olabels, timeline_device_index=next(iter(device_index), 0))
+                          orphan_labels=olabels, timeline_device_index=next(iter(device_index), 0),
+                          want_events=bool(pretty))
         else:
             res = _run_sharded(eng, registry, shard, comm)
     finally:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
@@ -364,6 +402,8 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
         s._gpu_result(res.report)
     for s in timeline:
         s._gpu_result(res.timeline)
+    for s in pretty:
+        _feed_pretty(s, res.events)
     results = {s.name: s.on_finish() for s in sinks}
     stats = IntervalStats(**res.stats)
     timing = {"kernel_ms": res.kernel_ms, "total_ms": res.total_ms, "h2d_bytes": res.h2d_bytes,
