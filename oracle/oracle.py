@@ -278,3 +278,65 @@ def pretty(raw_streams, registry) -> str:
         if seq + 1 < len(decoded[idx]):
             heapq.heappush(heap, (decoded[idx][seq + 1][0], _h, _p, _t, seq + 1, idx))
     return "\n".join(lines) + ("\n" if lines else "")
+
+
+# ---------------------------------------------------------------------------
+# ValidationSink restatement -- TEST INFRASTRUCTURE, pinned by
+# tests/golden/expected/validation_index.json (the reference's own findings)
+
+def validate(raw_streams, registry, rules, orphans):
+    """ValidationSink.on_message over mux_streams order, then on_finish (sinks.py:518-594);
+    ``rules``: paper_2504_03683_b200.validation.ValidationRules; ``orphans``: the interval stage's."""
+    import heapq
+
+    findings, live, executed, pending = [], {}, {}, {}
+    decoded = [_decode_stream(r.data, registry) if r.data else [] for r in raw_streams]
+    heap = [(recs[0][0], r.hostname or "", r.pid or 0, r.tid or 0, 0, idx)
+            for idx, (r, recs) in enumerate(zip(raw_streams, decoded)) if recs]
+    heapq.heapify(heap)
+    while heap:
+        ts, _h, _p, _t, seq, idx = heapq.heappop(heap)
+        r = raw_streams[idx]
+        _, schema, payload = decoded[idx][seq]
+        if seq + 1 < len(decoded[idx]):
+            heapq.heappush(heap, (decoded[idx][seq + 1][0], _h, _p, _t, seq + 1, idx))
+        label = f"{r.hostname}/{r.pid}/{r.tid}"
+        sid = schema.id
+        if sid in rules.pnext:
+            fn_name, blob_field = rules.pnext[sid]
+            blob = payload.get(blob_field, b"")
+            if len(blob) >= 8:
+                pnext = int.from_bytes(blob[:8], "little")
+                if pnext != 0:
+                    findings.append(("uninit_pnext", pnext, label, ts,
+                                     f"{fn_name}: extension slot pNext is 0x{pnext:x}, must be NULL"))
+        key = (r.hostname, r.pid, r.tid)
+        if schema.event_class == "host_entry":
+            pending[(key, schema.function)] = payload
+            if sid in rules.execute:
+                h = int(payload[rules.execute[sid]])
+                if executed.get(h):
+                    findings.append(("cmdlist_not_reset", h, label, ts,
+                                     f"command list 0x{h:x} executed again without a reset"))
+                executed[h] = True
+            continue
+        if schema.event_class != "host_exit":
+            continue
+        result = int(payload.get("result", 0))
+        if sid in rules.creators and result == 0:
+            fn_name, out_field = rules.creators[sid]
+            h = int(payload[out_field])
+            live[h] = ("leaked_event", h, label, ts, f"handle 0x{h:x} from {fn_name} never released")
+        elif sid in rules.releasers and result == 0:
+            fn_name, _entry_id, handle_param = rules.releasers[sid]
+            entry = pending.get((key, fn_name))
+            if entry is not None:
+                live.pop(int(entry[handle_param]), None)
+        elif sid in rules.resets and result == 0:
+            _entry_id, handle_param = rules.resets[sid]
+            entry = pending.get((key, schema.function))
+            if entry is not None:
+                executed[int(entry[handle_param])] = False
+    leaks = sorted(live.values(), key=lambda f: f[1])
+    orph = [("orphan_exit", 0, stream, ts, f"exit of {fn} without matching entry") for stream, ts, fn in orphans]
+    return findings + leaks + orph
