@@ -185,6 +185,7 @@ int hg_stage(hg_ctx* ctx);
 #define HG_WANT_TALLY 1u
 #define HG_WANT_TIMELINE 2u
 #define HG_WANT_EVENTS 4u   /* every record in mux order + PrettyPrintSink's text (events.cu) */
+#define HG_WANT_VALIDATE 8u /* ValidationSink's rules over the mux order (validate.cu) */
 int hg_run(hg_ctx* ctx, uint32_t want);
 
 /* split form for sharded (multi-GPU) runs: phase 1 over the local streams,
@@ -235,6 +236,31 @@ int hg_events_size(hg_ctx* ctx, uint64_t* n_bytes);
 int hg_get_events(hg_ctx* ctx, char* out, uint64_t cap);
 int hg_get_event_order(hg_ctx* ctx, uint32_t* stream, uint64_t* seq, uint64_t cap, uint64_t* n);
 int hg_events_ms(hg_ctx* ctx, float* ms);  /* device time of ordering + rendering */
+/* ValidationSink (sinks.py:448-594).  One rule row per schema (hg_set_registry order): kind bits
+ * 1 uninit-pNext check (field `pnext`: the struct blob), 2 command-list execution (`exec`: the
+ * handle), 4 creates a handle (`create`: the deref-out address; exits), 8 releases / 16 resets a
+ * handle (exits: the handle comes from the latest entry of the same function on the same stream,
+ * sinks.py:526-527, whose rule row has kind bit 32 and `rel` / `rst` = that parameter), `result`:
+ * the exit's result field (-1: none, treated as 0).  A run with HG_WANT_VALIDATE returns the
+ * findings: uninit_pnext / cmdlist_not_reset at their mux position, leaked handles (the host
+ * sorts them by subject); orphan_exit findings come from the orphan list. */
+enum { HG_FIND_PNEXT = 1, HG_FIND_CMDLIST = 2, HG_FIND_LEAK = 3 };
+typedef struct hg_validation_rule {
+  uint32_t kind;
+  int16_t pnext, exec, create, rel, rst, result;
+} hg_validation_rule;
+typedef struct hg_finding {
+  uint32_t rule;           /* HG_FIND_*                                       */
+  uint32_t sid;            /* schema id of the record that raised it           */
+  uint32_t stream;         /* its stream                                       */
+  uint32_t pad;
+  uint64_t pos;            /* its position in the mux order                    */
+  uint64_t ts;             /* its timestamp                                    */
+  uint64_t subject_lo;     /* subject = subject_hi * 2^64 + subject_lo - 2^63 for handles (65-bit key), */
+  int64_t subject_hi;      /* the pNext value itself (hi 0) for uninit_pnext   */
+} hg_finding;
+int hg_set_validation_rules(hg_ctx* ctx, const hg_validation_rule* rules, uint32_t n_schemas);
+int hg_get_findings(hg_ctx* ctx, hg_finding* out, uint64_t cap, uint64_t* n);
 /* TimelineSink(device_index=) (sinks.py:347-349): device pid 9000000 + index */
 int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index);
 

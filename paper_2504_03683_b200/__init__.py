@@ -19,5 +19,6 @@ from .tally import TallyReport, TallyRow, empty_report, fmt_duration, merge_tall
 from .timeline import check_timeline_object  # noqa: F401
 from .tracefile import EventRecord, StreamInfo, TraceReader, open_trace_reader  # noqa: F401
 from .harness import read_tally_json, tally_trace, write_tally_json  # noqa: F401
+from .validation import ValidationFinding, ValidationRules, ValidationSink, render_findings  # noqa: F401
 
 __version__ = "0.1.0"

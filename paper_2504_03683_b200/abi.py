@@ -26,7 +26,7 @@ ROLE_RESULT, ROLE_START, ROLE_END, ROLE_NAME, ROLE_TILE, ROLE_ENGINE, ROLE_CMDKI
 FEED_NONE, FEED_ALWAYS, FEED_TIMELINE = 0, 1, 2
 
 HG_OK, HG_TRACE_ERROR = 0, 1
-HG_WANT_TALLY, HG_WANT_TIMELINE, HG_WANT_EVENTS = 1, 2, 4
+HG_WANT_TALLY, HG_WANT_TIMELINE, HG_WANT_EVENTS, HG_WANT_VALIDATE = 1, 2, 4, 8
 
 (HG_ERR_TRUNC_HEADER, HG_ERR_TRUNC_PAYLOAD, HG_ERR_UNKNOWN_SCHEMA, HG_ERR_LEN_MISMATCH,
  HG_ERR_TRUNC_VAR, HG_ERR_TRAILING, HG_ERR_UTF8, HG_ERR_STRUCT, HG_ERR_ORDER, HG_ERR_FEED,
@@ -71,6 +71,16 @@ class HgTallyRow(C.Structure):
 
 class HgOrphan(C.Structure):
     _fields_ = [("stream", C.c_uint32), ("function", C.c_int32), ("ts", C.c_uint64), ("seq", C.c_uint64)]
+
+
+class HgValidationRule(C.Structure):
+    _fields_ = [("kind", C.c_uint32), ("pnext", C.c_int16), ("exec", C.c_int16), ("create", C.c_int16),
+                ("rel", C.c_int16), ("rst", C.c_int16), ("result", C.c_int16)]
+
+
+class HgFinding(C.Structure):
+    _fields_ = [("rule", C.c_uint32), ("sid", C.c_uint32), ("stream", C.c_uint32), ("pad", C.c_uint32),
+                ("pos", C.c_uint64), ("ts", C.c_uint64), ("subject_lo", C.c_uint64), ("subject_hi", C.c_int64)]
 
 
 class HgTraceError(C.Structure):

@@ -186,6 +186,15 @@ struct hg_ctx {
   uint64_t ev_size = 0;
   bool ev_ready = false;
   float ev_ms = 0;
+  // validation (validate.cu)
+  std::vector<hg_validation_rule> val_rules;
+  DBuf<hg_validation_rule> d_val_rules;
+  DBuf<unsigned int> d_val_cnt;
+  DBuf<uint32_t> d_val_order;
+  DBuf<TlItem> d_val_eq, d_val_xr, d_val_cr;
+  DBuf<hg_finding> d_val_fnd;
+  std::vector<hg_finding> val_findings;
+  bool val_ready = false;
   // ingest (ingest.cu): pinned staging pool and the last staging's numbers
   IngestPool* ingest = nullptr;
   IngestStats ingest_stats;
@@ -276,6 +285,7 @@ int launch_phase1(hg_ctx* ctx);    // seg.cu
 int run_timeline(hg_ctx* ctx, uint64_t global_last_ts);  // timeline.cu
 int ingest_streams(hg_ctx* ctx);   // ingest.cu
 int run_events(hg_ctx* ctx);       // events.cu
+int run_validation(hg_ctx* ctx);   // validate.cu
 int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
             const uint32_t** order);                                                   // timeline.cu
 int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint64_t* total);  // timeline.cu

@@ -771,7 +771,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;
-  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_TIMELINE | HG_WANT_EVENTS));
+  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_TIMELINE | HG_WANT_EVENTS | HG_WANT_VALIDATE));
   bool retried = false;
   for (int attempt = 0; attempt < 9; attempt++) {
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
@@ -939,12 +939,17 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->have_results = true;
   ctx->tl_ready = false;
   ctx->ev_ready = false;
+  ctx->val_ready = false;
   if (!ctx->errors.empty()) return HG_TRACE_ERROR;
   if (ctx->want & HG_WANT_TIMELINE) {
     int rc = run_timeline(ctx, global_last_ts);
     if (rc) return rc;
   }
-  if (ctx->want & HG_WANT_EVENTS) return run_events(ctx);
+  if (ctx->want & (HG_WANT_EVENTS | HG_WANT_VALIDATE)) {
+    int rc = run_events(ctx);
+    if (rc) return rc;
+  }
+  if (ctx->want & HG_WANT_VALIDATE) return run_validation(ctx);
   return HG_OK;
 }
 

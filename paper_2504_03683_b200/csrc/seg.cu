@@ -18,7 +18,7 @@ int launch_phase1(hg_ctx* ctx) {
     CK(cudaEventRecord(ctx->ev[7], ctx->stream));
     CK(cudaGetLastError());
     ctx->launches += 2;
-    if (ctx->want & (HG_WANT_TIMELINE | HG_WANT_EVENTS)) {
+    if (ctx->want & (HG_WANT_TIMELINE | HG_WANT_EVENTS | HG_WANT_VALIDATE)) {
       // timeline slots: one per record (segment decode), then compose's messages
       seg_rec_off_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_stream_nrec.ptr, ns, ctx->d_tl_rec_off.ptr,
                                                       ctx->d_counters.ptr + C_REC_TOTAL);

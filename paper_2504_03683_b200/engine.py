@@ -14,7 +14,8 @@ from dataclasses import dataclass
 
 from . import native
 from .abi import (
-    HG_OK, HG_TRACE_ERROR, HG_WANT_EVENTS, HG_WANT_TALLY, HG_WANT_TIMELINE, HgConfig, HgOrphan, HgStats, HgTallyRow,
+    HG_OK, HG_TRACE_ERROR, HG_WANT_EVENTS, HG_WANT_TALLY, HG_WANT_TIMELINE, HG_WANT_VALIDATE, HgConfig, HgFinding,
+    HgValidationRule, HgOrphan, HgStats, HgTallyRow,
     HgTraceError, flatten_registry,
 )
 from .errors import EngineError, UnsupportedTraceError
@@ -46,6 +47,7 @@ class RunResult:
     d2h_bytes: int
     launches: int
     events: bytes | None = None
+    findings: list | None = None
 
 
 class Engine:
@@ -217,6 +219,17 @@ class Engine:
         self._check(self._L.hg_get_event_order(self._ctx, st, sq, n.value, C.byref(n)), "hg_get_event_order")
         return list(zip(list(st)[: n.value], list(sq)[: n.value]))
 
+    def set_validation_rules(self, rows):
+        arr = (HgValidationRule * max(len(rows), 1))(*rows)
+        self._check(self._L.hg_set_validation_rules(self._ctx, arr, len(rows)), "hg_set_validation_rules")
+
+    def findings_raw(self):
+        n = C.c_uint64()
+        self._check(self._L.hg_get_findings(self._ctx, None, 0, C.byref(n)), "hg_get_findings")
+        arr = (HgFinding * max(n.value, 1))()
+        self._check(self._L.hg_get_findings(self._ctx, arr, n.value, C.byref(n)), "hg_get_findings")
+        return list(arr)[: n.value]
+
     def events_ms(self) -> float:
         ms = C.c_float()
         self._check(self._L.hg_events_ms(self._ctx, C.byref(ms)), "hg_events_ms")
@@ -366,7 +379,9 @@ class Engine:
 
     # -- the drop-in
     def run(self, raw_streams, registry, stream_infos=None, want_timeline=False, labels=None,
-            orphan_labels=None, timeline_device_index=0, reuse_streams=False, want_events=False) -> RunResult:
+            orphan_labels=None, timeline_device_index=0, reuse_streams=False, want_events=False,
+            validation=None) -> RunResult:
+        """validation: ValidationRules of a ValidationSink (its findings land in RunResult.findings)."""
         """reuse_streams: run again over the streams of the previous call (still resident in HBM)."""
         flat = self.set_registry(registry)
         self._check(self._L.hg_set_timeline_device(self._ctx, int(timeline_device_index)), "hg_set_timeline_device")
@@ -375,6 +390,11 @@ class Engine:
         if want_events and not self._event_ok:
             raise UnsupportedTraceError("event sinks: a schema with duplicate field names or an unknown field kind")
         want = HG_WANT_TALLY | (HG_WANT_TIMELINE if want_timeline else 0) | (HG_WANT_EVENTS if want_events else 0)
+        if validation is not None:
+            from .validation import rule_rows
+
+            self.set_validation_rules(rule_rows(validation, flat))
+            want |= HG_WANT_VALIDATE
         rc = self.run_raw(want)
         k, t, h2d, d2h, nl = self.timing()
         stats = self.stats()
@@ -404,4 +424,8 @@ class Engine:
         r = RunResult(report, stats, olist, None, timeline, k, t, h2d, d2h, nl)
         if want_events:
             r.events = self.events_text()
+        if validation is not None:
+            from .validation import findings_from_native
+
+            r.findings = findings_from_native(self.findings_raw(), validation, raw_streams)
         return r

@@ -28,7 +28,7 @@ NVCC_FLAGS = [
 
 def sources():
     """One translation unit per kernel family (ctx.h): they compile in parallel."""
-    return [CSRC / "engine.cu", CSRC / "fast.cu", CSRC / "seg.cu", CSRC / "timeline.cu", CSRC / "merge.cu", CSRC / "ingest.cu", CSRC / "events.cu"]
+    return [CSRC / "engine.cu", CSRC / "fast.cu", CSRC / "seg.cu", CSRC / "timeline.cu", CSRC / "merge.cu", CSRC / "ingest.cu", CSRC / "events.cu", CSRC / "validate.cu"]
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -113,6 +113,8 @@ def lib():
         "hg_get_events": ([vp, vp, u64], C.c_int),
         "hg_get_event_order": ([vp, vp, vp, u64, vp], C.c_int),
         "hg_events_ms": ([vp, vp], C.c_int),
+        "hg_set_validation_rules": ([vp, vp, u32], C.c_int),
+        "hg_get_findings": ([vp, vp, u64, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -132,5 +134,5 @@ EXPORTED = (
     "hg_timeline_ms", "hg_set_timeline_device", "hg_phase_timing", "hg_set_option", "hg_last_path",
     "hg_set_flush_order", "hg_merge_size", "hg_merge_export", "hg_merge_import", "hg_add_stream_device",
     "hg_add_stream_file", "hg_ingest_stats", "hg_set_schema_names", "hg_events_size", "hg_get_events",
-    "hg_get_event_order", "hg_events_ms",
+    "hg_get_event_order", "hg_events_ms", "hg_set_validation_rules", "hg_get_findings",
 )

@@ -367,12 +367,18 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
     tally = [s for s in sinks if isinstance(s, TallySink)]
     timeline = [s for s in sinks if isinstance(s, TimelineSink)]
     pretty = [s for s in sinks if _is_pretty(s)]
+    from .validation import ValidationSink
+
+    validate = [s for s in sinks if isinstance(s, ValidationSink)]
+    if len(validate) > 1:
+        raise UnsupportedTraceError("several ValidationSinks in one run")
     for s in sinks:
-        if not isinstance(s, (TallySink, TimelineSink)) and not _is_pretty(s) and not _is_passive(s):
+        if not isinstance(s, (TallySink, TimelineSink, ValidationSink)) and not _is_pretty(s) and not _is_passive(s):
             raise UnsupportedTraceError(
                 f"sink {s.name!r} needs per-message callbacks; hapigpu serves TallySink/TimelineSink/PrettyPrintSink")
-    if (timeline or pretty) and comm is not None:
-        raise UnsupportedTraceError("TimelineSink / PrettyPrintSink in a multi-rank run: run them on one rank")
+    if (timeline or pretty or validate) and comm is not None:
+        raise UnsupportedTraceError("TimelineSink / PrettyPrintSink / ValidationSink in a multi-rank run: "
+                                    "run them on one rank")
     device_index = {s.device_index for s in timeline}
     if len(device_index) > 1:
         raise UnsupportedTraceError("several TimelineSinks with different device_index")
@@ -388,7 +394,7 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
             olabels = [f"{r.hostname}/{r.pid}/{r.tid}" for r in raws]
             res = eng.run(raws, registry, infos, want_timeline=bool(timeline), labels=labels,
                           orphan_labels=olabels, timeline_device_index=next(iter(device_index), 0),
-                          want_events=bool(pretty))
+                          want_events=bool(pretty), validation=validate[0].rules if validate else None)
         else:
             res = _run_sharded(eng, registry, shard, comm)
     finally:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
@@ -404,6 +410,8 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
         s._gpu_result(res.timeline)
     for s in pretty:
         _feed_pretty(s, res.events)
+    for s in validate:
+        s._gpu_result(res.findings)
     results = {s.name: s.on_finish() for s in sinks}
     stats = IntervalStats(**res.stats)
     timing = {"kernel_ms": res.kernel_ms, "total_ms": res.total_ms, "h2d_bytes": res.h2d_bytes,

@@ -104,6 +104,95 @@ class ValidationRules:
                    {int(k): tuple(v) for k, v in d["resets"].items()})
 
 
+VK_PNEXT, VK_EXEC, VK_CREATE, VK_RELEASE, VK_RESET, VK_TRACK = 1, 2, 4, 8, 16, 32
+_INT_KINDS = ("u64", "i64", "address")
+
+
+def rule_rows(rules: ValidationRules, flat):
+    """hg_validation_rule rows in the registry's flat order (csrc/validate.cu); refuses layouts whose
+    reference behaviour the rows cannot express (UnsupportedTraceError, never a silent difference)."""
+    from .abi import HgValidationRule
+
+    by_id = flat.registry.by_id
+    rel_fn = {fn: param for fn, _en, param in rules.releasers.values()}
+    rst_fn = {}
+    for ex_id, (_en, param) in rules.resets.items():
+        rst_fn[by_id[ex_id].function] = param
+    rows = []
+    for h in flat.schemas:
+        sc = by_id[h.id]
+        idx = {}
+        for i, f in enumerate(sc.fields):
+            idx[f.name] = i  # payload dicts keep the last duplicate
+        kinds = {f.name: f.kind for f in sc.fields}
+
+        def fld(name, allowed):
+            if name not in idx:
+                return -1
+            if kinds[name] not in allowed:
+                raise UnsupportedTraceError(f"validation: field {sc.name}.{name} of kind {kinds[name]}")
+            return idx[name]
+
+        r = HgValidationRule(0, -1, -1, -1, -1, -1, -1)
+        if sc.id in rules.pnext:
+            r.pnext = fld(rules.pnext[sc.id][1], ("blob",))
+            if r.pnext >= 0:
+                r.kind |= VK_PNEXT
+        if sc.event_class == "host_entry":
+            if sc.id in rules.execute:
+                r.exec = fld(rules.execute[sc.id], _INT_KINDS)
+                if r.exec < 0:
+                    raise UnsupportedTraceError(f"validation: {sc.name} lacks {rules.execute[sc.id]}")
+                r.kind |= VK_EXEC
+            for fnmap, attr in ((rel_fn, "rel"), (rst_fn, "rst")):
+                if sc.function in fnmap:
+                    i = fld(fnmap[sc.function], _INT_KINDS)
+                    if i < 0:
+                        raise UnsupportedTraceError(f"validation: {sc.name} lacks {fnmap[sc.function]}")
+                    setattr(r, attr, i)
+                    r.kind |= VK_TRACK
+        elif sc.event_class == "host_exit":
+            if "result" in idx:
+                r.result = fld("result", ("u64", "i64"))
+            if sc.id in rules.creators:
+                r.create = fld(rules.creators[sc.id][1], _INT_KINDS)
+                if r.create < 0:
+                    raise UnsupportedTraceError(f"validation: {sc.name} lacks {rules.creators[sc.id][1]}")
+                r.kind |= VK_CREATE
+            elif sc.id in rules.releasers:
+                if rules.releasers[sc.id][0] != sc.function:
+                    raise UnsupportedTraceError(f"validation: releaser {sc.name} of another function")
+                r.kind |= VK_RELEASE
+            elif sc.id in rules.resets:
+                r.kind |= VK_RESET
+        rows.append(r)
+    return rows
+
+
+def findings_from_native(native, rules: ValidationRules, streams) -> list:
+    """ValidationFinding objects in the reference's order: in-order findings (mux position), then the
+    leaked handles sorted by subject (sinks.py:592-594)."""
+    in_order, leaks = [], []
+    for f in native:
+        s = streams[f.stream]
+        label = f"{s.hostname}/{s.pid}/{s.tid}"
+        if f.rule == 1:
+            pn = f.subject_lo
+            in_order.append((f.pos, ValidationFinding("uninit_pnext", pn, label, f.ts,
+                                                      f"{rules.pnext[f.sid][0]}: extension slot pNext is 0x{pn:x}, "
+                                                      "must be NULL")))
+            continue
+        h = (f.subject_hi << 64) + f.subject_lo - (1 << 63)
+        if f.rule == 2:
+            in_order.append((f.pos, ValidationFinding("cmdlist_not_reset", h, label, f.ts,
+                                                      f"command list 0x{h:x} executed again without a reset")))
+        else:
+            leaks.append(ValidationFinding("leaked_event", h, label, f.ts,
+                                           f"handle 0x{h:x} from {rules.creators[f.sid][0]} never released"))
+    in_order.sort(key=lambda x: x[0])
+    return [x[1] for x in in_order] + sorted(leaks, key=lambda f: f.subject)
+
+
 class ValidationSink:
     """Post-mortem rule checks (sinks.py:448-594); the events are examined by the GPU engine."""
 
