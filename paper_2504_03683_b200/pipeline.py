@@ -376,9 +376,9 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
         if not isinstance(s, (TallySink, TimelineSink, ValidationSink)) and not _is_pretty(s) and not _is_passive(s):
             raise UnsupportedTraceError(
                 f"sink {s.name!r} needs per-message callbacks; hapigpu serves TallySink/TimelineSink/PrettyPrintSink")
-    if (timeline or pretty or validate) and comm is not None:
-        raise UnsupportedTraceError("TimelineSink / PrettyPrintSink / ValidationSink in a multi-rank run: "
-                                    "run them on one rank")
+    # sinks that need the global mux order of every record (timeline, events, validation) are served
+    # by rank 0 from the whole trace in a multi-rank run; the other ranks return None for them
+    ordered = timeline + pretty + validate
     device_index = {s.device_index for s in timeline}
     if len(device_index) > 1:
         raise UnsupportedTraceError("several TimelineSinks with different device_index")
@@ -397,6 +397,13 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
                           want_events=bool(pretty), validation=validate[0].rules if validate else None)
         else:
             res = _run_sharded(eng, registry, shard, comm)
+            if ordered and res.error is None and comm.rank == 0:
+                full, _ = _resolve_source(source, registry)
+                r0 = eng.run(full, registry, infos, want_timeline=bool(timeline),
+                             labels=[r.name for r in full], orphan_labels=[f"{r.hostname}/{r.pid}/{r.tid}" for r in full],
+                             timeline_device_index=next(iter(device_index), 0), want_events=bool(pretty),
+                             validation=validate[0].rules if validate else None)
+                res.timeline, res.events, res.findings = r0.timeline, r0.events, r0.findings
     finally:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
         for s in sinks:
             hook = getattr(s, "on_diagnostics", None)
@@ -406,13 +413,15 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
         raise res.error
     for s in tally:
         s._gpu_result(res.report)
-    for s in timeline:
-        s._gpu_result(res.timeline)
-    for s in pretty:
-        _feed_pretty(s, res.events)
-    for s in validate:
-        s._gpu_result(res.findings)
-    results = {s.name: s.on_finish() for s in sinks}
+    root = comm is None or comm.rank == 0
+    if root:
+        for s in timeline:
+            s._gpu_result(res.timeline)
+        for s in pretty:
+            _feed_pretty(s, res.events)
+        for s in validate:
+            s._gpu_result(res.findings)
+    results = {s.name: (s.on_finish() if root or not any(s is o for o in ordered) else None) for s in sinks}
     stats = IntervalStats(**res.stats)
     timing = {"kernel_ms": res.kernel_ms, "total_ms": res.total_ms, "h2d_bytes": res.h2d_bytes,
               "d2h_bytes": res.d2h_bytes, "launches": res.launches}

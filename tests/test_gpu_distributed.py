@@ -55,6 +55,20 @@ def _worker(rank, world, port, q, case, tmp):
         eng = Engine(device=0)
         diag = Diag()
         try:
+            if case == "ordered":  # timeline / pretty / validation: rank 0 serves them from the whole trace
+                import json as _json
+
+                from paper_2504_03683_b200 import PrettyPrintSink, TimelineSink, ValidationRules, ValidationSink
+                from golden_util import GOLDEN
+
+                rules = ValidationRules.from_dict(_json.loads((GOLDEN / "expected" / "validation_rules.json").read_text()))
+                res = run_pipeline(open_trace_reader(d), [TallySink(), TimelineSink(), PrettyPrintSink(),
+                                                          ValidationSink(rules=rules)], engine=eng, distributed=True)
+                out = ("ok", res["tally"], res["timeline"], res["pretty"],
+                       None if res["validate"] is None else [tuple(vars(f).values()) for f in res["validate"]])
+                eng.close()
+                q.put((rank, out))
+                return
             res = run_pipeline(open_trace_reader(d), [TallySink(), diag], engine=eng, distributed=True)
             out = ("ok", res["tally"], vars(res.stats), res.orphans, diag.orphans, eng.last_path()[0])
         except Exception as e:  # noqa: BLE001
@@ -114,3 +128,27 @@ def test_two_ranks_one_gpu_raise_the_reference_first_error():
         e = unpack_exception(packed)
         assert type(e).__name__ == type(want.error).__name__ and str(e) == str(want.error)
         assert diag == want.orphans
+
+
+def test_two_ranks_ordered_sinks_served_by_rank0():
+    """TimelineSink / PrettyPrintSink / ValidationSink in a distributed run: rank 0 returns what one GPU
+    over the whole trace returns, the other ranks None; the tally is still the merged one."""
+    import json
+
+    from oracle import oracle
+    from test_distributed import _generate
+
+    from paper_2504_03683_b200 import ValidationRules
+    from golden_util import GOLDEN
+
+    outs = _run("ordered")
+    wl, raws = _generate()
+    want = oracle.run(raws, wl.registry, [r.info for r in raws], want_timeline=True)
+    rules = ValidationRules.from_dict(json.loads((GOLDEN / "expected" / "validation_rules.json").read_text()))
+    findings = oracle.validate(raws, wl.registry, rules, want.orphans)
+    kind, rep, tl, pretty, val = outs[0]
+    assert kind == "ok" and rep == want.report
+    assert tl == json.loads(want.timeline) and pretty == oracle.pretty(raws, wl.registry)
+    assert val == [tuple(f) for f in findings]
+    kind, rep, tl, pretty, val = outs[1]
+    assert kind == "ok" and rep == want.report and tl is None and pretty is None and val is None
