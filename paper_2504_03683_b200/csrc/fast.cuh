@@ -6,14 +6,13 @@
 //   decode every record (tracefile.py:147-215), the per-stream ordering check
 //   (pipeline.py:98), the IntervalBuilder LIFO automaton (pipeline.py:156-185)
 //   and the tally fold (sinks.py:123-132, 230-242),
-// reading the bytes from a private 512-byte ring in shared memory.  The warp
-// refills the rings cooperatively: every iteration the lanes that freed a
-// 128-byte slot are served four at a time by one cp.async (LDGSTS.128) warp
-// instruction (8 lanes x 16 B per line, whole coalesced lines), one commit
-// group per iteration; `cp.async.wait_group kRLag` then proves every group
-// older than kRLag iterations complete, so a lane may read a slot once its fill
-// group is that old.  HBM is read once, in whole lines; every record access is
-// an LDS.
+// reading the bytes from a private 256-byte ring in shared memory (8 slots of
+// 32 B, read with wrapped word indices).  Every iteration a lane whose oldest slot
+// is consumed copies its next 32 bytes itself with two 16-byte cp.async.cg
+// (LDGSTS: L2 -> shared, bypassing L1); one commit group per iteration and
+// `cp.async.wait_group kRLag` prove every fill older than kRLag iterations
+// complete, so readiness is a popcount of the lane's request shift register.  HBM
+// is read once; every record access on the inline path is an LDS.
 //
 // Range starts are speculative (first offset with three consistent record
 // headers).  fast_verify_kernel then checks, per stream, that every range
