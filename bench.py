@@ -423,7 +423,9 @@ def run_ours(args):
         if line["e2e_dropin"].get("parity", "exact") != "exact":
             parity = line["parity"] = "MISMATCH in e2e_dropin"
     if ws == 1 and not args.no_timeline:
-        line["timeline"] = timeline_side(eng)
+        line["timeline"] = timeline_side(eng, threads)
+        if line["timeline"]["parity"] != "exact" and parity == "exact":
+            parity = line["parity"] = "MISMATCH in timeline"
     if ws == 1 and not args.no_configs:
         line["other_configs"] = configs_side(eng, threads)
     traffic = REPO / "profiles" / ("fast_kernel_traffic.json" if single else "seg_decode_traffic.json")
@@ -481,31 +483,51 @@ def dropin_side(eng, wl, raws, rep, stats, args):
         shutil.rmtree(d, ignore_errors=True)
 
 
-def timeline_side(eng, config="c5", scale=0.1):
-    """Row a8 (TimelineSink): tally + timeline on the device-heavy config, device time of the ordering and
-    JSON formatting, with size-independent checks (object count = interval messages + metadata objects,
-    json.dump framing, tally equal to the tally-only run)."""
+def timeline_side(eng, threads, config="c5", scale=1.0):
+    """Row a8 (TimelineSink) on the device-heavy config at full size: tally + Chrome-trace JSON of
+    SURVEY.md §8(d) C5 (100M events, 30%+ device-profiling records).  Device time of phase 1 and of the
+    ordering + JSON formatting; roofline bytes = the trace read once + the JSON written once.  Checks
+    (size-independent): object count = interval messages + metadata objects, json.dump framing, the
+    tally of the timeline run equal to the CPU oracle's."""
     from paper_2504_03683_b200 import synth
+    from paper_2504_03683_b200.abi import HG_WANT_TALLY, HG_WANT_TIMELINE
+    from paper_2504_03683_b200.results import build_report
 
     wl = synth.config(config, scale)
-    raws = synth.generate(wl)
+    raws = synth.generate(wl, threads=threads)
     infos = [r.info for r in raws]
-    r0 = eng.run(raws, wl.registry, infos)
-    r1 = None
-    for _ in range(2):
-        r1 = eng.run(raws, wl.registry, infos, want_timeline=True)
-    ms = eng.timeline_ms()
-    tl, st = r1.timeline, r1.stats
+    in_bytes = sum(len(r.data) for r in raws)
+    eng.set_registry(wl.registry)
+    eng.set_streams(raws)
+    eng.stage()
+    p1, tlm = [], []
+    for i in range(3):
+        eng.run_raw(HG_WANT_TALLY | HG_WANT_TIMELINE)
+        k, t, *_ = eng.timing()
+        if i:
+            p1.append(k)
+            tlm.append(eng.timeline_ms())
+    st = eng.stats()
+    rep = build_report(eng._flat, eng.tally_rows(), eng.device_names(), infos,
+                       [(r.hostname, r.pid, r.tid) for r in raws], eng.stream_spans())
+    tl = eng.timeline_bytes()
     msgs = st["host_spans"] + st["truncated_spans"] + st["device_spans"] + st["samples"]
     n_obj = tl.count(b"\n {\n  \"name\": ")
     n_meta = tl.count(b"\"ph\": \"M\"")
-    assert tl[:3] == b"[\n " and tl[-2:] == b"\n]" and n_obj - n_meta == msgs and r1.report == r0.report
+    want, _ = oracle_check(raws, wl.registry, threads)
+    ok = tl[:3] == b"[\n " and tl[-2:] == b"\n]" and n_obj - n_meta == msgs and rep == want.report and \
+        st == want.stats
+    ph1, ms = statistics.mean(p1), statistics.mean(tlm)
+    peak, _ = _peaks()
+    gbs = (in_bytes + len(tl)) / ((ph1 + ms) / 1e3) / 1e9
     return {"workload": f"{config} x{scale}: SURVEY.md §8(d) C5 (device-profiling heavy) + full timeline export",
-            "events": st["events_in"], "messages": msgs, "json_bytes": len(tl),
-            "phase1_ms": r1.kernel_ms, "timeline_ms": ms, "json_gb_per_s": len(tl) / ms / 1e6,
-            "events_per_s": st["events_in"] / ((r1.kernel_ms + ms) / 1e3),
+            "events": st["events_in"], "messages": msgs, "trace_bytes": in_bytes, "json_bytes": len(tl),
+            "phase1_ms": ph1, "timeline_ms": ms, "json_gb_per_s": len(tl) / ms / 1e6,
+            "events_per_s": st["events_in"] / ((ph1 + ms) / 1e3),
+            "roofline": {"bytes": in_bytes + len(tl), "achieved_gb_per_s": gbs, "frac": gbs / peak},
+            "parity": "exact" if ok else "MISMATCH",
             "path": "exact three-kernel phase 1 (record-indexed messages) + k-way merge of the per-stream runs by mux key + JSON formatting",
-            "checks": "object count = messages + metadata, json.dump framing, tally == tally-only run"}
+            "checks": "object count = messages + metadata, json.dump framing, tally + IntervalStats == CPU oracle"}
 
 
 def configs_side(eng, threads, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 0.25), ("c5", 0.25))):
