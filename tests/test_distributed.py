@@ -87,6 +87,8 @@ def _worker(rank, world, port, q, case, tmp):
         wl, raws = _generate()
         if case == "corrupt":
             raws = _corrupt(raws, 5, 40)
+        if case == "few":  # more ranks than streams: some ranks own nothing
+            raws = raws[:2]
         d = os.path.join(tmp, "trace")
         if rank == 0:
             synth.write(wl, raws, d)
@@ -109,12 +111,12 @@ def _worker(rank, world, port, q, case, tmp):
         dist.destroy_process_group()
 
 
-def _run(case):
+def _run(case, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     with tempfile.TemporaryDirectory() as tmp:
-        procs = [ctx.Process(target=_worker, args=(r, 2, port, q, case, tmp)) for r in range(2)]
+        procs = [ctx.Process(target=_worker, args=(r, world, port, q, case, tmp)) for r in range(world)]
         for p in procs:
             p.start()
         outs = dict(q.get(timeout=300) for _ in procs)
@@ -131,6 +133,8 @@ def _oracle(case):
     wl, raws = _generate()
     if case == "corrupt":
         raws = _corrupt(raws, 5, 40)
+    if case == "few":
+        raws = raws[:2]
     return oracle.run(raws, wl.registry, [r.info for r in raws])
 
 
@@ -182,6 +186,15 @@ def test_engine_failure_on_one_rank_stops_both():
         kind, packed, _ = outs[rank]
         assert kind == "raised"
         assert "injected engine failure" in str(unpack_exception(packed))
+
+
+def test_four_ranks_two_streams_idle_ranks_still_agree():
+    """World size 4 over a 2-stream trace: two ranks own no stream, all four return the whole result."""
+    outs = _run("few", world=4)
+    want = _oracle("few")
+    for rank in range(4):
+        kind, rep, stats, orphans, diag = outs[rank]
+        assert kind == "ok" and rep == want.report and stats == want.stats and orphans == want.orphans
 
 
 def test_partition_lpt_balances_and_keeps_identities_together():

@@ -48,6 +48,8 @@ def _worker(rank, world, port, q, case, tmp):
         wl, raws = _generate()
         if case == "corrupt":
             raws = _corrupt(raws, 5, 40)
+        if case == "few":  # more ranks than streams: one rank owns nothing
+            raws = raws[:2]
         d = os.path.join(tmp, "trace")
         if rank == 0:
             synth.write(wl, raws, d)
@@ -79,12 +81,12 @@ def _worker(rank, world, port, q, case, tmp):
         dist.destroy_process_group()
 
 
-def _run(case):
+def _run(case, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     with tempfile.TemporaryDirectory() as tmp:
-        procs = [ctx.Process(target=_worker, args=(r, 2, port, q, case, tmp)) for r in range(2)]
+        procs = [ctx.Process(target=_worker, args=(r, world, port, q, case, tmp)) for r in range(world)]
         for p in procs:
             p.start()
         outs = dict(q.get(timeout=600) for _ in procs)
@@ -101,6 +103,8 @@ def _oracle(case):
     wl, raws = _generate()
     if case == "corrupt":
         raws = _corrupt(raws, 5, 40)
+    if case == "few":
+        raws = raws[:2]
     return oracle.run(raws, wl.registry, [r.info for r in raws])
 
 
@@ -114,6 +118,15 @@ def test_two_ranks_one_gpu_equal_single_process_oracle():
         assert rep == want.report
         assert stats == want.stats
         assert orphans == want.orphans == diag
+
+
+def test_three_ranks_two_streams_idle_rank():
+    """A rank with no stream runs an empty engine pass and still returns the whole trace's result."""
+    outs = _run("few", world=3)
+    want = _oracle("few")
+    for rank in range(3):
+        kind, rep, stats, orphans, diag, _path = outs[rank]
+        assert kind == "ok" and rep == want.report and stats == want.stats and orphans == want.orphans
 
 
 def test_two_ranks_one_gpu_raise_the_reference_first_error():
