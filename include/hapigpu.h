@@ -186,6 +186,7 @@ int hg_stage(hg_ctx* ctx);
 #define HG_WANT_TIMELINE 2u
 #define HG_WANT_EVENTS 4u   /* every record in mux order + PrettyPrintSink's text (events.cu) */
 #define HG_WANT_VALIDATE 8u /* ValidationSink's rules over the mux order (validate.cu) */
+#define HG_WANT_TL_ITEMS 16u /* this rank's timeline messages, sorted, for hg_tl_export (tldist.cu) */
 int hg_run(hg_ctx* ctx, uint32_t want);
 
 /* split form for sharded (multi-GPU) runs: phase 1 over the local streams,
@@ -261,6 +262,20 @@ typedef struct hg_finding {
 } hg_finding;
 int hg_set_validation_rules(hg_ctx* ctx, const hg_validation_rule* rules, uint32_t n_schemas);
 int hg_get_findings(hg_ctx* ctx, hg_finding* out, uint64_t cap, uint64_t* n);
+/* multi-rank timeline (collective (6) of SURVEY.md §8e): every rank runs with HG_WANT_TL_ITEMS
+ * (phase 1 + its timeline messages in mux order), then hg_tl_export writes them into device memory
+ * (`items`: 40-byte records, `payload`: the bytes of the device / telemetry records they print) with
+ * stream keys made global (stream_global[s], flush_global[s]: the stream's index in the whole trace's
+ * (hostname, pid, tid) order and in its (str(hostname), pid, tid) flush order).  Call once with NULL
+ * destinations for the sizes.  Rank 0 concatenates the ranks' exports (NCCL) and hg_tl_import merges
+ * the runs by mux key and formats the JSON exactly as a single run over the whole trace would
+ * (hg_get_timeline).  hosts / pids / tids: the whole trace's identities (NULL host = None, INT64_MIN
+ * pid / tid = None); flush_stream[k] = global stream of flush rank k. */
+int hg_tl_export(hg_ctx* ctx, const uint32_t* stream_global, const uint32_t* flush_global, void* items, void* payload,
+                 uint64_t* n_items, uint64_t* payload_bytes, uint64_t* n_device_spans);
+int hg_tl_import(hg_ctx* ctx, void* items, uint64_t n_items, const uint64_t* run_start, const uint64_t* payload_start,
+                 uint32_t n_runs, const void* payload, const char* const* hosts, const int64_t* pids, const int64_t* tids,
+                 uint32_t n_streams, const uint32_t* flush_stream, uint64_t n_device_spans, uint64_t global_last_ts);
 /* TimelineSink(device_index=) (sinks.py:347-349): device pid 9000000 + index */
 int hg_set_timeline_device(hg_ctx* ctx, int32_t device_index);
 

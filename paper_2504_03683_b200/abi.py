@@ -26,7 +26,7 @@ ROLE_RESULT, ROLE_START, ROLE_END, ROLE_NAME, ROLE_TILE, ROLE_ENGINE, ROLE_CMDKI
 FEED_NONE, FEED_ALWAYS, FEED_TIMELINE = 0, 1, 2
 
 HG_OK, HG_TRACE_ERROR = 0, 1
-HG_WANT_TALLY, HG_WANT_TIMELINE, HG_WANT_EVENTS, HG_WANT_VALIDATE = 1, 2, 4, 8
+HG_WANT_TALLY, HG_WANT_TIMELINE, HG_WANT_EVENTS, HG_WANT_VALIDATE, HG_WANT_TL_ITEMS = 1, 2, 4, 8, 16
 
 (HG_ERR_TRUNC_HEADER, HG_ERR_TRUNC_PAYLOAD, HG_ERR_UNKNOWN_SCHEMA, HG_ERR_LEN_MISMATCH,
  HG_ERR_TRUNC_VAR, HG_ERR_TRAILING, HG_ERR_UTF8, HG_ERR_STRUCT, HG_ERR_ORDER, HG_ERR_FEED,

@@ -59,6 +59,25 @@ struct IngestStats {
 };
 struct IngestPool;  // ingest.cu
 
+// timeline sources (timeline.cu): a context's own messages, or the merged runs of several ranks
+struct TlStreamName {
+  std::string host;
+  bool host_none;
+  int64_t pid;
+  bool pid_none;
+  int64_t tid;
+  bool tid_none;
+};
+struct TlSource {
+  const TlItem* items = nullptr;
+  uint32_t nrec_slots = 0, N = 0, ncomp = 0, n = 0;  // record region, all slots, compose's messages, messages
+  const unsigned long long* rec_off = nullptr;        // first slot of every record-region run (device)
+  uint32_t n_runs = 0;
+  std::vector<TlStreamName> streams;                  // identities the stream field of the keys indexes
+  const uint32_t* flush_stream = nullptr;             // device: flush rank -> stream (truncated spans)
+  uint64_t n_dev = 0;                                 // device spans (thread-name table bound)
+};
+
 struct hg_ctx {
   hg_config cfg{};
   std::string err;
@@ -135,6 +154,12 @@ struct hg_ctx {
   DBuf<unsigned long long> d_tl_th_hi, d_tl_th_lo;
   uint64_t tl_size = 0;
   bool tl_ready = false;
+  const uint32_t* tl_order = nullptr;  // HG_WANT_TL_ITEMS: the messages' mux order (run_timeline_order)
+  uint32_t tl_n = 0;
+  DBuf<uint32_t> d_tlx_len, d_tlx_map;       // multi-rank export: payload lengths, stream maps
+  DBuf<uint64_t> d_tlx_off;
+  DBuf<unsigned long long> d_tlx_runs;       // multi-rank import: run starts
+  DBuf<uint32_t> d_tlx_flush;
   float tl_ms = 0;
   uint64_t tl_comp_base = 0;
   float walk_ms = 0, chain_ms = 0, decode_ms = 0;
@@ -288,6 +313,10 @@ int run_events(hg_ctx* ctx);       // events.cu
 int run_validation(hg_ctx* ctx);   // validate.cu
 int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
             const uint32_t** order);                                                   // timeline.cu
+int tl_sort_runs(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
+                 const unsigned long long* rec_off, uint32_t n_runs, const uint32_t** order);  // timeline.cu
+int run_timeline_order(hg_ctx* ctx);                                                   // timeline.cu
+int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts);            // timeline.cu
 int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint64_t* total);  // timeline.cu
 void ingest_free(hg_ctx* ctx);     // ingest.cu
 }

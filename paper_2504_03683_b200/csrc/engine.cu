@@ -714,7 +714,7 @@ Params make_params(hg_ctx* ctx) {
   p.stack_scratch = ctx->d_stack.ptr;
   p.stack_used = C + C_STACK_USED;
   p.stack_cap = ctx->stack_cap;
-  p.tl_items = (ctx->want & HG_WANT_TIMELINE) ? ctx->d_tl_items.ptr : nullptr;
+  p.tl_items = (ctx->want & (HG_WANT_TIMELINE | HG_WANT_TL_ITEMS)) ? ctx->d_tl_items.ptr : nullptr;
   p.tl_n = C + C_TL_N;
   p.tl_n2 = C + C_TL_N2;
   p.tl_comp_base = ctx->tl_comp_base;
@@ -771,7 +771,8 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;
-  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_TIMELINE | HG_WANT_EVENTS | HG_WANT_VALIDATE));
+  bool fast = ctx->path_opt != 1 &&
+              !(want & (HG_WANT_TIMELINE | HG_WANT_EVENTS | HG_WANT_VALIDATE | HG_WANT_TL_ITEMS));
   bool retried = false;
   for (int attempt = 0; attempt < 9; attempt++) {
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
@@ -943,6 +944,9 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   if (!ctx->errors.empty()) return HG_TRACE_ERROR;
   if (ctx->want & HG_WANT_TIMELINE) {
     int rc = run_timeline(ctx, global_last_ts);
+    if (rc) return rc;
+  } else if (ctx->want & HG_WANT_TL_ITEMS) {
+    int rc = run_timeline_order(ctx);
     if (rc) return rc;
   }
   if (ctx->want & (HG_WANT_EVENTS | HG_WANT_VALIDATE)) {

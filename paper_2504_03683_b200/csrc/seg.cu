@@ -18,7 +18,7 @@ int launch_phase1(hg_ctx* ctx) {
     CK(cudaEventRecord(ctx->ev[7], ctx->stream));
     CK(cudaGetLastError());
     ctx->launches += 2;
-    if (ctx->want & (HG_WANT_TIMELINE | HG_WANT_EVENTS | HG_WANT_VALIDATE)) {
+    if (ctx->want & (HG_WANT_TIMELINE | HG_WANT_EVENTS | HG_WANT_VALIDATE | HG_WANT_TL_ITEMS)) {
       // timeline slots: one per record (segment decode), then compose's messages
       seg_rec_off_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_stream_nrec.ptr, ns, ctx->d_tl_rec_off.ptr,
                                                       ctx->d_counters.ptr + C_REC_TOTAL);
@@ -28,7 +28,7 @@ int launch_phase1(hg_ctx* ctx) {
       CK(cudaStreamSynchronize(ctx->stream));
       ctx->tl_comp_base = total;
       ctx->tl_cap = 2 * total + 64;  // compose adds at most one message per summary entry
-      if (ctx->want & HG_WANT_TIMELINE) CK(ctx->d_tl_items.ensure(ctx->tl_cap));
+      if (ctx->want & (HG_WANT_TIMELINE | HG_WANT_TL_ITEMS)) CK(ctx->d_tl_items.ensure(ctx->tl_cap));
       p = make_params(ctx);
     }
     const size_t smem = seg_smem_layout(ctx->n_fn).total;

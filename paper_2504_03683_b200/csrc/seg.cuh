@@ -645,7 +645,7 @@ static __device__ __noinline__ uint32_t seg_telemetry(const Params& p, const uin
     bad = util ? (bits > 1) : false;
   }
   if (bad) { aux = bits; return HG_ERR_TELEMETRY; }
-  if ((fl & SF_FEED_TIMELINE) && (p.want & HG_WANT_TIMELINE)) { aux = sid; return HG_ERR_FEED; }
+  if ((fl & SF_FEED_TIMELINE) && (p.want & (HG_WANT_TIMELINE | HG_WANT_TL_ITEMS))) { aux = sid; return HG_ERR_FEED; }
   return 0;
 }
 

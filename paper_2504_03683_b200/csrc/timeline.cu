@@ -8,10 +8,9 @@
 // compacted, compose's messages sorted per tile, then all runs merged pairwise with merge-path
 // passes -- the k-way merge of the reference's muxer (pipeline.py:68-114).  *order = item index
 // of every message in mux order (a scratch buffer of the context, valid until the next sort).
-int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
-            const uint32_t** order) {
+int tl_sort_runs(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
+                 const unsigned long long* rec_off, uint32_t ns, const uint32_t** order) {
   cudaStream_t st = ctx->stream;
-  const uint32_t ns = (uint32_t)ctx->streams.size();
   const uint32_t nrec = n - ncomp;
   const uint32_t n_rtiles = (nrec_slots + kSortTile - 1) / kSortTile;
   const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
@@ -32,7 +31,7 @@ int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, u
       ctx->launches += 2;
     }
     tl_compact_kernel<<<n_rtiles + std::max<uint32_t>(ntc, 1), kSortThreads, 0, st>>>(
-        items, nrec_slots, N, ctx->d_tl_tcnt.ptr, n_rtiles, ctx->d_tl_rec_off.ptr, ns, nrec, n,
+        items, nrec_slots, N, ctx->d_tl_tcnt.ptr, n_rtiles, rec_off, ns, nrec, n,
         ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, ctx->d_tl_ro[0].ptr);
     ctx->launches++;
     if (ntc) {
@@ -59,6 +58,11 @@ int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, u
   return HG_OK;
 }
 
+int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
+            const uint32_t** order) {
+  return tl_sort_runs(ctx, items, nrec_slots, N, ncomp, n, ctx->d_tl_rec_off.ptr, (uint32_t)ctx->streams.size(), order);
+}
+
 // exclusive scan of n u32 lengths into u64 offsets, *total (device) = the sum
 int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint64_t* total) {
   const uint32_t nsb = (n + kScanBlock - 1) / kScanBlock;
@@ -70,18 +74,51 @@ int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint6
   return HG_OK;
 }
 
-// order, format and store the timeline JSON (TimelineSink.on_finish, sinks.py:414-418)
+// the context's own messages: the record region of every stream + compose's messages
+static TlSource own_source(hg_ctx* ctx) {
+  const unsigned long long* C = ctx->counters.data();
+  TlSource S;
+  S.items = ctx->d_tl_items.ptr;
+  S.nrec_slots = (uint32_t)ctx->tl_comp_base;
+  S.N = (uint32_t)(ctx->tl_comp_base + C[C_TL_N2]);
+  S.ncomp = (uint32_t)C[C_TL_N2];
+  S.n = (uint32_t)(C[C_TL_N] + C[C_TL_N2]);  // messages; the sort moves the empty slots last
+  S.rec_off = ctx->d_tl_rec_off.ptr;
+  S.n_runs = (uint32_t)ctx->streams.size();
+  for (const HostStream& hs : ctx->streams)
+    S.streams.push_back(TlStreamName{hs.host, hs.host_none, hs.pid, hs.pid_none, hs.tid, hs.tid_none});
+  S.flush_stream = ctx->flush_order ? ctx->d_flush_stream.ptr : nullptr;
+  S.n_dev = C[C_STATS + ST_DEVICE];
+  return S;
+}
+
 int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->tl_ready = false;
-  if (!ctx->have_fn_names || ctx->fn_names.size() != ctx->n_fn)
-    return fail(ctx, HG_ESTATE, "hg_set_function_names is required for the timeline");
   const unsigned long long* C = ctx->counters.data();
   const uint64_t n_slots = ctx->tl_comp_base + C[C_TL_N2];
   if (n_slots > ctx->tl_cap || n_slots >= (1ull << 32))
     return fail(ctx, HG_ENOMEM, "timeline message buffer overflow");
-  const uint32_t n = (uint32_t)(C[C_TL_N] + C[C_TL_N2]);  // messages; the sort moves the empty slots last
-  const uint32_t N = (uint32_t)n_slots;
-  const uint32_t ns = (uint32_t)ctx->streams.size();
+  return timeline_from(ctx, own_source(ctx), global_last_ts);
+}
+
+// the messages of a context sorted by mux key only (a rank's share of a multi-rank timeline)
+int run_timeline_order(hg_ctx* ctx) {
+  ctx->tl_order = nullptr;
+  const unsigned long long* C = ctx->counters.data();
+  if (ctx->tl_comp_base + C[C_TL_N2] > ctx->tl_cap || ctx->tl_comp_base + C[C_TL_N2] >= (1ull << 32))
+    return fail(ctx, HG_ENOMEM, "timeline message buffer overflow");
+  const TlSource S = own_source(ctx);
+  ctx->tl_n = S.n;
+  return tl_sort_runs(ctx, S.items, S.nrec_slots, S.N, S.ncomp, S.n, S.rec_off, S.n_runs, &ctx->tl_order);
+}
+
+// order, format and store the timeline JSON (TimelineSink.on_finish, sinks.py:414-418)
+int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
+  ctx->tl_ready = false;
+  if (!ctx->have_fn_names || ctx->fn_names.size() != ctx->n_fn)
+    return fail(ctx, HG_ESTATE, "hg_set_function_names is required for the timeline");
+  const uint32_t n = S.n;
+  const uint32_t ns = (uint32_t)S.streams.size();
   cudaStream_t st = ctx->stream;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
@@ -101,7 +138,7 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   std::vector<uint32_t> sproc(std::max<uint32_t>(ns, 1), 0);
   std::map<int64_t, uint32_t> proc_id;  // process_name metas are keyed by (pid, 0)
   for (uint32_t s = 0; s < ns; s++) {
-    const HostStream& hs = ctx->streams[s];
+    const TlStreamName& hs = S.streams[s];
     // None pid / tid (record sources): JSON null, "None" in the process name (sinks.py:367-369)
     std::string a = hs.pid_none ? std::string("null") : std::to_string(hs.pid);
     std::string b = hs.tid_none ? std::string("null") : std::to_string(hs.tid);
@@ -129,14 +166,13 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   CK(upload(ctx->d_tl_devpid, devpid, st));
   // sort by mux key: the streams' record slots are sorted runs; drop the empty slots, sort
   // compose's messages per tile, merge the runs pairwise
-  const uint32_t ncomp = (uint32_t)C[C_TL_N2];
   const uint32_t* order = nullptr;
   {
-    int rc = tl_sort(ctx, ctx->d_tl_items.ptr, (uint32_t)ctx->tl_comp_base, N, ncomp, n, &order);
+    int rc = tl_sort_runs(ctx, S.items, S.nrec_slots, S.N, S.ncomp, n, S.rec_off, S.n_runs, &order);
     if (rc) return rc;
   }
   // metadata first occurrences
-  uint64_t n_dev = C[C_STATS + ST_DEVICE];
+  const uint64_t n_dev = S.n_dev;
   uint32_t th_size = 64;
   while (th_size < 2 * n_dev && th_size < (1u << 30)) th_size <<= 1;
   CK(ctx->d_tl_proc_first.ensure(n_proc));
@@ -150,7 +186,7 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   CK(ctx->d_tl_lens.ensure(std::max<uint32_t>(n, 1)));
   CK(ctx->d_tl_offs.ensure(std::max<uint32_t>(n, 1)));
   TlTables T{};
-  T.items = ctx->d_tl_items.ptr;
+  T.items = S.items;
   T.n = n;
   T.order = order;
   T.fnq = ctx->d_tl_fnq.ptr;
@@ -173,7 +209,7 @@ int run_timeline(hg_ctx* ctx, uint64_t global_last_ts) {
   T.kinds = ctx->d_kinds.ptr;
   T.max_sid = ctx->max_sid;
   T.last_ts = global_last_ts;
-  T.flush_stream = ctx->flush_order ? ctx->d_flush_stream.ptr : nullptr;
+  T.flush_stream = S.flush_stream;
   T.lens = ctx->d_tl_lens.ptr;
   T.offs = ctx->d_tl_offs.ptr;
   uint64_t total = 0;

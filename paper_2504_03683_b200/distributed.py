@@ -111,6 +111,31 @@ class Comm:
         self.dist.all_gather_object(out, obj, group=self.group)
         return out
 
+    def gather_to0(self, t, sizes):
+        """Rank 0 receives every rank's 1-D uint8 tensor (sizes[r] bytes each; point-to-point sends)."""
+        torch = self.torch
+        on_dev = self.device.type == "cuda"
+        if self.rank != 0:
+            if sizes[self.rank]:
+                self.dist.send(t if on_dev else t.cpu(), dst=0, group=self.group)
+            return None
+        out = [t]
+        for r in range(1, self.world):
+            buf = torch.empty(sizes[r], dtype=torch.uint8, device=self.device)
+            if sizes[r]:
+                self.dist.recv(buf, src=r, group=self.group)
+            out.append(buf)
+        return out
+
+
+def _all_gather_i64(comm, values):
+    """Every rank's small int list, concatenated in rank order."""
+    torch = comm.torch
+    t = torch.tensor(values, dtype=torch.int64, device=comm.device)
+    out = [torch.zeros_like(t) for _ in range(comm.world)]
+    comm.dist.all_gather(out, t, group=comm.group)
+    return [int(x) for o in out for x in o.tolist()]
+
 
 def _names_blob(names):
     enc = [n.encode("utf-8") for n in names]
@@ -297,6 +322,58 @@ class ShardedRun:
             if c is not None:
                 cuts.update(c[2])
         return key, exc, cuts
+
+    def timeline(self, device_index=0):
+        """The whole trace's TimelineSink JSON after a step with HG_WANT_TL_ITEMS (collective (6) of
+        SURVEY.md §8e): every rank exports its sorted messages with global stream keys
+        (hg_tl_export), rank 0 receives them and merges + formats them (hg_tl_import).  Returns the
+        bytes on rank 0, None on the other ranks."""
+        import ctypes as C
+
+        import torch
+
+        eng, comm = self.engine, self.comm
+        L, ctx = eng._L, eng._ctx
+        gs = self.global_streams
+        n_gs = len(gs)
+        order = sorted(range(n_gs), key=lambda i: (str(gs[i].hostname), gs[i].pid or 0, gs[i].tid or 0, i))
+        flush_rank = [0] * n_gs
+        for k, i in enumerate(order):
+            flush_rank[i] = k
+        sg = self.stream_global
+        ns = len(sg)
+        n, pb, ndev = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        eng._check(L.hg_tl_export(ctx, None, None, None, None, C.byref(n), C.byref(pb), C.byref(ndev)), "hg_tl_export")
+        dev = eng.tensor_device()
+        items = torch.empty(max(40 * n.value, 1), dtype=torch.uint8, device=dev)
+        pay = torch.empty(max(pb.value, 1), dtype=torch.uint8, device=dev)
+        smap = (C.c_uint32 * max(ns, 1))(*sg)
+        fmap = (C.c_uint32 * max(ns, 1))(*[flush_rank[g] for g in sg])
+        eng._check(L.hg_tl_export(ctx, smap, fmap, C.c_void_p(items.data_ptr()), C.c_void_p(pay.data_ptr()),
+                                  C.byref(n), C.byref(pb), C.byref(ndev)), "hg_tl_export")
+        meta = [int(x) for x in _all_gather_i64(comm, [n.value, pb.value, ndev.value])]
+        counts, pays, devs = meta[0::3], meta[1::3], meta[2::3]
+        got_items = comm.gather_to0(items[: 40 * n.value], [40 * c for c in counts])
+        got_pay = comm.gather_to0(pay[: pb.value], pays)
+        if comm.rank != 0:
+            return None
+        run0, pay0, a, b = [], [], 0, 0
+        for c, p_ in zip(counts, pays):
+            run0.append(a)
+            pay0.append(b)
+            a += c
+            b += p_
+        all_items = torch.cat([t.to(dev) for t in got_items] + [items[:40]])  # + padding: never empty
+        all_pay = torch.cat([t.to(dev) for t in got_pay] + [pay[:1]])
+        hosts = (C.c_char_p * max(n_gs, 1))(*[None if x.hostname is None else str(x.hostname).encode() for x in gs])
+        pids = (C.c_int64 * max(n_gs, 1))(*[-(1 << 63) if x.pid is None else int(x.pid) for x in gs])
+        tids = (C.c_int64 * max(n_gs, 1))(*[-(1 << 63) if x.tid is None else int(x.tid) for x in gs])
+        eng._check(L.hg_set_timeline_device(ctx, int(device_index)), "hg_set_timeline_device")
+        eng._check(L.hg_tl_import(ctx, C.c_void_p(all_items.data_ptr()), a, (C.c_uint64 * len(run0))(*run0),
+                                  (C.c_uint64 * len(pay0))(*pay0), len(run0), C.c_void_p(all_pay.data_ptr()), hosts,
+                                  pids, tids, n_gs, (C.c_uint32 * max(n_gs, 1))(*order), sum(devs),
+                                  self.global_last_ts), "hg_tl_import")
+        return eng.timeline_bytes()
 
     # the round-1 name, kept for callers that only want the tally
     def report(self, stream_infos=None):

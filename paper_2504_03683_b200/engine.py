@@ -266,6 +266,9 @@ class Engine:
             self._check(rc, "hg_run")
         return rc
 
+    def set_timeline_device(self, index: int):
+        self._check(self._L.hg_set_timeline_device(self._ctx, int(index)), "hg_set_timeline_device")
+
     def tensor_device(self):
         import torch
 

@@ -28,7 +28,7 @@ NVCC_FLAGS = [
 
 def sources():
     """One translation unit per kernel family (ctx.h): they compile in parallel."""
-    return [CSRC / "engine.cu", CSRC / "fast.cu", CSRC / "seg.cu", CSRC / "timeline.cu", CSRC / "merge.cu", CSRC / "ingest.cu", CSRC / "events.cu", CSRC / "validate.cu"]
+    return [CSRC / "engine.cu", CSRC / "fast.cu", CSRC / "seg.cu", CSRC / "timeline.cu", CSRC / "merge.cu", CSRC / "ingest.cu", CSRC / "events.cu", CSRC / "validate.cu", CSRC / "tldist.cu"]
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
@@ -115,6 +115,8 @@ def lib():
         "hg_events_ms": ([vp, vp], C.c_int),
         "hg_set_validation_rules": ([vp, vp, u32], C.c_int),
         "hg_get_findings": ([vp, vp, u64, vp], C.c_int),
+        "hg_tl_export": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "hg_tl_import": ([vp, vp, u64, vp, vp, u32, vp, vp, vp, vp, u32, vp, u64, u64], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -134,5 +136,6 @@ EXPORTED = (
     "hg_timeline_ms", "hg_set_timeline_device", "hg_phase_timing", "hg_set_option", "hg_last_path",
     "hg_set_flush_order", "hg_merge_size", "hg_merge_export", "hg_merge_import", "hg_add_stream_device",
     "hg_add_stream_file", "hg_ingest_stats", "hg_set_schema_names", "hg_events_size", "hg_get_events",
-    "hg_get_event_order", "hg_events_ms", "hg_set_validation_rules", "hg_get_findings",
+    "hg_get_event_order", "hg_events_ms", "hg_set_validation_rules", "hg_get_findings", "hg_tl_export",
+    "hg_tl_import",
 )

@@ -376,8 +376,9 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
         if not isinstance(s, (TallySink, TimelineSink, ValidationSink)) and not _is_pretty(s) and not _is_passive(s):
             raise UnsupportedTraceError(
                 f"sink {s.name!r} needs per-message callbacks; hapigpu serves TallySink/TimelineSink/PrettyPrintSink")
-    # sinks that need the global mux order of every record (timeline, events, validation) are served
-    # by rank 0 from the whole trace in a multi-rank run; the other ranks return None for them
+    # in a multi-rank run the timeline is merged across ranks (rank 0 formats it, ShardedRun.timeline);
+    # the event sinks (every record in global mux order) are served by rank 0 from the whole trace;
+    # the other ranks return None for these sinks
     ordered = timeline + pretty + validate
     device_index = {s.device_index for s in timeline}
     if len(device_index) > 1:
@@ -396,14 +397,14 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
                           orphan_labels=olabels, timeline_device_index=next(iter(device_index), 0),
                           want_events=bool(pretty), validation=validate[0].rules if validate else None)
         else:
-            res = _run_sharded(eng, registry, shard, comm)
-            if ordered and res.error is None and comm.rank == 0:
+            res = _run_sharded(eng, registry, shard, comm, timeline_device=next(iter(device_index), 0)
+                               if timeline else None)
+            if (pretty or validate) and res.error is None and comm.rank == 0:
                 full, _ = _resolve_source(source, registry)
-                r0 = eng.run(full, registry, infos, want_timeline=bool(timeline),
-                             labels=[r.name for r in full], orphan_labels=[f"{r.hostname}/{r.pid}/{r.tid}" for r in full],
-                             timeline_device_index=next(iter(device_index), 0), want_events=bool(pretty),
+                r0 = eng.run(full, registry, infos, labels=[r.name for r in full],
+                             orphan_labels=[f"{r.hostname}/{r.pid}/{r.tid}" for r in full], want_events=bool(pretty),
                              validation=validate[0].rules if validate else None)
-                res.timeline, res.events, res.findings = r0.timeline, r0.events, r0.findings
+                res.events, res.findings = r0.events, r0.findings
     finally:  # diagnostics reach interested sinks even when the run fails (pipeline.py:307-312)
         for s in sinks:
             hook = getattr(s, "on_diagnostics", None)
@@ -480,16 +481,23 @@ def _resolve_sharded(source, registry, comm) -> _Shard:
     return _Shard(merged, [first[(r.hostname, r.pid, r.tid)] for r in merged], ids, infos, None)
 
 
-def _run_sharded(eng, registry, shard, comm):
+def _run_sharded(eng, registry, shard, comm, timeline_device=None):
+    """timeline_device: the TimelineSink's device_index when the run also builds the timeline (every
+    rank's messages merged by rank 0, ShardedRun.timeline)."""
+    from .abi import HG_WANT_TALLY, HG_WANT_TL_ITEMS
     from .distributed import ShardedRun
     from .engine import RunResult
 
     eng.set_registry(registry)
     eng.set_streams(shard.raws)
     run = ShardedRun(eng, registry, comm, shard.stream_global, shard.global_streams)
-    info = run.step(input_error=shard.input_error)
+    want = HG_WANT_TALLY | (HG_WANT_TL_ITEMS if timeline_device is not None else 0)
+    info = run.step(want=want, input_error=shard.input_error)
     labels = [s.name for s in shard.global_streams]
     olabels = [f"{s.hostname}/{s.pid}/{s.tid}" for s in shard.global_streams]
     report, stats, orphans, error = run.result(shard.infos, labels, olabels)
-    return RunResult(report, stats, orphans, error, None, info["phase1_ms"], info["device_ms"], info["h2d_bytes"],
+    timeline = None
+    if timeline_device is not None and error is None:
+        timeline = run.timeline(timeline_device)
+    return RunResult(report, stats, orphans, error, timeline, info["phase1_ms"], info["device_ms"], info["h2d_bytes"],
                      info["d2h_bytes"], info["launches"])

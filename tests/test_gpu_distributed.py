@@ -25,6 +25,13 @@ def _free_port():
     return port
 
 
+def _c5():
+    from paper_2504_03683_b200 import synth
+
+    wl = synth.config("c5", 0.0004)  # 256 call streams + the telemetry sampler stream
+    return wl, synth.generate(wl)
+
+
 def _worker(rank, world, port, q, case, tmp):
     import torch.distributed as dist
 
@@ -45,7 +52,7 @@ def _worker(rank, world, port, q, case, tmp):
             def on_diagnostics(self, orphans):
                 self.orphans = orphans
 
-        wl, raws = _generate()
+        wl, raws = _generate() if case != "c5" else _c5()
         if case == "corrupt":
             raws = _corrupt(raws, 5, 40)
         if case == "few":  # more ranks than streams: one rank owns nothing
@@ -57,6 +64,14 @@ def _worker(rank, world, port, q, case, tmp):
         eng = Engine(device=0)
         diag = Diag()
         try:
+            if case == "c5":  # the timeline merged across ranks (device spans, samples, metadata objects)
+                from paper_2504_03683_b200 import TimelineSink
+
+                res = run_pipeline(open_trace_reader(d), [TallySink(), TimelineSink(device_index=3)], engine=eng,
+                                   distributed=True)
+                eng.close()
+                q.put((rank, ("ok", res["tally"], res["timeline"])))
+                return
             if case == "ordered":  # timeline / pretty / validation: rank 0 serves them from the whole trace
                 import json as _json
 
@@ -165,3 +180,20 @@ def test_two_ranks_ordered_sinks_served_by_rank0():
     assert val == [tuple(f) for f in findings]
     kind, rep, tl, pretty, val = outs[1]
     assert kind == "ok" and rep == want.report and tl is None and pretty is None and val is None
+
+
+def test_three_ranks_timeline_merged_across_ranks():
+    """Collective (6): each rank's timeline messages (global stream keys, record payloads attached)
+    merged and formatted by rank 0 -- equal to the single-process timeline of the whole trace."""
+    import json
+
+    from oracle import oracle
+
+    outs = _run("c5", world=3)
+    wl, raws = _c5()
+    want = oracle.run(raws, wl.registry, [r.info for r in raws], want_timeline=True, device_index=3)
+    kind, rep, tl = outs[0]
+    assert kind == "ok" and rep == want.report and tl == json.loads(want.timeline)
+    for rank in (1, 2):
+        kind, rep, tl = outs[rank]
+        assert kind == "ok" and rep == want.report and tl is None
