@@ -220,6 +220,10 @@ struct hg_ctx {
   DBuf<hg_finding> d_val_fnd;
   std::vector<hg_finding> val_findings;
   bool val_ready = false;
+  size_t compose_smem = 0;  // compose_kernel's dynamic shared memory attribute as last set
+  // pinned host staging of small results (counters, tally rows, names, orphans, errors): one sync
+  uint8_t* pin = nullptr;
+  size_t pin_cap = 0;
   // ingest (ingest.cu): pinned staging pool and the last staging's numbers
   IngestPool* ingest = nullptr;
   IngestStats ingest_stats;

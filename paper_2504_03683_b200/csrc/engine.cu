@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
         en.ts = 0; en.fn = 0;
         if (on) {
           en = gs.at(i);
-          hf.fold(p, en.fn, p.global_last_ts - en.ts, false);
+          hf.fold(p, en.fn, (p.last_ts_dev ? *p.last_ts : p.global_last_ts) - en.ts, false);
           trunc++;
           spans++;
         }
@@ -250,6 +250,8 @@ void hg_destroy(hg_ctx* ctx) {
   cudaSetDevice(ctx->cfg.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   ingest_free(ctx);
+  if (ctx->pin) cudaFreeHost(ctx->pin);
+  ctx->pin = nullptr;
   ctx->d_schemas.release(); ctx->d_sid_map.release(); ctx->d_kinds.release(); ctx->d_field_role.release();
   ctx->d_data.release(); ctx->d_base.release(); ctx->d_size.release();
   ctx->d_tile_stream.release(); ctx->d_stream_tile0.release();
@@ -757,10 +759,26 @@ int init_run(hg_ctx* ctx) {
   return HG_OK;
 }
 
+// pinned host staging for device -> host result copies (pageable destinations would make every
+// cudaMemcpyAsync a synchronous round trip)
+static int pinned(hg_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->pin_cap) return HG_OK;
+  if (ctx->pin) cudaFreeHost(ctx->pin);
+  ctx->pin = nullptr;
+  ctx->pin_cap = 0;
+  const size_t cap = std::max<size_t>(bytes + (bytes >> 1), 1 << 16);
+  CK(cudaHostAlloc(&ctx->pin, cap, cudaHostAllocDefault));
+  ctx->pin_cap = cap;
+  return HG_OK;
+}
+
 static int read_counters(hg_ctx* ctx) {
-  ctx->counters.resize(C_NUM);
-  CK(cudaMemcpyAsync(ctx->counters.data(), ctx->d_counters.ptr, C_NUM * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  int rc = pinned(ctx, C_NUM * 8);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(ctx->pin, ctx->d_counters.ptr, C_NUM * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  ctx->counters.assign(reinterpret_cast<const unsigned long long*>(ctx->pin),
+                       reinterpret_cast<const unsigned long long*>(ctx->pin) + C_NUM);
   return HG_OK;
 }
 
@@ -848,41 +866,55 @@ int hg_local_last_ts(hg_ctx* ctx, uint64_t* last_ts, uint64_t* n_events) {
   return HG_OK;
 }
 
+// cross-range / cross-segment composition and truncation (compose_kernel), queued on the stream
+static int launch_compose(hg_ctx* ctx, uint64_t global_last_ts, bool last_ts_on_device) {
+  const uint32_t ns = (uint32_t)ctx->streams.size();
+  if (!ns) return HG_OK;
+  Params p = make_params(ctx);
+  p.global_last_ts = global_last_ts;
+  p.last_ts_dev = last_ts_on_device ? 1u : 0u;
+  if (ctx->last_path == 1) {  // summaries per range (fast.cuh)
+    p.state = ctx->d_rseg.ptr;
+    p.stream_tile0 = ctx->d_stream_range0.ptr;
+    p.n_tiles = ctx->n_ranges;
+  }
+  CK(cudaMemsetAsync(p.stack_used, 0, 8, ctx->stream));
+  // the tally accumulators already hold phase-1 spans; compose adds the rest
+  size_t csmem = (ctx->n_fn <= kSmemFnMax ? ((sizeof(SmemRow) * ctx->n_fn + 15) & ~(size_t)15) : 0) +
+                 sizeof(SumEntry) * kComposeFast * kComposeWarps;
+  if (csmem != ctx->compose_smem) {
+    CK(cudaFuncSetAttribute(compose_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
+    CK(cudaFuncSetAttribute(compose_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
+    ctx->compose_smem = csmem;
+  }
+  if (ctx->last_path == 1 && ctx->n_blk < ctx->n_ranges) {
+    // blocks of 32 ranges first, then each stream over its block summaries
+    ComposeBlocks B{ctx->d_blk_stream.ptr, ctx->d_blk_u0.ptr, ctx->d_blk_state.ptr, ctx->n_blk};
+    compose_kernel<true><<<(ctx->n_blk + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem,
+                           ctx->stream>>>(p, B);
+    CK(cudaMemsetAsync(p.stack_used, 0, 8, ctx->stream));
+    p.state = ctx->d_blk_state.ptr;
+    p.stream_tile0 = ctx->d_stream_blk0.ptr;
+    p.n_tiles = ctx->n_blk;
+    ctx->launches++;
+  }
+  compose_kernel<false><<<(ns + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem, ctx->stream>>>(
+      p, ComposeBlocks{nullptr, nullptr, nullptr, 0});
+  CK(cudaGetLastError());
+  ctx->launches++;
+  return HG_OK;
+}
+
+static int collect_results(hg_ctx* ctx, uint64_t global_last_ts);
+
 int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   if (!ctx || !ctx->phase1_done) return HG_ESTATE;
   cudaSetDevice(ctx->cfg.device);
   const uint32_t ns = (uint32_t)ctx->streams.size();
   for (int attempt = 0; attempt < 3; attempt++) {
     if (ns) {
-      Params p = make_params(ctx);
-      p.global_last_ts = global_last_ts;
-      if (ctx->last_path == 1) {  // summaries per range (fast.cuh)
-        p.state = ctx->d_rseg.ptr;
-        p.stream_tile0 = ctx->d_stream_range0.ptr;
-        p.n_tiles = ctx->n_ranges;
-      }
-      unsigned long long zero = 0;
-      CK(cudaMemcpyAsync(p.stack_used, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
-      // the tally accumulators already hold phase-1 spans; compose adds the rest
-      size_t csmem = (ctx->n_fn <= kSmemFnMax ? ((sizeof(SmemRow) * ctx->n_fn + 15) & ~(size_t)15) : 0) +
-                     sizeof(SumEntry) * kComposeFast * kComposeWarps;
-      CK(cudaFuncSetAttribute(compose_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
-      CK(cudaFuncSetAttribute(compose_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(csmem, 1)));
-      if (ctx->last_path == 1 && ctx->n_blk < ctx->n_ranges) {
-        // blocks of 32 ranges first, then each stream over its block summaries
-        ComposeBlocks B{ctx->d_blk_stream.ptr, ctx->d_blk_u0.ptr, ctx->d_blk_state.ptr, ctx->n_blk};
-        compose_kernel<true><<<(ctx->n_blk + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem,
-                               ctx->stream>>>(p, B);
-        CK(cudaMemcpyAsync(p.stack_used, &zero, 8, cudaMemcpyHostToDevice, ctx->stream));
-        p.state = ctx->d_blk_state.ptr;
-        p.stream_tile0 = ctx->d_stream_blk0.ptr;
-        p.n_tiles = ctx->n_blk;
-        ctx->launches++;
-      }
-      compose_kernel<false><<<(ns + kComposeWarps - 1) / kComposeWarps, kComposeWarps * kWarp, csmem, ctx->stream>>>(
-          p, ComposeBlocks{nullptr, nullptr, nullptr, 0});
-      CK(cudaGetLastError());
-      ctx->launches++;
+      int lrc = launch_compose(ctx, global_last_ts, false);
+      if (lrc) return lrc;
     }
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
     int rc = read_counters(ctx);
@@ -893,33 +925,53 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
       break;
     return fail(ctx, HG_ENOMEM, "composition scratch overflow");  // TODO: rerun the whole pipeline with larger buffers
   }
-  // results to the host
+  return collect_results(ctx, global_last_ts);
+}
+
+// results to the host (every copy into one pinned staging buffer, one synchronisation), timings,
+// and the timeline / event / validation passes a run asked for
+static int collect_results(hg_ctx* ctx, uint64_t global_last_ts) {
+  const uint32_t ns = (uint32_t)ctx->streams.size();
   unsigned long long* C = ctx->counters.data();
   ctx->n_dev_rows = (uint32_t)std::min<unsigned long long>(C[C_N_ROWS], ctx->row_cap);
+  ctx->d2h_bytes = C_NUM * 8;
+  const uint64_t arena_used = std::min<uint64_t>(C[C_ARENA_USED], ctx->arena_cap);
+  const uint64_t n_orph = std::min<uint64_t>(C[C_N_ORPHANS], ctx->orphan_cap);
+  const uint32_t n_err = (uint32_t)std::min<unsigned long long>((uint32_t)C[C_N_ERRORS], ctx->error_cap);
+  struct Part { void* dst; const void* src; size_t bytes; size_t at; };
+  Part parts[8];
+  int np = 0;
+  size_t total = 0;
+  auto part = [&](void* dst, const void* src, size_t bytes) {
+    if (!bytes) return;
+    parts[np++] = Part{dst, src, bytes, total};
+    total += (bytes + 15) & ~(size_t)15;
+  };
   ctx->host_acc.resize(6ull * ctx->n_fn);
   ctx->dev_acc.resize(6ull * ctx->n_dev_rows);
-  ctx->d2h_bytes = C_NUM * 8;
-  if (ctx->n_fn) CK(cudaMemcpyAsync(ctx->host_acc.data(), ctx->d_host_acc.ptr, ctx->host_acc.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
-  if (ctx->n_dev_rows) CK(cudaMemcpyAsync(ctx->dev_acc.data(), ctx->d_dev_acc.ptr, ctx->dev_acc.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
   ctx->name_off.resize(ctx->n_dev_rows);
   ctx->name_len.resize(ctx->n_dev_rows);
-  uint64_t arena_used = std::min<uint64_t>(C[C_ARENA_USED], ctx->arena_cap);
   ctx->arena.resize(arena_used);
-  if (ctx->n_dev_rows) {
-    CK(cudaMemcpyAsync(ctx->name_off.data(), ctx->d_name_off.ptr, ctx->n_dev_rows * 8, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->name_len.data(), ctx->d_name_len.ptr, ctx->n_dev_rows * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  }
-  if (arena_used) CK(cudaMemcpyAsync(ctx->arena.data(), ctx->d_arena.ptr, arena_used, cudaMemcpyDeviceToHost, ctx->stream));
-  uint64_t n_orph = std::min<uint64_t>(C[C_N_ORPHANS], ctx->orphan_cap);
   ctx->orphans.resize(n_orph);
-  if (n_orph) CK(cudaMemcpyAsync(ctx->orphans.data(), ctx->d_orphans.ptr, n_orph * sizeof(hg_orphan), cudaMemcpyDeviceToHost, ctx->stream));
-  uint32_t n_err = (uint32_t)std::min<unsigned long long>((uint32_t)C[C_N_ERRORS], ctx->error_cap);
   ctx->errors.resize(n_err);
-  if (n_err) CK(cudaMemcpyAsync(ctx->errors.data(), ctx->d_errors.ptr, n_err * sizeof(hg_trace_error), cudaMemcpyDeviceToHost, ctx->stream));
   ctx->stream_spans.resize(ns);
-  if (ns) CK(cudaMemcpyAsync(ctx->stream_spans.data(), ctx->d_stream_spans.ptr, ns * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  part(ctx->host_acc.data(), ctx->d_host_acc.ptr, ctx->host_acc.size() * 8);
+  part(ctx->dev_acc.data(), ctx->d_dev_acc.ptr, ctx->dev_acc.size() * 8);
+  part(ctx->name_off.data(), ctx->d_name_off.ptr, ctx->n_dev_rows * 8ull);
+  part(ctx->name_len.data(), ctx->d_name_len.ptr, ctx->n_dev_rows * 4ull);
+  part(ctx->arena.data(), ctx->d_arena.ptr, arena_used);
+  part(ctx->orphans.data(), ctx->d_orphans.ptr, n_orph * sizeof(hg_orphan));
+  part(ctx->errors.data(), ctx->d_errors.ptr, n_err * sizeof(hg_trace_error));
+  part(ctx->stream_spans.data(), ctx->d_stream_spans.ptr, ns * 8ull);
+  {
+    int prc = pinned(ctx, total);
+    if (prc) return prc;
+  }
+  for (int i = 0; i < np; i++)
+    CK(cudaMemcpyAsync(ctx->pin + parts[i].at, parts[i].src, parts[i].bytes, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaEventRecord(ctx->ev[3], ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  for (int i = 0; i < np; i++) memcpy(parts[i].dst, ctx->pin + parts[i].at, parts[i].bytes);
   ctx->d2h_bytes += ctx->host_acc.size() * 8 + ctx->dev_acc.size() * 8 + arena_used + n_orph * sizeof(hg_orphan) +
                     n_err * sizeof(hg_trace_error) + ns * 8 + ctx->n_dev_rows * 12;
   float k_ms = 0, t_ms = 0;
@@ -957,7 +1009,55 @@ int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   return HG_OK;
 }
 
+// one rank, tally only, single pass: phase 1 and composition back to back -- compose reads the last
+// timestamp fast_verify left on the device -- and ONE synchronisation for the counters.  Anything
+// the single pass or the scratch sizes cannot vouch for is redone by the split path below.
+static int run_fused(hg_ctx* ctx, uint32_t want, bool& done) {
+  done = false;
+  ctx->want = want;
+  ctx->have_results = false;
+  ctx->merged = false;
+  ctx->phase1_done = false;
+  CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+  uint64_t h2d = 0;
+  if (!ctx->staged) {
+    int rc = stage(ctx);
+    if (rc) return rc;
+    h2d = ctx->h2d_bytes;
+  }
+  CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+  int rc = ensure_scratch(ctx, 0);
+  if (!rc) rc = launch_fast(ctx);
+  if (rc) return rc;
+  ctx->last_path = 1;
+  rc = launch_compose(ctx, 0, true);
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+  rc = read_counters(ctx);
+  if (rc) return rc;
+  ctx->h2d_bytes = h2d;
+  const unsigned long long* C = ctx->counters.data();
+  const bool clean = !(uint32_t)C[C_ANOM] && !(uint32_t)C[C_OVERFLOW] && !(uint32_t)C[C_WIDE] &&
+                     !(uint32_t)C[C_WATCHDOG] && !(uint32_t)C[C_N_ERRORS] && 2 * C[C_POOL_USED] <= ctx->pool_cap &&
+                     C[C_N_ORPHANS] <= ctx->orphan_cap && C[C_DEEP_USED] <= ctx->deep_cap &&
+                     C[C_STACK_USED] <= ctx->stack_cap;
+  if (!clean) return HG_OK;  // not done: the split path reruns everything
+  if (C[C_DEEP_USED] > 0) ctx->deep_inline = true;
+  ctx->local_last_ts = C[C_LAST_TS];
+  ctx->local_events = C[C_STATS + ST_EVENTS];
+  ctx->phase1_done = true;
+  done = true;
+  return collect_results(ctx, ctx->local_last_ts);
+}
+
 int hg_run(hg_ctx* ctx, uint32_t want) {
+  if (!ctx) return HG_EARG;
+  cudaSetDevice(ctx->cfg.device);
+  if (want == HG_WANT_TALLY && ctx->path_opt != 1 && !getenv("HAPIGPU_NO_FUSED")) {
+    bool done = false;
+    int rc = run_fused(ctx, want, done);
+    if (rc || done) return rc;
+  }
   int rc = hg_run_local(ctx, want);
   if (rc) return rc;
   return hg_finish(ctx, ctx->local_last_ts);

@@ -85,6 +85,7 @@ struct Params {
   unsigned long long* stack_used;
   uint64_t stack_cap;
   uint64_t global_last_ts;
+  uint32_t last_ts_dev;            // compose: the global last ts is *last_ts (one-rank fused run)
   // timeline messages (nullptr unless HG_WANT_TIMELINE): slots [0, tl_comp_base) are
   // indexed by global record number (segment decode), compose appends after them
   TlItem* tl_items;

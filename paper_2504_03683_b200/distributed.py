@@ -195,6 +195,13 @@ class ShardedRun:
         eng = self.engine
         sg = self.stream_global if self.stream_global is not None else list(range(len(eng._streams)))
         status, failure, last = STATUS_OK, None, 0
+        if self.world == 1 and input_error is None:  # one rank: hg_run (the fused single-rank path)
+            self.rc = eng.run_raw(want)
+            self.global_last_ts = eng.local_last_ts()
+            k, tot, h2d, d2h, nl = eng.timing()
+            walk, chain, decode = eng.phase_timing()
+            return {"device_ms": tot, "phase1_ms": k, "walk_ms": walk, "chain_ms": chain, "decode_ms": decode,
+                    "h2d_bytes": h2d, "d2h_bytes": d2h, "launches": nl, "rc": self.rc}
         if input_error is not None:
             status, failure = STATUS_INPUT, ((0, input_error[0]), pack_exception(input_error[1]))
         else:
