@@ -122,9 +122,12 @@ class TimelineSink(Sink):
     name = "timeline"
     consumes = "intervals"
 
-    def __init__(self, out_path=None, device_index: int = 0):
+    def __init__(self, out_path=None, device_index: int = 0, objects: bool = True):
+        """objects=False: on_finish returns the JSON bytes instead of the parsed object list (the
+        reference returns the list, sinks.py:414-418; parsing GBs of JSON on the host is optional)."""
         self.out_path = out_path
         self.device_index = device_index
+        self.objects = objects
         self._bytes = b"[]"
 
     def on_message(self, msg):
@@ -141,7 +144,7 @@ class TimelineSink(Sink):
         if self.out_path is not None:
             with open(self.out_path, "wb") as fh:
                 fh.write(self._bytes)
-        return json.loads(self._bytes)
+        return json.loads(self._bytes) if self.objects else self._bytes
 
 
 class PrettyPrintSink(Sink):
