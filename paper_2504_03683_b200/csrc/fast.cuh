@@ -14,7 +14,7 @@
 // complete, so readiness is a popcount of the lane's request shift register.  HBM
 // is read once; every record access on the inline path is an LDS.
 //
-// Range starts are speculative (first offset with three consistent record
+// Range starts are speculative (first offset with eight consistent record
 // headers).  fast_verify_kernel then checks, per stream, that every range
 // starts where the previous one ended and that timestamps keep rising across
 // ranges; it turns the range summaries into compose_kernel's input (pending
