@@ -1,0 +1,92 @@
+"""The GPU engine against the oracle on seeded random traces (tests/random_traces.py) through
+run_pipeline with every sink the engine serves: tally, timeline, pretty-print and validation -- or the
+same exception and the orphans delivered before it -- on the default path, and the tally alone on
+the exact path (the single pass falls back there for corrupt seeds)."""
+
+import json
+
+import pytest
+
+from golden_util import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+RULES = json.loads((GOLDEN / "expected" / "validation_rules.json").read_text())
+
+
+@pytest.fixture(scope="module")
+def engine():
+    from paper_2504_03683_b200.engine import Engine
+
+    eng = Engine(device=0)
+    yield eng
+    eng.close()
+
+
+@pytest.mark.parametrize("seed", list(range(150)))
+def test_engine_equals_oracle_on_random_traces(engine, seed):
+    from random_traces import random_trace
+
+    from oracle import oracle
+    from paper_2504_03683_b200 import (PrettyPrintSink, TallySink, TimelineSink, ValidationRules, ValidationSink,
+                                       run_pipeline)
+    from paper_2504_03683_b200.pipeline import Sink, merge_same_identity
+
+    ze, raws = random_trace(seed)
+
+    class Src:
+        registry = ze
+
+        def raw_streams(self):
+            return raws
+
+        def stream_infos(self):
+            return [r.info for r in raws]
+
+    class Diag(Sink):
+        name = "diag"
+
+        def on_diagnostics(self, orphans):
+            self.orphans = orphans
+
+    rules = ValidationRules.from_dict(RULES)
+    mine = merge_same_identity(raws)
+    want = oracle.run(mine, ze, [r.info for r in raws], want_timeline=True)
+    diag = Diag()
+    sinks = [TallySink(), TimelineSink(), PrettyPrintSink(), ValidationSink(rules=rules), diag]
+    if want.error is not None:
+        with pytest.raises(Exception) as ei:
+            run_pipeline(Src(), sinks, engine=engine)
+        assert type(ei.value).__name__ == type(want.error).__name__ and str(ei.value) == str(want.error)
+        assert diag.orphans == want.orphans
+        return
+    res = run_pipeline(Src(), sinks, engine=engine)
+    assert res["tally"] == want.report and vars(res.stats) == want.stats and res.orphans == want.orphans
+    assert res["timeline"] == json.loads(want.timeline)
+    assert res["pretty"] == oracle.pretty(mine, ze)
+    findings = oracle.validate(mine, ze, rules, want.orphans)
+    assert [tuple(vars(f).values()) for f in res["validate"]] == [tuple(f) for f in findings]
+
+
+@pytest.mark.parametrize("seed", list(range(0, 150, 3)))
+@pytest.mark.parametrize("path", [0, 1])
+def test_tally_paths_on_random_traces(engine, seed, path):
+    from random_traces import random_trace
+
+    from oracle import oracle
+    from paper_2504_03683_b200.engine import OPT_PATH
+    from paper_2504_03683_b200.pipeline import merge_same_identity
+
+    ze, raws = random_trace(seed)
+    mine = merge_same_identity(raws)
+    want = oracle.run(mine, ze, [r.info for r in raws])
+    engine.set_option(OPT_PATH, path)
+    try:
+        got = engine.run(mine, ze, [r.info for r in raws])
+    finally:
+        engine.set_option(OPT_PATH, 0)
+    if want.error is not None:
+        assert got.error is not None and type(got.error) is type(want.error) and str(got.error) == str(want.error)
+        assert got.orphans == want.orphans
+        return
+    assert got.error is None and got.report == want.report and got.stats == want.stats and got.orphans == want.orphans
