@@ -195,6 +195,10 @@ int hg_run(hg_ctx* ctx, uint32_t want);
 int hg_run_local(hg_ctx* ctx, uint32_t want);
 int hg_local_last_ts(hg_ctx* ctx, uint64_t* last_ts, uint64_t* n_events);
 int hg_finish(hg_ctx* ctx, uint64_t global_last_ts);
+/* after hg_run_local: HG_FLAG_WIDE_DEVICE = some device span is beyond +-2^63 ns (its tally row keeps
+ * 128-bit extrema; the multi-rank merge carries 64-bit extrema and refuses such runs) */
+#define HG_FLAG_WIDE_DEVICE 1u
+int hg_local_flags(hg_ctx* ctx, uint32_t* flags);
 
 /* results */
 int hg_get_stats(hg_ctx* ctx, hg_stats* out);                       /* IntervalStats */

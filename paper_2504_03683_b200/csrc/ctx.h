@@ -108,7 +108,7 @@ struct hg_ctx {
   uint32_t epoch = 0;
   DBuf<SumEntry> d_pool, d_stack;
   uint64_t pool_cap = 0, stack_cap = 0;
-  DBuf<unsigned long long> d_host_acc, d_dev_acc;
+  DBuf<unsigned long long> d_host_acc, d_dev_acc, d_dev_wide;
   DBuf<unsigned long long> d_counters;  // misc counters, see below
   DBuf<hg_orphan> d_orphans;
   uint64_t orphan_cap = 0;
@@ -126,7 +126,7 @@ struct hg_ctx {
   bool have_results = false;
   uint32_t want = 0;
   std::vector<unsigned long long> counters;
-  std::vector<unsigned long long> host_acc, dev_acc;
+  std::vector<unsigned long long> host_acc, dev_acc, dev_wide;
   std::vector<uint8_t> arena;
   std::vector<uint64_t> name_off;
   std::vector<uint32_t> name_len;

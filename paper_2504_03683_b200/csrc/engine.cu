@@ -205,7 +205,8 @@ __global__ void __launch_bounds__(kComposeWarps * kWarp) compose_kernel(Params p
   }
 }
 
-__global__ void init_acc_kernel(unsigned long long* host_acc, uint32_t n_fn, unsigned long long* dev_acc, uint32_t n_dev) {
+__global__ void init_acc_kernel(unsigned long long* host_acc, uint32_t n_fn, unsigned long long* dev_acc, uint32_t n_dev,
+                                unsigned long long* dev_wide) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n_fn) {
     unsigned long long* a = host_acc + 6ull * i;
@@ -214,6 +215,8 @@ __global__ void init_acc_kernel(unsigned long long* host_acc, uint32_t n_fn, uns
   if (i < n_dev) {
     unsigned long long* a = dev_acc + 6ull * i;
     a[0] = a[1] = a[2] = a[3] = 0; a[4] = ~0ull; a[5] = 0;
+    unsigned long long* w = dev_wide + 6ull * i;  // lock, count, min = INT128_MAX, max = INT128_MIN
+    w[0] = w[1] = 0; w[2] = ~0ull; w[3] = 0x7FFFFFFFFFFFFFFFull; w[4] = 0; w[5] = 0x8000000000000000ull;
   }
 }
 
@@ -256,7 +259,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_data.release(); ctx->d_base.release(); ctx->d_size.release();
   ctx->d_tile_stream.release(); ctx->d_stream_tile0.release();
   ctx->d_state.release(); ctx->d_pool.release(); ctx->d_stack.release();
-  ctx->d_host_acc.release(); ctx->d_dev_acc.release(); ctx->d_counters.release();
+  ctx->d_host_acc.release(); ctx->d_dev_acc.release(); ctx->d_dev_wide.release(); ctx->d_counters.release();
   ctx->d_orphans.release(); ctx->d_errors.release(); ctx->d_stream_spans.release();
   ctx->d_keys.release(); ctx->d_vals.release(); ctx->d_name_len.release(); ctx->d_small.release();
   ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release();
@@ -655,6 +658,7 @@ static int ensure_scratch(hg_ctx* ctx, uint64_t n_records_bound) {
   CK(ctx->d_errors.ensure(ctx->error_cap));
   CK(ctx->d_host_acc.ensure(6ull * std::max<uint32_t>(ctx->n_fn, 1)));
   CK(ctx->d_dev_acc.ensure(6ull * ctx->row_cap));
+  CK(ctx->d_dev_wide.ensure(6ull * ctx->row_cap));
   CK(ctx->d_counters.ensure(C_NUM));
   CK(ctx->d_stream_spans.ensure(std::max<uint32_t>(ns, 1)));
   CK(ctx->d_keys.ensure(ctx->dict_mask + 1));
@@ -689,6 +693,7 @@ Params make_params(hg_ctx* ctx) {
   p.pool_cap = ctx->pool_cap;
   p.host_acc = ctx->d_host_acc.ptr;
   p.dev_acc = ctx->d_dev_acc.ptr;
+  p.dev_wide = ctx->d_dev_wide.ptr;
   p.wide_flag = reinterpret_cast<uint32_t*>(C + C_WIDE);
   p.names.keys = ctx->d_keys.ptr;
   p.names.vals = ctx->d_vals.ptr;
@@ -754,7 +759,7 @@ int init_run(hg_ctx* ctx) {
   CK(cudaMemsetAsync(ctx->d_vals.ptr, 0, (ctx->dict_mask + 1) * 4, ctx->stream));
   uint32_t nmax = std::max(ctx->n_fn, ctx->row_cap);
   init_acc_kernel<<<(nmax + 255) / 256, 256, 0, ctx->stream>>>(ctx->d_host_acc.ptr, ctx->n_fn, ctx->d_dev_acc.ptr,
-                                                                ctx->row_cap);
+                                                                ctx->row_cap, ctx->d_dev_wide.ptr);
   ctx->launches = 1;
   return HG_OK;
 }
@@ -851,8 +856,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   if (fast && ctx->counters[C_DEEP_USED] > 0) ctx->deep_inline = true;
   if ((uint32_t)ctx->counters[C_WATCHDOG])
     return fail(ctx, HG_ECUDA, "tile look-back watchdog fired (engine bug)");
-  if ((uint32_t)ctx->counters[C_WIDE])
-    return fail(ctx, HG_EUNSUPPORTED, "device span durations beyond the signed 64-bit range");
+
   ctx->local_last_ts = ctx->counters[C_LAST_TS];
   ctx->local_events = ctx->counters[C_STATS + ST_EVENTS];
   ctx->phase1_done = true;
@@ -907,6 +911,13 @@ static int launch_compose(hg_ctx* ctx, uint64_t global_last_ts, bool last_ts_on_
 
 static int collect_results(hg_ctx* ctx, uint64_t global_last_ts);
 
+int hg_local_flags(hg_ctx* ctx, uint32_t* flags) {
+  if (!ctx || !flags) return HG_EARG;
+  if (!ctx->phase1_done) return HG_ESTATE;
+  *flags = (uint32_t)ctx->counters[C_WIDE] ? HG_FLAG_WIDE_DEVICE : 0u;
+  return HG_OK;
+}
+
 int hg_finish(hg_ctx* ctx, uint64_t global_last_ts) {
   if (!ctx || !ctx->phase1_done) return HG_ESTATE;
   cudaSetDevice(ctx->cfg.device);
@@ -939,7 +950,7 @@ static int collect_results(hg_ctx* ctx, uint64_t global_last_ts) {
   const uint64_t n_orph = std::min<uint64_t>(C[C_N_ORPHANS], ctx->orphan_cap);
   const uint32_t n_err = (uint32_t)std::min<unsigned long long>((uint32_t)C[C_N_ERRORS], ctx->error_cap);
   struct Part { void* dst; const void* src; size_t bytes; size_t at; };
-  Part parts[8];
+  Part parts[9];
   int np = 0;
   size_t total = 0;
   auto part = [&](void* dst, const void* src, size_t bytes) {
@@ -955,6 +966,8 @@ static int collect_results(hg_ctx* ctx, uint64_t global_last_ts) {
   ctx->orphans.resize(n_orph);
   ctx->errors.resize(n_err);
   ctx->stream_spans.resize(ns);
+  ctx->dev_wide.assign((uint32_t)ctx->counters[C_WIDE] ? 6ull * ctx->n_dev_rows : 0, 0);
+  part(ctx->dev_wide.data(), ctx->d_dev_wide.ptr, ctx->dev_wide.size() * 8);
   part(ctx->host_acc.data(), ctx->d_host_acc.ptr, ctx->host_acc.size() * 8);
   part(ctx->dev_acc.data(), ctx->d_dev_acc.ptr, ctx->dev_acc.size() * 8);
   part(ctx->name_off.data(), ctx->d_name_off.ptr, ctx->n_dev_rows * 8ull);
@@ -1037,7 +1050,7 @@ static int run_fused(hg_ctx* ctx, uint32_t want, bool& done) {
   if (rc) return rc;
   ctx->h2d_bytes = h2d;
   const unsigned long long* C = ctx->counters.data();
-  const bool clean = !(uint32_t)C[C_ANOM] && !(uint32_t)C[C_OVERFLOW] && !(uint32_t)C[C_WIDE] &&
+  const bool clean = !(uint32_t)C[C_ANOM] && !(uint32_t)C[C_OVERFLOW] &&
                      !(uint32_t)C[C_WATCHDOG] && !(uint32_t)C[C_N_ERRORS] && 2 * C[C_POOL_USED] <= ctx->pool_cap &&
                      C[C_N_ORPHANS] <= ctx->orphan_cap && C[C_DEEP_USED] <= ctx->deep_cap &&
                      C[C_STACK_USED] <= ctx->stack_cap;
@@ -1102,6 +1115,15 @@ int hg_get_tally(hg_ctx* ctx, hg_tally_row* rows, uint64_t cap, uint64_t* n_rows
       int64_t mn = (int64_t)(a[4] ^ 0x8000000000000000ull), mx = (int64_t)(a[5] ^ 0x8000000000000000ull);
       r.min_lo = (uint64_t)mn; r.min_hi = mn < 0 ? -1 : 0;
       r.max_lo = (uint64_t)mx; r.max_hi = mx < 0 ? -1 : 0;
+      if (!ctx->merged && !ctx->dev_wide.empty() && ctx->dev_wide[6ull * d + 1]) {  // spans beyond +-2^63 ns
+        const unsigned long long* w = &ctx->dev_wide[6ull * d];
+        const bool narrow = a[0] > w[1];  // some span of the row fit 64 bits
+        const __int128 wmn = ((__int128)(int64_t)w[3] << 64) | w[2], wmx = ((__int128)(int64_t)w[5] << 64) | w[4];
+        const __int128 nmn = mn, nmx = mx;
+        const __int128 fmn = narrow && nmn < wmn ? nmn : wmn, fmx = narrow && nmx > wmx ? nmx : wmx;
+        r.min_lo = (uint64_t)fmn; r.min_hi = (int64_t)(fmn >> 64);
+        r.max_lo = (uint64_t)fmx; r.max_hi = (int64_t)(fmx >> 64);
+      }
     }
     n++;
   }

@@ -66,6 +66,7 @@ struct Params {
   uint64_t pool_cap;
   unsigned long long* host_acc;   // n_fn x 6: count, err, sum_lo, sum_hi, min, max
   unsigned long long* dev_acc;    // row_cap x 6: count, err, sum_lo, sum_hi, min_b, max_b
+  unsigned long long* dev_wide;   // row_cap x 6: lock, count, min lo/hi, max lo/hi of spans beyond +-2^63 ns
   uint32_t* wide_flag;
   NameDict names;
   hg_orphan* orphans;
@@ -213,6 +214,27 @@ struct HostFold {
 };
 
 // device rows: CTA cache keyed by the global row id, global atomics on a miss
+// signed 128-bit a < b
+__device__ __forceinline__ bool lt128(int64_t ahi, uint64_t alo, int64_t bhi, uint64_t blo) {
+  return ahi < bhi || (ahi == bhi && alo < blo);
+}
+
+// a device span beyond +-2^63 ns (Python ints have no width, sinks.py:123-132): 128-bit extrema of
+// the row under a per-row lock (rare: negative or huge device_end - device_start)
+static __device__ __noinline__ void fold_device_wide(const Params& p, uint32_t row, uint64_t d_lo, int64_t d_hi) {
+  unsigned long long* w = p.dev_wide + 6ull * row;
+  while (atomicCAS(&w[0], 0ull, 1ull) != 0ull) {
+  }
+  __threadfence();
+  volatile unsigned long long* v = w;
+  v[1] = v[1] + 1;
+  if (lt128(d_hi, d_lo, (int64_t)v[3], v[2])) { v[2] = d_lo; v[3] = (uint64_t)d_hi; }
+  if (lt128((int64_t)v[5], v[4], d_hi, d_lo)) { v[4] = d_lo; v[5] = (uint64_t)d_hi; }
+  __threadfence();
+  atomicExch(&w[0], 0ull);
+  atomicExch(p.wide_flag, 1u);  // the multi-rank merge carries 64-bit extrema only
+}
+
 static __device__ __noinline__ void fold_device_global(const Params& p, uint32_t row, uint64_t d_lo, int64_t d_hi) {
   unsigned long long* a = p.dev_acc + 6ull * row;
   atomicAdd(&a[0], 1ull);
@@ -221,7 +243,7 @@ static __device__ __noinline__ void fold_device_global(const Params& p, uint32_t
     atomicMin(&a[4], bias64((int64_t)d_lo));
     atomicMax(&a[5], bias64((int64_t)d_lo));
   } else {
-    atomicExch(p.wide_flag, 1u);
+    fold_device_wide(p, row, d_lo, d_hi);
   }
 }
 

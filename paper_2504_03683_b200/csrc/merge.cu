@@ -76,6 +76,8 @@ int hg_merge_export(hg_ctx* ctx, void* dst, const uint32_t* dev_map, uint32_t n_
   if (!ctx || !dst) return HG_EARG;
   if (!ctx->have_results) return fail(ctx, HG_ESTATE, "hg_merge_export before hg_finish");
   if (n_dev_local != ctx->n_dev_rows) return fail(ctx, HG_EARG, "dev_map must cover every local device row");
+  if ((uint32_t)ctx->counters[C_WIDE])
+    return fail(ctx, HG_EUNSUPPORTED, "multi-rank merge of device spans beyond the signed 64-bit range");
   const uint32_t ns = (uint32_t)ctx->streams.size();
   for (uint32_t d = 0; d < n_dev_local; d++)
     if (dev_map[d] >= n_dev_global) return fail(ctx, HG_EARG, "dev_map entry out of range");

@@ -208,6 +208,10 @@ class ShardedRun:
             try:
                 eng.run_local(want)
                 last = eng.local_last_ts()
+                if eng.local_flags() & 1:
+                    from .errors import UnsupportedTraceError
+
+                    raise UnsupportedTraceError("multi-rank merge of device spans beyond the signed 64-bit range")
             except Exception as e:  # noqa: BLE001  (an engine failure: reported to every rank)
                 status, failure = STATUS_ENGINE, ((2, self.rank), pack_exception(e))
         g, gstatus = last, status

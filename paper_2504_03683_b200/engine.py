@@ -279,6 +279,12 @@ class Engine:
         """hg_run_local: phase 1 over this context's streams; raises on an engine failure."""
         self._check(self._L.hg_run_local(self._ctx, want), "hg_run_local")
 
+    def local_flags(self) -> int:
+        """hg_local_flags after run_local: 1 = a device span beyond +-2^63 ns."""
+        f = C.c_uint32()
+        self._check(self._L.hg_local_flags(self._ctx, C.byref(f)), "hg_local_flags")
+        return f.value
+
     def local_last_ts(self) -> int:
         last = C.c_uint64()
         self._check(self._L.hg_local_last_ts(self._ctx, C.byref(last), None), "hg_local_last_ts")

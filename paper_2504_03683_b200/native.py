@@ -116,6 +116,7 @@ def lib():
         "hg_set_validation_rules": ([vp, vp, u32], C.c_int),
         "hg_get_findings": ([vp, vp, u64, vp], C.c_int),
         "hg_tl_export": ([vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "hg_local_flags": ([vp, vp], C.c_int),
         "hg_tl_import": ([vp, vp, u64, vp, vp, u32, vp, vp, vp, vp, u32, vp, u64, u64], C.c_int),
     }
     for name, (args, res) in sig.items():
@@ -137,5 +138,5 @@ EXPORTED = (
     "hg_set_flush_order", "hg_merge_size", "hg_merge_export", "hg_merge_import", "hg_add_stream_device",
     "hg_add_stream_file", "hg_ingest_stats", "hg_set_schema_names", "hg_events_size", "hg_get_events",
     "hg_get_event_order", "hg_events_ms", "hg_set_validation_rules", "hg_get_findings", "hg_tl_export",
-    "hg_tl_import",
+    "hg_tl_import", "hg_local_flags",
 )

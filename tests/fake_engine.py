@@ -85,6 +85,9 @@ class FakeEngine:
     def local_last_ts(self):
         return self._last
 
+    def local_flags(self):
+        return 0
+
     def finish(self, g):
         """Rows, names, stats and span identities with truncation at the global last ts g."""
         from oracle import oracle
