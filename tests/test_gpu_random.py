@@ -90,3 +90,28 @@ def test_tally_paths_on_random_traces(engine, seed, path):
         assert got.orphans == want.orphans
         return
     assert got.error is None and got.report == want.report and got.stats == want.stats and got.orphans == want.orphans
+
+
+@pytest.mark.parametrize("seed", list(range(1, 150, 5)))
+@pytest.mark.parametrize("range_bytes", [32, 112, 600])
+def test_single_pass_small_ranges_on_random_traces(engine, seed, range_bytes):
+    """Many speculative ranges per stream (escaped names, wide values, orphans, mismatches, unclosed calls
+    crossing range cuts): the single pass either vouches for the exact result or falls back."""
+    from random_traces import random_trace
+
+    from oracle import oracle
+    from paper_2504_03683_b200.engine import OPT_RANGE_BYTES
+    from paper_2504_03683_b200.pipeline import merge_same_identity
+
+    ze, raws = random_trace(seed, corrupt=False)
+    mine = merge_same_identity(raws)
+    want = oracle.run(mine, ze, [r.info for r in raws])
+    engine.set_option(OPT_RANGE_BYTES, range_bytes)
+    try:
+        got = engine.run(mine, ze, [r.info for r in raws])
+    finally:
+        engine.set_option(OPT_RANGE_BYTES, 0)
+    if want.error is not None:
+        assert got.error is not None and str(got.error) == str(want.error)
+        return
+    assert got.error is None and got.report == want.report and got.stats == want.stats and got.orphans == want.orphans
