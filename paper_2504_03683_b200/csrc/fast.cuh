@@ -29,12 +29,21 @@
 namespace hg {
 
 constexpr uint32_t kRChunk = 32;                    // bytes per ring slot (one sector)
-constexpr uint32_t kRSlots = 8;                     // slots per lane
+#ifndef HG_RING_SLOTS
+#define HG_RING_SLOTS 8
+#endif
+#ifndef HG_RINLINE
+#define HG_RINLINE 128
+#endif
+#ifndef HG_FAST_WARPS
+#define HG_FAST_WARPS 12
+#endif
+constexpr uint32_t kRSlots = HG_RING_SLOTS;         // slots per lane
 constexpr uint32_t kRRing = kRChunk * kRSlots;      // 256-byte ring
 constexpr uint32_t kRWordMask = kRRing / 4 - 1;
 constexpr uint32_t kRMirror = 0;                    // (no mirror: header words are read with wrapped indices)
 constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: header + first field need no wrap
-constexpr uint32_t kRInline = 128;                  // records up to this long are decoded from the ring
+constexpr uint32_t kRInline = HG_RINLINE;           // records up to this long are decoded from the ring
 constexpr int kRLag = 2;                            // iterations before a fill group is waited for
 constexpr int kRLS = 4;                             // open entries per lane in shared memory
 constexpr int kRLP = 4;                             // pending exits per lane in shared memory
@@ -510,7 +519,7 @@ static __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, c
   return K;
 }
 
-constexpr int kRMaxThreads = 12 * kWarp;
+constexpr int kRMaxThreads = HG_FAST_WARPS * kWarp;
 
 // strict UTF-8 of the one string field of inline records (tracefile.py:165), one per lane, from HBM
 static __device__ __noinline__ void r_drain_str(const Params& p, const uint64_t* q_off, const uint32_t* q_s, uint32_t n) {

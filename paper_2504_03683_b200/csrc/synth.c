@@ -249,3 +249,17 @@ int synth_sampler(const uint32_t* tel_sids, uint64_t device, uint64_t start, uin
   *out_events = k.events;
   return k.overflow ? -2 : 0;
 }
+
+/* timestamp of the last record of an encoded stream (header walk), 0 if none */
+uint64_t synth_last_ts(const uint8_t* data, uint64_t len) {
+  uint64_t off = 16, last = 0;
+  while (off + 16 <= len) {
+    uint64_t ts;
+    uint32_t plen;
+    memcpy(&ts, data + off + 4, 8);
+    memcpy(&plen, data + off + 12, 4);
+    last = ts;
+    off += 16 + (uint64_t)plen;
+  }
+  return last;
+}

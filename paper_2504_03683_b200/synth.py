@@ -79,6 +79,8 @@ def _L():
         L.synth_sampler.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p]
         L.synth_sampler.restype = C.c_int
+        L.synth_last_ts.argtypes = [C.c_char_p, C.c_uint64]
+        L.synth_last_ts.restype = C.c_uint64
         _lib = L
     return _lib
 
@@ -156,7 +158,17 @@ DEFAULTS = dict(max_depth=4, gap_lo=1, gap_hi=600, ts0_hi=1000, push_p=0.5, err_
                 dev_off_hi=10_000, dev_lo=1_000, dev_hi=100_000)
 
 
-def generate_stream(wl: Workload, spec: StreamSpec, flat=None, until_ns=None) -> bytes:
+def _buffer(cap: int):
+    """An uninitialised byte buffer for the C generator (zero-filling GBs of ctypes arrays cost more than
+    generating the records) and its address."""
+    import numpy as np
+
+    a = np.empty(cap, dtype=np.uint8)
+    return a, a.ctypes.data
+
+
+def generate_stream(wl: Workload, spec: StreamSpec, flat=None, until_ns=None, counts=None) -> bytes:
+    """One stream's file bytes; ``counts`` (a list) receives its record count."""
     L = _L()
     flat = flat or flatten_registry(wl.registry)
     max_id = max(s.id for s in flat.schemas)
@@ -168,12 +180,14 @@ def generate_stream(wl: Workload, spec: StreamSpec, flat=None, until_ns=None) ->
                                  for k, _ in TELEMETRY_COUNTERS])
         n_inst = (until_ns or 0) // wl.sampler_period_ns + 1
         cap = 16 + n_inst * 9 * 32
-        buf = (C.c_uint8 * cap)()
+        arr, buf = _buffer(cap)
         ln, ev = C.c_uint64(), C.c_uint64()
         rc = L.synth_sampler(sids, 0, 0, wl.sampler_period_ns, until_ns or 0, spec.seed, buf, cap,
                              C.byref(ln), C.byref(ev))
         assert rc == 0
-        return C.string_at(buf, ln.value)
+        if counts is not None:
+            counts.append(ev.value)
+        return arr[: ln.value].tobytes()
     p = dict(DEFAULTS)
     p.update(wl.params)
     fns = functions_of(wl.registry, wl.layers)
@@ -184,46 +198,44 @@ def generate_stream(wl: Workload, spec: StreamSpec, flat=None, until_ns=None) ->
     P = SynthParams(seed=spec.seed, n_events=spec.n_events, meta_sid=meta[0] if meta else -1,
                     **{k: v for k, v in p.items()})
     cap = 16 + spec.n_events * 96 + 4096
-    buf = (C.c_uint8 * cap)()
+    arr, buf = _buffer(cap)
     ln, ev = C.c_uint64(), C.c_uint64()
     rc = L.synth_stream(C.byref(P), by_id, max_id + 1, flat.kinds, farr, len(fns), name_arr, len(names),
                         buf, cap, C.byref(ln), C.byref(ev))
     if rc != 0:
         raise RuntimeError(f"synth_stream failed ({rc})")
-    return C.string_at(buf, ln.value)
+    if counts is not None:
+        counts.append(ev.value)
+    return arr[: ln.value].tobytes()
 
 
 def last_timestamp(data: bytes) -> int:
-    """ts of the final record (streams are ts-monotone)."""
-    import struct
-
-    off, last = 16, 0
-    # walk record headers only
-    while off + 16 <= len(data):
-        _, ts, plen = struct.unpack_from("<IQI", data, off)
-        last = ts
-        off += 16 + plen
-    return last
+    """ts of the final record (streams are ts-monotone), by a header walk in C."""
+    return _L().synth_last_ts(data, len(data))
 
 
 def generate(wl: Workload, threads: int | None = None) -> list:
     """All streams of a workload as RawStream objects in (hostname, pid, tid) order."""
     flat = flatten_registry(wl.registry)
     calls = [s for s in wl.streams if s.kind == "calls"]
+    def one(s, until=None):
+        c = []
+        d = generate_stream(wl, s, flat, until_ns=until, counts=c)
+        return d, c[0]
+
     with ThreadPoolExecutor(max_workers=threads or os.cpu_count() or 4) as ex:
-        datas = list(ex.map(lambda s: generate_stream(wl, s, flat), calls))
+        datas = list(ex.map(one, calls))
     out = {}
-    for s, d in zip(calls, datas):
-        out[(s.hostname, s.pid, s.tid)] = (s, d)
+    for s, dn in zip(calls, datas):
+        out[(s.hostname, s.pid, s.tid)] = (s, dn)
     samplers = [s for s in wl.streams if s.kind == "sampler"]
     if samplers:
-        until = max(last_timestamp(d) for d in datas) if datas else 0
+        until = max(last_timestamp(d) for d, _ in datas) if datas else 0
         for s in samplers:
-            out[(s.hostname, s.pid, s.tid)] = (s, generate_stream(wl, s, flat, until_ns=until))
+            out[(s.hostname, s.pid, s.tid)] = (s, one(s, until))
     raws = []
     for key in sorted(out):
-        s, d = out[key]
-        n = count_records(d)
+        s, (d, n) = out[key]
         name = s.file or f"stream_{s.pid}_{s.tid}.bin"
         raws.append(RawStream(s.hostname, s.pid, s.tid, name, d, StreamInfo(s.hostname, s.pid, s.tid, n, 0)))
     return raws
