@@ -413,8 +413,8 @@ def run_ours(args):
         "e2e": {"value": tot_events / e2e, "unit": "events/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h,
                 "path": "Engine.set_streams_pinned + ShardedRun.step + ShardedRun.result (hg_add_stream host "
-                        "pointers into pinned memory, hg_run_local/hg_finish, merge), wall clock per step, max "
-                        "over ranks"},
+                        "pointers into pinned memory; hg_run at N=1, hg_run_local/hg_finish + merge at N>1), wall "
+                        "clock per step, max over ranks"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
