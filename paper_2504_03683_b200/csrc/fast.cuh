@@ -155,7 +155,10 @@ struct RLane {
 // non-decreasing timestamps (or a shorter one that ends exactly at the stream end).
 // A wrong guess is caught by fast_verify_kernel and costs a whole exact pass, so the
 // single pass demands a longer chain than the segment walk (seg_walk_kernel: three).
-constexpr int kScanDepth = 8;
+#ifndef HG_SCAN_DEPTH
+#define HG_SCAN_DEPTH 8
+#endif
+constexpr int kScanDepth = HG_SCAN_DEPTH;
 
 static __device__ __noinline__ uint64_t r_scan(const Params& p, const uint8_t* g, uint64_t size, uint64_t t0, uint64_t t1) {
   for (uint64_t o = t0; o < t1; o++) {
@@ -722,7 +725,10 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     asm volatile("cp.async.wait_group %0;" ::"n"(kRLag) : "memory");
     __syncwarp();
     // ---- every chunk requested before the last kRLag iterations is in the ring; first the header
-    const uint32_t cr = R.ci - __popc(R.recent & kPend);
+    // (right after a range switch ci restarts at 0 while the old range's last fills may still be
+    // pending: nothing of the new range is in the ring yet -- no wrap-around to "all ready")
+    const uint32_t pend = __popc(R.recent & kPend);
+    const uint32_t cr = R.ci > pend ? R.ci - pend : 0u;
     const bool ready = act && min((R.o + 15u) / kRChunk, R.clast) < cr;
     const uint32_t pos = R.o & (kRRing - 1);
     const uint32_t wb0 = pos >> 2;
