@@ -177,12 +177,12 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
   while (th_size < 2 * n_dev && th_size < (1u << 30)) th_size <<= 1;
   CK(ctx->d_tl_proc_first.ensure(n_proc));
   CK(ctx->d_tl_th_state.ensure(th_size));
-  CK(ctx->d_tl_th_first.ensure(th_size));
+  CK(ctx->d_tl_th_first.ensure(kThDirect + th_size));
   CK(ctx->d_tl_th_hi.ensure(th_size));
   CK(ctx->d_tl_th_lo.ensure(th_size));
   CK(cudaMemsetAsync(ctx->d_tl_proc_first.ptr, 0xFF, n_proc * 4, st));
   CK(cudaMemsetAsync(ctx->d_tl_th_state.ptr, 0, (size_t)th_size * 4, st));
-  CK(cudaMemsetAsync(ctx->d_tl_th_first.ptr, 0xFF, (size_t)th_size * 4, st));
+  CK(cudaMemsetAsync(ctx->d_tl_th_first.ptr, 0xFF, (size_t)(kThDirect + th_size) * 4, st));
   CK(ctx->d_tl_lens.ensure(std::max<uint32_t>(n, 1)));
   CK(ctx->d_tl_offs.ensure(std::max<uint32_t>(n, 1)));
   TlTables T{};
@@ -214,10 +214,10 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
   T.offs = ctx->d_tl_offs.ptr;
   uint64_t total = 0;
   if (n) {
-    const uint32_t g = std::min<uint32_t>((n + 255) / 256, (uint32_t)ctx->sm_count * 16);
-    tl_len_kernel<<<g, 256, 0, st>>>(T);
-    tl_meta_len_kernel<<<std::min<uint32_t>((n_proc + th_size + 255) / 256, (uint32_t)ctx->sm_count * 8), 256, 0, st>>>(
-        T, n_proc, th_size);
+    const uint32_t g = std::min<uint32_t>((n + kTlTile - 1) / kTlTile, (uint32_t)ctx->sm_count * HG_TL_LEN_MINB * 2);
+    tl_len_kernel<<<g, kTlTile, 0, st>>>(T);
+    tl_meta_len_kernel<<<std::min<uint32_t>((n_proc + kThDirect + th_size + 255) / 256, (uint32_t)ctx->sm_count * 8), 256,
+                         0, st>>>(T, n_proc, kThDirect + th_size);
     tl_scan(ctx, T.lens, n, T.offs, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
     CK(cudaGetLastError());
     ctx->launches += 2;
@@ -235,8 +235,10 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
   if (n) {
     CK(cudaMemcpyAsync(T.out, open_close, 1, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(T.out + 1 + total, open_close + 1, 2, cudaMemcpyHostToDevice, st));
-    const uint32_t g = std::min<uint32_t>((n + kTlWarps * 32 - 1) / (kTlWarps * 32), (uint32_t)ctx->sm_count * 8);
-    tl_write_kernel<<<g, kTlWarps * 32, 0, st>>>(T);
+    const uint32_t g = std::min<uint32_t>((n + kTlTile - 1) / kTlTile, (uint32_t)ctx->sm_count * HG_TL_WRITE_MINB);
+    const size_t smem = tl_write_smem();
+    CK(cudaFuncSetAttribute(tl_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    tl_write_kernel<<<g, kTlTile, smem, st>>>(T);
     CK(cudaGetLastError());
     ctx->launches++;
   } else {

@@ -14,8 +14,8 @@
 //        emits at first sight (sinks.py:351-359)
 //   tl_meta_len_kernel   the lengths of the items that carry metadata objects
 //   tl_scan*          exclusive scan -> byte offsets
-//   tl_write_kernel   formats each warp's 32 consecutive items into a shared
-//        staging buffer, then stores it with aligned 16-byte writes
+//   tl_write_kernel   formats each CTA's kTlTile consecutive items (grouped by kind)
+//        into a shared staging buffer, then stores it with aligned 16-byte writes
 //
 // The bytes equal json.dump(objects, fh, indent=1) (sinks.py:414-418): floats
 // via numfmt.cuh (CPython repr), strings JSON-escaped with ensure_ascii.
@@ -281,8 +281,19 @@ __device__ __forceinline__ I128 dev_tid(I128 tile, I128 engine) {
   return add128(t2, engine);
 }
 
-// thread_name meta table (keyed by tid)
-static __device__ __noinline__ int th_slot(const TlTables& T, I128 tid, bool insert) {
+// thread_name meta table (keyed by tid): th_first[tid] for tid < kThDirect, else th_first[kThDirect +
+// slot of an open-addressing table]
+constexpr uint32_t kThDirect = 1024;
+
+static __device__ __noinline__ int th_slot_hash(const TlTables& T, I128 tid, bool insert);
+
+__device__ __forceinline__ int th_slot(const TlTables& T, I128 tid, bool insert) {
+  if (tid.hi == 0 && tid.lo < kThDirect) return (int)tid.lo;
+  const int h = th_slot_hash(T, tid, insert);
+  return h < 0 ? h : (int)kThDirect + h;
+}
+
+static __device__ __noinline__ int th_slot_hash(const TlTables& T, I128 tid, bool insert) {
   uint64_t h = (tid.lo * 0x9E3779B97F4A7C15ull) ^ ((uint64_t)tid.hi * 0xC2B2AE3D27D4EB4Full);
   h ^= h >> 29;
   for (uint32_t probe = 0, slot = (uint32_t)h & T.th_mask; probe <= T.th_mask; probe++, slot = (slot + 1) & T.th_mask) {
@@ -647,9 +658,10 @@ __device__ __forceinline__ void meta_obj(W& w, bool first, bool thread, const ch
 // kLen: the length pass -- the item's own text only, while recording the first occurrences of
 // its metadata keys (TimelineSink._meta, sinks.py:351-359); tl_meta_len_kernel then measures
 // the items that carry metadata again, with it
+// meta: the item opens a metadata key (flagged by tl_meta_len_kernel; the write pass looks the
+// keys up only then)
 template <class W, bool kLen = false>
-__device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
-  const TlItem it = T.items[T.order[i]];
+__device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, const TlItem& it, W& w, bool meta = true) {
   const uint32_t kind = it.kind & 3u;
   bool first = i == 0;
   if (kind == TL_HOST) {
@@ -657,7 +669,7 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
     const uint64_t* so = T.sstr_off + 3ull * s;
     if (kLen) {
       first_min(&T.proc_first[T.stream_proc[s]], i);
-    } else if (T.proc_first[T.stream_proc[s]] == i) {
+    } else if (meta && T.proc_first[T.stream_proc[s]] == i) {
       meta_obj(w, first, false, T.sstr + so[0], (uint32_t)(so[1] - so[0]), I128{0, 0}, T.sstr + so[2],
                (uint32_t)(so[3] - so[2]), nullptr, 0);
       first = false;
@@ -702,11 +714,11 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
       first_min(&T.proc_first[T.dev_proc], i);
       const int slot = th_slot(T, tid, true);
       if (slot >= 0) first_min(&T.th_first[slot], i);
-    } else if (T.proc_first[T.dev_proc] == i) {
+    } else if (meta && T.proc_first[T.dev_proc] == i) {
       meta_obj(w, first, false, T.dev_pid, T.dev_pid_len, I128{0, 0}, "\"Device 0\"", 10, nullptr, 0);
       first = false;
     }
-    const int slot = kLen ? -1 : th_slot(T, tid, false);
+    const int slot = (kLen || !meta) ? -1 : th_slot(T, tid, false);
     if (slot >= 0 && T.th_first[slot] == i) {
       // _DEVICE_TRACK_NAMES (sinks.py:323-328)
       const bool known = tile.hi == 0 && engine.hi == 0 && tile.lo <= 1 && engine.lo <= 1;
@@ -769,21 +781,77 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, W& w) {
   w.lit("\n  }\n }");
 }
 
+// Items are formatted in CTA tiles of kTlTile consecutive sorted positions, gathered once into
+// shared memory and handed to the threads grouped by kind (host spans, device spans, samples), so
+// that a warp runs one kind's formatting code instead of all three.
+#ifndef HG_TL_TILE
+#define HG_TL_TILE 128  // small tiles: the CTA barrier waits for its slowest item, more CTAs per SM hide that
+#endif
+constexpr int kTlTile = HG_TL_TILE;
+constexpr uint32_t kTlMeta = 1u << 31;  // lens[i] flag: the item carries metadata objects
+
+struct TlTileSmem {
+  TlItem it[kTlTile];
+  uint16_t list[kTlTile];   // tile positions grouped by kind
+  uint32_t cur[4];
+};
+
+// gathers the tile's items and groups them by kind; returns this thread's tile position (or ~0)
+__device__ __forceinline__ uint32_t tl_tile_group(const TlTables& T, uint64_t i0, TlTileSmem& S) {
+  const uint32_t t = threadIdx.x;
+  const uint64_t i = i0 + t;
+  const bool on = i < T.n;
+  uint32_t kind = 3;
+  if (on) {
+    const TlItem it = T.items[T.order[i]];
+    S.it[t] = it;
+    kind = it.kind & 3u;
+  }
+  if (t < 4) S.cur[t] = 0;
+  __syncthreads();
+  uint32_t pos = 0;
+  const uint32_t lane = t & 31;
+  #pragma unroll
+  for (uint32_t k = 0; k < 3; k++) {
+    const uint32_t m = __ballot_sync(0xffffffffu, kind == k);
+    if (m) {
+      const uint32_t leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(&S.cur[k], (uint32_t)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (kind == k) pos = base + __popc(m & ((1u << lane) - 1u));
+    }
+  }
+  __syncthreads();
+  if (on) {
+    const uint32_t n0 = S.cur[0], n1 = S.cur[1];
+    S.list[kind == 0 ? pos : kind == 1 ? n0 + pos : n0 + n1 + pos] = (uint16_t)t;
+  }
+  const uint32_t cnt = S.cur[0] + S.cur[1] + S.cur[2];
+  __syncthreads();
+  return t < cnt ? S.list[t] : 0xffffffffu;
+}
+
 #ifndef HG_TL_LEN_MINB
-#define HG_TL_LEN_MINB 3  // 3 CTAs per SM (80 registers): 3.85 vs 5.2 ms for the timeline of C5 x0.1
+#define HG_TL_LEN_MINB (768 / HG_TL_TILE)  // 80 registers
 #endif
 #ifdef HG_TL_KERNELS
-__global__ void __launch_bounds__(256, HG_TL_LEN_MINB) tl_len_kernel(TlTables T) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += (uint64_t)gridDim.x * blockDim.x) {
-    TC w{0};
-    tl_format<TC, true>(T, (uint32_t)i, w);
-    T.lens[i] = (uint32_t)w.n;
+__global__ void __launch_bounds__(kTlTile, HG_TL_LEN_MINB) tl_len_kernel(TlTables T) {
+  __shared__ TlTileSmem S;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kTlTile; i0 < T.n; i0 += (uint64_t)gridDim.x * kTlTile) {
+    const uint32_t j = tl_tile_group(T, i0, S);
+    if (j != 0xffffffffu) {
+      TC w{0};
+      tl_format<TC, true>(T, (uint32_t)(i0 + j), S.it[j], w);
+      T.lens[i0 + j] = (uint32_t)w.n;
+    }
+    __syncthreads();
   }
 }
 #endif  // HG_TL_KERNELS
 
-// the items that open a metadata key: their length with the metadata objects (two keys may
-// share an item: both threads store the same length)
+// the items that open a metadata key: their length with the metadata objects, flagged for the
+// write pass (two keys may share an item: both threads store the same value)
 #ifdef HG_TL_KERNELS
 __global__ void tl_meta_len_kernel(TlTables T, uint32_t n_proc, uint32_t th_size) {
   for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (uint64_t)n_proc + th_size;
@@ -791,8 +859,8 @@ __global__ void tl_meta_len_kernel(TlTables T, uint32_t n_proc, uint32_t th_size
     const uint32_t f = e < n_proc ? T.proc_first[e] : T.th_first[e - n_proc];
     if (f >= T.n) continue;
     TC w{0};
-    tl_format<TC, false>(T, f, w);
-    T.lens[f] = (uint32_t)w.n;
+    tl_format<TC, false>(T, f, T.items[T.order[f]], w);
+    T.lens[f] = (uint32_t)w.n | kTlMeta;
   }
 }
 #endif  // HG_TL_KERNELS
@@ -831,7 +899,7 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t* total)
 __global__ void __launch_bounds__(kScanBlock) tl_scan1_kernel(const uint32_t* lens, uint32_t n, uint64_t* bsum) {
   const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
   uint64_t tot;
-  block_excl_scan(i < n ? lens[i] : 0, &tot);
+  block_excl_scan(i < n ? lens[i] & ~kTlMeta : 0, &tot);
   if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
 }
 #endif  // HG_TL_KERNELS
@@ -855,54 +923,75 @@ __global__ void __launch_bounds__(kScanBlock) tl_scan2_kernel(uint64_t* bsum, ui
 __global__ void __launch_bounds__(kScanBlock) tl_scan3_kernel(const uint32_t* lens, uint32_t n, const uint64_t* bsum,
                                                               uint64_t* offs) {
   const uint64_t i = (uint64_t)blockIdx.x * kScanBlock + threadIdx.x;
-  const uint64_t ex = block_excl_scan(i < n ? lens[i] : 0, nullptr);
+  const uint64_t ex = block_excl_scan(i < n ? lens[i] & ~kTlMeta : 0, nullptr);
   if (i < n) offs[i] = bsum[blockIdx.x] + ex;
 }
 #endif  // HG_TL_KERNELS
 
 // ---------------------------------------------------------------------------
-// writer: a warp formats 32 consecutive items into shared memory, then stores
-// the contiguous range with aligned 16-byte writes
+// writer: a CTA formats a tile of items (grouped by kind) into a shared staging buffer at their
+// offsets, then stores the tile's contiguous byte range with aligned 16-byte writes
 
-constexpr int kTlWarps = 8;
-constexpr int kTlStage = 5120;
+constexpr uint32_t kTlStage = kTlTile * 224;  // objects average ~160 bytes; larger tiles are written directly
+
+struct TlWriteSmem {
+  TlTileSmem g;
+  uint32_t rel[kTlTile];    // offset of the item's text in the staging buffer
+  uint64_t o0, oend;
+  __align__(16) char stage[kTlStage + 16];
+};
+
+inline size_t tl_write_smem() { return sizeof(TlWriteSmem); }
 
 #ifndef HG_TL_WRITE_MINB
-#define HG_TL_WRITE_MINB 3  // (with the length pass at 3: both at 80 registers, the spills are cheaper than the latency)
+#define HG_TL_WRITE_MINB (768 / HG_TL_TILE)
 #endif
 #ifdef HG_TL_KERNELS
-__global__ void __launch_bounds__(kTlWarps * 32, HG_TL_WRITE_MINB) tl_write_kernel(TlTables T) {
-  __shared__ __align__(16) char stage[kTlWarps][kTlStage + 32];
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  char* buf = stage[warp];
-  for (uint64_t base = ((uint64_t)blockIdx.x * kTlWarps + warp) * 32; base < T.n;
-       base += (uint64_t)gridDim.x * kTlWarps * 32) {
-    const uint64_t i = base + lane;
-    const bool on = i < T.n;
-    const uint64_t off = on ? 1 + T.offs[i] : 0;
-    const uint64_t len = on ? T.lens[i] : 0;
-    const uint32_t last = (uint32_t)(min((uint64_t)T.n, base + 32) - 1 - base);
-    const uint64_t o0 = __shfl_sync(0xffffffffu, off, 0);
-    const uint64_t oend = __shfl_sync(0xffffffffu, off + len, last);
-    const uint64_t al = o0 & ~15ull;
-    const uint64_t total = oend - al;
-    if (total <= (uint64_t)kTlStage) {
-      if (on) {
-        TW w{buf + (off - al), 0};
-        tl_format(T, (uint32_t)i, w);
+__global__ void __launch_bounds__(kTlTile, HG_TL_WRITE_MINB) tl_write_kernel(TlTables T) {
+  extern __shared__ __align__(16) char tl_smem[];
+  TlWriteSmem& S = *reinterpret_cast<TlWriteSmem*>(tl_smem);
+  const uint32_t t = threadIdx.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kTlTile; i0 < T.n; i0 += (uint64_t)gridDim.x * kTlTile) {
+    const uint64_t i = i0 + t;
+    const uint64_t last = min((uint64_t)T.n, i0 + kTlTile) - 1;
+    uint64_t off = 0;
+    uint32_t len = 0;
+    if (i <= last) {
+      off = 1 + T.offs[i];
+      len = T.lens[i];
+      if (t == 0) S.o0 = off;
+      if (i == last) S.oend = off + (len & ~kTlMeta);
+    }
+    const uint32_t j = tl_tile_group(T, i0, S.g);  // (its barriers publish o0 / oend)
+    const uint64_t al = S.o0 & ~15ull, total = S.oend - al;
+    const bool staged = total <= (uint64_t)kTlStage;
+    if (i <= last) S.rel[t] = (uint32_t)(off - al) | (len & kTlMeta);
+    __syncthreads();
+    if (j != 0xffffffffu) {
+      const uint32_t r = S.rel[j];
+      const uint64_t gi = i0 + j;
+      if (staged) {
+        TW w{S.stage + (r & ~kTlMeta), 0};
+        tl_format(T, (uint32_t)gi, S.g.it[j], w, (r & kTlMeta) != 0);
+      } else {
+        TW w{T.out + al + (r & ~kTlMeta), 0};
+        tl_format(T, (uint32_t)gi, S.g.it[j], w, (r & kTlMeta) != 0);
       }
-      __syncwarp();
+    }
+    __syncthreads();
+    if (staged) {
+      const uint64_t o0 = S.o0, oend = S.oend;
       const uint32_t nch = (uint32_t)((total + 15) / 16);
-      for (uint32_t c = lane; c < nch; c += 32) {
+      for (uint32_t c = t; c < nch; c += kTlTile) {
         const uint64_t g0 = al + 16ull * c;
-        const uint64_t lo = g0 > o0 ? g0 : o0, hi = g0 + 16 < oend ? g0 + 16 : oend;
-        if (lo == g0 && hi == g0 + 16) *reinterpret_cast<uint4*>(T.out + g0) = *reinterpret_cast<const uint4*>(buf + 16 * c);
-        else for (uint64_t b = lo; b < hi; b++) T.out[b] = buf[b - al];
+        if (g0 >= o0 && g0 + 16 <= oend) {
+          *reinterpret_cast<uint4*>(T.out + g0) = *reinterpret_cast<const uint4*>(S.stage + 16 * c);
+        } else {
+          const uint64_t lo = g0 > o0 ? g0 : o0, hi = g0 + 16 < oend ? g0 + 16 : oend;
+          for (uint64_t b = lo; b < hi; b++) T.out[b] = S.stage[b - al];
+        }
       }
-      __syncwarp();
-    } else if (on) {
-      TW w{T.out + off, 0};
-      tl_format(T, (uint32_t)i, w);
+      __syncthreads();
     }
   }
 }
