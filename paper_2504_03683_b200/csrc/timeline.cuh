@@ -582,7 +582,9 @@ __global__ void tl_split_kernel(const ulonglong2* ki, const uint32_t* ro, uint32
 __global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2* ki, const uint32_t* ii, ulonglong2* ko,
                                                                 uint32_t* io, const uint32_t* ro, uint32_t R,
                                                                 const uint32_t* tile0, const uint32_t* split) {
-  __shared__ ulonglong2 sk[kSortTile];
+  // keys as two 8-byte arrays (the merge compares the high words first: half the shared-memory
+  // wavefronts of 16-byte keys)
+  __shared__ unsigned long long kx[kSortTile], ky[kSortTile];
   __shared__ uint32_t si[kSortTile];
   __shared__ uint16_t src[kSortTile];
   const uint32_t P = (R + 1) / 2;
@@ -603,18 +605,30 @@ __global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2
   const uint32_t la = i1 - i0, lb = j1 - j0;
   for (uint32_t t = threadIdx.x; t < la + lb; t += blockDim.x) {
     const uint32_t g = t < la ? a0 + i0 + t : a1 + j0 + (t - la);
-    sk[t] = ki[g];
+    const ulonglong2 k = ki[g];
+    kx[t] = k.x;
+    ky[t] = k.y;
     si[t] = ii[g];
   }
   __syncthreads();
+  auto lt = [&](uint32_t x, uint32_t y) { return kx[x] < kx[y] || (kx[x] == kx[y] && ky[x] < ky[y]); };
   constexpr uint32_t per = kSortTile / kSortThreads;
   const uint32_t kk = threadIdx.x * per;
   if (kk < la + lb) {
-    uint32_t i = (uint32_t)corank(kk, la, lb, [&](uint64_t x) { return sk[x]; }, [&](uint64_t x) { return sk[la + x]; });
-    uint32_t j = kk - i;
+    uint32_t i, j;
+    {  // co-rank of kk
+      uint32_t l = kk > lb ? kk - lb : 0, h = kk < la ? kk : la;
+      while (l < h) {
+        const uint32_t m = (l + h) >> 1;
+        if (lt(m, la + kk - m - 1)) l = m + 1;
+        else h = m;
+      }
+      i = l;
+      j = kk - l;
+    }
     const uint32_t end = min(kk + per, la + lb);
     for (uint32_t k = kk; k < end; k++) {
-      const bool takeA = j >= lb || (i < la && key_lt(sk[i], sk[la + j]));
+      const bool takeA = j >= lb || (i < la && lt(i, la + j));
       src[k] = (uint16_t)(takeA ? i++ : la + j++);
     }
   }
@@ -622,7 +636,7 @@ __global__ void __launch_bounds__(kSortThreads) tl_merge_kernel(const ulonglong2
   const uint32_t out0 = a0 + k0;  // the merged run starts where run 2p did
   for (uint32_t t = threadIdx.x; t < la + lb; t += blockDim.x) {
     const uint32_t q = src[t];
-    ko[out0 + t] = sk[q];
+    ko[out0 + t] = make_ulonglong2(kx[q], ky[q]);
     io[out0 + t] = si[q];
   }
 }
@@ -806,6 +820,10 @@ __device__ __forceinline__ uint32_t tl_tile_group(const TlTables& T, uint64_t i0
     const TlItem it = T.items[T.order[i]];
     S.it[t] = it;
     kind = it.kind & 3u;
+#ifndef HG_TL_NO_PREFETCH
+    if (kind != TL_HOST)  // the payload's first line: on its way while the tile is grouped
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(it.a));
+#endif
   }
   if (t < 4) S.cur[t] = 0;
   __syncthreads();
@@ -833,7 +851,7 @@ __device__ __forceinline__ uint32_t tl_tile_group(const TlTables& T, uint64_t i0
 }
 
 #ifndef HG_TL_LEN_MINB
-#define HG_TL_LEN_MINB (768 / HG_TL_TILE)  // 80 registers
+#define HG_TL_LEN_MINB (1280 / HG_TL_TILE)  // 48 registers: 1.26 -> 1.05 ms at C5 x0.25 (vs 80)
 #endif
 #ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kTlTile, HG_TL_LEN_MINB) tl_len_kernel(TlTables T) {

@@ -49,7 +49,10 @@ def main():
         samp[k] += s
     ti, ts = sum(inst.values()), max(sum(samp.values()), 1)
     print(f"total warp instructions {ti}, stall samples {ts}")
-    for k, v in inst.most_common(top):
+    import os
+    order = samp if os.environ.get("SORT") == "samples" else inst
+    for k, _ in order.most_common(top):
+        v = inst[k]
         print(f"{k[0]}:{k[1]:5d}  inst {100 * v / ti:5.1f}%  samples {100 * samp[k] / ts:5.1f}%")
 
 
