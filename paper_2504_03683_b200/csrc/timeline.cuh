@@ -997,17 +997,16 @@ __global__ void __launch_bounds__(kTlTile, HG_TL_WRITE_MINB) tl_write_kernel(TlT
       }
     }
     __syncthreads();
-    if (staged) {
-      const uint64_t o0 = S.o0, oend = S.oend;
-      const uint32_t nch = (uint32_t)((total + 15) / 16);
-      for (uint32_t c = t; c < nch; c += kTlTile) {
-        const uint64_t g0 = al + 16ull * c;
-        if (g0 >= o0 && g0 + 16 <= oend) {
-          *reinterpret_cast<uint4*>(T.out + g0) = *reinterpret_cast<const uint4*>(S.stage + 16 * c);
-        } else {
-          const uint64_t lo = g0 > o0 ? g0 : o0, hi = g0 + 16 < oend ? g0 + 16 : oend;
-          for (uint64_t b = lo; b < hi; b++) T.out[b] = S.stage[b - al];
-        }
+    if (staged) {  // bytes [head, end) of the 16-byte aligned window at al
+      char* gout = T.out + al;
+      const uint32_t head = (uint32_t)(S.o0 - al), end = (uint32_t)total;
+      const uint32_t full_end = end & ~15u;
+      for (uint32_t b0 = 16u * t + (head ? 16u : 0u); b0 < full_end; b0 += 16u * kTlTile)
+        *reinterpret_cast<uint4*>(gout + b0) = *reinterpret_cast<const uint4*>(S.stage + b0);
+      if (t < 16) {  // the partial first and last chunks, a byte per thread
+        if (head && head + t < 16u && head + t < end) gout[head + t] = S.stage[head + t];
+        const uint32_t b = full_end + t;
+        if (b < end && (b >= 16u || !head)) gout[b] = S.stage[b];
       }
       __syncthreads();
     }

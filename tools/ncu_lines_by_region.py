@@ -6,6 +6,7 @@ Reads the ncu source page (per SASS instruction) and maps every SASS address to 
 (inlined-at line in fast.cuh when inlined) with nvdisasm -g of the object's cubin."""
 
 import collections
+import os
 import csv
 import io
 import re
@@ -37,7 +38,10 @@ def main():
         m = re.search(r'//## File "([^"]+)", line (\d+)(.*)', l)
         if m:
             inl = re.search(r'inlined at "([^"]+)", line (\d+)', m.group(3))
-            cur = (Path(inl.group(1)).name, int(inl.group(2))) if inl else (Path(m.group(1)).name, int(m.group(2)))
+            if inl and not os.environ.get("INNER"):
+                cur = (Path(inl.group(1)).name, int(inl.group(2)))
+            else:
+                cur = (Path(m.group(1)).name, int(m.group(2)))
             continue
         m = re.search(r"/\*([0-9a-f]{4,})\*/", l)
         if m and cur:
