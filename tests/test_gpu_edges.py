@@ -116,6 +116,20 @@ def test_timeline_device_heavy_2m_events(engine):
     _check(engine, raws, wl, timeline=True)
 
 
+@pytest.mark.parametrize("name_len", [300, 4000])
+def test_timeline_long_names(engine, name_len):
+    """Kernel names of hundreds to thousands of bytes (escapes and non-ASCII among them): formatting
+    tiles larger than the shared staging buffer are written straight to the output."""
+    from paper_2504_03683_b200 import synth
+
+    P = synth.PID_BASE
+    names = [("k%d_" % i) + ("x\u00e9\"" if i % 3 == 0 else "y") * (name_len // 4) for i in range(24)]
+    names = [n.encode().decode("unicode_escape") for n in names]
+    streams = [synth.StreamSpec("long", P, P + i, 4_000, 77_000 + i) for i in range(6)]
+    wl = synth.Workload("long", synth.ze_registry(), streams, dict(prof_p=0.8), kernel_names=names)
+    _check(engine, synth.generate(wl), wl, timeline=True)
+
+
 def test_shared_identity_streams_merge(engine):
     """Two cursors per identity with interleaved calls (entries in one, exits in the other)
     through run_pipeline: one merged stream per identity, equal to the oracle that keys
