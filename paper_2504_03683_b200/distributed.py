@@ -23,6 +23,7 @@ CPU for gloo, so the same code runs in the world-size-2 CPU tests.
 
 from __future__ import annotations
 
+import os
 from types import SimpleNamespace
 
 from .abi import HG_TRACE_ERROR, HG_WANT_TALLY
@@ -180,6 +181,9 @@ class ShardedRun:
         self.comm = comm
         self.world = comm.world if comm is not None else 1
         self.rank = comm.rank if comm is not None else 0
+        # the multi-rank protocol (split run, collectives, merge); HAPIGPU_COLLECTIVES=1 keeps it at
+        # world size 1 (tests of the NCCL flavour on one GPU)
+        self.multi = comm is not None and (self.world > 1 or os.environ.get("HAPIGPU_COLLECTIVES") == "1")
         self.stream_global = stream_global
         self.global_streams = global_streams
         self.global_last_ts = None
@@ -195,7 +199,7 @@ class ShardedRun:
         eng = self.engine
         sg = self.stream_global if self.stream_global is not None else list(range(len(eng._streams)))
         status, failure, last = STATUS_OK, None, 0
-        if self.world == 1 and input_error is None:  # one rank: hg_run (the fused single-rank path)
+        if not self.multi and input_error is None:  # one rank: hg_run (the fused single-rank path)
             self.rc = eng.run_raw(want)
             self.global_last_ts = eng.local_last_ts()
             k, tot, h2d, d2h, nl = eng.timing()
@@ -215,14 +219,14 @@ class ShardedRun:
             except Exception as e:  # noqa: BLE001  (an engine failure: reported to every rank)
                 status, failure = STATUS_ENGINE, ((2, self.rank), pack_exception(e))
         g, gstatus = last, status
-        if self.world > 1:
+        if self.multi:
             g, gstatus = self.comm.max_i64([last - _BIAS, status])
             g += _BIAS
         if gstatus:
             self._raise_first(failure)
         self.global_last_ts = g
         self.rc = eng.finish(g)
-        if self.world > 1:
+        if self.multi:
             self._merge(sg)
         k, tot, h2d, d2h, nl = eng.timing()
         walk, chain, decode = eng.phase_timing()
@@ -230,7 +234,7 @@ class ShardedRun:
                 "h2d_bytes": h2d, "d2h_bytes": d2h, "launches": nl, "rc": self.rc}
 
     def _raise_first(self, failure):
-        packed = [failure] if self.world == 1 else self.comm.all_gather_object(failure)
+        packed = [failure] if not self.multi else self.comm.all_gather_object(failure)
         key, exc = min((f for f in packed if f is not None), key=lambda f: f[0])
         if key[0] == 2 and failure is None:
             raise EngineError(f"rank {key[1]} failed: {unpack_exception(exc)}")
@@ -276,7 +280,7 @@ class ShardedRun:
         eng = self.engine
         flat = eng._flat
         stats = self.stats()
-        if self.world == 1:
+        if not self.multi:
             gs = eng._streams
             idents = [(s.hostname, s.pid, s.tid) for s in gs]
             spans = eng.stream_spans()
@@ -296,11 +300,11 @@ class ShardedRun:
                       for o in eng.orphans_raw()]
         if any_error:
             err = self._first_error(sg, labels)
-            orphans = orph_local if self.world == 1 else [o for g in self.comm.all_gather_object(orph_local) for o in g]
+            orphans = orph_local if not self.multi else [o for g in self.comm.all_gather_object(orph_local) for o in g]
             key, exc, cut = err
             olist = orphan_list(orphans, orphan_labels, flat, cutoff=key, cut_streams=cut)
             return None, stats, olist, unpack_exception(exc)
-        if self.world > 1 and stats["orphan_exits"]:
+        if self.multi and stats["orphan_exits"]:
             orphans = [o for g in self.comm.all_gather_object(orph_local) for o in g]
         else:
             orphans = orph_local
@@ -326,7 +330,7 @@ class ShardedRun:
             s = eng._streams[e.local]
             named = RawStream(s.hostname, s.pid, s.tid, labels[e.stream], s.data, getattr(s, "info", None))
             mine = (error_key(e), pack_exception(make_exception(e, named, eng._flat)), cut)
-        allc = [mine] if self.world == 1 else self.comm.all_gather_object(mine)
+        allc = [mine] if not self.multi else self.comm.all_gather_object(mine)
         key, exc, _ = min((c for c in allc if c is not None), key=lambda c: c[0])
         cuts = {}
         for c in allc:

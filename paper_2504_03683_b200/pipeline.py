@@ -17,6 +17,7 @@ is no CPU fallback path.
 from __future__ import annotations
 
 import json
+import os
 import threading
 from dataclasses import dataclass, field
 
@@ -357,7 +358,7 @@ def run_pipeline(source, sinks=(), registry=None, engine=None, distributed=False
         from .distributed import Comm
 
         comm = Comm(None if distributed is True else distributed)
-        if comm.world == 1:
+        if comm.world == 1 and os.environ.get("HAPIGPU_COLLECTIVES") != "1":
             comm = None
     if comm is None:
         raws, infos = _resolve_source(source, registry)

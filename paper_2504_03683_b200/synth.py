@@ -197,7 +197,7 @@ def generate_stream(wl: Workload, spec: StreamSpec, flat=None, until_ns=None, co
     meta = [s.id for s in wl.registry.schemas if s.event_class == "meta"]
     P = SynthParams(seed=spec.seed, n_events=spec.n_events, meta_sid=meta[0] if meta else -1,
                     **{k: v for k, v in p.items()})
-    cap = 16 + spec.n_events * 96 + 4096
+    cap = 16 + spec.n_events * (96 + max((len(n) for n in names), default=0)) + 4096
     arr, buf = _buffer(cap)
     ln, ev = C.c_uint64(), C.c_uint64()
     rc = L.synth_stream(C.byref(P), by_id, max_id + 1, flat.kinds, farr, len(fns), name_arr, len(names),

@@ -70,6 +70,8 @@ def _worker(rank, world, port, q, case, tmp):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    if world == 1:
+        os.environ["HAPIGPU_COLLECTIVES"] = "1"  # the multi-rank protocol at world size 1
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from fake_engine import FakeEngine
@@ -195,6 +197,23 @@ def test_four_ranks_two_streams_idle_ranks_still_agree():
     for rank in range(4):
         kind, rep, stats, orphans, diag = outs[rank]
         assert kind == "ok" and rep == want.report and stats == want.stats and orphans == want.orphans
+
+
+@pytest.mark.parametrize("case", ["clean", "corrupt"])
+def test_one_rank_through_the_collectives(case):
+    """World size 1 with the multi-rank protocol forced (split run, merge buffer, error exchange)."""
+    outs = _run(case, world=1)
+    want = _oracle(case)
+    if case == "corrupt":
+        from paper_2504_03683_b200.distributed import unpack_exception
+
+        kind, packed, diag = outs[0]
+        e = unpack_exception(packed)
+        assert kind == "raised" and type(e).__name__ == type(want.error).__name__ and str(e) == str(want.error)
+        assert diag == want.orphans
+        return
+    kind, rep, stats, orphans, diag = outs[0]
+    assert kind == "ok" and rep == want.report and stats == want.stats and orphans == want.orphans == diag
 
 
 def test_partition_lpt_balances_and_keeps_identities_together():

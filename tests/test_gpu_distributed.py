@@ -32,12 +32,16 @@ def _c5():
     return wl, synth.generate(wl)
 
 
-def _worker(rank, world, port, q, case, tmp):
+def _worker(rank, world, port, q, case, tmp, backend="gloo"):
+    import torch
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        torch.cuda.set_device(0)
+        os.environ["HAPIGPU_COLLECTIVES"] = "1"  # the multi-rank protocol at world size 1
+    dist.init_process_group(backend, rank=rank, world_size=world)
     try:
         from test_distributed import _corrupt, _generate
         from paper_2504_03683_b200 import run_pipeline, synth
@@ -96,12 +100,12 @@ def _worker(rank, world, port, q, case, tmp):
         dist.destroy_process_group()
 
 
-def _run(case, world=2):
+def _run(case, world=2, backend="gloo"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     with tempfile.TemporaryDirectory() as tmp:
-        procs = [ctx.Process(target=_worker, args=(r, world, port, q, case, tmp)) for r in range(world)]
+        procs = [ctx.Process(target=_worker, args=(r, world, port, q, case, tmp, backend)) for r in range(world)]
         for p in procs:
             p.start()
         outs = dict(q.get(timeout=600) for _ in procs)
@@ -197,3 +201,29 @@ def test_three_ranks_timeline_merged_across_ranks():
     for rank in (1, 2):
         kind, rep, tl = outs[rank]
         assert kind == "ok" and rep == want.report and tl is None
+
+
+@pytest.mark.parametrize("case", ["clean", "corrupt", "c5"])
+def test_nccl_one_rank(case):
+    """The NCCL flavour of the collectives (CUDA tensors, the merge buffer all-reduced in HBM, the
+    timeline runs gathered on the device) at world size 1 -- the only NCCL world one GPU allows."""
+    import json
+
+    from oracle import oracle
+    from paper_2504_03683_b200.distributed import unpack_exception
+
+    outs = _run(case, world=1, backend="nccl")
+    if case == "c5":
+        wl, raws = _c5()
+        want = oracle.run(raws, wl.registry, [r.info for r in raws], want_timeline=True, device_index=3)
+        kind, rep, tl = outs[0]
+        assert kind == "ok" and rep == want.report and tl == json.loads(want.timeline)
+        return
+    want = _oracle(case)
+    if case == "corrupt":
+        kind, packed, diag = outs[0]
+        e = unpack_exception(packed)
+        assert kind == "raised" and type(e).__name__ == type(want.error).__name__ and str(e) == str(want.error)
+        return
+    kind, rep, stats, orphans, diag, path = outs[0]
+    assert kind == "ok" and rep == want.report and stats == want.stats and orphans == want.orphans == diag
