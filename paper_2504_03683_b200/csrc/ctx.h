@@ -76,6 +76,13 @@ struct TlSource {
   std::vector<TlStreamName> streams;                  // identities the stream field of the keys indexes
   const uint32_t* flush_stream = nullptr;             // device: flush rank -> stream (truncated spans)
   uint64_t n_dev = 0;                                 // device spans (thread-name table bound)
+  // messages of the single pass (tl_ranges): range r's at items[r * rcap ...], rn[r] of them
+  bool ranges = false;
+  uint32_t n_ranges = 0, rcap = 0;
+  const uint32_t* rn = nullptr;
+  const uint32_t* range_stream = nullptr;
+  const unsigned long long* range_base = nullptr;
+  const uint32_t* stream_range0 = nullptr;
 };
 
 struct hg_ctx {
@@ -144,6 +151,12 @@ struct hg_ctx {
   bool have_fn_names = false;
   DBuf<TlItem> d_tl_items;
   uint64_t tl_cap = 0;
+  // timeline messages from the single pass: per range, in record order (Params::tl_ritems)
+  bool tl_ranges = false;          // the last timeline run's messages are per range
+  uint32_t tl_rcap = 0;            // message slots per range
+  DBuf<uint32_t> d_tl_rn;          // messages per range
+  DBuf<unsigned long long> d_tl_pres;  // result bits of the first pending exits per range
+  DBuf<uint32_t> d_tl_rpre;        // exclusive scan of d_tl_rn
   DBuf<ulonglong2> d_tl_keys[2];
   DBuf<uint32_t> d_tl_idx[2];
   DBuf<uint32_t> d_tl_ro[2], d_tl_tcnt, d_tl_tile0, d_tl_split;  // sort: run offsets, tile counts, merge splits
@@ -320,6 +333,8 @@ int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, u
 int tl_sort_runs(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
                  const unsigned long long* rec_off, uint32_t n_runs, const uint32_t** order);  // timeline.cu
 int run_timeline_order(hg_ctx* ctx);                                                   // timeline.cu
+int tl_merge_passes(hg_ctx* ctx, uint32_t R, uint32_t n, const uint32_t** order);          // timeline.cu
+int tl_sort_ranges(hg_ctx* ctx, const TlSource& S, uint32_t* n_out, const uint32_t** order);  // timeline.cu
 int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts);            // timeline.cu
 int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint64_t* total);  // timeline.cu
 void ingest_free(hg_ctx* ctx);     // ingest.cu

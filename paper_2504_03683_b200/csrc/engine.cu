@@ -263,7 +263,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_orphans.release(); ctx->d_errors.release(); ctx->d_stream_spans.release();
   ctx->d_keys.release(); ctx->d_vals.release(); ctx->d_name_len.release(); ctx->d_small.release();
   ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release();
-  ctx->d_tl_items.release();
+  ctx->d_tl_items.release(); ctx->d_tl_rn.release(); ctx->d_tl_pres.release(); ctx->d_tl_rpre.release();
   for (int k = 0; k < 2; k++) { ctx->d_tl_keys[k].release(); ctx->d_tl_idx[k].release(); ctx->d_tl_ro[k].release(); }
   ctx->d_tl_tcnt.release(); ctx->d_tl_tile0.release(); ctx->d_tl_split.release();
   ctx->d_tl_lens.release(); ctx->d_tl_stream_proc.release(); ctx->d_tl_offs.release(); ctx->d_tl_bsum.release();
@@ -727,6 +727,10 @@ Params make_params(hg_ctx* ctx) {
   p.tl_comp_base = ctx->tl_comp_base;
   p.tl_cap = ctx->tl_cap;
   p.tl_rec_off = ctx->d_tl_rec_off.ptr;
+  p.tl_ritems = ctx->tl_ranges ? ctx->d_tl_items.ptr : nullptr;
+  p.tl_rcap = ctx->tl_rcap;
+  p.tl_rn = ctx->tl_ranges ? ctx->d_tl_rn.ptr : nullptr;
+  p.tl_pres = ctx->tl_ranges ? ctx->d_tl_pres.ptr : nullptr;
   p.seg_bytes = ctx->seg_bytes;
   p.deep = ctx->d_deep.ptr;
   p.deep_used = C + C_DEEP_USED;
@@ -787,6 +791,25 @@ static int read_counters(hg_ctx* ctx) {
   return HG_OK;
 }
 
+// timeline messages of the single pass: rcap slots per range (a record is at least 16 bytes),
+// compose's messages after them (at most one per summary entry); false when they do not fit
+static bool tl_range_buffers(hg_ctx* ctx) {
+  const uint64_t rcap = ctx->range_bytes / 16ull + 2;
+  const uint64_t base = (uint64_t)ctx->n_ranges * rcap;
+  const uint64_t cap = base + ctx->pool_cap + 64;
+  if (cap >= (1ull << 32)) return false;
+  if (ctx->d_tl_items.ensure(cap) != cudaSuccess || ctx->d_tl_rn.ensure(std::max<uint32_t>(ctx->n_ranges, 1)) != cudaSuccess ||
+      ctx->d_tl_pres.ensure(std::max<uint64_t>((uint64_t)ctx->n_ranges * kRLP, 1)) != cudaSuccess) {
+    cudaGetLastError();  // (clear the allocation failure)
+    return false;
+  }
+  ctx->tl_rcap = (uint32_t)rcap;
+  ctx->tl_comp_base = base;
+  ctx->tl_cap = cap;
+  ctx->tl_ranges = true;
+  return true;
+}
+
 int hg_run_local(hg_ctx* ctx, uint32_t want) {
   if (!ctx) return HG_EARG;
   cudaSetDevice(ctx->cfg.device);
@@ -794,8 +817,11 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;
-  bool fast = ctx->path_opt != 1 &&
-              !(want & (HG_WANT_TIMELINE | HG_WANT_EVENTS | HG_WANT_VALIDATE | HG_WANT_TL_ITEMS));
+  // the single pass serves tally and timeline runs (event order, validation and a rank's share of a
+  // multi-rank timeline need record indices per slot: the exact path)
+  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_EVENTS | HG_WANT_VALIDATE | HG_WANT_TL_ITEMS)) &&
+              !((want & HG_WANT_TIMELINE) && getenv("HAPIGPU_TL_EXACT"));
+  ctx->tl_ranges = false;
   bool retried = false;
   for (int attempt = 0; attempt < 9; attempt++) {
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
@@ -808,6 +834,8 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     CK(cudaEventRecord(ctx->ev[1], ctx->stream));
     int rc = ensure_scratch(ctx, 0);
     if (rc) return rc;
+    ctx->tl_ranges = false;
+    if (fast && (want & HG_WANT_TIMELINE) && !tl_range_buffers(ctx)) fast = false;  // too large: the exact path
     rc = fast ? launch_fast(ctx) : launch_phase1(ctx);
     if (rc) return rc;
     rc = read_counters(ctx);
@@ -1028,6 +1056,7 @@ static int collect_results(hg_ctx* ctx, uint64_t global_last_ts) {
 static int run_fused(hg_ctx* ctx, uint32_t want, bool& done) {
   done = false;
   ctx->want = want;
+  ctx->tl_ranges = false;  // (a tally run: no timeline messages; the last timeline run's buffers are stale)
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;

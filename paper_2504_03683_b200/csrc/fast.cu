@@ -13,8 +13,13 @@ int launch_fast(hg_ctx* ctx) {
   const uint32_t nw = ctx->fast_warps;
   const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
   const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
-  auto kern = sd ? (ctx->deep_inline ? fast_kernel<true, true> : fast_kernel<true, false>)
-                 : (ctx->deep_inline ? fast_kernel<false, true> : fast_kernel<false, false>);
+  using K = void (*)(Params, const Params*);
+  static const K kerns[8] = {fast_kernel<false, false, false>, fast_kernel<false, true, false>,
+                             fast_kernel<true, false, false>,  fast_kernel<true, true, false>,
+                             fast_kernel<false, false, true>,  fast_kernel<false, true, true>,
+                             fast_kernel<true, false, true>,   fast_kernel<true, true, true>};
+  const bool tl = p.tl_ritems != nullptr;
+  const K kern = kerns[(tl ? 4 : 0) + (sd ? 2 : 0) + (ctx->deep_inline ? 1 : 0)];
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint32_t per_cta = nw * kWarp;
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));

@@ -147,9 +147,18 @@ struct RLane {
   uint32_t ci, clast;   // chunks requested, last chunk this range reads
   uint32_t recent;      // bit i: a chunk was requested i iterations ago (its fill group may be pending)
   uint32_t np, ne;
+  uint32_t ti;          // timeline messages of this range so far (timeline runs)
   bool bad;
   bool fresh;           // no requests until every pending fill of this lane completed (slot reuse)
 };
+
+// one timeline message of the lane's range, in record order (k: the record's index in the range)
+__device__ __forceinline__ void r_item(const Params& p, RLane& R, uint64_t khi, uint64_t k, uint64_t a, uint64_t b,
+                                       uint32_t kind, uint32_t x) {
+  TlItem it;
+  it.khi = khi; it.klo = k; it.a = a; it.b = b; it.kind = kind; it.x = x;
+  p.tl_ritems[(uint64_t)R.r * p.tl_rcap + R.ti++] = it;
+}
 
 // first offset in [t0, t1) that starts a chain of kScanDepth plausible headers with
 // non-decreasing timestamps (or a shorter one that ends exactly at the stream end).
@@ -190,6 +199,7 @@ __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, u
       st.entry = kNone; st.exit = kNone; st.first_ts = 0; st.last_ts = 0; st.pool_off = 0;
       st.n = 0; st.np = 0; st.ne = 0; st.pad = 0;
       p.rstate[r] = st;
+      if (p.tl_rn) p.tl_rn[r] = 0;
       continue;
     }
     R.C0 = entry & ~(uint64_t)(kRChunk - 1);
@@ -204,12 +214,12 @@ __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, u
     R.ci = 0; R.fresh = true;
     R.prev_ts = 0; R.first_ts = 0;
     R.deep = nullptr;
-    R.r = r; R.s = s; R.n = 0; R.spans = 0; R.np = 0; R.ne = 0; R.bad = false;
+    R.r = r; R.s = s; R.n = 0; R.spans = 0; R.np = 0; R.ne = 0; R.ti = 0; R.bad = false;
     return true;
   }
   R.r = p.n_ranges;
   R.o = R.t1 = R.entry = 0; R.C0 = 0; R.size = 0; R.size32 = 0; R.g = p.data;
-  R.n = R.np = R.ne = R.ci = R.clast = 0;
+  R.n = R.np = R.ne = R.ci = R.clast = R.ti = 0;
   R.bad = false; R.fresh = true;
   return false;
 }
@@ -241,7 +251,8 @@ __device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T)
     for (uint32_t i = 0; i < R.np; i++) {
       SumEntry e;
       if (i < (uint32_t)kRLP) {
-        e.ts = T.pd_ts[i * kWarp]; e.result = 0;  // result bits only feed the timeline (exact path)
+        e.ts = T.pd_ts[i * kWarp];
+        e.result = p.tl_pres ? p.tl_pres[(uint64_t)R.r * kRLP + i] : 0ull;  // result bits: the timeline only
         const uint32_t m = T.pd_meta[i * kWarp];
         e.fn = m_fn(m); e.flags = m >> 19; e.seq = T.pd_k[i * kWarp];
       } else {
@@ -266,6 +277,7 @@ __device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T)
   st.pool_off = poff;
   st.n = R.n; st.np = R.np; st.ne = R.ne; st.pad = 0;
   p.rstate[R.r] = st;
+  if (p.tl_rn) p.tl_rn[R.r] = R.ti;
   if (R.spans) atomicAdd(&p.stream_spans[R.s], (unsigned long long)R.spans);
   if (R.bad) atomicOr(p.anom, 1u);   // anomaly reasons (bits): 1 record, 2 drain, 4 string, 8 chain, 16 order
 }
@@ -321,6 +333,8 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
   R.o = (uint32_t)(a + L);
   if (dt) {
     if (cls == HG_CLASS_DEVICE) R.spans++;  // a device span's identity (sinks.py:240-242)
+    if (p.tl_ritems) r_item(p, R, h.ts, k, reinterpret_cast<uint64_t>(R.g + a + 16), 0,
+                            cls == HG_CLASS_DEVICE ? TL_DEVICE : TL_SAMPLE, h.sid);
     return true;
   }
   const uint32_t fnm = d.x & M_FN;
@@ -364,6 +378,7 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
         hf.fold(p, (int32_t)fnm, h.ts - ets, (xf & 2u) != 0);
         K.host++;
         R.spans++;
+        if (p.tl_ritems) r_item(p, R, h.ts, k, ets, res, TL_HOST | (result_kind(fl) << 4), fnm);
       } else {
         push_orphan(p, R.s, m_fn(fnm), h.ts, (1ull << 63) | ((uint64_t)R.r << 24) | k);
         K.orph++;
@@ -373,6 +388,7 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
       if (i < (uint32_t)kRLP) {
         T.pd_ts[i * kWarp] = h.ts; T.pd_meta[i * kWarp] = fnm | (xf << 19);
         T.pd_k[i * kWarp] = k;
+        if (p.tl_pres) p.tl_pres[(uint64_t)R.r * kRLP + i] = res;
       } else {
         if (i >= (uint32_t)kRLP + kRDeepHalf || !r_deep(p, R)) { R.bad = true; return false; }
         SumEntry e;
@@ -659,8 +675,9 @@ static __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, 
 
 // kSD: the registry's inline descriptors fit in shared memory (max_sid < kSdescMax);
 // kDeep: stacks deeper than kRLS stay on the inline path (overflow chunk) -- chosen by the host
-// once a run of the trace needed overflow chunks
-template <bool kSD, bool kDeep>
+// once a run of the trace needed overflow chunks; kTL: a timeline run (every host span, device
+// span and sample also leaves a message in its range's list, r_item)
+template <bool kSD, bool kDeep, bool kTL>
 __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const Params* gp) {
   const Params& gpr = *gp;
   const uint32_t nw = blockDim.x >> 5;
@@ -807,6 +824,12 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       T.pd_ts[i] = ts;
       T.pd_meta[i] = fnm | ((1u | (err ? 2u : 0u) | (((D.x >> 26) & 3u) << 4)) << 19);
       T.pd_k[i] = R.n - 1;
+      if (kTL) p.tl_pres[(uint64_t)R.r * kRLP + np] = res;
+    }
+    if (kTL) {
+      if (fXp) r_item(p, R, ts, R.n - 1, ets, res, TL_HOST | (((D.x >> 26) & 3u) << 4), fnm);
+      if (qflag) r_item(p, R, ts, R.n - 1, reinterpret_cast<uint64_t>(R.g + o_start + 16u), 0,
+                        (D.x & FD_ISDEV) ? TL_DEVICE : TL_SAMPLE, sid);
     }
     R.ne = ne + (fE ? 1u : 0u) - (fXp ? 1u : 0u);
     R.np = np + (fXq ? 1u : 0u);

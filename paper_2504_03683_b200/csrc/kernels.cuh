@@ -95,6 +95,14 @@ struct Params {
   uint64_t tl_comp_base;
   uint64_t tl_cap;
   const unsigned long long* tl_rec_off;  // per stream: global record number of its first record
+  // timeline messages of the single pass (nullptr unless a timeline run takes it): range r's
+  // messages in record order at tl_ritems[r * tl_rcap ...], their number in tl_rn[r], klo = the
+  // record's index within the range (tl_range_compact makes it the mux key); tl_pres: result bits
+  // of each range's first kRLP pending exits (compose's cross-range spans)
+  TlItem* tl_ritems;
+  uint32_t tl_rcap;
+  uint32_t* tl_rn;
+  unsigned long long* tl_pres;
   // segments
   uint32_t seg_bytes;
   SumEntry* deep;                  // per-lane automaton chunks of deep segments

@@ -23,7 +23,6 @@ int tl_sort_runs(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t
   CK(ctx->d_tl_tcnt.ensure(n_rtiles + 2));
   CK(ctx->d_tl_tile0.ensure(R / 2 + 3));
   CK(ctx->d_tl_split.ensure(n / kSortTile + R / 2 + 3));
-  int cur = 0;
   if (n) {
     if (n_rtiles) {
       tl_count_kernel<<<n_rtiles, kSortThreads, 0, st>>>(items, nrec_slots, ctx->d_tl_tcnt.ptr);
@@ -39,6 +38,16 @@ int tl_sort_runs(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t
       ctx->launches++;
     }
     CK(cudaGetLastError());
+  }
+  return tl_merge_passes(ctx, R, n, order);
+}
+
+// the merge-path passes over the R sorted runs in d_tl_keys[0] / d_tl_idx[0] (run offsets in
+// d_tl_ro[0]); returns the item index of every message in mux order
+int tl_merge_passes(hg_ctx* ctx, uint32_t R, uint32_t n, const uint32_t** order) {
+  cudaStream_t st = ctx->stream;
+  int cur = 0;
+  if (n) {
     while (R > 1) {
       const uint32_t P = (R + 1) / 2;
       const uint32_t tiles = n / kSortTile + P + 1;  // bound on the output tiles of the pass
@@ -56,6 +65,44 @@ int tl_sort_runs(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t
   }
   *order = ctx->d_tl_idx[cur].ptr;
   return HG_OK;
+}
+
+// the single pass's messages (per range) + compose's: keys of every range appended in range order
+// (tl_range_compact_kernel), compose's tiles sorted, then the merge passes
+int tl_sort_ranges(hg_ctx* ctx, const TlSource& S, uint32_t* n_out, const uint32_t** order) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t nr = S.n_ranges, ns = S.n_runs, ncomp = S.ncomp;
+  CK(ctx->d_tl_rpre.ensure(nr + 1));
+  if (nr) CK(cudaMemcpyAsync(ctx->d_tl_rpre.ptr, S.rn, nr * 4ull, cudaMemcpyDeviceToDevice, st));
+  tl_small_scan_kernel<<<1, 1024, 0, st>>>(ctx->d_tl_rpre.ptr, nr);  // exclusive; [nr] = the total
+  uint32_t nrec = 0;
+  CK(cudaMemcpyAsync(&nrec, ctx->d_tl_rpre.ptr + nr, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->launches++;
+  const uint64_t n64 = (uint64_t)nrec + ncomp;
+  if (n64 >= (1ull << 32)) return fail(ctx, HG_EUNSUPPORTED, "timeline: more than 2^32 messages");
+  const uint32_t n = (uint32_t)n64;
+  const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
+  const uint32_t R = ns + ntc;
+  for (int k = 0; k < 2; k++) {
+    CK(ctx->d_tl_keys[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_idx[k].ensure(std::max<uint32_t>(n, 1)));
+    CK(ctx->d_tl_ro[k].ensure(R + 2));
+  }
+  CK(ctx->d_tl_tile0.ensure(R / 2 + 3));
+  CK(ctx->d_tl_split.ensure(n / kSortTile + R / 2 + 3));
+  const uint32_t nrb = (nr + kSortThreads / 32 - 1) / (kSortThreads / 32);
+  tl_range_compact_kernel<<<nrb + std::max<uint32_t>(ntc, 1), kSortThreads, 0, st>>>(
+      const_cast<TlItem*>(S.items), nr, S.rcap, S.rn, ctx->d_tl_rpre.ptr, S.range_stream, S.range_base,
+      S.stream_range0, ns, S.nrec_slots, ncomp, nrec, ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, ctx->d_tl_ro[0].ptr);
+  ctx->launches++;
+  if (ntc) {
+    tl_tilesort_kernel<<<ntc, kSortThreads, 0, st>>>(ctx->d_tl_keys[0].ptr, ctx->d_tl_idx[0].ptr, nrec, ncomp);
+    ctx->launches++;
+  }
+  CK(cudaGetLastError());
+  *n_out = n;
+  return tl_merge_passes(ctx, R, n, order);
 }
 
 int tl_sort(hg_ctx* ctx, const TlItem* items, uint32_t nrec_slots, uint32_t N, uint32_t ncomp, uint32_t n,
@@ -78,6 +125,15 @@ int tl_scan(hg_ctx* ctx, const uint32_t* lens, uint32_t n, uint64_t* offs, uint6
 static TlSource own_source(hg_ctx* ctx) {
   const unsigned long long* C = ctx->counters.data();
   TlSource S;
+  if (ctx->tl_ranges) {  // the single pass's per-range messages (n: known after their scan)
+    S.ranges = true;
+    S.n_ranges = ctx->n_ranges;
+    S.rcap = ctx->tl_rcap;
+    S.rn = ctx->d_tl_rn.ptr;
+    S.range_stream = ctx->d_range_stream.ptr;
+    S.range_base = ctx->d_range_base.ptr;
+    S.stream_range0 = ctx->d_stream_range0.ptr;
+  }
   S.items = ctx->d_tl_items.ptr;
   S.nrec_slots = (uint32_t)ctx->tl_comp_base;
   S.N = (uint32_t)(ctx->tl_comp_base + C[C_TL_N2]);
@@ -117,7 +173,7 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
   ctx->tl_ready = false;
   if (!ctx->have_fn_names || ctx->fn_names.size() != ctx->n_fn)
     return fail(ctx, HG_ESTATE, "hg_set_function_names is required for the timeline");
-  const uint32_t n = S.n;
+  uint32_t n = S.n;
   const uint32_t ns = (uint32_t)S.streams.size();
   cudaStream_t st = ctx->stream;
   cudaEvent_t e0, e1;
@@ -168,7 +224,8 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
   // compose's messages per tile, merge the runs pairwise
   const uint32_t* order = nullptr;
   {
-    int rc = tl_sort_runs(ctx, S.items, S.nrec_slots, S.N, S.ncomp, n, S.rec_off, S.n_runs, &order);
+    int rc = S.ranges ? tl_sort_ranges(ctx, S, &n, &order)
+                      : tl_sort_runs(ctx, S.items, S.nrec_slots, S.N, S.ncomp, n, S.rec_off, S.n_runs, &order);
     if (rc) return rc;
   }
   // metadata first occurrences

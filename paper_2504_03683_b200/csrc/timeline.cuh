@@ -492,6 +492,51 @@ __global__ void __launch_bounds__(kSortThreads) tl_compact_kernel(const TlItem* 
 }
 #endif  // HG_TL_KERNELS
 
+// the single pass's messages (per range, in record order, klo = index in the range): one warp per
+// range writes the mux keys (stream << 40 | range_base + index: the record's index in its stream)
+// back into the items and appends keys + item indices at the range's offset rpre[r], so every
+// stream's ranges form one sorted run; blocks past the ranges copy compose's messages like
+// tl_compact_kernel and write the run offsets
+#ifdef HG_TL_KERNELS
+__global__ void __launch_bounds__(kSortThreads) tl_range_compact_kernel(
+    TlItem* items, uint32_t n_ranges, uint32_t rcap, const uint32_t* rn, const uint32_t* rpre,
+    const uint32_t* range_stream, const unsigned long long* range_base, const uint32_t* stream_range0, uint32_t ns,
+    uint64_t comp_base, uint32_t ncomp, uint32_t nrec, ulonglong2* keys, uint32_t* idx, uint32_t* run_off) {
+  constexpr uint32_t kWarpsPerBlock = kSortThreads / 32;
+  const uint32_t nrb = (n_ranges + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const uint32_t lane = threadIdx.x & 31;
+  if (blockIdx.x < nrb) {
+    const uint32_t r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (r >= n_ranges) return;
+    const uint32_t cnt = rn[r], base = rpre[r];
+    const uint64_t hi = (uint64_t)range_stream[r] << 40, rb = range_base[r];
+    for (uint32_t j = lane; j < cnt; j += 32) {
+      const uint64_t g = (uint64_t)r * rcap + j;
+      const uint64_t khi = items[g].khi, klo = hi | (rb + items[g].klo);
+      items[g].klo = klo;
+      keys[base + j] = make_ulonglong2(khi, klo);
+      idx[base + j] = (uint32_t)g;
+    }
+    return;
+  }
+  const uint64_t c0 = (uint64_t)(blockIdx.x - nrb) * kSortTile;
+  for (uint32_t t = threadIdx.x; t < kSortTile; t += blockDim.x) {
+    const uint64_t c = c0 + t;
+    if (c < ncomp) {
+      const uint64_t g = comp_base + c;
+      keys[nrec + c] = make_ulonglong2(items[g].khi, items[g].klo);
+      idx[nrec + c] = (uint32_t)g;
+    }
+  }
+  if (blockIdx.x == nrb) {
+    for (uint32_t s = threadIdx.x; s < ns; s += blockDim.x) run_off[s] = rpre[stream_range0[s]];
+    const uint32_t ntc = (ncomp + kSortTile - 1) / kSortTile;
+    for (uint32_t c = threadIdx.x; c < ntc; c += blockDim.x) run_off[ns + c] = nrec + c * kSortTile;
+    if (threadIdx.x == 0) run_off[ns + ntc] = nrec + ncomp;
+  }
+}
+#endif  // HG_TL_KERNELS
+
 // one compose tile sorted in place (bitonic, 2048 keys); the last tile is padded with ~0 keys
 #ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kSortThreads) tl_tilesort_kernel(ulonglong2* keys, uint32_t* idx, uint32_t base,

@@ -115,3 +115,33 @@ def test_single_pass_small_ranges_on_random_traces(engine, seed, range_bytes):
         assert got.error is not None and str(got.error) == str(want.error)
         return
     assert got.error is None and got.report == want.report and got.stats == want.stats and got.orphans == want.orphans
+
+
+@pytest.mark.parametrize("range_bytes", [0, 112])
+@pytest.mark.parametrize("seed", list(range(120)))
+def test_single_pass_timeline_on_random_traces(engine, seed, range_bytes):
+    """Tally + timeline runs take the single pass (per-range messages, compose's cross-range spans
+    with the result bits of pending exits); 112-byte ranges split the streams into many ranges."""
+    from random_traces import random_trace
+
+    from oracle import oracle
+    from paper_2504_03683_b200.engine import OPT_RANGE_BYTES
+    from paper_2504_03683_b200.pipeline import merge_same_identity
+
+    ze, raws = random_trace(seed)
+    mine = merge_same_identity(raws)
+    infos = [r.info for r in mine]
+    want = oracle.run(mine, ze, infos, want_timeline=True)
+    engine.set_option(OPT_RANGE_BYTES, range_bytes)
+    try:
+        got = engine.run(mine, ze, infos, want_timeline=True)
+    finally:
+        engine.set_option(OPT_RANGE_BYTES, 0)
+    assert (got.error is None) == (want.error is None), (got.error, want.error)
+    if want.error is not None:
+        assert type(got.error) is type(want.error) and str(got.error) == str(want.error)
+        return
+    assert got.report == want.report and got.stats == want.stats and got.orphans == want.orphans
+    assert got.timeline == want.timeline.encode()
+    if range_bytes == 0:
+        assert engine.last_path()[0] == 1
