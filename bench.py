@@ -526,7 +526,9 @@ def timeline_side(eng, threads, config="c5", scale=1.0):
             "events_per_s": st["events_in"] / ((ph1 + ms) / 1e3),
             "roofline": {"bytes": in_bytes + len(tl), "achieved_gb_per_s": gbs, "frac": gbs / peak},
             "parity": "exact" if ok else "MISMATCH",
-            "path": "exact three-kernel phase 1 (record-indexed messages) + k-way merge of the per-stream runs by mux key + JSON formatting",
+            "path": ("single pass (fast_kernel<kTL>: per-range message lists)" if eng.last_path()[0] == 1 else
+                     "exact three-kernel phase 1 (record-indexed messages)") +
+                    " + k-way merge of the per-stream runs by mux key + JSON formatting",
             "checks": "object count = messages + metadata, json.dump framing, tally + IntervalStats == CPU oracle"}
 
 
