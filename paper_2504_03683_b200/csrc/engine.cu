@@ -817,10 +817,11 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;
-  // the single pass serves tally and timeline runs (event order, validation and a rank's share of a
-  // multi-rank timeline need record indices per slot: the exact path)
-  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_EVENTS | HG_WANT_VALIDATE | HG_WANT_TL_ITEMS)) &&
-              !((want & HG_WANT_TIMELINE) && getenv("HAPIGPU_TL_EXACT"));
+  // the single pass serves tally and timeline runs (event order and validation need a slot per
+  // record: the exact path)
+  const uint32_t tlw = want & (HG_WANT_TIMELINE | HG_WANT_TL_ITEMS);
+  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_EVENTS | HG_WANT_VALIDATE)) &&
+              !(tlw && getenv("HAPIGPU_TL_EXACT"));
   ctx->tl_ranges = false;
   bool retried = false;
   for (int attempt = 0; attempt < 9; attempt++) {
@@ -835,7 +836,7 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     int rc = ensure_scratch(ctx, 0);
     if (rc) return rc;
     ctx->tl_ranges = false;
-    if (fast && (want & HG_WANT_TIMELINE) && !tl_range_buffers(ctx)) fast = false;  // too large: the exact path
+    if (fast && tlw && !tl_range_buffers(ctx)) fast = false;  // too large: the exact path
     rc = fast ? launch_fast(ctx) : launch_phase1(ctx);
     if (rc) return rc;
     rc = read_counters(ctx);

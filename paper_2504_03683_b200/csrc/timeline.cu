@@ -164,6 +164,7 @@ int run_timeline_order(hg_ctx* ctx) {
   if (ctx->tl_comp_base + C[C_TL_N2] > ctx->tl_cap || ctx->tl_comp_base + C[C_TL_N2] >= (1ull << 32))
     return fail(ctx, HG_ENOMEM, "timeline message buffer overflow");
   const TlSource S = own_source(ctx);
+  if (S.ranges) return tl_sort_ranges(ctx, S, &ctx->tl_n, &ctx->tl_order);
   ctx->tl_n = S.n;
   return tl_sort_runs(ctx, S.items, S.nrec_slots, S.N, S.ncomp, S.n, S.rec_off, S.n_runs, &ctx->tl_order);
 }
