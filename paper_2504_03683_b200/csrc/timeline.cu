@@ -273,7 +273,7 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
   uint64_t total = 0;
   if (n) {
     const uint32_t g = std::min<uint32_t>((n + kTlTile - 1) / kTlTile, (uint32_t)ctx->sm_count * HG_TL_LEN_MINB * 2);
-    tl_len_kernel<<<g, kTlTile, 0, st>>>(T);
+    tl_len_kernel<<<g, kTlThreads, 0, st>>>(T);
     tl_meta_len_kernel<<<std::min<uint32_t>((n_proc + kThDirect + th_size + 255) / 256, (uint32_t)ctx->sm_count * 8), 256,
                          0, st>>>(T, n_proc, kThDirect + th_size);
     tl_scan(ctx, T.lens, n, T.offs, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
@@ -296,7 +296,7 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
     const uint32_t g = std::min<uint32_t>((n + kTlTile - 1) / kTlTile, (uint32_t)ctx->sm_count * HG_TL_WRITE_MINB);
     const size_t smem = tl_write_smem();
     CK(cudaFuncSetAttribute(tl_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    tl_write_kernel<<<g, kTlTile, smem, st>>>(T);
+    tl_write_kernel<<<g, kTlThreads, smem, st>>>(T);
     CK(cudaGetLastError());
     ctx->launches++;
   } else {

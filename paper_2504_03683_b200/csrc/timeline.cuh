@@ -842,11 +842,18 @@ __device__ __forceinline__ void tl_format(const TlTables& T, uint32_t i, const T
 
 // Items are formatted in CTA tiles of kTlTile consecutive sorted positions, gathered once into
 // shared memory and handed to the threads grouped by kind (host spans, device spans, samples), so
-// that a warp runs one kind's formatting code instead of all three.
+// that a warp runs one kind's formatting code instead of all three.  With kTlRounds > 1 every
+// thread formats kTlRounds items of the kind-sorted list, kTlThreads apart: a warp's rounds mix
+// cheap and costly kinds, which evens out the warps' times before the tile's barrier.
 #ifndef HG_TL_TILE
 #define HG_TL_TILE 128  // small tiles: the CTA barrier waits for its slowest item, more CTAs per SM hide that
 #endif
+#ifndef HG_TL_ROUNDS
+#define HG_TL_ROUNDS 1
+#endif
 constexpr int kTlTile = HG_TL_TILE;
+constexpr int kTlRounds = HG_TL_ROUNDS;
+constexpr int kTlThreads = kTlTile / kTlRounds;
 constexpr uint32_t kTlMeta = 1u << 31;  // lens[i] flag: the item carries metadata objects
 
 struct TlTileSmem {
@@ -855,58 +862,66 @@ struct TlTileSmem {
   uint32_t cur[4];
 };
 
-// gathers the tile's items and groups them by kind; returns this thread's tile position (or ~0)
+// gathers the tile's items and groups them by kind; returns the number of items in the tile
 __device__ __forceinline__ uint32_t tl_tile_group(const TlTables& T, uint64_t i0, TlTileSmem& S) {
-  const uint32_t t = threadIdx.x;
-  const uint64_t i = i0 + t;
-  const bool on = i < T.n;
-  uint32_t kind = 3;
-  if (on) {
-    const TlItem it = T.items[T.order[i]];
-    S.it[t] = it;
-    kind = it.kind & 3u;
-#ifndef HG_TL_NO_PREFETCH
-    if (kind != TL_HOST)  // the payload's first line: on its way while the tile is grouped
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(it.a));
-#endif
+  const uint32_t t = threadIdx.x, lane = t & 31;
+  uint32_t kind[kTlRounds];
+  #pragma unroll
+  for (int r = 0; r < kTlRounds; r++) {
+    const uint32_t q = t + r * kTlThreads;
+    kind[r] = 3;
+    if (i0 + q < T.n) {
+      const TlItem it = T.items[T.order[i0 + q]];
+      S.it[q] = it;
+      kind[r] = it.kind & 3u;
+    }
   }
   if (t < 4) S.cur[t] = 0;
   __syncthreads();
-  uint32_t pos = 0;
-  const uint32_t lane = t & 31;
+  uint32_t pos[kTlRounds];
   #pragma unroll
-  for (uint32_t k = 0; k < 3; k++) {
-    const uint32_t m = __ballot_sync(0xffffffffu, kind == k);
-    if (m) {
-      const uint32_t leader = __ffs(m) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(&S.cur[k], (uint32_t)__popc(m));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if (kind == k) pos = base + __popc(m & ((1u << lane) - 1u));
+  for (int r = 0; r < kTlRounds; r++) {
+    pos[r] = 0;
+    #pragma unroll
+    for (uint32_t k = 0; k < 3; k++) {
+      const uint32_t m = __ballot_sync(0xffffffffu, kind[r] == k);
+      if (m) {
+        const uint32_t leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&S.cur[k], (uint32_t)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (kind[r] == k) pos[r] = base + __popc(m & ((1u << lane) - 1u));
+      }
     }
   }
   __syncthreads();
-  if (on) {
-    const uint32_t n0 = S.cur[0], n1 = S.cur[1];
-    S.list[kind == 0 ? pos : kind == 1 ? n0 + pos : n0 + n1 + pos] = (uint16_t)t;
-  }
-  const uint32_t cnt = S.cur[0] + S.cur[1] + S.cur[2];
+  const uint32_t n0 = S.cur[0], n1 = S.cur[1];
+  #pragma unroll
+  for (int r = 0; r < kTlRounds; r++)
+    if (kind[r] < 3) S.list[kind[r] == 0 ? pos[r] : kind[r] == 1 ? n0 + pos[r] : n0 + n1 + pos[r]] =
+        (uint16_t)(t + r * kTlThreads);
+  const uint32_t cnt = n0 + n1 + S.cur[2];
   __syncthreads();
-  return t < cnt ? S.list[t] : 0xffffffffu;
+  return cnt;
 }
 
 #ifndef HG_TL_LEN_MINB
-#define HG_TL_LEN_MINB (1280 / HG_TL_TILE)  // 48 registers: 1.26 -> 1.05 ms at C5 x0.25 (vs 80)
+#define HG_TL_LEN_MINB (1280 / kTlThreads)  // 48 registers: 1.26 -> 1.05 ms at C5 x0.25 (vs 80)
 #endif
 #ifdef HG_TL_KERNELS
-__global__ void __launch_bounds__(kTlTile, HG_TL_LEN_MINB) tl_len_kernel(TlTables T) {
+__global__ void __launch_bounds__(kTlThreads, HG_TL_LEN_MINB) tl_len_kernel(TlTables T) {
   __shared__ TlTileSmem S;
   for (uint64_t i0 = (uint64_t)blockIdx.x * kTlTile; i0 < T.n; i0 += (uint64_t)gridDim.x * kTlTile) {
-    const uint32_t j = tl_tile_group(T, i0, S);
-    if (j != 0xffffffffu) {
-      TC w{0};
-      tl_format<TC, true>(T, (uint32_t)(i0 + j), S.it[j], w);
-      T.lens[i0 + j] = (uint32_t)w.n;
+    const uint32_t cnt = tl_tile_group(T, i0, S);
+    #pragma unroll
+    for (int r = 0; r < kTlRounds; r++) {
+      const uint32_t q = threadIdx.x + r * kTlThreads;
+      if (q < cnt) {
+        const uint32_t j = S.list[q];
+        TC w{0};
+        tl_format<TC, true>(T, (uint32_t)(i0 + j), S.it[j], w);
+        T.lens[i0 + j] = (uint32_t)w.n;
+      }
     }
     __syncthreads();
   }
@@ -1007,38 +1022,50 @@ struct TlWriteSmem {
 inline size_t tl_write_smem() { return sizeof(TlWriteSmem); }
 
 #ifndef HG_TL_WRITE_MINB
-#define HG_TL_WRITE_MINB (768 / HG_TL_TILE)
+#define HG_TL_WRITE_MINB (768 / kTlThreads)
 #endif
 #ifdef HG_TL_KERNELS
-__global__ void __launch_bounds__(kTlTile, HG_TL_WRITE_MINB) tl_write_kernel(TlTables T) {
+__global__ void __launch_bounds__(kTlThreads, HG_TL_WRITE_MINB) tl_write_kernel(TlTables T) {
   extern __shared__ __align__(16) char tl_smem[];
   TlWriteSmem& S = *reinterpret_cast<TlWriteSmem*>(tl_smem);
   const uint32_t t = threadIdx.x;
   for (uint64_t i0 = (uint64_t)blockIdx.x * kTlTile; i0 < T.n; i0 += (uint64_t)gridDim.x * kTlTile) {
-    const uint64_t i = i0 + t;
     const uint64_t last = min((uint64_t)T.n, i0 + kTlTile) - 1;
-    uint64_t off = 0;
-    uint32_t len = 0;
-    if (i <= last) {
-      off = 1 + T.offs[i];
-      len = T.lens[i];
-      if (t == 0) S.o0 = off;
-      if (i == last) S.oend = off + (len & ~kTlMeta);
+    uint64_t off[kTlRounds];
+    uint32_t len[kTlRounds];
+    #pragma unroll
+    for (int r = 0; r < kTlRounds; r++) {
+      const uint64_t i = i0 + t + r * kTlThreads;
+      off[r] = 0;
+      len[r] = 0;
+      if (i <= last) {
+        off[r] = 1 + T.offs[i];
+        len[r] = T.lens[i];
+        if (i == i0) S.o0 = off[r];
+        if (i == last) S.oend = off[r] + (len[r] & ~kTlMeta);
+      }
     }
-    const uint32_t j = tl_tile_group(T, i0, S.g);  // (its barriers publish o0 / oend)
+    const uint32_t cnt = tl_tile_group(T, i0, S.g);  // (its barriers publish o0 / oend)
     const uint64_t al = S.o0 & ~15ull, total = S.oend - al;
     const bool staged = total <= (uint64_t)kTlStage;
-    if (i <= last) S.rel[t] = (uint32_t)(off - al) | (len & kTlMeta);
+    #pragma unroll
+    for (int r = 0; r < kTlRounds; r++)
+      if (i0 + t + r * kTlThreads <= last) S.rel[t + r * kTlThreads] = (uint32_t)(off[r] - al) | (len[r] & kTlMeta);
     __syncthreads();
-    if (j != 0xffffffffu) {
-      const uint32_t r = S.rel[j];
-      const uint64_t gi = i0 + j;
-      if (staged) {
-        TW w{S.stage + (r & ~kTlMeta), 0};
-        tl_format(T, (uint32_t)gi, S.g.it[j], w, (r & kTlMeta) != 0);
-      } else {
-        TW w{T.out + al + (r & ~kTlMeta), 0};
-        tl_format(T, (uint32_t)gi, S.g.it[j], w, (r & kTlMeta) != 0);
+    #pragma unroll
+    for (int r = 0; r < kTlRounds; r++) {
+      const uint32_t q = t + r * kTlThreads;
+      if (q < cnt) {
+        const uint32_t j = S.g.list[q];
+        const uint32_t rl = S.rel[j];
+        const uint64_t gi = i0 + j;
+        if (staged) {
+          TW w{S.stage + (rl & ~kTlMeta), 0};
+          tl_format(T, (uint32_t)gi, S.g.it[j], w, (rl & kTlMeta) != 0);
+        } else {
+          TW w{T.out + al + (rl & ~kTlMeta), 0};
+          tl_format(T, (uint32_t)gi, S.g.it[j], w, (rl & kTlMeta) != 0);
+        }
       }
     }
     __syncthreads();
@@ -1046,7 +1073,7 @@ __global__ void __launch_bounds__(kTlTile, HG_TL_WRITE_MINB) tl_write_kernel(TlT
       char* gout = T.out + al;
       const uint32_t head = (uint32_t)(S.o0 - al), end = (uint32_t)total;
       const uint32_t full_end = end & ~15u;
-      for (uint32_t b0 = 16u * t + (head ? 16u : 0u); b0 < full_end; b0 += 16u * kTlTile)
+      for (uint32_t b0 = 16u * t + (head ? 16u : 0u); b0 < full_end; b0 += 16u * kTlThreads)
         *reinterpret_cast<uint4*>(gout + b0) = *reinterpret_cast<const uint4*>(S.stage + b0);
       if (t < 16) {  // the partial first and last chunks, a byte per thread
         if (head && head + t < 16u && head + t < end) gout[head + t] = S.stage[head + t];
