@@ -294,7 +294,11 @@ int timeline_from(hg_ctx* ctx, const TlSource& S, uint64_t global_last_ts) {
     CK(cudaMemcpyAsync(T.out, open_close, 1, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(T.out + 1 + total, open_close + 1, 2, cudaMemcpyHostToDevice, st));
     const uint32_t g = std::min<uint32_t>((n + kTlTile - 1) / kTlTile, (uint32_t)ctx->sm_count * HG_TL_WRITE_MINB);
-    const size_t smem = tl_write_smem();
+    // staging: 1/16 above the tile's average bytes (about 4 standard deviations of a 128-object
+    // tile), 16-byte granular; the kernel's 8 CTAs per SM fit while objects average below ~165 bytes
+    const uint64_t avg_tile = (total + n - 1) / n * kTlTile;
+    T.stage_cap = (uint32_t)std::min<uint64_t>(((avg_tile + avg_tile / 16) + 15) & ~15ull, 160u * 1024u);
+    const size_t smem = tl_write_smem(T.stage_cap);
     CK(cudaFuncSetAttribute(tl_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     tl_write_kernel<<<g, kTlThreads, smem, st>>>(T);
     CK(cudaGetLastError());

@@ -53,6 +53,7 @@ struct TlTables {
   uint32_t* lens;
   uint64_t* offs;
   char* out;                      // output buffer; item text starts at 1 + offs[i]
+  uint32_t stage_cap;             // tl_write_kernel: staging bytes per tile
 };
 
 // ---------------------------------------------------------------------------
@@ -1010,19 +1011,21 @@ __global__ void __launch_bounds__(kScanBlock) tl_scan3_kernel(const uint32_t* le
 // writer: a CTA formats a tile of items (grouped by kind) into a shared staging buffer at their
 // offsets, then stores the tile's contiguous byte range with aligned 16-byte writes
 
-constexpr uint32_t kTlStage = kTlTile * 224;  // objects average ~160 bytes; larger tiles are written directly
+// The staging buffer is sized at launch from this timeline's average object length (TlTables::
+// stage_cap, 1/16 above kTlTile x the average: a tile rarely exceeds it, and one that does is
+// written straight to HBM) -- as small as the objects allow, for 8 CTAs per SM.
 
 struct TlWriteSmem {
   TlTileSmem g;
   uint32_t rel[kTlTile];    // offset of the item's text in the staging buffer
   uint64_t o0, oend;
-  __align__(16) char stage[kTlStage + 16];
+  __align__(16) char stage[16];  // stage_cap + 16 bytes (dynamic shared memory)
 };
 
-inline size_t tl_write_smem() { return sizeof(TlWriteSmem); }
+inline size_t tl_write_smem(uint32_t stage_cap) { return sizeof(TlWriteSmem) + stage_cap; }
 
 #ifndef HG_TL_WRITE_MINB
-#define HG_TL_WRITE_MINB (768 / kTlThreads)
+#define HG_TL_WRITE_MINB (1024 / kTlThreads)  // 64 registers: 8 CTAs per SM (3.25 -> 2.81 ms at C5 x0.25 vs 6)
 #endif
 #ifdef HG_TL_KERNELS
 __global__ void __launch_bounds__(kTlThreads, HG_TL_WRITE_MINB) tl_write_kernel(TlTables T) {
@@ -1047,7 +1050,7 @@ __global__ void __launch_bounds__(kTlThreads, HG_TL_WRITE_MINB) tl_write_kernel(
     }
     const uint32_t cnt = tl_tile_group(T, i0, S.g);  // (its barriers publish o0 / oend)
     const uint64_t al = S.o0 & ~15ull, total = S.oend - al;
-    const bool staged = total <= (uint64_t)kTlStage;
+    const bool staged = total <= (uint64_t)T.stage_cap;
     #pragma unroll
     for (int r = 0; r < kTlRounds; r++)
       if (i0 + t + r * kTlThreads <= last) S.rel[t + r * kTlThreads] = (uint32_t)(off[r] - al) | (len[r] & kTlMeta);
