@@ -34,6 +34,7 @@ struct EvTables {
   uint32_t* lens;
   const uint64_t* offs;
   char* out;
+  uint32_t stage_cap;  // ev_write_kernel: staging bytes per tile
 };
 
 __global__ void __launch_bounds__(256) ev_index_kernel(const SegInfo* info, const uint32_t* tile_stream, uint32_t n_tiles,
@@ -99,8 +100,7 @@ __device__ __forceinline__ void w_repr(W& w, uint64_t bits) {
 }
 
 template <class W>
-__device__ void ev_line(const EvTables& T, uint32_t i, W& w) {
-  const TlItem it = T.items[T.order[i]];
+__device__ void ev_line(const EvTables& T, const TlItem& it, W& w) {
   const uint32_t s = (uint32_t)(it.klo >> 40);
   const int32_t si = T.sid_map[it.x];
   const DSchema& sc = T.schemas[si];
@@ -161,15 +161,54 @@ __device__ void ev_line(const EvTables& T, uint32_t i, W& w) {
 __global__ void __launch_bounds__(256) ev_len_kernel(EvTables T) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += gridDim.x * blockDim.x) {
     TC c{0};
-    ev_line(T, i, c);
+    ev_line(T, T.items[T.order[i]], c);
     T.lens[i] = (uint32_t)c.n;
   }
 }
 
-__global__ void __launch_bounds__(256) ev_write_kernel(EvTables T) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += gridDim.x * blockDim.x) {
-    TW w{T.out + T.offs[i], 0};
-    ev_line(T, i, w);
+// a CTA formats kEvTile consecutive lines into a shared staging buffer at their offsets and stores
+// the tile's byte window with aligned 16-byte writes (tiles beyond the buffer write straight to HBM)
+constexpr uint32_t kEvTile = 128;
+struct EvWriteSmem {
+  uint64_t o0, oend;
+  __align__(16) char stage[16];  // stage_cap + 16 bytes (dynamic shared memory)
+};
+
+__global__ void __launch_bounds__(kEvTile, 8) ev_write_kernel(EvTables T) {
+  extern __shared__ __align__(16) char ev_smem[];
+  EvWriteSmem& S = *reinterpret_cast<EvWriteSmem*>(ev_smem);
+  const uint32_t t = threadIdx.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kEvTile; i0 < T.n; i0 += (uint64_t)gridDim.x * kEvTile) {
+    const uint64_t i = i0 + t, last = min((uint64_t)T.n, i0 + kEvTile) - 1;
+    uint64_t off = 0;
+    TlItem it;
+    if (i <= last) {
+      it = T.items[T.order[i]];
+      off = T.offs[i];
+      if (i == i0) S.o0 = off;
+      if (i == last) S.oend = off + T.lens[i];
+    }
+    __syncthreads();
+    const uint64_t al = S.o0 & ~15ull, total = S.oend - al;
+    const bool staged = total <= (uint64_t)T.stage_cap;
+    if (i <= last) {
+      TW w{staged ? S.stage + (off - al) : T.out + off, 0};
+      ev_line(T, it, w);
+    }
+    __syncthreads();
+    if (staged) {  // bytes [head, end) of the 16-byte aligned window at al
+      char* gout = T.out + al;
+      const uint32_t head = (uint32_t)(S.o0 - al), end = (uint32_t)total;
+      const uint32_t full_end = end & ~15u;
+      for (uint32_t b0 = 16u * t + (head ? 16u : 0u); b0 < full_end; b0 += 16u * kEvTile)
+        *reinterpret_cast<uint4*>(gout + b0) = *reinterpret_cast<const uint4*>(S.stage + b0);
+      if (t < 16) {  // the partial first and last chunks, a byte per thread
+        if (head && head + t < 16u && head + t < end) gout[head + t] = S.stage[head + t];
+        const uint32_t b = full_end + t;
+        if (b < end && (b >= 16u || !head)) gout[b] = S.stage[b];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -260,7 +299,13 @@ int run_events(hg_ctx* ctx) {
     bytes = tot;
     CK(ctx->d_ev_out.ensure(bytes + 32));
     T.out = ctx->d_ev_out.ptr;
-    ev_write_kernel<<<g, 256, 0, st>>>(T);
+    // staging: 1/16 above the tile's average bytes (16-byte granular)
+    const uint64_t avg_tile = (bytes + n - 1) / n * kEvTile;
+    T.stage_cap = (uint32_t)std::min<uint64_t>(((avg_tile + avg_tile / 16) + 15) & ~15ull, 160u * 1024u);
+    const size_t smem = sizeof(EvWriteSmem) + T.stage_cap;
+    CK(cudaFuncSetAttribute(ev_write_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint32_t gw = std::min<uint32_t>((n + kEvTile - 1) / kEvTile, (uint32_t)ctx->sm_count * 8);
+    ev_write_kernel<<<gw, kEvTile, smem, st>>>(T);
     CK(cudaGetLastError());
     ctx->launches++;
   }
