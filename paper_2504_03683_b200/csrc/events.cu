@@ -121,11 +121,22 @@ __device__ void ev_line(const EvTables& T, const TlItem& it, W& w) {
         const uint32_t len = ldu32(q);
         if (kind == HG_KIND_STRING) {
           json_str(w, q + 4, len);
-        } else {  // "[ " + ", ".join(str(b)) + " ]"
+        } else {  // "[ " + ", ".join(str(b)) + " ]": four bytes per load, a byte's digits by compares
           w.lit("[ ");
-          for (uint32_t j = 0; j < len; j++) {
-            if (j) w.lit(", ");
-            w_dec(w, q[4 + j]);
+          for (uint32_t j = 0; j < len; j += 4) {
+            const uint32_t word = ldu32(q + 4 + j);  // (the data array is padded past its last byte)
+            const uint32_t m = len - j < 4u ? len - j : 4u;
+            for (uint32_t k = 0; k < m; k++) {
+              if (j + k) w.lit(", ");
+              const uint32_t b = (word >> (8u * k)) & 255u;
+              if constexpr (W::kWrite) {
+                if (b >= 100u) w.c((char)('0' + b / 100u));
+                if (b >= 10u) w.c((char)('0' + b / 10u % 10u));
+                w.c((char)('0' + b % 10u));
+              } else {
+                w.s(nullptr, b >= 100u ? 3u : b >= 10u ? 2u : 1u);
+              }
+            }
           }
           w.lit(" ]");
         }
@@ -158,18 +169,59 @@ __device__ void ev_line(const EvTables& T, const TlItem& it, W& w) {
   w.c('\n');
 }
 
-__global__ void __launch_bounds__(256) ev_len_kernel(EvTables T) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < T.n; i += gridDim.x * blockDim.x) {
-    TC c{0};
-    ev_line(T, T.items[T.order[i]], c);
-    T.lens[i] = (uint32_t)c.n;
+// Lines are formatted in CTA tiles of kEvTile consecutive mux positions, handed to the threads in
+// schema order (a bitonic sort of (schema id, position) keys in shared memory): the lines of a
+// schema run the same field loop, so a warp's lanes stay together (7 of 32 active otherwise).
+constexpr uint32_t kEvTile = 128;
+
+struct EvTile {
+  TlItem it[kEvTile];
+  uint32_t key[kEvTile];  // schema id << 7 | tile position, ~0 past the end
+};
+
+// gathers the tile's items (thread t: position t) and sorts the keys; returns this thread's position or ~0
+__device__ __forceinline__ uint32_t ev_tile_sort(const EvTables& T, uint64_t i0, EvTile& S) {
+  const uint32_t t = threadIdx.x;
+  uint32_t key = 0xFFFFFFFFu;
+  if (i0 + t < T.n) {
+    const TlItem it = T.items[T.order[i0 + t]];
+    S.it[t] = it;
+    key = (it.x << 7) | t;
+  }
+  S.key[t] = key;
+  __syncthreads();
+  for (uint32_t k = 2; k <= kEvTile; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t u = t ^ j;
+      if (u > t) {
+        const uint32_t a = S.key[t], b = S.key[u];
+        if ((a > b) == ((t & k) == 0)) { S.key[t] = b; S.key[u] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  const uint32_t q = S.key[t];
+  return q == 0xFFFFFFFFu ? q : (q & (kEvTile - 1));
+}
+
+__global__ void __launch_bounds__(kEvTile, 8) ev_len_kernel(EvTables T) {
+  __shared__ EvTile S;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * kEvTile; i0 < T.n; i0 += (uint64_t)gridDim.x * kEvTile) {
+    const uint32_t j = ev_tile_sort(T, i0, S);
+    if (j != 0xFFFFFFFFu) {
+      TC c{0};
+      ev_line(T, S.it[j], c);
+      T.lens[i0 + j] = (uint32_t)c.n;
+    }
+    __syncthreads();
   }
 }
 
-// a CTA formats kEvTile consecutive lines into a shared staging buffer at their offsets and stores
-// the tile's byte window with aligned 16-byte writes (tiles beyond the buffer write straight to HBM)
-constexpr uint32_t kEvTile = 128;
+// a CTA formats its tile's lines into a shared staging buffer at their offsets and stores the
+// tile's byte window with aligned 16-byte writes (tiles beyond the buffer write straight to HBM)
 struct EvWriteSmem {
+  EvTile g;
+  uint64_t off[kEvTile];
   uint64_t o0, oend;
   __align__(16) char stage[16];  // stage_cap + 16 bytes (dynamic shared memory)
 };
@@ -180,20 +232,19 @@ __global__ void __launch_bounds__(kEvTile, 8) ev_write_kernel(EvTables T) {
   const uint32_t t = threadIdx.x;
   for (uint64_t i0 = (uint64_t)blockIdx.x * kEvTile; i0 < T.n; i0 += (uint64_t)gridDim.x * kEvTile) {
     const uint64_t i = i0 + t, last = min((uint64_t)T.n, i0 + kEvTile) - 1;
-    uint64_t off = 0;
-    TlItem it;
     if (i <= last) {
-      it = T.items[T.order[i]];
-      off = T.offs[i];
+      const uint64_t off = T.offs[i];
+      S.off[t] = off;
       if (i == i0) S.o0 = off;
       if (i == last) S.oend = off + T.lens[i];
     }
-    __syncthreads();
+    const uint32_t j = ev_tile_sort(T, i0, S.g);  // (its barriers publish off / o0 / oend)
     const uint64_t al = S.o0 & ~15ull, total = S.oend - al;
     const bool staged = total <= (uint64_t)T.stage_cap;
-    if (i <= last) {
+    if (j != 0xFFFFFFFFu) {
+      const uint64_t off = S.off[j];
       TW w{staged ? S.stage + (off - al) : T.out + off, 0};
-      ev_line(T, it, w);
+      ev_line(T, S.g.it[j], w);
     }
     __syncthreads();
     if (staged) {  // bytes [head, end) of the 16-byte aligned window at al
@@ -288,8 +339,8 @@ int run_events(hg_ctx* ctx) {
   T.offs = ctx->d_ev_offs.ptr;
   uint64_t bytes = 0;
   if (n) {
-    const uint32_t g = std::min<uint32_t>((n + 255) / 256, (uint32_t)ctx->sm_count * 16);
-    ev_len_kernel<<<g, 256, 0, st>>>(T);
+    const uint32_t g = std::min<uint32_t>((n + kEvTile - 1) / kEvTile, (uint32_t)ctx->sm_count * 8);
+    ev_len_kernel<<<g, kEvTile, 0, st>>>(T);
     rc = tl_scan(ctx, T.lens, n, ctx->d_ev_offs.ptr, reinterpret_cast<uint64_t*>(ctx->d_counters.ptr + C_TL_TOTAL));
     if (rc) return rc;
     ctx->launches++;
