@@ -157,6 +157,9 @@ struct hg_ctx {
   DBuf<uint32_t> d_tl_rn;          // messages per range
   DBuf<unsigned long long> d_tl_pres;  // result bits of the first pending exits per range
   DBuf<uint32_t> d_tl_rpre;        // exclusive scan of d_tl_rn
+  bool ev_ranges = false;          // the last event run's records are per range (d_ev_items, d_ev_rn)
+  DBuf<uint32_t> d_ev_rn;
+  DBuf<unsigned long long> d_ev_seq;  // hg_get_event_order scratch
   DBuf<ulonglong2> d_tl_keys[2];
   DBuf<uint32_t> d_tl_idx[2];
   DBuf<uint32_t> d_tl_ro[2], d_tl_tcnt, d_tl_tile0, d_tl_split;  // sort: run offsets, tile counts, merge splits

@@ -264,6 +264,7 @@ void hg_destroy(hg_ctx* ctx) {
   ctx->d_keys.release(); ctx->d_vals.release(); ctx->d_name_len.release(); ctx->d_small.release();
   ctx->d_name_off.release(); ctx->d_arena.release(); ctx->d_desc.release();
   ctx->d_tl_items.release(); ctx->d_tl_rn.release(); ctx->d_tl_pres.release(); ctx->d_tl_rpre.release();
+  ctx->d_ev_rn.release(); ctx->d_ev_seq.release();
   for (int k = 0; k < 2; k++) { ctx->d_tl_keys[k].release(); ctx->d_tl_idx[k].release(); ctx->d_tl_ro[k].release(); }
   ctx->d_tl_tcnt.release(); ctx->d_tl_tile0.release(); ctx->d_tl_split.release();
   ctx->d_tl_lens.release(); ctx->d_tl_stream_proc.release(); ctx->d_tl_offs.release(); ctx->d_tl_bsum.release();
@@ -731,6 +732,8 @@ Params make_params(hg_ctx* ctx) {
   p.tl_rcap = ctx->tl_rcap;
   p.tl_rn = ctx->tl_ranges ? ctx->d_tl_rn.ptr : nullptr;
   p.tl_pres = ctx->tl_ranges ? ctx->d_tl_pres.ptr : nullptr;
+  p.ev_ritems = ctx->ev_ranges ? ctx->d_ev_items.ptr : nullptr;
+  p.ev_rn = ctx->ev_ranges ? ctx->d_ev_rn.ptr : nullptr;
   p.seg_bytes = ctx->seg_bytes;
   p.deep = ctx->d_deep.ptr;
   p.deep_used = C + C_DEEP_USED;
@@ -810,6 +813,21 @@ static bool tl_range_buffers(hg_ctx* ctx) {
   return true;
 }
 
+// every record of the single pass for the event sinks: rcap slots per range
+static bool ev_range_buffers(hg_ctx* ctx) {
+  const uint64_t rcap = ctx->range_bytes / 16ull + 2;
+  const uint64_t cap = (uint64_t)ctx->n_ranges * rcap;
+  if (cap >= (1ull << 32)) return false;
+  if (ctx->d_ev_items.ensure(std::max<uint64_t>(cap, 1)) != cudaSuccess ||
+      ctx->d_ev_rn.ensure(std::max<uint32_t>(ctx->n_ranges, 1)) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  ctx->tl_rcap = (uint32_t)rcap;
+  ctx->ev_ranges = true;
+  return true;
+}
+
 int hg_run_local(hg_ctx* ctx, uint32_t want) {
   if (!ctx) return HG_EARG;
   cudaSetDevice(ctx->cfg.device);
@@ -817,12 +835,13 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;
-  // the single pass serves tally and timeline runs (event order and validation need a slot per
-  // record: the exact path)
+  // the single pass serves tally, timeline and event runs (per-range lists of the timeline's
+  // messages or of every record); a run that wants both lists takes the exact path
   const uint32_t tlw = want & (HG_WANT_TIMELINE | HG_WANT_TL_ITEMS);
-  bool fast = ctx->path_opt != 1 && !(want & (HG_WANT_EVENTS | HG_WANT_VALIDATE)) &&
-              !(tlw && getenv("HAPIGPU_TL_EXACT"));
+  const uint32_t evw = want & (HG_WANT_EVENTS | HG_WANT_VALIDATE);
+  bool fast = ctx->path_opt != 1 && !(tlw && evw) && !((tlw || evw) && getenv("HAPIGPU_TL_EXACT"));
   ctx->tl_ranges = false;
+  ctx->ev_ranges = false;
   bool retried = false;
   for (int attempt = 0; attempt < 9; attempt++) {
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
@@ -836,7 +855,9 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     int rc = ensure_scratch(ctx, 0);
     if (rc) return rc;
     ctx->tl_ranges = false;
+    ctx->ev_ranges = false;
     if (fast && tlw && !tl_range_buffers(ctx)) fast = false;  // too large: the exact path
+    if (fast && evw && !ev_range_buffers(ctx)) fast = false;
     rc = fast ? launch_fast(ctx) : launch_phase1(ctx);
     if (rc) return rc;
     rc = read_counters(ctx);
@@ -1058,6 +1079,7 @@ static int run_fused(hg_ctx* ctx, uint32_t want, bool& done) {
   done = false;
   ctx->want = want;
   ctx->tl_ranges = false;  // (a tally run: no timeline messages; the last timeline run's buffers are stale)
+  ctx->ev_ranges = false;
   ctx->have_results = false;
   ctx->merged = false;
   ctx->phase1_done = false;

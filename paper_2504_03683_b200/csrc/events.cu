@@ -263,6 +263,16 @@ __global__ void __launch_bounds__(kEvTile, 8) ev_write_kernel(EvTables T) {
   }
 }
 
+// (stream, record index) of every event in mux order
+__global__ void ev_order_kernel(const TlItem* items, const uint32_t* order, uint32_t n, uint32_t* stream,
+                                unsigned long long* seq) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t klo = items[order[i]].klo;
+    stream[i] = (uint32_t)(klo >> 40);
+    seq[i] = klo & ((1ull << 40) - 1);
+  }
+}
+
 static std::string py_str_int(bool none, int64_t v) { return none ? std::string("None") : std::to_string(v); }
 
 }  // namespace
@@ -270,7 +280,7 @@ static std::string py_str_int(bool none, int64_t v) { return none ? std::string(
 // after hg_finish: order every record by the muxer's key and render PrettyPrintSink's lines
 int run_events(hg_ctx* ctx) {
   ctx->ev_ready = false;
-  if (ctx->last_path != 0) return fail(ctx, HG_ESTATE, "event sinks need the exact phase-1 path");
+  if (ctx->last_path != 0 && !ctx->ev_ranges) return fail(ctx, HG_ESTATE, "event sinks: no record lists of the run");
   if (!ctx->have_schema_names) return fail(ctx, HG_ESTATE, "hg_set_schema_names is required for event sinks");
   cudaStream_t st = ctx->stream;
   const uint32_t ns = (uint32_t)ctx->streams.size();
@@ -281,8 +291,26 @@ int run_events(hg_ctx* ctx) {
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, st));
-  CK(ctx->d_ev_items.ensure(std::max<uint32_t>(n, 1)));
-  const uint32_t nt = (uint32_t)ctx->tile_stream.size();
+  const uint32_t* order = nullptr;
+  if (ctx->last_path == 1) {  // the single pass's per-range record lists: keys, then the merge passes
+    TlSource S;
+    S.ranges = true;
+    S.items = ctx->d_ev_items.ptr;
+    S.n_ranges = ctx->n_ranges;
+    S.rcap = ctx->tl_rcap;
+    S.rn = ctx->d_ev_rn.ptr;
+    S.range_stream = ctx->d_range_stream.ptr;
+    S.range_base = ctx->d_range_base.ptr;
+    S.stream_range0 = ctx->d_stream_range0.ptr;
+    S.nrec_slots = ctx->n_ranges * ctx->tl_rcap;
+    S.n_runs = ns;
+    uint32_t n2 = 0;
+    int rc = tl_sort_ranges(ctx, S, &n2, &order);
+    if (rc) return rc;
+    if (n2 != n) return fail(ctx, HG_ECUDA, "event sinks: record lists do not cover the run (engine bug)");
+  }
+  if (ctx->last_path == 0) CK(ctx->d_ev_items.ensure(std::max<uint32_t>(n, 1)));
+  const uint32_t nt = ctx->last_path == 0 ? (uint32_t)ctx->tile_stream.size() : 0u;
   if (nt) {
     ev_index_kernel<<<std::min<uint32_t>((nt + 255) / 256, (uint32_t)ctx->sm_count * 8), 256, 0, st>>>(
         ctx->d_seginfo.ptr, ctx->d_tile_stream.ptr, nt, ctx->d_data.ptr, ctx->d_base.ptr, ctx->d_tl_rec_off.ptr,
@@ -290,9 +318,11 @@ int run_events(hg_ctx* ctx) {
     CK(cudaGetLastError());
     ctx->launches++;
   }
-  const uint32_t* order = nullptr;
-  int rc = tl_sort(ctx, ctx->d_ev_items.ptr, n, n, 0, n, &order);
-  if (rc) return rc;
+  int rc = HG_OK;
+  if (ctx->last_path == 0) {
+    rc = tl_sort(ctx, ctx->d_ev_items.ptr, n, n, 0, n, &order);
+    if (rc) return rc;
+  }
   // host tables
   std::vector<char> spre, sname;
   std::vector<uint64_t> spre_off(1, 0), sname_off(1, 0);
@@ -409,16 +439,21 @@ int hg_get_event_order(hg_ctx* ctx, uint32_t* stream, uint64_t* seq, uint64_t ca
   *n = total;
   if (!stream && !seq) return HG_OK;
   if (cap < total) return fail(ctx, HG_EARG, "event order buffer too small");
-  std::vector<uint32_t> ord(total);
-  std::vector<TlItem> items(total);
-  if (total) {
-    CK(cudaMemcpy(ord.data(), ctx->ev_order, total * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(items.data(), ctx->d_ev_items.ptr, total * sizeof(TlItem), cudaMemcpyDeviceToHost));
-  }
+  if (!total) return HG_OK;
+  cudaSetDevice(ctx->cfg.device);
+  CK(ctx->d_ev_lens.ensure(total));  // (scratch: the line lengths are no longer needed)
+  CK(ctx->d_ev_seq.ensure(total));
+  ev_order_kernel<<<std::min<uint64_t>((total + 255) / 256, (uint64_t)ctx->sm_count * 8), 256, 0, ctx->stream>>>(
+      ctx->d_ev_items.ptr, ctx->ev_order, (uint32_t)total, ctx->d_ev_lens.ptr, ctx->d_ev_seq.ptr);
+  CK(cudaGetLastError());
+  std::vector<uint32_t> s32(total);
+  std::vector<unsigned long long> s64(total);
+  CK(cudaMemcpyAsync(s32.data(), ctx->d_ev_lens.ptr, total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(s64.data(), ctx->d_ev_seq.ptr, total * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   for (uint64_t i = 0; i < total; i++) {
-    const TlItem& it = items[ord[i]];
-    if (stream) stream[i] = (uint32_t)(it.klo >> 40);
-    if (seq) seq[i] = it.klo & ((1ull << 40) - 1);
+    if (stream) stream[i] = s32[i];
+    if (seq) seq[i] = s64[i];
   }
   return HG_OK;
 }

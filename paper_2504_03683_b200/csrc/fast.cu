@@ -14,12 +14,14 @@ int launch_fast(hg_ctx* ctx) {
   const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
   const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
   using K = void (*)(Params, const Params*);
-  static const K kerns[8] = {fast_kernel<false, false, false>, fast_kernel<false, true, false>,
-                             fast_kernel<true, false, false>,  fast_kernel<true, true, false>,
-                             fast_kernel<false, false, true>,  fast_kernel<false, true, true>,
-                             fast_kernel<true, false, true>,   fast_kernel<true, true, true>};
-  const bool tl = p.tl_ritems != nullptr;
-  const K kern = kerns[(tl ? 4 : 0) + (sd ? 2 : 0) + (ctx->deep_inline ? 1 : 0)];
+  static const K kerns[12] = {fast_kernel<false, false, 0>, fast_kernel<false, true, 0>,
+                              fast_kernel<true, false, 0>,  fast_kernel<true, true, 0>,
+                              fast_kernel<false, false, 1>, fast_kernel<false, true, 1>,
+                              fast_kernel<true, false, 1>,  fast_kernel<true, true, 1>,
+                              fast_kernel<false, false, 2>, fast_kernel<false, true, 2>,
+                              fast_kernel<true, false, 2>,  fast_kernel<true, true, 2>};
+  const int mode = p.tl_ritems ? 1 : p.ev_ritems ? 2 : 0;
+  const K kern = kerns[4 * mode + (sd ? 2 : 0) + (ctx->deep_inline ? 1 : 0)];
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint32_t per_cta = nw * kWarp;
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));

@@ -152,6 +152,15 @@ struct RLane {
   bool fresh;           // no requests until every pending fill of this lane completed (slot reuse)
 };
 
+// one record of the lane's range for the event sinks: slot k of the range (its index in the range);
+// a = the record's offset in the data array (ev_line)
+__device__ __forceinline__ void r_event(const Params& p, const RLane& R, uint32_t k, uint64_t ts, uint64_t o,
+                                        uint32_t sid) {
+  TlItem it;
+  it.khi = ts; it.klo = k; it.a = (uint64_t)(R.g - p.data) + o; it.b = 0; it.kind = 0; it.x = sid;
+  p.ev_ritems[(uint64_t)R.r * p.tl_rcap + k] = it;
+}
+
 // one timeline message of the lane's range, in record order (k: the record's index in the range)
 __device__ __forceinline__ void r_item(const Params& p, RLane& R, uint64_t khi, uint64_t k, uint64_t a, uint64_t b,
                                        uint32_t kind, uint32_t x) {
@@ -200,6 +209,7 @@ __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, u
       st.n = 0; st.np = 0; st.ne = 0; st.pad = 0;
       p.rstate[r] = st;
       if (p.tl_rn) p.tl_rn[r] = 0;
+      if (p.ev_rn) p.ev_rn[r] = 0;
       continue;
     }
     R.C0 = entry & ~(uint64_t)(kRChunk - 1);
@@ -278,6 +288,7 @@ __device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T)
   st.n = R.n; st.np = R.np; st.ne = R.ne; st.pad = 0;
   p.rstate[R.r] = st;
   if (p.tl_rn) p.tl_rn[R.r] = R.ti;
+  if (p.ev_rn) p.ev_rn[R.r] = R.n;
   if (R.spans) atomicAdd(&p.stream_spans[R.s], (unsigned long long)R.spans);
   if (R.bad) atomicOr(p.anom, 1u);   // anomaly reasons (bits): 1 record, 2 drain, 4 string, 8 chain, 16 order
 }
@@ -331,6 +342,7 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
   if (!k) R.first_ts = h.ts;
   R.prev_ts = h.ts;
   R.o = (uint32_t)(a + L);
+  if (p.ev_ritems) r_event(p, R, k, h.ts, a, h.sid);
   if (dt) {
     if (cls == HG_CLASS_DEVICE) R.spans++;  // a device span's identity (sinks.py:240-242)
     if (p.tl_ritems) r_item(p, R, h.ts, k, reinterpret_cast<uint64_t>(R.g + a + 16), 0,
@@ -675,9 +687,10 @@ static __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, 
 
 // kSD: the registry's inline descriptors fit in shared memory (max_sid < kSdescMax);
 // kDeep: stacks deeper than kRLS stay on the inline path (overflow chunk) -- chosen by the host
-// once a run of the trace needed overflow chunks; kTL: a timeline run (every host span, device
-// span and sample also leaves a message in its range's list, r_item)
-template <bool kSD, bool kDeep, bool kTL>
+// once a run of the trace needed overflow chunks; kMode: 1 a timeline run (every host span, device
+// span and sample also leaves a message in its range's list, r_item), 2 an event run (every
+// record, r_event)
+template <bool kSD, bool kDeep, int kMode>
 __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const Params* gp) {
   const Params& gpr = *gp;
   const uint32_t nw = blockDim.x >> 5;
@@ -806,6 +819,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const uint64_t res = (D.x & FD_RES) ? ((uint64_t)__funnelshift_r(w5, w6, sh) << 32) | __funnelshift_r(w4, w5, sh) : 0ull;
     const bool err = res != 0;
     if (fast) {
+      if (kMode == 2) r_event(p, R, R.n, ts, o_start, sid);
       R.first_ts = R.n ? R.first_ts : ts;
       R.n++;
       R.prev_ts = ts;
@@ -824,9 +838,9 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       T.pd_ts[i] = ts;
       T.pd_meta[i] = fnm | ((1u | (err ? 2u : 0u) | (((D.x >> 26) & 3u) << 4)) << 19);
       T.pd_k[i] = R.n - 1;
-      if (kTL) p.tl_pres[(uint64_t)R.r * kRLP + np] = res;
+      if (kMode == 1) p.tl_pres[(uint64_t)R.r * kRLP + np] = res;
     }
-    if (kTL) {
+    if (kMode == 1) {
       if (fXp) r_item(p, R, ts, R.n - 1, ets, res, TL_HOST | (((D.x >> 26) & 3u) << 4), fnm);
       if (qflag) r_item(p, R, ts, R.n - 1, reinterpret_cast<uint64_t>(R.g + o_start + 16u), 0,
                         (D.x & FD_ISDEV) ? TL_DEVICE : TL_SAMPLE, sid);

@@ -103,6 +103,10 @@ struct Params {
   uint32_t tl_rcap;
   uint32_t* tl_rn;
   unsigned long long* tl_pres;
+  // every record of the single pass for event sinks (nullptr unless an event run takes it): range
+  // r's records at ev_ritems[r * tl_rcap + k] (k: index in the range), ev_rn[r] of them
+  TlItem* ev_ritems;
+  uint32_t* ev_rn;
   // segments
   uint32_t seg_bytes;
   SumEntry* deep;                  // per-lane automaton chunks of deep segments

@@ -145,3 +145,56 @@ def test_single_pass_timeline_on_random_traces(engine, seed, range_bytes):
     assert got.timeline == want.timeline.encode()
     if range_bytes == 0:
         assert engine.last_path()[0] == 1
+
+
+@pytest.mark.parametrize("range_bytes", [0, 112])
+@pytest.mark.parametrize("seed", list(range(100)))
+def test_single_pass_events_on_random_traces(engine, seed, range_bytes):
+    """PrettyPrintSink + ValidationSink runs (no timeline) take the single pass: every record in its
+    range's list, then the muxer's order by the merge passes."""
+    from random_traces import random_trace
+
+    from oracle import oracle
+    from paper_2504_03683_b200 import PrettyPrintSink, TallySink, ValidationRules, ValidationSink, run_pipeline
+    from paper_2504_03683_b200.engine import OPT_RANGE_BYTES
+    from paper_2504_03683_b200.pipeline import Sink, merge_same_identity
+
+    ze, raws = random_trace(seed)
+
+    class Src:
+        registry = ze
+
+        def raw_streams(self):
+            return raws
+
+        def stream_infos(self):
+            return [r.info for r in raws]
+
+    class Diag(Sink):
+        name = "diag"
+
+        def on_diagnostics(self, orphans):
+            self.orphans = orphans
+
+    rules = ValidationRules.from_dict(RULES)
+    mine = merge_same_identity(raws)
+    want = oracle.run(mine, ze, [r.info for r in raws])
+    diag = Diag()
+    sinks = [TallySink(), PrettyPrintSink(), ValidationSink(rules=rules), diag]
+    engine.set_option(OPT_RANGE_BYTES, range_bytes)
+    try:
+        if want.error is not None:
+            with pytest.raises(Exception) as ei:
+                run_pipeline(Src(), sinks, engine=engine)
+            assert type(ei.value).__name__ == type(want.error).__name__ and str(ei.value) == str(want.error)
+            assert diag.orphans == want.orphans
+            return
+        res = run_pipeline(Src(), sinks, engine=engine)
+    finally:
+        engine.set_option(OPT_RANGE_BYTES, 0)
+    assert res["tally"] == want.report and vars(res.stats) == want.stats and res.orphans == want.orphans
+    assert res["pretty"] == oracle.pretty(mine, ze)
+    findings = oracle.validate(mine, ze, rules, want.orphans)
+    assert [tuple(vars(f).values()) for f in res["validate"]] == [tuple(f) for f in findings]
+    if range_bytes == 0:
+        assert engine.last_path()[0] == 1
