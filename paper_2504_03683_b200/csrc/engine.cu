@@ -836,10 +836,10 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
   ctx->merged = false;
   ctx->phase1_done = false;
   // the single pass serves tally, timeline and event runs (per-range lists of the timeline's
-  // messages or of every record); a run that wants both lists takes the exact path
+  // messages and / or of every record)
   const uint32_t tlw = want & (HG_WANT_TIMELINE | HG_WANT_TL_ITEMS);
   const uint32_t evw = want & (HG_WANT_EVENTS | HG_WANT_VALIDATE);
-  bool fast = ctx->path_opt != 1 && !(tlw && evw) && !((tlw || evw) && getenv("HAPIGPU_TL_EXACT"));
+  bool fast = ctx->path_opt != 1 && !((tlw || evw) && getenv("HAPIGPU_TL_EXACT"));
   ctx->tl_ranges = false;
   ctx->ev_ranges = false;
   bool retried = false;

@@ -14,13 +14,15 @@ int launch_fast(hg_ctx* ctx) {
   const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
   const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
   using K = void (*)(Params, const Params*);
-  static const K kerns[12] = {fast_kernel<false, false, 0>, fast_kernel<false, true, 0>,
+  static const K kerns[16] = {fast_kernel<false, false, 0>, fast_kernel<false, true, 0>,
                               fast_kernel<true, false, 0>,  fast_kernel<true, true, 0>,
                               fast_kernel<false, false, 1>, fast_kernel<false, true, 1>,
                               fast_kernel<true, false, 1>,  fast_kernel<true, true, 1>,
                               fast_kernel<false, false, 2>, fast_kernel<false, true, 2>,
-                              fast_kernel<true, false, 2>,  fast_kernel<true, true, 2>};
-  const int mode = p.tl_ritems ? 1 : p.ev_ritems ? 2 : 0;
+                              fast_kernel<true, false, 2>,  fast_kernel<true, true, 2>,
+                              fast_kernel<false, false, 3>, fast_kernel<false, true, 3>,
+                              fast_kernel<true, false, 3>,  fast_kernel<true, true, 3>};
+  const int mode = (p.tl_ritems ? 1 : 0) | (p.ev_ritems ? 2 : 0);
   const K kern = kerns[4 * mode + (sd ? 2 : 0) + (ctx->deep_inline ? 1 : 0)];
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint32_t per_cta = nw * kWarp;

@@ -687,9 +687,9 @@ static __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, 
 
 // kSD: the registry's inline descriptors fit in shared memory (max_sid < kSdescMax);
 // kDeep: stacks deeper than kRLS stay on the inline path (overflow chunk) -- chosen by the host
-// once a run of the trace needed overflow chunks; kMode: 1 a timeline run (every host span, device
-// span and sample also leaves a message in its range's list, r_item), 2 an event run (every
-// record, r_event)
+// once a run of the trace needed overflow chunks; kMode bits: 1 a timeline run (every host span,
+// device span and sample also leaves a message in its range's list, r_item), 2 an event run
+// (every record, r_event)
 template <bool kSD, bool kDeep, int kMode>
 __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const Params* gp) {
   const Params& gpr = *gp;
@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const uint64_t res = (D.x & FD_RES) ? ((uint64_t)__funnelshift_r(w5, w6, sh) << 32) | __funnelshift_r(w4, w5, sh) : 0ull;
     const bool err = res != 0;
     if (fast) {
-      if (kMode == 2) r_event(p, R, R.n, ts, o_start, sid);
+      if (kMode & 2) r_event(p, R, R.n, ts, o_start, sid);
       R.first_ts = R.n ? R.first_ts : ts;
       R.n++;
       R.prev_ts = ts;
@@ -838,9 +838,9 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       T.pd_ts[i] = ts;
       T.pd_meta[i] = fnm | ((1u | (err ? 2u : 0u) | (((D.x >> 26) & 3u) << 4)) << 19);
       T.pd_k[i] = R.n - 1;
-      if (kMode == 1) p.tl_pres[(uint64_t)R.r * kRLP + np] = res;
+      if (kMode & 1) p.tl_pres[(uint64_t)R.r * kRLP + np] = res;
     }
-    if (kMode == 1) {
+    if (kMode & 1) {
       if (fXp) r_item(p, R, ts, R.n - 1, ets, res, TL_HOST | (((D.x >> 26) & 3u) << 4), fnm);
       if (qflag) r_item(p, R, ts, R.n - 1, reinterpret_cast<uint64_t>(R.g + o_start + 16u), 0,
                         (D.x & FD_ISDEV) ? TL_DEVICE : TL_SAMPLE, sid);
