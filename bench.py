@@ -532,7 +532,7 @@ def timeline_side(eng, threads, config="c5", scale=1.0):
             "checks": "object count = messages + metadata, json.dump framing, tally + IntervalStats == CPU oracle"}
 
 
-def configs_side(eng, threads, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 0.25), ("c5", 0.25))):
+def configs_side(eng, threads, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 1.0), ("c5", 1.0))):
     """The other SURVEY.md §8(d) shapes (tally, device-resident, single pass unless it falls back):
     phase-1 device time and events/s at a bounded scale each, and the tally + IntervalStats of the
     last run against the CPU oracle over the same streams."""
@@ -559,8 +559,10 @@ def configs_side(eng, threads, plan=(("c1", 1.0), ("c3", 0.1), ("c4", 0.25), ("c
                            [(r.hostname, r.pid, r.tid) for r in raws], eng.stream_spans())
         want, _ = oracle_check(raws, wl.registry, threads)
         d = statistics.mean(ms)
+        nb = sum(len(r.data) for r in raws)
         out.append({"config": name, "scale": scale, "events": st["events_in"], "streams": len(raws),
-                    "bytes": sum(len(r.data) for r in raws), "device_ms": d, "events_per_s": st["events_in"] / (d / 1e3),
+                    "bytes": nb, "device_ms": d, "events_per_s": st["events_in"] / (d / 1e3),
+                    "roofline_frac": nb / (d / 1e3) / 1e9 / _peaks()[0],
                     "path": "single pass" if path == 1 else "exact", "range_bytes": rb,
                     "parity": _parity_line(rep, st, want.report, want.stats)})
     return out

@@ -199,6 +199,8 @@ struct hg_ctx {
   std::vector<uint32_t> vplan;
   DBuf<uint32_t> d_vplan;
   std::vector<uint4> fdesc, dplan;
+  bool has_dev = true;
+  int desc_mode = 0;                // fast_kernel descriptors: 0 global (L1), 1 shared uint4, 2 shared compact              // some schema is device-profiling (the range kernel's name cache)
   DBuf<uint4> d_fdesc, d_dplan;
   int last_path = 0;                // 1 = the last run's phase 1 was the single pass
   uint64_t fallbacks = 0;

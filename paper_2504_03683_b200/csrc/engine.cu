@@ -424,6 +424,8 @@ int hg_set_registry(hg_ctx* ctx, const hg_schema* schemas, uint32_t n_schemas, c
               ((d.role_kind[HG_ROLE_END] == HG_KIND_I64 ? 1u : 0u) << 20) | (1u << 31),
           (uint32_t)d.role_delta[HG_ROLE_START] | ((uint32_t)d.role_delta[HG_ROLE_END] << 16), 0u);
   }
+  ctx->has_dev = false;
+  for (const DSchema& d : ctx->schemas) ctx->has_dev |= d.cls == HG_CLASS_DEVICE;
   ctx->fast_warps = 0;
   ctx->staged = false;
   cudaSetDevice(ctx->cfg.device);
@@ -509,9 +511,10 @@ static int build_layout(hg_ctx* ctx) {
 // every cut point (the retry after a failed range speculation)
 static int build_ranges(hg_ctx* ctx) {
   const uint32_t ns = (uint32_t)ctx->streams.size();
-  const uint32_t n_fd = ctx->max_sid < (uint32_t)kSdescMax ? ctx->max_sid + 2 : 0u;
+  uint32_t n_fd = 0, n_cd = 0;
+  ctx->desc_mode = fast_desc_mode(ctx->max_sid, ctx->n_fn, ctx->has_dev, (uint32_t)ctx->smem_optin, n_fd, n_cd);
   uint32_t nw = kRMaxThreads / kWarp;
-  while (nw > 1 && fast_smem_layout(ctx->n_fn, nw, n_fd).total > (uint32_t)ctx->smem_optin) nw--;
+  while (nw > 1 && fast_smem_layout(ctx->n_fn, nw, n_fd, n_cd, ctx->has_dev).total > (uint32_t)ctx->smem_optin) nw--;
   ctx->fast_warps = nw;
   const uint64_t lanes = (uint64_t)std::max(ctx->sm_count, 1) * nw * kWarp;
   uint64_t payload = 0, max_pay = 0;
@@ -747,6 +750,7 @@ Params make_params(hg_ctx* ctx) {
   p.anom = reinterpret_cast<uint32_t*>(C + C_ANOM);
   p.vplan = ctx->d_vplan.ptr;
   p.fdesc = ctx->d_fdesc.ptr;
+  p.has_dev = ctx->has_dev ? 1u : 0u;
   p.dplan = ctx->d_dplan.ptr;
   p.flush_rank = ctx->flush_order ? ctx->d_flush_rank.ptr : nullptr;
   return p;

@@ -11,19 +11,16 @@ int launch_fast(hg_ctx* ctx) {
   Params p = make_params(ctx);
   p.state = ctx->d_rseg.ptr;
   const uint32_t nw = ctx->fast_warps;
-  const bool sd = ctx->max_sid < (uint32_t)kSdescMax;
-  const size_t smem = fast_smem_layout(ctx->n_fn, nw, sd ? ctx->max_sid + 2 : 0u).total;
+  uint32_t n_fd = 0, n_cd = 0;
+  const int sd = fast_desc_mode(ctx->max_sid, ctx->n_fn, ctx->has_dev, (uint32_t)ctx->smem_optin, n_fd, n_cd);
+  const size_t smem = fast_smem_layout(ctx->n_fn, nw, n_fd, n_cd, ctx->has_dev).total;
   using K = void (*)(Params, const Params*);
-  static const K kerns[16] = {fast_kernel<false, false, 0>, fast_kernel<false, true, 0>,
-                              fast_kernel<true, false, 0>,  fast_kernel<true, true, 0>,
-                              fast_kernel<false, false, 1>, fast_kernel<false, true, 1>,
-                              fast_kernel<true, false, 1>,  fast_kernel<true, true, 1>,
-                              fast_kernel<false, false, 2>, fast_kernel<false, true, 2>,
-                              fast_kernel<true, false, 2>,  fast_kernel<true, true, 2>,
-                              fast_kernel<false, false, 3>, fast_kernel<false, true, 3>,
-                              fast_kernel<true, false, 3>,  fast_kernel<true, true, 3>};
+#define HG_FK(m) fast_kernel<0, false, m>, fast_kernel<0, true, m>, fast_kernel<1, false, m>, fast_kernel<1, true, m>, \
+                 fast_kernel<2, false, m>, fast_kernel<2, true, m>
+  static const K kerns[24] = {HG_FK(0), HG_FK(1), HG_FK(2), HG_FK(3)};
+#undef HG_FK
   const int mode = (p.tl_ritems ? 1 : 0) | (p.ev_ritems ? 2 : 0);
-  const K kern = kerns[4 * mode + (sd ? 2 : 0) + (ctx->deep_inline ? 1 : 0)];
+  const K kern = kerns[6 * mode + 2 * sd + (ctx->deep_inline ? 1 : 0)];
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint32_t per_cta = nw * kWarp;
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));

@@ -45,11 +45,13 @@ constexpr uint32_t kRMirror = 0;                    // (no mirror: header words 
 constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: header + first field need no wrap
 constexpr uint32_t kRInline = HG_RINLINE;           // records up to this long are decoded from the ring
 constexpr int kRLag = 2;                            // iterations before a fill group is waited for
-constexpr int kRLS = 4;                             // open entries per lane in shared memory
+constexpr int kRLS = 4;                             // open entries per lane in shared memory: the stack's top
+                                                    // window (depth d in slot d % kRLS), older ones spilled
 constexpr int kRLP = 4;                             // pending exits per lane in shared memory
 constexpr int kRQ = 64;                             // deferred-record queues per warp (drained at 32)
-constexpr uint32_t kRDeep = 128;                    // per-lane overflow chunk (SumEntry)
-constexpr uint32_t kRDeepHalf = kRDeep / 2;
+constexpr uint32_t kRDeepHalf = 64;                 // per-lane overflow chunk (SumEntry): pending exits beyond
+constexpr uint32_t kRDepthMax = 72;                 // kRLP at [0, 64), open entries of depth d at 64 + d
+constexpr uint32_t kRDeep = kRDeepHalf + kRDepthMax;
 #ifndef HG_RNAMES
 #define HG_RNAMES 256  // 64 -> 256: C2 phase 1 1.99 -> 1.90 ms, C5 x0.25 1.96 -> 1.91 ms (fewer dictionary lookups)
 #endif
@@ -75,10 +77,13 @@ struct RSmem {
 
 __host__ __device__ inline uint32_t r_align(uint32_t x) { return (x + 127u) & ~127u; }
 
-// n_fd: inline-record descriptors staged in shared memory (0: read through L1)
-__host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw, uint32_t n_fd) {
+// n_fd: inline-record descriptors staged in shared memory as uint4 (0: read through L1); n_cd: the
+// same as 4-byte compact descriptors (large registries: max_sid >= kSdescMax, desc_of reads HBM, so
+// they take its place); dev: the registry has device schemas (else no CTA name cache)
+__host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw, uint32_t n_fd, uint32_t n_cd = 0,
+                                                  bool dev = true) {
   RSmem L;
-  uint32_t off = r_align(8u * kSdescMax);  // compact descriptors first (desc_of, kernels.cuh)
+  uint32_t off = n_cd ? r_align(4u * n_cd) : r_align(8u * kSdescMax);  // desc_of's table (kernels.cuh) or cdesc
   const bool small = n_fn <= kSmallF;
   L.tab = off;
   if (!small && n_fn <= kSmemFnMax) off += r_align((uint32_t)sizeof(SmemRow) * n_fn);
@@ -87,7 +92,7 @@ __host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw, ui
   L.dcache = off;
   off += r_align((uint32_t)sizeof(DevRow) * kDevSlots);
   L.ncache = off;  // kRNames x 64 B seqlocked name cache (fast.cuh), not seg.cuh's NameSlot table
-  off += 64u * kRNames;
+  off += dev ? 64u * kRNames : 0u;
   L.fdesc = off;
   off += r_align(16u * n_fd);
   L.warps = off;
@@ -147,6 +152,8 @@ struct RLane {
   uint32_t ci, clast;   // chunks requested, last chunk this range reads
   uint32_t recent;      // bit i: a chunk was requested i iterations ago (its fill group may be pending)
   uint32_t np, ne;
+  uint32_t nw;          // open entries in the shared top window (depths ne - nw .. ne - 1); kept once `deep`
+                        // exists (before, nothing was spilled: the window holds all ne)
   uint32_t ti;          // timeline messages of this range so far (timeline runs)
   bool bad;
   bool fresh;           // no requests until every pending fill of this lane completed (slot reuse)
@@ -224,12 +231,12 @@ __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, u
     R.ci = 0; R.fresh = true;
     R.prev_ts = 0; R.first_ts = 0;
     R.deep = nullptr;
-    R.r = r; R.s = s; R.n = 0; R.spans = 0; R.np = 0; R.ne = 0; R.ti = 0; R.bad = false;
+    R.r = r; R.s = s; R.n = 0; R.spans = 0; R.np = 0; R.ne = 0; R.nw = 0; R.ti = 0; R.bad = false;
     return true;
   }
   R.r = p.n_ranges;
   R.o = R.t1 = R.entry = 0; R.C0 = 0; R.size = 0; R.size32 = 0; R.g = p.data;
-  R.n = R.np = R.ne = R.ci = R.clast = R.ti = 0;
+  R.n = R.np = R.ne = R.nw = R.ci = R.clast = R.ti = 0;
   R.bad = false; R.fresh = true;
   return false;
 }
@@ -272,13 +279,16 @@ __device__ __forceinline__ void r_end(const Params& p, RLane& R, const RTabs& T)
     }
     for (uint32_t i = 0; i < R.ne; i++) {
       SumEntry e;
-      if (i < (uint32_t)kRLS) {
-        e.ts = T.st_ts[i * kWarp];
-        e.fn = m_fn(T.st_fn[i * kWarp]);
-        e.seq = 0; e.flags = 0; e.result = 0;
-      } else {
-        e = R.deep[kRDeepHalf + i - kRLS];
+      if (!R.deep || i + R.nw >= R.ne) {  // in the top window
+        const uint32_t j = (i & (kRLS - 1)) * kWarp;
+        e.ts = T.st_ts[j];
+        e.fn = m_fn(T.st_fn[j]);
+      } else {                 // spilled (ts and fn only)
+        const SumEntry* d = R.deep + kRDeepHalf + i;
+        e.ts = d->ts;
+        e.fn = d->fn;
       }
+      e.seq = 0; e.flags = 0; e.result = 0;
       p.pool[poff + R.np + i] = e;
     }
   }
@@ -307,7 +317,16 @@ __device__ __forceinline__ bool r_deep(const Params& p, RLane& R) {
   const unsigned long long off = atomicAdd(p.deep_used, (unsigned long long)kRDeep);
   if (off + kRDeep > p.deep_cap) return false;  // the host grows the pool and reruns
   R.deep = p.deep + off;
+  R.nw = R.ne;  // nothing spilled yet
   return true;
+}
+
+// the top window is full and depth i is pushed: its slot holds depth i - kRLS, which moves to the chunk
+__device__ __forceinline__ void r_spill(RLane& R, const RTabs& T, uint32_t i) {
+  const uint32_t j = (i & (kRLS - 1)) * kWarp;
+  SumEntry* d = R.deep + kRDeepHalf + (i - kRLS);
+  d->ts = T.st_ts[j];
+  d->fn = m_fn(T.st_fn[j]);
 }
 
 // every record the inline path does not take, decoded from HBM: long records,
@@ -352,14 +371,13 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
   const uint32_t fnm = d.x & M_FN;
   if (cls == HG_CLASS_ENTRY) {
     const uint32_t i = R.ne;
-    if (i < (uint32_t)kRLS) {
-      T.st_ts[i * kWarp] = h.ts; T.st_fn[i * kWarp] = fnm;
-    } else {
-      if (i >= (uint32_t)kRLS + kRDeepHalf || !r_deep(p, R)) { R.bad = true; return false; }
-      SumEntry e;
-      e.ts = h.ts; e.seq = 0; e.fn = m_fn(fnm); e.flags = 0; e.result = 0;
-      R.deep[kRDeepHalf + i - kRLS] = e;
+    if (i >= kRDepthMax) { R.bad = true; return false; }
+    if (R.deep || i >= (uint32_t)kRLS) {
+      if (!r_deep(p, R)) { R.bad = true; return false; }
+      if (R.nw == (uint32_t)kRLS) r_spill(R, T, i);  // the window is full: its oldest entry (depth i - kRLS, same slot) moves
+      else R.nw++;
     }
+    T.st_ts[(i & (kRLS - 1)) * kWarp] = h.ts; T.st_fn[(i & (kRLS - 1)) * kWarp] = fnm;
     R.ne = i + 1;
   } else if (cls == HG_CLASS_EXIT) {
     uint64_t res = 0;
@@ -379,14 +397,15 @@ __device__ __forceinline__ bool r_record_slow(const Params& p, RLane& R, const R
     if (ne) {  // pipeline.py:156-168
       uint64_t ets;
       uint32_t tfn;
-      if (ne <= (uint32_t)kRLS) {
-        ets = T.st_ts[(ne - 1) * kWarp]; tfn = T.st_fn[(ne - 1) * kWarp];
+      if (!R.deep || R.nw) {
+        ets = T.st_ts[((ne - 1) & (kRLS - 1)) * kWarp]; tfn = T.st_fn[((ne - 1) & (kRLS - 1)) * kWarp];
       } else {
-        const SumEntry e = R.deep[kRDeepHalf + ne - 1 - kRLS];
-        ets = e.ts; tfn = e.fn < 0 ? M_FN : (uint32_t)e.fn;
+        const SumEntry* e = R.deep + kRDeepHalf + ne - 1;
+        ets = e->ts; tfn = e->fn < 0 ? M_FN : (uint32_t)e->fn;
       }
       if (tfn == fnm) {
         R.ne = ne - 1;
+        R.nw -= R.nw ? 1u : 0u;
         hf.fold(p, (int32_t)fnm, h.ts - ets, (xf & 2u) != 0);
         K.host++;
         R.spans++;
@@ -592,7 +611,32 @@ static __device__ __noinline__ void r_fold_flush(const Params& p, uint32_t fn, u
   add_i128(&a[2], &a[3], cs & (kFCount - 1), 0);
 }
 
-__device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uint32_t nw, uint32_t n_fd) {
+// 4-byte inline descriptor (large registries): valid << 31 | fdesc.x bits 20-28 (kind, flags) |
+// fixed payload length << 12 | function (0xFFF: M_FN); records with a variable field, a function
+// id >= 0xFFF or a payload range keep the uint4 (valid = 0: read through L1)
+__host__ __device__ inline uint32_t r_compact(uint4 D) {
+  const uint32_t fn = D.x & M_FN, lo = D.y & 0xFFFFu, hi = D.y >> 16;
+  const uint32_t kind = (D.x >> 20) & 7u;
+  if (kind == FK_NEVER) return 0x80000FFFu | (FK_NEVER << 20);
+  if ((D.x & FD_VAR) || lo != hi || lo > 0xFFu || (fn >= 0xFFFu && fn != M_FN)) return 0u;
+  return 0x80000000u | (D.x & 0x1FF00000u) | (lo << 12) | (fn == M_FN ? 0xFFFu : fn);
+}
+
+__device__ __forceinline__ uint4 r_expand(uint32_t c) {
+  const uint32_t fn = c & 0xFFFu, len = (c >> 12) & 0xFFu;
+  return make_uint4((fn == 0xFFFu ? M_FN : fn) | (c & 0x1FF00000u), len | (len << 16), 0u, 0u);
+}
+
+// descriptor mode of the range kernel: 1 uint4 table in shared memory (small registries), 2 compact
+// table (fits next to 12 warps), 0 through L1
+inline int fast_desc_mode(uint32_t max_sid, uint32_t n_fn, bool dev, uint32_t optin, uint32_t& n_fd, uint32_t& n_cd) {
+  n_fd = n_cd = 0;
+  if (max_sid < (uint32_t)kSdescMax) { n_fd = max_sid + 2; return 1; }
+  if (fast_smem_layout(n_fn, HG_FAST_WARPS, 0, max_sid + 2, dev).total <= optin) { n_cd = max_sid + 2; return 2; }
+  return 0;
+}
+
+__device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uint32_t nw, uint32_t n_fd, uint32_t n_cd) {
   uint4* fd = reinterpret_cast<uint4*>(g_smem + RL.fdesc);
   for (uint32_t i = threadIdx.x; i < n_fd; i += blockDim.x) fd[i] = __ldg(&p.fdesc[i]);
   if (p.max_sid < (uint32_t)kSdescMax) {
@@ -619,7 +663,10 @@ __device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uin
     dcache[i] = z;
   }
   uint32_t* ncache = reinterpret_cast<uint32_t*>(g_smem + RL.ncache);
-  for (uint32_t i = threadIdx.x; i < kRNames; i += blockDim.x) ncache[16 * i] = 0;  // seq 0: empty
+  if (p.has_dev)
+    for (uint32_t i = threadIdx.x; i < kRNames; i += blockDim.x) ncache[16 * i] = 0;  // seq 0: empty
+  uint32_t* cd = reinterpret_cast<uint32_t*>(g_smem);
+  for (uint32_t i = threadIdx.x; i < n_cd; i += blockDim.x) cd[i] = r_compact(__ldg(&p.fdesc[i]));
   (void)nw;
   __syncthreads();
 }
@@ -685,17 +732,19 @@ static __device__ __noinline__ void r_epilogue(const Params& p, const RSmem RL, 
   }
 }
 
-// kSD: the registry's inline descriptors fit in shared memory (max_sid < kSdescMax);
+// kSD: descriptor mode (fast_desc_mode): 1 the registry's inline descriptors in shared memory (max_sid <
+// kSdescMax), 2 compact descriptors in shared memory, 0 through L1;
 // kDeep: stacks deeper than kRLS stay on the inline path (overflow chunk) -- chosen by the host
 // once a run of the trace needed overflow chunks; kMode bits: 1 a timeline run (every host span,
 // device span and sample also leaves a message in its range's list, r_item), 2 an event run
 // (every record, r_event)
-template <bool kSD, bool kDeep, int kMode>
+template <int kSD, bool kDeep, int kMode>
 __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const Params* gp) {
   const Params& gpr = *gp;
   const uint32_t nw = blockDim.x >> 5;
-  const uint32_t n_fd = kSD ? p.max_sid + 2 : 0u;
-  const RSmem RL = fast_smem_layout(p.n_fn, nw, n_fd);
+  const uint32_t n_fd = kSD == 1 ? p.max_sid + 2 : 0u, n_cd = kSD == 2 ? p.max_sid + 2 : 0u;
+  const RSmem RL = fast_smem_layout(p.n_fn, nw, n_fd, n_cd, p.has_dev != 0);
+  const uint32_t* cdesc_s = reinterpret_cast<const uint32_t*>(g_smem);
   const uint4* fdesc_s = reinterpret_cast<const uint4*>(g_smem + RL.fdesc);
   const SegSmem L = r_segsmem(RL);
   const uint32_t lane = lane_id();
@@ -703,7 +752,7 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
   const uint32_t* ring = reinterpret_cast<const uint32_t*>(wb + RL.ring + lane * kRStride);
   const uint32_t ring_s = s_addr(ring);
   const uint32_t nc_s = s_addr(g_smem + RL.ncache);
-  r_prologue(p, RL, nw, n_fd);
+  r_prologue(p, RL, nw, n_fd, n_cd);
   SegCounters K;
   K.passed = K.host = K.dev = K.samples = K.orph = K.items = 0;
   HostFold hf;  // the slow path's fold: CTA table (medium function sets) or global rows
@@ -769,15 +818,23 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const uint32_t sid = __funnelshift_r(w0, w1, sh);
     const uint64_t ts = ((uint64_t)__funnelshift_r(w2, w3, sh) << 32) | __funnelshift_r(w1, w2, sh);
     const uint32_t plen = __funnelshift_r(w3, w4, sh);
-    const uint4 D = kSD ? fdesc_s[min(sid, sid_cap)] : __ldg(&p.fdesc[min(sid, sid_cap)]);
+    uint4 D;
+    if (kSD == 1) {
+      D = fdesc_s[min(sid, sid_cap)];
+    } else if (kSD == 2) {
+      const uint32_t c = cdesc_s[min(sid, sid_cap)];
+      D = (c >> 31) ? r_expand(c) : __ldg(&p.fdesc[min(sid, sid_cap)]);
+    } else {
+      D = __ldg(&p.fdesc[min(sid, sid_cap)]);
+    }
     const uint32_t fnm = D.x & M_FN;
     const uint32_t kind = (D.x >> 20) & 7u;
     const uint32_t ne = R.ne, np = R.np;
-    const uint32_t topi = ((ne - 1u) < (uint32_t)kRLS ? ne - 1u : 0u) * kWarp;
+    const uint32_t topi = ((ne - 1u) & (uint32_t)(kRLS - 1)) * kWarp;
     uint64_t ets = T.st_ts[topi];
     uint32_t tfn = T.st_fn[topi];
-    if (kDeep && ne > (uint32_t)kRLS && R.deep) {  // deeper entries live in the lane's overflow chunk (HBM, L1)
-      const SumEntry* de = R.deep + kRDeepHalf + (ne - 1u - kRLS);
+    if (kDeep && ne && R.deep && !R.nw) {  // the window is empty: the top was spilled to the lane's overflow chunk (HBM, L1)
+      const SumEntry* de = R.deep + kRDeepHalf + (ne - 1u);
       ets = de->ts;
       tfn = de->fn < 0 ? M_FN : (uint32_t)de->fn;
     }
@@ -787,9 +844,11 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
                       R.o + 16u + plen <= R.size32 && (R.n == 0 || ts >= R.prev_ts);
     const bool stall = ready && !good && plen <= kRInline - 16u && (R.o + 15u + plen) / kRChunk >= cr &&
                        (uint64_t)R.o + 16u + plen <= R.size;
-    const uint32_t cap = (kDeep && R.deep) ? (uint32_t)kRLS + kRDeepHalf : (uint32_t)kRLS;  // entries held inline
-    const bool fE = good && kind == FK_ENTRY && ne < cap;
-    const bool fXp = good && kind == FK_EXIT && ne - 1u < cap && tfn == fnm;  // pops a same-function top
+    // a push spills when the window is full, a pop reads the chunk when it is empty (kDeep, chunk allocated)
+    // (without kDeep a lane whose range allocated a chunk leaves every push / pop to the slow path)
+    const bool fE = good && kind == FK_ENTRY && (kDeep ? ne < kRDepthMax && (R.deep || ne < (uint32_t)kRLS)
+                                                       : ne < (uint32_t)kRLS && !R.deep);
+    const bool fXp = good && kind == FK_EXIT && ne && (kDeep || !R.deep) && tfn == fnm;  // pops a same-function top
     const bool fXq = good && kind == FK_EXIT && ne == 0 && np < (uint32_t)kRLP;          // pending: compose decides
     const bool fO = good && (kind == FK_PASS || kind == FK_DEFER);
     // one variable field (blob / string): exact length here, UTF-8 of strings in the drain
@@ -825,14 +884,12 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
       R.prev_ts = ts;
       R.o += 16u + plen;
     }
-    if (kDeep && fE && ne >= (uint32_t)kRLS) {
-      SumEntry e;
-      e.ts = ts; e.seq = 0; e.fn = m_fn(fnm); e.flags = 0; e.result = 0;
-      R.deep[kRDeepHalf + ne - kRLS] = e;
-    } else if (fE) {
-      T.st_ts[ne * kWarp] = ts;
-      T.st_fn[ne * kWarp] = fnm;
+    if (fE) {
+      if (kDeep && R.deep && R.nw == (uint32_t)kRLS) r_spill(R, T, ne);
+      T.st_ts[(ne & (kRLS - 1)) * kWarp] = ts;
+      T.st_fn[(ne & (kRLS - 1)) * kWarp] = fnm;
     }
+    if (kDeep) R.nw = R.nw + ((fE && R.nw < (uint32_t)kRLS) ? 1u : 0u) - ((fXp && R.nw) ? 1u : 0u);
     if (fXq) {
       const uint32_t i = np * kWarp;
       T.pd_ts[i] = ts;

@@ -124,6 +124,7 @@ struct Params {
   const uint4* fdesc;              // per schema id (+ one sentinel): inline-record descriptor (fast.cuh)
   const uint4* dplan;              // per schema id: device-record layout for the drain (fast.cuh)
   const uint32_t* flush_rank;      // stream -> rank in the truncation flush order (nullptr: stream order)
+  uint32_t has_dev;                // the registry has device-profiling schemas (fast.cuh: CTA name cache)
 };
 
 // compact descriptor: x = fn(20) | cls(3)<<20 | flags(8)<<23 ; y = fixed_len(16) | result field index(8)<<16 | counter(8)<<24

@@ -167,3 +167,36 @@ def test_device_heavy_repeated_runs(engine, name, scale, prof_p):
         got = engine.run(raws, wl.registry, infos, reuse_streams=i > 0)
         assert engine.last_path()[0] == 1
         assert got.stats == want.stats and got.report == want.report and got.orphans == want.orphans
+
+
+@pytest.mark.parametrize("n_top,n_low", [(1000, 1000), (3000, 1500)])
+@pytest.mark.parametrize("range_bytes", [0, 1008])
+def test_large_registry_deep_stacks(engine, n_top, n_low, range_bytes):
+    """Large registries (max schema id >= 512): descriptors as 4-byte compact entries in shared
+    memory (functions >= 0xFFF and the variable-field annotation schema keep the uint4 read through
+    L1); depth-64 stacks in the shared top window with older entries spilled.  Three runs on the same
+    streams (the first picks the overflow-chunk kernel variant for the next) match the oracle."""
+    from oracle import oracle
+    from paper_2504_03683_b200 import synth
+    from paper_2504_03683_b200.engine import OPT_PATH, OPT_RANGE_BYTES
+
+    reg = synth.layered_registry(n_top=n_top, n_low=n_low)
+    layers = {s.function: (0 if s.function.startswith("sycl") else 1)
+              for s in reg.schemas if s.event_class == "host_entry"}
+    P = synth.PID_BASE
+    streams = [synth.StreamSpec("h", P, P + i, 6000 + 1501 * i, 9100 + i) for i in range(8)]
+    wl = synth.Workload("big", reg, streams, {"max_depth": 64, "push_p": 0.55, "zipf_s": 1.1, "n_layers": 2,
+                                              "mismatch_p": 0.002, "close_at_end": 0}, layers=layers)
+    raws = synth.generate(wl)
+    infos = [r.info for r in raws]
+    want = oracle.run(raws, wl.registry, infos)
+    engine.set_option(OPT_PATH, 2)
+    engine.set_option(OPT_RANGE_BYTES, range_bytes)
+    try:
+        for i in range(3):
+            got = engine.run(raws, wl.registry, infos, reuse_streams=i > 0)
+            assert engine.last_path()[0] == 1
+            assert got.stats == want.stats and got.report == want.report and got.orphans == want.orphans
+    finally:
+        engine.set_option(OPT_PATH, 0)
+        engine.set_option(OPT_RANGE_BYTES, 0)
