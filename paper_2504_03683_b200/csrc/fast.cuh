@@ -53,10 +53,11 @@ constexpr uint32_t kRDeepHalf = 64;                 // per-lane overflow chunk (
 constexpr uint32_t kRDepthMax = 72;                 // kRLP at [0, 64), open entries of depth d at 64 + d
 constexpr uint32_t kRDeep = kRDeepHalf + kRDepthMax;
 #ifndef HG_RNAMES
-#define HG_RNAMES 256  // 64 -> 256: C2 phase 1 1.99 -> 1.90 ms, C5 x0.25 1.96 -> 1.91 ms (fewer dictionary lookups)
+#define HG_RNAMES 512  // 64 -> 256 slots of 64 B: C2 phase 1 1.99 -> 1.90 ms, C5 x0.25 1.96 -> 1.91 ms; 512 of 32 B, 2-way
 #endif
-constexpr uint32_t kRNames = HG_RNAMES;                   // CTA name cache slots (64 B: seq, row, len, hash, 40 name bytes)
-constexpr uint32_t kRNameMax = 40;         // first half pending exits, second half open entries
+constexpr uint32_t kRNames = HG_RNAMES;    // CTA name cache: 2-way sets of 32-byte slots (seq, row | len << 24,
+constexpr uint32_t kRNameMax = 40;         // hash bits 32-63, name); register strings up to kRNameMax bytes
+constexpr uint32_t kRNameCache = 20;       // names up to this long are cached
 
 struct RangeState {
   uint64_t entry;      // speculative first record (kNone: no plausible header in the range)
@@ -92,7 +93,7 @@ __host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw, ui
   L.dcache = off;
   off += r_align((uint32_t)sizeof(DevRow) * kDevSlots);
   L.ncache = off;  // kRNames x 64 B seqlocked name cache (fast.cuh), not seg.cuh's NameSlot table
-  off += dev ? 64u * kRNames : 0u;
+  off += dev ? 32u * kRNames : 0u;
   L.fdesc = off;
   off += r_align(16u * n_fd);
   L.warps = off;
@@ -443,46 +444,101 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   return v;
 }
 
-// fill the CTA name cache slot of a name found in (or added to) the global dictionary
-__device__ __forceinline__ void r_name_fill(uint32_t nc_s, uint64_t h, uint32_t row, const uint8_t* g, uint64_t no,
-                                            uint32_t nl) {
-  if (nl > kRNameMax) return;
-  const uint32_t slot = nc_s + (uint32_t)(h & (kRNames - 1)) * 64u;
-  uint32_t s;
-  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s) : "r"(slot) : "memory");
+// ---- strings of up to kRNameMax bytes in registers: the words are loaded in one round trip
+// (aligned loads, funnel-shifted with a static index), then checked, hashed and compared there
+constexpr uint32_t kDW = kRNameMax / 4;
+
+// the kRNameMax bytes at o as words (the stream is 256-aligned and the data buffer zero-padded by
+// kDataPad, so reading past a short string is safe); every load is issued before any is used
+__device__ __forceinline__ void r_words(const uint8_t* g, uint64_t o, uint32_t (&w)[kDW]) {
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(g) + (o >> 2);
+  const uint32_t sh = (uint32_t)(o & 3) * 8;
+  uint32_t r[kDW + 1];
+  #pragma unroll
+  for (uint32_t j = 0; j <= kDW; j++) r[j] = __ldg(p + j);
+  #pragma unroll
+  for (uint32_t j = 0; j < kDW; j++) w[j] = __funnelshift_r(r[j], r[j + 1], sh);
+}
+
+// zero every byte from n on (n <= kRNameMax)
+__device__ __forceinline__ void r_words_mask(uint32_t (&w)[kDW], uint32_t n) {
+  #pragma unroll
+  for (uint32_t j = 0; j < kDW; j++)
+    w[j] = 4 * j >= n ? 0u : 4 * j + 4 <= n ? w[j] : w[j] & (0xffffffffu >> (8 * (4 - (n - 4 * j))));
+}
+
+__device__ __forceinline__ bool r_words_ascii(const uint32_t (&w)[kDW]) {
+  uint32_t acc = 0;
+  #pragma unroll
+  for (uint32_t j = 0; j < kDW; j++) acc |= w[j];
+  return (acc & 0x80808080u) == 0;
+}
+
+// g_hash (seg.cuh) over register words
+__device__ __forceinline__ uint64_t r_words_hash(const uint32_t (&w)[kDW], uint32_t n) {
+  uint64_t h = 0x9E3779B97F4A7C15ull ^ ((uint64_t)n * 0xff51afd7ed558ccdull);
+  #pragma unroll
+  for (uint32_t j = 0; j < kDW; j++) {
+    if (4 * j + 4 <= n) {
+      h ^= w[j];
+      h *= 0x100000001b3ull;
+      h ^= h >> 29;
+    } else if (4 * j < n) {
+      h ^= w[j];
+      h *= 0x100000001b3ull;
+    }
+  }
+  h ^= h >> 33; h *= 0xc4ceb9fe1a85ec53ull; h ^= h >> 33;
+  return h | 1ull;
+}
+
+// CTA name cache (device rows by kernel name): set h % (kRNames / 2), two 32-byte ways under a
+// sequence lock each; a hit needs the length, hash bits 32-63 and every name byte to match, so the
+// cache never changes which row a name gets (the global dictionary decides, seg.cuh g_name_lookup)
+__device__ __forceinline__ uint32_t r_name_probe_w(uint32_t nc_s, uint64_t h, const uint32_t (&w)[kDW], uint32_t nl) {
+  if (nl > kRNameCache) return 0xffffffffu;
+  const uint32_t set = nc_s + (uint32_t)(h & (kRNames / 2 - 1)) * 64u;
+  #pragma unroll
+  for (uint32_t way = 0; way < 2; way++) {
+    const uint32_t slot = set + 32u * way;
+    uint32_t s1;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s1) : "r"(slot) : "memory");
+    if (!s1 || (s1 & 1u)) continue;
+    const uint32_t rl = lds32(slot + 4), hh = lds32(slot + 8);
+    if ((rl >> 24) != nl || hh != (uint32_t)(h >> 32)) continue;
+    uint32_t diff = 0;
+    #pragma unroll
+    for (uint32_t j = 0; j < kRNameCache / 4; j++)
+      if (4 * j < nl) diff |= lds32(slot + 12 + 4 * j) ^ w[j];  // both zero beyond nl
+    if (diff) continue;
+    uint32_t s2;
+    asm volatile("membar.cta; ld.volatile.shared.u32 %0, [%1];" : "=r"(s2) : "r"(slot) : "memory");
+    if (s2 == s1) return rl & 0xFFFFFFu;
+  }
+  return 0xffffffffu;
+}
+
+// fill a way of the name's set (an empty one, else the way picked by hash bit 40)
+__device__ __forceinline__ void r_name_fill_w(uint32_t nc_s, uint64_t h, uint32_t row, const uint32_t (&w)[kDW],
+                                              uint32_t nl) {
+  if (nl > kRNameCache || row > 0xFFFFFFu) return;
+  const uint32_t set = nc_s + (uint32_t)(h & (kRNames / 2 - 1)) * 64u;
+  uint32_t s0, s1;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s0) : "r"(set) : "memory");
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s1) : "r"(set + 32u) : "memory");
+  const uint32_t way = !s0 ? 0u : !s1 ? 1u : (uint32_t)(h >> 40) & 1u;
+  const uint32_t slot = set + 32u * way;
+  const uint32_t s = way ? s1 : s0;
   if (s & 1u) return;
   uint32_t old;
   asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(slot), "r"(s), "r"(s + 1u) : "memory");
   if (old != s) return;
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 4), "r"(row) : "memory");
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 8), "r"(nl) : "memory");
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 16), "r"((uint32_t)h) : "memory");
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 20), "r"((uint32_t)(h >> 32)) : "memory");
-  for (uint32_t i = 0; i < nl; i += 4) {
-    uint32_t w = g32(g, no + i);
-    if (nl - i < 4) w &= 0xffffffffu >> (8u * (4u - (nl - i)));
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 24 + i), "r"(w) : "memory");
-  }
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 4), "r"(row | (nl << 24)) : "memory");
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 8), "r"((uint32_t)(h >> 32)) : "memory");
+  #pragma unroll
+  for (uint32_t j = 0; j < kRNameCache / 4; j++)
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(slot + 12 + 4 * j), "r"(w[j]) : "memory");
   asm volatile("membar.cta; st.volatile.shared.u32 [%0], %1;" ::"r"(slot), "r"(s + 2u) : "memory");
-}
-
-// CTA cache lookup of a name in HBM: the row, or ~0 (miss, long name or a slot being written)
-__device__ __forceinline__ uint32_t r_name_probe(uint32_t nc_s, uint64_t h, const uint8_t* g, uint64_t no, uint32_t nl) {
-  if (nl > kRNameMax) return 0xffffffffu;
-  const uint32_t slot = nc_s + (uint32_t)(h & (kRNames - 1)) * 64u;
-  uint32_t s1;
-  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s1) : "r"(slot) : "memory");
-  if (!s1 || (s1 & 1u)) return 0xffffffffu;
-  const uint32_t row = lds32(slot + 4), len = lds32(slot + 8);
-  const uint64_t sh = ((uint64_t)lds32(slot + 20) << 32) | lds32(slot + 16);
-  if (sh != h || len != nl) return 0xffffffffu;
-  for (uint32_t i = 0; i < nl; i += 4) {
-    const uint32_t m = nl - i < 4 ? 0xffffffffu >> (8u * (4u - (nl - i))) : 0xffffffffu;
-    if ((g32(g, no + i) & m) != (lds32(slot + 24 + i) & m)) return 0xffffffffu;
-  }
-  uint32_t s2;
-  asm volatile("membar.cta; ld.volatile.shared.u32 %0, [%1];" : "=r"(s2) : "r"(slot) : "memory");
-  return s2 == s1 ? row : 0xffffffffu;
 }
 
 // deferred records, one per lane, read from HBM (L2): device-profiling and telemetry
@@ -506,24 +562,45 @@ static __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, c
     uint64_t aux = 0;
     uint32_t err = 0;
     const uint4 dp = cls == HG_CLASS_DEVICE ? __ldg(&p.dplan[h.sid]) : make_uint4(0, 0, 0, 0);
-    if (dp.y >> 31) {  // usual device layout (dplan): three dependent HBM round trips instead of a field walk
+    uint32_t nw_[kDW];     // the name in registers (nreg) when it is at most kRNameMax bytes
+    bool nreg = false;
+    uint64_t ua_ = 0, ub_ = 0;
+    if (dp.y >> 31) {  // usual device layout (dplan): start / end and the first length in one round trip,
+                       // the second length and both strings' words in the next
       const uint32_t lead0 = dp.x & 0xFFFFu, lead1 = dp.x >> 16, lead2 = dp.y & 0xFFFFu;
       const uint64_t body = a + 16;
       const uint32_t l0 = g32(gb, body + lead0);
       rp[HG_ROLE_START] = body + (dp.z & 0xFFFFu);
       rp[HG_ROLE_END] = body + (dp.z >> 16);
+      ua_ = g64(gb, rp[HG_ROLE_START]);
+      ub_ = g64(gb, rp[HG_ROLE_END]);
       if ((uint64_t)lead0 + 4u + l0 + lead1 + 4u > h.plen) {
         err = HG_ERR_TRUNC_VAR;
       } else {
         const uint64_t b1 = body + lead0 + 4u + l0 + lead1;
-        const uint32_t l1 = g32(gb, b1);
-        if ((uint64_t)lead0 + 4u + l0 + lead1 + 4u + l1 + lead2 != h.plen) err = HG_ERR_TRAILING;
-        else if ((((dp.y >> 17) & 1u) && !g_utf8(gb, body + lead0 + 4u, l0)) ||
-                 (((dp.y >> 18) & 1u) && !g_utf8(gb, b1 + 4u, l1)))
-          err = HG_ERR_UTF8;
         const bool second = (dp.y >> 16) & 1u;
-        rp[HG_ROLE_NAME] = second ? b1 + 4u : body + lead0 + 4u;
-        rl[HG_ROLE_NAME] = second ? l1 : l0;
+        const uint64_t s0 = body + lead0 + 4u, s1 = b1 + 4u;
+        const uint32_t l1 = g32(gb, b1);
+        uint32_t ow[kDW];  // the other string, when short
+        r_words(gb, second ? s0 : s1, ow);
+        r_words(gb, second ? s1 : s0, nw_);
+        const uint32_t nl = second ? l1 : l0, ol = second ? l0 : l1;
+        if ((uint64_t)lead0 + 4u + l0 + lead1 + 4u + l1 + lead2 != h.plen) {
+          err = HG_ERR_TRAILING;
+        } else {
+          const bool nstr = ((dp.y >> (second ? 18 : 17)) & 1u) != 0, ostr = ((dp.y >> (second ? 17 : 18)) & 1u) != 0;
+          nreg = nl <= kRNameMax;
+          if (nreg) r_words_mask(nw_, nl);
+          if (ostr) {
+            bool ok;
+            if (ol <= kRNameMax) { r_words_mask(ow, ol); ok = r_words_ascii(ow) || g_utf8(gb, second ? s0 : s1, ol); }
+            else ok = g_utf8(gb, second ? s0 : s1, ol);
+            if (!ok) err = HG_ERR_UTF8;
+          }
+          if (nstr && !err && !((nreg && r_words_ascii(nw_)) || g_utf8(gb, second ? s1 : s0, nl))) err = HG_ERR_UTF8;
+        }
+        rp[HG_ROLE_NAME] = second ? s1 : s0;
+        rl[HG_ROLE_NAME] = nl;
       }
     } else if (roles) {
       err = seg_fields(p, gb, size, a, h.sid, h.plen, rp, rl, aux, roles);
@@ -537,18 +614,20 @@ static __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, c
         err = HG_ERR_FEED;
       } else {
         const DSchema* sc = schema_of(p, h.sid);
-        const uint64_t ua = g64(gb, rp[HG_ROLE_START]), ub = g64(gb, rp[HG_ROLE_END]);
+        const uint64_t ua = (dp.y >> 31) ? ua_ : g64(gb, rp[HG_ROLE_START]);
+        const uint64_t ub = (dp.y >> 31) ? ub_ : g64(gb, rp[HG_ROLE_END]);
         const bool si = (dp.y >> 31) ? ((dp.y >> 19) & 1u) != 0 : sc->role_kind[HG_ROLE_START] == HG_KIND_I64;
         const bool ei = (dp.y >> 31) ? ((dp.y >> 20) & 1u) != 0 : sc->role_kind[HG_ROLE_END] == HG_KIND_I64;
         const int64_t ah = (si && (int64_t)ua < 0) ? -1 : 0;
         const int64_t bh = (ei && (int64_t)ub < 0) ? -1 : 0;
         const uint64_t no = rp[HG_ROLE_NAME];
         const uint32_t nl = rl[HG_ROLE_NAME];
-        const uint64_t hh = g_hash(gb, no, nl);
-        uint32_t row = r_name_probe(nc_s, hh, gb, no, nl);  // CTA cache: no global atomics on a hit
+        const uint64_t hh = nreg ? r_words_hash(nw_, nl) : g_hash(gb, no, nl);
+        // CTA cache: no global atomics on a hit
+        uint32_t row = nreg ? r_name_probe_w(nc_s, hh, nw_, nl) : 0xffffffffu;
         if (row == 0xffffffffu) {
           row = g_name_lookup(p.names, gb, no, nl, hh);
-          if (row != 0xffffffffu) r_name_fill(nc_s, hh, row, gb, no, nl);
+          if (row != 0xffffffffu && nreg) r_name_fill_w(nc_s, hh, row, nw_, nl);
         }
         if (row != 0xffffffffu) {
           fold_device(p, reinterpret_cast<DevRow*>(g_smem + L.dcache), row, ub - ua, bh - ah - (ub < ua ? 1 : 0));
@@ -664,7 +743,7 @@ __device__ __forceinline__ void r_prologue(const Params& p, const RSmem& RL, uin
   }
   uint32_t* ncache = reinterpret_cast<uint32_t*>(g_smem + RL.ncache);
   if (p.has_dev)
-    for (uint32_t i = threadIdx.x; i < kRNames; i += blockDim.x) ncache[16 * i] = 0;  // seq 0: empty
+    for (uint32_t i = threadIdx.x; i < kRNames; i += blockDim.x) ncache[8 * i] = 0;  // seq 0: empty
   uint32_t* cd = reinterpret_cast<uint32_t*>(g_smem);
   for (uint32_t i = threadIdx.x; i < n_cd; i += blockDim.x) cd[i] = r_compact(__ldg(&p.fdesc[i]));
   (void)nw;
