@@ -58,6 +58,10 @@ constexpr uint32_t kRDeep = kRDeepHalf + kRDepthMax;
 constexpr uint32_t kRNames = HG_RNAMES;    // CTA name cache: 2-way sets of 32-byte slots (seq, row | len << 24,
 constexpr uint32_t kRNameMax = 40;         // hash bits 32-63, name); register strings up to kRNameMax bytes
 constexpr uint32_t kRNameCache = 20;       // names up to this long are cached
+#ifndef HG_RWAYS
+#define HG_RWAYS 1  // C5 x1.0 phase 1: 1 way 6.71 ms, 2 ways 6.94, 4 ways 7.21 (probes cost more than misses)
+#endif
+constexpr uint32_t kRWays = HG_RWAYS;      // ways per set
 
 struct RangeState {
   uint64_t entry;      // speculative first record (kNone: no plausible header in the range)
@@ -492,14 +496,14 @@ __device__ __forceinline__ uint64_t r_words_hash(const uint32_t (&w)[kDW], uint3
   return h | 1ull;
 }
 
-// CTA name cache (device rows by kernel name): set h % (kRNames / 2), two 32-byte ways under a
+// CTA name cache (device rows by kernel name): set h % (kRNames / kRWays), kRWays 32-byte ways (one: direct mapped) under a
 // sequence lock each; a hit needs the length, hash bits 32-63 and every name byte to match, so the
 // cache never changes which row a name gets (the global dictionary decides, seg.cuh g_name_lookup)
 __device__ __forceinline__ uint32_t r_name_probe_w(uint32_t nc_s, uint64_t h, const uint32_t (&w)[kDW], uint32_t nl) {
   if (nl > kRNameCache) return 0xffffffffu;
-  const uint32_t set = nc_s + (uint32_t)(h & (kRNames / 2 - 1)) * 64u;
+  const uint32_t set = nc_s + (uint32_t)(h & (kRNames / kRWays - 1)) * 32u * kRWays;
   #pragma unroll
-  for (uint32_t way = 0; way < 2; way++) {
+  for (uint32_t way = 0; way < kRWays; way++) {
     const uint32_t slot = set + 32u * way;
     uint32_t s1;
     asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s1) : "r"(slot) : "memory");
@@ -518,17 +522,20 @@ __device__ __forceinline__ uint32_t r_name_probe_w(uint32_t nc_s, uint64_t h, co
   return 0xffffffffu;
 }
 
-// fill a way of the name's set (an empty one, else the way picked by hash bit 40)
+// fill a way of the name's set (an empty one, else the way picked by hash bits 40-)
 __device__ __forceinline__ void r_name_fill_w(uint32_t nc_s, uint64_t h, uint32_t row, const uint32_t (&w)[kDW],
                                               uint32_t nl) {
   if (nl > kRNameCache || row > 0xFFFFFFu) return;
-  const uint32_t set = nc_s + (uint32_t)(h & (kRNames / 2 - 1)) * 64u;
-  uint32_t s0, s1;
-  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s0) : "r"(set) : "memory");
-  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s1) : "r"(set + 32u) : "memory");
-  const uint32_t way = !s0 ? 0u : !s1 ? 1u : (uint32_t)(h >> 40) & 1u;
+  const uint32_t set = nc_s + (uint32_t)(h & (kRNames / kRWays - 1)) * 32u * kRWays;
+  uint32_t way = (uint32_t)(h >> 40) & (kRWays - 1), s = 0;
+  asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(s) : "r"(set + 32u * way) : "memory");
+  #pragma unroll
+  for (uint32_t k = 0; k < kRWays; k++) {
+    uint32_t sk;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(sk) : "r"(set + 32u * k) : "memory");
+    if (!sk && s) { way = k; s = 0; }
+  }
   const uint32_t slot = set + 32u * way;
-  const uint32_t s = way ? s1 : s0;
   if (s & 1u) return;
   uint32_t old;
   asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(old) : "r"(slot), "r"(s), "r"(s + 1u) : "memory");
