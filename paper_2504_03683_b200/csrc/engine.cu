@@ -751,6 +751,7 @@ Params make_params(hg_ctx* ctx) {
   p.vplan = ctx->d_vplan.ptr;
   p.fdesc = ctx->d_fdesc.ptr;
   p.has_dev = ctx->has_dev ? 1u : 0u;
+  p.prescan = 0;
   p.dplan = ctx->d_dplan.ptr;
   p.flush_rank = ctx->flush_order ? ctx->d_flush_rank.ptr : nullptr;
   return p;

@@ -24,9 +24,15 @@ int launch_fast(hg_ctx* ctx) {
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const uint32_t per_cta = nw * kWarp;
   const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>((uint32_t)ctx->sm_count, (ctx->n_ranges + per_cta - 1) / per_cta));
+  p.prescan = 1;
   CK(ctx->d_params.ensure(1));
   CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
+  {
+    const uint32_t sgrid = std::max<uint32_t>(1, std::min<uint32_t>((ctx->n_ranges + 7) / 8, (uint32_t)ctx->sm_count * 8));
+    const size_t ssm = ctx->max_sid < (uint32_t)kSdescMax ? 8u * (ctx->max_sid + 1) : 0u;
+    fast_scan_kernel<<<sgrid, 256, ssm, ctx->stream>>>(p);
+  }
   kern<<<grid, per_cta, smem, ctx->stream>>>(p, ctx->d_params.ptr);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[7], ctx->stream));
@@ -35,7 +41,7 @@ int launch_fast(hg_ctx* ctx) {
   fast_orphan_fix_kernel<<<32, 256, 0, ctx->stream>>>(p);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[5], ctx->stream));
-  ctx->launches += 3;
+  ctx->launches += 4;
   return HG_OK;
 }
 

@@ -190,20 +190,56 @@ __device__ __forceinline__ void r_item(const Params& p, RLane& R, uint64_t khi, 
 #endif
 constexpr int kScanDepth = HG_SCAN_DEPTH;
 
-static __device__ __noinline__ uint64_t r_scan(const Params& p, const uint8_t* g, uint64_t size, uint64_t t0, uint64_t t1) {
-  for (uint64_t o = t0; o < t1; o++) {
-    uint64_t cur = o, nxt, ts, prev = 0;
-    int k = 0;
-    for (; k < kScanDepth; k++) {
-      if (!seg_plausible(p, g, size, cur, nxt, ts) || (k && ts < prev)) break;
-      prev = ts;
-      cur = nxt;
-      if (cur == size) { k = kScanDepth; break; }
-    }
-    if (k == kScanDepth) return o;
+__device__ __forceinline__ bool r_scan_at(const Params& p, const uint8_t* g, uint64_t size, uint64_t o) {
+  uint64_t cur = o, nxt, ts, prev = 0;
+  int k = 0;
+  for (; k < kScanDepth; k++) {
+    if (!seg_plausible(p, g, size, cur, nxt, ts) || (k && ts < prev)) break;
+    prev = ts;
+    cur = nxt;
+    if (cur == size) { k = kScanDepth; break; }
   }
+  return k == kScanDepth;
+}
+
+static __device__ __noinline__ uint64_t r_scan(const Params& p, const uint8_t* g, uint64_t size, uint64_t t0, uint64_t t1) {
+  for (uint64_t o = t0; o < t1; o++)
+    if (r_scan_at(p, g, size, o)) return o;
   return kNone;
 }
+
+// every range's speculative start before the range kernel, one warp per range testing 32
+// consecutive offsets at once (the same first offset as r_scan: the lowest lane that passes).
+// A lane of the range kernel scanning alone paid one dependent L2/HBM round trip per offset
+// at kernel start (4% of C2's stall samples, profiles/r21_*).
+#ifdef HG_FAST_KERNELS
+__global__ void __launch_bounds__(256) fast_scan_kernel(Params p) {
+  if (p.max_sid < (uint32_t)kSdescMax) {  // desc_of reads shared memory for such registries
+    uint2* t = reinterpret_cast<uint2*>(g_smem);
+    for (uint32_t i = threadIdx.x; i <= p.max_sid; i += blockDim.x) t[i] = __ldg(&p.desc[i]);
+    __syncthreads();
+  }
+  const uint32_t lane = lane_id();
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < p.n_ranges; r += nwarps) {
+    const uint32_t s = p.range_stream[r];
+    const uint32_t j = r - p.stream_range0[s];
+    uint64_t found = j == 0 ? 16ull : kNone;
+    if (j) {
+      const uint64_t size = p.stream_size[s];
+      const uint8_t* g = p.data + p.stream_base[s];
+      const uint64_t t0 = 16 + (uint64_t)j * p.range_bytes;
+      const uint64_t t1 = min(t0 + (uint64_t)p.range_bytes, size);
+      for (uint64_t base = t0; base < t1; base += kWarp) {
+        const uint64_t o = base + lane;
+        const uint32_t m = __ballot_sync(0xffffffffu, o < t1 && r_scan_at(p, g, size, o));
+        if (m) { found = base + (uint32_t)(__ffs(m) - 1); break; }
+      }
+    }
+    if (lane == 0) p.rstate[r].entry = found;
+  }
+}
+#endif
 
 // open the lane's next range (ranges without a plausible header are recorded and skipped)
 __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, uint32_t stride) {
@@ -214,7 +250,7 @@ __device__ __forceinline__ bool r_begin(const Params& p, RLane& R, uint32_t r, u
     const uint8_t* g = p.data + p.stream_base[s];
     const uint64_t t0 = 16 + (uint64_t)j * p.range_bytes;
     const uint64_t t1 = min(t0 + (uint64_t)p.range_bytes, size);
-    const uint64_t entry = j == 0 ? 16ull : r_scan(p, g, size, t0, t1);
+    const uint64_t entry = j == 0 ? 16ull : p.prescan ? p.rstate[r].entry : r_scan(p, g, size, t0, t1);
     if (entry == kNone) {
       RangeState st;
       st.entry = kNone; st.exit = kNone; st.first_ts = 0; st.last_ts = 0; st.pool_off = 0;

@@ -125,6 +125,7 @@ struct Params {
   const uint4* dplan;              // per schema id: device-record layout for the drain (fast.cuh)
   const uint32_t* flush_rank;      // stream -> rank in the truncation flush order (nullptr: stream order)
   uint32_t has_dev;                // the registry has device-profiling schemas (fast.cuh: CTA name cache)
+  uint32_t prescan;                // range starts found by fast_scan_kernel (rstate[r].entry), not by each lane
 };
 
 // compact descriptor: x = fn(20) | cls(3)<<20 | flags(8)<<23 ; y = fixed_len(16) | result field index(8)<<16 | counter(8)<<24
