@@ -514,6 +514,18 @@ __device__ __forceinline__ bool r_words_ascii(const uint32_t (&w)[kDW]) {
   return (acc & 0x80808080u) == 0;
 }
 
+// strict UTF-8 (tracefile.py:165) of n bytes at o: all-ASCII checked kRNameMax bytes per round trip
+// (g_utf8's word loop waits for every load before the next), anything else by the byte automaton
+__device__ __forceinline__ bool r_utf8(const uint8_t* g, uint64_t o, uint32_t n) {
+  for (uint32_t i = 0; i < n; i += kRNameMax) {
+    uint32_t w[kDW];
+    r_words(g, o + i, w);
+    r_words_mask(w, min(n - i, kRNameMax));
+    if (!r_words_ascii(w)) return g_utf8_slow(g, o, n);
+  }
+  return true;
+}
+
 // g_hash (seg.cuh) over register words
 __device__ __forceinline__ uint64_t r_words_hash(const uint32_t (&w)[kDW], uint32_t n) {
   uint64_t h = 0x9E3779B97F4A7C15ull ^ ((uint64_t)n * 0xff51afd7ed558ccdull);
@@ -636,11 +648,12 @@ static __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, c
           if (nreg) r_words_mask(nw_, nl);
           if (ostr) {
             bool ok;
-            if (ol <= kRNameMax) { r_words_mask(ow, ol); ok = r_words_ascii(ow) || g_utf8(gb, second ? s0 : s1, ol); }
-            else ok = g_utf8(gb, second ? s0 : s1, ol);
+            if (ol <= kRNameMax) { r_words_mask(ow, ol); ok = r_words_ascii(ow) || g_utf8_slow(gb, second ? s0 : s1, ol); }
+            else ok = r_utf8(gb, second ? s0 : s1, ol);
             if (!ok) err = HG_ERR_UTF8;
           }
-          if (nstr && !err && !((nreg && r_words_ascii(nw_)) || g_utf8(gb, second ? s1 : s0, nl))) err = HG_ERR_UTF8;
+          if (nstr && !err && !(nreg ? r_words_ascii(nw_) || g_utf8_slow(gb, second ? s1 : s0, nl) : r_utf8(gb, second ? s1 : s0, nl)))
+            err = HG_ERR_UTF8;
         }
         rp[HG_ROLE_NAME] = second ? s1 : s0;
         rl[HG_ROLE_NAME] = nl;
@@ -650,7 +663,7 @@ static __device__ __noinline__ uint2 r_drain(const Params& p, const SegSmem L, c
     } else {  // the inline record's one string field (length already checked): strict UTF-8
       const uint32_t vp = __ldg(&p.vplan[h.sid]);
       const uint64_t at = a + 16 + (vp & 0x3FFFu);
-      if (!g_utf8(gb, at + 4, g32(gb, at))) err = HG_ERR_UTF8;
+      if (!r_utf8(gb, at + 4, g32(gb, at))) err = HG_ERR_UTF8;
     }
     if (!err && cls == HG_CLASS_DEVICE) {  // seg_device with the global dictionary, then fill the CTA cache
       if (d_flags(d) & SF_FEED_ALWAYS) {
@@ -701,7 +714,7 @@ static __device__ __noinline__ void r_drain_str(const Params& p, const uint64_t*
     const uint8_t* gb = p.data + p.stream_base[q_s[lane]];
     const uint32_t vp = __ldg(&p.vplan[g32(gb, a)]);
     const uint64_t at = a + 16 + (vp & 0x3FFFu);
-    if (!g_utf8(gb, at + 4, g32(gb, at))) atomicOr(p.anom, 4u);
+    if (!r_utf8(gb, at + 4, g32(gb, at))) atomicOr(p.anom, 4u);
   }
   __syncwarp();
 }
