@@ -398,11 +398,11 @@ def run_ours(args):
             "unit": "GB/s",
             "frac": achieved / peak,
             "traffic": None,
-            "kernel": "fast_kernel" if single else "seg_decode_kernel",
+            "kernel": "fast_scan_kernel + fast_kernel" if single else "seg_decode_kernel",
             "kernel_ms": tms,
             "algorithmic_bytes_per_launch": n_bytes,
             "peak_source": peak_src,
-            "phase1": {"kernels": ("fast_kernel + fast_verify_kernel + fast_orphan_fix_kernel" if single
+            "phase1": {"kernels": ("fast_scan_kernel + fast_kernel + fast_verify_kernel + fast_orphan_fix_kernel" if single
                                    else "seg_walk_kernel + seg_chain_kernel + seg_decode_kernel"),
                        "path": "single pass over HBM (csrc/fast.cuh)" if single else "exact three-kernel path",
                        "range_bytes": range_bytes, "fallbacks": fallbacks, "ms": p1,
