@@ -88,7 +88,8 @@ __host__ __device__ inline uint32_t r_align(uint32_t x) { return (x + 127u) & ~1
 __host__ __device__ inline RSmem fast_smem_layout(uint32_t n_fn, uint32_t nw, uint32_t n_fd, uint32_t n_cd = 0,
                                                   bool dev = true) {
   RSmem L;
-  uint32_t off = n_cd ? r_align(4u * n_cd) : r_align(8u * kSdescMax);  // desc_of's table (kernels.cuh) or cdesc
+  // desc_of's table (kernels.cuh; max_sid + 1 entries when max_sid < kSdescMax, else it reads HBM) or cdesc
+  uint32_t off = n_cd ? r_align(4u * n_cd) : n_fd ? r_align(8u * n_fd) : 0u;
   const bool small = n_fn <= kSmallF;
   L.tab = off;
   if (!small && n_fn <= kSmemFnMax) off += r_align((uint32_t)sizeof(SmemRow) * n_fn);
