@@ -16,7 +16,10 @@ extern __shared__ __align__(128) uint8_t g_smem[];
 
 constexpr uint32_t kSmallF = 16;               // per-lane tally columns up to this many functions
 constexpr uint32_t kSmemFnMax = 2048;          // CTA-shared tally table up to this many functions
-constexpr int kDevSlots = 64;                  // CTA cache of device rows
+#ifndef HG_DEV_SLOTS
+#define HG_DEV_SLOTS 64
+#endif
+constexpr int kDevSlots = HG_DEV_SLOTS;        // CTA cache of device rows
 constexpr int kSdescMax = 512;                 // schema ids screened from shared memory
 
 // function id field of packed stack metadata: fn (19 bits), M_FN = none
