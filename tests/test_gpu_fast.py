@@ -200,3 +200,49 @@ def test_large_registry_deep_stacks(engine, n_top, n_low, range_bytes):
     finally:
         engine.set_option(OPT_PATH, 0)
         engine.set_option(OPT_RANGE_BYTES, 0)
+
+
+def _shift_ids(wl, raws, delta):
+    """The same workload with every schema id moved up by `delta` (registry and record headers)."""
+    import dataclasses
+    import struct
+
+    from paper_2504_03683_b200.registry import SchemaRegistry
+
+    doc = wl.registry.to_dict()
+    for s in doc["schemas"]:
+        s["id"] += delta
+    reg = SchemaRegistry.from_dict(doc)
+    out = []
+    for r in raws:
+        d = bytearray(r.data)
+        o = 16
+        while o + 16 <= len(d):
+            sid, _ts, plen = struct.unpack_from("<IQI", d, o)
+            struct.pack_into("<I", d, o, sid + delta)
+            o += 16 + plen
+        out.append(dataclasses.replace(r, data=bytes(d)) if dataclasses.is_dataclass(r) else r._replace(data=bytes(d)))
+    return dataclasses.replace(wl, registry=reg), out
+
+
+@pytest.mark.parametrize("name,scale", [("c5", 0.002), ("c2", 0.002)])
+def test_sparse_ids_device_registry(engine, name, scale):
+    """Schema ids above kSdescMax with device-profiling schemas: compact descriptors for the fixed
+    host records, the uint4 through L1 for variable ones (device records, strings), the CTA name
+    cache kept; tally, stats and orphans match the oracle on both runs of the same streams."""
+    from oracle import oracle
+    from paper_2504_03683_b200 import synth
+    from paper_2504_03683_b200.engine import OPT_PATH
+
+    wl = synth.config(name, scale)
+    wl, raws = _shift_ids(wl, synth.generate(wl), 1000)
+    infos = [r.info for r in raws]
+    want = oracle.run(raws, wl.registry, infos)
+    engine.set_option(OPT_PATH, 2)
+    try:
+        for i in range(2):
+            got = engine.run(raws, wl.registry, infos, reuse_streams=i > 0)
+            assert engine.last_path()[0] == 1
+            assert got.stats == want.stats and got.report == want.report and got.orphans == want.orphans
+    finally:
+        engine.set_option(OPT_PATH, 0)
