@@ -987,7 +987,10 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     const bool fE = good && kind == FK_ENTRY && (kDeep ? ne < kRDepthMax && (R.deep || ne < (uint32_t)kRLS)
                                                        : ne < (uint32_t)kRLS && !R.deep);
     const bool fXp = good && kind == FK_EXIT && ne && (kDeep || !R.deep) && tfn == fnm;  // pops a same-function top
-    const bool fXq = good && kind == FK_EXIT && ne == 0 && np < (uint32_t)kRLP;          // pending: compose decides
+    // pending (compose decides); with kDeep beyond kRLP into the lane's chunk (a range that starts deep
+    // in a call stack meets tens of exits before its first entry: they took the slow path, C4)
+    const bool fXq = good && kind == FK_EXIT && ne == 0 &&
+                     (np < (uint32_t)kRLP || (kDeep && R.deep && np < (uint32_t)kRLP + kRDeepHalf));
     const bool fO = good && (kind == FK_PASS || kind == FK_DEFER);
     // one variable field (blob / string): exact length here, UTF-8 of strings in the drain
     const uint32_t lead0 = D.z & 0xFFFFu, lead1 = D.z >> 16;
@@ -1029,11 +1032,18 @@ __global__ void __launch_bounds__(kRMaxThreads, 1) fast_kernel(Params p, const P
     }
     if (kDeep) R.nw = R.nw + ((fE && R.nw < (uint32_t)kRLS) ? 1u : 0u) - ((fXp && R.nw) ? 1u : 0u);
     if (fXq) {
-      const uint32_t i = np * kWarp;
-      T.pd_ts[i] = ts;
-      T.pd_meta[i] = fnm | ((1u | (err ? 2u : 0u) | (((D.x >> 26) & 3u) << 4)) << 19);
-      T.pd_k[i] = R.n - 1;
-      if (kMode & 1) p.tl_pres[(uint64_t)R.r * kRLP + np] = res;
+      const uint32_t xf = 1u | (err ? 2u : 0u) | (((D.x >> 26) & 3u) << 4);
+      if (kDeep && np >= (uint32_t)kRLP) {  // as r_record_slow stores it
+        SumEntry e;
+        e.ts = ts; e.seq = R.n - 1; e.fn = m_fn(fnm); e.flags = xf; e.result = res;
+        R.deep[np - kRLP] = e;
+      } else {
+        const uint32_t i = np * kWarp;
+        T.pd_ts[i] = ts;
+        T.pd_meta[i] = fnm | (xf << 19);
+        T.pd_k[i] = R.n - 1;
+        if (kMode & 1) p.tl_pres[(uint64_t)R.r * kRLP + np] = res;
+      }
     }
     if (kMode & 1) {
       if (fXp) r_item(p, R, ts, R.n - 1, ets, res, TL_HOST | (((D.x >> 26) & 3u) << 4), fnm);
