@@ -305,7 +305,7 @@ int hg_merge_import(hg_ctx* ctx, const void* src, uint32_t n_dev_global, uint32_
                     const char* names, const uint64_t* name_offsets);
 
 /* timing of the last run, CUDA events on the engine's stream: kernel_ms = the
- * dominant kernel (fast_kernel on the single pass, the decode kernel on the exact path), total_ms = whole run from staging to results
+ * dominant kernel (fast_scan_kernel + fast_kernel on the single pass, the decode kernel on the exact path), total_ms = whole run from staging to results
  * on the host; bytes moved host<->device and kernel launches of that run */
 int hg_last_timing(hg_ctx* ctx, float* kernel_ms, float* total_ms, uint64_t* h2d_bytes, uint64_t* d2h_bytes,
                    uint64_t* kernel_launches);
