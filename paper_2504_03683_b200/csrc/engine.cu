@@ -877,6 +877,8 @@ int hg_run_local(hg_ctx* ctx, uint32_t want) {
     }
     if (C[C_N_ORPHANS] > ctx->orphan_cap) { ctx->orphan_cap = C[C_N_ORPHANS] * 2; grow = true; }
     if (C[C_DEEP_USED] > ctx->deep_cap) { ctx->deep_cap = C[C_DEEP_USED] * 2; grow = true; }
+    // stacks overflowed the inline slots: a rerun (buffers grown) already takes the deep variant
+    if (fast && grow && C[C_DEEP_USED] > 0) ctx->deep_inline = true;
     if ((uint32_t)C[C_N_ERRORS] > ctx->error_cap) { ctx->error_cap = (uint32_t)C[C_N_ERRORS] * 2; grow = true; }
     if ((uint32_t)C[C_OVERFLOW]) {
       ctx->row_cap *= 4; ctx->dict_mask = ctx->dict_mask * 4 + 3; ctx->arena_cap = std::max<uint64_t>(ctx->arena_cap * 4, C[C_ARENA_USED] * 2);
@@ -1111,8 +1113,8 @@ static int run_fused(hg_ctx* ctx, uint32_t want, bool& done) {
                      !(uint32_t)C[C_WATCHDOG] && !(uint32_t)C[C_N_ERRORS] && 2 * C[C_POOL_USED] <= ctx->pool_cap &&
                      C[C_N_ORPHANS] <= ctx->orphan_cap && C[C_DEEP_USED] <= ctx->deep_cap &&
                      C[C_STACK_USED] <= ctx->stack_cap;
+  if (C[C_DEEP_USED] > 0) ctx->deep_inline = true;  // later passes (the split path's too) keep stacks inline
   if (!clean) return HG_OK;  // not done: the split path reruns everything
-  if (C[C_DEEP_USED] > 0) ctx->deep_inline = true;
   ctx->local_last_ts = C[C_LAST_TS];
   ctx->local_events = C[C_STATS + ST_EVENTS];
   ctx->phase1_done = true;
