@@ -479,17 +479,29 @@ __device__ __forceinline__ uint64_t g_hash(const uint8_t* g, uint64_t o, uint32_
   return h | 1ull;
 }
 
-__device__ __forceinline__ bool g_name_equal(const NameDict& d, uint32_t row, const uint8_t* g, uint64_t o, uint32_t n) {
-  if (__ldg(&d.name_len[row]) != n) return false;
-  const uint32_t* a = reinterpret_cast<const uint32_t*>(d.arena + d.name_off[row]);
+// the row's length, offset and bytes were written by another SM during this kernel (published by
+// its fence + vals store).  A read through L1 / the read-only cache can only be stale the other way
+// (a sector cached before the row was written): equal bytes there mean equal names (a stale match
+// would need a 64-bit hash collision), a mismatch is confirmed at L2 (ld.global.cg) before the
+// lookup believes it -- else a stale line could make a second row for one name
+template <bool kL2>
+__device__ __forceinline__ bool g_name_equal_at(const NameDict& d, uint32_t row, const uint8_t* g, uint64_t o, uint32_t n) {
+  const uint32_t len = kL2 ? __ldcg(&d.name_len[row]) : d.name_len[row];
+  if (len != n) return false;
+  const uint64_t off = kL2 ? (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(d.name_off) + row) : d.name_off[row];
+  const uint32_t* a = reinterpret_cast<const uint32_t*>(d.arena + off);
   uint32_t i = 0;
   for (; i + 4 <= n; i += 4)
-    if (a[i >> 2] != g32(g, o + i)) return false;
+    if ((kL2 ? __ldcg(a + (i >> 2)) : a[i >> 2]) != g32(g, o + i)) return false;
   if (i < n) {
     const uint32_t m = 0xffffffffu >> (8 * (4 - (n - i)));
-    if ((a[i >> 2] & m) != (g32(g, o + i) & m)) return false;
+    if (((kL2 ? __ldcg(a + (i >> 2)) : a[i >> 2]) & m) != (g32(g, o + i) & m)) return false;
   }
   return true;
+}
+
+__device__ __forceinline__ bool g_name_equal(const NameDict& d, uint32_t row, const uint8_t* g, uint64_t o, uint32_t n) {
+  return g_name_equal_at<false>(d, row, g, o, n) || g_name_equal_at<true>(d, row, g, o, n);
 }
 
 // device-name dictionary lookup/insert (same layout, hash and probing as name_lookup)
