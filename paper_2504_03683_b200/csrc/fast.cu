@@ -29,7 +29,7 @@ int launch_fast(hg_ctx* ctx) {
   CK(cudaMemcpyAsync(ctx->d_params.ptr, &p, sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
   CK(cudaEventRecord(ctx->ev[4], ctx->stream));
   {
-    const uint32_t sgrid = std::max<uint32_t>(1, std::min<uint32_t>((ctx->n_ranges + 7) / 8, (uint32_t)ctx->sm_count * 8));
+    const uint32_t sgrid = std::max<uint32_t>(1, (ctx->n_ranges + 7) / 8);  // a warp per range (54 -> 46 us on C2)
     const size_t ssm = ctx->max_sid < (uint32_t)kSdescMax ? 8u * (ctx->max_sid + 1) : 0u;
     fast_scan_kernel<<<sgrid, 256, ssm, ctx->stream>>>(p);
   }
