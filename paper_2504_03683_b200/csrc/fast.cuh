@@ -44,7 +44,10 @@ constexpr uint32_t kRWordMask = kRRing / 4 - 1;
 constexpr uint32_t kRMirror = 0;                    // (no mirror: header words are read with wrapped indices)
 constexpr uint32_t kRStride = kRRing + kRMirror;    // ring bytes per lane: header + first field need no wrap
 constexpr uint32_t kRInline = HG_RINLINE;           // records up to this long are decoded from the ring
-constexpr int kRLag = 2;                            // iterations before a fill group is waited for
+#ifndef HG_RLAG
+#define HG_RLAG 2  // C2 x1.0 phase 1: lag 1 1.888 ms, 2 1.875, 3 1.880
+#endif
+constexpr int kRLag = HG_RLAG;                            // iterations before a fill group is waited for
 constexpr int kRLS = 4;                             // open entries per lane in shared memory: the stack's top
                                                     // window (depth d in slot d % kRLS), older ones spilled
 constexpr int kRLP = 4;                             // pending exits per lane in shared memory
